@@ -1,1 +1,28 @@
-"""B200-native phasor-field NLOS reconstruction engine (placeholder during bring-up)."""
+"""B200-native phasor-field NLOS reconstruction engine (drop-in for the reference hot path).
+
+Public names mirror the reference package ``phasorfield`` (reference
+``__init__.py:19-89``) for the hot path: the phasor kernel and temporal
+transform, the eight reconstruction algorithms, the dispatcher, the video
+renderer and the depth projection, plus the boundary types.  Compute runs in
+``libpfgpu.so`` (hand-written sm_100a CUDA); there is no CPU fallback.
+"""
+
+from .core import (PROPAGATION_SIGN, SPEED_OF_LIGHT, CuboidGrid, ExplicitVoxels,
+                   FrequencySlices, FrustumGrid, NonPlanarRelay, NonUniformPlanarRelay, PointList,
+                   ReconstructionVolume, TransientMeasurement, UniformGrid2D, UniformGrid3D,
+                   UniformRelay, ValidationError, VoxelPlane, grid_coordinates,
+                   illumination_coordinates)
+from .phasor import (DeviceFrequencySlices, PhasorKernel, build_kernel, to_frequency,
+                     to_frequency_device)
+from .reconstruct import (ALGORITHM_NAMES, RsdEngine, light_transport_video, project_max_depth,
+                          reconstruct, rsd)
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    # the non-rsd algorithms live in .algorithms (loaded on first use)
+    if name in ("srsd", "nursd1", "nursd2", "nursd3", "nursd3d", "srsd_nursd2", "rsd3d"):
+        from . import algorithms
+        return getattr(algorithms, name)
+    raise AttributeError(name)

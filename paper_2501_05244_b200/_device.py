@@ -1,0 +1,140 @@
+"""Device plumbing: CUDA checks, streams, FFT plans (radix choice + fp64 twiddle tables).
+
+PyTorch is used only for device memory, streams and collectives; every
+arithmetic kernel on the path lives in ``libpfgpu.so``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._fastlen import factorize
+
+
+class DeviceUnavailable(RuntimeError):
+    """No CUDA device / no built extension: the engine has no CPU fallback."""
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise DeviceUnavailable("paper_2501_05244_b200 needs a CUDA device (sm_100a); "
+                                "there is no CPU fallback")
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t: torch.Tensor) -> int:
+    return int(t.data_ptr())
+
+
+def radices_for(n: int) -> list[int]:
+    """Stage radices: powers of two merged into as few even stages as possible."""
+    f = factorize(n)
+    k = f.count(2)
+    odd = [p for p in f if p != 2]
+    pow2 = []
+    if k:
+        s = (k + 3) // 4
+        bits = [k // s + (1 if i < k % s else 0) for i in range(s)]
+        pow2 = [1 << b for b in bits]
+    return pow2 + sorted(odd, reverse=True)
+
+
+class FftPlan:
+    """Mixed-radix plan for one length on one device (twiddles built in float64)."""
+
+    def __init__(self, n: int, device: torch.device):
+        self.n = int(n)
+        rad = radices_for(self.n) if self.n > 1 else []
+        m = np.arange(self.n, dtype=np.float64)
+        w = np.exp(-2j * np.pi * m / self.n).astype(np.complex64)
+        self.tw = torch.from_numpy(w).to(device)
+        self.c = _lib.PfFftPlan()
+        self.c.n = self.n
+        self.c.nst = len(rad)
+        for i, r in enumerate(rad):
+            self.c.radix[i] = r
+        self.c.tw = ctypes.c_void_p(ptr(self.tw))
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.c)
+
+
+_PLANS: dict[tuple[int, int], FftPlan] = {}
+
+
+def fft_plan(n: int, device: torch.device) -> FftPlan:
+    key = (int(n), device.index or 0)
+    p = _PLANS.get(key)
+    if p is None:
+        p = FftPlan(n, device)
+        _PLANS[key] = p
+    return p
+
+
+def fft_lines(data: torch.Tensor, n: int, nlines: int, inner: int, inner_stride: int,
+              outer_stride: int, elem_stride: int, direction: int, scale: float = 1.0,
+              stream=None) -> None:
+    plan = fft_plan(n, data.device)
+    _lib.call("pf_fft_lines", ptr(data), plan.ref, nlines, inner, inner_stride, outer_stride,
+              elem_stride, direction, scale, stream_ptr(stream))
+
+
+def fft2_natural(buf: torch.Tensor, ny: int, nx: int, nbatch: int, direction: int,
+                 scale: float = 1.0, stream=None) -> None:
+    """In-place 2D FFT of ``nbatch`` contiguous [ny, nx] c64 planes (natural order)."""
+    if nx > 1:
+        fft_lines(buf, nx, nbatch * ny, 1, 0, nx, 1, direction, 1.0, stream)
+    if ny > 1:
+        fft_lines(buf, ny, nbatch * nx, nx, 1, ny * nx, nx, direction, scale, stream)
+    elif scale != 1.0:
+        buf.mul_(scale)
+
+
+def fftn_natural(buf: torch.Tensor, shape: tuple[int, ...], nbatch: int, direction: int,
+                 scale: float = 1.0, stream=None) -> None:
+    """In-place N-D FFT (N = 1..3) of ``nbatch`` contiguous arrays of ``shape``."""
+    total = int(np.prod(shape))
+    d = len(shape)
+    done_scale = False
+    for ax in range(d - 1, -1, -1):
+        n = shape[ax]
+        if n == 1:
+            continue
+        inner = int(np.prod(shape[ax + 1:])) if ax + 1 < d else 1
+        outer_block = inner * n
+        nlines = nbatch * total // n
+        s = scale if not done_scale else 1.0
+        done_scale = True
+        if inner == 1:
+            fft_lines(buf, n, nlines, 1, 0, n, 1, direction, s, stream)
+        else:
+            fft_lines(buf, n, nlines, inner, 1, outer_block, inner, direction, s, stream)
+    if not done_scale and scale != 1.0:
+        buf.mul_(scale)
+
+
+def c64(t: torch.Tensor) -> torch.Tensor:
+    """View a complex64 tensor; ensures contiguity."""
+    assert t.dtype == torch.complex64
+    return t.contiguous()
+
+
+def phase_factors(omega: np.ndarray, times: np.ndarray) -> np.ndarray:
+    """exp(1j w t) in float64, rounded to complex64 [F, n_frames]."""
+    return np.exp(1j * np.outer(omega, times)).astype(np.complex64)
+
+
+def pow2_ceil(x: int) -> int:
+    return 1 << max(0, math.ceil(math.log2(max(1, x))))

@@ -1,0 +1,97 @@
+"""ctypes binding of ``libpfgpu.so`` (the C-ABI declared in ``include/pfgpu.h``).
+
+The shared library is built in-tree by ``paper_2501_05244_b200.build`` (nvcc,
+``-gencode arch=compute_100a,code=sm_100a``).  There is no CPU fallback: if the
+library or a CUDA device is missing, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpfgpu.so")
+
+PF_MAX_STAGES = 24
+
+
+class PfFftPlan(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("nst", ctypes.c_int),
+                ("radix", ctypes.c_int * PF_MAX_STAGES), ("tw", ctypes.c_void_p)]
+
+
+class PfPlane(ctypes.Structure):
+    _fields_ = [("dz", ctypes.c_double), ("lag_dx", ctypes.c_double), ("lag_dy", ctypes.c_double),
+                ("x0", ctypes.c_double), ("dx", ctypes.c_double), ("y0", ctypes.c_double),
+                ("dy", ctypes.c_double), ("z", ctypes.c_double), ("uhat_off", ctypes.c_int64),
+                ("vol_plane", ctypes.c_int64)]
+
+
+class PfPropGeom(ctypes.Structure):
+    _fields_ = [("px", ctypes.c_int), ("py", ctypes.c_int), ("nx", ctypes.c_int),
+                ("ny", ctypes.c_int), ("nu0x", ctypes.c_int), ("nu0y", ctypes.c_int),
+                ("n_illum", ctypes.c_int), ("include_illum", ctypes.c_int),
+                ("uhat_illum_stride", ctypes.c_int64)]
+
+
+_vp, _i, _i64, _d, _f = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_float
+_P = ctypes.POINTER
+
+# name -> argtypes (restype int unless listed in _RESTYPES)
+_SIGNATURES = {
+    "pf_version": [],
+    "pf_last_error": [ctypes.c_char_p, ctypes.c_size_t],
+    "pf_temporal_dft": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, _vp],
+    "pf_temporal_dft_direct": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, _vp],
+    "pf_fft_lines": [_vp, _P(PfFftPlan), _i64, _i64, _i64, _i64, _i64, _i, _f, _vp],
+    "pf_embed_centered": [_vp, _i64, _i, _i, _i64, _vp, _i, _i, _vp],
+    "pf_prop_ws_a": [_P(PfPropGeom), _i],
+    "pf_prop_ws_b": [_P(PfPropGeom), _i],
+    "pf_prop_kernel_rows": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp],
+    "pf_prop_columns": [_vp, _i, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _vp],
+    "pf_prop_rows_out": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp,
+                         _i64, _vp],
+}
+_RESTYPES = {"pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64}
+
+_lib = None
+
+
+class PfError(RuntimeError):
+    """A libpfgpu call failed (argument or CUDA error)."""
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGNATURES)
+
+
+def load(path: str = LIB_PATH):
+    """Load the library (no device needed) and bind every declared entry point."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise PfError(f"libpfgpu.so not built at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    for name, args in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    buf = ctypes.create_string_buffer(1024)
+    load().pf_last_error(buf, 1024)
+    return buf.value.decode(errors="replace")
+
+
+def call(name: str, *args) -> int:
+    rc = getattr(load(), name)(*args)
+    if name in _RESTYPES:
+        return rc
+    if rc != 0:
+        raise PfError(f"{name} failed ({rc}): {last_error()}")
+    return rc

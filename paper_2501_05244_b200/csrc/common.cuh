@@ -1,0 +1,67 @@
+// Shared device helpers for libpfgpu (complex arithmetic, phase reduction,
+// error plumbing).  sm_100a only; no host fallback exists anywhere.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PF_TWO_PI 6.283185307179586476925286766559
+#define PF_INV_TWO_PI 0.15915494309189533576888376337251
+
+// ---------------------------------------------------------------- complex
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ void cacc(float2& acc, float2 a, float2 b) {  // acc += a*b
+  acc.x = fmaf(a.x, b.x, fmaf(-a.y, b.y, acc.x));
+  acc.y = fmaf(a.x, b.y, fmaf(a.y, b.x, acc.y));
+}
+
+// exp(+1j * phase) with the argument reduced in float64 first (SURVEY F5:
+// k*r reaches ~10^3 rad, so the reduction must not happen in float32).
+__device__ __forceinline__ float2 expi_reduced(double phase) {
+  const double q = rint(phase * PF_INV_TWO_PI);
+  const float red = (float)fma(-q, PF_TWO_PI, phase);
+  float s, c;
+  __sincosf(red, &s, &c);
+  return make_float2(c, s);
+}
+
+// centred index of natural slot j on a length-n axis: [-n/2, n - n/2)
+__device__ __forceinline__ int centred(int j, int n) { return j < n - n / 2 ? j : j - n; }
+// natural slot of centred index c (any integer) on a length-n axis
+__device__ __forceinline__ int natural(long long c, int n) {
+  long long m = c % n;
+  return (int)(m < 0 ? m + n : m);
+}
+
+// ---------------------------------------------------------------- errors
+// Thread-local last-error message; every extern "C" entry point returns 0 on
+// success, <0 for an argument error, >0 for a CUDA error.
+void pf_set_error(const char* fmt, ...);
+
+#define PF_LAUNCH_CHECK(what)                                              \
+  do {                                                                     \
+    cudaError_t e__ = cudaGetLastError();                                  \
+    if (e__ != cudaSuccess) {                                              \
+      pf_set_error("%s: %s", what, cudaGetErrorString(e__));               \
+      return (int)e__;                                                     \
+    }                                                                      \
+  } while (0)
+
+#define PF_ARG_CHECK(cond, msg)                                            \
+  do {                                                                     \
+    if (!(cond)) {                                                         \
+      pf_set_error("%s", msg);                                             \
+      return -1;                                                           \
+    }                                                                      \
+  } while (0)
+
+static inline int pf_cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }

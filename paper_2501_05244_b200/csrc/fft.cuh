@@ -1,0 +1,200 @@
+// Mixed-radix (2,3,4,5,7,8,11,16) self-sorting Stockham FFT on shared memory.
+//
+// Replaces numpy's pocketfft inside the reference's centred transforms
+// (reference spectral.py:107-124, phasor.py:119) with a block-cooperative
+// transform: every stage reads R operands at stride n/R, applies the stage
+// twiddles W_{Ns R}^{r k} (fp64-built table, float2), runs a compile-time
+// radix-R butterfly in registers and writes them at stride Ns, ping-ponging
+// between two shared-memory buffers.  Lengths are the reference's 11-smooth
+// pads (next_fast_len), so radices 2..11 cover every size the path needs.
+#pragma once
+#include "common.cuh"
+#include "../../include/pfgpu.h"
+
+template <int R>
+struct Unit;
+#include "unit_roots.inc"
+
+// v * exp(DIR * 1j * theta) given (cos theta, sin theta); DIR=-1 forward.
+template <int DIR>
+__device__ __forceinline__ float2 rot(float2 v, float c, float s) {
+  return DIR < 0 ? make_float2(fmaf(v.x, c, v.y * s), fmaf(v.y, c, -v.x * s))
+                 : make_float2(fmaf(v.x, c, -v.y * s), fmaf(v.y, c, v.x * s));
+}
+
+template <int R, int DIR>
+struct Dft;
+
+template <int DIR>
+struct Dft<1, DIR> {
+  static __device__ __forceinline__ void run(float2*) {}
+};
+
+template <int DIR>
+struct Dft<2, DIR> {
+  static __device__ __forceinline__ void run(float2* v) {
+    float2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  }
+};
+
+template <int DIR>
+struct Dft<4, DIR> {
+  static __device__ __forceinline__ void run(float2* v) {
+    float2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
+    float2 s13 = cadd(v[1], v[3]), d13 = csub(v[1], v[3]);
+    // forward: X1 = d02 - i d13, X3 = d02 + i d13
+    float2 jd = DIR < 0 ? make_float2(d13.y, -d13.x) : make_float2(-d13.y, d13.x);
+    v[0] = cadd(s02, s13);
+    v[2] = csub(s02, s13);
+    v[1] = cadd(d02, jd);
+    v[3] = csub(d02, jd);
+  }
+};
+
+// radix-2 split of a power-of-two length (8, 16)
+template <int R, int DIR>
+__device__ __forceinline__ void dft_split(float2* v) {
+  float2 e[R / 2], o[R / 2];
+#pragma unroll
+  for (int i = 0; i < R / 2; i++) {
+    e[i] = v[2 * i];
+    o[i] = v[2 * i + 1];
+  }
+  Dft<R / 2, DIR>::run(e);
+  Dft<R / 2, DIR>::run(o);
+#pragma unroll
+  for (int k = 0; k < R / 2; k++) {
+    float2 t = (k == 0) ? o[k] : rot<DIR>(o[k], Unit<R>::c(k), Unit<R>::s(k));
+    v[k] = cadd(e[k], t);
+    v[k + R / 2] = csub(e[k], t);
+  }
+}
+
+template <int DIR>
+struct Dft<8, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_split<8, DIR>(v); }
+};
+template <int DIR>
+struct Dft<16, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_split<16, DIR>(v); }
+};
+template <int DIR>
+struct Dft<32, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_split<32, DIR>(v); }
+};
+
+// odd prime radix: pair j with R-j (real cosine / sine halves)
+template <int R, int DIR>
+__device__ __forceinline__ void dft_odd(float2* v) {
+  constexpr int H = (R - 1) / 2;
+  float2 sp[H], sm[H];
+  float2 x0 = v[0], sum = v[0];
+#pragma unroll
+  for (int j = 1; j <= H; j++) {
+    sp[j - 1] = cadd(v[j], v[R - j]);
+    sm[j - 1] = csub(v[j], v[R - j]);
+    sum = cadd(sum, sp[j - 1]);
+  }
+  float2 out[R];
+  out[0] = sum;
+#pragma unroll
+  for (int k = 1; k <= H; k++) {
+    float2 a = x0, b = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 1; j <= H; j++) {
+      const int m = (j * k) % R;
+      const float c = Unit<R>::c(m), s = Unit<R>::s(m);
+      a.x = fmaf(sp[j - 1].x, c, a.x);
+      a.y = fmaf(sp[j - 1].y, c, a.y);
+      b.x = fmaf(sm[j - 1].x, s, b.x);
+      b.y = fmaf(sm[j - 1].y, s, b.y);
+    }
+    // forward: X[k] = a - i b, X[R-k] = a + i b
+    out[k] = make_float2(a.x - DIR * b.y, a.y + DIR * b.x);
+    out[R - k] = make_float2(a.x + DIR * b.y, a.y - DIR * b.x);
+  }
+#pragma unroll
+  for (int k = 0; k < R; k++) v[k] = out[k];
+}
+
+template <int DIR>
+struct Dft<3, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_odd<3, DIR>(v); }
+};
+template <int DIR>
+struct Dft<5, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_odd<5, DIR>(v); }
+};
+template <int DIR>
+struct Dft<7, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_odd<7, DIR>(v); }
+};
+template <int DIR>
+struct Dft<11, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_odd<11, DIR>(v); }
+};
+
+// One Stockham stage over `cnt` transforms (transform b at buf + b*ld).
+template <int R, int DIR>
+__device__ __forceinline__ void stockham_stage(const float2* __restrict__ src,
+                                               float2* __restrict__ dst, int n, int Ns,
+                                               int cnt, int ld, const float2* __restrict__ tw) {
+  const int nb = n / R;
+  const int total = nb * cnt;
+  const int twstride = n / (Ns * R);
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    const int b = t / nb;
+    const int j = t - b * nb;
+    const float2* s = src + b * ld;
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) v[r] = s[j + r * nb];
+    const int k = j % Ns;
+    if (k != 0) {
+#pragma unroll
+      for (int r = 1; r < R; r++) {
+        const float2 w = __ldg(tw + r * k * twstride);
+        v[r] = DIR < 0 ? cmul(v[r], w) : cmulc(v[r], w);
+      }
+    }
+    Dft<R, DIR>::run(v);
+    float2* d = dst + b * ld + (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; r++) d[r * Ns] = v[r];
+  }
+}
+
+// Run the full transform on `cnt` length-n lines held in `a` (scratch `b`).
+// Caller must __syncthreads() after filling `a`.  Returns the buffer holding
+// the natural-order result; all threads are synchronised on return.
+template <int DIR>
+__device__ float2* fft_smem(float2* a, float2* b, int ld, int cnt, const pf_fft_plan& p) {
+  int Ns = 1;
+  float2* src = a;
+  float2* dst = b;
+  const float2* tw = reinterpret_cast<const float2*>(p.tw);
+  for (int s = 0; s < p.nst; s++) {
+    const int R = p.radix[s];
+    switch (R) {
+      case 2: stockham_stage<2, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
+      case 3: stockham_stage<3, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
+      case 4: stockham_stage<4, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
+      case 5: stockham_stage<5, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
+      case 7: stockham_stage<7, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
+      case 8: stockham_stage<8, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
+      case 11: stockham_stage<11, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
+      default: stockham_stage<16, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
+    }
+    __syncthreads();
+    Ns *= R;
+    float2* t = src;
+    src = dst;
+    dst = t;
+  }
+  return src;
+}
+
+// padded leading dimension for `cnt` lines of length n in shared memory
+__host__ __device__ __forceinline__ int pf_ld(int n) { return n + ((n % 16) == 0 ? 1 : 0); }

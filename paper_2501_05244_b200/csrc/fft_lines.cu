@@ -1,0 +1,121 @@
+// Batched strided 1D FFTs over c64 arrays + centred embedding.
+//
+// pf_fft_lines is the engine's replacement for numpy.fft.fftn/ifftn on the
+// hot path (reference spectral.py:107-124, 156, 167, 356, 375): any axis of
+// a 2D/3D array is a set of lines (base offset, element stride).  A CTA stages
+// `cnt` lines in shared memory with coalesced loads (element-major when the
+// lines are columns, line-major when they are rows), runs the Stockham
+// transform (fft.cuh), and writes them back in place.
+#include "fft.cuh"
+
+namespace {
+
+constexpr int FL_THREADS = 256;
+constexpr size_t FL_SMEM_BUDGET = 200 * 1024;
+
+__device__ __forceinline__ long long line_base(long long l, long long inner, long long istr,
+                                               long long ostr) {
+  return (l / inner) * ostr + (l % inner) * istr;
+}
+
+template <int DIR>
+__global__ void __launch_bounds__(FL_THREADS)
+k_fft_lines(float2* __restrict__ data, pf_fft_plan plan, long long nlines, long long inner,
+            long long istr, long long ostr, long long estr, int cnt, float scale) {
+  extern __shared__ float2 sm[];
+  const int n = plan.n;
+  const int ld = pf_ld(n);
+  float2* a = sm;
+  float2* b = sm + (size_t)cnt * ld;
+  const long long l0 = (long long)blockIdx.x * cnt;
+  const int nl = (int)(nlines - l0 < cnt ? nlines - l0 : cnt);
+  const int tot = nl * n;
+  const bool rows = (estr == 1);
+  for (int e = threadIdx.x; e < tot; e += FL_THREADS) {
+    int c, i;
+    if (rows) { c = e / n; i = e - c * n; } else { i = e / nl; c = e - i * nl; }
+    a[c * ld + i] = data[line_base(l0 + c, inner, istr, ostr) + (long long)i * estr];
+  }
+  __syncthreads();
+  const float2* r = fft_smem<DIR>(a, b, ld, nl, plan);
+  for (int e = threadIdx.x; e < tot; e += FL_THREADS) {
+    int c, i;
+    if (rows) { c = e / n; i = e - c * n; } else { i = e / nl; c = e - i * nl; }
+    data[line_base(l0 + c, inner, istr, ostr) + (long long)i * estr] = cscale(r[c * ld + i], scale);
+  }
+}
+
+__global__ void k_embed_centered(const float2* __restrict__ src, long long nb, int ny, int nx,
+                                 long long sbs, float2* __restrict__ dst, int py, int px) {
+  const long long total = nb * (long long)py * px;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long bb = e / ((long long)py * px);
+    const int rem = (int)(e - bb * (long long)py * px);
+    const int jy = rem / px, jx = rem - jy * px;
+    const int iy = centred(jy, py) + ny / 2;
+    const int ix = centred(jx, px) + nx / 2;
+    float2 v = make_float2(0.f, 0.f);
+    if (iy >= 0 && iy < ny && ix >= 0 && ix < nx) v = src[bb * sbs + (long long)iy * nx + ix];
+    dst[e] = v;
+  }
+}
+
+template <int DIR>
+int launch_lines(float2* data, const pf_fft_plan& p, long long nlines, long long inner,
+                 long long istr, long long ostr, long long estr, float scale, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft_lines<DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)FL_SMEM_BUDGET);
+    attr = true;
+  }
+  const int ld = pf_ld(p.n);
+  const size_t per_line = 2 * (size_t)ld * sizeof(float2);
+  int cnt = (int)(FL_SMEM_BUDGET / per_line);
+  if (cnt < 1) {
+    pf_set_error("pf_fft_lines: length %d does not fit shared memory", p.n);
+    return -1;
+  }
+  // enough lines per CTA to keep 256 threads busy, but leave work for all SMs
+  const int want = (4 * FL_THREADS + p.n - 1) / p.n;
+  if (cnt > want) cnt = want < 1 ? 1 : want;
+  if (estr != 1 && cnt < 8 && (size_t)8 * per_line <= FL_SMEM_BUDGET) cnt = 8;  // coalescing
+  if (cnt > nlines) cnt = (int)nlines;
+  const int grid = (int)((nlines + cnt - 1) / cnt);
+  k_fft_lines<DIR><<<grid, FL_THREADS, cnt * per_line, st>>>(data, p, nlines, inner, istr, ostr,
+                                                             estr, cnt, scale);
+  PF_LAUNCH_CHECK("k_fft_lines");
+  return 0;
+}
+
+}  // namespace
+
+extern "C" int pf_fft_lines(void* data, const pf_fft_plan* plan, int64_t nlines, int64_t inner,
+                            int64_t inner_stride, int64_t outer_stride, int64_t elem_stride,
+                            int dir, float scale, void* stream) {
+  PF_ARG_CHECK(plan != nullptr && plan->n >= 1 && plan->nst <= PF_MAX_STAGES,
+               "pf_fft_lines: bad plan");
+  PF_ARG_CHECK(inner >= 1 && nlines >= 0, "pf_fft_lines: bad line layout");
+  if (nlines == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dir < 0)
+    return launch_lines<-1>((float2*)data, *plan, nlines, inner, inner_stride, outer_stride,
+                            elem_stride, scale, st);
+  return launch_lines<1>((float2*)data, *plan, nlines, inner, inner_stride, outer_stride,
+                         elem_stride, scale, st);
+}
+
+extern "C" int pf_embed_centered(const void* src, int64_t nb, int ny, int nx,
+                                 int64_t src_batch_stride, void* dst, int py, int px,
+                                 void* stream) {
+  PF_ARG_CHECK(nb >= 0 && ny >= 1 && nx >= 1 && py >= ny && px >= nx,
+               "pf_embed_centered: bad sizes");
+  if (nb == 0) return 0;
+  const long long total = nb * (long long)py * px;
+  const int grid = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+  k_embed_centered<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      (const float2*)src, nb, ny, nx, src_batch_stride, (float2*)dst, py, px);
+  PF_LAUNCH_CHECK("k_embed_centered");
+  return 0;
+}

@@ -1,0 +1,234 @@
+// Plane-to-plane RSD propagation (the per-frequency, per-plane hot loop).
+//
+// Reference: rsd reconstruct.py:254-266, srsd :312-325, nursd1 :372-383,
+// nursd3d stage 2 :641-659.  For every (frequency f, plane k):
+//     plane = cifft2(Uhat_f * cfft2(G_fk))[rows, cols] * mask_fk,  vol[k] += plane
+// G_fk[l] = exp(1j khat r)/r, r = |(lag_x, lag_y, dz_k)|, is synthesised on the
+// fly (float64 radius and phase reduction) instead of being built
+// and stored per plane (the reference holds Nz kernels per frequency: 4.5 GB
+// at config 4).
+//
+// Symmetry: on the length-p torus the lag of natural slot p-j is minus the lag
+// of slot j (slot p/2 is its own mirror), and G depends on lag^2, so G is even
+// and Ghat(-k) = Ghat(k) exactly.  Kernel A therefore synthesises only rows
+// 0..py/2 and keeps columns 0..px/2 of the x-transform; kernel B rebuilds each
+// full column by mirroring, transforms it once and uses it for both column kx
+// and px-kx.  That removes ~3/8 of the kernel-spectrum work.
+//
+// Layouts (c64, natural FFT order):
+//   ws_a  [nplanes][py/2+1][px/2+1]     kernel spectrum, x-transformed quadrant
+//   uhat  [.. per plane offset ..][n_illum][py][px]
+//   ws_b  [nplanes][n_illum][ny][px]    column pass output (rows already cropped)
+//   vol   [n_frames][.. plane k at k*ny*nx ..]
+#include "fft.cuh"
+
+namespace {
+
+constexpr int PT = 256;
+constexpr size_t PSMEM = 200 * 1024;
+
+__device__ __forceinline__ float2 rsd_kernel(double khat, double lx, double ly, double dz) {
+  const double r = sqrt(fma(lx, lx, fma(ly, ly, dz * dz)));
+  const float2 e = expi_reduced(khat * r);
+  const float ir = (float)(1.0 / r);
+  return make_float2(e.x * ir, e.y * ir);
+}
+
+// (A) kernel rows jy in [0, py/2] -> x-FFT -> keep kx in [0, px/2]
+__global__ void __launch_bounds__(PT)
+k_prop_kernel_rows(const pf_plane* __restrict__ planes, double khat, pf_prop_geom g,
+                   pf_fft_plan plan_x, float2* __restrict__ ws_a, int rows_per_cta) {
+  extern __shared__ float2 sm[];
+  const pf_plane pl = planes[blockIdx.y];
+  const int px = g.px, py = g.py;
+  const int rows_a = py / 2 + 1, cols_a = px / 2 + 1;
+  const int ld = pf_ld(px);
+  const int r0 = blockIdx.x * rows_per_cta;
+  const int nr = min(rows_per_cta, rows_a - r0);
+  float2* a = sm;
+  float2* b = sm + (size_t)rows_per_cta * ld;
+  for (int e = threadIdx.x; e < nr * px; e += PT) {
+    const int c = e / px, jx = e - c * px;
+    const double lx = (double)centred(jx, px) * pl.lag_dx;
+    const double ly = (double)(r0 + c) * pl.lag_dy;
+    a[c * ld + jx] = rsd_kernel(khat, lx, ly, pl.dz);
+  }
+  __syncthreads();
+  const float2* res = fft_smem<-1>(a, b, ld, nr, plan_x);
+  float2* dst = ws_a + ((long long)blockIdx.y * rows_a + r0) * cols_a;
+  for (int e = threadIdx.x; e < nr * cols_a; e += PT) {
+    const int c = e / cols_a, kx = e - c * cols_a;
+    dst[(long long)c * cols_a + kx] = res[c * ld + kx];
+  }
+}
+
+// (B) per column kx in [0, px/2]: mirror -> y-FFT (Ghat column) -> for each
+// illumination and for columns kx and px-kx: * Uhat column -> y-IFFT -> crop rows
+__global__ void __launch_bounds__(PT)
+k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan plan_y,
+               const float2* __restrict__ ws_a, const float2* __restrict__ uhat,
+               float2* __restrict__ ws_b, int cols_per_cta) {
+  extern __shared__ float2 sm[];
+  const pf_plane pl = planes[blockIdx.y];
+  const int px = g.px, py = g.py, ny = g.ny;
+  const int rows_a = py / 2 + 1, cols_a = px / 2 + 1;
+  const int ld = pf_ld(py);
+  const int C = cols_per_cta;
+  const int k0 = blockIdx.x * C;
+  const int nc = min(C, cols_a - k0);
+  float2* buf0 = sm;
+  float2* buf1 = sm + (size_t)C * ld;
+  float2* buf2 = sm + (size_t)2 * C * ld;
+  const float2* src = ws_a + (long long)blockIdx.y * rows_a * cols_a + k0;
+  for (int e = threadIdx.x; e < nc * py; e += PT) {
+    const int jy = e / nc, c = e - jy * nc;
+    const int sy = jy < rows_a ? jy : py - jy;
+    buf0[c * ld + jy] = src[(long long)sy * cols_a + c];
+  }
+  __syncthreads();
+  float2* gh = fft_smem<-1>(buf0, buf1, ld, nc, plan_y);
+  float2* w0 = (gh == buf0) ? buf1 : buf0;
+  float2* w1 = buf2;
+  const float2* up = uhat + pl.uhat_off;
+  for (int p = 0; p < g.n_illum; p++) {
+    const float2* u = up + (long long)p * g.uhat_illum_stride;
+    float2* outp = ws_b + ((long long)blockIdx.y * g.n_illum + p) * (long long)ny * px;
+    for (int side = 0; side < 2; side++) {
+      // column handled by slot c on this side; mirrors that coincide are skipped
+      for (int e = threadIdx.x; e < nc * py; e += PT) {
+        const int jy = e / nc, c = e - jy * nc;
+        const int kx = k0 + c;
+        const int col = side == 0 ? kx : (px - kx) % px;
+        w0[c * ld + jy] = cmul(gh[c * ld + jy], u[(long long)jy * px + col]);
+      }
+      __syncthreads();
+      const float2* res = fft_smem<1>(w0, w1, ld, nc, plan_y);
+      for (int e = threadIdx.x; e < nc * ny; e += PT) {
+        const int i = e / nc, c = e - i * nc;
+        const int kx = k0 + c;
+        const int col = side == 0 ? kx : (px - kx) % px;
+        if (side == 1 && col == kx) continue;
+        const int jy = natural((long long)g.nu0y + i, py);
+        outp[(long long)i * px + col] = res[c * ld + jy];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// (C) per output row: x-IFFT -> crop columns -> scale -> illumination phase -> accumulate
+__global__ void __launch_bounds__(PT)
+k_prop_rows_out(const pf_plane* __restrict__ planes, double khat, pf_prop_geom g,
+                pf_fft_plan plan_x, const float2* __restrict__ ws_b,
+                const double* __restrict__ ill, const float2* __restrict__ frame_w, int n_frames,
+                float2* __restrict__ vol, long long vol_frame_stride, int rows_per_cta) {
+  extern __shared__ float2 sm[];
+  const pf_plane pl = planes[blockIdx.y];
+  const int px = g.px, nx = g.nx, ny = g.ny;
+  const int ld = pf_ld(px);
+  const int i0 = blockIdx.x * rows_per_cta;
+  const int nr = min(rows_per_cta, ny - i0);
+  float2* a = sm;
+  float2* b = sm + (size_t)rows_per_cta * ld;
+  const float scale = 1.0f / ((float)g.px * (float)g.py);
+  for (int p = 0; p < g.n_illum; p++) {
+    const float2* src = ws_b + (((long long)blockIdx.y * g.n_illum + p) * ny + i0) * (long long)px;
+    for (int e = threadIdx.x; e < nr * px; e += PT) {
+      const int c = e / px, jx = e - c * px;
+      a[c * ld + jx] = src[(long long)c * px + jx];
+    }
+    __syncthreads();
+    const float2* res = fft_smem<1>(a, b, ld, nr, plan_x);
+    const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
+    for (int e = threadIdx.x; e < nr * nx; e += PT) {
+      const int c = e / nx, m = e - c * nx;
+      float2 v = cscale(res[c * ld + natural((long long)g.nu0x + m, px)], scale);
+      if (g.include_illum) {
+        const double dx = pl.x0 + pl.dx * m - sx;
+        const double dy = pl.y0 + pl.dy * (i0 + c) - sy;
+        const double dz = pl.z - sz;
+        v = cmul(v, expi_reduced(khat * sqrt(fma(dx, dx, fma(dy, dy, dz * dz)))));
+      }
+      const long long off = (pl.vol_plane * ny + i0 + c) * (long long)nx + m;
+      for (int t = 0; t < n_frames; t++) {
+        float2* d = vol + t * vol_frame_stride + off;
+        *d = cadd(*d, cmul(v, frame_w[t]));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename K>
+void allow_smem(K kern) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PSMEM);
+}
+
+int rows_fit(int n, int bufs, int want) {
+  const size_t per = (size_t)bufs * pf_ld(n) * sizeof(float2);
+  int r = (int)(PSMEM / per);
+  return r < want ? r : want;
+}
+
+}  // namespace
+
+extern "C" int64_t pf_prop_ws_a(const pf_prop_geom* g, int nplanes) {
+  return (int64_t)nplanes * (g->py / 2 + 1) * (g->px / 2 + 1);
+}
+
+extern "C" int64_t pf_prop_ws_b(const pf_prop_geom* g, int nplanes) {
+  return (int64_t)nplanes * g->n_illum * g->ny * (int64_t)g->px;
+}
+
+extern "C" int pf_prop_kernel_rows(const pf_plane* planes, int nplanes, double khat,
+                                   const pf_prop_geom* g, const pf_fft_plan* plan_x, void* ws_a,
+                                   void* stream) {
+  PF_ARG_CHECK(g && plan_x && plan_x->n == g->px && nplanes >= 1, "pf_prop_kernel_rows: bad args");
+  static bool attr = false;
+  if (!attr) { allow_smem(k_prop_kernel_rows); attr = true; }
+  const int rows_a = g->py / 2 + 1;
+  int rpc = rows_fit(g->px, 2, (2 * PT + g->px - 1) / g->px);
+  if (rpc < 1) { pf_set_error("pf_prop_kernel_rows: px too large"); return -1; }
+  dim3 grid(pf_cdiv(rows_a, rpc), nplanes);
+  const size_t smem = (size_t)2 * rpc * pf_ld(g->px) * sizeof(float2);
+  k_prop_kernel_rows<<<grid, PT, smem, (cudaStream_t)stream>>>(planes, khat, *g, *plan_x,
+                                                               (float2*)ws_a, rpc);
+  PF_LAUNCH_CHECK("k_prop_kernel_rows");
+  return 0;
+}
+
+extern "C" int pf_prop_columns(const pf_plane* planes, int nplanes, const pf_prop_geom* g,
+                               const pf_fft_plan* plan_y, const void* ws_a, const void* uhat,
+                               void* ws_b, void* stream) {
+  PF_ARG_CHECK(g && plan_y && plan_y->n == g->py && nplanes >= 1, "pf_prop_columns: bad args");
+  static bool attr = false;
+  if (!attr) { allow_smem(k_prop_columns); attr = true; }
+  const int cols_a = g->px / 2 + 1;
+  int cpc = rows_fit(g->py, 3, 8);
+  if (cpc < 1) { pf_set_error("pf_prop_columns: py too large"); return -1; }
+  dim3 grid(pf_cdiv(cols_a, cpc), nplanes);
+  const size_t smem = (size_t)3 * cpc * pf_ld(g->py) * sizeof(float2);
+  k_prop_columns<<<grid, PT, smem, (cudaStream_t)stream>>>(
+      planes, *g, *plan_y, (const float2*)ws_a, (const float2*)uhat, (float2*)ws_b, cpc);
+  PF_LAUNCH_CHECK("k_prop_columns");
+  return 0;
+}
+
+extern "C" int pf_prop_rows_out(const pf_plane* planes, int nplanes, double khat,
+                                const pf_prop_geom* g, const pf_fft_plan* plan_x,
+                                const void* ws_b, const double* ill_xyz, const void* frame_w,
+                                int n_frames, void* vol, int64_t vol_frame_stride, void* stream) {
+  PF_ARG_CHECK(g && plan_x && plan_x->n == g->px && nplanes >= 1 && n_frames >= 1,
+               "pf_prop_rows_out: bad args");
+  static bool attr = false;
+  if (!attr) { allow_smem(k_prop_rows_out); attr = true; }
+  int rpc = rows_fit(g->px, 2, (2 * PT + g->px - 1) / g->px);
+  if (rpc < 1) { pf_set_error("pf_prop_rows_out: px too large"); return -1; }
+  dim3 grid(pf_cdiv(g->ny, rpc), nplanes);
+  const size_t smem = (size_t)2 * rpc * pf_ld(g->px) * sizeof(float2);
+  k_prop_rows_out<<<grid, PT, smem, (cudaStream_t)stream>>>(
+      planes, khat, *g, *plan_x, (const float2*)ws_b, ill_xyz, (const float2*)frame_w, n_frames,
+      (float2*)vol, vol_frame_stride, rpc);
+  PF_LAUNCH_CHECK("k_prop_rows_out");
+  return 0;
+}

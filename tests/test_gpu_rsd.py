@@ -1,0 +1,146 @@
+"""GPU parity: K1 temporal transform, FFT core and rsd against the oracle / golden vectors."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2501_05244_b200 as pf
+from oracle import pf_oracle as O
+from golden_io import grid_from, load, slices_from
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4   # north-star tolerance: relative L2 on the complex volume, fp32 vs float64
+
+
+def _argmax_same(a, b, shape):
+    pa = np.abs(a.reshape(shape)).max(axis=0)
+    pb = np.abs(b.reshape(shape)).max(axis=0)
+    return int(np.argmax(pa)) == int(np.argmax(pb))
+
+
+@pytest.mark.parametrize("i", range(4))
+def test_to_frequency_golden(i):
+    d = load("phasor")
+    nb, dt, t0, lam = d[f"tf{i}_args"]
+    h = d[f"tf{i}_hist"]
+    relay = pf.NonUniformPlanarRelay(pf.PointList(np.zeros((h.shape[1], 2))), 0.0)
+    ill = pf.PointList(np.zeros((h.shape[0], 2)))
+    m = pf.TransientMeasurement(relay, ill, h, dt, t0=t0)
+    k = pf.build_kernel(lam, int(nb), dt)
+    sl = pf.to_frequency(m, k)
+    assert O.rel_l2(sl.coefficients, d[f"tf{i}_coeff"]) < 1e-6
+
+
+def test_to_frequency_kats(rng):
+    # reference test_phasor.py:94-125: single delta, direct weighted DFT, linearity
+    n_bins, dt, t0, b = 512, 16e-12, 3e-10, 41
+    relay = pf.NonUniformPlanarRelay(pf.PointList(np.zeros((4, 2))), 0.0)
+    ill = pf.PointList(np.zeros((1, 2)))
+    h = np.zeros((1, 4, n_bins), np.float32)
+    h[0, 2, b] = 2.5
+    k = pf.build_kernel(0.06, n_bins, dt)
+    sl = pf.to_frequency(pf.TransientMeasurement(relay, ill, h, dt, t0=t0), k)
+    pred = k.weights * 2.5 * np.exp(-1j * k.frequencies * (t0 + b * dt))
+    assert O.rel_linf(sl.coefficients[0, 2], pred) < 1e-6
+    assert np.all(sl.coefficients[0, [0, 1, 3]] == 0)
+    h1 = rng.uniform(0, 1, (1, 4, 128)).astype(np.float32)
+    h2 = rng.uniform(0, 1, (1, 4, 128)).astype(np.float32)
+    k2 = pf.build_kernel(0.08, 128, 32e-12)
+    c = [pf.to_frequency(pf.TransientMeasurement(relay, ill, h, 32e-12), k2).coefficients
+         for h in (h1, h2, 2 * h1 + 3 * h2)]
+    assert O.rel_linf(c[2], 2 * c[0] + 3 * c[1]) < 1e-5
+
+
+@pytest.mark.parametrize("T", [64, 128, 1024, 2048, 4096, 8192, 960, 1000])
+def test_to_frequency_sizes(rng, T):
+    dt = 4e-12 if T >= 4096 else 8e-12
+    relay = pf.NonUniformPlanarRelay(pf.PointList(np.zeros((37, 2))), 0.0)
+    ill = pf.PointList(np.zeros((2, 2)))
+    h = rng.poisson(3.0, size=(2, 37, T)).astype(np.float32)
+    lam = 40 * dt * 3e8 / 4 if T < 256 else 0.03 * T * dt / (4096 * 4e-12)
+    k = pf.build_kernel(max(lam, 0.006), T, dt, threshold=0.001)
+    sl = pf.to_frequency(pf.TransientMeasurement(relay, ill, h, dt, t0=2e-10), k)
+    ref = O.to_frequency(h, k.bin_indices, k.frequencies, k.weights, 2e-10)
+    assert O.rel_l2(sl.coefficients, ref) < 2e-6
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 8, 11, 12, 16, 30, 49, 64, 121, 128, 140, 280,
+                               512, 525, 1024, 1050, 2048, 2100])
+def test_fft_lines_vs_numpy(rng, n):
+    from paper_2501_05244_b200 import _device as dev
+    x = (rng.normal(size=(3, n)) + 1j * rng.normal(size=(3, n))).astype(np.complex64)
+    t = torch.from_numpy(x).cuda()
+    dev.fft_lines(t, n, 3, 1, 0, n, 1, -1)
+    assert O.rel_l2(t.cpu().numpy(), np.fft.fft(x.astype(np.complex128), axis=1)) < 2e-6
+    dev.fft_lines(t, n, 3, 1, 0, n, 1, +1, 1.0 / n)
+    assert O.rel_l2(t.cpu().numpy(), x) < 2e-6
+
+
+@pytest.mark.parametrize("shape", [(6, 10), (9, 7), (64, 64), (140, 140), (20, 16, 8)])
+def test_fftn_vs_numpy(rng, shape):
+    from paper_2501_05244_b200 import _device as dev
+    x = (rng.normal(size=(2,) + shape) + 1j * rng.normal(size=(2,) + shape)).astype(np.complex64)
+    t = torch.from_numpy(x).cuda()
+    dev.fftn_natural(t, shape, 2, -1)
+    ref = np.fft.fftn(x.astype(np.complex128), axes=tuple(range(1, len(shape) + 1)))
+    assert O.rel_l2(t.cpu().numpy(), ref) < 2e-6
+
+
+RSD_CASES = ["rsd_small", "rsd_small_noill", "rsd_full16", "rsd_none16", "rsd_video",
+             "chain_rsd", "rsd_odd", "rsd_odd_none"]
+
+
+@pytest.mark.parametrize("name", RSD_CASES)
+def test_rsd_golden(name):
+    d = load(f"rec_{name}")
+    sl, grid = slices_from(d), grid_from(d)
+    kw = {}
+    if "noill" in name:
+        kw["include_illumination"] = False
+    if "none" in name:
+        kw["padding"] = "none"
+    if name == "rsd_video":
+        kw["times"] = d["times"]
+    vol = pf.rsd(sl, grid, **kw)
+    assert O.rel_l2(vol.field, d["field"]) < TOL
+    if "literal" in d:
+        assert O.rel_l2(vol.field, d["literal"]) < TOL
+    if name != "rsd_video":
+        assert _argmax_same(vol.field, d["field"], grid.shape)
+
+
+def test_rsd_repeat_is_bit_identical():
+    d = load("rec_rsd_full16")
+    sl, grid = slices_from(d), grid_from(d)
+    a = pf.rsd(sl, grid).field
+    b = pf.rsd(sl, grid, threads=4).field
+    assert np.array_equal(a, b)
+
+
+def test_rsd_from_device_slices_matches_host_path():
+    d = load("rec_chain_rsd")
+    sl, grid = slices_from(d), grid_from(d)
+    dsl = pf.DeviceFrequencySlices(sl.frequencies,
+                                   torch.from_numpy(np.ascontiguousarray(
+                                       sl.coefficients.transpose(2, 0, 1)).astype(np.complex64)).cuda(),
+                                   sl.relay, sl.illuminations)
+    assert np.array_equal(pf.rsd(dsl, grid).field, pf.rsd(sl, grid).field)
+
+
+def test_rsd_c0_like_end_to_end(rng):
+    """A config-0 shaped (smaller) run from transients through rsd, against the oracle."""
+    n, T, dt = 32, 2048, 8e-12
+    pitch = 2.0 / n
+    relay = pf.UniformRelay(pf.UniformGrid2D(n, n, pitch, pitch, -1 + pitch / 2, -1 + pitch / 2, 0.0))
+    ill = pf.PointList(np.array([[0.0, 0.0]]))
+    h = rng.poisson(0.5, size=(1, n * n, T)).astype(np.float32)
+    h[0, :, 700:720] += 20.0
+    m = pf.TransientMeasurement(relay, ill, h, dt)
+    k = pf.build_kernel(0.06, T, dt)
+    sl = pf.to_frequency(m, k)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(n, n, 6, pitch, pitch, 0.3, -1 + pitch / 2,
+                                          -1 + pitch / 2, 0.5))
+    vol = pf.rsd(sl, grid)
+    ref = O.rsd(sl.to_host(), grid)
+    assert O.rel_l2(vol.field, ref) < TOL
+    assert _argmax_same(vol.field, ref, grid.shape)

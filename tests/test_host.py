@@ -1,0 +1,106 @@
+"""CPU-only checks: size rules, plans, the C-ABI library surface, validation messages."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2501_05244_b200 as pf
+from paper_2501_05244_b200 import _fastlen, _lib
+from paper_2501_05244_b200._device import radices_for
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_next_fast_len_kats():
+    # pinned sizes of the reference pad rule (scipy's 11-smooth next_fast_len)
+    for n, want in [(136, 140), (138, 140), (520, 525), (1023, 1024), (1034, 1050), (13, 14),
+                    (169, 175), (1025, 1029), (2049, 2058), (1, 1), (2, 2), (128, 128)]:
+        assert _fastlen.next_fast_len(n) == want
+
+
+def test_next_fast_len_matches_scipy():
+    sp = pytest.importorskip("scipy.fft")
+    for n in range(1, 3000):
+        assert _fastlen.next_fast_len(n) == sp.next_fast_len(n)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 7, 11, 16, 128, 140, 280, 512, 525, 1024, 1050, 2048, 2100])
+def test_radices_multiply_back(n):
+    r = radices_for(n)
+    assert int(np.prod(r)) == n
+    assert all(x in (2, 3, 4, 5, 7, 8, 11, 16) for x in r)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    header = open(os.path.join(ROOT, "include", "pfgpu.h")).read()
+    declared = set(re.findall(r"^(?:int|int64_t)\s+(pf_\w+)\(", header, flags=re.M))
+    assert declared, "no declarations parsed"
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared <= set(_lib.exported_symbols())
+    assert lib.pf_version() >= 1
+
+
+def test_error_channel_without_device():
+    lib = _lib.load()
+    # argument errors are reported before any CUDA call
+    rc = lib.pf_embed_centered(None, 1, 4, 4, 16, None, 2, 2, None)
+    assert rc < 0
+    assert "pf_embed_centered" in _lib.last_error()
+
+
+def _slices16():
+    relay = pf.UniformRelay(pf.UniformGrid2D(16, 16, 0.02, 0.02, -0.15, -0.15, 0.0))
+    ill = pf.PointList(np.array([[0.0, 0.0]]))
+    coeff = np.ones((1, 256, 3), dtype=np.complex128)
+    return pf.FrequencySlices(np.array([1e10, 1.1e10, 1.2e10]), coeff, relay, ill)
+
+
+@pytest.mark.parametrize("grid,kw,match", [
+    (pf.CuboidGrid(pf.UniformGrid3D(4, 4, 1, 0.03, 0.02, 0.1, -0.03, -0.01, 0.9)), {}, "pitch"),
+    (pf.CuboidGrid(pf.UniformGrid3D(4, 4, 1, 0.02, 0.02, 0.1, -0.025, -0.01, 0.9)), {}, "origin"),
+    (pf.CuboidGrid(pf.UniformGrid3D(4, 4, 2, 0.02, 0.02, 0.1, -0.03, -0.01, -0.05)), {},
+     "beyond the relay"),
+    (pf.CuboidGrid(pf.UniformGrid3D(4, 3, 2, 0.02, 0.02, 0.1, -0.03, -0.01, 0.85)),
+     {"padding": "none"}, "padding="),
+    (pf.CuboidGrid(pf.UniformGrid3D(4, 3, 2, 0.02, 0.02, 0.1, -0.03, -0.01, 0.85)),
+     {"padding": "wrap"}, "padding"),
+    (pf.ExplicitVoxels((pf.VoxelPlane(0.9, pf.PointList(np.array([[0.0, 0.0]]))),)), {}, "cuboid"),
+    (pf.CuboidGrid(pf.UniformGrid3D(4, 3, 2, 0.02, 0.02, 0.1, -0.03, -0.01, 0.85)),
+     {"times": np.zeros((2, 2))}, "times"),
+])
+def test_rsd_validation_messages(grid, kw, match):
+    # reference test_reconstruct.py:148-183 (raised before any device work)
+    with pytest.raises(pf.ValidationError, match=match):
+        pf.rsd(_slices16(), grid, **kw)
+
+
+def test_dispatcher_names_and_errors():
+    assert pf.ALGORITHM_NAMES == ("rsd", "srsd", "nursd1", "nursd2", "nursd3", "rsd3d",
+                                  "nursd3d", "srsd-nursd2")
+    grid = pf.CuboidGrid(pf.UniformGrid3D(4, 3, 2, 0.02, 0.02, 0.1, -0.03, -0.01, 0.85))
+    with pytest.raises(pf.ValidationError, match="unknown algorithm"):
+        pf.reconstruct(_slices16(), grid, "fbp")
+    ev = pf.ExplicitVoxels((pf.VoxelPlane(0.9, pf.PointList(np.array([[0.0, 0.0]]))),))
+    with pytest.raises(pf.ValidationError, match="alpha"):
+        pf.reconstruct(_slices16(), ev, "srsd-nursd2")
+
+
+def test_build_kernel_matches_reference_kat():
+    k = pf.build_kernel(0.04, 4096, 16e-12)
+    assert k.n_freq == 95  # reference test_phasor.py:29-30
+    with pytest.raises(pf.ValidationError):
+        pf.build_kernel(0.04, 4096, 16e-12, threshold=0.9999999)
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    grid = pf.CuboidGrid(pf.UniformGrid3D(4, 3, 2, 0.02, 0.02, 0.1, -0.03, -0.01, 0.85))
+    with pytest.raises(RuntimeError, match="CUDA"):
+        pf.rsd(_slices16(), grid)
