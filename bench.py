@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Bench: reconstructed voxels/s for BASELINE config 4 (RSD, 512x512 relay, 256 planes).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
+
+A step = one pass of the hot path over one capture: the temporal phasor
+transform of all 262,144 x 4,096 float32 transients (K1) followed by RSD
+propagation to the 512x512x256 complex volume.  ``value`` is device-timed with
+inputs resident in HBM; ``e2e`` goes through the public host API
+(``TransientReconstructor``: pinned host transients -> H2D -> K1 -> rsd ->
+D2H volume) with the copies inside the timed region.
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): detectors are sharded for K1
+and the slices all-gathered; depth planes are sharded contiguously for the
+propagation and the finished plane blocks gathered to rank 0.  Total work is
+fixed, so scaling is "strong".  Timing is max over ranks of CUDA-event time.
+
+``--impl reference`` times the reference algorithm on the host CPU (the
+oracle port of the pure-Python reference; /root/reference cannot travel to
+the GPU box), process-parallel over (frequency, plane) units on all cores,
+each step a bounded sample extrapolated to the full workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "reconstructed voxels/sec (device-timed, 1/2/4/8 B200) + % HBM roofline vs CPU ref"
+UNIT = "voxel/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of n items owned by ``rank`` (balanced, ordered)."""
+    base, rem = divmod(n, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_05244_b200 as pf
+    from paper_2501_05244_b200 import _lib, configs
+    from paper_2501_05244_b200.pipeline import TransientReconstructor
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    cfg = configs.config(args.config)
+    kernel = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
+    hist = configs.transients(cfg, device=device)            # [1, D, T] float32, identical per rank
+    I, D, T = hist.shape
+    F = kernel.n_freq
+    nz = cfg.grid.grid.nz
+    d_lo, d_hi = shard_range(D, world, rank)
+    k_lo, k_hi = shard_range(nz, world, rank)
+    hist_shard = hist[:, d_lo:d_hi].contiguous()
+    del hist
+    torch.cuda.empty_cache()
+    rec = TransientReconstructor(kernel, cfg.relay, cfg.illuminations, cfg.grid, t0=cfg.t0,
+                                 plane_range=(k_lo, k_hi), device=device)
+    eng = rec.engine
+    plane_vox = cfg.grid.grid.nx * cfg.grid.grid.ny
+    local_shard = torch.empty((F, I, d_hi - d_lo), dtype=torch.complex64, device=device)
+    full_coeff = torch.empty((F, I, D), dtype=torch.complex64, device=device)
+    if world > 1:
+        counts = [shard_range(D, world, r) for r in range(world)]
+        maxd = max(h - l for l, h in counts)
+        gather_buf = torch.empty((world, F * I * maxd), dtype=torch.complex64, device=device)
+        send_buf = torch.zeros((F * I * maxd,), dtype=torch.complex64, device=device)
+        kcounts = [shard_range(nz, world, r) for r in range(world)]
+        maxk = max(h - l for l, h in kcounts)
+        vol_send = torch.zeros((maxk * plane_vox,), dtype=torch.complex64, device=device)
+        vol_all = (torch.empty((world, maxk * plane_vox), dtype=torch.complex64, device=device)
+                   if rank == 0 else None)
+    stream = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+
+    def step():
+        ev[0].record(stream)
+        rec.temporal.run(hist_shard.view(-1, T), local_shard.view(F, -1), stream)
+        ev[1].record(stream)
+        if world > 1:
+            n_loc = F * I * (d_hi - d_lo)
+            send_buf[:n_loc].copy_(local_shard.view(-1))
+            dist.all_gather_into_tensor(gather_buf.view(-1), send_buf)
+            for r, (l, h) in enumerate(counts):
+                full_coeff[:, :, l:h].copy_(gather_buf[r, :F * I * (h - l)].view(F, I, h - l))
+            coeff = full_coeff
+        else:
+            coeff = local_shard
+        ev[2].record(stream)
+        eng.run(coeff, rec.vol, stream)
+        ev[3].record(stream)
+        if world > 1:
+            vol_send[:rec.vol.numel()].copy_(rec.vol.view(-1))
+            dist.gather(vol_send, [vol_all[r] for r in range(world)] if rank == 0 else None, dst=0)
+        ev[4].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_k1, t_s3, t_step = [], [], []
+    launches0 = _lib.launch_count
+    with ClockSampler(local) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+            torch.cuda.synchronize()
+            t_k1.append(ev[0].elapsed_time(ev[1]))
+            t_s3.append(ev[2].elapsed_time(ev[3]))
+            t_step.append(ev[0].elapsed_time(ev[4]))
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = (_lib.launch_count - launches0) // max(1, args.steps)
+    total_ms = start.elapsed_time(end)
+    if world > 1:
+        dist.barrier()
+        tt = torch.tensor([total_ms], device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    value = cfg.n_voxels / (ms_per_step * 1e-3)
+
+    # ---- end-to-end through the public host API ---------------------------------------
+    hist_host = torch.empty(hist_shard.shape, dtype=torch.float32, pin_memory=True)
+    hist_host.copy_(hist_shard)
+    for _ in range(2):
+        rec(hist_host)
+        if world > 1:
+            dist.barrier()
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for _ in range(max(2, min(args.steps, 5))):
+        if world > 1:
+            dist.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        rec(hist_host)
+        b.record()
+        torch.cuda.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e = statistics.median(e2e_ms)
+    if world > 1:
+        tt = torch.tensor([e2e], device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = float(tt.item())
+
+    hbm_peak, sm_max, peak_src = _peaks()
+    k1_ms = statistics.mean(t_k1)
+    s3_ms = statistics.mean(t_s3)
+    k1_bytes = (d_hi - d_lo) * I * T * 4 + F * I * (d_hi - d_lo) * 8
+    P = eng.px
+    units = F * (k_hi - k_lo) * I
+    s3_flops = (2 * units + F * I) * 5.0 * P * P * math.log2(P * P)
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    clocks = clk.summary()
+    roof_k1 = {"bound": "hbm", "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "peak": hbm_peak,
+               "unit": "GB/s", "traffic": _traffic("k_temporal_dft"), "kernel": "k_temporal_dft (K1)",
+               "ms": k1_ms, "peak_source": peak_src}
+    roof_k1["frac"] = roof_k1["achieved"] / hbm_peak
+    roof_s3 = {"bound": "fp32", "achieved": s3_flops / (s3_ms * 1e-3) / 1e12, "peak": fp32_peak,
+               "unit": "TFLOP/s", "traffic": _traffic("k_prop"),
+               "kernel": "propagation k_prop_kernel_rows+k_prop_columns+k_prop_rows_out (S3)",
+               "ms": s3_ms, "peak_source": "nominal 148 SM x 128 FP32 lanes x 2 x sm_max_mhz "
+                                           "(MEASURED_PEAKS.json has no FP32 entry)",
+               "flops_model": "(2*F*Nz*I + F*I) * 5 P^2 log2(P^2), P=%d" % P}
+    roof_s3["frac"] = roof_s3["achieved"] / fp32_peak
+    dominant, other = (roof_s3, roof_k1) if s3_ms >= k1_ms else (roof_k1, roof_s3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c64 (fp32 arithmetic, fp64 phases)",
+        "data": "synthetic (seeded GPU three-bounce renderer, Poisson noise; BASELINE config 4)",
+        "config": {"workload": f"config{args.config}-rsd", "relay": f"{cfg.relay.grid.nx}x"
+                   f"{cfg.relay.grid.ny}", "n_bins": T, "n_freq": F, "planes": nz,
+                   "voxels": cfg.n_voxels, "pad": P, "parallelism": f"planes+detectors x{world}",
+                   "l2": "inputs (4.3 GB transients) exceed the 126 MB L2; no flush needed",
+                   "timed": "K1 + slice gather + propagation + volume gather"},
+        "roofline": dominant, "roofline_other": other,
+        "stage_ms": {"k1": k1_ms, "propagation": s3_ms, "step_event": statistics.mean(t_step)},
+        "e2e": {"value": cfg.n_voxels / (e2e * 1e-3), "unit": UNIT, "ms_per_step": e2e,
+                "h2d_bytes_per_step": int(hist_host.numel() * 4 * world),
+                "d2h_bytes_per_step": int(cfg.n_voxels * 8),
+                "path": "TransientReconstructor (pinned host f32 -> chunked H2D||K1 -> rsd -> D2H)"},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_sample(cfg, kernel, hist_shard, rec, args)
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def _traffic(kernel_prefix):
+    """DRAM bytes per launch from the committed ncu capture summary, if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t.get(kernel_prefix)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines (oracle port of the reference; test infrastructure)
+# ---------------------------------------------------------------------------
+
+
+def _cpu_units(cfg, n_f, n_k):
+    """Bounded sample: all-detector slices for n_f frequencies x n_k planes."""
+    return n_f, n_k
+
+
+def cpu_baseline_sample(cfg, kernel, hist_dev, rec, args):
+    from oracle import pf_oracle as O
+
+    F, nz = kernel.n_freq, cfg.grid.grid.nz
+    n_tr = 4096
+    h = hist_dev.view(-1, cfg.n_bins)[:n_tr].cpu().numpy().astype(np.float64)
+    t = time.perf_counter()
+    O.to_frequency(h, kernel.bin_indices, kernel.frequencies, kernel.weights, cfg.t0)
+    t1 = (time.perf_counter() - t) * (hist_dev.shape[1] / n_tr)
+    coeff = rec.coeff.permute(1, 2, 0).cpu().numpy().astype(np.complex128)
+    sl = _HostSlices(kernel.frequencies, coeff, cfg.relay, cfg.illuminations)
+    n_f, n_k = 2, 8
+    t = time.perf_counter()
+    O.rsd(sl, cfg.grid, freq_range=(0, n_f), plane_range=(0, n_k))
+    t3 = (time.perf_counter() - t) * (F * nz) / (n_f * n_k)
+    return {"value": cfg.n_voxels / (t1 + t3), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle.to_frequency on {n_tr} of {hist_dev.shape[1]} traces + oracle.rsd "
+                      f"(reference P=1050) on {n_f} freqs x {n_k} planes of {F}x{nz}; "
+                      "linear extrapolation per trace / per (f,k) unit",
+            "s1_s": t1, "s3_s": t3}
+
+
+class _HostSlices:
+    def __init__(self, freqs, coeff, relay, ill):
+        self.frequencies = np.asarray(freqs)
+        self.coefficients = coeff
+        self.relay = relay
+        self.illuminations = ill
+        self.n_freq = self.frequencies.size
+
+
+_REF_STATE = {}
+
+
+def _ref_unit(unit):
+    """Worker: oracle rsd on one (frequency, plane-range) block; returns seconds."""
+    from oracle import pf_oracle as O
+    f, k0, k1 = unit
+    t = time.perf_counter()
+    O.rsd(_REF_STATE["slices"], _REF_STATE["grid"], freq_range=(f, f + 1), plane_range=(k0, k1))
+    return time.perf_counter() - t
+
+
+def run_reference(args):
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    import paper_2501_05244_b200 as pf
+    from oracle import pf_oracle as O
+    from paper_2501_05244_b200 import configs
+
+    cfg = configs.config(args.config)
+    kernel = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
+    F, nz = kernel.n_freq, cfg.grid.grid.nz
+    D = cfg.relay.count
+    rng = np.random.default_rng(cfg.seed)
+    # S3 cost is data-independent FFT work: seeded random-phase coefficients stand in
+    coeff = np.exp(2j * np.pi * rng.random((1, D, F)))
+    sl = _HostSlices(kernel.frequencies, coeff, cfg.relay, cfg.illuminations)
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    n_tr = 2048
+    h = rng.poisson(2.0, size=(n_tr, cfg.n_bins)).astype(np.float64)
+    units = [(i % F, (2 * i) % nz, (2 * i) % nz + 2) for i in range(ncores)]
+    _REF_STATE["slices"], _REF_STATE["grid"] = sl, cfg.grid
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(ncores) as pool:
+        for it in range(args.warmup + args.steps):
+            t = time.perf_counter()
+            pool.map(_ref_unit, units)
+            t_par = time.perf_counter() - t
+            t = time.perf_counter()
+            O.to_frequency(h, kernel.bin_indices, kernel.frequencies, kernel.weights, cfg.t0)
+            t_s1 = (time.perf_counter() - t) * D / n_tr / ncores
+            if it >= args.warmup:
+                sample_units = len(units) * 2
+                est = t_par * (F * nz) / sample_units + t_s1
+                times.append(est)
+    est = statistics.mean(times)
+    value = cfg.n_voxels / est
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c128 (float64)", "data": "synthetic (seeded random-phase slices, Poisson hist)",
+        "config": {"workload": f"config{args.config}-rsd", "voxels": cfg.n_voxels,
+                   "pad": "reference 1050"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
+                         "sample": f"per step: {len(units)} processes x (1 freq x 2 planes) of "
+                                   f"oracle.rsd + to_frequency on {n_tr} traces, extrapolated to "
+                                   f"{F}x{nz} units and {D} traces"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

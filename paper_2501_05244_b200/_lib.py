@@ -57,6 +57,11 @@ _RESTYPES = {"pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64}
 
 _lib = None
 
+# calls that enqueue kernels (bench.py reports how many ran in its timed region)
+_LAUNCHERS = {"pf_temporal_dft", "pf_temporal_dft_direct", "pf_fft_lines", "pf_embed_centered",
+              "pf_prop_kernel_rows", "pf_prop_columns", "pf_prop_rows_out"}
+launch_count = 0
+
 
 class PfError(RuntimeError):
     """A libpfgpu call failed (argument or CUDA error)."""
@@ -89,7 +94,10 @@ def last_error() -> str:
 
 
 def call(name: str, *args) -> int:
+    global launch_count
     rc = getattr(load(), name)(*args)
+    if name in _LAUNCHERS:
+        launch_count += 1
     if name in _RESTYPES:
         return rc
     if rc != 0:

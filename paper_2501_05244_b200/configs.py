@@ -1,0 +1,106 @@
+"""The BASELINE.json configurations as seeded synthetic instances.
+
+Shared conventions: relay lattice cell-centred on [-1, 1]^2, laser at the
+relay centre, scatterers uniform with ``default_rng(1000 + c)``, albedo
+U[0.5, 1], transients per ``sim.simulate_device`` (out-of-window returns
+dropped), Poisson noise at a mean peak of 100 counts, kernel from
+``build_kernel`` (default threshold) -> F = 16/16/16/24/32.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import core
+from .core import SPEED_OF_LIGHT
+
+
+@dataclass
+class Config:
+    name: str
+    relay: object
+    illuminations: core.PointList
+    grid: object
+    scatterers: np.ndarray
+    albedo: np.ndarray
+    n_bins: int
+    delta_t: float
+    lambda_c: float
+    t0: float
+    algorithm: str
+    seed: int
+
+    @property
+    def n_voxels(self) -> int:
+        return int(self.grid.count)
+
+
+def _lattice(n: int) -> core.UniformGrid2D:
+    p = 2.0 / n
+    return core.UniformGrid2D(n, n, p, p, -1.0 + p / 2, -1.0 + p / 2, 0.0)
+
+
+def _rect_scene(rng, centres, depths, half, per):
+    pts = []
+    for (cx, cy), z in zip(centres, depths):
+        xy = rng.uniform(-half, half, size=(per, 2)) + np.array([cx, cy])
+        pts.append(np.column_stack([xy, np.full(per, z)]))
+    return np.vstack(pts)
+
+
+def config(c: int) -> Config:
+    seed = 1000 + c
+    rng = np.random.default_rng(seed)
+    ill = core.PointList(np.array([[0.0, 0.0]]))
+    if c in (0, 1):
+        n, T, dt, lam = 64, 2048, 8e-12, 0.06
+        sc = _rect_scene(rng, [(-0.5, -0.5), (0.0, 0.0), (0.5, 0.5)], [0.8, 1.2, 1.6], 0.25, 500)
+        al = rng.uniform(0.5, 1.0, size=sc.shape[0])
+        g2 = _lattice(n)
+        grid = core.CuboidGrid(core.UniformGrid3D(n, n, 64, g2.dx, g2.dy, 1.5 / 63, g2.x0, g2.y0,
+                                                  0.5))
+        if c == 0:
+            relay = core.UniformRelay(g2)
+            alg = "rsd"
+        else:
+            pts = rng.uniform(-1.0, 1.0, size=(4096, 2))
+            relay = core.NonUniformPlanarRelay(core.PointList(pts), 0.0)
+            alg = "nursd1"
+        return Config(f"c{c}", relay, ill, grid, sc, al, T, dt, lam, 0.0, alg, seed)
+    if c == 3:
+        n, T, dt, lam = 256, 4096, 8e-12, 0.08
+        sc = _rect_scene(rng, [(-0.4, -0.4), (0.4, -0.3), (0.0, 0.0), (-0.5, 0.6), (0.7, 0.7)],
+                         [1.0, 2.0, 3.0, 4.5, 6.0], 0.25, 2000)
+        al = rng.uniform(0.5, 1.0, size=sc.shape[0])
+        g2 = _lattice(n)
+        zs = np.linspace(1.0, 6.0, 128)
+        a = zs[0] / zs
+        grid = core.FrustumGrid(g2, zs, a, a)
+        return Config("c3", core.UniformRelay(g2), ill, grid, sc, al, T, dt, lam,
+                      1.0 / SPEED_OF_LIGHT, "srsd", seed)
+    if c == 4:
+        n, T, dt, lam = 512, 4096, 4e-12, 0.03
+        xy = rng.uniform(-1.0, 1.0, size=(10000, 2))
+        z = rng.uniform(0.5, 3.0, size=10000)
+        sc = np.column_stack([xy, z])
+        al = rng.uniform(0.5, 1.0, size=sc.shape[0])
+        g2 = _lattice(n)
+        grid = core.CuboidGrid(core.UniformGrid3D(n, n, 256, g2.dx, g2.dy, 2.5 / 255, g2.x0,
+                                                  g2.y0, 0.5))
+        return Config("c4", core.UniformRelay(g2), ill, grid, sc, al, T, dt, lam,
+                      0.9 / SPEED_OF_LIGHT, "rsd", seed)
+    raise ValueError(f"config {c} is not a bench configuration")
+
+
+def transients(cfg: Config, device=None, noise: bool = True):
+    """Float32 device histograms [1, D, T] for ``cfg`` (seeded)."""
+    from .sim import add_poisson_noise_device, simulate_device
+    det = cfg.relay.coordinates()
+    ill = core.illumination_coordinates(cfg.relay, cfg.illuminations)
+    h = simulate_device(cfg.scatterers, cfg.albedo, det, ill, cfg.n_bins, cfg.delta_t, cfg.t0,
+                        device=device)
+    if noise:
+        h = add_poisson_noise_device(h, 100.0, cfg.seed)
+    return h

@@ -1,0 +1,101 @@
+"""End-to-end public API: host transients in, host volume out.
+
+``TransientReconstructor`` is what a user of the reference calls as
+``to_frequency`` + ``reconstruct`` (reference phasor.py:107-127,
+reconstruct.py:776-809) when the capture sits in host memory: it streams the
+float32 histograms to the GPU in chunks on a copy stream, overlapping each
+chunk's host->device transfer with the temporal transform (K1) of the previous
+chunk, runs the propagation on the device and returns the volume to (pinned)
+host memory.  The device-resident sub-steps are exposed for benchmarking.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from .core import ReconstructionVolume
+from .phasor import TemporalPlan
+from .reconstruct import RsdEngine
+
+
+class _Meta:
+    """Slices geometry without coefficients (what the engines need to plan)."""
+
+    def __init__(self, kernel, relay, illuminations):
+        self.frequencies = np.asarray(kernel.frequencies)
+        self.relay = relay
+        self.illuminations = illuminations
+        self.n_freq = int(self.frequencies.size)
+
+
+class TransientReconstructor:
+    """rsd from host histograms [I, D, T] (float32) to a host volume.
+
+    ``plane_range`` restricts the planes (multi-GPU sharding); ``trace_range``
+    restricts the detectors this instance transforms (K1 sharding).
+    """
+
+    def __init__(self, kernel, relay, illuminations, grid, t0: float = 0.0, padding="exact",
+                 include_illumination=True, times=None, plane_range=None, chunks: int = 8,
+                 device=None):
+        self.device = device or dev.require_cuda()
+        self.kernel = kernel
+        self.meta = _Meta(kernel, relay, illuminations)
+        self.engine = RsdEngine(self.meta, grid, padding, include_illumination, times,
+                                device=self.device, plane_range=plane_range)
+        self.temporal = TemporalPlan(kernel, t0, self.device)
+        self.n_illum = illuminations.count
+        self.n_det = relay.count
+        self.coeff = torch.empty((kernel.n_freq, self.n_illum, self.n_det), dtype=torch.complex64,
+                                 device=self.device)
+        self.vol = torch.zeros((self.engine.n_frames, self.engine.n_voxels), dtype=torch.complex64,
+                               device=self.device)
+        self.chunks = max(1, int(chunks))
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self._hist_dev = None
+        self._vol_host = None
+
+    # -- device-resident pieces -------------------------------------------------
+    def transform(self, hist_dev: torch.Tensor, stream=None) -> torch.Tensor:
+        """K1 over device histograms [I, D, T] -> self.coeff [F, I, D]."""
+        i_n, d_n, t_n = hist_dev.shape
+        self.temporal.run(hist_dev.view(i_n * d_n, t_n), self.coeff.view(self.kernel.n_freq, -1),
+                          stream)
+        return self.coeff
+
+    def propagate(self, coeff: torch.Tensor, stream=None) -> torch.Tensor:
+        return self.engine.run(coeff, self.vol, stream)
+
+    # -- host in, host out ------------------------------------------------------
+    def __call__(self, hist_host: torch.Tensor) -> torch.Tensor:
+        """hist_host: pinned float32 [I, D, T]; returns pinned host complex64 [frames, V]."""
+        i_n, d_n, t_n = hist_host.shape
+        n_tr = i_n * d_n
+        if self._hist_dev is None or self._hist_dev.shape != hist_host.shape:
+            self._hist_dev = torch.empty_like(hist_host, device=self.device)
+        if self._vol_host is None:
+            self._vol_host = torch.empty(self.vol.shape, dtype=self.vol.dtype, pin_memory=True)
+        src = hist_host.view(n_tr, t_n)
+        dst = self._hist_dev.view(n_tr, t_n)
+        out = self.coeff.view(self.kernel.n_freq, n_tr)
+        main = torch.cuda.current_stream(self.device)
+        step = (n_tr + self.chunks - 1) // self.chunks
+        for c0 in range(0, n_tr, step):
+            c1 = min(n_tr, c0 + step)
+            with torch.cuda.stream(self.copy_stream):
+                dst[c0:c1].copy_(src[c0:c1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.copy_stream)
+            main.wait_event(ev)
+            self.temporal.run(dst[c0:c1], out[:, c0:c1], main)
+        self.propagate(self.coeff, main)
+        self._vol_host.copy_(self.vol, non_blocking=True)
+        main.synchronize()
+        return self._vol_host
+
+    def volume(self, host_vol: torch.Tensor) -> ReconstructionVolume:
+        field = host_vol.numpy().astype(np.complex128)
+        times = self.engine.times
+        return ReconstructionVolume(self.engine.grid, field[0] if times is None else field, times)
