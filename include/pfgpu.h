@@ -76,9 +76,10 @@ int pf_fft_lines(void* data, const pf_fft_plan* plan, int64_t nlines, int64_t in
 /* Embed relay planes into zero-padded natural-order grids (the reference's
  * _pad_embed + ifftshift, reconstruct.py:113-119 with spectral.py:107-109).
  * src: c64 [nb][ny][nx] (row pitch src_ld), dst: c64 [nb][py][px].  Centred
- * relay index i - n//2 lands at natural slot (i - n//2) mod p. */
+ * relay index i - n//2 lands at natural slot (i - n//2) mod p.  transpose=1 writes
+ * the transposed grid [nb][px][py] (the register path consumes Uhat^T). */
 int pf_embed_centered(const void* src, int64_t nb, int ny, int nx, int64_t src_batch_stride,
-                      void* dst, int py, int px, void* stream);
+                      void* dst, int py, int px, int transpose, void* stream);
 
 /* ---------------------------------------------------------------- propagation
  * Plane-to-plane RSD propagation, the per-(frequency, plane) inner loop of
@@ -107,6 +108,10 @@ typedef struct pf_prop_geom {
   int include_illum;
   int64_t uhat_illum_stride; /* elements between illuminations inside uhat */
 } pf_prop_geom;
+
+/* Pad size handled by the register-FFT path (square power-of-two 128..1024), else 0.
+ * When nonzero, the three stages expect uhat TRANSPOSED: Uhat^T[col][row]. */
+int pf_prop_fast(const pf_prop_geom* g);
 
 /* workspace element counts (c64) for a batch of nplanes */
 int64_t pf_prop_ws_a(const pf_prop_geom* g, int nplanes);

@@ -45,7 +45,8 @@ _SIGNATURES = {
     "pf_temporal_dft": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, _vp],
     "pf_temporal_dft_direct": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, _vp],
     "pf_fft_lines": [_vp, _P(PfFftPlan), _i64, _i64, _i64, _i64, _i64, _i, _f, _vp],
-    "pf_embed_centered": [_vp, _i64, _i, _i, _i64, _vp, _i, _i, _vp],
+    "pf_embed_centered": [_vp, _i64, _i, _i, _i64, _vp, _i, _i, _i, _vp],
+    "pf_prop_fast": [_P(PfPropGeom)],
     "pf_prop_ws_a": [_P(PfPropGeom), _i],
     "pf_prop_ws_b": [_P(PfPropGeom), _i],
     "pf_prop_kernel_rows": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp],
@@ -53,7 +54,8 @@ _SIGNATURES = {
     "pf_prop_rows_out": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp,
                          _i64, _vp],
 }
-_RESTYPES = {"pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64}
+_RESTYPES = {"pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
+             "pf_prop_fast": ctypes.c_int}
 
 _lib = None
 

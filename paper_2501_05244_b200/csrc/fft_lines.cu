@@ -45,14 +45,17 @@ k_fft_lines(float2* __restrict__ data, pf_fft_plan plan, long long nlines, long 
   }
 }
 
+// transpose=1 writes dst[bb][jx][jy] (the transposed grid, px rows of py)
 __global__ void k_embed_centered(const float2* __restrict__ src, long long nb, int ny, int nx,
-                                 long long sbs, float2* __restrict__ dst, int py, int px) {
+                                 long long sbs, float2* __restrict__ dst, int py, int px,
+                                 int transpose) {
   const long long total = nb * (long long)py * px;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long bb = e / ((long long)py * px);
     const int rem = (int)(e - bb * (long long)py * px);
-    const int jy = rem / px, jx = rem - jy * px;
+    int jy, jx;
+    if (transpose) { jx = rem / py; jy = rem - jx * py; } else { jy = rem / px; jx = rem - jy * px; }
     const int iy = centred(jy, py) + ny / 2;
     const int ix = centred(jx, px) + nx / 2;
     float2 v = make_float2(0.f, 0.f);
@@ -108,14 +111,14 @@ extern "C" int pf_fft_lines(void* data, const pf_fft_plan* plan, int64_t nlines,
 
 extern "C" int pf_embed_centered(const void* src, int64_t nb, int ny, int nx,
                                  int64_t src_batch_stride, void* dst, int py, int px,
-                                 void* stream) {
+                                 int transpose, void* stream) {
   PF_ARG_CHECK(nb >= 0 && ny >= 1 && nx >= 1 && py >= ny && px >= nx,
                "pf_embed_centered: bad sizes");
   if (nb == 0) return 0;
   const long long total = nb * (long long)py * px;
   const int grid = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
   k_embed_centered<<<grid, 256, 0, (cudaStream_t)stream>>>(
-      (const float2*)src, nb, ny, nx, src_batch_stride, (float2*)dst, py, px);
+      (const float2*)src, nb, ny, nx, src_batch_stride, (float2*)dst, py, px, transpose);
   PF_LAUNCH_CHECK("k_embed_centered");
   return 0;
 }

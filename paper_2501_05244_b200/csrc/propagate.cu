@@ -172,6 +172,15 @@ int rows_fit(int n, int bufs, int want) {
 
 }  // namespace
 
+int pf_prop_fast_L(const pf_prop_geom* g);
+int pf_prop_fast_stage(int stage, const pf_plane* planes, int nplanes, double khat,
+                       const pf_prop_geom* g, const pf_fft_plan* plan, const void* ws_a_in,
+                       void* ws_a_out, const void* uhat, const void* ws_b_in, void* ws_b_out,
+                       const double* ill, const void* frame_w, int n_frames, void* vol,
+                       long long vfs, cudaStream_t st);
+
+extern "C" int pf_prop_fast(const pf_prop_geom* g) { return g ? 32 * pf_prop_fast_L(g) : 0; }
+
 extern "C" int64_t pf_prop_ws_a(const pf_prop_geom* g, int nplanes) {
   return (int64_t)nplanes * (g->py / 2 + 1) * (g->px / 2 + 1);
 }
@@ -184,6 +193,9 @@ extern "C" int pf_prop_kernel_rows(const pf_plane* planes, int nplanes, double k
                                    const pf_prop_geom* g, const pf_fft_plan* plan_x, void* ws_a,
                                    void* stream) {
   PF_ARG_CHECK(g && plan_x && plan_x->n == g->px && nplanes >= 1, "pf_prop_kernel_rows: bad args");
+  if (pf_prop_fast_L(g))
+    return pf_prop_fast_stage(0, planes, nplanes, khat, g, plan_x, nullptr, ws_a, nullptr, nullptr,
+                              nullptr, nullptr, nullptr, 0, nullptr, 0, (cudaStream_t)stream);
   static bool attr = false;
   if (!attr) { allow_smem(k_prop_kernel_rows); attr = true; }
   const int rows_a = g->py / 2 + 1;
@@ -201,6 +213,9 @@ extern "C" int pf_prop_columns(const pf_plane* planes, int nplanes, const pf_pro
                                const pf_fft_plan* plan_y, const void* ws_a, const void* uhat,
                                void* ws_b, void* stream) {
   PF_ARG_CHECK(g && plan_y && plan_y->n == g->py && nplanes >= 1, "pf_prop_columns: bad args");
+  if (pf_prop_fast_L(g))
+    return pf_prop_fast_stage(1, planes, nplanes, 0.0, g, plan_y, ws_a, nullptr, uhat, nullptr,
+                              ws_b, nullptr, nullptr, 0, nullptr, 0, (cudaStream_t)stream);
   static bool attr = false;
   if (!attr) { allow_smem(k_prop_columns); attr = true; }
   const int cols_a = g->px / 2 + 1;
@@ -220,6 +235,10 @@ extern "C" int pf_prop_rows_out(const pf_plane* planes, int nplanes, double khat
                                 int n_frames, void* vol, int64_t vol_frame_stride, void* stream) {
   PF_ARG_CHECK(g && plan_x && plan_x->n == g->px && nplanes >= 1 && n_frames >= 1,
                "pf_prop_rows_out: bad args");
+  if (pf_prop_fast_L(g))
+    return pf_prop_fast_stage(2, planes, nplanes, khat, g, plan_x, nullptr, nullptr, nullptr, ws_b,
+                              nullptr, ill_xyz, frame_w, n_frames, vol, vol_frame_stride,
+                              (cudaStream_t)stream);
   static bool attr = false;
   if (!attr) { allow_smem(k_prop_rows_out); attr = true; }
   int rpc = rows_fit(g->px, 2, (2 * PT + g->px - 1) / g->px);

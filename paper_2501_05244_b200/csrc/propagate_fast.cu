@@ -1,0 +1,295 @@
+// Register-FFT propagation path for square power-of-two pads P = 32 L
+// (L = 4..32: P = 128 .. 1024; configs 0, 3 and 4).
+//
+// Same math as propagate.cu (reference rsd reconstruct.py:254-266 and its
+// siblings), restructured around warp_fft.cuh so each 1D transform lives in
+// registers (one shared-memory exchange per transform) and every global
+// access is a contiguous run:
+//   (A) line = kernel row jy in [0, P/2]: synthesise G, x-FFT, keep kx <= P/2,
+//       stage through shared memory, store transposed  At[plane][kx][jy].
+//   (B) line = (plane, kx):  read At row (mirrored to P), y-FFT -> Ghat column;
+//       for each illumination and each of the columns kx, P-kx: * Uhat^T row,
+//       y-IFFT, store the cropped rows to Tt[plane][p][col][i] (contiguous i).
+//   (C) tile of output rows i: load Tt[.][.][col][i0..i0+R) (contiguous runs),
+//       transpose in shared memory, x-IFFT per row, crop, illumination phase,
+//       sum illuminations, accumulate frames into the volume.
+// Uhat is consumed TRANSPOSED (Uhat^T[col][jy]) on this path; the host asks
+// pf_prop_fast() before building it.
+#include "warp_fft.cuh"
+
+namespace {
+
+constexpr int FT = 256;  // 8 warps
+
+// exp(1j * 2 pi * kturns * r) / r with r = sqrt(r2): float sqrt + one float64
+// Newton correction, phase reduced in turns (float64) -- ~10 DP ops, no DP sqrt.
+__device__ __forceinline__ float2 g_kernel(double r2, double kturns) {
+  const float rf = sqrtf((float)r2);
+  const double e = fma(-(double)rf, (double)rf, r2);
+  const float d = (float)e * (0.5f / rf);
+  const double turns = fma(kturns, (double)rf, kturns * (double)d);
+  const float fr = (float)(turns - rint(turns));
+  float s, c;
+  __sincosf(6.28318530717958647692f * fr, &s, &c);
+  const float ir = 1.0f / rf;
+  return make_float2(c * ir, s * ir);
+}
+
+__device__ __forceinline__ float2 phase_turns(double r2, double kturns) {
+  const float rf = sqrtf((float)r2);
+  const double e = fma(-(double)rf, (double)rf, r2);
+  const float d = (float)e * (0.5f / rf);
+  const double turns = fma(kturns, (double)rf, kturns * (double)d);
+  const float fr = (float)(turns - rint(turns));
+  float s, c;
+  __sincosf(6.28318530717958647692f * fr, &s, &c);
+  return make_float2(c, s);
+}
+
+template <int L>
+__global__ void __launch_bounds__(FT, 2)
+k_pa(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
+     const float2* __restrict__ tw, float2* __restrict__ ws_a) {
+  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
+  constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
+  extern __shared__ float2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int r = warp * LPW + line;
+  const int jy0 = blockIdx.x * RPC;
+  const int jy = jy0 + r;
+  const pf_plane pl = planes[blockIdx.y];
+  const double ly = (double)jy * pl.lag_dy;
+  const double base = fma(ly, ly, pl.dz * pl.dz);
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 32; m++) {
+    const double lx = (double)centred(t + L * m, P) * pl.lag_dx;
+    v[m] = g_kernel(fma(lx, lx, base), kturns);
+  }
+  wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
+  __syncthreads();
+  if (jy <= H) {
+#pragma unroll
+    for (int m = 0; m < 32; m++) {
+      const int kx = t + L * m;
+      if (kx <= H) sm[kx * SLD + r] = v[m];
+    }
+  }
+  __syncthreads();
+  const int nr = min(RPC, NA - jy0);
+  float2* dst = ws_a + (long long)blockIdx.y * NA * NA + jy0;
+  for (int e = threadIdx.x; e < NA * nr; e += FT) {
+    const int kx = e / nr, rr = e - kx * nr;
+    dst[(long long)kx * NA + rr] = sm[kx * SLD + rr];
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(FT, 1)
+k_pb(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
+     const float2* __restrict__ tw, const float2* __restrict__ ws_a,
+     const float2* __restrict__ uhat_t, float2* __restrict__ ws_b) {
+  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
+  constexpr int LPW = 32 / L;
+  extern __shared__ float2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int kx = blockIdx.x;
+  const int b = (blockIdx.y * 8 + warp) * LPW + line;
+  const bool active = b < nplanes;
+  const int bb = active ? b : nplanes - 1;
+  const pf_plane pl = planes[bb];
+  const float2* arow = ws_a + ((long long)bb * NA + kx) * NA;
+  float2 gh[32];
+#pragma unroll
+  for (int m = 0; m < 32; m++) {
+    const int jy = t + L * m;
+    gh[m] = __ldg(arow + (jy <= H ? jy : P - jy));
+  }
+  float2* xch = sm + warp * WFFT_XCH;
+  wfft<L, -1>(gh, xch, tw);
+  const int ny = g.ny;
+  for (int p = 0; p < g.n_illum; p++) {
+    const float2* up = uhat_t + pl.uhat_off + (long long)p * g.uhat_illum_stride;
+    float2* outp = ws_b + ((long long)bb * g.n_illum + p) * (long long)P * ny;
+#pragma unroll 1
+    for (int side = 0; side < 2; side++) {
+      const int col = side == 0 ? kx : (P - kx) % P;
+      if (side == 1 && col == kx) break;
+      const float2* ucol = up + (long long)col * P;
+      float2 w[32];
+#pragma unroll
+      for (int m = 0; m < 32; m++) w[m] = cmul(gh[m], __ldg(ucol + t + L * m));
+      wfft<L, 1>(w, xch, tw);
+      if (active) {
+        float2* dcol = outp + (long long)col * ny;
+#pragma unroll
+        for (int m = 0; m < 32; m++) {
+          const int i = (t + L * m - g.nu0y) & (P - 1);
+          if (i < ny) dcol[i] = w[m];
+        }
+      }
+    }
+  }
+}
+
+// MULTI: more than one illumination (contributions summed in registers first)
+template <int L, bool MULTI>
+__global__ void __launch_bounds__(FT, MULTI ? 1 : 2)
+k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
+     const float2* __restrict__ tw, const float2* __restrict__ ws_b,
+     const double* __restrict__ ill, const float2* __restrict__ frame_w, int n_frames,
+     float2* __restrict__ vol, long long vol_frame_stride) {
+  constexpr int P = 32 * L;
+  constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
+  extern __shared__ float2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int r = warp * LPW + line;
+  const int ny = g.ny, nx = g.nx;
+  const int i0 = blockIdx.x * RPC;
+  const int i = i0 + r;
+  const int nr = min(RPC, ny - i0);
+  const pf_plane pl = planes[blockIdx.y];
+  const float scale = 1.0f / ((float)P * (float)P);
+  float2 acc[MULTI ? 32 : 1];
+  float2 v[32];
+  const double yv = pl.y0 + pl.dy * i;
+  const int n_ill = MULTI ? g.n_illum : 1;
+#pragma unroll 1
+  for (int p = 0; p < n_ill; p++) {
+    const float2* src = ws_b + ((long long)blockIdx.y * g.n_illum + p) * (long long)P * ny + i0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < P * nr; e += FT) {
+      const int col = e / nr, rr = e - col * nr;
+      sm[col * SLD + rr] = src[(long long)col * ny + rr];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 32; m++) v[m] = sm[(t + L * m) * SLD + r];
+    __syncthreads();
+    wfft<L, 1>(v, sm + warp * WFFT_XCH, tw);
+    const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
+    const double dy = yv - sy, dz = pl.z - sz;
+    const double byz = fma(dy, dy, dz * dz);
+    const long long off = (pl.vol_plane * ny + i) * (long long)nx;
+#pragma unroll
+    for (int m = 0; m < 32; m++) {
+      const int mo = (t + L * m - g.nu0x) & (P - 1);
+      float2 val = cscale(v[m], scale);
+      if (g.include_illum) {
+        const double dx = pl.x0 + pl.dx * mo - sx;
+        val = cmul(val, phase_turns(fma(dx, dx, byz), kturns));
+      }
+      if (MULTI) {
+        if (p == 0) acc[m] = val; else acc[m] = cadd(acc[m], val);
+      } else if (i < ny && mo < nx) {
+        for (int fr = 0; fr < n_frames; fr++) {
+          float2* d = vol + fr * vol_frame_stride + off + mo;
+          *d = cadd(*d, cmul(val, frame_w[fr]));
+        }
+      }
+    }
+  }
+  if (MULTI && i < ny) {
+    const long long off = (pl.vol_plane * ny + i) * (long long)nx;
+    for (int fr = 0; fr < n_frames; fr++) {
+      const float2 fw = frame_w[fr];
+      float2* drow = vol + fr * vol_frame_stride + off;
+#pragma unroll
+      for (int m = 0; m < 32; m++) {
+        const int mo = (t + L * m - g.nu0x) & (P - 1);
+        if (mo < nx) drow[mo] = cadd(drow[mo], cmul(acc[m], fw));
+      }
+    }
+  }
+}
+
+template <int L>
+size_t smem_a() {
+  constexpr int P = 32 * L, NA = P / 2 + 1, RPC = 8 * (32 / L);
+  size_t x = 8 * WFFT_XCH, s = (size_t)NA * (RPC + 1);
+  return (x > s ? x : s) * sizeof(float2);
+}
+template <int L>
+size_t smem_c() {
+  constexpr int P = 32 * L, RPC = 8 * (32 / L);
+  size_t x = 8 * WFFT_XCH, s = (size_t)P * (RPC + 1);
+  return (x > s ? x : s) * sizeof(float2);
+}
+
+template <int L>
+int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const pf_prop_geom& g,
+              const float2* tw, const float2* ws_a, float2* ws_a_out, const float2* uhat,
+              const float2* ws_b, float2* ws_b_out, const double* ill, const float2* frame_w,
+              int n_frames, float2* vol, long long vfs, cudaStream_t st) {
+  constexpr int P = 32 * L, NA = P / 2 + 1, RPC = 8 * (32 / L), LPW = 32 / L;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pa<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_pb<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_pc<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_pc<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const double kturns = khat / PF_TWO_PI;
+  if (stage == 0) {
+    dim3 grid(pf_cdiv(NA, RPC), nplanes);
+    k_pa<L><<<grid, FT, smem_a<L>(), st>>>(planes, kturns, g, tw, ws_a_out);
+    PF_LAUNCH_CHECK("k_pa");
+  } else if (stage == 1) {
+    dim3 grid(NA, pf_cdiv(nplanes, 8 * LPW));
+    k_pb<L><<<grid, FT, 8 * WFFT_XCH * sizeof(float2), st>>>(planes, nplanes, g, tw, ws_a, uhat,
+                                                             ws_b_out);
+    PF_LAUNCH_CHECK("k_pb");
+  } else {
+    dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
+    if (g.n_illum > 1)
+      k_pc<L, true><<<grid, FT, smem_c<L>(), st>>>(planes, kturns, g, tw, ws_b, ill, frame_w,
+                                                   n_frames, vol, vfs);
+    else
+      k_pc<L, false><<<grid, FT, smem_c<L>(), st>>>(planes, kturns, g, tw, ws_b, ill, frame_w,
+                                                    n_frames, vol, vfs);
+    PF_LAUNCH_CHECK("k_pc");
+  }
+  return 0;
+}
+
+}  // namespace
+
+// 32*L when the register path applies (square power-of-two pad 128..1024), else 0
+int pf_prop_fast_L(const pf_prop_geom* g) {
+  if (g->px != g->py) return 0;
+  switch (g->px) {
+    case 128: return 4;
+    case 256: return 8;
+    case 512: return 16;
+    case 1024: return 32;
+    default: return 0;
+  }
+}
+
+int pf_prop_fast_stage(int stage, const pf_plane* planes, int nplanes, double khat,
+                       const pf_prop_geom* g, const pf_fft_plan* plan, const void* ws_a_in,
+                       void* ws_a_out, const void* uhat, const void* ws_b_in, void* ws_b_out,
+                       const double* ill, const void* frame_w, int n_frames, void* vol,
+                       long long vfs, cudaStream_t st) {
+  const float2* tw = (const float2*)plan->tw;
+#define PF_FAST_CASE(LL)                                                                      \
+  case LL:                                                                                    \
+    return run_stage<LL>(stage, planes, nplanes, khat, *g, tw, (const float2*)ws_a_in,        \
+                         (float2*)ws_a_out, (const float2*)uhat, (const float2*)ws_b_in,      \
+                         (float2*)ws_b_out, ill, (const float2*)frame_w, n_frames,            \
+                         (float2*)vol, vfs, st);
+  switch (pf_prop_fast_L(g)) {
+    PF_FAST_CASE(4)
+    PF_FAST_CASE(8)
+    PF_FAST_CASE(16)
+    PF_FAST_CASE(32)
+    default: break;
+  }
+#undef PF_FAST_CASE
+  pf_set_error("pf_prop_fast_stage: geometry not eligible");
+  return -1;
+}

@@ -161,6 +161,8 @@ class Propagator:
                                 dtype=torch.complex64, device=device)
         self.plan_x = dev.fft_plan(px, device)
         self.plan_y = dev.fft_plan(py, device)
+        # register-FFT path (square power-of-two pads) consumes Uhat transposed
+        self.transposed = bool(_lib.call("pf_prop_fast", ctypes.byref(g)))
 
     def run_frequency(self, uhat_ptr: int, khat: float, ill_ptr: int, frame_w_ptr: int,
                       n_frames: int, vol: torch.Tensor, vol_frame_stride: int,
@@ -271,9 +273,13 @@ class RsdEngine:
         """Uhat_f = cfft2(pad_embed(u_f)) for all (f, p), natural order (reconstruct.py:259-260)."""
         g = self.relay_grid
         F, I = self.freqs.size, self.n_illum
+        tr = self.prop.transposed
         _lib.call("pf_embed_centered", dev.ptr(coeff), F * I, g.ny, g.nx, g.ny * g.nx,
-                  dev.ptr(self.uhat), self.py, self.px, dev.stream_ptr(stream))
-        dev.fft2_natural(self.uhat, self.py, self.px, F * I, -1, 1.0, stream)
+                  dev.ptr(self.uhat), self.py, self.px, int(tr), dev.stream_ptr(stream))
+        if tr:   # FFT2 of the transposed grid is the transposed spectrum
+            dev.fft2_natural(self.uhat, self.px, self.py, F * I, -1, 1.0, stream)
+        else:
+            dev.fft2_natural(self.uhat, self.py, self.px, F * I, -1, 1.0, stream)
         return self.uhat
 
     def run(self, coeff: torch.Tensor, vol: torch.Tensor | None = None, stream=None):

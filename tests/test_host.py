@@ -48,7 +48,7 @@ def test_library_exports_every_declared_symbol():
 def test_error_channel_without_device():
     lib = _lib.load()
     # argument errors are reported before any CUDA call
-    rc = lib.pf_embed_centered(None, 1, 4, 4, 16, None, 2, 2, None)
+    rc = lib.pf_embed_centered(None, 1, 4, 4, 16, None, 2, 2, 0, None)
     assert rc < 0
     assert "pf_embed_centered" in _lib.last_error()
 
