@@ -290,11 +290,16 @@ class RsdEngine:
             vol.zero_()
         uhat = self.relay_spectra(coeff, stream)
         per_f = self.n_illum * self.py * self.px
-        for fi in range(self.freqs.size):
-            khat = float(self.freqs[fi]) / SPEED_OF_LIGHT
-            self.prop.run_frequency(dev.ptr(uhat) + 8 * fi * per_f, khat, dev.ptr(self.ill),
-                                    dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
-                                    self.n_frames, vol, self.n_voxels, stream=stream)
+        # plane batches outer, frequencies inner: the batch's volume slice stays
+        # L2-resident across its ascending-frequency accumulation
+        for b0 in range(0, self.prop.nplanes, self.prop.batch):
+            b1 = min(self.prop.nplanes, b0 + self.prop.batch)
+            for fi in range(self.freqs.size):
+                khat = float(self.freqs[fi]) / SPEED_OF_LIGHT
+                self.prop.run_frequency(dev.ptr(uhat) + 8 * fi * per_f, khat, dev.ptr(self.ill),
+                                        dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
+                                        self.n_frames, vol, self.n_voxels, plane_lo=b0,
+                                        plane_hi=b1, stream=stream)
         return vol
 
 
