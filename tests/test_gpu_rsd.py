@@ -144,3 +144,49 @@ def test_rsd_c0_like_end_to_end(rng):
     ref = O.rsd(sl.to_host(), grid)
     assert O.rel_l2(vol.field, ref) < TOL
     assert _argmax_same(vol.field, ref, grid.shape)
+
+
+def _random_slices(rng, relay, n_freq=4, n_ill=1, w0=2 * np.pi * 3e8 / 0.06):
+    freqs = w0 * (1.0 + 0.02 * np.arange(n_freq))
+    D = relay.count
+    coeff = (rng.normal(size=(n_ill, D, n_freq)) + 1j * rng.normal(size=(n_ill, D, n_freq)))
+    ill = pf.PointList(rng.uniform(-0.5, 0.5, size=(n_ill, 2)))
+    return pf.FrequencySlices(freqs, coeff, relay, ill)
+
+
+@pytest.mark.parametrize("n,nx,ny,off,n_ill,video", [
+    (64, 64, 64, 0, 1, False),      # P = 128 register path, config-0 geometry
+    (64, 40, 24, 3, 2, False),      # offset output window, two illuminations (MULTI kernel)
+    (128, 128, 128, 0, 1, True),    # P = 256, time-resolved frames
+    (256, 256, 256, 0, 1, False),   # P = 512
+])
+def test_rsd_register_path_vs_oracle(rng, n, nx, ny, off, n_ill, video):
+    pitch = 2.0 / n
+    g = pf.UniformGrid2D(n, n, pitch, pitch, -1 + pitch / 2, -1 + pitch / 2, 0.0)
+    relay = pf.UniformRelay(g)
+    sl = _random_slices(rng, relay, n_freq=3, n_ill=n_ill)
+    x0 = g.x0 + pitch * ((n - nx) // 2 + off)
+    y0 = g.y0 + pitch * ((n - ny) // 2 - off)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(nx, ny, 3, pitch, pitch, 0.37, x0, y0, 0.45))
+    times = np.array([0.0, 2e-10, -1e-10]) if video else None
+    from paper_2501_05244_b200.reconstruct import RsdEngine
+    eng = RsdEngine(sl, grid, times=times)
+    assert eng.prop.transposed, (eng.px, eng.py)
+    vol = pf.rsd(sl, grid, times=times)
+    ref = O.rsd(sl, grid, times=times)
+    assert O.rel_l2(vol.field, ref) < TOL
+    if not video:
+        assert _argmax_same(vol.field, ref, grid.shape)
+
+
+def test_rsd_register_path_literal_subsample(rng):
+    """Exact physics (1/r literal sum, reference helpers.py:69-101) on a voxel subsample."""
+    n = 64
+    pitch = 2.0 / n
+    g = pf.UniformGrid2D(n, n, pitch, pitch, -1 + pitch / 2, -1 + pitch / 2, 0.0)
+    sl = _random_slices(rng, pf.UniformRelay(g), n_freq=2)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(n, n, 2, pitch, pitch, 0.5, g.x0, g.y0, 0.6))
+    vol = pf.rsd(sl, grid)
+    idx = rng.choice(grid.count, size=40, replace=False)
+    lit = O.literal_field(sl, grid.coordinates()[idx])
+    assert O.rel_l2(vol.field[idx], lit) < TOL
