@@ -71,8 +71,11 @@ def _exact_pad(lag_max: float, nu_max: float, n_min: int) -> int:
     changes the volume by <= 6e-16), so the GPU drops the reference's +8 margin
     (140 -> 128 at config 0, 1050 -> 1024 at config 4).
     """
-    need = 2 * math.ceil(max(lag_max, nu_max)) + 2
-    return next_fast_len(max(n_min, need))
+    need = max(n_min, 2 * math.ceil(max(lag_max, nu_max)) + 2)
+    p2 = dev.pow2_ceil(need)
+    if 64 < need and p2 <= 1024 and p2 * 5 <= need * 8:
+        return p2   # square power-of-two pads take the register-FFT path
+    return next_fast_len(need)
 
 
 def _uniform_relay(slices):
