@@ -61,11 +61,21 @@ k_pa(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
   const pf_plane pl = planes[blockIdx.y];
   const double ly = (double)jy * pl.lag_dy;
   const double base = fma(ly, ly, pl.dz * pl.dz);
+  // G is even in x: slots jx and P-jx hold the same value.  Synthesise
+  // m = 0..16 (jx <= P/2 + t) and fetch m = 17..31 from the mirror lane
+  // (L - t, element 31 - m), or from this lane's element 32 - m when t = 0.
   float2 v[32];
 #pragma unroll
-  for (int m = 0; m < 32; m++) {
+  for (int m = 0; m <= 16; m++) {
     const double lx = (double)centred(t + L * m, P) * pl.lag_dx;
     v[m] = g_kernel(fma(lx, lx, base), kturns);
+  }
+  const int mirror = (lane - t) + ((L - t) & (L - 1));
+#pragma unroll
+  for (int m = 17; m < 32; m++) {
+    const float2 o = make_float2(__shfl_sync(0xffffffffu, v[31 - m].x, mirror),
+                                 __shfl_sync(0xffffffffu, v[31 - m].y, mirror));
+    v[m] = (t == 0) ? v[32 - m] : o;
   }
   wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
   __syncthreads();
@@ -79,9 +89,9 @@ k_pa(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
   __syncthreads();
   const int nr = min(RPC, NA - jy0);
   float2* dst = ws_a + (long long)blockIdx.y * NA * NA + jy0;
-  for (int e = threadIdx.x; e < NA * nr; e += FT) {
-    const int kx = e / nr, rr = e - kx * nr;
-    dst[(long long)kx * NA + rr] = sm[kx * SLD + rr];
+  for (int e = threadIdx.x; e < NA * RPC; e += FT) {
+    const int kx = e / RPC, rr = e % RPC;   // compile-time divisor
+    if (rr < nr) dst[(long long)kx * NA + rr] = sm[kx * SLD + rr];
   }
 }
 
@@ -134,8 +144,10 @@ k_pb(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
   }
 }
 
-// MULTI: more than one illumination (contributions summed in registers first)
-template <int L, bool MULTI>
+// MULTI: more than one illumination (contributions summed in registers first).
+// PRE: single frame and the CTA's volume rows fit next to the tile: they are
+// prefetched with cp.async at entry so the accumulate is load-free at the end.
+template <int L, bool MULTI, bool PRE>
 __global__ void __launch_bounds__(FT, MULTI ? 1 : 2)
 k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
      const float2* __restrict__ tw, const float2* __restrict__ ws_b,
@@ -143,7 +155,9 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
      float2* __restrict__ vol, long long vol_frame_stride) {
   constexpr int P = 32 * L;
   constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
+  constexpr int UNION = (8 * WFFT_XCH > P * SLD) ? 8 * WFFT_XCH : P * SLD;
   extern __shared__ float2 sm[];
+  float2* volbuf = sm + UNION;   // [RPC][nx] when PRE
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = lane % L, line = lane / L;
   const int r = warp * LPW + line;
@@ -153,6 +167,13 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
   const int nr = min(RPC, ny - i0);
   const pf_plane pl = planes[blockIdx.y];
   const float scale = 1.0f / ((float)P * (float)P);
+  const long long vol_row0 = (pl.vol_plane * ny + i0) * (long long)nx;
+  if (PRE) {
+    for (int rr = 0; rr < nr; rr++)
+      for (int mo = threadIdx.x; mo < nx; mo += FT)
+        cp_async8(volbuf + rr * nx + mo, vol + vol_row0 + (long long)rr * nx + mo);
+    cp_async_commit();
+  }
   float2 acc[MULTI ? 32 : 1];
   float2 v[32];
   const double yv = pl.y0 + pl.dy * i;
@@ -160,11 +181,13 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
 #pragma unroll 1
   for (int p = 0; p < n_ill; p++) {
     const float2* src = ws_b + ((long long)blockIdx.y * g.n_illum + p) * (long long)P * ny + i0;
-    __syncthreads();
-    for (int e = threadIdx.x; e < P * nr; e += FT) {
-      const int col = e / nr, rr = e - col * nr;
-      sm[col * SLD + rr] = src[(long long)col * ny + rr];
+    if (p > 0) __syncthreads();
+    for (int e = threadIdx.x; e < P * RPC; e += FT) {
+      const int col = e / RPC, rr = e % RPC;
+      if (rr < nr) cp_async8(sm + col * SLD + rr, src + (long long)col * ny + rr);
     }
+    cp_async_commit();
+    cp_async_wait_all();
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < 32; m++) v[m] = sm[(t + L * m) * SLD + r];
@@ -173,7 +196,6 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
     const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
     const double dy = yv - sy, dz = pl.z - sz;
     const double byz = fma(dy, dy, dz * dz);
-    const long long off = (pl.vol_plane * ny + i) * (long long)nx;
 #pragma unroll
     for (int m = 0; m < 32; m++) {
       const int mo = (t + L * m - g.nu0x) & (P - 1);
@@ -184,23 +206,30 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
       }
       if (MULTI) {
         if (p == 0) acc[m] = val; else acc[m] = cadd(acc[m], val);
-      } else if (i < ny && mo < nx) {
-        for (int fr = 0; fr < n_frames; fr++) {
-          float2* d = vol + fr * vol_frame_stride + off + mo;
-          *d = cadd(*d, cmul(val, frame_w[fr]));
-        }
+      } else {
+        v[m] = val;
       }
     }
   }
-  if (MULTI && i < ny) {
-    const long long off = (pl.vol_plane * ny + i) * (long long)nx;
-    for (int fr = 0; fr < n_frames; fr++) {
-      const float2 fw = frame_w[fr];
-      float2* drow = vol + fr * vol_frame_stride + off;
+  if (i < ny) {
+    const long long off = vol_row0 + (long long)r * nx;
+    if (PRE) {
+      const float2* old = volbuf + r * nx;
+      const float2 fw = frame_w[0];
 #pragma unroll
       for (int m = 0; m < 32; m++) {
         const int mo = (t + L * m - g.nu0x) & (P - 1);
-        if (mo < nx) drow[mo] = cadd(drow[mo], cmul(acc[m], fw));
+        if (mo < nx) vol[off + mo] = cadd(old[mo], cmul(MULTI ? acc[m] : v[m], fw));
+      }
+    } else {
+      for (int fr = 0; fr < n_frames; fr++) {
+        const float2 fw = frame_w[fr];
+        float2* drow = vol + fr * vol_frame_stride + off;
+#pragma unroll
+        for (int m = 0; m < 32; m++) {
+          const int mo = (t + L * m - g.nu0x) & (P - 1);
+          if (mo < nx) drow[mo] = cadd(drow[mo], cmul(MULTI ? acc[m] : v[m], fw));
+        }
       }
     }
   }
@@ -213,10 +242,10 @@ size_t smem_a() {
   return (x > s ? x : s) * sizeof(float2);
 }
 template <int L>
-size_t smem_c() {
+size_t smem_c(int nx, bool pre) {
   constexpr int P = 32 * L, RPC = 8 * (32 / L);
   size_t x = 8 * WFFT_XCH, s = (size_t)P * (RPC + 1);
-  return (x > s ? x : s) * sizeof(float2);
+  return ((x > s ? x : s) + (pre ? (size_t)RPC * nx : 0)) * sizeof(float2);
 }
 
 template <int L>
@@ -229,8 +258,10 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
   if (!attr) {
     cudaFuncSetAttribute(k_pa<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_pb<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_pc<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_pc<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_pc<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_pc<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_pc<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_pc<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   const double kturns = khat / PF_TWO_PI;
@@ -245,12 +276,15 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     PF_LAUNCH_CHECK("k_pb");
   } else {
     dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
-    if (g.n_illum > 1)
-      k_pc<L, true><<<grid, FT, smem_c<L>(), st>>>(planes, kturns, g, tw, ws_b, ill, frame_w,
-                                                   n_frames, vol, vfs);
-    else
-      k_pc<L, false><<<grid, FT, smem_c<L>(), st>>>(planes, kturns, g, tw, ws_b, ill, frame_w,
-                                                    n_frames, vol, vfs);
+    const bool pre = n_frames == 1 && frame_w != nullptr && (size_t)RPC * g.nx * 8 <= 64 * 1024;
+    const size_t sm = smem_c<L>(g.nx, pre);
+    if (g.n_illum > 1) {
+      if (pre) k_pc<L, true, true><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
+      else k_pc<L, true, false><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
+    } else {
+      if (pre) k_pc<L, false, true><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
+      else k_pc<L, false, false><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
+    }
     PF_LAUNCH_CHECK("k_pc");
   }
   return 0;

@@ -148,8 +148,12 @@ class Propagator:
         self.geom = g
         self.nplanes = len(planes)
         per_plane = 8 * ((py // 2 + 1) * (px // 2 + 1) + n_illum * ny * px)
+        fast_l = px // 32 if (px == py and px in (128, 256, 512, 1024)) else 0
         if batch is None:
             batch = max(1, min(self.nplanes, _BATCH_BYTES // per_plane))
+            if fast_l:   # kernel B packs 8 warps x (32/L) lines of planes per CTA
+                q = 8 * (32 // fast_l)
+                batch = min(self.nplanes, max(q, (batch // q) * q))
         self.batch = int(batch)
         arr = (_lib.PfPlane * self.nplanes)()
         for i, p in enumerate(planes):
