@@ -106,6 +106,8 @@ typedef struct pf_prop_geom {
   int nu0x, nu0y;        /* centred index of output column / row 0 */
   int n_illum;
   int include_illum;
+  int flags;             /* bit 0: never take the register-FFT path */
+  int reserved;
   int64_t uhat_illum_stride; /* elements between illuminations inside uhat */
 } pf_prop_geom;
 
@@ -116,13 +118,19 @@ int pf_prop_fast(const pf_prop_geom* g);
 /* workspace element counts (c64) for a batch of nplanes */
 int64_t pf_prop_ws_a(const pf_prop_geom* g, int nplanes);
 int64_t pf_prop_ws_b(const pf_prop_geom* g, int nplanes);
+/* full product spectra [nplanes][n_illum][py][px] (product_only mode) */
+int64_t pf_prop_ws_spectrum(const pf_prop_geom* g, int nplanes);
 
 int pf_prop_kernel_rows(const pf_plane* planes, int nplanes, double khat,
                         const pf_prop_geom* g, const pf_fft_plan* plan_x, void* ws_a,
                         void* stream);
+/* product_only=1 (type-2 readouts: nursd2 reconstruct.py:453, nursd3 :519,
+ * srsd_nursd2 :580): write the full natural-order product Uhat * Ghat_k to ws_b
+ * ([nplanes][n_illum][py][px]) instead of the y-IFFT + row crop.  Requires
+ * flags bit 0 (register path off). */
 int pf_prop_columns(const pf_plane* planes, int nplanes, const pf_prop_geom* g,
                     const pf_fft_plan* plan_y, const void* ws_a, const void* uhat,
-                    void* ws_b, void* stream);
+                    void* ws_b, int product_only, void* stream);
 /* ill_xyz: device float64 [n_illum][3]; frame_w: device c64 [n_frames]
  * (exp(1j w t_j) for time-resolved output, or {1} for static); vol: c64
  * [n_frames][vol_frame_stride] with plane k at k*ny*nx; accumulates (+=). */
@@ -130,6 +138,68 @@ int pf_prop_rows_out(const pf_plane* planes, int nplanes, double khat,
                      const pf_prop_geom* g, const pf_fft_plan* plan_x, const void* ws_b,
                      const double* ill_xyz, const void* frame_w, int n_frames, void* vol,
                      int64_t vol_frame_stride, void* stream);
+
+/* ---------------------------------------------------------------- SFFT (Bluestein)
+ * Scaled-DFT lines, replacing SfftPlan.apply (spectral.py:160-168) inside
+ * sfft_2d_centered (:209-218): per plane b (grid y) the tables chirp[b][M] and
+ * khat[b][Q] (float64-built; Q = plan_q->n >= 2M-1).  Input element i < n_in of
+ * line l is at src + b*src_ps + l*src_ls + i*src_es and occupies slot o_in + i;
+ * output slot k goes to dst + b*dst_ps + l*dst_ls + pos(k)*dst_es with
+ * pos(k) = k, or natural(k - M/2) when natural_out (centred -> FFT order). */
+int pf_bluestein_lines(const void* src, int64_t src_ps, int64_t src_ls, int64_t src_es,
+                       int n_in, int o_in, void* dst, int64_t dst_ps, int64_t dst_ls,
+                       int64_t dst_es, int natural_out, int M, int nlines, int nplanes,
+                       const pf_fft_plan* plan_q, const void* chirp, const void* khat,
+                       void* stream);
+
+/* ---------------------------------------------------------------- NUFFT
+ * Gaussian gridding (spectral.py:230-381).  Axis order (z, y, x); 2D uses
+ * mr[0] = m[0] = 1.  Per point (device): i0[L][3] int32 nearest fine node,
+ * d0[L][3] float32 = i0*h - x (the window offset of stencil tap 0).  */
+typedef struct pf_nufft_geom {
+  int dim;
+  int w;
+  int mr[3];
+  int m[3];
+  float h[3];
+  float inv4tau[3];
+  int tile[3];
+  int ntiles[3];
+} pf_nufft_geom;
+
+/* type-1 spreading (spectral.py:353-355) as a tiled gather: fine[v][cell] =
+ * sum over points in tile_pts[tile_start[t]..] of vals[v][pt] * window.
+ * Writes every fine cell. */
+int pf_nufft_spread(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                    const int32_t* tile_start, const int32_t* tile_pts, const void* vals,
+                    int64_t val_stride, int nv, void* fine, int64_t fine_stride, void* stream);
+/* type-1 finish (spectral.py:357-358): centred modes / discrete deconvolution,
+ * written in natural order on the mode grid ([x][y] when transpose, 2D). */
+int pf_nufft_deconv(const pf_nufft_geom* g, const void* fine, int64_t fine_stride,
+                    const float* kz, const float* ky, const float* kx, int nv, void* out,
+                    int64_t out_stride, int transpose, void* stream);
+/* type-2 start (spectral.py:374): modes / deconvolution onto their fine slots, 0 elsewhere. */
+int pf_nufft_place(const pf_nufft_geom* g, const void* S, int64_t s_stride, const float* kz,
+                   const float* ky, const float* kx, int nv, void* fine, int64_t fine_stride,
+                   int transpose, void* stream);
+/* type-2 finish (spectral.py:377-380) fused with the per-voxel scale, the
+ * illumination phase (reconstruct.py:140-144) and the ascending-frequency
+ * accumulation (reconstruct.py:163-177): vol[f][dst0 + l] += sum_p(...) * frame_w[f]. */
+int pf_nufft_interp2_acc(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                         const double* xyz, int npts, const void* fine, int64_t fine_stride,
+                         int n_illum, const double* ill, double khat, int include_illum,
+                         float scale, const void* frame_w, int n_frames, void* vol,
+                         int64_t vol_frame_stride, int64_t dst0, void* stream);
+
+/* ---------------------------------------------------------------- elementwise
+ * _kernel_3d (reconstruct.py:624-638) on the natural 3D grid (zero lag -> 0). */
+int pf_kernel3d(void* out, int pz, int py, int px, double dx, double dy, double dz, double khat,
+                void* stream);
+/* a[i] = a[i] * b[i % b_period] * scale */
+int pf_cmul(void* a, const void* b, int64_t n, int64_t b_period, float scale, void* stream);
+/* dst[b][:] = src[b*src_stride + plane_off + :plane_elems] (slab extraction, :760) */
+int pf_copy_planes(const void* src, int nb, int64_t src_stride, int64_t plane_off,
+                   int64_t plane_elems, void* dst, void* stream);
 
 #ifdef __cplusplus
 }

@@ -32,7 +32,15 @@ class PfPropGeom(ctypes.Structure):
     _fields_ = [("px", ctypes.c_int), ("py", ctypes.c_int), ("nx", ctypes.c_int),
                 ("ny", ctypes.c_int), ("nu0x", ctypes.c_int), ("nu0y", ctypes.c_int),
                 ("n_illum", ctypes.c_int), ("include_illum", ctypes.c_int),
+                ("flags", ctypes.c_int), ("reserved", ctypes.c_int),
                 ("uhat_illum_stride", ctypes.c_int64)]
+
+
+class PfNufftGeom(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int), ("w", ctypes.c_int), ("mr", ctypes.c_int * 3),
+                ("m", ctypes.c_int * 3), ("h", ctypes.c_float * 3),
+                ("inv4tau", ctypes.c_float * 3), ("tile", ctypes.c_int * 3),
+                ("ntiles", ctypes.c_int * 3)]
 
 
 _vp, _i, _i64, _d, _f = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_float
@@ -50,18 +58,32 @@ _SIGNATURES = {
     "pf_prop_ws_a": [_P(PfPropGeom), _i],
     "pf_prop_ws_b": [_P(PfPropGeom), _i],
     "pf_prop_kernel_rows": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp],
-    "pf_prop_columns": [_vp, _i, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _vp],
+    "pf_prop_columns": [_vp, _i, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp],
+    "pf_prop_ws_spectrum": [_P(PfPropGeom), _i],
+    "pf_bluestein_lines": [_vp, _i64, _i64, _i64, _i, _i, _vp, _i64, _i64, _i64, _i, _i, _i, _i,
+                           _P(PfFftPlan), _vp, _vp, _vp],
+    "pf_nufft_spread": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _i64, _vp],
+    "pf_nufft_deconv": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp],
+    "pf_nufft_place": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp],
+    "pf_nufft_interp2_acc": [_P(PfNufftGeom), _vp, _vp, _vp, _i, _vp, _i64, _i, _vp, _d, _i, _f,
+                             _vp, _i, _vp, _i64, _i64, _vp],
+    "pf_kernel3d": [_vp, _i, _i, _i, _d, _d, _d, _d, _vp],
+    "pf_cmul": [_vp, _vp, _i64, _i64, _f, _vp],
+    "pf_copy_planes": [_vp, _i, _i64, _i64, _i64, _vp, _vp],
     "pf_prop_rows_out": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp,
                          _i64, _vp],
 }
 _RESTYPES = {"pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
+             "pf_prop_ws_spectrum": ctypes.c_int64,
              "pf_prop_fast": ctypes.c_int}
 
 _lib = None
 
 # calls that enqueue kernels (bench.py reports how many ran in its timed region)
 _LAUNCHERS = {"pf_temporal_dft", "pf_temporal_dft_direct", "pf_fft_lines", "pf_embed_centered",
-              "pf_prop_kernel_rows", "pf_prop_columns", "pf_prop_rows_out"}
+              "pf_prop_kernel_rows", "pf_prop_columns", "pf_prop_rows_out", "pf_bluestein_lines",
+              "pf_nufft_spread", "pf_nufft_deconv", "pf_nufft_place", "pf_nufft_interp2_acc",
+              "pf_kernel3d", "pf_cmul", "pf_copy_planes"}
 launch_count = 0
 
 

@@ -1,10 +1,612 @@
-"""SRSD / NURSD family on the GPU (filled in next)."""
+"""GPU drop-ins for srsd, nursd1, nursd2, nursd3, srsd_nursd2, nursd3d (reference reconstruct.py).
+
+Host code computes sizes exactly as the reference does (the pad rules decide the
+result wherever the relay or the voxels sit off the lattice: SURVEY F2/F3) and
+drives the ``libpfgpu`` kernels: Bluestein lines (srsd), NUFFT type 1
+(nursd1/3, nursd3d stage 1), the propagation kernels A/B/C, and the type-2
+readout (product -> place -> inverse FFT -> interpolate+accumulate).
+"""
 
 from __future__ import annotations
 
+import ctypes
+import math
 
-def _todo(*a, **k):
-    raise NotImplementedError("not yet ported to the GPU engine")
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _lib
+from . import nufft as nu
+from ._fastlen import next_fast_len
+from .core import (SPEED_OF_LIGHT, ReconstructionVolume, _require, illumination_coordinates)
+from .phasor import device_coefficients
+from .reconstruct import (PlaneSpec, Propagator, _check_depths, _check_times, _close,
+                          _exact_pad, _frame_weights, _ill_tensor, _kind, _nonplanar_relay,
+                          _pad_size, _planar_relay, _uniform_relay, _volume, rsd)
+
+C = SPEED_OF_LIGHT
+_BATCH_BYTES = 96 << 20
 
 
-srsd = nursd1 = nursd2 = nursd3 = nursd3d = srsd_nursd2 = rsd3d = _todo
+def _center_nu0(n: int) -> int:
+    return -(n // 2)
+
+
+# ---------------------------------------------------------------------------
+# scaled-FFT tables (reference spectral.py:143-158, cached like :171-180)
+# ---------------------------------------------------------------------------
+
+_SFFT_TABLES: dict = {}
+
+
+def _sfft_tables(m: int, alpha: float, offset: int, q: int):
+    key = (m, float(alpha), offset, q)
+    t = _SFFT_TABLES.get(key)
+    if t is None:
+        n = np.arange(m, dtype=np.float64) - offset
+        chirp = np.exp(-1j * np.pi * alpha * n * n / m)
+        lags = np.arange(1 - m, m)
+        kern = np.zeros(q, dtype=np.complex128)
+        kern[lags % q] = np.exp(1j * np.pi * alpha * lags * lags / m)
+        t = (chirp.astype(np.complex64), np.fft.fft(kern).astype(np.complex64))
+        _SFFT_TABLES[key] = t
+    return t
+
+
+class _ScaledTables:
+    """Per-plane chirps / kernel spectra for both axes, on the device."""
+
+    def __init__(self, mx, my, alphas, betas, device):
+        self.qx = next_fast_len(max(1, 2 * mx - 1))
+        self.qy = next_fast_len(max(1, 2 * my - 1))
+        cx, kx, cy, ky = [], [], [], []
+        for a, b in zip(alphas, betas):
+            c, k = _sfft_tables(mx, a, mx // 2, self.qx)
+            cx.append(c)
+            kx.append(k)
+            c, k = _sfft_tables(my, b, my // 2, self.qy)
+            cy.append(c)
+            ky.append(k)
+        t = lambda xs: torch.from_numpy(np.ascontiguousarray(np.stack(xs))).to(device)  # noqa: E731
+        self.chirp_x, self.khat_x = t(cx), t(kx)
+        self.chirp_y, self.khat_y = t(cy), t(ky)
+        self.plan_qx = dev.fft_plan(self.qx, device)
+        self.plan_qy = dev.fft_plan(self.qy, device)
+
+
+def _scaled_spectra(coeff_fp: torch.Tensor, ny: int, nx: int, py: int, px: int,
+                    tabs: _ScaledTables, t0: int, nb: int, xbuf: torch.Tensor,
+                    out: torch.Tensor, out_plane_stride: int, transposed: bool, stream=None):
+    """sfft_2d_centered(pad_embed(u), a_k, b_k) for planes t0..t0+nb of the tables.
+
+    x pass over the ny embedded relay rows (zero rows transform to zero), written
+    with natural column order; y pass over all px columns into natural-order
+    spectra (reference spectral.py:196-218, reconstruct.py:318-320).
+    """
+    s = dev.stream_ptr(stream)
+    csz = 8
+    _lib.call("pf_bluestein_lines", dev.ptr(coeff_fp), 0, nx, 1, nx, px // 2 - nx // 2,
+              dev.ptr(xbuf), ny * px, px, 1, 1, px, ny, nb, tabs.plan_qx.ref,
+              dev.ptr(tabs.chirp_x) + csz * t0 * px, dev.ptr(tabs.khat_x) + csz * t0 * tabs.qx, s)
+    if transposed:   # out[b][col][row]
+        _lib.call("pf_bluestein_lines", dev.ptr(xbuf), ny * px, 1, px, ny, py // 2 - ny // 2,
+                  dev.ptr(out), out_plane_stride, py, 1, 1, py, px, nb, tabs.plan_qy.ref,
+                  dev.ptr(tabs.chirp_y) + csz * t0 * py, dev.ptr(tabs.khat_y) + csz * t0 * tabs.qy,
+                  s)
+    else:            # out[b][row][col]
+        _lib.call("pf_bluestein_lines", dev.ptr(xbuf), ny * px, 1, px, ny, py // 2 - ny // 2,
+                  dev.ptr(out), out_plane_stride, 1, px, 1, py, px, nb, tabs.plan_qy.ref,
+                  dev.ptr(tabs.chirp_y) + csz * t0 * py, dev.ptr(tabs.khat_y) + csz * t0 * tabs.qy,
+                  s)
+
+
+# ---------------------------------------------------------------------------
+# srsd: uniform relay -> depth-scaled frustum (reconstruct.py:276-327)
+# ---------------------------------------------------------------------------
+
+
+class SrsdEngine:
+    def __init__(self, slices, grid, include_illumination=True, times=None, device=None,
+                 plane_range=None):
+        _require(_kind(grid) == "frustum", "srsd reconstructs onto a frustum grid")
+        relay = _uniform_relay(slices)
+        g = relay.grid
+        b = grid.base
+        _require(b.nx == g.nx and b.ny == g.ny and _close(b.dx, g.dx) and _close(b.dy, g.dy)
+                 and _close(b.x0, g.x0) and _close(b.y0, g.y0),
+                 "the frustum base must coincide with the relay lattice")
+        _check_depths(grid.zs, g.z)
+        self.times = _check_times(times)
+        self.device = device or dev.require_cuda()
+        # P = next_fast_len(2N): the SRSD result depends on it
+        px, py = next_fast_len(2 * g.nx), next_fast_len(2 * g.ny)
+        self.px, self.py, self.g, self.grid = px, py, g, grid
+        self.freqs = np.asarray(slices.frequencies, dtype=np.float64)
+        self.n_illum = int(slices.illuminations.count)
+        k_lo, k_hi = plane_range or (0, grid.n_planes)
+        self.k_lo, self.k_hi = k_lo, k_hi
+        ks = list(range(k_lo, k_hi))
+        cx, cy = g.center()
+        I = self.n_illum
+        planes = []
+        tmp = Propagator(self.device, px, py, g.nx, g.ny, 0, 0, I, include_illumination,
+                         [PlaneSpec(1, 1, 1, 0, 1, 0, 1, 1)], py * px, batch=1)
+        self.transposed = tmp.transposed
+        per_plane = 8 * (2 * I * py * px + I * g.ny * px)
+        batch = max(1, min(len(ks), _BATCH_BYTES // per_plane))
+        if self.transposed:
+            q = 8 * (32 // (px // 32))
+            batch = min(len(ks), max(q, (batch // q) * q))
+        self.batch = batch
+        for i, k in enumerate(ks):
+            al, be = float(grid.alphas[k]), float(grid.betas[k])
+            pxk, pyk = g.dx / al, g.dy / be
+            planes.append(PlaneSpec(float(grid.zs[k]) - g.z, pxk, pyk,
+                                    cx - (g.nx // 2) * pxk, pxk, cy - (g.ny // 2) * pyk, pyk,
+                                    float(grid.zs[k]), (i % batch) * I * py * px, i))
+        self.prop = Propagator(self.device, px, py, g.nx, g.ny, _center_nu0(g.nx),
+                               _center_nu0(g.ny), I, include_illumination, planes, py * px,
+                               batch=batch)
+        self.tabs = _ScaledTables(px, py, [grid.alphas[k] for k in ks],
+                                  [grid.betas[k] for k in ks], self.device)
+        self.uhat = torch.empty((batch * I * py * px,), dtype=torch.complex64, device=self.device)
+        self.xbuf = torch.empty((batch * g.ny * px,), dtype=torch.complex64, device=self.device)
+        self.ill = _ill_tensor(slices, self.device)
+        self.frame_w = _frame_weights(self.freqs, self.times, self.device)
+        self.n_frames = 1 if self.times is None else self.times.size
+        self.n_voxels = len(ks) * g.nx * g.ny
+
+    def run(self, coeff: torch.Tensor, vol=None, stream=None):
+        if vol is None:
+            vol = torch.zeros((self.n_frames, self.n_voxels), dtype=torch.complex64,
+                              device=self.device)
+        else:
+            vol.zero_()
+        g, I, px, py = self.g, self.n_illum, self.px, self.py
+        D = g.nx * g.ny
+        nplanes = self.k_hi - self.k_lo
+        for b0 in range(0, nplanes, self.batch):
+            b1 = min(nplanes, b0 + self.batch)
+            nb = b1 - b0
+            for fi in range(self.freqs.size):
+                for p in range(I):
+                    src = coeff[fi, p]
+                    out = self.uhat[p * py * px:]
+                    _scaled_spectra(src, g.ny, g.nx, py, px, self.tabs, b0, nb, self.xbuf, out,
+                                    I * py * px, self.transposed, stream)
+                khat = float(self.freqs[fi]) / C
+                self.prop.run_frequency(dev.ptr(self.uhat), khat, dev.ptr(self.ill),
+                                        dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
+                                        self.n_frames, vol, self.n_voxels, plane_lo=b0,
+                                        plane_hi=b1, stream=stream)
+        return vol
+
+
+def srsd(slices, grid, times=None, threads: int = 1, include_illumination: bool = True):
+    """Scaled propagation onto a depth-widening frustum (reconstruct.py:276-327)."""
+    eng = SrsdEngine(slices, grid, include_illumination, times)
+    return _volume(grid, eng.run(device_coefficients(slices)), eng.times)
+
+
+# ---------------------------------------------------------------------------
+# nursd1: scattered planar relay -> cuboid (reconstruct.py:335-385)
+# ---------------------------------------------------------------------------
+
+
+class _UhatPropEngine:
+    """Shared tail of nursd1 / nursd3d: per-frequency relay spectra -> propagate."""
+
+    def _setup_prop(self, px, py, vg, z_src, include_illumination, k_range, flags=0):
+        zs = vg.z_coords()
+        k_lo, k_hi = k_range
+        planes = [PlaneSpec(zs[k] - z_src, vg.dx, vg.dy, vg.x0, vg.dx, vg.y0, vg.dy, zs[k], 0,
+                            k - k_lo) for k in range(k_lo, k_hi)]
+        self.prop = Propagator(self.device, px, py, vg.nx, vg.ny, _center_nu0(vg.nx),
+                               _center_nu0(vg.ny), self.n_illum, include_illumination, planes,
+                               py * px)
+        self.n_voxels = (k_hi - k_lo) * vg.nx * vg.ny
+
+    def _propagate(self, uhat, vol, stream):
+        per_f = self.n_illum * self.py * self.px
+        for b0 in range(0, self.prop.nplanes, self.prop.batch):
+            b1 = min(self.prop.nplanes, b0 + self.prop.batch)
+            for fi in range(self.freqs.size):
+                khat = float(self.freqs[fi]) / C
+                self.prop.run_frequency(dev.ptr(uhat) + 8 * fi * per_f, khat, dev.ptr(self.ill),
+                                        dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
+                                        self.n_frames, vol, self.n_voxels, plane_lo=b0,
+                                        plane_hi=b1, stream=stream)
+        return vol
+
+
+class Nursd1Engine(_UhatPropEngine):
+    def __init__(self, slices, grid, eps=1e-6, include_illumination=True, times=None,
+                 device=None, plane_range=None):
+        _require(_kind(grid) == "cuboid", "nursd1 reconstructs onto a cuboid grid")
+        relay = _planar_relay(slices)
+        vg = grid.grid
+        zs = vg.z_coords()
+        _check_depths(zs, relay.z)
+        self.times = _check_times(times)
+        self.device = device or dev.require_cuda()
+        cx = vg.x0 + (vg.nx // 2) * vg.dx
+        cy = vg.y0 + (vg.ny // 2) * vg.dy
+        rel = np.asarray(relay.points.points)
+        nu_rx = (rel[:, 0] - cx) / vg.dx
+        nu_ry = (rel[:, 1] - cy) / vg.dy
+        lo_x, hi_x = -(vg.nx // 2), vg.nx - vg.nx // 2 - 1
+        lo_y, hi_y = -(vg.ny // 2), vg.ny - vg.ny // 2 - 1
+        lx = max(hi_x - nu_rx.min(), nu_rx.max() - lo_x)
+        ly = max(hi_y - nu_ry.min(), nu_ry.max() - lo_y)
+        on_lattice = (np.abs(nu_rx - np.round(nu_rx)).max() < 1e-9
+                      and np.abs(nu_ry - np.round(nu_ry)).max() < 1e-9)
+        # off-lattice points make the result depend on P: keep the reference rule
+        # (SURVEY F3); lattice points are P-independent (F4), so pick a fast pad
+        pad = _exact_pad if on_lattice else _pad_size
+        px = pad(lx, max(abs(nu_rx).max(), vg.nx // 2), vg.nx)
+        py = pad(ly, max(abs(nu_ry).max(), vg.ny // 2), vg.ny)
+        self.px, self.py = px, py
+        torus = np.column_stack([2.0 * np.pi * nu_rx / px, 2.0 * np.pi * nu_ry / py])
+        self.plan = nu.NufftPlan((py, px), eps, self.device)
+        self.pts = self.plan.points(torus)
+        self.freqs = np.asarray(slices.frequencies, dtype=np.float64)
+        self.n_illum = int(slices.illuminations.count)
+        self._setup_prop(px, py, vg, relay.z, include_illumination,
+                         plane_range or (0, vg.nz))
+        F, I = self.freqs.size, self.n_illum
+        self.uhat = torch.empty((F * I * py * px,), dtype=torch.complex64, device=self.device)
+        self.fine = torch.empty((F * I, self.plan.fine_elems), dtype=torch.complex64,
+                                device=self.device)
+        self.ill = _ill_tensor(slices, self.device)
+        self.frame_w = _frame_weights(self.freqs, self.times, self.device)
+        self.n_frames = 1 if self.times is None else self.times.size
+        self.grid = grid
+
+    def relay_spectra(self, coeff, stream=None):
+        F, I = self.freqs.size, self.n_illum
+        nu.type1(self.plan, self.pts, coeff, F * I, coeff.shape[-1], self.uhat,
+                 self.py * self.px, self.fine, self.prop.transposed, stream)
+        return self.uhat
+
+    def run(self, coeff, vol=None, stream=None):
+        if vol is None:
+            vol = torch.zeros((self.n_frames, self.n_voxels), dtype=torch.complex64,
+                              device=self.device)
+        else:
+            vol.zero_()
+        return self._propagate(self.relay_spectra(coeff, stream), vol, stream)
+
+
+def nursd1(slices, grid, eps: float = 1e-6, times=None, threads: int = 1,
+           include_illumination: bool = True):
+    """Scattered planar relay -> cuboid via type-1 NUFFT (reconstruct.py:335-385)."""
+    eng = Nursd1Engine(slices, grid, eps, include_illumination, times)
+    return _volume(grid, eng.run(device_coefficients(slices)), eng.times)
+
+
+# ---------------------------------------------------------------------------
+# type-2 readout family: nursd2, nursd3, srsd_nursd2 (reconstruct.py:393-586)
+# ---------------------------------------------------------------------------
+
+
+def _explicit_geo(grid, cx, cy, dx, dy, sx=1.0, sy=1.0):
+    """Per-plane fractional lattice indices (reconstruct.py:393-410)."""
+    geo, start = [], 0
+    for pl in grid.planes:
+        pts = np.asarray(pl.points.points)
+        geo.append((start, pts.shape[0], sx * (pts[:, 0] - cx) / dx, sy * (pts[:, 1] - cy) / dy,
+                    pts, float(pl.z)))
+        start += pts.shape[0]
+    return geo
+
+
+class _Type2Readout:
+    """cfft2(G_k) * Uhat -> nufft2 at the plane's voxels * scale * illumination phase."""
+
+    def __init__(self, device, slices, grid, geo, px, py, lag_dx, lag_dy, z_src, eps,
+                 include_illumination, times):
+        self.device = device
+        self.geo = geo
+        self.px, self.py = px, py
+        self.freqs = np.asarray(slices.frequencies, dtype=np.float64)
+        self.n_illum = I = int(slices.illuminations.count)
+        self.times = times
+        self.n_frames = 1 if times is None else times.size
+        self.count = grid.count
+        self.include = bool(include_illumination)
+        planes = [PlaneSpec(z - z_src, lag_dx, lag_dy, 0, 1, 0, 1, z, 0, i)
+                  for i, (*_, z) in enumerate(geo)]
+        self.prop = Propagator(device, px, py, px, py, 0, 0, I, include_illumination, planes,
+                               py * px, batch=1)
+        self.prop.geom.flags = 1      # register path off: generic product-only columns
+        self.plan = nu.NufftPlan((py, px), eps, device)
+        self.points = []
+        for (start, cnt, nux, nuy, pts, z) in geo:
+            tor = np.column_stack([2.0 * np.pi * nux / px, 2.0 * np.pi * nuy / py])
+            xyz = np.column_stack([pts[:, 0], pts[:, 1], np.full(cnt, z)])
+            self.points.append((start, cnt, self.plan.points(tor),
+                                torch.from_numpy(np.ascontiguousarray(xyz)).to(device)))
+        self.spec = torch.empty((I * py * px,), dtype=torch.complex64, device=device)
+        self.fine = torch.empty((I, self.plan.fine_elems), dtype=torch.complex64, device=device)
+        self.ill = _ill_tensor(slices, device)
+        self.frame_w = _frame_weights(self.freqs, times, device)
+
+    def run(self, uhat_of, vol, stream=None):
+        s = dev.stream_ptr(stream)
+        I, py, px = self.n_illum, self.py, self.px
+        gref = ctypes.byref(self.prop.geom)
+        base = dev.ptr(self.prop.planes_dev)
+        for fi in range(self.freqs.size):
+            khat = float(self.freqs[fi]) / C
+            uhat = uhat_of(fi)
+            fw = dev.ptr(self.frame_w) + 8 * fi * self.n_frames
+            for k, (start, cnt, pts, xyz) in enumerate(self.points):
+                pp = base + k * self.prop.plane_size
+                _lib.call("pf_prop_kernel_rows", pp, 1, khat, gref, self.prop.plan_x.ref,
+                          dev.ptr(self.prop.ws_a), s)
+                _lib.call("pf_prop_columns", pp, 1, gref, self.prop.plan_y.ref,
+                          dev.ptr(self.prop.ws_a), dev.ptr(uhat), dev.ptr(self.spec), 1, s)
+                nu.place_and_inverse(self.plan, self.spec, I, py * px, self.fine, stream)
+                _lib.call("pf_nufft_interp2_acc", self.plan.gref, dev.ptr(pts.i0),
+                          dev.ptr(pts.d0), dev.ptr(xyz), cnt, dev.ptr(self.fine),
+                          self.plan.fine_elems, I, dev.ptr(self.ill), khat, int(self.include),
+                          1.0 / (px * py), fw, self.n_frames, dev.ptr(vol), self.count, start, s)
+        return vol
+
+
+def _readout_setup(slices, grid, times):
+    _require(_kind(grid) == "explicit", "this algorithm reconstructs onto explicit voxels")
+    return dev.require_cuda(), _check_times(times)
+
+
+def nursd2(slices, grid, eps: float = 1e-6, times=None, threads: int = 1,
+           include_illumination: bool = True):
+    """Uniform relay -> explicit voxels (reconstruct.py:413-459)."""
+    _require(_kind(grid) == "explicit", "nursd2 reconstructs onto explicit voxels")
+    relay = _uniform_relay(slices)
+    g = relay.grid
+    cx, cy = g.center()
+    geo = _explicit_geo(grid, cx, cy, g.dx, g.dy)
+    _check_depths(np.asarray([t[-1] for t in geo]), g.z)
+    times = _check_times(times)
+    device = dev.require_cuda()
+    jx_lo, jx_hi = -(g.nx // 2), g.nx - g.nx // 2 - 1
+    jy_lo, jy_hi = -(g.ny // 2), g.ny - g.ny // 2 - 1
+    ax = np.concatenate([t[2] for t in geo])
+    ay = np.concatenate([t[3] for t in geo])
+    px = _pad_size(max(ax.max() - jx_lo, jx_hi - ax.min()), max(abs(ax).max(), g.nx // 2), g.nx)
+    py = _pad_size(max(ay.max() - jy_lo, jy_hi - ay.min()), max(abs(ay).max(), g.ny // 2), g.ny)
+    ro = _Type2Readout(device, slices, grid, geo, px, py, g.dx, g.dy, g.z, eps,
+                       include_illumination, times)
+    coeff = device_coefficients(slices)
+    F, I = ro.freqs.size, ro.n_illum
+    uhat = torch.empty((F * I * py * px,), dtype=torch.complex64, device=device)
+    _lib.call("pf_embed_centered", dev.ptr(coeff), F * I, g.ny, g.nx, g.ny * g.nx, dev.ptr(uhat),
+              py, px, 0, dev.stream_ptr())
+    dev.fft2_natural(uhat, py, px, F * I, -1)
+    vol = torch.zeros((ro.n_frames, grid.count), dtype=torch.complex64, device=device)
+    ro.run(lambda fi: uhat[fi * I * py * px:], vol)
+    return _volume(grid, vol, times)
+
+
+def nursd3(slices, grid, eps: float = 1e-6, lattice_pitch: float | None = None, times=None,
+           threads: int = 1, include_illumination: bool = True):
+    """Scattered planar relay -> explicit voxels through a virtual lattice (reconstruct.py:467-525)."""
+    _require(_kind(grid) == "explicit", "nursd3 reconstructs onto explicit voxels")
+    relay = _planar_relay(slices)
+    pitch = (float(lattice_pitch) if lattice_pitch is not None
+             else slices.shortest_wavelength / 2.0)
+    _require(pitch > 0, "lattice pitch must be > 0")
+    rel = np.asarray(relay.points.points)
+    tgt = np.vstack([np.asarray(p.points.points) for p in grid.planes])
+    lo = np.minimum(rel.min(axis=0), tgt.min(axis=0))
+    hi = np.maximum(rel.max(axis=0), tgt.max(axis=0))
+    anchor = rel[0] + np.round(((lo + hi) / 2.0 - rel[0]) / pitch) * pitch
+    cx, cy = float(anchor[0]), float(anchor[1])
+    nu_rx = (rel[:, 0] - cx) / pitch
+    nu_ry = (rel[:, 1] - cy) / pitch
+    geo = _explicit_geo(grid, cx, cy, pitch, pitch)
+    _check_depths(np.asarray([t[-1] for t in geo]), relay.z)
+    times = _check_times(times)
+    device = dev.require_cuda()
+    ax = np.concatenate([t[2] for t in geo])
+    ay = np.concatenate([t[3] for t in geo])
+    px = _pad_size(max(ax.max() - nu_rx.min(), nu_rx.max() - ax.min()),
+                   max(abs(ax).max(), abs(nu_rx).max()), 1)
+    py = _pad_size(max(ay.max() - nu_ry.min(), nu_ry.max() - ay.min()),
+                   max(abs(ay).max(), abs(nu_ry).max()), 1)
+    ro = _Type2Readout(device, slices, grid, geo, px, py, pitch, pitch, float(relay.z), eps,
+                       include_illumination, times)
+    coeff = device_coefficients(slices)
+    F, I = ro.freqs.size, ro.n_illum
+    plan = nu.NufftPlan((py, px), eps, device)
+    pts = plan.points(np.column_stack([2.0 * np.pi * nu_rx / px, 2.0 * np.pi * nu_ry / py]))
+    uhat = torch.empty((F * I * py * px,), dtype=torch.complex64, device=device)
+    nu.type1(plan, pts, coeff, F * I, coeff.shape[-1], uhat, py * px)
+    vol = torch.zeros((ro.n_frames, grid.count), dtype=torch.complex64, device=device)
+    ro.run(lambda fi: uhat[fi * I * py * px:], vol)
+    return _volume(grid, vol, times)
+
+
+def srsd_nursd2(slices, grid, alpha: float, beta: float | None = None, eps: float = 1e-6,
+                times=None, threads: int = 1, include_illumination: bool = True):
+    """Uniform relay -> explicit voxels through one scaled transform (reconstruct.py:533-586)."""
+    _require(_kind(grid) == "explicit", "srsd-nursd2 reconstructs onto explicit voxels")
+    if beta is None:
+        beta = alpha
+    _require(0 < alpha <= 1 and 0 < beta <= 1, "scale factors must lie in (0, 1]")
+    relay = _uniform_relay(slices)
+    g = relay.grid
+    cx, cy = g.center()
+    geo = _explicit_geo(grid, cx, cy, g.dx, g.dy, alpha, beta)
+    _check_depths(np.asarray([t[-1] for t in geo]), g.z)
+    times = _check_times(times)
+    device = dev.require_cuda()
+    jx_lo, jx_hi = -(g.nx // 2), g.nx - g.nx // 2 - 1
+    jy_lo, jy_hi = -(g.ny // 2), g.ny - g.ny // 2 - 1
+    ax = np.concatenate([t[2] for t in geo])
+    ay = np.concatenate([t[3] for t in geo])
+    px = _pad_size(max(ax.max() - alpha * jx_lo, alpha * jx_hi - ax.min()),
+                   max(abs(ax).max(), g.nx // 2), g.nx)
+    py = _pad_size(max(ay.max() - beta * jy_lo, beta * jy_hi - ay.min()),
+                   max(abs(ay).max(), g.ny // 2), g.ny)
+    ro = _Type2Readout(device, slices, grid, geo, px, py, g.dx / alpha, g.dy / beta, g.z, eps,
+                       include_illumination, times)
+    coeff = device_coefficients(slices)
+    F, I = ro.freqs.size, ro.n_illum
+    tabs = _ScaledTables(px, py, [alpha], [beta], device)
+    uhat = torch.empty((F * I * py * px,), dtype=torch.complex64, device=device)
+    xbuf = torch.empty((g.ny * px,), dtype=torch.complex64, device=device)
+    for fi in range(F):
+        for p in range(I):
+            _scaled_spectra(coeff[fi, p], g.ny, g.nx, py, px, tabs, 0, 1, xbuf,
+                            uhat[(fi * I + p) * py * px:], py * px, False)
+    vol = torch.zeros((ro.n_frames, grid.count), dtype=torch.complex64, device=device)
+    ro.run(lambda fi: uhat[fi * I * py * px:], vol)
+    return _volume(grid, vol, times)
+
+
+# ---------------------------------------------------------------------------
+# nursd3d: scattered 3D relay -> cuboid (reconstruct.py:594-765)
+# ---------------------------------------------------------------------------
+
+
+class _FlatSlices:
+    """A 3D relay whose points share one z viewed as a planar relay (reconstruct.py:735-740)."""
+
+    def __init__(self, slices, rel):
+        from .core import NonUniformPlanarRelay, PointList
+        self.frequencies = slices.frequencies
+        self.illuminations = slices.illuminations
+        self.relay = NonUniformPlanarRelay(PointList(rel[:, :2]), float(rel[0, 2]))
+        self._src = slices
+        self.n_freq = int(np.asarray(slices.frequencies).size)
+
+    @property
+    def coefficients(self):
+        return self._src.coefficients
+
+    @property
+    def device_coefficients(self):
+        return device_coefficients(self._src)
+
+
+def _lattice_3d(slices, grid, z_pitch):
+    """Virtual-lattice geometry shared by the non-planar algorithms (reconstruct.py:594-621)."""
+    relay = _nonplanar_relay(slices)
+    vg = grid.grid
+    rel = np.asarray(relay.points.points)
+    dz3 = float(z_pitch) if z_pitch else slices.shortest_wavelength / 2.0
+    _require(dz3 > 0, "depth lattice pitch must be > 0")
+    z_min = float(rel[:, 2].min())
+    z_ext = float(rel[:, 2].max()) - z_min
+    nz3 = max(1, math.ceil(z_ext / dz3) + 1)
+    pz = next_fast_len(2 * nz3 + 2)
+    z0 = z_min + nz3 * dz3
+    zs = vg.z_coords()
+    _require(bool((zs > z0).all()),
+             "every voxel plane must lie beyond the relay surface's far face "
+             f"(z > {z0:.6g})")
+    cx = vg.x0 + (vg.nx // 2) * vg.dx
+    cy = vg.y0 + (vg.ny // 2) * vg.dy
+    nu_rx = (rel[:, 0] - cx) / vg.dx
+    nu_ry = (rel[:, 1] - cy) / vg.dy
+    lo_x, hi_x = -(vg.nx // 2), vg.nx - vg.nx // 2 - 1
+    lo_y, hi_y = -(vg.ny // 2), vg.ny - vg.ny // 2 - 1
+    lx = max(hi_x - nu_rx.min(), nu_rx.max() - lo_x)
+    ly = max(hi_y - nu_ry.min(), nu_ry.max() - lo_y)
+    px = _pad_size(lx, max(abs(nu_rx).max(), vg.nx // 2), vg.nx)
+    py = _pad_size(ly, max(abs(nu_ry).max(), vg.ny // 2), vg.ny)
+    slab = pz // 2 + (nz3 - nz3 // 2)
+    return rel, dz3, z_min, nz3, pz, z0, nu_rx, nu_ry, px, py, slab
+
+
+class Nursd3dEngine(_UhatPropEngine):
+    """Stage 1: 3D type-1 NUFFT -> x cfft_n(G3) -> cifft_n -> slab -> cfft_2d; stage 2: propagate."""
+
+    def __init__(self, slices, grid, eps=1e-6, z_pitch=None, include_illumination=True,
+                 times=None, device=None, plane_range=None):
+        _require(_kind(grid) == "cuboid", "nursd3d reconstructs onto a cuboid grid")
+        (rel, dz3, z_min, nz3, pz, z0, nu_rx, nu_ry, px, py, slab) = _lattice_3d(slices, grid,
+                                                                                 z_pitch)
+        self.times = _check_times(times)
+        self.device = device or dev.require_cuda()
+        vg = grid.grid
+        self.vg, self.grid = vg, grid
+        self.px, self.py, self.pz, self.dz3, self.z0 = px, py, pz, dz3, z0
+        self.slab_nat = (slab - pz // 2) % pz
+        c_z = z_min + (nz3 // 2) * dz3
+        nu_rz = (rel[:, 2] - c_z) / dz3
+        torus = np.column_stack([2.0 * np.pi * nu_rx / px, 2.0 * np.pi * nu_ry / py,
+                                 2.0 * np.pi * nu_rz / pz])
+        self.plan = nu.NufftPlan((pz, py, px), eps, self.device)
+        self.pts = self.plan.points(torus)
+        self.freqs = np.asarray(slices.frequencies, dtype=np.float64)
+        self.n_illum = int(slices.illuminations.count)
+        self._setup_prop(px, py, vg, z0, include_illumination, plane_range or (0, vg.nz))
+        self.ill = _ill_tensor(slices, self.device)
+        self.frame_w = _frame_weights(self.freqs, self.times, self.device)
+        self.n_frames = 1 if self.times is None else self.times.size
+
+    def relay_spectra(self, coeff, stream=None):
+        F, I = self.freqs.size, self.n_illum
+        px, py, pz = self.px, self.py, self.pz
+        n3 = pz * py * px
+        s = dev.stream_ptr(stream)
+        uhat3 = torch.empty((I * n3,), dtype=torch.complex64, device=self.device)
+        g3 = torch.empty((n3,), dtype=torch.complex64, device=self.device)
+        fine = torch.empty((I, self.plan.fine_elems), dtype=torch.complex64, device=self.device)
+        out = torch.empty((F * I * py * px,), dtype=torch.complex64, device=self.device)
+        for fi in range(F):
+            nu.type1(self.plan, self.pts, coeff[fi], I, coeff.shape[-1], uhat3, n3, fine,
+                     False, stream)
+            khat = float(self.freqs[fi]) / C
+            _lib.call("pf_kernel3d", dev.ptr(g3), pz, py, px, self.vg.dx, self.vg.dy, self.dz3,
+                      khat, s)
+            dev.fftn_natural(g3, (pz, py, px), 1, -1, 1.0, stream)
+            _lib.call("pf_cmul", dev.ptr(uhat3), dev.ptr(g3), I * n3, n3, 1.0, s)
+            dev.fftn_natural(uhat3, (pz, py, px), I, +1, 1.0 / n3, stream)
+            _lib.call("pf_copy_planes", dev.ptr(uhat3), I, n3, self.slab_nat * py * px, py * px,
+                      dev.ptr(out) + 8 * fi * I * py * px, s)
+        if self.prop.transposed:
+            t = out.view(F * I, py, px).transpose(1, 2).contiguous()
+            dev.fft2_natural(t, px, py, F * I, -1, 1.0, stream)
+            return t.view(-1)
+        dev.fft2_natural(out, py, px, F * I, -1, 1.0, stream)
+        return out
+
+    def run(self, coeff, vol=None, stream=None):
+        if vol is None:
+            vol = torch.zeros((self.n_frames, self.n_voxels), dtype=torch.complex64,
+                              device=self.device)
+        else:
+            vol.zero_()
+        return self._propagate(self.relay_spectra(coeff, stream), vol, stream)
+
+
+def nursd3d(slices, grid, eps: float = 1e-6, z_pitch: float | None = None, times=None,
+            threads: int = 1, include_illumination: bool = True):
+    """Scattered 3D relay -> cuboid (reconstruct.py:722-765)."""
+    _require(_kind(grid) == "cuboid", "nursd3d reconstructs onto a cuboid grid")
+    relay = _nonplanar_relay(slices)
+    rel = np.asarray(relay.points.points)
+    if float(rel[:, 2].max() - rel[:, 2].min()) == 0.0:
+        flat = _FlatSlices(slices, rel)
+        eng = Nursd1Engine(flat, grid, eps, include_illumination, times)
+        return _volume(grid, eng.run(device_coefficients(slices)), eng.times)
+    eng = Nursd3dEngine(slices, grid, eps, z_pitch, include_illumination, times)
+    return _volume(grid, eng.run(device_coefficients(slices)), eng.times)
+
+
+def rsd3d(slices, grid, scatter: str = "trilinear", z_pitch: float | None = None, times=None,
+          threads: int = 1, include_illumination: bool = True):
+    """3D trilinear-gridding variant (reference reconstruct.py:662-719).
+
+    Out of the accelerated scope (no config names it); validated here
+    so callers get the reference's errors, then refused explicitly.
+    """
+    _require(_kind(grid) == "cuboid", "rsd3d reconstructs onto a cuboid grid")
+    _require(scatter in ("nearest", "trilinear"), "scatter must be 'nearest' or 'trilinear'")
+    _lattice_3d(slices, grid, z_pitch)
+    raise NotImplementedError("rsd3d is outside the GPU engine's scope (use nursd3d)")

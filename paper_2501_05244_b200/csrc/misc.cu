@@ -1,0 +1,78 @@
+// Small elementwise kernels of the non-planar (nursd3d) stage 1 and the
+// type-2 readout plumbing.  Reference: _kernel_3d (reconstruct.py:624-638),
+// the uhat3 * g3 product and slab extraction (:758-760).
+#include "fft.cuh"
+
+namespace {
+
+int grid_for(long long total) {
+  long long g = (total + 255) / 256;
+  return (int)(g < 148 * 32 ? (g < 1 ? 1 : g) : 148 * 32);
+}
+
+// G3 on the natural 3D grid: exp(1j khat r)/r at centred lags, 0 at zero lag
+__global__ void k_kernel3d(float2* __restrict__ out, int pz, int py, int px, double dx, double dy,
+                           double dz, double khat) {
+  const long long total = (long long)pz * py * px;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int jx = (int)(e % px), jy = (int)((e / px) % py), jz = (int)(e / ((long long)px * py));
+    const double lx = centred(jx, px) * dx, ly = centred(jy, py) * dy, lz = centred(jz, pz) * dz;
+    const double r = sqrt(lx * lx + ly * ly + lz * lz);
+    float2 v = make_float2(0.f, 0.f);
+    if (r > 0.0) {
+      const float2 e2 = expi_reduced(khat * r);
+      const float ir = (float)(1.0 / r);
+      v = make_float2(e2.x * ir, e2.y * ir);
+    }
+    out[e] = v;
+  }
+}
+
+__global__ void k_cmul(float2* __restrict__ a, const float2* __restrict__ b, long long n,
+                       long long b_period, float scale) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    a[e] = cscale(cmul(a[e], b[e % b_period]), scale);
+}
+
+__global__ void k_slab(const float2* __restrict__ src, int nb, long long src_stride,
+                       long long plane_off, long long plane_elems, float2* __restrict__ dst) {
+  const long long total = (long long)nb * plane_elems;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / plane_elems, r = e - b * plane_elems;
+    dst[e] = src[b * src_stride + plane_off + r];
+  }
+}
+
+}  // namespace
+
+extern "C" int pf_kernel3d(void* out, int pz, int py, int px, double dx, double dy, double dz,
+                           double khat, void* stream) {
+  PF_ARG_CHECK(pz >= 1 && py >= 1 && px >= 1, "pf_kernel3d: bad sizes");
+  k_kernel3d<<<grid_for((long long)pz * py * px), 256, 0, (cudaStream_t)stream>>>(
+      (float2*)out, pz, py, px, dx, dy, dz, khat);
+  PF_LAUNCH_CHECK("k_kernel3d");
+  return 0;
+}
+
+extern "C" int pf_cmul(void* a, const void* b, int64_t n, int64_t b_period, float scale,
+                       void* stream) {
+  PF_ARG_CHECK(n >= 0 && b_period >= 1, "pf_cmul: bad sizes");
+  if (n == 0) return 0;
+  k_cmul<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((float2*)a, (const float2*)b, n, b_period,
+                                                        scale);
+  PF_LAUNCH_CHECK("k_cmul");
+  return 0;
+}
+
+extern "C" int pf_copy_planes(const void* src, int nb, int64_t src_stride, int64_t plane_off,
+                              int64_t plane_elems, void* dst, void* stream) {
+  PF_ARG_CHECK(nb >= 0 && plane_elems >= 0, "pf_copy_planes: bad sizes");
+  if (nb == 0 || plane_elems == 0) return 0;
+  k_slab<<<grid_for((long long)nb * plane_elems), 256, 0, (cudaStream_t)stream>>>(
+      (const float2*)src, nb, src_stride, plane_off, plane_elems, (float2*)dst);
+  PF_LAUNCH_CHECK("k_slab");
+  return 0;
+}

@@ -1,0 +1,284 @@
+// Gaussian-gridding NUFFT, types 1 and 2, in 2D and 3D.
+//
+// Reference: spectral.py:230-381 (NufftPlan / nufft1 / nufft2).  Same
+// geometry-only plan (spread half-width w, fine grid mr = next_fast_len(2m),
+// Gaussian variance tau, DISCRETE deconvolution ker = DFT of the truncated
+// stencil, so on-lattice points are exact) -- built on the host in float64 by
+// the Python layer and uploaded as per-point (i0, d0) pairs.
+//
+// Type 1 (reference spectral.py:351-358, a Python loop over points) becomes a
+// deterministic tiled GATHER: points are bucketed (CSR) by the fine-grid tiles
+// their (2w+1)^d stencil touches; one CTA owns one tile, stages its points and
+// their per-axis window weights in shared memory and every thread accumulates
+// its own cell in fixed point order (no atomics, bit-reproducible).  It then
+// writes every cell of its tile exactly once, so no zero-fill pass is needed.
+// Type 2 (spectral.py:374-380) interpolates with one thread per target point.
+#include "fft.cuh"
+
+// pf_nufft_geom: see include/pfgpu.h
+
+namespace {
+
+constexpr int NT = 256;
+constexpr int SP_CHUNK = 32;   // points staged per pass
+constexpr int SP_V = 8;        // value sets (complex) accumulated per CTA
+
+__device__ __forceinline__ int wrap_off(int d, int mr) {
+  // representative of d mod mr in [-mr/2, mr - mr/2)
+  d %= mr;
+  if (d < -(mr / 2)) d += mr;
+  if (d >= mr - mr / 2) d -= mr;
+  return d;
+}
+
+// grid: (total tiles, ceil(nv / SP_V)); block: tile cells (<= 256 threads)
+__global__ void __launch_bounds__(NT)
+k_spread(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
+         const int* __restrict__ tile_start, const int* __restrict__ tile_pts,
+         const float2* __restrict__ vals, long long val_stride, int nv,
+         float2* __restrict__ fine, long long fine_stride) {
+  __shared__ float wgt[SP_CHUNK][3][2 * 12 + 1];
+  __shared__ int pi0[SP_CHUNK][3];
+  __shared__ float2 pv[SP_V][SP_CHUNK];
+  const int tid = threadIdx.x;
+  const int tile = blockIdx.x;
+  const int tz = tile / (G.ntiles[1] * G.ntiles[2]);
+  const int ty = (tile / G.ntiles[2]) % G.ntiles[1];
+  const int tx = tile % G.ntiles[2];
+  const int cx = tx * G.tile[2] + tid % G.tile[2];
+  const int cy = ty * G.tile[1] + (tid / G.tile[2]) % G.tile[1];
+  const int cz = tz * G.tile[0] + tid / (G.tile[2] * G.tile[1]);
+  const bool inside = tid < G.tile[0] * G.tile[1] * G.tile[2] && cx < G.mr[2] && cy < G.mr[1] &&
+                      cz < G.mr[0];
+  const int v0 = blockIdx.y * SP_V;
+  const int nvv = min(SP_V, nv - v0);
+  const int W = 2 * G.w + 1;
+  float2 acc[SP_V];
+#pragma unroll
+  for (int v = 0; v < SP_V; v++) acc[v] = make_float2(0.f, 0.f);
+  const int s0 = tile_start[tile], s1 = tile_start[tile + 1];
+  for (int c0 = s0; c0 < s1; c0 += SP_CHUNK) {
+    const int nc = min(SP_CHUNK, s1 - c0);
+    __syncthreads();
+    for (int e = tid; e < nc * 3 * W; e += NT) {
+      const int p = e / (3 * W), a = (e / W) % 3, o = e % W;
+      const int pt = tile_pts[c0 + p];
+      if (a >= 3 - G.dim) {
+        const float dl = d0[3 * pt + a] + (float)(o - G.w) * G.h[a];
+        wgt[p][a][o] = __expf(-dl * dl * G.inv4tau[a]);
+      } else {
+        wgt[p][a][o] = 1.0f;
+      }
+      if (o == 0) pi0[p][a] = a >= 3 - G.dim ? i0[3 * pt + a] : 0;
+    }
+    for (int e = tid; e < nc * nvv; e += NT) {
+      const int p = e % nc, v = e / nc;
+      pv[v][p] = vals[(long long)(v0 + v) * val_stride + tile_pts[c0 + p]];
+    }
+    __syncthreads();
+    if (inside) {
+      for (int p = 0; p < nc; p++) {
+        const int ox = wrap_off(cx - pi0[p][2], G.mr[2]);
+        const int oy = wrap_off(cy - pi0[p][1], G.mr[1]);
+        const int oz = G.dim == 3 ? wrap_off(cz - pi0[p][0], G.mr[0]) : 0;
+        if (abs(ox) > G.w || abs(oy) > G.w || abs(oz) > G.w) continue;
+        float wv = wgt[p][2][ox + G.w] * wgt[p][1][oy + G.w];
+        if (G.dim == 3) wv *= wgt[p][0][oz + G.w];
+#pragma unroll
+        for (int v = 0; v < SP_V; v++) {
+          if (v < nvv) {
+            acc[v].x = fmaf(wv, pv[v][p].x, acc[v].x);
+            acc[v].y = fmaf(wv, pv[v][p].y, acc[v].y);
+          }
+        }
+      }
+    }
+  }
+  if (inside) {
+    const long long cell = ((long long)cz * G.mr[1] + cy) * G.mr[2] + cx;
+    for (int v = 0; v < nvv; v++) fine[(long long)(v0 + v) * fine_stride + cell] = acc[v];
+  }
+}
+
+// type-1 finish: modes (natural order on the m-grid) = fine_hat[c mod mr] / prod ker
+// transpose (2D only): write [v][x][y]
+__global__ void k_deconv_gather(pf_nufft_geom G, const float2* __restrict__ fine,
+                                long long fine_stride, const float* __restrict__ kz,
+                                const float* __restrict__ ky, const float* __restrict__ kx,
+                                int nv, float2* __restrict__ out, long long out_stride,
+                                int transpose) {
+  const long long per = (long long)G.m[0] * G.m[1] * G.m[2];
+  const long long total = per * nv;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(e / per);
+    const long long rem = e - (long long)v * per;
+    int jz, jy, jx;
+    if (transpose) {
+      jy = (int)(rem % G.m[1]);
+      jx = (int)((rem / G.m[1]) % G.m[2]);
+      jz = 0;
+    } else {
+      jx = (int)(rem % G.m[2]);
+      jy = (int)((rem / G.m[2]) % G.m[1]);
+      jz = (int)(rem / ((long long)G.m[2] * G.m[1]));
+    }
+    const int czc = centred(jz, G.m[0]), cyc = centred(jy, G.m[1]), cxc = centred(jx, G.m[2]);
+    const long long cell = ((long long)natural(czc, G.mr[0]) * G.mr[1] + natural(cyc, G.mr[1])) *
+                               G.mr[2] + natural(cxc, G.mr[2]);
+    const float den = kz[czc + G.m[0] / 2] * ky[cyc + G.m[1] / 2] * kx[cxc + G.m[2] / 2];
+    const float2 f = fine[(long long)v * fine_stride + cell];
+    out[(long long)v * out_stride + rem] = make_float2(f.x / den, f.y / den);
+  }
+}
+
+// type-2 start: fine[v][cell] = S[v][mode] / prod ker on mode slots, 0 elsewhere.
+// S is natural order on the m-grid (or transposed [x][y] in 2D).
+__global__ void k_place(pf_nufft_geom G, const float2* __restrict__ S, long long s_stride,
+                        const float* __restrict__ kz, const float* __restrict__ ky,
+                        const float* __restrict__ kx, int nv, float2* __restrict__ fine,
+                        long long fine_stride, int transpose) {
+  const long long per = (long long)G.mr[0] * G.mr[1] * G.mr[2];
+  const long long total = per * nv;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(e / per);
+    const long long cell = e - (long long)v * per;
+    const int fx = (int)(cell % G.mr[2]);
+    const int fy = (int)((cell / G.mr[2]) % G.mr[1]);
+    const int fz = (int)(cell / ((long long)G.mr[2] * G.mr[1]));
+    // centred mode of each fine slot, or out of band
+    int c[3];
+    const int f3[3] = {fz, fy, fx};
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      const int m = G.m[a], mr = G.mr[a];
+      int cc = f3[a] < mr - mr / 2 ? f3[a] : f3[a] - mr;
+      if (cc < -(m / 2) || cc >= m - m / 2) ok = false;
+      c[a] = cc;
+    }
+    float2 val = make_float2(0.f, 0.f);
+    if (ok) {
+      const int jz = natural(c[0], G.m[0]), jy = natural(c[1], G.m[1]), jx = natural(c[2], G.m[2]);
+      const long long idx = transpose ? ((long long)jx * G.m[1] + jy)
+                                      : (((long long)jz * G.m[1] + jy) * G.m[2] + jx);
+      const float den = kz[c[0] + G.m[0] / 2] * ky[c[1] + G.m[1] / 2] * kx[c[2] + G.m[2] / 2];
+      const float2 s = S[(long long)v * s_stride + idx];
+      val = make_float2(s.x / den, s.y / den);
+    }
+    fine[(long long)v * fine_stride + cell] = val;
+  }
+}
+
+// type-2 finish (2D): out = sum_stencil fine * wy * wx, then * scale * exp(1j khat r_ill),
+// accumulated into vol[frame][dst0 + l] (frames: exp(1j w t) weights).
+__global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
+                              const float* __restrict__ d0, const double* __restrict__ xyz,
+                              int npts, const float2* __restrict__ fine, long long fine_stride,
+                              int n_illum, const double* __restrict__ ill, double kturns,
+                              int include_illum, float scale, const float2* __restrict__ frame_w,
+                              int n_frames, float2* __restrict__ vol, long long vol_frame_stride,
+                              long long dst0) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= npts) return;
+  const int W = 2 * G.w + 1;
+  float wy[2 * 12 + 1], wx[2 * 12 + 1];
+  for (int o = 0; o < W; o++) {
+    const float dy = d0[3 * l + 1] + (float)(o - G.w) * G.h[1];
+    const float dx = d0[3 * l + 2] + (float)(o - G.w) * G.h[2];
+    wy[o] = __expf(-dy * dy * G.inv4tau[1]);
+    wx[o] = __expf(-dx * dx * G.inv4tau[2]);
+  }
+  const int iy = i0[3 * l + 1], ix = i0[3 * l + 2];
+  float2 tot = make_float2(0.f, 0.f);
+  for (int p = 0; p < n_illum; p++) {
+    const float2* fp = fine + (long long)p * fine_stride;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int oy = 0; oy < W; oy++) {
+      const int cy = natural((long long)iy + oy - G.w, G.mr[1]);
+      float2 row = make_float2(0.f, 0.f);
+      for (int ox = 0; ox < W; ox++) {
+        const int cx = natural((long long)ix + ox - G.w, G.mr[2]);
+        const float2 f = fp[(long long)cy * G.mr[2] + cx];
+        row.x = fmaf(wx[ox], f.x, row.x);
+        row.y = fmaf(wx[ox], f.y, row.y);
+      }
+      acc.x = fmaf(wy[oy], row.x, acc.x);
+      acc.y = fmaf(wy[oy], row.y, acc.y);
+    }
+    float2 val = cscale(acc, scale);
+    if (include_illum) {
+      const double dx = xyz[3 * l] - ill[3 * p], dy = xyz[3 * l + 1] - ill[3 * p + 1];
+      const double dz = xyz[3 * l + 2] - ill[3 * p + 2];
+      val = cmul(val, expi_reduced(PF_TWO_PI * kturns * sqrt(dx * dx + dy * dy + dz * dz)));
+    }
+    tot = cadd(tot, val);
+  }
+  for (int f = 0; f < n_frames; f++) {
+    float2* d = vol + f * vol_frame_stride + dst0 + l;
+    *d = cadd(*d, cmul(tot, frame_w[f]));
+  }
+}
+
+int grid1d(long long total) {
+  long long g = (total + 255) / 256;
+  return (int)(g < 148 * 32 ? (g < 1 ? 1 : g) : 148 * 32);
+}
+
+}  // namespace
+
+extern "C" int pf_nufft_spread(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                               const int32_t* tile_start, const int32_t* tile_pts,
+                               const void* vals, int64_t val_stride, int nv, void* fine,
+                               int64_t fine_stride, void* stream) {
+  PF_ARG_CHECK(g && (g->dim == 2 || g->dim == 3) && g->w >= 1 && g->w <= 12 && nv >= 1,
+               "pf_nufft_spread: bad geometry");
+  PF_ARG_CHECK(g->tile[0] * g->tile[1] * g->tile[2] <= NT, "pf_nufft_spread: tile too large");
+  const int ntiles = g->ntiles[0] * g->ntiles[1] * g->ntiles[2];
+  dim3 grid(ntiles, pf_cdiv(nv, SP_V));
+  k_spread<<<grid, NT, 0, (cudaStream_t)stream>>>(*g, i0, d0, tile_start, tile_pts,
+                                                  (const float2*)vals, val_stride, nv,
+                                                  (float2*)fine, fine_stride);
+  PF_LAUNCH_CHECK("k_spread");
+  return 0;
+}
+
+extern "C" int pf_nufft_deconv(const pf_nufft_geom* g, const void* fine, int64_t fine_stride,
+                               const float* kz, const float* ky, const float* kx, int nv,
+                               void* out, int64_t out_stride, int transpose, void* stream) {
+  PF_ARG_CHECK(g && nv >= 1, "pf_nufft_deconv: bad args");
+  const long long total = (long long)g->m[0] * g->m[1] * g->m[2] * nv;
+  k_deconv_gather<<<grid1d(total), 256, 0, (cudaStream_t)stream>>>(
+      *g, (const float2*)fine, fine_stride, kz, ky, kx, nv, (float2*)out, out_stride, transpose);
+  PF_LAUNCH_CHECK("k_deconv_gather");
+  return 0;
+}
+
+extern "C" int pf_nufft_place(const pf_nufft_geom* g, const void* S, int64_t s_stride,
+                              const float* kz, const float* ky, const float* kx, int nv,
+                              void* fine, int64_t fine_stride, int transpose, void* stream) {
+  PF_ARG_CHECK(g && nv >= 1, "pf_nufft_place: bad args");
+  const long long total = (long long)g->mr[0] * g->mr[1] * g->mr[2] * nv;
+  k_place<<<grid1d(total), 256, 0, (cudaStream_t)stream>>>(*g, (const float2*)S, s_stride, kz, ky,
+                                                           kx, nv, (float2*)fine, fine_stride,
+                                                           transpose);
+  PF_LAUNCH_CHECK("k_place");
+  return 0;
+}
+
+extern "C" int pf_nufft_interp2_acc(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                                    const double* xyz, int npts, const void* fine,
+                                    int64_t fine_stride, int n_illum, const double* ill,
+                                    double khat, int include_illum, float scale,
+                                    const void* frame_w, int n_frames, void* vol,
+                                    int64_t vol_frame_stride, int64_t dst0, void* stream) {
+  PF_ARG_CHECK(g && g->dim == 2 && g->w <= 12 && npts >= 0, "pf_nufft_interp2_acc: bad args");
+  if (npts == 0) return 0;
+  k_interp2_acc<<<pf_cdiv(npts, 128), 128, 0, (cudaStream_t)stream>>>(
+      *g, i0, d0, xyz, npts, (const float2*)fine, fine_stride, n_illum, ill, khat / PF_TWO_PI,
+      include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride,
+      dst0);
+  PF_LAUNCH_CHECK("k_interp2_acc");
+  return 0;
+}

@@ -67,7 +67,7 @@ k_prop_kernel_rows(const pf_plane* __restrict__ planes, double khat, pf_prop_geo
 __global__ void __launch_bounds__(PT)
 k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan plan_y,
                const float2* __restrict__ ws_a, const float2* __restrict__ uhat,
-               float2* __restrict__ ws_b, int cols_per_cta) {
+               float2* __restrict__ ws_b, int cols_per_cta, int product_only) {
   extern __shared__ float2 sm[];
   const pf_plane pl = planes[blockIdx.y];
   const int px = g.px, py = g.py, ny = g.ny;
@@ -102,6 +102,18 @@ k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan 
         w0[c * ld + jy] = cmul(gh[c * ld + jy], u[(long long)jy * px + col]);
       }
       __syncthreads();
+      if (product_only) {   // full spectrum column for a type-2 readout: [plane][p][py][px]
+        float2* sp = ws_b + ((long long)blockIdx.y * g.n_illum + p) * (long long)py * px;
+        for (int e = threadIdx.x; e < nc * py; e += PT) {
+          const int jy = e / nc, c = e - jy * nc;
+          const int kx = k0 + c;
+          const int col = side == 0 ? kx : (px - kx) % px;
+          if (side == 1 && col == kx) continue;
+          sp[(long long)jy * px + col] = w0[c * ld + jy];
+        }
+        __syncthreads();
+        continue;
+      }
       const float2* res = fft_smem<1>(w0, w1, ld, nc, plan_y);
       for (int e = threadIdx.x; e < nc * ny; e += PT) {
         const int i = e / nc, c = e - i * nc;
@@ -189,6 +201,10 @@ extern "C" int64_t pf_prop_ws_b(const pf_prop_geom* g, int nplanes) {
   return (int64_t)nplanes * g->n_illum * g->ny * (int64_t)g->px;
 }
 
+extern "C" int64_t pf_prop_ws_spectrum(const pf_prop_geom* g, int nplanes) {
+  return (int64_t)nplanes * g->n_illum * g->py * (int64_t)g->px;
+}
+
 extern "C" int pf_prop_kernel_rows(const pf_plane* planes, int nplanes, double khat,
                                    const pf_prop_geom* g, const pf_fft_plan* plan_x, void* ws_a,
                                    void* stream) {
@@ -211,8 +227,10 @@ extern "C" int pf_prop_kernel_rows(const pf_plane* planes, int nplanes, double k
 
 extern "C" int pf_prop_columns(const pf_plane* planes, int nplanes, const pf_prop_geom* g,
                                const pf_fft_plan* plan_y, const void* ws_a, const void* uhat,
-                               void* ws_b, void* stream) {
+                               void* ws_b, int product_only, void* stream) {
   PF_ARG_CHECK(g && plan_y && plan_y->n == g->py && nplanes >= 1, "pf_prop_columns: bad args");
+  PF_ARG_CHECK(!(product_only && pf_prop_fast_L(g)),
+               "pf_prop_columns: product_only needs a non-register-path geometry");
   if (pf_prop_fast_L(g))
     return pf_prop_fast_stage(1, planes, nplanes, 0.0, g, plan_y, ws_a, nullptr, uhat, nullptr,
                               ws_b, nullptr, nullptr, 0, nullptr, 0, (cudaStream_t)stream);
@@ -224,7 +242,8 @@ extern "C" int pf_prop_columns(const pf_plane* planes, int nplanes, const pf_pro
   dim3 grid(pf_cdiv(cols_a, cpc), nplanes);
   const size_t smem = (size_t)3 * cpc * pf_ld(g->py) * sizeof(float2);
   k_prop_columns<<<grid, PT, smem, (cudaStream_t)stream>>>(
-      planes, *g, *plan_y, (const float2*)ws_a, (const float2*)uhat, (float2*)ws_b, cpc);
+      planes, *g, *plan_y, (const float2*)ws_a, (const float2*)uhat, (float2*)ws_b, cpc,
+      product_only);
   PF_LAUNCH_CHECK("k_prop_columns");
   return 0;
 }

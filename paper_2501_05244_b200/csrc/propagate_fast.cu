@@ -294,7 +294,7 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
 
 // 32*L when the register path applies (square power-of-two pad 128..1024), else 0
 int pf_prop_fast_L(const pf_prop_geom* g) {
-  if (g->px != g->py) return 0;
+  if ((g->flags & 1) || g->px != g->py) return 0;
   switch (g->px) {
     case 128: return 4;
     case 256: return 8;

@@ -1,0 +1,196 @@
+"""Host plans for the GPU NUFFT (geometry only, float64) and the type-1/type-2 drivers.
+
+Mirrors reference ``NufftPlan`` (spectral.py:230-315): spread half-width
+``w = max(2, ceil(log10(1/eps)) + 2)``, fine grid ``mr = next_fast_len(max(2m, 2w+2))``,
+``tau = pi w / (s (s - 1/2) m^2)`` with ``s = mr/m``, and the DISCRETE
+deconvolution ``ker[k] = 1 + 2 sum_j exp(-(j h)^2 / 4 tau) cos(k j h)`` so that
+points on fine-grid nodes are exact.  The per-point stencil anchors ``i0`` and
+window offsets ``d0`` (spectral.py:281-303) and the tile buckets of the
+gather-spread kernel are computed here once per geometry.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _lib
+from ._fastlen import next_fast_len
+from .core import _require
+
+_EPS_MIN, _EPS_MAX = 1e-14, 1e-1
+_COORD_TOL = 1e-9
+TILE_2D = (1, 16, 16)
+TILE_3D = (4, 8, 8)
+
+
+class NufftPlan:
+    """Plan for modes ``(m_y, m_x)`` or ``(m_z, m_y, m_x)`` at accuracy ``eps``."""
+
+    def __init__(self, modes, eps: float, device):
+        modes = tuple(int(m) for m in modes)
+        _require(len(modes) in (2, 3), "supported dimensionalities are 2 and 3")
+        _require(all(m >= 1 for m in modes), "mode counts must be >= 1")
+        _require(math.isfinite(eps) and _EPS_MIN <= eps <= _EPS_MAX,
+                 f"accuracy target must lie in [{_EPS_MIN:g}, {_EPS_MAX:g}]")
+        self.dim = len(modes)
+        self.modes3 = (1,) * (3 - self.dim) + modes
+        self.w = max(2, math.ceil(math.log10(1.0 / eps)) + 2)
+        _require(self.w <= 12, "accuracy target too tight for the GPU stencil (w <= 12)")
+        self.device = device
+        mrs, taus, kers = [], [], []
+        for m in self.modes3:
+            if m == 1 and len(mrs) < 3 - self.dim:
+                mrs.append(1)
+                taus.append(1.0)
+                kers.append(np.ones(1))
+                continue
+            mr = next_fast_len(max(2 * m, 2 * self.w + 2))
+            s = mr / m
+            tau = math.pi * self.w / (s * (s - 0.5) * m * m)
+            h = 2.0 * math.pi / mr
+            k = np.arange(m) - m // 2
+            j = np.arange(1, self.w + 1)
+            ker = 1.0 + 2.0 * (np.exp(-(j * h) ** 2 / (4.0 * tau))[None, :]
+                               * np.cos(np.outer(k, j * h))).sum(axis=1)
+            assert (ker > 0).all()
+            mrs.append(mr)
+            taus.append(tau)
+            kers.append(ker)
+        self.mrs = tuple(mrs)
+        self.taus = tuple(taus)
+        self.tile = TILE_2D if self.dim == 2 else TILE_3D
+        g = _lib.PfNufftGeom()
+        g.dim, g.w = self.dim, self.w
+        for a in range(3):
+            g.mr[a] = self.mrs[a]
+            g.m[a] = self.modes3[a]
+            g.h[a] = 2.0 * math.pi / self.mrs[a]
+            g.inv4tau[a] = 1.0 / (4.0 * self.taus[a])
+            g.tile[a] = self.tile[a]
+            g.ntiles[a] = -(-self.mrs[a] // self.tile[a])
+        self.geom = g
+        self.kers = [torch.from_numpy(k.astype(np.float32)).to(device) for k in kers]
+        self.fine_elems = int(np.prod(self.mrs))
+        self.mode_elems = int(np.prod(self.modes3))
+
+    @property
+    def gref(self):
+        return ctypes.byref(self.geom)
+
+    # -- per-geometry point data ------------------------------------------------------
+    def points(self, pts: np.ndarray) -> "NufftPoints":
+        return NufftPoints(self, pts)
+
+
+def check_points(pts, d: int) -> np.ndarray:
+    """Torus coordinates [L, d] in [-pi, pi) (reference spectral.py:318-329)."""
+    pts = np.asarray(pts, dtype=np.float64)
+    if pts.ndim == 1:
+        pts = pts[:, None]
+    _require(pts.ndim == 2 and pts.shape[1] == d, f"points must be [L, {d}] for {d}-dimensional modes")
+    _require(pts.shape[0] >= 1, "need at least one point")
+    _require(bool(np.isfinite(pts).all()), "point coordinates must be finite")
+    _require(bool((pts >= -math.pi - _COORD_TOL).all() and (pts < math.pi + _COORD_TOL).all()),
+             "point coordinates must lie in [-pi, pi)")
+    return pts
+
+
+class NufftPoints:
+    """Stencil anchors + tile buckets of one point set under one plan (device tensors)."""
+
+    def __init__(self, plan: NufftPlan, pts: np.ndarray):
+        pts = check_points(pts, plan.dim)
+        L = pts.shape[0]
+        self.n = L
+        i0 = np.zeros((L, 3), dtype=np.int64)
+        d0 = np.zeros((L, 3), dtype=np.float64)
+        for a in range(3 - plan.dim, 3):
+            # mode axis a (z, y, x order) pairs with point column (2 - a) (x is column 0)
+            x = pts[:, 2 - a]
+            mr = plan.mrs[a]
+            h = 2.0 * math.pi / mr
+            xi = x - 2.0 * math.pi * np.floor(x / (2.0 * math.pi))
+            k = np.floor(xi / h + 0.5).astype(np.int64)
+            i0[:, a] = k
+            d0[:, a] = k * h - xi
+        dv = plan.device
+        self.i0 = torch.from_numpy(i0.astype(np.int32)).to(dv)
+        self.d0 = torch.from_numpy(d0.astype(np.float32)).to(dv)
+        self._i0_host = i0
+        self.plan = plan
+        self._tiles = None
+
+    def tiles(self):
+        """CSR (tile_start, tile_pts) of the tiles each point's stencil touches."""
+        if self._tiles is not None:
+            return self._tiles
+        p = self.plan
+        w = p.w
+        per_axis = []
+        for a in range(3):
+            if p.mrs[a] == 1:
+                per_axis.append(np.zeros((self.n, 1), dtype=np.int64))
+                continue
+            cells = (self._i0_host[:, a][:, None] + np.arange(-w, w + 1)[None, :]) % p.mrs[a]
+            t = np.sort(cells // p.tile[a], axis=1)
+            dup = np.zeros_like(t, dtype=bool)
+            dup[:, 1:] = t[:, 1:] == t[:, :-1]
+            t[dup] = -1
+            keep = (~dup).sum(axis=1).max()
+            t = -np.sort(-t, axis=1)[:, :keep]   # valid ids first, -1 padding last
+            per_axis.append(t)
+        nt = [int(p.geom.ntiles[a]) for a in range(3)]
+        tz, ty, tx = per_axis
+        comb = (tz[:, :, None, None] * nt[1] + ty[:, None, :, None]) * nt[2] + tx[:, None, None, :]
+        valid = (tz[:, :, None, None] >= 0) & (ty[:, None, :, None] >= 0) & (tx[:, None, None, :] >= 0)
+        comb = np.where(valid, comb, -1).reshape(self.n, -1)
+        pid = np.broadcast_to(np.arange(self.n)[:, None], comb.shape)
+        sel = comb >= 0
+        tid, pts = comb[sel], pid[sel]
+        order = np.argsort(tid, kind="stable")
+        tid, pts = tid[order], pts[order]
+        ntot = nt[0] * nt[1] * nt[2]
+        start = np.zeros(ntot + 1, dtype=np.int64)
+        np.cumsum(np.bincount(tid, minlength=ntot), out=start[1:])
+        dv = p.device
+        self._tiles = (torch.from_numpy(start.astype(np.int32)).to(dv),
+                       torch.from_numpy(pts.astype(np.int32)).to(dv))
+        return self._tiles
+
+
+def type1(plan: NufftPlan, pts: NufftPoints, vals: torch.Tensor, nv: int, val_stride: int,
+          out: torch.Tensor, out_stride: int, fine: torch.Tensor | None = None,
+          transpose: bool = False, stream=None) -> torch.Tensor:
+    """U[v][k] = sum_l vals[v][l] exp(-1j k.x_l) for centred k (spectral.py:336-358).
+
+    ``out`` receives natural-order modes ([v][..modes..], or [v][x][y] with
+    ``transpose`` in 2D).  ``fine`` is scratch [nv][prod(mr)] complex64.
+    """
+    if fine is None:
+        fine = torch.empty((nv, plan.fine_elems), dtype=torch.complex64, device=plan.device)
+    ts, tp = pts.tiles()
+    s = dev.stream_ptr(stream)
+    _lib.call("pf_nufft_spread", plan.gref, dev.ptr(pts.i0), dev.ptr(pts.d0), dev.ptr(ts),
+              dev.ptr(tp), dev.ptr(vals), val_stride, nv, dev.ptr(fine), plan.fine_elems, s)
+    shape = tuple(m for m in plan.mrs if True)[3 - plan.dim:]
+    dev.fftn_natural(fine, shape, nv, -1, 1.0, stream)
+    kz, ky, kx = plan.kers
+    _lib.call("pf_nufft_deconv", plan.gref, dev.ptr(fine), plan.fine_elems, dev.ptr(kz),
+              dev.ptr(ky), dev.ptr(kx), nv, dev.ptr(out), out_stride, int(transpose), s)
+    return out
+
+
+def place_and_inverse(plan: NufftPlan, S: torch.Tensor, nv: int, s_stride: int,
+                      fine: torch.Tensor, stream=None) -> torch.Tensor:
+    """Type-2 first half (spectral.py:373-375): fine = ifftn(place(S / ker)) * prod(mr)."""
+    kz, ky, kx = plan.kers
+    _lib.call("pf_nufft_place", plan.gref, dev.ptr(S), s_stride, dev.ptr(kz), dev.ptr(ky),
+              dev.ptr(kx), nv, dev.ptr(fine), plan.fine_elems, 0, dev.stream_ptr(stream))
+    shape = plan.mrs[3 - plan.dim:]
+    dev.fftn_natural(fine, shape, nv, +1, 1.0, stream)
+    return fine

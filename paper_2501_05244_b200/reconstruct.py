@@ -186,7 +186,7 @@ class Propagator:
             _lib.call("pf_prop_kernel_rows", pp, nb, khat, gref, self.plan_x.ref,
                       dev.ptr(self.ws_a), s)
             _lib.call("pf_prop_columns", pp, nb, gref, self.plan_y.ref, dev.ptr(self.ws_a), up,
-                      dev.ptr(self.ws_b), s)
+                      dev.ptr(self.ws_b), 0, s)
             _lib.call("pf_prop_rows_out", pp, nb, khat, gref, self.plan_x.ref,
                       dev.ptr(self.ws_b), ill_ptr, frame_w_ptr, n_frames, dev.ptr(vol),
                       vol_frame_stride, s)

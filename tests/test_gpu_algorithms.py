@@ -1,0 +1,107 @@
+"""GPU parity of srsd / nursd1 / nursd2 / nursd3 / srsd_nursd2 / nursd3d vs reference goldens + oracle."""
+
+import numpy as np
+import pytest
+
+import paper_2501_05244_b200 as pf
+from oracle import pf_oracle as O
+from golden_io import case_call, grid_from, load, slices_from
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+CASES = ["chain_srsd_unit", "chain_srsd_08", "chain_nursd1", "chain_nursd2", "chain_nursd3",
+         "chain_hybrid", "chain_nursd3d_flat", "nursd1_random", "nursd2_random", "nursd3_random",
+         "hybrid_random", "srsd_linear16", "srsd_aniso16", "nursd3d_curved"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_algorithm_golden(name):
+    d = load(f"rec_{name}")
+    sl, grid = slices_from(d), grid_from(d)
+    alg, kw = case_call(name)
+    vol = pf.reconstruct(sl, grid, alg, **kw)
+    assert O.rel_l2(vol.field, d["field"]) < TOL, name
+    if grid.kind != "explicit":
+        a = np.abs(vol.field.reshape(grid.shape)).max(axis=0)
+        b = np.abs(d["field"].reshape(grid.shape)).max(axis=0)
+        assert int(np.argmax(a)) == int(np.argmax(b))
+    if "video" in d:
+        v = pf.srsd(sl, grid, times=np.array([0.0, 5e-10]))
+        assert O.rel_l2(v.field, d["video"]) < TOL
+
+
+def test_degeneracy_chain_against_rsd():
+    """Every variant on degenerate input equals rsd (reference test_reconstruct.py:191-239)."""
+    ref = load("rec_chain_rsd")["field"]
+    for name in ["chain_srsd_unit", "chain_nursd1", "chain_nursd2", "chain_nursd3", "chain_hybrid"]:
+        d = load(f"rec_{name}")
+        alg, kw = case_call(name)
+        vol = pf.reconstruct(slices_from(d), grid_from(d), alg, **kw)
+        assert O.rel_l2(vol.field, ref) < TOL, name
+
+
+def _rand_slices(rng, relay, n_freq=3, n_ill=1, lam=0.06):
+    w0 = 2 * np.pi * 299792458.0 / lam
+    freqs = w0 * (1.0 + 0.03 * np.arange(n_freq))
+    coeff = rng.normal(size=(n_ill, relay.count, n_freq)) + 1j * rng.normal(size=(n_ill, relay.count, n_freq))
+    ill = pf.PointList(rng.uniform(-0.3, 0.3, size=(n_ill, 2)))
+    return pf.FrequencySlices(freqs, coeff, relay, ill)
+
+
+def test_nursd1_c1_like(rng):
+    """Config-1 shape (i.i.d. relay points, P=140 from the reference pad rule), reduced size."""
+    pts = rng.uniform(-1.0, 1.0, size=(4096, 2))
+    sl = _rand_slices(rng, pf.NonUniformPlanarRelay(pf.PointList(pts), 0.0), n_freq=2)
+    p = 2.0 / 64
+    grid = pf.CuboidGrid(pf.UniformGrid3D(64, 64, 3, p, p, 0.5, -1 + p / 2, -1 + p / 2, 0.5))
+    vol = pf.nursd1(sl, grid)
+    ref = O.nursd1(sl, grid)
+    assert O.rel_l2(vol.field, ref) < TOL
+
+
+def test_nursd1_on_lattice_register_path(rng):
+    """Lattice-subsampled relay (config-4 NURSD variant, F4): P-independent, fast pads."""
+    n = 64
+    p = 2.0 / n
+    g = pf.UniformGrid2D(n, n, p, p, -1 + p / 2, -1 + p / 2, 0.0)
+    xy = pf.grid_coordinates(g).points
+    keep = rng.random(xy.shape[0]) < 0.5
+    sl = _rand_slices(rng, pf.NonUniformPlanarRelay(pf.PointList(xy[keep]), 0.0), n_freq=2)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(n, n, 3, p, p, 0.5, g.x0, g.y0, 0.5))
+    from paper_2501_05244_b200.algorithms import Nursd1Engine
+    eng = Nursd1Engine(sl, grid)
+    assert eng.prop.transposed and eng.px == 128
+    vol = pf.nursd1(sl, grid)
+    # equals rsd on the zero-filled lattice (reference test_acceptance.py:174-176)
+    full = np.zeros((1, n * n, 2), complex)
+    full[:, keep, :] = sl.coefficients
+    slu = pf.FrequencySlices(sl.frequencies, full, pf.UniformRelay(g), sl.illuminations)
+    assert O.rel_l2(vol.field, O.rsd(slu, grid)) < TOL
+    assert O.rel_l2(vol.field, O.nursd1(sl, grid)) < TOL
+
+
+@pytest.mark.parametrize("n,frames", [(64, False), (128, True)])
+def test_srsd_frustum_vs_oracle(rng, n, frames):
+    """Config-3 shape (linear frustum, P = next_fast_len(2N) power of two), reduced size."""
+    p = 2.0 / n
+    g = pf.UniformGrid2D(n, n, p, p, -1 + p / 2, -1 + p / 2, 0.0)
+    sl = _rand_slices(rng, pf.UniformRelay(g), n_freq=2, lam=0.08)
+    zs = np.linspace(1.0, 3.0, 3)
+    grid = pf.FrustumGrid(g, zs, zs[0] / zs, zs[0] / zs)
+    times = np.array([0.0, 3e-10]) if frames else None
+    vol = pf.srsd(sl, grid, times=times)
+    ref = O.srsd(sl, grid, times=times)
+    assert O.rel_l2(vol.field, ref) < TOL
+
+
+def test_nursd2_offlattice_voxels(rng):
+    n = 24
+    p = 0.02
+    g = pf.UniformGrid2D(n, n, p, p, -(n - 1) * p / 2, -(n - 1) * p / 2, 0.0)
+    sl = _rand_slices(rng, pf.UniformRelay(g), n_freq=2, n_ill=2)
+    planes = tuple(pf.VoxelPlane(z, pf.PointList(rng.uniform(-0.2, 0.2, size=(50, 2))))
+                   for z in (0.7, 0.9))
+    ev = pf.ExplicitVoxels(planes)
+    vol = pf.nursd2(sl, ev)
+    assert O.rel_l2(vol.field, O.nursd2(sl, ev)) < TOL
