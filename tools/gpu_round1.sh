@@ -8,5 +8,5 @@ python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_r1.
 python tools/prof_rsd.py > gpurun_out/prof_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv --log-file gpurun_out/launches_r1.csv python tools/prof_rsd.py > /dev/null 2>&1
 python tools/prof_rsd.py > /dev/null 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_temporal_dft|k_p[abc]" -s 1 -c 4 -o gpurun_out/prof_r1_full python tools/prof_rsd.py > gpurun_out/ncu_full_r1.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_temporal_dft|k_p[abc]" -s 0 -c 4 -o gpurun_out/prof_r1_full python tools/prof_rsd.py > gpurun_out/ncu_full_r1.log 2>&1
 tail -2 gpurun_out/ncu_full_r1.log
