@@ -102,13 +102,6 @@ def _dist_env():
     return world, rank, local
 
 
-def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous block [lo, hi) of n items owned by ``rank`` (balanced, ordered)."""
-    base, rem = divmod(n, world)
-    lo = rank * base + min(rank, rem)
-    return lo, lo + base + (1 if rank < rem else 0)
-
-
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -120,6 +113,7 @@ def run_ours(args):
 
     import paper_2501_05244_b200 as pf
     from paper_2501_05244_b200 import _lib, configs
+    from paper_2501_05244_b200.distributed import SliceGather, VolumeGather, shard_range
     from paper_2501_05244_b200.pipeline import TransientReconstructor
 
     world, rank, local = _dist_env()
@@ -138,22 +132,17 @@ def run_ours(args):
     hist_shard = hist[:, d_lo:d_hi].contiguous()
     del hist
     torch.cuda.empty_cache()
-    rec = TransientReconstructor(kernel, cfg.relay, cfg.illuminations, cfg.grid, t0=cfg.t0,
-                                 plane_range=(k_lo, k_hi), device=device)
-    eng = rec.engine
     plane_vox = cfg.grid.grid.nx * cfg.grid.grid.ny
-    local_shard = torch.empty((F, I, d_hi - d_lo), dtype=torch.complex64, device=device)
-    full_coeff = torch.empty((F, I, D), dtype=torch.complex64, device=device)
+    sgather = vgather = None
     if world > 1:
-        counts = [shard_range(D, world, r) for r in range(world)]
-        maxd = max(h - l for l, h in counts)
-        gather_buf = torch.empty((world, F * I * maxd), dtype=torch.complex64, device=device)
-        send_buf = torch.zeros((F * I * maxd,), dtype=torch.complex64, device=device)
-        kcounts = [shard_range(nz, world, r) for r in range(world)]
-        maxk = max(h - l for l, h in kcounts)
-        vol_send = torch.zeros((maxk * plane_vox,), dtype=torch.complex64, device=device)
-        vol_all = (torch.empty((world, maxk * plane_vox), dtype=torch.complex64, device=device)
-                   if rank == 0 else None)
+        sgather = SliceGather(F, I, D, world, device)
+        vgather = VolumeGather(nz, plane_vox, 1, world, rank, device)
+    rec = TransientReconstructor(kernel, cfg.relay, cfg.illuminations, cfg.grid, t0=cfg.t0,
+                                 plane_range=(k_lo, k_hi), device=device,
+                                 trace_range=(d_lo, d_hi), slice_gather=sgather,
+                                 volume_gather=vgather)
+    eng = rec.engine
+    local_shard = rec.coeff
     stream = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
 
@@ -161,21 +150,12 @@ def run_ours(args):
         ev[0].record(stream)
         rec.temporal.run(hist_shard.view(-1, T), local_shard.view(F, -1), stream)
         ev[1].record(stream)
-        if world > 1:
-            n_loc = F * I * (d_hi - d_lo)
-            send_buf[:n_loc].copy_(local_shard.view(-1))
-            dist.all_gather_into_tensor(gather_buf.view(-1), send_buf)
-            for r, (l, h) in enumerate(counts):
-                full_coeff[:, :, l:h].copy_(gather_buf[r, :F * I * (h - l)].view(F, I, h - l))
-            coeff = full_coeff
-        else:
-            coeff = local_shard
+        coeff = sgather(local_shard) if world > 1 else local_shard
         ev[2].record(stream)
         eng.run(coeff, rec.vol, stream)
         ev[3].record(stream)
         if world > 1:
-            vol_send[:rec.vol.numel()].copy_(rec.vol.view(-1))
-            dist.gather(vol_send, [vol_all[r] for r in range(world)] if rank == 0 else None, dst=0)
+            vgather(rec.vol)
         ev[4].record(stream)
 
     for _ in range(args.warmup):
@@ -247,7 +227,7 @@ def run_ours(args):
                "ms": k1_ms, "peak_source": peak_src}
     roof_k1["frac"] = roof_k1["achieved"] / hbm_peak
     roof_s3 = {"bound": "fp32", "achieved": s3_flops / (s3_ms * 1e-3) / 1e12, "peak": fp32_peak,
-               "unit": "TFLOP/s", "traffic": _traffic("k_prop"),
+               "unit": "TFLOP/s", "traffic": _prop_traffic(F, k_hi - k_lo),
                "kernel": "propagation k_prop_kernel_rows+k_prop_columns+k_prop_rows_out (S3)",
                "ms": s3_ms, "peak_source": "nominal 148 SM x 128 FP32 lanes x 2 x sm_max_mhz "
                                            "(MEASURED_PEAKS.json has no FP32 entry)",
@@ -279,6 +259,14 @@ def run_ours(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def _prop_traffic(n_freq, n_planes):
+    """Per-step DRAM bytes of the propagation stage from the committed ncu capture."""
+    per_batch = _traffic("k_prop_per_batch_of_8_planes")
+    if per_batch is None:
+        return None
+    return per_batch * n_freq * (n_planes / 8.0)
 
 
 def _traffic(kernel_prefix):

@@ -1,0 +1,77 @@
+"""Multi-GPU plumbing: depth-plane sharding, slice all-gather, volume gather.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch on the box,
+gloo in the CPU tests).  The work partitions without a data-path exchange
+inside the propagation: every voxel's ascending-frequency sum lives on the
+rank that owns its depth plane, so results are bitwise independent of the
+number of GPUs.  The two exchanges are at the edges of the path:
+
+* K1 shards the detectors; the frequency slices (64 MiB at config 4) are
+  all-gathered so every rank holds ``[F, I, D]`` (the north star's "frequency
+  slices broadcast over NVLink");
+* the finished plane blocks are gathered to rank 0.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of n items owned by ``rank`` (balanced, in order)."""
+    base, rem = divmod(n, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def _real(t: torch.Tensor) -> torch.Tensor:
+    return torch.view_as_real(t) if t.is_complex() else t
+
+
+class SliceGather:
+    """All-gather detector-sharded slices [F, I, D_r] into [F, I, D] on every rank."""
+
+    def __init__(self, n_freq: int, n_illum: int, n_det: int, world: int, device, group=None):
+        self.world, self.group = world, group
+        self.F, self.I, self.D = n_freq, n_illum, n_det
+        self.ranges = [shard_range(n_det, world, r) for r in range(world)]
+        self.maxd = max(h - l for l, h in self.ranges)
+        self.send = torch.zeros((n_freq * n_illum * self.maxd,), dtype=torch.complex64, device=device)
+        self.recv = [torch.empty_like(self.send) for _ in range(world)]
+        self.full = torch.empty((n_freq, n_illum, n_det), dtype=torch.complex64, device=device)
+
+    def __call__(self, local: torch.Tensor) -> torch.Tensor:
+        n = local.numel()
+        self.send[:n].copy_(local.reshape(-1))
+        dist.all_gather([_real(r) for r in self.recv], _real(self.send), group=self.group)
+        for r, (lo, hi) in enumerate(self.ranges):
+            cnt = self.F * self.I * (hi - lo)
+            self.full[:, :, lo:hi].copy_(self.recv[r][:cnt].view(self.F, self.I, hi - lo))
+        return self.full
+
+
+class VolumeGather:
+    """Gather plane-sharded volumes [frames, V_r] into [frames, V] on rank 0."""
+
+    def __init__(self, n_planes: int, plane_voxels: int, n_frames: int, world: int, rank: int,
+                 device, group=None):
+        self.world, self.rank, self.group = world, rank, group
+        self.ranges = [shard_range(n_planes, world, r) for r in range(world)]
+        self.pv, self.nf = plane_voxels, n_frames
+        self.maxv = max(h - l for l, h in self.ranges) * plane_voxels
+        self.send = torch.zeros((n_frames, self.maxv), dtype=torch.complex64, device=device)
+        self.recv = ([torch.empty_like(self.send) for _ in range(world)] if rank == 0 else None)
+        self.full = (torch.empty((n_frames, n_planes * plane_voxels), dtype=torch.complex64,
+                                 device=device) if rank == 0 else None)
+
+    def __call__(self, local: torch.Tensor):
+        self.send[:, :local.shape[1]].copy_(local)
+        dist.gather(_real(self.send), [_real(r) for r in self.recv] if self.rank == 0 else None,
+                    dst=0, group=self.group)
+        if self.rank != 0:
+            return None
+        for r, (lo, hi) in enumerate(self.ranges):
+            n = (hi - lo) * self.pv
+            self.full[:, lo * self.pv:hi * self.pv].copy_(self.recv[r][:, :n])
+        return self.full

@@ -39,7 +39,7 @@ class TransientReconstructor:
 
     def __init__(self, kernel, relay, illuminations, grid, t0: float = 0.0, padding="exact",
                  include_illumination=True, times=None, plane_range=None, chunks: int = 8,
-                 device=None):
+                 device=None, trace_range=None, slice_gather=None, volume_gather=None):
         self.device = device or dev.require_cuda()
         self.kernel = kernel
         self.meta = _Meta(kernel, relay, illuminations)
@@ -48,8 +48,11 @@ class TransientReconstructor:
         self.temporal = TemporalPlan(kernel, t0, self.device)
         self.n_illum = illuminations.count
         self.n_det = relay.count
-        self.coeff = torch.empty((kernel.n_freq, self.n_illum, self.n_det), dtype=torch.complex64,
-                                 device=self.device)
+        lo, hi = trace_range or (0, self.n_det)
+        self.n_det_local = hi - lo
+        self.slice_gather, self.volume_gather = slice_gather, volume_gather
+        self.coeff = torch.empty((kernel.n_freq, self.n_illum, self.n_det_local),
+                                 dtype=torch.complex64, device=self.device)
         self.vol = torch.zeros((self.engine.n_frames, self.engine.n_voxels), dtype=torch.complex64,
                                device=self.device)
         self.chunks = max(1, int(chunks))
@@ -76,7 +79,10 @@ class TransientReconstructor:
         if self._hist_dev is None or self._hist_dev.shape != hist_host.shape:
             self._hist_dev = torch.empty_like(hist_host, device=self.device)
         if self._vol_host is None:
-            self._vol_host = torch.empty(self.vol.shape, dtype=self.vol.dtype, pin_memory=True)
+            shape = self.vol.shape
+            if self.volume_gather is not None:
+                shape = (self.vol.shape[0], self.engine.grid.count)
+            self._vol_host = torch.empty(shape, dtype=self.vol.dtype, pin_memory=True)
         src = hist_host.view(n_tr, t_n)
         dst = self._hist_dev.view(n_tr, t_n)
         out = self.coeff.view(self.kernel.n_freq, n_tr)
@@ -90,8 +96,15 @@ class TransientReconstructor:
                 ev.record(self.copy_stream)
             main.wait_event(ev)
             self.temporal.run(dst[c0:c1], out[:, c0:c1], main)
-        self.propagate(self.coeff, main)
-        self._vol_host.copy_(self.vol, non_blocking=True)
+        coeff = self.slice_gather(self.coeff) if self.slice_gather is not None else self.coeff
+        self.propagate(coeff, main)
+        vol = self.vol
+        if self.volume_gather is not None:
+            vol = self.volume_gather(self.vol)      # full volume on rank 0, None elsewhere
+            if vol is None:
+                main.synchronize()
+                return None
+        self._vol_host.copy_(vol, non_blocking=True)
         main.synchronize()
         return self._vol_host
 
