@@ -150,8 +150,11 @@ class SrsdEngine:
                                batch=batch)
         self.tabs = _ScaledTables(px, py, [grid.alphas[k] for k in ks],
                                   [grid.betas[k] for k in ks], self.device)
-        self.uhat = torch.empty((batch * I * py * px,), dtype=torch.complex64, device=self.device)
-        self.xbuf = torch.empty((batch * g.ny * px,), dtype=torch.complex64, device=self.device)
+        nl = len(self.prop.lane_streams)
+        self.uhat_l = [torch.empty((batch * I * py * px,), dtype=torch.complex64,
+                                   device=self.device) for _ in range(nl)]
+        self.xbuf_l = [torch.empty((batch * g.ny * px,), dtype=torch.complex64,
+                                   device=self.device) for _ in range(nl)]
         self.ill = _ill_tensor(slices, self.device)
         self.frame_w = _frame_weights(self.freqs, self.times, self.device)
         self.n_frames = 1 if self.times is None else self.times.size
@@ -164,22 +167,21 @@ class SrsdEngine:
         else:
             vol.zero_()
         g, I, px, py = self.g, self.n_illum, self.px, self.py
-        D = g.nx * g.ny
-        nplanes = self.k_hi - self.k_lo
-        for b0 in range(0, nplanes, self.batch):
-            b1 = min(nplanes, b0 + self.batch)
+
+        def body(b0, b1, lane, ls):
             nb = b1 - b0
+            uhat, xbuf = self.uhat_l[lane], self.xbuf_l[lane]
             for fi in range(self.freqs.size):
                 for p in range(I):
-                    src = coeff[fi, p]
-                    out = self.uhat[p * py * px:]
-                    _scaled_spectra(src, g.ny, g.nx, py, px, self.tabs, b0, nb, self.xbuf, out,
-                                    I * py * px, self.transposed, stream)
+                    _scaled_spectra(coeff[fi, p], g.ny, g.nx, py, px, self.tabs, b0, nb, xbuf,
+                                    uhat[p * py * px:], I * py * px, self.transposed, ls)
                 khat = float(self.freqs[fi]) / C
-                self.prop.run_frequency(dev.ptr(self.uhat), khat, dev.ptr(self.ill),
+                self.prop.run_frequency(dev.ptr(uhat), khat, dev.ptr(self.ill),
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
-                                        plane_hi=b1, stream=stream)
+                                        plane_hi=b1, stream=ls, lane=lane)
+
+        self.prop.run_batches(body, stream)
         return vol
 
 
@@ -209,14 +211,16 @@ class _UhatPropEngine:
 
     def _propagate(self, uhat, vol, stream):
         per_f = self.n_illum * self.py * self.px
-        for b0 in range(0, self.prop.nplanes, self.prop.batch):
-            b1 = min(self.prop.nplanes, b0 + self.prop.batch)
+
+        def body(b0, b1, lane, ls):
             for fi in range(self.freqs.size):
                 khat = float(self.freqs[fi]) / C
                 self.prop.run_frequency(dev.ptr(uhat) + 8 * fi * per_f, khat, dev.ptr(self.ill),
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
-                                        plane_hi=b1, stream=stream)
+                                        plane_hi=b1, stream=ls, lane=lane)
+
+        self.prop.run_batches(body, stream)
         return vol
 
 

@@ -162,10 +162,16 @@ class Propagator:
         raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
         self.planes_dev = torch.from_numpy(raw).to(device)
         self.plane_size = ctypes.sizeof(_lib.PfPlane)
-        self.ws_a = torch.empty(_lib.call("pf_prop_ws_a", ctypes.byref(g), self.batch),
-                                dtype=torch.complex64, device=device)
-        self.ws_b = torch.empty(_lib.call("pf_prop_ws_b", ctypes.byref(g), self.batch),
-                                dtype=torch.complex64, device=device)
+        # two independent lanes (workspace + stream): consecutive plane batches run
+        # concurrently so the synthesis-bound kernel A of one batch overlaps the
+        # load-bound kernels B/C of the other on the same SMs
+        nlanes = 2 if self.nplanes > self.batch else 1
+        self.ws_a_l = [torch.empty(_lib.call("pf_prop_ws_a", ctypes.byref(g), self.batch),
+                                   dtype=torch.complex64, device=device) for _ in range(nlanes)]
+        self.ws_b_l = [torch.empty(_lib.call("pf_prop_ws_b", ctypes.byref(g), self.batch),
+                                   dtype=torch.complex64, device=device) for _ in range(nlanes)]
+        self.ws_a, self.ws_b = self.ws_a_l[0], self.ws_b_l[0]
+        self.lane_streams = [torch.cuda.Stream(device=device) for _ in range(nlanes)]
         self.plan_x = dev.fft_plan(px, device)
         self.plan_y = dev.fft_plan(py, device)
         # register-FFT path (square power-of-two pads) consumes Uhat transposed
@@ -174,22 +180,36 @@ class Propagator:
     def run_frequency(self, uhat_ptr: int, khat: float, ill_ptr: int, frame_w_ptr: int,
                       n_frames: int, vol: torch.Tensor, vol_frame_stride: int,
                       plane_lo: int = 0, plane_hi: int | None = None, stream=None,
-                      uhat_ptr_for_batch=None) -> None:
+                      uhat_ptr_for_batch=None, lane: int = 0) -> None:
         plane_hi = self.nplanes if plane_hi is None else plane_hi
         s = dev.stream_ptr(stream)
         gref = ctypes.byref(self.geom)
         base = dev.ptr(self.planes_dev)
+        wa, wb = dev.ptr(self.ws_a_l[lane]), dev.ptr(self.ws_b_l[lane])
         for b0 in range(plane_lo, plane_hi, self.batch):
             nb = min(self.batch, plane_hi - b0)
             pp = base + b0 * self.plane_size
             up = uhat_ptr if uhat_ptr_for_batch is None else uhat_ptr_for_batch(b0, nb)
-            _lib.call("pf_prop_kernel_rows", pp, nb, khat, gref, self.plan_x.ref,
-                      dev.ptr(self.ws_a), s)
-            _lib.call("pf_prop_columns", pp, nb, gref, self.plan_y.ref, dev.ptr(self.ws_a), up,
-                      dev.ptr(self.ws_b), 0, s)
-            _lib.call("pf_prop_rows_out", pp, nb, khat, gref, self.plan_x.ref,
-                      dev.ptr(self.ws_b), ill_ptr, frame_w_ptr, n_frames, dev.ptr(vol),
-                      vol_frame_stride, s)
+            _lib.call("pf_prop_kernel_rows", pp, nb, khat, gref, self.plan_x.ref, wa, s)
+            _lib.call("pf_prop_columns", pp, nb, gref, self.plan_y.ref, wa, up, wb, 0, s)
+            _lib.call("pf_prop_rows_out", pp, nb, khat, gref, self.plan_x.ref, wb, ill_ptr,
+                      frame_w_ptr, n_frames, dev.ptr(vol), vol_frame_stride, s)
+
+    def run_batches(self, body, stream=None) -> None:
+        """Call ``body(b0, b1, lane, lane_stream)`` for every plane batch, alternating lanes.
+
+        Lanes wait for ``stream`` (inputs ready) and ``stream`` waits for every lane.
+        """
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        for ls in self.lane_streams:
+            ls.wait_stream(main)
+        for i, b0 in enumerate(range(0, self.nplanes, self.batch)):
+            lane = i % len(self.lane_streams)
+            ls = self.lane_streams[lane]
+            with torch.cuda.stream(ls):
+                body(b0, min(self.nplanes, b0 + self.batch), lane, ls)
+        for ls in self.lane_streams:
+            main.wait_stream(ls)
 
 
 def _frame_weights(freqs: np.ndarray, times, device) -> torch.Tensor:
@@ -297,16 +317,18 @@ class RsdEngine:
             vol.zero_()
         uhat = self.relay_spectra(coeff, stream)
         per_f = self.n_illum * self.py * self.px
+
         # plane batches outer, frequencies inner: the batch's volume slice stays
         # L2-resident across its ascending-frequency accumulation
-        for b0 in range(0, self.prop.nplanes, self.prop.batch):
-            b1 = min(self.prop.nplanes, b0 + self.prop.batch)
+        def body(b0, b1, lane, ls):
             for fi in range(self.freqs.size):
                 khat = float(self.freqs[fi]) / SPEED_OF_LIGHT
                 self.prop.run_frequency(dev.ptr(uhat) + 8 * fi * per_f, khat, dev.ptr(self.ill),
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
-                                        plane_hi=b1, stream=stream)
+                                        plane_hi=b1, stream=ls, lane=lane)
+
+        self.prop.run_batches(body, stream)
         return vol
 
 
