@@ -15,6 +15,8 @@
 //       sum illuminations, accumulate frames into the volume.
 // Uhat is consumed TRANSPOSED (Uhat^T[col][jy]) on this path; the host asks
 // pf_prop_fast() before building it.
+#include <stdlib.h>
+
 #include "warp_fft.cuh"
 
 namespace {
@@ -235,6 +237,189 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
   }
 }
 
+// ---- persistent variants: one CTA per SM loops over work items and prefetches
+// the next item's inputs with cp.async while it computes the current one.
+
+// B, persistent: item = (kx, group of 8*LPW planes).  Stage buffers hold the
+// group's At rows and the Uhat^T columns kx, P-kx of every illumination.
+template <int L>
+__global__ void __launch_bounds__(FT, 1)
+k_pbp(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
+      const float2* __restrict__ tw, const float2* __restrict__ ws_a,
+      const float2* __restrict__ uhat_t, float2* __restrict__ ws_b, int n_items) {
+  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
+  constexpr int LPW = 32 / L, PPC = 8 * LPW;
+  extern __shared__ float2 sm[];
+  const int I = g.n_illum;
+  float2* xchb = sm;                                   // [8][WFFT_XCH]
+  float2* abuf = sm + 8 * WFFT_XCH;                    // [2][PPC][NA]
+  float2* ubuf = abuf + 2 * PPC * NA;                  // [2][2][I][P]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int lidx = warp * LPW + line;
+  const int ny = g.ny;
+  auto issue = [&](int item, int stage) {
+    const int kx = item % NA, grp = item / NA;
+    float2* ab = abuf + stage * PPC * NA;
+    for (int e = threadIdx.x; e < PPC * NA; e += FT) {
+      const int li = e / NA, jy = e - li * NA;
+      const int b = min(grp * PPC + li, nplanes - 1);
+      cp_async8(ab + e, ws_a + ((long long)b * NA + kx) * NA + jy);
+    }
+    const pf_plane& pl = planes[min(grp * PPC, nplanes - 1)];
+    float2* ub = ubuf + stage * 2 * I * P;
+    for (int e = threadIdx.x; e < 2 * I * P; e += FT) {
+      const int side = e / (I * P), rem = e - side * I * P, p = rem / P, jy = rem - p * P;
+      const int col = side == 0 ? kx : (P - kx) % P;
+      cp_async8(ub + e, uhat_t + pl.uhat_off + (long long)p * g.uhat_illum_stride +
+                            (long long)col * P + jy);
+    }
+    cp_async_commit();
+  };
+  int it = blockIdx.x;
+  if (it < n_items) issue(it, 0);
+  for (int k = 0; it < n_items; it += gridDim.x, k++) {
+    const int stage = k & 1;
+    cp_async_wait_all();
+    __syncthreads();
+    if (it + (int)gridDim.x < n_items) issue(it + gridDim.x, stage ^ 1);
+    const int kx = it % NA, grp = it / NA;
+    const int b = grp * PPC + lidx;
+    const bool active = b < nplanes;
+    const int bb = active ? b : nplanes - 1;
+    const float2* arow = abuf + stage * PPC * NA + lidx * NA;
+    float2 gh[32];
+#pragma unroll
+    for (int m = 0; m < 32; m++) {
+      const int jy = t + L * m;
+      gh[m] = arow[jy <= H ? jy : P - jy];
+    }
+    float2* xch = xchb + warp * WFFT_XCH;
+    wfft<L, -1>(gh, xch, tw);
+    const float2* ub = ubuf + stage * 2 * I * P;
+    for (int p = 0; p < I; p++) {
+      float2* outp = ws_b + ((long long)bb * I + p) * (long long)P * ny;
+#pragma unroll 1
+      for (int side = 0; side < 2; side++) {
+        const int col = side == 0 ? kx : (P - kx) % P;
+        if (side == 1 && col == kx) break;
+        const float2* ucol = ub + (side * I + p) * P;
+        float2 w[32];
+#pragma unroll
+        for (int m = 0; m < 32; m++) w[m] = cmul(gh[m], ucol[t + L * m]);
+        wfft<L, 1>(w, xch, tw);
+        if (active) {
+          float2* dcol = outp + (long long)col * ny;
+#pragma unroll
+          for (int m = 0; m < 32; m++) {
+            const int i = (t + L * m - g.nu0y) & (P - 1);
+            if (i < ny) dcol[i] = w[m];
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// C, persistent: item = (plane, tile of RPC output rows); the next item's
+// transposed tile streams into the other stage while this one is transformed.
+template <int L, bool MULTI>
+__global__ void __launch_bounds__(FT, 1)
+k_pcp(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
+      const float2* __restrict__ tw, const float2* __restrict__ ws_b,
+      const double* __restrict__ ill, const float2* __restrict__ frame_w, int n_frames,
+      float2* __restrict__ vol, long long vol_frame_stride, int n_items) {
+  constexpr int P = 32 * L;
+  constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
+  constexpr int TILE = P * SLD;
+  extern __shared__ float2 sm[];
+  float2* xchb = sm;                          // [8][WFFT_XCH]
+  float2* tiles = sm + 8 * WFFT_XCH;          // [2 * I][TILE]
+  const int I = MULTI ? g.n_illum : 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int r = warp * LPW + line;
+  const int ny = g.ny, nx = g.nx;
+  const int tiles_per_plane = (ny + RPC - 1) / RPC;
+  const float scale = 1.0f / ((float)P * (float)P);
+  auto issue = [&](int item, int stage) {
+    const int pb = item / tiles_per_plane, i0 = (item % tiles_per_plane) * RPC;
+    const int nr = min(RPC, ny - i0);
+    for (int p = 0; p < I; p++) {
+      const float2* src = ws_b + ((long long)pb * g.n_illum + p) * (long long)P * ny + i0;
+      float2* dst = tiles + (stage * I + p) * TILE;
+      for (int e = threadIdx.x; e < P * RPC; e += FT) {
+        const int col = e / RPC, rr = e % RPC;
+        if (rr < nr) cp_async8(dst + col * SLD + rr, src + (long long)col * ny + rr);
+      }
+    }
+    cp_async_commit();
+  };
+  int it = blockIdx.x;
+  if (it < n_items) issue(it, 0);
+  for (int k = 0; it < n_items; it += gridDim.x, k++) {
+    const int stage = k & 1;
+    cp_async_wait_all();
+    __syncthreads();
+    if (it + (int)gridDim.x < n_items) issue(it + gridDim.x, stage ^ 1);
+    const int pb = it / tiles_per_plane, i0 = (it % tiles_per_plane) * RPC;
+    const int i = i0 + r;
+    const pf_plane pl = planes[pb];
+    const double yv = pl.y0 + pl.dy * i;
+    const long long off = (pl.vol_plane * ny + i) * (long long)nx;
+    float2 acc[32];
+#pragma unroll 1
+    for (int p = 0; p < I; p++) {
+      float2 v[32];
+      const float2* tl = tiles + (stage * I + p) * TILE;
+#pragma unroll
+      for (int m = 0; m < 32; m++) v[m] = tl[(t + L * m) * SLD + r];
+      wfft<L, 1>(v, xchb + warp * WFFT_XCH, tw);
+      const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
+      const double dy = yv - sy, dz = pl.z - sz;
+      const double byz = fma(dy, dy, dz * dz);
+#pragma unroll
+      for (int m = 0; m < 32; m++) {
+        const int mo = (t + L * m - g.nu0x) & (P - 1);
+        float2 val = cscale(v[m], scale);
+        if (g.include_illum) {
+          const double dx = pl.x0 + pl.dx * mo - sx;
+          val = cmul(val, phase_turns(fma(dx, dx, byz), kturns));
+        }
+        acc[m] = p == 0 ? val : cadd(acc[m], val);
+      }
+    }
+    if (i < ny) {
+      for (int fr = 0; fr < n_frames; fr++) {
+        const float2 fw = frame_w[fr];
+        float2* drow = vol + fr * vol_frame_stride + off;
+        float2 old[32];
+#pragma unroll
+        for (int m = 0; m < 32; m++) {
+          const int mo = (t + L * m - g.nu0x) & (P - 1);
+          old[m] = mo < nx ? drow[mo] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int m = 0; m < 32; m++) {
+          const int mo = (t + L * m - g.nu0x) & (P - 1);
+          if (mo < nx) drow[mo] = cadd(old[m], cmul(acc[m], fw));
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+static int pf_persist_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PF_PERSIST");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
 template <int L>
 size_t smem_a() {
   constexpr int P = 32 * L, NA = P / 2 + 1, RPC = 8 * (32 / L);
@@ -246,6 +431,16 @@ size_t smem_c(int nx, bool pre) {
   constexpr int P = 32 * L, RPC = 8 * (32 / L);
   size_t x = 8 * WFFT_XCH, s = (size_t)P * (RPC + 1);
   return ((x > s ? x : s) + (pre ? (size_t)RPC * nx : 0)) * sizeof(float2);
+}
+
+int nsm() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
 }
 
 template <int L>
@@ -269,11 +464,45 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     dim3 grid(pf_cdiv(NA, RPC), nplanes);
     k_pa<L><<<grid, FT, smem_a<L>(), st>>>(planes, kturns, g, tw, ws_a_out);
     PF_LAUNCH_CHECK("k_pa");
+  } else if (stage == 1 && pf_persist_env()) {
+    const int I = g.n_illum;
+    const size_t sm = (8 * WFFT_XCH + 2 * (size_t)8 * LPW * NA + 4 * (size_t)I * P) * sizeof(float2);
+    const int items = NA * pf_cdiv(nplanes, 8 * LPW);
+    if (sm <= 220 * 1024) {
+      static bool a2 = false;
+      if (!a2) { cudaFuncSetAttribute(k_pbp<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); a2 = true; }
+      k_pbp<L><<<items < nsm() ? items : nsm(), FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat,
+                                                               ws_b_out, items);
+      PF_LAUNCH_CHECK("k_pbp");
+      return 0;
+    }
+    dim3 grid(NA, pf_cdiv(nplanes, 8 * LPW));
+    k_pb<L><<<grid, FT, 8 * WFFT_XCH * sizeof(float2), st>>>(planes, nplanes, g, tw, ws_a, uhat,
+                                                             ws_b_out);
+    PF_LAUNCH_CHECK("k_pb");
   } else if (stage == 1) {
     dim3 grid(NA, pf_cdiv(nplanes, 8 * LPW));
     k_pb<L><<<grid, FT, 8 * WFFT_XCH * sizeof(float2), st>>>(planes, nplanes, g, tw, ws_a, uhat,
                                                              ws_b_out);
     PF_LAUNCH_CHECK("k_pb");
+  } else if (pf_persist_env() &&
+             (8 * WFFT_XCH + 2 * (size_t)g.n_illum * P * (RPC + 1)) * sizeof(float2) <= 220 * 1024) {
+    const size_t sm = (8 * WFFT_XCH + 2 * (size_t)g.n_illum * P * (RPC + 1)) * sizeof(float2);
+    const int items = pf_cdiv(g.ny, RPC) * nplanes;
+    const int grid = items < nsm() ? items : nsm();
+    static bool a3 = false;
+    if (!a3) {
+      cudaFuncSetAttribute(k_pcp<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(k_pcp<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      a3 = true;
+    }
+    if (g.n_illum > 1)
+      k_pcp<L, true><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames,
+                                           vol, vfs, items);
+    else
+      k_pcp<L, false><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames,
+                                            vol, vfs, items);
+    PF_LAUNCH_CHECK("k_pcp");
   } else {
     dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
     const bool pre = n_frames == 1 && frame_w != nullptr && (size_t)RPC * g.nx * 8 <= 64 * 1024;
