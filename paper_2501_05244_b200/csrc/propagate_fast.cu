@@ -23,29 +23,34 @@ namespace {
 
 constexpr int FT = 256;  // 8 warps
 
-// exp(1j * 2 pi * kturns * r) / r with r = sqrt(r2): float sqrt + one float64
-// Newton correction, phase reduced in turns (float64) -- ~10 DP ops, no DP sqrt.
-__device__ __forceinline__ float2 g_kernel(double r2, double kturns) {
-  const float rf = sqrtf((float)r2);
-  const double e = fma(-(double)rf, (double)rf, r2);
-  const float d = (float)e * (0.5f / rf);
-  const double turns = fma(kturns, (double)rf, kturns * (double)d);
-  const float fr = (float)(turns - rint(turns));
-  float s, c;
-  __sincosf(6.28318530717958647692f * fr, &s, &c);
-  const float ir = 1.0f / rf;
-  return make_float2(c * ir, s * ir);
-}
-
-__device__ __forceinline__ float2 phase_turns(double r2, double kturns) {
-  const float rf = sqrtf((float)r2);
-  const double e = fma(-(double)rf, (double)rf, r2);
-  const float d = (float)e * (0.5f / rf);
-  const double turns = fma(kturns, (double)rf, kturns * (double)d);
-  const float fr = (float)(turns - rint(turns));
+// exp(1j * 2 pi * kturns * r) / r with r = sqrt(r2): float rsqrt + one float64
+// Newton correction (r = rf + (r2 - rf^2) / (2 rf), error ~ (eps_f)^2 r), phase
+// reduced in turns with the large part in float64 and the tiny correction in
+// float32 -- no float64 square root or division.
+__device__ __forceinline__ float2 turns_to_unit(double t_hi, float t_lo) {
+  const float fr = (float)(t_hi - rint(t_hi)) + t_lo;
   float s, c;
   __sincosf(6.28318530717958647692f * fr, &s, &c);
   return make_float2(c, s);
+}
+
+__device__ __forceinline__ float2 g_kernel(double r2, double kturns, float kturns_f) {
+  const float r2f = (float)r2;
+  const float ir = rsqrtf(r2f);
+  const float rf = r2f * ir;
+  const float e = (float)fma(-(double)rf, (double)rf, r2);
+  const float d = 0.5f * e * ir;
+  const float2 u = turns_to_unit(kturns * (double)rf, kturns_f * d);
+  const float inv = ir * (1.0f - d * ir);   // 1/(rf + d) to first order
+  return make_float2(u.x * inv, u.y * inv);
+}
+
+__device__ __forceinline__ float2 phase_turns(double r2, double kturns, float kturns_f) {
+  const float r2f = (float)r2;
+  const float ir = rsqrtf(r2f);
+  const float rf = r2f * ir;
+  const float e = (float)fma(-(double)rf, (double)rf, r2);
+  return turns_to_unit(kturns * (double)rf, kturns_f * (0.5f * e * ir));
 }
 
 template <int L>
@@ -70,7 +75,7 @@ k_pa(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
 #pragma unroll
   for (int m = 0; m <= 16; m++) {
     const double lx = (double)centred(t + L * m, P) * pl.lag_dx;
-    v[m] = g_kernel(fma(lx, lx, base), kturns);
+    v[m] = g_kernel(fma(lx, lx, base), kturns, (float)kturns);
   }
   const int mirror = (lane - t) + ((L - t) & (L - 1));
 #pragma unroll
@@ -120,7 +125,7 @@ k_pb(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
     gh[m] = __ldg(arow + (jy <= H ? jy : P - jy));
   }
   float2* xch = sm + warp * WFFT_XCH;
-  wfft<L, -1>(gh, xch, tw);
+  wfft<L, -1, true>(gh, xch, tw);
   const int ny = g.ny;
   for (int p = 0; p < g.n_illum; p++) {
     const float2* up = uhat_t + pl.uhat_off + (long long)p * g.uhat_illum_stride;
@@ -133,7 +138,7 @@ k_pb(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
       float2 w[32];
 #pragma unroll
       for (int m = 0; m < 32; m++) w[m] = cmul(gh[m], __ldg(ucol + t + L * m));
-      wfft<L, 1>(w, xch, tw);
+      wfft<L, 1, true>(w, xch, tw);
       if (active) {
         float2* dcol = outp + (long long)col * ny;
 #pragma unroll
@@ -202,9 +207,9 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
     for (int m = 0; m < 32; m++) {
       const int mo = (t + L * m - g.nu0x) & (P - 1);
       float2 val = cscale(v[m], scale);
-      if (g.include_illum) {
+      if (g.include_illum && mo < nx) {   // cropped-away columns need no phase
         const double dx = pl.x0 + pl.dx * mo - sx;
-        val = cmul(val, phase_turns(fma(dx, dx, byz), kturns));
+        val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
       }
       if (MULTI) {
         if (p == 0) acc[m] = val; else acc[m] = cadd(acc[m], val);
@@ -385,7 +390,7 @@ k_pcp(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
         float2 val = cscale(v[m], scale);
         if (g.include_illum) {
           const double dx = pl.x0 + pl.dx * mo - sx;
-          val = cmul(val, phase_turns(fma(dx, dx, byz), kturns));
+          val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
         }
         acc[m] = p == 0 ? val : cadd(acc[m], val);
       }
@@ -415,7 +420,7 @@ static int pf_persist_env() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PF_PERSIST");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;   // off by default: slower on B200
   }
   return v;
 }

@@ -18,18 +18,29 @@
 
 constexpr int WFFT_XCH = 32 * 33;  // float2 per warp exchange buffer
 
-template <int L, int DIR>
+// EARLY: issue the 31 twiddle loads before the first 32-point DFT so their
+// latency hides behind it (costs 62 registers; for kernels with headroom).
+template <int L, int DIR, bool EARLY = false>
 __device__ __forceinline__ void wfft(float2 (&v)[32], float2* __restrict__ xch,
                                      const float2* __restrict__ tw) {
   static_assert(L == 4 || L == 8 || L == 16 || L == 32, "L must be 4, 8, 16 or 32");
   const int lane = threadIdx.x & 31;
   const int t = lane % L;
-  Dft<32, DIR>::run(v);
-  if (t != 0) {
+  if (EARLY) {
+    float2 w[32];
 #pragma unroll
-    for (int k1 = 1; k1 < 32; k1++) {
-      const float2 w = __ldg(tw + t * k1);
-      v[k1] = DIR < 0 ? cmul(v[k1], w) : cmulc(v[k1], w);
+    for (int k1 = 1; k1 < 32; k1++) w[k1] = __ldg(tw + t * k1);
+    Dft<32, DIR>::run(v);
+#pragma unroll
+    for (int k1 = 1; k1 < 32; k1++) v[k1] = DIR < 0 ? cmul(v[k1], w[k1]) : cmulc(v[k1], w[k1]);
+  } else {
+    Dft<32, DIR>::run(v);
+    if (t != 0) {
+#pragma unroll
+      for (int k1 = 1; k1 < 32; k1++) {
+        const float2 w = __ldg(tw + t * k1);
+        v[k1] = DIR < 0 ? cmul(v[k1], w) : cmulc(v[k1], w);
+      }
     }
   }
   float2* row = xch + lane * 33;  // (line, t) row: line*L*33 + t*33
