@@ -242,6 +242,89 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
   }
 }
 
+// ---- B split in two register-light kernels (128 registers, 16 warps/SM):
+// B1: in place on ws_a, each line = one At row (plane b, kx): mirror, y-FFT,
+//     keep ky <= P/2  ->  Ghat quadrant Gq[b][kx][ky] (Ghat is even in ky too).
+// B2: line = (plane b, side): Gq row (mirrored) * Uhat^T column, y-IFFT, crop.
+template <int L>
+__global__ void __launch_bounds__(FT, 2)
+k_pb1(int nplanes, const float2* __restrict__ tw, float2* __restrict__ ws_a) {
+  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
+  constexpr int LPW = 32 / L;
+  extern __shared__ float2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int row = (blockIdx.x * 8 + warp) * LPW + line;     // kx
+  const int b = blockIdx.y;
+  const bool active = row < NA;
+  float2* arow = ws_a + ((long long)b * NA + (active ? row : 0)) * NA;
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 32; m++) {
+    const int jy = t + L * m;
+    v[m] = arow[jy <= H ? jy : P - jy];
+  }
+  wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
+  if (active) {
+#pragma unroll
+    for (int m = 0; m <= 16; m++) {   // ky = t + L m <= P/2 for m < 16 (and m = 16, t = 0)
+      const int ky = t + L * m;
+      if (ky <= H) arow[ky] = v[m];
+    }
+  }
+}
+
+template <int L, bool MULTI>
+__global__ void __launch_bounds__(FT, 2)
+k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
+      const float2* __restrict__ tw, const float2* __restrict__ ws_a,
+      const float2* __restrict__ uhat_t, float2* __restrict__ ws_b) {
+  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
+  constexpr int LPW = 32 / L;
+  extern __shared__ float2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int kx = blockIdx.x;
+  const int li = (blockIdx.y * 8 + warp) * LPW + line;
+  const int b = li >> 1, side = li & 1;
+  const int col = side == 0 ? kx : (P - kx) % P;
+  const bool active = b < nplanes && !(side == 1 && col == kx);
+  const int bb = b < nplanes ? b : nplanes - 1;
+  const pf_plane pl = planes[bb];
+  const float2* grow = ws_a + ((long long)bb * NA + kx) * NA;
+  const int ny = g.ny;
+  const int n_ill = MULTI ? g.n_illum : 1;
+#pragma unroll 1
+  for (int p = 0; p < n_ill; p++) {
+    const float2* ucol = uhat_t + pl.uhat_off + (long long)p * g.uhat_illum_stride +
+                         (long long)col * P;
+    float2 w[32];
+#pragma unroll
+    for (int m = 0; m < 32; m++) {
+      const int ky = t + L * m;
+      w[m] = cmul(__ldg(grow + (ky <= H ? ky : P - ky)), __ldg(ucol + ky));
+    }
+    wfft<L, 1>(w, sm + warp * WFFT_XCH, tw);
+    if (active) {
+      float2* dcol = ws_b + ((long long)bb * g.n_illum + p) * (long long)P * ny + (long long)col * ny;
+#pragma unroll
+      for (int m = 0; m < 32; m++) {
+        const int i = (t + L * m - g.nu0y) & (P - 1);
+        if (i < ny) dcol[i] = w[m];
+      }
+    }
+  }
+}
+
+static int pf_splitb_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PF_SPLITB");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
 // ---- persistent variants: one CTA per SM loops over work items and prefetches
 // the next item's inputs with cp.async while it computes the current one.
 
@@ -469,6 +552,24 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     dim3 grid(pf_cdiv(NA, RPC), nplanes);
     k_pa<L><<<grid, FT, smem_a<L>(), st>>>(planes, kturns, g, tw, ws_a_out);
     PF_LAUNCH_CHECK("k_pa");
+  } else if (stage == 1 && pf_splitb_env()) {
+    static bool a4 = false;
+    if (!a4) {
+      cudaFuncSetAttribute(k_pb1<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_pb2<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_pb2<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      a4 = true;
+    }
+    const size_t sm = 8 * WFFT_XCH * sizeof(float2);
+    dim3 g1(pf_cdiv(NA, 8 * LPW), nplanes);
+    k_pb1<L><<<g1, FT, sm, st>>>(nplanes, tw, const_cast<float2*>(ws_a));
+    PF_LAUNCH_CHECK("k_pb1");
+    dim3 g2(NA, pf_cdiv(2 * nplanes, 8 * LPW));
+    if (g.n_illum > 1)
+      k_pb2<L, true><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out);
+    else
+      k_pb2<L, false><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out);
+    PF_LAUNCH_CHECK("k_pb2");
   } else if (stage == 1 && pf_persist_env()) {
     const int I = g.n_illum;
     const size_t sm = (8 * WFFT_XCH + 2 * (size_t)8 * LPW * NA + 4 * (size_t)I * P) * sizeof(float2);
