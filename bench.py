@@ -126,13 +126,13 @@ def run_ours(args):
     hist = configs.transients(cfg, device=device)            # [1, D, T] float32, identical per rank
     I, D, T = hist.shape
     F = kernel.n_freq
-    nz = cfg.grid.grid.nz
+    nz = cfg.grid.n_planes if cfg.grid.kind == "frustum" else cfg.grid.grid.nz
     d_lo, d_hi = shard_range(D, world, rank)
     k_lo, k_hi = shard_range(nz, world, rank)
     hist_shard = hist[:, d_lo:d_hi].contiguous()
     del hist
     torch.cuda.empty_cache()
-    plane_vox = cfg.grid.grid.nx * cfg.grid.grid.ny
+    plane_vox = cfg.n_voxels // nz
     sgather = vgather = None
     if world > 1:
         sgather = SliceGather(F, I, D, world, device)
@@ -140,7 +140,7 @@ def run_ours(args):
     rec = TransientReconstructor(kernel, cfg.relay, cfg.illuminations, cfg.grid, t0=cfg.t0,
                                  plane_range=(k_lo, k_hi), device=device,
                                  trace_range=(d_lo, d_hi), slice_gather=sgather,
-                                 volume_gather=vgather)
+                                 volume_gather=vgather, algorithm=cfg.algorithm)
     eng = rec.engine
     local_shard = rec.coeff
     stream = torch.cuda.current_stream()
@@ -220,6 +220,9 @@ def run_ours(args):
     P = eng.px
     units = F * (k_hi - k_lo) * I
     s3_flops = (2 * units + F * I) * 5.0 * P * P * math.log2(P * P)
+    if cfg.algorithm == "srsd":   # + per-unit Bluestein x (N rows) and y (P columns) passes
+        Q = 2 * P
+        s3_flops += units * (cfg.relay.grid.ny + P) * 2 * 5.0 * Q * math.log2(Q)
     fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
     clocks = clk.summary()
     roof_k1 = {"bound": "hbm", "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "peak": hbm_peak,
@@ -238,9 +241,10 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c64 (fp32 arithmetic, fp64 phases)",
-        "data": "synthetic (seeded GPU three-bounce renderer, Poisson noise; BASELINE config 4)",
-        "config": {"workload": f"config{args.config}-rsd", "relay": f"{cfg.relay.grid.nx}x"
-                   f"{cfg.relay.grid.ny}", "n_bins": T, "n_freq": F, "planes": nz,
+        "data": f"synthetic (seeded GPU three-bounce renderer, Poisson noise; BASELINE config "
+                f"{args.config})",
+        "config": {"workload": f"config{args.config}-{cfg.algorithm}", "relay": cfg.relay.count,
+                   "n_bins": T, "n_freq": F, "planes": nz,
                    "voxels": cfg.n_voxels, "pad": P, "parallelism": f"planes+detectors x{world}",
                    "l2": "inputs (4.3 GB transients) exceed the 126 MB L2; no flush needed",
                    "timed": "K1 + slice gather + propagation + volume gather"},
@@ -293,7 +297,8 @@ def _cpu_units(cfg, n_f, n_k):
 def cpu_baseline_sample(cfg, kernel, hist_dev, rec, args):
     from oracle import pf_oracle as O
 
-    F, nz = kernel.n_freq, cfg.grid.grid.nz
+    F = kernel.n_freq
+    nz = cfg.grid.n_planes if cfg.grid.kind == "frustum" else cfg.grid.grid.nz
     n_tr = 4096
     h = hist_dev.view(-1, cfg.n_bins)[:n_tr].cpu().numpy().astype(np.float64)
     t = time.perf_counter()
@@ -301,14 +306,26 @@ def cpu_baseline_sample(cfg, kernel, hist_dev, rec, args):
     t1 = (time.perf_counter() - t) * (hist_dev.shape[1] / n_tr)
     coeff = rec.coeff.permute(1, 2, 0).cpu().numpy().astype(np.complex128)
     sl = _HostSlices(kernel.frequencies, coeff, cfg.relay, cfg.illuminations)
-    n_f, n_k = 2, 8
-    t = time.perf_counter()
-    O.rsd(sl, cfg.grid, freq_range=(0, n_f), plane_range=(0, n_k))
-    t3 = (time.perf_counter() - t) * (F * nz) / (n_f * n_k)
+    fn = {"rsd": O.rsd, "srsd": O.srsd, "nursd1": O.nursd1}[cfg.algorithm]
+    # per-frequency setup (relay spectrum / NUFFT) and per-plane cost separated by
+    # timing 1 and 3 planes per frequency, then extrapolated to F x Nz
+    n_f = 2
+    per_f, per_k = [], []
+    for f in range(n_f):
+        t = time.perf_counter()
+        fn(sl, cfg.grid, freq_range=(f, f + 1), plane_range=(0, 1))
+        a = time.perf_counter() - t
+        t = time.perf_counter()
+        fn(sl, cfg.grid, freq_range=(f, f + 1), plane_range=(0, 3))
+        b = time.perf_counter() - t
+        per_k.append(max(b - a, 1e-9) / 2)
+        per_f.append(max(a - per_k[-1], 0.0))
+    t3 = F * (statistics.mean(per_f) + nz * statistics.mean(per_k))
+    n_k = 3
     return {"value": cfg.n_voxels / (t1 + t3), "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"oracle.to_frequency on {n_tr} of {hist_dev.shape[1]} traces + oracle.rsd "
-                      f"(reference P=1050) on {n_f} freqs x {n_k} planes of {F}x{nz}; "
-                      "linear extrapolation per trace / per (f,k) unit",
+            "sample": f"oracle.to_frequency on {n_tr} of {hist_dev.shape[1]} traces + oracle."
+                      f"{cfg.algorithm} (reference pads) on {n_f} freqs x (1 and 3) planes of "
+                      f"{F}x{nz}; per-trace and per-frequency + per-plane linear extrapolation",
             "s1_s": t1, "s3_s": t3}
 
 
@@ -325,12 +342,19 @@ _REF_STATE = {}
 
 
 def _ref_unit(unit):
-    """Worker: oracle rsd on one (frequency, plane-range) block; returns seconds."""
+    """Worker: oracle on 1 and 3 planes of one frequency -> (per-frequency, per-plane) seconds."""
     from oracle import pf_oracle as O
-    f, k0, k1 = unit
+    f, k0 = unit
+    fn = {"rsd": O.rsd, "srsd": O.srsd, "nursd1": O.nursd1}[_REF_STATE["alg"]]
+    sl, grid = _REF_STATE["slices"], _REF_STATE["grid"]
     t = time.perf_counter()
-    O.rsd(_REF_STATE["slices"], _REF_STATE["grid"], freq_range=(f, f + 1), plane_range=(k0, k1))
-    return time.perf_counter() - t
+    fn(sl, grid, freq_range=(f, f + 1), plane_range=(k0, k0 + 1))
+    a = time.perf_counter() - t
+    t = time.perf_counter()
+    fn(sl, grid, freq_range=(f, f + 1), plane_range=(k0, k0 + 3))
+    b = time.perf_counter() - t
+    per_k = max(b - a, 1e-9) / 2
+    return max(a - per_k, 0.0), per_k
 
 
 def run_reference(args):
@@ -345,7 +369,8 @@ def run_reference(args):
 
     cfg = configs.config(args.config)
     kernel = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
-    F, nz = kernel.n_freq, cfg.grid.grid.nz
+    F = kernel.n_freq
+    nz = cfg.grid.n_planes if cfg.grid.kind == "frustum" else cfg.grid.grid.nz
     D = cfg.relay.count
     rng = np.random.default_rng(cfg.seed)
     # S3 cost is data-independent FFT work: seeded random-phase coefficients stand in
@@ -354,22 +379,24 @@ def run_reference(args):
     ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     n_tr = 2048
     h = rng.poisson(2.0, size=(n_tr, cfg.n_bins)).astype(np.float64)
-    units = [(i % F, (2 * i) % nz, (2 * i) % nz + 2) for i in range(ncores)]
-    _REF_STATE["slices"], _REF_STATE["grid"] = sl, cfg.grid
+    units = [(i % F, (3 * i) % max(1, nz - 3)) for i in range(ncores)]
+    _REF_STATE["slices"], _REF_STATE["grid"], _REF_STATE["alg"] = sl, cfg.grid, cfg.algorithm
     ctx = mp.get_context("fork")
     times = []
     with ctx.Pool(ncores) as pool:
         for it in range(args.warmup + args.steps):
             t = time.perf_counter()
-            pool.map(_ref_unit, units)
+            res = pool.map(_ref_unit, units)
             t_par = time.perf_counter() - t
+            per_f = statistics.mean(r[0] for r in res)
+            per_k = statistics.mean(r[1] for r in res)
+            # ncores processes share the F x Nz units; each step's sample is 4 planes per process
+            serial = F * (per_f + nz * per_k)
             t = time.perf_counter()
             O.to_frequency(h, kernel.bin_indices, kernel.frequencies, kernel.weights, cfg.t0)
             t_s1 = (time.perf_counter() - t) * D / n_tr / ncores
             if it >= args.warmup:
-                sample_units = len(units) * 2
-                est = t_par * (F * nz) / sample_units + t_s1
-                times.append(est)
+                times.append(serial / ncores + t_s1)
     est = statistics.mean(times)
     value = cfg.n_voxels / est
     print(json.dumps({
@@ -377,11 +404,11 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "c128 (float64)", "data": "synthetic (seeded random-phase slices, Poisson hist)",
-        "config": {"workload": f"config{args.config}-rsd", "voxels": cfg.n_voxels,
-                   "pad": "reference 1050"},
+        "config": {"workload": f"config{args.config}-{cfg.algorithm}", "voxels": cfg.n_voxels,
+                   "pad": "reference pad rule"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
-                         "sample": f"per step: {len(units)} processes x (1 freq x 2 planes) of "
-                                   f"oracle.rsd + to_frequency on {n_tr} traces, extrapolated to "
+                         "sample": f"per step: {len(units)} processes x (1 freq x 1+3 planes) of "
+                                   f"oracle.{cfg.algorithm} + to_frequency on {n_tr} traces, extrapolated to "
                                    f"{F}x{nz} units and {D} traces"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)

@@ -30,8 +30,25 @@ class _Meta:
         self.n_freq = int(self.frequencies.size)
 
 
+def make_engine(algorithm, meta, grid, device, plane_range=None, times=None,
+                include_illumination=True, padding="exact", eps=1e-6):
+    """Device engine (``run(coeff, vol, stream)``) for a cuboid/frustum algorithm."""
+    name = algorithm.replace("_", "-").lower()
+    if name == "rsd":
+        return RsdEngine(meta, grid, padding, include_illumination, times, device=device,
+                         plane_range=plane_range)
+    from .algorithms import Nursd1Engine, SrsdEngine
+    if name == "srsd":
+        return SrsdEngine(meta, grid, include_illumination, times, device=device,
+                          plane_range=plane_range)
+    if name == "nursd1":
+        return Nursd1Engine(meta, grid, eps, include_illumination, times, device=device,
+                            plane_range=plane_range)
+    raise ValueError(f"no streaming engine for {algorithm!r}")
+
+
 class TransientReconstructor:
-    """rsd from host histograms [I, D, T] (float32) to a host volume.
+    """rsd / srsd / nursd1 from host histograms [I, D, T] (float32) to a host volume.
 
     ``plane_range`` restricts the planes (multi-GPU sharding); ``trace_range``
     restricts the detectors this instance transforms (K1 sharding).
@@ -39,12 +56,14 @@ class TransientReconstructor:
 
     def __init__(self, kernel, relay, illuminations, grid, t0: float = 0.0, padding="exact",
                  include_illumination=True, times=None, plane_range=None, chunks: int = 8,
-                 device=None, trace_range=None, slice_gather=None, volume_gather=None):
+                 device=None, trace_range=None, slice_gather=None, volume_gather=None,
+                 algorithm="rsd", eps=1e-6):
         self.device = device or dev.require_cuda()
         self.kernel = kernel
+        self.grid = grid
         self.meta = _Meta(kernel, relay, illuminations)
-        self.engine = RsdEngine(self.meta, grid, padding, include_illumination, times,
-                                device=self.device, plane_range=plane_range)
+        self.engine = make_engine(algorithm, self.meta, grid, self.device, plane_range, times,
+                                  include_illumination, padding, eps)
         self.temporal = TemporalPlan(kernel, t0, self.device)
         self.n_illum = illuminations.count
         self.n_det = relay.count
@@ -81,7 +100,7 @@ class TransientReconstructor:
         if self._vol_host is None:
             shape = self.vol.shape
             if self.volume_gather is not None:
-                shape = (self.vol.shape[0], self.engine.grid.count)
+                shape = (self.vol.shape[0], self.grid.count)
             self._vol_host = torch.empty(shape, dtype=self.vol.dtype, pin_memory=True)
         src = hist_host.view(n_tr, t_n)
         dst = self._hist_dev.view(n_tr, t_n)
@@ -111,4 +130,4 @@ class TransientReconstructor:
     def volume(self, host_vol: torch.Tensor) -> ReconstructionVolume:
         field = host_vol.numpy().astype(np.complex128)
         times = self.engine.times
-        return ReconstructionVolume(self.engine.grid, field[0] if times is None else field, times)
+        return ReconstructionVolume(self.grid, field[0] if times is None else field, times)
