@@ -57,8 +57,15 @@ class FftPlan:
         self.n = int(n)
         rad = radices_for(self.n) if self.n > 1 else []
         m = np.arange(self.n, dtype=np.float64)
-        w = np.exp(-2j * np.pi * m / self.n).astype(np.complex64)
-        self.tw = torch.from_numpy(w).to(device)
+        w = np.exp(-2j * np.pi * m / self.n)
+        if self.n in (128, 256, 512, 1024):
+            # register-FFT twiddles laid out k1-major ([k1][t], n = 32 L) right after
+            # the unit-root table, so a warp's 32 lanes read one contiguous run
+            L = self.n // 32
+            k1 = np.arange(32)[:, None]
+            t = np.arange(L)[None, :]
+            w = np.concatenate([w, np.exp(-2j * np.pi * ((k1 * t) % self.n) / self.n).ravel()])
+        self.tw = torch.from_numpy(w.astype(np.complex64)).to(device)
         self.c = _lib.PfFftPlan()
         self.c.n = self.n
         self.c.nst = len(rad)

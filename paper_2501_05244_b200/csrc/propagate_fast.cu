@@ -96,9 +96,20 @@ k_pa(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
   __syncthreads();
   const int nr = min(RPC, NA - jy0);
   float2* dst = ws_a + (long long)blockIdx.y * NA * NA + jy0;
-  for (int e = threadIdx.x; e < NA * RPC; e += FT) {
-    const int kx = e / RPC, rr = e % RPC;   // compile-time divisor
-    if (rr < nr) dst[(long long)kx * NA + rr] = sm[kx * SLD + rr];
+  {
+    // thread -> (kx row within a group of FT/RPC rows, rr); stride FT/RPC rows per step
+    constexpr int KSTEP = FT / RPC;
+    const int rr = threadIdx.x % RPC, k0 = threadIdx.x / RPC;
+    if (rr < nr) {
+      float2* d = dst + (long long)k0 * NA + rr;
+      const float2* q = sm + k0 * SLD + rr;
+#pragma unroll 4
+      for (int kx = k0; kx < NA; kx += KSTEP) {
+        *d = *q;
+        d += (long long)KSTEP * NA;
+        q += KSTEP * SLD;
+      }
+    }
   }
 }
 
@@ -176,9 +187,11 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
   const float scale = 1.0f / ((float)P * (float)P);
   const long long vol_row0 = (pl.vol_plane * ny + i0) * (long long)nx;
   if (PRE) {
-    for (int rr = 0; rr < nr; rr++)
-      for (int mo = threadIdx.x; mo < nx; mo += FT)
-        cp_async8(volbuf + rr * nx + mo, vol + vol_row0 + (long long)rr * nx + mo);
+    for (int rr = 0; rr < nr; rr++) {
+      const float2* src = vol + vol_row0 + (long long)rr * nx;
+#pragma unroll 4
+      for (int mo = threadIdx.x; mo < nx; mo += FT) cp_async8(volbuf + rr * nx + mo, src + mo);
+    }
     cp_async_commit();
   }
   float2 acc[MULTI ? 32 : 1];
@@ -189,9 +202,19 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
   for (int p = 0; p < n_ill; p++) {
     const float2* src = ws_b + ((long long)blockIdx.y * g.n_illum + p) * (long long)P * ny + i0;
     if (p > 0) __syncthreads();
-    for (int e = threadIdx.x; e < P * RPC; e += FT) {
-      const int col = e / RPC, rr = e % RPC;
-      if (rr < nr) cp_async8(sm + col * SLD + rr, src + (long long)col * ny + rr);
+    {
+      constexpr int CSTEP = FT / RPC;
+      const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
+      if (rr < nr) {
+        const float2* q = src + (long long)c0 * ny + rr;
+        float2* d = sm + c0 * SLD + rr;
+#pragma unroll 8
+        for (int col = c0; col < P; col += CSTEP) {
+          cp_async8(d, q);
+          q += (long long)CSTEP * ny;
+          d += CSTEP * SLD;
+        }
+      }
     }
     cp_async_commit();
     cp_async_wait_all();

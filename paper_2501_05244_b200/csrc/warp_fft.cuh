@@ -18,18 +18,21 @@
 
 constexpr int WFFT_XCH = 32 * 33;  // float2 per warp exchange buffer
 
+// `tw` is the plan table: n unit roots followed by the k1-major twiddles
+// tw2[k1 * L + t] = W_n^{t k1} (one contiguous run per k1 across the lanes).
 // EARLY: issue the 31 twiddle loads before the first 32-point DFT so their
 // latency hides behind it (costs 62 registers; for kernels with headroom).
 template <int L, int DIR, bool EARLY = false>
 __device__ __forceinline__ void wfft(float2 (&v)[32], float2* __restrict__ xch,
-                                     const float2* __restrict__ tw) {
+                                     const float2* __restrict__ tw_plan) {
   static_assert(L == 4 || L == 8 || L == 16 || L == 32, "L must be 4, 8, 16 or 32");
   const int lane = threadIdx.x & 31;
   const int t = lane % L;
+  const float2* __restrict__ tw = tw_plan + 32 * L + t;
   if (EARLY) {
     float2 w[32];
 #pragma unroll
-    for (int k1 = 1; k1 < 32; k1++) w[k1] = __ldg(tw + t * k1);
+    for (int k1 = 1; k1 < 32; k1++) w[k1] = __ldg(tw + k1 * L);
     Dft<32, DIR>::run(v);
 #pragma unroll
     for (int k1 = 1; k1 < 32; k1++) v[k1] = DIR < 0 ? cmul(v[k1], w[k1]) : cmulc(v[k1], w[k1]);
@@ -38,7 +41,7 @@ __device__ __forceinline__ void wfft(float2 (&v)[32], float2* __restrict__ xch,
     if (t != 0) {
 #pragma unroll
       for (int k1 = 1; k1 < 32; k1++) {
-        const float2 w = __ldg(tw + t * k1);
+        const float2 w = __ldg(tw + k1 * L);
         v[k1] = DIR < 0 ? cmul(v[k1], w) : cmulc(v[k1], w);
       }
     }
