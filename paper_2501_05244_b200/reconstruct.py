@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -39,6 +40,8 @@ ALGORITHM_NAMES = ("rsd", "srsd", "nursd1", "nursd2", "nursd3", "rsd3d", "nursd3
 
 # workspace budget per propagation batch: keep ws_a + ws_b L2-resident (126 MB L2)
 _BATCH_BYTES = 64 << 20
+_LANES = int(os.environ.get("PF_LANES", "2"))
+_FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "8"))
 
 
 # ---------------------------------------------------------------------------
@@ -152,8 +155,8 @@ class Propagator:
         if batch is None:
             batch = max(1, min(self.nplanes, _BATCH_BYTES // per_plane))
             if fast_l:   # kernel B packs 8 warps x (32/L) lines of planes per CTA
-                q = 8 * (32 // fast_l)
-                batch = min(self.nplanes, max(q, (batch // q) * q))
+                q = 4 * (32 // fast_l)
+                batch = min(self.nplanes, max(q, (batch // q) * q), _FAST_BATCH_CAP * (32 // fast_l))
         self.batch = int(batch)
         arr = (_lib.PfPlane * self.nplanes)()
         for i, p in enumerate(planes):
@@ -165,7 +168,7 @@ class Propagator:
         # two independent lanes (workspace + stream): consecutive plane batches run
         # concurrently so the synthesis-bound kernel A of one batch overlaps the
         # load-bound kernels B/C of the other on the same SMs
-        nlanes = 2 if self.nplanes > self.batch else 1
+        nlanes = min(_LANES, -(-self.nplanes // self.batch))
         self.ws_a_l = [torch.empty(_lib.call("pf_prop_ws_a", ctypes.byref(g), self.batch),
                                    dtype=torch.complex64, device=device) for _ in range(nlanes)]
         self.ws_b_l = [torch.empty(_lib.call("pf_prop_ws_b", ctypes.byref(g), self.batch),
