@@ -152,6 +152,17 @@ int pf_bluestein_lines(const void* src, int64_t src_ps, int64_t src_ls, int64_t 
                        const pf_fft_plan* plan_q, const void* chirp, const void* khat,
                        void* stream);
 
+/* Register-FFT Bluestein pass for Q = plan_q->n in {128,256,512,1024} (plan_q->tw
+ * must carry the warp-FFT twiddle extension).  Lines are contiguous input rows
+ * (element i at src + b*src_ps + l*src_ls + i, slot o_in + i).  xpass=1 stores
+ * the pass TRANSPOSED with natural column order: dst[b*dst_ps + col*dst_ls + l];
+ * xpass=0 stores dst[b*dst_ps + l*dst_ls + row_nat] (Uhat^T for the register
+ * propagation path). */
+int pf_bluestein_warp(int xpass, const void* src, int64_t src_ps, int64_t src_ls, int n_in,
+                      int o_in, void* dst, int64_t dst_ps, int64_t dst_ls, int M, int nlines,
+                      int nplanes, const pf_fft_plan* plan_q, const void* chirp,
+                      const void* khat, void* stream);
+
 /* ---------------------------------------------------------------- NUFFT
  * Gaussian gridding (spectral.py:230-381).  Axis order (z, y, x); 2D uses
  * mr[0] = m[0] = 1.  Per point (device): i0[L][3] int32 nearest fine node,

@@ -86,6 +86,18 @@ def _scaled_spectra(coeff_fp: torch.Tensor, ny: int, nx: int, py: int, px: int,
     """
     s = dev.stream_ptr(stream)
     csz = 8
+    if transposed and tabs.qx in (128, 256, 512, 1024) and tabs.qy in (128, 256, 512, 1024):
+        # register-FFT passes: x pass stored transposed (xbuf[b][col][iy]), y pass
+        # reads contiguous rows of it and writes Uhat^T[b][col][row]
+        _lib.call("pf_bluestein_warp", 1, dev.ptr(coeff_fp), 0, nx, nx, px // 2 - nx // 2,
+                  dev.ptr(xbuf), px * ny, ny, px, ny, nb, tabs.plan_qx.ref,
+                  dev.ptr(tabs.chirp_x) + csz * t0 * px, dev.ptr(tabs.khat_x) + csz * t0 * tabs.qx,
+                  s)
+        _lib.call("pf_bluestein_warp", 0, dev.ptr(xbuf), px * ny, ny, ny, py // 2 - ny // 2,
+                  dev.ptr(out), out_plane_stride, py, py, px, nb, tabs.plan_qy.ref,
+                  dev.ptr(tabs.chirp_y) + csz * t0 * py, dev.ptr(tabs.khat_y) + csz * t0 * tabs.qy,
+                  s)
+        return
     _lib.call("pf_bluestein_lines", dev.ptr(coeff_fp), 0, nx, 1, nx, px // 2 - nx // 2,
               dev.ptr(xbuf), ny * px, px, 1, 1, px, ny, nb, tabs.plan_qx.ref,
               dev.ptr(tabs.chirp_x) + csz * t0 * px, dev.ptr(tabs.khat_x) + csz * t0 * tabs.qx, s)

@@ -93,3 +93,132 @@ extern "C" int pf_bluestein_lines(const void* src, int64_t src_ps, int64_t src_l
   PF_LAUNCH_CHECK("k_bluestein");
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Register-FFT Bluestein for power-of-two Q = 32 L (the SRSD configs: M = 512,
+// Q = 1024).  One line per L lanes; the Q-point transforms stay in registers
+// (warp_fft.cuh).  Two passes of sfft_2d_centered (spectral.py:205-206):
+//   X pass: line = relay row iy (contiguous input); output staged through
+//           shared memory and stored TRANSPOSED, xT[b][col_nat][iy], so that
+//   Y pass: line = column col (contiguous input xT row); output stored as the
+//           transposed spectrum Uhat^T[b][col][row_nat] the register
+//           propagation path consumes.
+#include "warp_fft.cuh"
+
+namespace {
+
+template <int L, bool XPASS>
+__global__ void __launch_bounds__(256, 2)
+k_bluestein_w(const float2* __restrict__ src, long long src_ps, long long src_ls, int n_in,
+              int o_in, float2* __restrict__ dst, long long dst_ps, long long dst_ls, int M,
+              int nlines, int n_out_lines, const float2* __restrict__ tw,
+              const float2* __restrict__ chirp, const float2* __restrict__ khat) {
+  constexpr int Q = 32 * L, LPW = 32 / L, LPC = 8 * LPW;
+  extern __shared__ float2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int r = warp * LPW + line;
+  const int b = blockIdx.y;
+  const int l0 = blockIdx.x * LPC;
+  const int l = l0 + r;
+  const bool active = l < nlines;
+  const float2* ch = chirp + (long long)b * M;
+  const float2* kh = khat + (long long)b * Q;
+  const float2* s = src + b * src_ps + (long long)(active ? l : 0) * src_ls;
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 32; m++) {
+    const int q = t + L * m;
+    const int i = q - o_in;
+    float2 x = make_float2(0.f, 0.f);
+    if (q < M && i >= 0 && i < n_in) x = cmul(__ldg(s + i), __ldg(ch + q));
+    v[m] = x;
+  }
+  float2* xch = sm + warp * WFFT_XCH;
+  wfft<L, -1>(v, xch, tw);
+#pragma unroll
+  for (int m = 0; m < 32; m++) v[m] = cmul(v[m], __ldg(kh + t + L * m));
+  wfft<L, 1>(v, xch, tw);
+  const float inv_q = 1.0f / (float)Q;
+  if (XPASS) {
+    // stage [M][LPC] then write xT[b][col_nat][l0 .. l0+LPC)
+    constexpr int SLD = LPC + 1;
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 32; m++) {
+      const int k = t + L * m;
+      if (k < M) sm[k * SLD + r] = cscale(cmul(v[m], __ldg(ch + k)), inv_q);
+    }
+    __syncthreads();
+    const int nl = min(LPC, nlines - l0);
+    float2* d = dst + b * dst_ps + l0;
+    for (int e = threadIdx.x; e < M * LPC; e += 256) {
+      const int k = e / LPC, rr = e % LPC;
+      if (rr < nl) d[(long long)natural((long long)k - M / 2, M) * dst_ls + rr] = sm[k * SLD + rr];
+    }
+  } else if (active) {
+    float2* d = dst + b * dst_ps + (long long)l * dst_ls;
+#pragma unroll
+    for (int m = 0; m < 32; m++) {
+      const int k = t + L * m;
+      if (k < M) d[natural((long long)k - M / 2, M)] = cscale(cmul(v[m], __ldg(ch + k)), inv_q);
+    }
+  }
+}
+
+template <int L>
+int launch_bw(int xpass, const float2* src, long long src_ps, long long src_ls, int n_in, int o_in,
+              float2* dst, long long dst_ps, long long dst_ls, int M, int nlines, int nplanes,
+              const float2* tw, const float2* chirp, const float2* khat, cudaStream_t st) {
+  constexpr int LPC = 8 * (32 / L), Q = 32 * L;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_bluestein_w<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_bluestein_w<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  size_t sm = 8 * WFFT_XCH;
+  if (xpass && (size_t)M * (LPC + 1) > sm) sm = (size_t)M * (LPC + 1);
+  sm *= sizeof(float2);
+  dim3 grid(pf_cdiv(nlines, LPC), nplanes);
+  (void)Q;
+  if (xpass)
+    k_bluestein_w<L, true><<<grid, 256, sm, st>>>(src, src_ps, src_ls, n_in, o_in, dst, dst_ps,
+                                                  dst_ls, M, nlines, 0, tw, chirp, khat);
+  else
+    k_bluestein_w<L, false><<<grid, 256, sm, st>>>(src, src_ps, src_ls, n_in, o_in, dst, dst_ps,
+                                                   dst_ls, M, nlines, 0, tw, chirp, khat);
+  PF_LAUNCH_CHECK("k_bluestein_w");
+  return 0;
+}
+
+}  // namespace
+
+// Register-path Bluestein pass (Q = plan_q->n in {128, 256, 512, 1024}).
+// xpass=1: lines are contiguous rows (src + b*src_ps + l*src_ls + i), output
+//          transposed: dst[b*dst_ps + col_nat*dst_ls + l].
+// xpass=0: lines are contiguous rows, output dst[b*dst_ps + l*dst_ls + row_nat].
+extern "C" int pf_bluestein_warp(int xpass, const void* src, int64_t src_ps, int64_t src_ls,
+                                 int n_in, int o_in, void* dst, int64_t dst_ps, int64_t dst_ls,
+                                 int M, int nlines, int nplanes, const pf_fft_plan* plan_q,
+                                 const void* chirp, const void* khat, void* stream) {
+  PF_ARG_CHECK(plan_q && plan_q->n >= 2 * M - 1 && nplanes >= 1 && nlines >= 0,
+               "pf_bluestein_warp: bad args");
+  if (nlines == 0) return 0;
+  const float2* tw = (const float2*)plan_q->tw;
+  cudaStream_t st = (cudaStream_t)stream;
+#define BW(LL)                                                                                \
+  return launch_bw<LL>(xpass, (const float2*)src, src_ps, src_ls, n_in, o_in, (float2*)dst,   \
+                       dst_ps, dst_ls, M, nlines, nplanes, tw, (const float2*)chirp,          \
+                       (const float2*)khat, st);
+  switch (plan_q->n) {
+    case 128: BW(4)
+    case 256: BW(8)
+    case 512: BW(16)
+    case 1024: BW(32)
+    default: break;
+  }
+#undef BW
+  pf_set_error("pf_bluestein_warp: Q must be 128, 256, 512 or 1024");
+  return -1;
+}
