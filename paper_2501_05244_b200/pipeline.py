@@ -127,6 +127,80 @@ class TransientReconstructor:
         main.synchronize()
         return self._vol_host
 
+    # -- pipelined streaming of successive captures -----------------------------------
+    def submit(self, hist_host: torch.Tensor):
+        """Enqueue one capture; returns a handle for :meth:`result`.
+
+        Two captures are in flight: the host->device copy of capture i+1 (copy
+        stream) overlaps the propagation of capture i (compute stream) and the
+        device->host read of volume i-1 (d2h stream).  Each capture still pays its
+        own H2D and D2H; only their overlap with compute changes.
+        """
+        if not hasattr(self, "_slots"):
+            self._init_slots(hist_host)
+        k = self._next
+        self._next ^= 1
+        sl = self._slots[k]
+        i_n, d_n, t_n = hist_host.shape
+        n_tr = i_n * d_n
+        main = torch.cuda.current_stream(self.device)
+        src = hist_host.view(n_tr, t_n)
+        dst = sl["hist"].view(n_tr, t_n)
+        out = sl["coeff"].view(self.kernel.n_freq, n_tr)
+        step = (n_tr + self.chunks - 1) // self.chunks
+        self.copy_stream.wait_event(sl["hist_free"])
+        for c0 in range(0, n_tr, step):
+            c1 = min(n_tr, c0 + step)
+            with torch.cuda.stream(self.copy_stream):
+                dst[c0:c1].copy_(src[c0:c1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.copy_stream)
+            main.wait_event(ev)
+            self.temporal.run(dst[c0:c1], out[:, c0:c1], main)
+        sl["hist_free"].record(main)
+        coeff = self.slice_gather(sl["coeff"]) if self.slice_gather is not None else sl["coeff"]
+        main.wait_event(sl["vol_free"])
+        self.engine.run(coeff, sl["vol"], main)
+        vol = sl["vol"]
+        if self.volume_gather is not None:
+            vol = self.volume_gather(sl["vol"])
+        done = torch.cuda.Event()
+        if vol is not None:
+            sl["vol_ready"].record(main)
+            self.d2h_stream.wait_event(sl["vol_ready"])
+            with torch.cuda.stream(self.d2h_stream):
+                sl["host"].copy_(vol, non_blocking=True)
+                sl["vol_free"].record(self.d2h_stream)
+                done.record(self.d2h_stream)
+        else:
+            sl["vol_free"].record(main)
+            done.record(main)
+        return (k, done)
+
+    def result(self, handle):
+        k, done = handle
+        done.synchronize()
+        return self._slots[k]["host"] if self.volume_gather is None or \
+            self.volume_gather.rank == 0 else None
+
+    def _init_slots(self, hist_host):
+        self.d2h_stream = torch.cuda.Stream(device=self.device)
+        self._next = 0
+        self._slots = []
+        vshape = self.vol.shape
+        if self.volume_gather is not None:
+            vshape = (self.vol.shape[0], self.grid.count)
+        for _ in range(2):
+            sl = {"hist": torch.empty_like(hist_host, device=self.device),
+                  "coeff": torch.empty_like(self.coeff),
+                  "vol": torch.zeros_like(self.vol),
+                  "host": torch.empty(vshape, dtype=self.vol.dtype, pin_memory=True),
+                  "hist_free": torch.cuda.Event(), "vol_free": torch.cuda.Event(),
+                  "vol_ready": torch.cuda.Event()}
+            sl["hist_free"].record()
+            sl["vol_free"].record()
+            self._slots.append(sl)
+
     def volume(self, host_vol: torch.Tensor) -> ReconstructionVolume:
         field = host_vol.numpy().astype(np.complex128)
         times = self.engine.times
