@@ -21,7 +21,7 @@ from . import nufft as nu
 from ._fastlen import next_fast_len
 from .core import (SPEED_OF_LIGHT, ReconstructionVolume, _require, illumination_coordinates)
 from .phasor import device_coefficients
-from .reconstruct import (PlaneSpec, Propagator, _check_depths, _check_times, _close,
+from .reconstruct import (GraphedRun, PlaneSpec, Propagator, _check_depths, _check_times, _close,
                           _exact_pad, _frame_weights, _ill_tensor, _kind, _nonplanar_relay,
                           _pad_size, _planar_relay, _uniform_relay, _volume, rsd)
 
@@ -118,7 +118,7 @@ def _scaled_spectra(coeff_fp: torch.Tensor, ny: int, nx: int, py: int, px: int,
 # ---------------------------------------------------------------------------
 
 
-class SrsdEngine:
+class SrsdEngine(GraphedRun):
     def __init__(self, slices, grid, include_illumination=True, times=None, device=None,
                  plane_range=None):
         _require(_kind(grid) == "frustum", "srsd reconstructs onto a frustum grid")
@@ -208,7 +208,7 @@ def srsd(slices, grid, times=None, threads: int = 1, include_illumination: bool 
 # ---------------------------------------------------------------------------
 
 
-class _UhatPropEngine:
+class _UhatPropEngine(GraphedRun):
     """Shared tail of nursd1 / nursd3d: per-frequency relay spectra -> propagate."""
 
     def _setup_prop(self, px, py, vg, z_src, include_illumination, k_range, flags=0):

@@ -75,6 +75,7 @@ class TransientReconstructor:
         self.vol = torch.zeros((self.engine.n_frames, self.engine.n_voxels), dtype=torch.complex64,
                                device=self.device)
         self.chunks = max(1, int(chunks))
+        self.use_graphs = True
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self._hist_dev = None
         self._vol_host = None
@@ -88,6 +89,8 @@ class TransientReconstructor:
         return self.coeff
 
     def propagate(self, coeff: torch.Tensor, stream=None) -> torch.Tensor:
+        if self.use_graphs:
+            return self.engine.run_graphed(coeff, self.vol, stream)
         return self.engine.run(coeff, self.vol, stream)
 
     # -- host in, host out ------------------------------------------------------
@@ -160,7 +163,10 @@ class TransientReconstructor:
         sl["hist_free"].record(main)
         coeff = self.slice_gather(sl["coeff"]) if self.slice_gather is not None else sl["coeff"]
         main.wait_event(sl["vol_free"])
-        self.engine.run(coeff, sl["vol"], main)
+        if self.use_graphs:
+            self.engine.run_graphed(coeff, sl["vol"], main)
+        else:
+            self.engine.run(coeff, sl["vol"], main)
         vol = sl["vol"]
         if self.volume_gather is not None:
             vol = self.volume_gather(sl["vol"])
