@@ -117,10 +117,15 @@ def run_ours(args):
     from paper_2501_05244_b200.pipeline import TransientReconstructor
 
     world, rank, local = _dist_env()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("PF_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:   # gloo: CPU-staged collectives (used to exercise N>1 logic on one GPU)
+            dist.init_process_group(backend)
     cfg = configs.config(args.config)
     kernel = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
     hist = configs.transients(cfg, device=device)            # [1, D, T] float32, identical per rank
@@ -183,7 +188,9 @@ def run_ours(args):
     total_ms = start.elapsed_time(end)
     if world > 1:
         dist.barrier()
-        tt = torch.tensor([total_ms], device=device)
+        tt = torch.tensor([total_ms])
+        if dist.get_backend() == "nccl":
+            tt = tt.to(device)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
     ms_per_step = total_ms / args.steps
@@ -219,7 +226,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_latency = (time.perf_counter() - a) * 1e3
     if world > 1:
-        tt = torch.tensor([e2e, e2e_latency], device=device)
+        tt = torch.tensor([e2e, e2e_latency])
+        if dist.get_backend() == "nccl":
+            tt = tt.to(device)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e, e2e_latency = float(tt[0].item()), float(tt[1].item())
 

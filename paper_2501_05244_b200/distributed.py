@@ -29,6 +29,11 @@ def _real(t: torch.Tensor) -> torch.Tensor:
     return torch.view_as_real(t) if t.is_complex() else t
 
 
+def _host_staged(group) -> bool:
+    """gloo cannot reduce/gather device tensors: stage those collectives through the host."""
+    return dist.get_backend(group) == "gloo"
+
+
 class SliceGather:
     """All-gather detector-sharded slices [F, I, D_r] into [F, I, D] on every rank."""
 
@@ -44,7 +49,14 @@ class SliceGather:
     def __call__(self, local: torch.Tensor) -> torch.Tensor:
         n = local.numel()
         self.send[:n].copy_(local.reshape(-1))
-        dist.all_gather([_real(r) for r in self.recv], _real(self.send), group=self.group)
+        if self.send.is_cuda and _host_staged(self.group):
+            send = self.send.cpu()
+            recv = [torch.empty_like(send) for _ in self.recv]
+            dist.all_gather([_real(r) for r in recv], _real(send), group=self.group)
+            for d, h in zip(self.recv, recv):
+                d.copy_(h)
+        else:
+            dist.all_gather([_real(r) for r in self.recv], _real(self.send), group=self.group)
         for r, (lo, hi) in enumerate(self.ranges):
             cnt = self.F * self.I * (hi - lo)
             self.full[:, :, lo:hi].copy_(self.recv[r][:cnt].view(self.F, self.I, hi - lo))
@@ -67,8 +79,17 @@ class VolumeGather:
 
     def __call__(self, local: torch.Tensor):
         self.send[:, :local.shape[1]].copy_(local)
-        dist.gather(_real(self.send), [_real(r) for r in self.recv] if self.rank == 0 else None,
-                    dst=0, group=self.group)
+        if self.send.is_cuda and _host_staged(self.group):
+            send = self.send.cpu()
+            recv = [torch.empty_like(send) for _ in range(self.world)] if self.rank == 0 else None
+            dist.gather(_real(send), [_real(r) for r in recv] if recv else None, dst=0,
+                        group=self.group)
+            if self.rank == 0:
+                for d, h in zip(self.recv, recv):
+                    d.copy_(h)
+        else:
+            dist.gather(_real(self.send), [_real(r) for r in self.recv] if self.rank == 0 else None,
+                        dst=0, group=self.group)
         if self.rank != 0:
             return None
         for r, (lo, hi) in enumerate(self.ranges):
