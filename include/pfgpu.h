@@ -212,6 +212,12 @@ int pf_cmul(void* a, const void* b, int64_t n, int64_t b_period, float scale, vo
 int pf_copy_planes(const void* src, int nb, int64_t src_stride, int64_t plane_off,
                    int64_t plane_elems, void* dst, void* stream);
 
+/* circular shift of the trailing axes (n0, n1, n2) of nb arrays:
+ * dst[b][j] = src[b][(j + s) mod n] per axis (ifftshift: s = n/2, fftshift: s = n - n/2;
+ * the index maps of cfft_n / cifft_n, spectral.py:107-114). */
+int pf_roll(const void* src, void* dst, int64_t nb, int n0, int n1, int n2, int s0, int s1, int s2,
+            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

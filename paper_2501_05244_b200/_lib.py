@@ -72,6 +72,7 @@ _SIGNATURES = {
     "pf_kernel3d": [_vp, _i, _i, _i, _d, _d, _d, _d, _vp],
     "pf_cmul": [_vp, _vp, _i64, _i64, _f, _vp],
     "pf_copy_planes": [_vp, _i, _i64, _i64, _i64, _vp, _vp],
+    "pf_roll": [_vp, _vp, _i64, _i, _i, _i, _i, _i, _i, _vp],
     "pf_prop_rows_out": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp,
                          _i64, _vp],
 }
@@ -85,7 +86,7 @@ _lib = None
 _LAUNCHERS = {"pf_temporal_dft", "pf_temporal_dft_direct", "pf_fft_lines", "pf_embed_centered",
               "pf_prop_kernel_rows", "pf_prop_columns", "pf_prop_rows_out", "pf_bluestein_lines", "pf_bluestein_warp",
               "pf_nufft_spread", "pf_nufft_deconv", "pf_nufft_place", "pf_nufft_interp2_acc",
-              "pf_kernel3d", "pf_cmul", "pf_copy_planes"}
+              "pf_kernel3d", "pf_cmul", "pf_copy_planes", "pf_roll"}
 launch_count = 0
 
 

@@ -76,3 +76,31 @@ extern "C" int pf_copy_planes(const void* src, int nb, int64_t src_stride, int64
   PF_LAUNCH_CHECK("k_slab");
   return 0;
 }
+
+// circular shift of the trailing (up to 3) axes: dst[b][j] = src[b][(j + s) mod n]
+// per axis -- ifftshift uses s = n/2, fftshift s = n - n/2 (spectral.py:107-114)
+namespace {
+__global__ void k_roll3(const float2* __restrict__ src, float2* __restrict__ dst, long long nb,
+                        int n0, int n1, int n2, int s0, int s1, int s2) {
+  const long long per = (long long)n0 * n1 * n2, total = per * nb;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / per, r = e - b * per;
+    const int j2 = (int)(r % n2), j1 = (int)((r / n2) % n1), j0 = (int)(r / ((long long)n1 * n2));
+    const int a0 = (j0 + s0) % n0, a1 = (j1 + s1) % n1, a2 = (j2 + s2) % n2;
+    dst[e] = src[b * per + ((long long)a0 * n1 + a1) * n2 + a2];
+  }
+}
+}  // namespace
+
+extern "C" int pf_roll(const void* src, void* dst, int64_t nb, int n0, int n1, int n2, int s0,
+                       int s1, int s2, void* stream) {
+  PF_ARG_CHECK(nb >= 0 && n0 >= 1 && n1 >= 1 && n2 >= 1 && s0 >= 0 && s1 >= 0 && s2 >= 0,
+               "pf_roll: bad sizes");
+  if (nb == 0) return 0;
+  const long long total = nb * (long long)n0 * n1 * n2;
+  k_roll3<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>((const float2*)src, (float2*)dst, nb,
+                                                             n0, n1, n2, s0, s1, s2);
+  PF_LAUNCH_CHECK("k_roll3");
+  return 0;
+}

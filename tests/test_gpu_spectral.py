@@ -1,0 +1,68 @@
+"""GPU transform primitives vs reference goldens (reference test_spectral.py semantics)."""
+
+import numpy as np
+import pytest
+
+from oracle import pf_oracle as O
+from golden_io import load
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-6
+
+
+def test_centred_ffts_golden():
+    from paper_2501_05244_b200 import spectral as S
+    d = load("spectral")
+    for i in range(int(d["n_c"])):
+        assert O.rel_l2(S.cfft_2d(d[f"c{i}_u"]), d[f"c{i}_fwd"]) < TOL
+        assert O.rel_l2(S.cifft_2d(d[f"c{i}_u"]), d[f"c{i}_inv"]) < TOL
+
+
+def test_centred_roundtrip_and_delta(rng):
+    from paper_2501_05244_b200 import spectral as S
+    for n in (1, 2, 3, 8, 15):
+        u = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+        assert O.rel_l2(S.cifft_2d(S.cfft_2d(u)), u) < TOL
+    for n in (4, 5, 9, 16):
+        u = np.zeros(n, complex)
+        u[n // 2] = 1.0
+        assert O.rel_l2(S.cfft_n(u, (-1,)), np.ones(n)) < TOL
+
+
+def test_sfft_golden():
+    from paper_2501_05244_b200 import spectral as S
+    d = load("spectral")
+    for i in range(int(d["n_s"])):
+        m, a, o = d[f"s{i}_args"]
+        got = S.sfft_1d(d[f"s{i}_u"], a, int(o))
+        assert O.rel_l2(got, d[f"s{i}_out"]) < 1e-5, (m, a, o)
+    assert O.rel_l2(S.sfft_2d_centered(d["s2d_u"], 0.45, 0.8), d["s2d_out"]) < 1e-5
+
+
+def test_nufft_golden():
+    from paper_2501_05244_b200 import spectral as S
+    d = load("spectral")
+    for i in range(int(d["n_n"])):
+        modes = tuple(int(m) for m in d[f"n{i}_modes"])
+        eps = float(d[f"n{i}_eps"])
+        t1 = S.nufft1(d[f"n{i}_pts"], d[f"n{i}_vals"], modes, eps)
+        assert O.rel_l2(t1, d[f"n{i}_t1"]) < max(1e-5, 10 * eps), modes
+        if len(modes) <= 2:
+            t2 = S.nufft2(d[f"n{i}_coeff"], d[f"n{i}_pts"], eps)
+            assert O.rel_l2(t2, d[f"n{i}_t2"]) < max(1e-5, 10 * eps), modes
+
+
+def test_nufft_on_grid_exact_and_adjoint(rng):
+    from paper_2501_05244_b200 import spectral as S
+    m = 8
+    j = rng.integers(0, m, size=20)
+    pts = (-np.pi + 2 * np.pi * j / m).reshape(-1, 1)
+    vals = rng.normal(size=20) + 1j * rng.normal(size=20)
+    assert O.rel_l2(S.nufft1(pts, vals, (m,), 1e-4), O.nudft1(pts, vals, (m,))) < TOL
+    modes = (9, 7)
+    p = rng.uniform(-np.pi, np.pi, size=(31, 2))
+    v = rng.normal(size=31) + 1j * rng.normal(size=31)
+    c = rng.normal(size=modes) + 1j * rng.normal(size=modes)
+    lhs = np.vdot(S.nufft1(p, v, modes, 1e-10), c)
+    rhs = np.vdot(v, S.nufft2(c, p, 1e-10))
+    assert abs(lhs - rhs) / abs(lhs) < 1e-5
