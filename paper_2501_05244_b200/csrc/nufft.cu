@@ -37,7 +37,7 @@ k_spread(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ 
          const int* __restrict__ tile_start, const int* __restrict__ tile_pts,
          const float2* __restrict__ vals, long long val_stride, int nv,
          float2* __restrict__ fine, long long fine_stride) {
-  __shared__ float wgt[SP_CHUNK][3][2 * 12 + 1];
+  __shared__ float wgt[SP_CHUNK][3][2 * 16 + 1];
   __shared__ int pi0[SP_CHUNK][3];
   __shared__ float2 pv[SP_V][SP_CHUNK];
   const int tid = threadIdx.x;
@@ -183,7 +183,7 @@ __global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= npts) return;
   const int W = 2 * G.w + 1;
-  float wy[2 * 12 + 1], wx[2 * 12 + 1];
+  float wy[2 * 16 + 1], wx[2 * 16 + 1];
   for (int o = 0; o < W; o++) {
     const float dy = d0[3 * l + 1] + (float)(o - G.w) * G.h[1];
     const float dx = d0[3 * l + 2] + (float)(o - G.w) * G.h[2];
@@ -232,7 +232,7 @@ extern "C" int pf_nufft_spread(const pf_nufft_geom* g, const int32_t* i0, const 
                                const int32_t* tile_start, const int32_t* tile_pts,
                                const void* vals, int64_t val_stride, int nv, void* fine,
                                int64_t fine_stride, void* stream) {
-  PF_ARG_CHECK(g && (g->dim == 2 || g->dim == 3) && g->w >= 1 && g->w <= 12 && nv >= 1,
+  PF_ARG_CHECK(g && (g->dim == 2 || g->dim == 3) && g->w >= 1 && g->w <= 16 && nv >= 1,
                "pf_nufft_spread: bad geometry");
   PF_ARG_CHECK(g->tile[0] * g->tile[1] * g->tile[2] <= NT, "pf_nufft_spread: tile too large");
   const int ntiles = g->ntiles[0] * g->ntiles[1] * g->ntiles[2];
@@ -273,7 +273,7 @@ extern "C" int pf_nufft_interp2_acc(const pf_nufft_geom* g, const int32_t* i0, c
                                     double khat, int include_illum, float scale,
                                     const void* frame_w, int n_frames, void* vol,
                                     int64_t vol_frame_stride, int64_t dst0, void* stream) {
-  PF_ARG_CHECK(g && g->dim == 2 && g->w <= 12 && npts >= 0, "pf_nufft_interp2_acc: bad args");
+  PF_ARG_CHECK(g && g->dim == 2 && g->w <= 16 && npts >= 0, "pf_nufft_interp2_acc: bad args");
   if (npts == 0) return 0;
   k_interp2_acc<<<pf_cdiv(npts, 128), 128, 0, (cudaStream_t)stream>>>(
       *g, i0, d0, xyz, npts, (const float2*)fine, fine_stride, n_illum, ill, khat / PF_TWO_PI,

@@ -40,7 +40,7 @@ class NufftPlan:
         self.dim = len(modes)
         self.modes3 = (1,) * (3 - self.dim) + modes
         self.w = max(2, math.ceil(math.log10(1.0 / eps)) + 2)
-        _require(self.w <= 12, "accuracy target too tight for the GPU stencil (w <= 12)")
+        _require(self.w <= 16, "accuracy target too tight for the GPU stencil (w <= 16)")
         self.device = device
         mrs, taus, kers = [], [], []
         for m in self.modes3:
