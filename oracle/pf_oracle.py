@@ -718,6 +718,28 @@ def nursd3d(slices, grid, eps=1e-6, z_pitch=None, times=None, include_illuminati
     return _reduce((term(f) for f in range(slices.n_freq)), freqs, grid.count, times)
 
 
+def nursd3d_explicit(slices, grid, lattice, eps=1e-6, z_pitch=None, times=None,
+                     include_illumination=True):
+    """Config-2 composed oracle: nursd3d stage 1 to the virtual plane z0
+    (reconstruct.py:741-760), then nursd2 (:413-459) from a uniform relay at z0 that
+    carries that plane's centred-slot coefficients."""
+    geo, uplanes = nursd3d_stage1(slices, lattice, eps, z_pitch)
+    vg = lattice.grid
+    px, py = geo["px"], geo["py"]
+    cx = vg.x0 + (vg.nx // 2) * vg.dx
+    cy = vg.y0 + (vg.ny // 2) * vg.dy
+    waves = [cifft2(u) for u in uplanes]                 # [I, py, px] per f, slot order
+    coeff = np.stack([w.reshape(w.shape[0], -1) for w in waves], axis=-1)   # [I, D, F]
+    grid2 = type("G", (), dict(nx=px, ny=py, dx=vg.dx, dy=vg.dy, x0=cx - (px // 2) * vg.dx,
+                              y0=cy - (py // 2) * vg.dy, z=geo["z0"],
+                              center=lambda self: (cx, cy)))()
+    relay = type("R", (), dict(kind="uniform", grid=grid2, z=geo["z0"], count=px * py))()
+    vs = type("S", (), dict(frequencies=slices.frequencies, coefficients=coeff, relay=relay,
+                            illuminations=slices.illuminations,
+                            n_freq=int(np.asarray(slices.frequencies).size)))()
+    return nursd2(vs, grid, eps=eps, times=times, include_illumination=include_illumination)
+
+
 class _FlatView:
     """A 3D relay whose points share one z, viewed as a planar relay (reconstruct.py:735-740)."""
 

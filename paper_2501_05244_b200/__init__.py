@@ -22,7 +22,12 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # the non-rsd algorithms live in .algorithms (loaded on first use)
-    if name in ("srsd", "nursd1", "nursd2", "nursd3", "nursd3d", "srsd_nursd2", "rsd3d"):
+    if name in ("srsd", "nursd1", "nursd2", "nursd3", "nursd3d", "srsd_nursd2", "rsd3d",
+                "nursd3d_explicit"):
         from . import algorithms
         return getattr(algorithms, name)
+    if name in ("cfft_n", "cifft_n", "cfft_2d", "cifft_2d", "sfft_1d", "sfft_2d",
+                "sfft_2d_centered", "nufft1", "nufft2", "next_fast_len"):
+        from . import spectral
+        return getattr(spectral, name)
     raise AttributeError(name)

@@ -565,7 +565,8 @@ class Nursd3dEngine(_UhatPropEngine):
         self.frame_w = _frame_weights(self.freqs, self.times, self.device)
         self.n_frames = 1 if self.times is None else self.times.size
 
-    def relay_spectra(self, coeff, stream=None):
+    def virtual_planes(self, coeff, stream=None):
+        """wave[slab] per (f, illumination), natural order [F*I][py][px] (reconstruct.py:741-760)."""
         F, I = self.freqs.size, self.n_illum
         px, py, pz = self.px, self.py, self.pz
         n3 = pz * py * px
@@ -585,6 +586,12 @@ class Nursd3dEngine(_UhatPropEngine):
             dev.fftn_natural(uhat3, (pz, py, px), I, +1, 1.0 / n3, stream)
             _lib.call("pf_copy_planes", dev.ptr(uhat3), I, n3, self.slab_nat * py * px, py * px,
                       dev.ptr(out) + 8 * fi * I * py * px, s)
+        return out
+
+    def relay_spectra(self, coeff, stream=None):
+        F, I = self.freqs.size, self.n_illum
+        px, py = self.px, self.py
+        out = self.virtual_planes(coeff, stream)
         if self.prop.transposed:
             t = out.view(F * I, py, px).transpose(1, 2).contiguous()
             dev.fft2_natural(t, px, py, F * I, -1, 1.0, stream)
@@ -626,3 +633,43 @@ def rsd3d(slices, grid, scatter: str = "trilinear", z_pitch: float | None = None
     _require(scatter in ("nearest", "trilinear"), "scatter must be 'nearest' or 'trilinear'")
     _lattice_3d(slices, grid, z_pitch)
     raise NotImplementedError("rsd3d is outside the GPU engine's scope (use nursd3d)")
+
+
+# ---------------------------------------------------------------------------
+# config 2: non-planar relay -> arbitrary voxels (3D NURSD stage 1 + NURSD-2)
+# ---------------------------------------------------------------------------
+
+
+def nursd3d_explicit(slices, grid, lattice, eps: float = 1e-6, z_pitch: float | None = None,
+                     times=None, threads: int = 1, include_illumination: bool = True):
+    """Non-planar relay -> explicit voxels: the paper's 3D NURSD + NURSD-2 fusion.
+
+    The reference has no single entry point for this; it is composed
+    from reference pieces exactly as SURVEY 8(d) specifies the config-2 oracle:
+    the ``nursd3d`` stage 1 (reconstruct.py:741-760) propagates the scattered 3D
+    relay to the virtual plane z0 on the lattice of the ``lattice`` cuboid
+    (``_lattice_3d``, :594-621); that plane, in the lattice's centred slot
+    order, becomes a uniform relay at z0 whose coefficients ``nursd2``
+    (:413-459) reads out at the explicit voxels (every voxel plane beyond z0).
+    """
+    from .core import FrequencySlices, PointList, UniformGrid2D, UniformRelay
+    _require(_kind(grid) == "explicit", "nursd3d-explicit reconstructs onto explicit voxels")
+    _require(_kind(lattice) == "cuboid", "the stage-1 lattice must be a cuboid grid")
+    eng = Nursd3dEngine(slices, lattice, eps, z_pitch, include_illumination, None)
+    coeff = device_coefficients(slices)
+    F, I = eng.freqs.size, eng.n_illum
+    px, py = eng.px, eng.py
+    planes = eng.virtual_planes(coeff).view(F * I, py, px)
+    # natural -> centred slot order (fftshift) and relay coefficient layout [F][I][py*px]
+    slot = torch.empty_like(planes)
+    _lib.call("pf_roll", dev.ptr(planes), dev.ptr(slot), F * I, 1, py, px, 0, py - py // 2,
+              px - px // 2, dev.stream_ptr())
+    vg = lattice.grid
+    cx = vg.x0 + (vg.nx // 2) * vg.dx
+    cy = vg.y0 + (vg.ny // 2) * vg.dy
+    vrel = UniformRelay(UniformGrid2D(px, py, vg.dx, vg.dy, cx - (px // 2) * vg.dx,
+                                      cy - (py // 2) * vg.dy, eng.z0))
+    from .phasor import DeviceFrequencySlices
+    vs = DeviceFrequencySlices(slices.frequencies, slot.view(F, I, py * px), vrel,
+                               slices.illuminations)
+    return nursd2(vs, grid, eps=eps, times=times, include_illumination=include_illumination)

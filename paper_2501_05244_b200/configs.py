@@ -69,6 +69,25 @@ def config(c: int) -> Config:
             relay = core.NonUniformPlanarRelay(core.PointList(pts), 0.0)
             alg = "nursd1"
         return Config(f"c{c}", relay, ill, grid, sc, al, T, dt, lam, 0.0, alg, seed)
+    if c == 2:
+        T, dt, lam = 4096, 4e-12, 0.06
+        xy = rng.uniform(-1.0, 1.0, size=(16384, 2))
+        zz = 0.1 * np.sin(2 * np.pi * xy[:, 0] / 1.0) * np.cos(2 * np.pi * xy[:, 1] / 1.5)
+        relay = core.NonPlanarRelay(core.PointList(np.column_stack([xy, zz])))
+        ill3 = core.PointList(np.array([[0.0, 0.0, 0.0]]))
+        sc = np.column_stack([rng.uniform(-0.5, 0.5, size=(2000, 2)),
+                              rng.uniform(1.0, 2.0, size=2000)])
+        al = rng.uniform(0.5, 1.0, size=sc.shape[0])
+        # 1e6 voxels = 64 depth planes x 15,625 random lateral positions in the box
+        planes = tuple(core.VoxelPlane(float(z), core.PointList(rng.uniform(-0.5, 0.5,
+                                                                         size=(15625, 2))))
+                       for z in np.linspace(1.0, 2.0, 64))
+        cfg = Config("c2", relay, ill3, core.ExplicitVoxels(planes), sc, al, T, dt, lam,
+                     1.5 / SPEED_OF_LIGHT, "nursd3d-explicit", seed)
+        p = 2.0 / 128
+        cfg.lattice = core.CuboidGrid(core.UniformGrid3D(128, 128, 1, p, p, 0.1, -1 + p / 2,
+                                                         -1 + p / 2, 1.0))
+        return cfg
     if c == 3:
         n, T, dt, lam = 256, 4096, 8e-12, 0.08
         sc = _rect_scene(rng, [(-0.4, -0.4), (0.4, -0.3), (0.0, 0.0), (-0.5, 0.6), (0.7, 0.7)],

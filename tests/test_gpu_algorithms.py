@@ -105,3 +105,22 @@ def test_nursd2_offlattice_voxels(rng):
     ev = pf.ExplicitVoxels(planes)
     vol = pf.nursd2(sl, ev)
     assert O.rel_l2(vol.field, O.nursd2(sl, ev)) < TOL
+
+
+def test_config2_composed_small(rng):
+    """Config-2 family (non-planar relay -> arbitrary voxels) against the composed oracle."""
+    from paper_2501_05244_b200.algorithms import nursd3d_explicit
+    xy = rng.uniform(-0.3, 0.3, size=(600, 2))
+    zz = 0.03 * np.sin(2 * np.pi * xy[:, 0] / 0.6) * np.cos(2 * np.pi * xy[:, 1] / 0.9)
+    relay = pf.NonPlanarRelay(pf.PointList(np.column_stack([xy, zz])))
+    freqs = 2 * np.pi * 299792458.0 / 0.06 * (1.0 + 0.03 * np.arange(2))
+    coeff = rng.normal(size=(1, 600, 2)) + 1j * rng.normal(size=(1, 600, 2))
+    sl = pf.FrequencySlices(freqs, coeff, relay, pf.PointList(np.array([[0.0, 0.0, 0.0]])))
+    p = 0.6 / 24
+    lattice = pf.CuboidGrid(pf.UniformGrid3D(24, 24, 1, p, p, 0.1, -0.3 + p / 2, -0.3 + p / 2, 0.6))
+    planes = tuple(pf.VoxelPlane(z, pf.PointList(rng.uniform(-0.15, 0.15, size=(40, 2))))
+                   for z in (0.5, 0.7))
+    ev = pf.ExplicitVoxels(planes)
+    vol = nursd3d_explicit(sl, ev, lattice)
+    ref = O.nursd3d_explicit(sl, ev, lattice)
+    assert O.rel_l2(vol.field, ref) < TOL
