@@ -23,7 +23,7 @@ def simulate_device(scatterers: np.ndarray, albedo: np.ndarray, det_xyz: np.ndar
                     falloff: bool = True, device=None, chunk: int = 32) -> torch.Tensor:
     """Float32 histograms [n_illum, n_detect, n_bins] on ``device``."""
     device = device or torch.device("cuda")
-    det = torch.as_tensor(det_xyz, dtype=torch.float64, device=device)
+    det = torch.as_tensor(np.array(det_xyz, dtype=np.float64), device=device)
     ill = torch.as_tensor(ill_xyz, dtype=torch.float64, device=device)
     sc = torch.as_tensor(scatterers, dtype=torch.float64, device=device)
     al = torch.as_tensor(albedo, dtype=torch.float64, device=device)
