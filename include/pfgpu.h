@@ -139,6 +139,17 @@ int pf_prop_rows_out(const pf_plane* planes, int nplanes, double khat,
                      const double* ill_xyz, const void* frame_w, int n_frames, void* vol,
                      int64_t vol_frame_stride, void* stream);
 
+/* All nf frequencies of a plane batch at once (register path, static volume):
+ * kturns: device float64 [nf] = khat_f / (2 pi); ws_a / uhat / ws_b advance by
+ * the given per-frequency strides (elements); frame_w: device c64 [nf] weights
+ * (ones for a static volume); kernel C sums the frequencies in ascending order
+ * in registers and adds the result to vol once.  For small configurations
+ * (config 0/1) where per-launch latency dominates. */
+int pf_prop_fbatch(const pf_plane* planes, int nplanes, const double* kturns, int nf,
+                   const pf_prop_geom* g, const pf_fft_plan* plan, void* ws_a, int64_t ws_a_fs,
+                   const void* uhat, int64_t uhat_fs, void* ws_b, int64_t ws_b_fs,
+                   const double* ill_xyz, const void* frame_w, void* vol, void* stream);
+
 /* ---------------------------------------------------------------- SFFT (Bluestein)
  * Scaled-DFT lines, replacing SfftPlan.apply (spectral.py:160-168) inside
  * sfft_2d_centered (:209-218): per plane b (grid y) the tables chirp[b][M] and

@@ -60,6 +60,8 @@ _SIGNATURES = {
     "pf_prop_kernel_rows": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp],
     "pf_prop_columns": [_vp, _i, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp],
     "pf_prop_ws_spectrum": [_P(PfPropGeom), _i],
+    "pf_prop_fbatch": [_vp, _i, _vp, _i, _P(PfPropGeom), _P(PfFftPlan), _vp, _i64, _vp, _i64, _vp,
+                       _i64, _vp, _vp, _vp, _vp],
     "pf_bluestein_lines": [_vp, _i64, _i64, _i64, _i, _i, _vp, _i64, _i64, _i64, _i, _i, _i, _i,
                            _P(PfFftPlan), _vp, _vp, _vp],
     "pf_bluestein_warp": [_i, _vp, _i64, _i64, _i, _i, _vp, _i64, _i64, _i, _i, _i, _P(PfFftPlan),
@@ -84,7 +86,7 @@ _lib = None
 
 # calls that enqueue kernels (bench.py reports how many ran in its timed region)
 _LAUNCHERS = {"pf_temporal_dft", "pf_temporal_dft_direct", "pf_fft_lines", "pf_embed_centered",
-              "pf_prop_kernel_rows", "pf_prop_columns", "pf_prop_rows_out", "pf_bluestein_lines", "pf_bluestein_warp",
+              "pf_prop_kernel_rows", "pf_prop_columns", "pf_prop_rows_out", "pf_prop_fbatch", "pf_bluestein_lines", "pf_bluestein_warp",
               "pf_nufft_spread", "pf_nufft_deconv", "pf_nufft_place", "pf_nufft_interp2_acc",
               "pf_kernel3d", "pf_cmul", "pf_copy_planes", "pf_roll"}
 launch_count = 0

@@ -223,6 +223,10 @@ class _UhatPropEngine(GraphedRun):
 
     def _propagate(self, uhat, vol, stream):
         per_f = self.n_illum * self.py * self.px
+        if self.prop.fbatch_ok(self.freqs.size, self.n_frames):
+            self.prop.run_fbatch(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w, vol,
+                                 stream)
+            return vol
 
         def body(b0, b1, lane, ls):
             for fi in range(self.freqs.size):

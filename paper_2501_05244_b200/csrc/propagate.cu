@@ -193,6 +193,28 @@ int pf_prop_fast_stage(int stage, const pf_plane* planes, int nplanes, double kh
 
 extern "C" int pf_prop_fast(const pf_prop_geom* g) { return g ? 32 * pf_prop_fast_L(g) : 0; }
 
+int pf_prop_fbatch_stage(int stage, const pf_plane* planes, int nplanes, const double* kturns,
+                         int nf, const pf_prop_geom* g, const pf_fft_plan* plan, void* ws_a,
+                         long long ws_a_fs, const void* uhat, long long uhat_fs, void* ws_b,
+                         long long ws_b_fs, const double* ill, const void* frame_w, void* vol,
+                         cudaStream_t st);
+
+extern "C" int pf_prop_fbatch(const pf_plane* planes, int nplanes, const double* kturns, int nf,
+                              const pf_prop_geom* g, const pf_fft_plan* plan, void* ws_a,
+                              int64_t ws_a_fs, const void* uhat, int64_t uhat_fs, void* ws_b,
+                              int64_t ws_b_fs, const double* ill_xyz, const void* frame_w,
+                              void* vol, void* stream) {
+  PF_ARG_CHECK(g && plan && nf >= 1 && nplanes >= 1 && pf_prop_fast_L(g) && plan->n == g->px,
+               "pf_prop_fbatch: needs the register path (square power-of-two pad)");
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int stage = 0; stage < 3; stage++) {
+    const int rc = pf_prop_fbatch_stage(stage, planes, nplanes, kturns, nf, g, plan, ws_a, ws_a_fs,
+                                        uhat, uhat_fs, ws_b, ws_b_fs, ill_xyz, frame_w, vol, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
 extern "C" int64_t pf_prop_ws_a(const pf_prop_geom* g, int nplanes) {
   return (int64_t)nplanes * (g->py / 2 + 1) * (g->px / 2 + 1);
 }

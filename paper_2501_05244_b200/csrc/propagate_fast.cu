@@ -23,6 +23,14 @@ namespace {
 
 constexpr int FT = 256;  // 8 warps
 
+// Frequency batching (small configs): blockIdx.z indexes the frequency; per-f
+// kernel wavenumbers (turns/m) and per-f workspace / spectrum strides.
+struct FBatch {
+  const double* kturns;   // nullptr: single frequency (scalar argument)
+  long long ws_a_fs, ws_b_fs, uhat_fs;
+  int nf;
+};
+
 // exp(1j * 2 pi * kturns * r) / r with r = sqrt(r2): float rsqrt + one float64
 // Newton correction (r = rf + (r2 - rf^2) / (2 rf), error ~ (eps_f)^2 r), phase
 // reduced in turns with the large part in float64 and the tiny correction in
@@ -55,8 +63,10 @@ __device__ __forceinline__ float2 phase_turns(double r2, double kturns, float kt
 
 template <int L>
 __global__ void __launch_bounds__(FT, 2)
-k_pa(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
-     const float2* __restrict__ tw, float2* __restrict__ ws_a) {
+k_pa(const pf_plane* __restrict__ planes, double kturns_s, pf_prop_geom g,
+     const float2* __restrict__ tw, float2* __restrict__ ws_a, FBatch fb) {
+  const double kturns = fb.kturns ? fb.kturns[blockIdx.z] : kturns_s;
+  ws_a += blockIdx.z * fb.ws_a_fs;
   constexpr int P = 32 * L, H = P / 2, NA = H + 1;
   constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
   extern __shared__ float2 sm[];
@@ -271,7 +281,8 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
 // B2: line = (plane b, side): Gq row (mirrored) * Uhat^T column, y-IFFT, crop.
 template <int L>
 __global__ void __launch_bounds__(FT, 2)
-k_pb1(int nplanes, const float2* __restrict__ tw, float2* __restrict__ ws_a) {
+k_pb1(int nplanes, const float2* __restrict__ tw, float2* __restrict__ ws_a, FBatch fb) {
+  ws_a += blockIdx.z * fb.ws_a_fs;
   constexpr int P = 32 * L, H = P / 2, NA = H + 1;
   constexpr int LPW = 32 / L;
   extern __shared__ float2 sm[];
@@ -301,7 +312,10 @@ template <int L, bool MULTI>
 __global__ void __launch_bounds__(FT, 2)
 k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
       const float2* __restrict__ tw, const float2* __restrict__ ws_a,
-      const float2* __restrict__ uhat_t, float2* __restrict__ ws_b) {
+      const float2* __restrict__ uhat_t, float2* __restrict__ ws_b, FBatch fb) {
+  ws_a += blockIdx.z * fb.ws_a_fs;
+  uhat_t += blockIdx.z * fb.uhat_fs;
+  ws_b += blockIdx.z * fb.ws_b_fs;
   constexpr int P = 32 * L, H = P / 2, NA = H + 1;
   constexpr int LPW = 32 / L;
   extern __shared__ float2 sm[];
@@ -346,6 +360,86 @@ static int pf_splitb_env() {
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v;
+}
+
+// C over all frequencies of the batch in one launch: per (plane, row tile) the
+// ascending-frequency sum is formed in registers and written once.
+template <int L, bool MULTI>
+__global__ void __launch_bounds__(FT, 1)
+k_pcf(const pf_plane* __restrict__ planes, pf_prop_geom g, const float2* __restrict__ tw,
+      const float2* __restrict__ ws_b, const double* __restrict__ ill,
+      const float2* __restrict__ frame_w, float2* __restrict__ vol, FBatch fb) {
+  constexpr int P = 32 * L;
+  constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
+  extern __shared__ float2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int r = warp * LPW + line;
+  const int ny = g.ny, nx = g.nx;
+  const int i0 = blockIdx.x * RPC;
+  const int i = i0 + r;
+  const int nr = min(RPC, ny - i0);
+  const pf_plane pl = planes[blockIdx.y];
+  const float scale = 1.0f / ((float)P * (float)P);
+  const double yv = pl.y0 + pl.dy * i;
+  float2 acc[32];
+#pragma unroll
+  for (int m = 0; m < 32; m++) acc[m] = make_float2(0.f, 0.f);
+  const int n_ill = MULTI ? g.n_illum : 1;
+#pragma unroll 1
+  for (int f = 0; f < fb.nf; f++) {
+    const double kturns = fb.kturns[f];
+    const float2 fw = frame_w[f];
+#pragma unroll 1
+    for (int p = 0; p < n_ill; p++) {
+      const float2* src = ws_b + f * fb.ws_b_fs +
+                          ((long long)blockIdx.y * g.n_illum + p) * (long long)P * ny + i0;
+      __syncthreads();
+      {
+        constexpr int CSTEP = FT / RPC;
+        const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
+        if (rr < nr) {
+          const float2* q = src + (long long)c0 * ny + rr;
+          float2* d = sm + c0 * SLD + rr;
+#pragma unroll 8
+          for (int col = c0; col < P; col += CSTEP) {
+            cp_async8(d, q);
+            q += (long long)CSTEP * ny;
+            d += CSTEP * SLD;
+          }
+        }
+      }
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncthreads();
+      float2 v[32];
+#pragma unroll
+      for (int m = 0; m < 32; m++) v[m] = sm[(t + L * m) * SLD + r];
+      __syncthreads();
+      wfft<L, 1>(v, sm + warp * WFFT_XCH, tw);
+      const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
+      const double dy = yv - sy, dz = pl.z - sz;
+      const double byz = fma(dy, dy, dz * dz);
+#pragma unroll
+      for (int m = 0; m < 32; m++) {
+        const int mo = (t + L * m - g.nu0x) & (P - 1);
+        float2 val = cscale(v[m], scale);
+        if (g.include_illum && mo < nx) {
+          const double dx = pl.x0 + pl.dx * mo - sx;
+          val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
+        }
+        acc[m] = cadd(acc[m], cmul(val, fw));
+      }
+    }
+  }
+  if (i < ny) {
+    float2* drow = vol + (pl.vol_plane * ny + i) * (long long)nx;
+#pragma unroll
+    for (int m = 0; m < 32; m++) {
+      const int mo = (t + L * m - g.nu0x) & (P - 1);
+      if (mo < nx) drow[mo] = cadd(drow[mo], acc[m]);
+    }
+  }
 }
 
 // ---- persistent variants: one CTA per SM loops over work items and prefetches
@@ -558,7 +652,8 @@ template <int L>
 int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const pf_prop_geom& g,
               const float2* tw, const float2* ws_a, float2* ws_a_out, const float2* uhat,
               const float2* ws_b, float2* ws_b_out, const double* ill, const float2* frame_w,
-              int n_frames, float2* vol, long long vfs, cudaStream_t st) {
+              int n_frames, float2* vol, long long vfs, cudaStream_t st,
+              FBatch fb = FBatch{nullptr, 0, 0, 0, 1}) {
   constexpr int P = 32 * L, NA = P / 2 + 1, RPC = 8 * (32 / L), LPW = 32 / L;
   static bool attr = false;
   if (!attr) {
@@ -572,8 +667,8 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
   }
   const double kturns = khat / PF_TWO_PI;
   if (stage == 0) {
-    dim3 grid(pf_cdiv(NA, RPC), nplanes);
-    k_pa<L><<<grid, FT, smem_a<L>(), st>>>(planes, kturns, g, tw, ws_a_out);
+    dim3 grid(pf_cdiv(NA, RPC), nplanes, fb.nf);
+    k_pa<L><<<grid, FT, smem_a<L>(), st>>>(planes, kturns, g, tw, ws_a_out, fb);
     PF_LAUNCH_CHECK("k_pa");
   } else if (stage == 1 && pf_splitb_env()) {
     static bool a4 = false;
@@ -584,14 +679,14 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
       a4 = true;
     }
     const size_t sm = 8 * WFFT_XCH * sizeof(float2);
-    dim3 g1(pf_cdiv(NA, 8 * LPW), nplanes);
-    k_pb1<L><<<g1, FT, sm, st>>>(nplanes, tw, const_cast<float2*>(ws_a));
+    dim3 g1(pf_cdiv(NA, 8 * LPW), nplanes, fb.nf);
+    k_pb1<L><<<g1, FT, sm, st>>>(nplanes, tw, const_cast<float2*>(ws_a), fb);
     PF_LAUNCH_CHECK("k_pb1");
-    dim3 g2(NA, pf_cdiv(2 * nplanes, 8 * LPW));
+    dim3 g2(NA, pf_cdiv(2 * nplanes, 8 * LPW), fb.nf);
     if (g.n_illum > 1)
-      k_pb2<L, true><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out);
+      k_pb2<L, true><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
     else
-      k_pb2<L, false><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out);
+      k_pb2<L, false><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
     PF_LAUNCH_CHECK("k_pb2");
   } else if (stage == 1 && pf_persist_env()) {
     const int I = g.n_illum;
@@ -614,6 +709,20 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     k_pb<L><<<grid, FT, 8 * WFFT_XCH * sizeof(float2), st>>>(planes, nplanes, g, tw, ws_a, uhat,
                                                              ws_b_out);
     PF_LAUNCH_CHECK("k_pb");
+  } else if (fb.kturns != nullptr) {
+    static bool a5 = false;
+    if (!a5) {
+      cudaFuncSetAttribute(k_pcf<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_pcf<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      a5 = true;
+    }
+    dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
+    const size_t sm = smem_c<L>(g.nx, false);
+    if (g.n_illum > 1)
+      k_pcf<L, true><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+    else
+      k_pcf<L, false><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+    PF_LAUNCH_CHECK("k_pcf");
   } else if (pf_persist_env() &&
              (8 * WFFT_XCH + 2 * (size_t)g.n_illum * P * (RPC + 1)) * sizeof(float2) <= 220 * 1024) {
     const size_t sm = (8 * WFFT_XCH + 2 * (size_t)g.n_illum * P * (RPC + 1)) * sizeof(float2);
@@ -683,5 +792,32 @@ int pf_prop_fast_stage(int stage, const pf_plane* planes, int nplanes, double kh
   }
 #undef PF_FAST_CASE
   pf_set_error("pf_prop_fast_stage: geometry not eligible");
+  return -1;
+}
+
+// Frequency-batched stages (all nf frequencies of a plane batch in one launch
+// per stage; kernel C sums them in registers).  Register path only.
+int pf_prop_fbatch_stage(int stage, const pf_plane* planes, int nplanes, const double* kturns,
+                         int nf, const pf_prop_geom* g, const pf_fft_plan* plan, void* ws_a,
+                         long long ws_a_fs, const void* uhat, long long uhat_fs, void* ws_b,
+                         long long ws_b_fs, const double* ill, const void* frame_w, void* vol,
+                         cudaStream_t st) {
+  const float2* tw = (const float2*)plan->tw;
+  FBatch fb{kturns, ws_a_fs, ws_b_fs, uhat_fs, nf};
+#define PF_FB_CASE(LL)                                                                        \
+  case LL:                                                                                    \
+    return run_stage<LL>(stage, planes, nplanes, 0.0, *g, tw, (const float2*)ws_a,            \
+                         (float2*)ws_a, (const float2*)uhat, (const float2*)ws_b,             \
+                         (float2*)ws_b, ill, (const float2*)frame_w, 1, (float2*)vol, 0, st,  \
+                         fb);
+  switch (pf_prop_fast_L(g)) {
+    PF_FB_CASE(4)
+    PF_FB_CASE(8)
+    PF_FB_CASE(16)
+    PF_FB_CASE(32)
+    default: break;
+  }
+#undef PF_FB_CASE
+  pf_set_error("pf_prop_fbatch: geometry not eligible for the register path");
   return -1;
 }

@@ -42,6 +42,7 @@ ALGORITHM_NAMES = ("rsd", "srsd", "nursd1", "nursd2", "nursd3", "rsd3d", "nursd3
 _BATCH_BYTES = 64 << 20
 _LANES = int(os.environ.get("PF_LANES", "3"))
 _FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "4"))
+_FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
 
 
 # ---------------------------------------------------------------------------
@@ -198,6 +199,35 @@ class Propagator:
             _lib.call("pf_prop_rows_out", pp, nb, khat, gref, self.plan_x.ref, wb, ill_ptr,
                       frame_w_ptr, n_frames, dev.ptr(vol), vol_frame_stride, s)
 
+    def fbatch_ok(self, n_freq: int, n_frames: int) -> bool:
+        """All frequencies in one launch per stage (small configs, static volume)."""
+        if not self.transposed or n_frames != 1:
+            return False
+        g = self.geom
+        per = 8 * ((g.py // 2 + 1) * (g.px // 2 + 1) + g.n_illum * g.ny * g.px)
+        return n_freq * self.nplanes * per <= _FBATCH_BYTES
+
+    def run_fbatch(self, uhat: torch.Tensor, uhat_fs: int, freqs: np.ndarray, ill_ptr: int,
+                   frame_w: torch.Tensor, vol: torch.Tensor, stream=None) -> None:
+        g = self.geom
+        nf = int(freqs.size)
+        key = ("fb", nf)
+        if getattr(self, "_fb_key", None) != key:
+            na = (g.py // 2 + 1) * (g.px // 2 + 1)
+            self._fb_ws_a = torch.empty((nf * self.nplanes * na,), dtype=torch.complex64,
+                                        device=self.device)
+            nb = self.nplanes * g.n_illum * g.ny * g.px
+            self._fb_ws_b = torch.empty((nf * nb,), dtype=torch.complex64, device=self.device)
+            self._fb_kt = torch.from_numpy(np.asarray(freqs, dtype=np.float64)
+                                           / (SPEED_OF_LIGHT * 2 * np.pi)).to(self.device)
+            self._fb_strides = (self.nplanes * na, nb)
+            self._fb_key = key
+        fa, fbs = self._fb_strides
+        _lib.call("pf_prop_fbatch", dev.ptr(self.planes_dev), self.nplanes, dev.ptr(self._fb_kt),
+                  nf, ctypes.byref(g), self.plan_x.ref, dev.ptr(self._fb_ws_a), fa, dev.ptr(uhat),
+                  uhat_fs, dev.ptr(self._fb_ws_b), fbs, ill_ptr, dev.ptr(frame_w), dev.ptr(vol),
+                  dev.stream_ptr(stream))
+
     def run_batches(self, body, stream=None) -> None:
         """Call ``body(b0, b1, lane, lane_stream)`` for every plane batch, alternating lanes.
 
@@ -352,6 +382,10 @@ class RsdEngine(GraphedRun):
             vol.zero_()
         uhat = self.relay_spectra(coeff, stream)
         per_f = self.n_illum * self.py * self.px
+        if self.prop.fbatch_ok(self.freqs.size, self.n_frames):
+            self.prop.run_fbatch(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w, vol,
+                                 stream)
+            return vol
 
         # plane batches outer, frequencies inner: the batch's volume slice stays
         # L2-resident across its ascending-frequency accumulation
