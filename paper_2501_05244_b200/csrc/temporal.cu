@@ -40,7 +40,7 @@ __device__ __forceinline__ void real_dft64(const float* x, float2* X) {
 }
 
 template <int M>
-__global__ void __launch_bounds__(K1_THREADS, 2)
+__global__ void __launch_bounds__(K1_THREADS)
 k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __restrict__ bins,
                const float2* __restrict__ twt /*[M][twt_ld]*/, int twt_ld,
                const float2* __restrict__ wphase, int F, float2* __restrict__ out,
@@ -58,22 +58,14 @@ k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __
 
   const int g = threadIdx.x / M;
   const int r = threadIdx.x - g * M;
-  // phase-B work split: TPP threads per (trace, bin) pair, each summing M/TPP terms
-  const int pairs = G * F;
-  int tpp = 1;
-  while (tpp * 2 * pairs <= K1_THREADS && tpp * 2 <= M && tpp < 32) tpp *= 2;
   const long long n_groups = (n_traces + G - 1) / G;
-  float x[64];
-  long long grp = blockIdx.x;
-  if (grp < n_groups) {
+  for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
     const long long trace = grp * G + g;
-    const float* h = hist + (trace < n_traces ? trace : 0) * (long long)T + r;
+    if (trace < n_traces) {
+      const float* h = hist + trace * (long long)T + r;
+      float x[64];
 #pragma unroll
-    for (int q = 0; q < 64; q++) x[q] = __ldg(h + q * M);
-  }
-  for (; grp < n_groups; grp += gridDim.x) {
-    const long long trace = grp * G + g;
-    {
+      for (int q = 0; q < 64; q++) x[q] = __ldg(h + q * M);
       float2 X[K1_KB];
       real_dft64(x, X);
       float2* dst = xs + g * TS + r * K1_KB;
@@ -81,40 +73,22 @@ k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __
       for (int k = 0; k < K1_KB; k++) dst[k] = X[k];
     }
     __syncthreads();
-    // prefetch the next group's samples: their latency hides behind phase B
-    const long long nxt = grp + gridDim.x;
-    if (nxt < n_groups) {
-      const long long tn = nxt * G + g;
-      const float* h = hist + (tn < n_traces ? tn : 0) * (long long)T + r;
-#pragma unroll
-      for (int q = 0; q < 64; q++) x[q] = __ldg(h + q * M);
-    }
-    const int n_work = pairs * tpp;
-    for (int wb = 0; wb < n_work; wb += K1_THREADS) {   // warp-uniform trip count
-      const int w = wb + threadIdx.x;
-      const bool valid = w < n_work;
-      const int p = valid ? w / tpp : 0, part = w - (w / tpp) * tpp;
+    for (int p = threadIdx.x; p < G * F; p += K1_THREADS) {
       const int gg = p % G, f = p / G;
       const long long tr = grp * G + gg;
+      if (tr >= n_traces) continue;
       const int k = kb[f];
       const bool cj = k > 32;
       const int kk = cj ? 64 - k : k;
       const float2* src = xs + gg * TS + kk;
       float2 acc = make_float2(0.f, 0.f);
-      const int r0 = part * (M / tpp), r1 = r0 + M / tpp;
 #pragma unroll 8
-      for (int rr = r0; rr < r1; rr++) {
+      for (int rr = 0; rr < M; rr++) {
         float2 z = src[rr * K1_KB];
         if (cj) z.y = -z.y;
         cacc(acc, z, tws[rr * F + f]);
       }
-      // combine the tpp partial sums (consecutive lanes)
-      for (int o = 1; o < tpp; o <<= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-      }
-      if (valid && part == 0 && tr < n_traces)
-        out[(long long)f * out_stride + tr] = cmul(acc, wphase[f]);
+      out[(long long)f * out_stride + tr] = cmul(acc, wphase[f]);
     }
     __syncthreads();
   }
