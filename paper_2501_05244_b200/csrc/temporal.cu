@@ -59,8 +59,6 @@ k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __
   const int g = threadIdx.x / M;
   const int r = threadIdx.x - g * M;
   const long long n_groups = (n_traces + G - 1) / G;
-  int tpp = 1;   // lanes per (trace, bin) pair in phase B (power of two <= 32)
-  while (tpp * 2 * G * F <= K1_THREADS && tpp * 2 <= M && tpp < 32) tpp *= 2;
   for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
     const long long trace = grp * G + g;
     if (trace < n_traces) {
@@ -75,34 +73,22 @@ k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __
       for (int k = 0; k < K1_KB; k++) dst[k] = X[k];
     }
     __syncthreads();
-    // phase B: TPP consecutive lanes share one (trace, bin) pair, M/TPP terms each
-    const int n_work = G * F * tpp;
-    for (int wb = 0; wb < n_work; wb += K1_THREADS) {   // warp-uniform trip count
-      const int w = wb + threadIdx.x;
-      const bool valid = w < n_work;
-      const int p = w / tpp, part = w - p * tpp;
-      const int gg = p % G, f = valid ? p / G : 0;
+    for (int p = threadIdx.x; p < G * F; p += K1_THREADS) {
+      const int gg = p % G, f = p / G;
       const long long tr = grp * G + gg;
+      if (tr >= n_traces) continue;
       const int k = kb[f];
       const bool cj = k > 32;
       const int kk = cj ? 64 - k : k;
       const float2* src = xs + gg * TS + kk;
       float2 acc = make_float2(0.f, 0.f);
-      if (valid) {
-        const int r0 = part * (M / tpp), r1 = r0 + M / tpp;
 #pragma unroll 8
-        for (int rr = r0; rr < r1; rr++) {
-          float2 z = src[rr * K1_KB];
-          if (cj) z.y = -z.y;
-          cacc(acc, z, tws[rr * F + f]);
-        }
+      for (int rr = 0; rr < M; rr++) {
+        float2 z = src[rr * K1_KB];
+        if (cj) z.y = -z.y;
+        cacc(acc, z, tws[rr * F + f]);
       }
-      for (int o = 1; o < tpp; o <<= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-      }
-      if (valid && part == 0 && tr < n_traces)
-        out[(long long)f * out_stride + tr] = cmul(acc, wphase[f]);
+      out[(long long)f * out_stride + tr] = cmul(acc, wphase[f]);
     }
     __syncthreads();
   }
