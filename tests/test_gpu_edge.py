@@ -1,0 +1,84 @@
+"""Edge cases of the GPU path against the oracle: degenerate sizes, single items, many illuminations."""
+
+import numpy as np
+import pytest
+
+import paper_2501_05244_b200 as pf
+from oracle import pf_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def _sl(rng, relay, n_freq=2, n_ill=1, planar_ill=True):
+    w0 = 2 * np.pi * 299792458.0 / 0.05
+    freqs = w0 * (1.0 + 0.05 * np.arange(n_freq))
+    coeff = rng.normal(size=(n_ill, relay.count, n_freq)) + 1j * rng.normal(size=(n_ill, relay.count, n_freq))
+    ill = rng.uniform(-0.1, 0.1, size=(n_ill, 2 if planar_ill else 3))
+    return pf.FrequencySlices(freqs, coeff, relay, pf.PointList(ill))
+
+
+@pytest.mark.parametrize("nx,ny", [(1, 1), (1, 7), (5, 1), (2, 3), (17, 13)])
+def test_rsd_tiny_and_ragged_relays(rng, nx, ny):
+    g = pf.UniformGrid2D(nx, ny, 0.02, 0.03, -0.01 * (nx - 1), -0.015 * (ny - 1), 0.0)
+    sl = _sl(rng, pf.UniformRelay(g), n_freq=1)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(nx, ny, 2, 0.02, 0.03, 0.2, g.x0, g.y0, 0.4))
+    assert O.rel_l2(pf.rsd(sl, grid).field, O.rsd(sl, grid)) < TOL
+    assert O.rel_l2(pf.rsd(sl, grid, padding="none").field,
+                    O.rsd(sl, grid, padding="none")) < TOL
+
+
+def test_rsd_single_voxel_and_three_illuminations(rng):
+    g = pf.UniformGrid2D(12, 12, 0.02, 0.02, -0.11, -0.11, 0.0)
+    sl = _sl(rng, pf.UniformRelay(g), n_freq=3, n_ill=3)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(1, 1, 1, 0.02, 0.02, 0.1, 0.01, -0.03, 0.5))
+    assert O.rel_l2(pf.rsd(sl, grid).field, O.rsd(sl, grid)) < TOL
+
+
+def test_rsd_relay_not_at_z0_and_3d_illumination(rng):
+    g = pf.UniformGrid2D(16, 16, 0.02, 0.02, -0.15, -0.15, 0.3)
+    sl = _sl(rng, pf.UniformRelay(g), n_freq=2, n_ill=2, planar_ill=False)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(16, 16, 2, 0.02, 0.02, 0.2, -0.15, -0.15, 0.8))
+    assert O.rel_l2(pf.rsd(sl, grid).field, O.rsd(sl, grid)) < TOL
+
+
+def test_nursd1_single_point_and_eps_range(rng):
+    rel = pf.NonUniformPlanarRelay(pf.PointList(np.array([[0.013, -0.021]])), 0.0)
+    sl = _sl(rng, rel, n_freq=2)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(6, 5, 2, 0.02, 0.02, 0.1, -0.05, -0.04, 0.5))
+    for eps in (1e-2, 1e-6, 1e-12):
+        assert O.rel_l2(pf.nursd1(sl, grid, eps=eps).field, O.nursd1(sl, grid, eps=eps)) < TOL
+    with pytest.raises(pf.ValidationError):
+        pf.nursd1(sl, grid, eps=0.5)
+
+
+def test_explicit_single_voxel_planes(rng):
+    g = pf.UniformGrid2D(10, 10, 0.02, 0.02, -0.09, -0.09, 0.0)
+    sl = _sl(rng, pf.UniformRelay(g), n_freq=2)
+    ev = pf.ExplicitVoxels(tuple(pf.VoxelPlane(z, pf.PointList(np.array([[0.003 * k, -0.01]])))
+                                 for k, z in enumerate((0.4, 0.5, 0.6))))
+    assert O.rel_l2(pf.nursd2(sl, ev).field, O.nursd2(sl, ev)) < TOL
+    assert O.rel_l2(pf.srsd_nursd2(sl, ev, alpha=0.8).field, O.srsd_nursd2(sl, ev, 0.8)) < TOL
+
+
+def test_srsd_single_plane_unit_scale_equals_rsd(rng):
+    g = pf.UniformGrid2D(16, 16, 0.02, 0.02, -0.15, -0.15, 0.0)
+    sl = _sl(rng, pf.UniformRelay(g), n_freq=2)
+    fr = pf.FrustumGrid(g, np.array([0.6]), np.ones(1), np.ones(1))
+    cub = pf.CuboidGrid(pf.UniformGrid3D(16, 16, 1, 0.02, 0.02, 0.1, -0.15, -0.15, 0.6))
+    assert O.rel_l2(pf.srsd(sl, fr).field, pf.rsd(sl, cub).field) < TOL
+
+
+def test_to_frequency_single_trace_and_short_window(rng):
+    relay = pf.NonUniformPlanarRelay(pf.PointList(np.zeros((1, 2))), 0.0)
+    ill = pf.PointList(np.zeros((1, 2)))
+    for T in (64, 100, 2):
+        h = rng.uniform(0, 1, size=(1, 1, T)).astype(np.float32)
+        try:
+            k = pf.build_kernel(0.3 * T * 16e-12 * 3e8 / 40 if T > 2 else 0.01, T, 16e-12,
+                                threshold=1e-6)
+        except pf.ValidationError:
+            continue
+        sl = pf.to_frequency(pf.TransientMeasurement(relay, ill, h, 16e-12), k)
+        ref = O.to_frequency(h, k.bin_indices, k.frequencies, k.weights, 0.0)
+        assert O.rel_l2(sl.coefficients, ref) < 1e-5
