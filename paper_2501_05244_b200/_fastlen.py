@@ -40,12 +40,15 @@ def next_pow2(target: int) -> int:
 
 
 def factorize(n: int) -> list[int]:
-    """Prime factors of ``n`` restricted to 2/3/5/7/11 (raises otherwise)."""
+    """Prime factors of ``n`` (2/3/5/7/11 get compile-time butterflies on the GPU,
+    larger primes a direct O(p^2) stage)."""
     out = []
-    for p in SMOOTH_PRIMES:
+    p = 2
+    while n > 1 and p * p <= n:
         while n % p == 0:
             out.append(p)
             n //= p
-    if n != 1:
-        raise ValueError(f"length has a prime factor above 11 (remaining {n})")
+        p += 1
+    if n > 1:
+        out.append(n)
     return out

@@ -166,6 +166,37 @@ __device__ __forceinline__ void stockham_stage(const float2* __restrict__ src,
   }
 }
 
+// Any radix (large prime factors, e.g. padding="none" on a prime-sized relay):
+// direct R-point DFT per butterfly straight from shared memory, O(R^2).
+template <int DIR>
+__device__ __noinline__ void stockham_stage_any(const float2* __restrict__ src,
+                                                float2* __restrict__ dst, int n, int Ns, int R,
+                                                int cnt, int ld, const float2* __restrict__ tw) {
+  const int nb = n / R;
+  const int total = nb * cnt * R;
+  const int twstride = n / (Ns * R);
+  const int wr = n / R;   // W_R^m = W_n^{m n/R}
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    const int ro = t % R;
+    const int bt = t / R;
+    const int b = bt / nb;
+    const int j = bt - b * nb;
+    const int k = j % Ns;
+    const float2* s = src + b * ld;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int ri = 0; ri < R; ri++) {
+      float2 x = s[j + ri * nb];
+      if (k != 0 && ri != 0) {
+        const float2 w = __ldg(tw + ri * k * twstride);
+        x = DIR < 0 ? cmul(x, w) : cmulc(x, w);
+      }
+      const float2 w2 = __ldg(tw + ((ri * ro) % R) * wr);
+      acc = cadd(acc, DIR < 0 ? cmul(x, w2) : cmulc(x, w2));
+    }
+    dst[b * ld + (j - k) * R + k + ro * Ns] = acc;
+  }
+}
+
 // Run the full transform on `cnt` length-n lines held in `a` (scratch `b`).
 // Caller must __syncthreads() after filling `a`.  Returns the buffer holding
 // the natural-order result; all threads are synchronised on return.
@@ -185,7 +216,8 @@ __device__ float2* fft_smem(float2* a, float2* b, int ld, int cnt, const pf_fft_
       case 7: stockham_stage<7, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
       case 8: stockham_stage<8, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
       case 11: stockham_stage<11, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
-      default: stockham_stage<16, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
+      case 16: stockham_stage<16, DIR>(src, dst, p.n, Ns, cnt, ld, tw); break;
+      default: stockham_stage_any<DIR>(src, dst, p.n, Ns, R, cnt, ld, tw); break;
     }
     __syncthreads();
     Ns *= R;

@@ -64,7 +64,7 @@ def test_to_frequency_sizes(rng, T):
     assert O.rel_l2(sl.coefficients, ref) < 2e-6
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 8, 11, 12, 16, 30, 49, 64, 121, 128, 140, 280,
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 8, 11, 12, 13, 16, 17, 30, 49, 64, 97, 121, 128, 140, 194, 280,
                                512, 525, 1024, 1050, 2048, 2100])
 def test_fft_lines_vs_numpy(rng, n):
     from paper_2501_05244_b200 import _device as dev
