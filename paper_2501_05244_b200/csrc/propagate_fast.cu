@@ -61,14 +61,15 @@ __device__ __forceinline__ float2 phase_turns(double r2, double kturns, float kt
   return turns_to_unit(kturns * (double)rf, kturns_f * (0.5f * e * ir));
 }
 
-template <int L>
-__global__ void __launch_bounds__(FT, 2)
+template <int L, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, 16 / NW)
 k_pa(const pf_plane* __restrict__ planes, double kturns_s, pf_prop_geom g,
      const float2* __restrict__ tw, float2* __restrict__ ws_a, FBatch fb) {
   const double kturns = fb.kturns ? fb.kturns[blockIdx.z] : kturns_s;
   ws_a += blockIdx.z * fb.ws_a_fs;
   constexpr int P = 32 * L, H = P / 2, NA = H + 1;
-  constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
+  constexpr int LPW = 32 / L, RPC = NW * LPW, SLD = RPC + 1;
+  constexpr int NT = NW * 32;
   extern __shared__ float2 sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = lane % L, line = lane / L;
@@ -107,8 +108,8 @@ k_pa(const pf_plane* __restrict__ planes, double kturns_s, pf_prop_geom g,
   const int nr = min(RPC, NA - jy0);
   float2* dst = ws_a + (long long)blockIdx.y * NA * NA + jy0;
   {
-    // thread -> (kx row within a group of FT/RPC rows, rr); stride FT/RPC rows per step
-    constexpr int KSTEP = FT / RPC;
+    // thread -> (kx row within a group of NT/RPC rows, rr); stride NT/RPC rows per step
+    constexpr int KSTEP = NT / RPC;
     const int rr = threadIdx.x % RPC, k0 = threadIdx.x / RPC;
     if (rr < nr) {
       float2* d = dst + (long long)k0 * NA + rr;
@@ -175,15 +176,16 @@ k_pb(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
 // MULTI: more than one illumination (contributions summed in registers first).
 // PRE: single frame and the CTA's volume rows fit next to the tile: they are
 // prefetched with cp.async at entry so the accumulate is load-free at the end.
-template <int L, bool MULTI, bool PRE>
-__global__ void __launch_bounds__(FT, MULTI ? 1 : 2)
+template <int L, bool MULTI, bool PRE, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, MULTI ? 8 / NW : 16 / NW)
 k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
      const float2* __restrict__ tw, const float2* __restrict__ ws_b,
      const double* __restrict__ ill, const float2* __restrict__ frame_w, int n_frames,
      float2* __restrict__ vol, long long vol_frame_stride) {
   constexpr int P = 32 * L;
-  constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
-  constexpr int UNION = (8 * WFFT_XCH > P * SLD) ? 8 * WFFT_XCH : P * SLD;
+  constexpr int LPW = 32 / L, RPC = NW * LPW, SLD = RPC + 1;
+  constexpr int NT = NW * 32;
+  constexpr int UNION = (NW * WFFT_XCH > P * SLD) ? NW * WFFT_XCH : P * SLD;
   extern __shared__ float2 sm[];
   float2* volbuf = sm + UNION;   // [RPC][nx] when PRE
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -200,7 +202,7 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
     for (int rr = 0; rr < nr; rr++) {
       const float2* src = vol + vol_row0 + (long long)rr * nx;
 #pragma unroll 4
-      for (int mo = threadIdx.x; mo < nx; mo += FT) cp_async8(volbuf + rr * nx + mo, src + mo);
+      for (int mo = threadIdx.x; mo < nx; mo += NT) cp_async8(volbuf + rr * nx + mo, src + mo);
     }
     cp_async_commit();
   }
@@ -213,7 +215,7 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
     const float2* src = ws_b + ((long long)blockIdx.y * g.n_illum + p) * (long long)P * ny + i0;
     if (p > 0) __syncthreads();
     {
-      constexpr int CSTEP = FT / RPC;
+      constexpr int CSTEP = NT / RPC;
       const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
       if (rr < nr) {
         const float2* q = src + (long long)c0 * ny + rr;
@@ -625,17 +627,26 @@ static int pf_persist_env() {
   return v;
 }
 
-template <int L>
+template <int L, int NW = 8>
 size_t smem_a() {
-  constexpr int P = 32 * L, NA = P / 2 + 1, RPC = 8 * (32 / L);
-  size_t x = 8 * WFFT_XCH, s = (size_t)NA * (RPC + 1);
+  constexpr int P = 32 * L, NA = P / 2 + 1, RPC = NW * (32 / L);
+  size_t x = NW * WFFT_XCH, s = (size_t)NA * (RPC + 1);
   return (x > s ? x : s) * sizeof(float2);
 }
-template <int L>
+template <int L, int NW = 8>
 size_t smem_c(int nx, bool pre) {
-  constexpr int P = 32 * L, RPC = 8 * (32 / L);
-  size_t x = 8 * WFFT_XCH, s = (size_t)P * (RPC + 1);
+  constexpr int P = 32 * L, RPC = NW * (32 / L);
+  size_t x = NW * WFFT_XCH, s = (size_t)P * (RPC + 1);
   return ((x > s ? x : s) + (pre ? (size_t)RPC * nx : 0)) * sizeof(float2);
+}
+
+static int pf_nw_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PF_NW");
+    v = (e && e[0] == '4') ? 4 : 8;
+  }
+  return v;
 }
 
 int nsm() {
@@ -666,7 +677,13 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     attr = true;
   }
   const double kturns = khat / PF_TWO_PI;
-  if (stage == 0) {
+  if (stage == 0 && pf_nw_env() == 4) {
+    static bool a6 = false;
+    if (!a6) { cudaFuncSetAttribute(k_pa<L, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); a6 = true; }
+    dim3 grid(pf_cdiv(NA, RPC / 2), nplanes, fb.nf);
+    k_pa<L, 4><<<grid, 128, smem_a<L, 4>(), st>>>(planes, kturns, g, tw, ws_a_out, fb);
+    PF_LAUNCH_CHECK("k_pa");
+  } else if (stage == 0) {
     dim3 grid(pf_cdiv(NA, RPC), nplanes, fb.nf);
     k_pa<L><<<grid, FT, smem_a<L>(), st>>>(planes, kturns, g, tw, ws_a_out, fb);
     PF_LAUNCH_CHECK("k_pa");
@@ -741,6 +758,20 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
       k_pcp<L, false><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames,
                                             vol, vfs, items);
     PF_LAUNCH_CHECK("k_pcp");
+  } else if (pf_nw_env() == 4 && g.n_illum == 1) {
+    static bool a7 = false;
+    if (!a7) {
+      cudaFuncSetAttribute(k_pc<L, false, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_pc<L, false, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      a7 = true;
+    }
+    dim3 grid(pf_cdiv(g.ny, RPC / 2), nplanes);
+    const bool pre = n_frames == 1 && frame_w != nullptr && getenv("PF_NOPRE") == nullptr &&
+                     (size_t)(RPC / 2) * g.nx * 8 <= 64 * 1024;
+    const size_t sm = smem_c<L, 4>(g.nx, pre);
+    if (pre) k_pc<L, false, true, 4><<<grid, 128, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
+    else k_pc<L, false, false, 4><<<grid, 128, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
+    PF_LAUNCH_CHECK("k_pc");
   } else {
     dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
     const bool pre = n_frames == 1 && frame_w != nullptr && (size_t)RPC * g.nx * 8 <= 64 * 1024;
