@@ -294,16 +294,13 @@ k_pb1(int nplanes, const float2* __restrict__ tw, float2* __restrict__ ws_a, FBa
   const int b = blockIdx.y;
   const bool active = row < NA;
   float2* arow = ws_a + ((long long)b * NA + (active ? row : 0)) * NA;
-  float2* tws = sm + 8 * WFFT_XCH;
-  wfft_stage_twiddles<L>(tws, tw);
   float2 v[32];
 #pragma unroll
   for (int m = 0; m < 32; m++) {
     const int jy = t + L * m;
     v[m] = arow[jy <= H ? jy : P - jy];
   }
-  __syncthreads();
-  wfft<L, -1, false, true>(v, sm + warp * WFFT_XCH, tws);
+  wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
   if (active) {
 #pragma unroll
     for (int m = 0; m <= 16; m++) {   // ky = t + L m <= P/2 for m < 16 (and m = 16, t = 0)
@@ -335,9 +332,6 @@ k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
   const pf_plane pl = planes[bb];
   const float2* grow = ws_a + ((long long)bb * NA + kx) * NA;
   const int ny = g.ny;
-  float2* tws = sm + 8 * WFFT_XCH;
-  wfft_stage_twiddles<L>(tws, tw);
-  __syncthreads();
   const int n_ill = MULTI ? g.n_illum : 1;
 #pragma unroll 1
   for (int p = 0; p < n_ill; p++) {
@@ -349,7 +343,7 @@ k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
       const int ky = t + L * m;
       w[m] = cmul(__ldg(grow + (ky <= H ? ky : P - ky)), __ldg(ucol + ky));
     }
-    wfft<L, 1, false, true>(w, sm + warp * WFFT_XCH, tws);
+    wfft<L, 1>(w, sm + warp * WFFT_XCH, tw);
     if (active) {
       float2* dcol = ws_b + ((long long)bb * g.n_illum + p) * (long long)P * ny + (long long)col * ny;
 #pragma unroll
@@ -701,7 +695,7 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
       cudaFuncSetAttribute(k_pb2<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       a4 = true;
     }
-    const size_t sm = (8 * WFFT_XCH + 32 * L) * sizeof(float2);
+    const size_t sm = 8 * WFFT_XCH * sizeof(float2);
     dim3 g1(pf_cdiv(NA, 8 * LPW), nplanes, fb.nf);
     k_pb1<L><<<g1, FT, sm, st>>>(nplanes, tw, const_cast<float2*>(ws_a), fb);
     PF_LAUNCH_CHECK("k_pb1");

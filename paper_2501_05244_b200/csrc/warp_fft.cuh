@@ -22,19 +22,17 @@ constexpr int WFFT_XCH = 32 * 33;  // float2 per warp exchange buffer
 // tw2[k1 * L + t] = W_n^{t k1} (one contiguous run per k1 across the lanes).
 // EARLY: issue the 31 twiddle loads before the first 32-point DFT so their
 // latency hides behind it (costs 62 registers; for kernels with headroom).
-// SMEM_TW: `tw_plan` points at a shared-memory copy of the k1-major table
-// itself (see wfft_stage_twiddles) instead of the plan table in global memory.
-template <int L, int DIR, bool EARLY = false, bool SMEM_TW = false>
+template <int L, int DIR, bool EARLY = false>
 __device__ __forceinline__ void wfft(float2 (&v)[32], float2* __restrict__ xch,
                                      const float2* __restrict__ tw_plan) {
   static_assert(L == 4 || L == 8 || L == 16 || L == 32, "L must be 4, 8, 16 or 32");
   const int lane = threadIdx.x & 31;
   const int t = lane % L;
-  const float2* __restrict__ tw = (SMEM_TW ? tw_plan : tw_plan + 32 * L) + t;
+  const float2* __restrict__ tw = tw_plan + 32 * L + t;
   if (EARLY) {
     float2 w[32];
 #pragma unroll
-    for (int k1 = 1; k1 < 32; k1++) w[k1] = SMEM_TW ? tw[k1 * L] : __ldg(tw + k1 * L);
+    for (int k1 = 1; k1 < 32; k1++) w[k1] = __ldg(tw + k1 * L);
     Dft<32, DIR>::run(v);
 #pragma unroll
     for (int k1 = 1; k1 < 32; k1++) v[k1] = DIR < 0 ? cmul(v[k1], w[k1]) : cmulc(v[k1], w[k1]);
@@ -43,7 +41,7 @@ __device__ __forceinline__ void wfft(float2 (&v)[32], float2* __restrict__ xch,
     if (t != 0) {
 #pragma unroll
       for (int k1 = 1; k1 < 32; k1++) {
-        const float2 w = SMEM_TW ? tw[k1 * L] : __ldg(tw + k1 * L);
+        const float2 w = __ldg(tw + k1 * L);
         v[k1] = DIR < 0 ? cmul(v[k1], w) : cmulc(v[k1], w);
       }
     }
@@ -66,11 +64,4 @@ __device__ __forceinline__ void wfft(float2 (&v)[32], float2* __restrict__ xch,
     for (int k2 = 0; k2 < L; k2++) v[q + Q * k2] = w[k2];
   }
   __syncwarp();
-}
-
-// copy the k1-major twiddles (32 L entries after the n unit roots) into shared memory
-template <int L>
-__device__ __forceinline__ void wfft_stage_twiddles(float2* __restrict__ dst,
-                                                    const float2* __restrict__ tw_plan) {
-  for (int e = threadIdx.x; e < 32 * L; e += blockDim.x) dst[e] = __ldg(tw_plan + 32 * L + e);
 }
