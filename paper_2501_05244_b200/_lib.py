@@ -62,6 +62,10 @@ _SIGNATURES = {
     "pf_prop_ws_spectrum": [_P(PfPropGeom), _i],
     "pf_prop_fbatch": [_vp, _i, _vp, _i, _P(PfPropGeom), _P(PfFftPlan), _vp, _i64, _vp, _i64, _vp,
                        _i64, _vp, _vp, _vp, _vp],
+    "pf_prop_mega_ws": [_P(PfPropGeom), _i, _i],
+    "pf_prop_mega": [_vp, _vp, _i, _vp, _P(PfPropGeom), _P(PfFftPlan), _vp, _i64, _vp, _vp, _i,
+                     _vp, _i64, _vp, _vp, _i, _i, _vp, _vp],
+    "pf_prop_mega_aborted": [_vp, _i],
     "pf_bluestein_lines": [_vp, _i64, _i64, _i64, _i, _i, _vp, _i64, _i64, _i64, _i, _i, _i, _i,
                            _P(PfFftPlan), _vp, _vp, _vp],
     "pf_bluestein_warp": [_i, _vp, _i64, _i64, _i, _i, _vp, _i64, _i64, _i, _i, _i, _P(PfFftPlan),
@@ -70,7 +74,7 @@ _SIGNATURES = {
     "pf_nufft_deconv": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp],
     "pf_nufft_place": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp],
     "pf_nufft_interp2_acc": [_P(PfNufftGeom), _vp, _vp, _vp, _i, _vp, _i64, _i, _vp, _d, _i, _f,
-                             _vp, _i, _vp, _i64, _i64, _vp],
+                             _vp, _i, _vp, _i64, _i64, _vp, _vp],
     "pf_kernel3d": [_vp, _i, _i, _i, _d, _d, _d, _d, _vp],
     "pf_cmul": [_vp, _vp, _i64, _i64, _f, _vp],
     "pf_copy_planes": [_vp, _i, _i64, _i64, _i64, _vp, _vp],
@@ -78,7 +82,7 @@ _SIGNATURES = {
     "pf_prop_rows_out": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp,
                          _i64, _vp],
 }
-_RESTYPES = {"pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
+_RESTYPES = {"pf_prop_mega_ws": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
              "pf_prop_ws_spectrum": ctypes.c_int64,
              "pf_prop_fast": ctypes.c_int}
 
@@ -86,7 +90,7 @@ _lib = None
 
 # calls that enqueue kernels (bench.py reports how many ran in its timed region)
 _LAUNCHERS = {"pf_temporal_dft", "pf_temporal_dft_direct", "pf_fft_lines", "pf_embed_centered",
-              "pf_prop_kernel_rows", "pf_prop_columns", "pf_prop_rows_out", "pf_prop_fbatch", "pf_bluestein_lines", "pf_bluestein_warp",
+              "pf_prop_kernel_rows", "pf_prop_columns", "pf_prop_rows_out", "pf_prop_fbatch", "pf_prop_mega", "pf_bluestein_lines", "pf_bluestein_warp",
               "pf_nufft_spread", "pf_nufft_deconv", "pf_nufft_place", "pf_nufft_interp2_acc",
               "pf_kernel3d", "pf_cmul", "pf_copy_planes", "pf_roll"}
 launch_count = 0

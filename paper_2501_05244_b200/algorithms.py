@@ -227,6 +227,9 @@ class _UhatPropEngine(GraphedRun):
             self.prop.run_fbatch(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w, vol,
                                  stream)
             return vol
+        if self.prop.run_mega(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w,
+                              self.n_frames, vol, self.n_voxels, stream):
+            return vol
 
         def body(b0, b1, lane, ls):
             for fi in range(self.freqs.size):
@@ -344,8 +347,9 @@ class _Type2Readout:
         self.points = []
         for (start, cnt, nux, nuy, pts, z) in geo:
             tor = np.column_stack([2.0 * np.pi * nux / px, 2.0 * np.pi * nuy / py])
-            xyz = np.column_stack([pts[:, 0], pts[:, 1], np.full(cnt, z)])
-            self.points.append((start, cnt, self.plan.points(tor),
+            npts = self.plan.points(tor, cell_sorted=True)
+            xyz = np.column_stack([pts[:, 0], pts[:, 1], np.full(cnt, z)])[npts.order]
+            self.points.append((start, cnt, npts,
                                 torch.from_numpy(np.ascontiguousarray(xyz)).to(device)))
         self.spec = torch.empty((I * py * px,), dtype=torch.complex64, device=device)
         self.fine = torch.empty((I, self.plan.fine_elems), dtype=torch.complex64, device=device)
@@ -371,7 +375,8 @@ class _Type2Readout:
                 _lib.call("pf_nufft_interp2_acc", self.plan.gref, dev.ptr(pts.i0),
                           dev.ptr(pts.d0), dev.ptr(xyz), cnt, dev.ptr(self.fine),
                           self.plan.fine_elems, I, dev.ptr(self.ill), khat, int(self.include),
-                          1.0 / (px * py), fw, self.n_frames, dev.ptr(vol), self.count, start, s)
+                          1.0 / (px * py), fw, self.n_frames, dev.ptr(vol), self.count, start,
+                          dev.ptr(pts.perm), s)
         return vol
 
 

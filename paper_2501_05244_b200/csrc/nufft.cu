@@ -179,7 +179,7 @@ __global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
                               int n_illum, const double* __restrict__ ill, double kturns,
                               int include_illum, float scale, const float2* __restrict__ frame_w,
                               int n_frames, float2* __restrict__ vol, long long vol_frame_stride,
-                              long long dst0) {
+                              long long dst0, const int* __restrict__ perm) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= npts) return;
   const int W = 2 * G.w + 1;
@@ -215,8 +215,9 @@ __global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
     }
     tot = cadd(tot, val);
   }
+  const long long lo = perm ? perm[l] : l;   // points may be stored cell-sorted
   for (int f = 0; f < n_frames; f++) {
-    float2* d = vol + f * vol_frame_stride + dst0 + l;
+    float2* d = vol + f * vol_frame_stride + dst0 + lo;
     *d = cadd(*d, cmul(tot, frame_w[f]));
   }
 }
@@ -272,13 +273,14 @@ extern "C" int pf_nufft_interp2_acc(const pf_nufft_geom* g, const int32_t* i0, c
                                     int64_t fine_stride, int n_illum, const double* ill,
                                     double khat, int include_illum, float scale,
                                     const void* frame_w, int n_frames, void* vol,
-                                    int64_t vol_frame_stride, int64_t dst0, void* stream) {
+                                    int64_t vol_frame_stride, int64_t dst0, const int32_t* perm,
+                                    void* stream) {
   PF_ARG_CHECK(g && g->dim == 2 && g->w <= 16 && npts >= 0, "pf_nufft_interp2_acc: bad args");
   if (npts == 0) return 0;
   k_interp2_acc<<<pf_cdiv(npts, 128), 128, 0, (cudaStream_t)stream>>>(
       *g, i0, d0, xyz, npts, (const float2*)fine, fine_stride, n_illum, ill, khat / PF_TWO_PI,
       include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride,
-      dst0);
+      dst0, perm);
   PF_LAUNCH_CHECK("k_interp2_acc");
   return 0;
 }

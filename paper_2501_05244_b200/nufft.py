@@ -83,8 +83,8 @@ class NufftPlan:
         return ctypes.byref(self.geom)
 
     # -- per-geometry point data ------------------------------------------------------
-    def points(self, pts: np.ndarray) -> "NufftPoints":
-        return NufftPoints(self, pts)
+    def points(self, pts: np.ndarray, cell_sorted: bool = False) -> "NufftPoints":
+        return NufftPoints(self, pts, cell_sorted)
 
 
 def check_points(pts, d: int) -> np.ndarray:
@@ -101,12 +101,18 @@ def check_points(pts, d: int) -> np.ndarray:
 
 
 class NufftPoints:
-    """Stencil anchors + tile buckets of one point set under one plan (device tensors)."""
+    """Stencil anchors + tile buckets of one point set under one plan (device tensors).
 
-    def __init__(self, plan: NufftPlan, pts: np.ndarray):
+    ``cell_sorted=True`` (type-2 readouts) stores the points ordered by their stencil
+    anchor so neighbouring threads gather overlapping fine-grid patches; ``perm`` maps
+    the stored order back to the caller's point index.
+    """
+
+    def __init__(self, plan: NufftPlan, pts: np.ndarray, cell_sorted: bool = False):
         pts = check_points(pts, plan.dim)
         L = pts.shape[0]
         self.n = L
+        self.order = None
         i0 = np.zeros((L, 3), dtype=np.int64)
         d0 = np.zeros((L, 3), dtype=np.float64)
         for a in range(3 - plan.dim, 3):
@@ -119,6 +125,12 @@ class NufftPoints:
             i0[:, a] = k
             d0[:, a] = k * h - xi
         dv = plan.device
+        self.perm = None
+        if cell_sorted:
+            order = np.lexsort([i0[:, 2], i0[:, 1], i0[:, 0]])
+            i0, d0 = i0[order], d0[order]
+            self.order = order
+            self.perm = torch.from_numpy(order.astype(np.int32)).to(dv)
         self.i0 = torch.from_numpy(i0.astype(np.int32)).to(dv)
         self.d0 = torch.from_numpy(d0.astype(np.float32)).to(dv)
         self._i0_host = i0

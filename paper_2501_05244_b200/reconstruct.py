@@ -44,6 +44,9 @@ _LANES = int(os.environ.get("PF_LANES", "3"))
 _FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "4"))
 _FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
 _FGROUP = int(os.environ.get("PF_FGROUP", "1"))
+_MEGA = os.environ.get("PF_MEGA", "0") == "1"   # measured slower
+_MEGA_LAG = int(os.environ.get("PF_MEGA_LAG", "2"))
+_MEGA_GP = int(os.environ.get("PF_MEGA_GP", "4"))
 
 
 # ---------------------------------------------------------------------------
@@ -260,6 +263,55 @@ class Propagator:
 
         self.run_batches(body, stream)
 
+    def run_mega(self, uhat: torch.Tensor, uhat_fs: int, freqs: np.ndarray, ill_ptr: int,
+                 frame_w: torch.Tensor, n_frames: int, vol: torch.Tensor, vol_frame_stride: int,
+                 stream=None) -> bool:
+        """All (plane, frequency) jobs in one persistent launch (``pf_prop_mega``).
+
+        Jobs run in groups of ``_MEGA_GP`` planes, frequencies ascending inside a
+        group, so a group's volume slice and each Uhat_f stay L2-resident.
+        Returns False when the register path does not apply.
+        """
+        if not (_MEGA and self.transposed):
+            return False
+        g = self.geom
+        nf = int(freqs.size)
+        key = (nf, n_frames)
+        if getattr(self, "_mega_key", None) != key:
+            lag = max(1, _MEGA_LAG)
+            slots = 3 * lag + 2
+            jobs, last = [], {}
+            for p0 in range(0, self.nplanes, max(1, _MEGA_GP)):
+                grp = range(p0, min(self.nplanes, p0 + max(1, _MEGA_GP)))
+                for f in range(nf):
+                    for p in grp:
+                        jobs.append((p, f, last.get(p, -1), 0))
+                        last[p] = len(jobs) - 1
+            self._mega_jobs = torch.tensor(jobs, dtype=torch.int32, device=self.device)
+            self._mega_kt = torch.from_numpy(np.asarray(freqs, dtype=np.float64)
+                                             / (SPEED_OF_LIGHT * 2 * np.pi)).to(self.device)
+            gref = ctypes.byref(g)
+            self._mega_wa = torch.empty(_lib.call("pf_prop_mega_ws", gref, slots, 0),
+                                        dtype=torch.complex64, device=self.device)
+            self._mega_wb = torch.empty(_lib.call("pf_prop_mega_ws", gref, slots, 1),
+                                        dtype=torch.complex64, device=self.device)
+            self._mega_ctr = torch.zeros(4 * len(jobs) + 2, dtype=torch.int32, device=self.device)
+            self._mega_cfg = (len(jobs), slots, lag)
+            self._mega_key = key
+        njobs, slots, lag = self._mega_cfg
+        _lib.call("pf_prop_mega", dev.ptr(self.planes_dev), dev.ptr(self._mega_jobs), njobs,
+                  dev.ptr(self._mega_kt), ctypes.byref(g), self.plan_x.ref, dev.ptr(uhat),
+                  uhat_fs, ill_ptr, dev.ptr(frame_w), n_frames, dev.ptr(vol), vol_frame_stride,
+                  dev.ptr(self._mega_wa), dev.ptr(self._mega_wb), slots, lag,
+                  dev.ptr(self._mega_ctr), dev.stream_ptr(stream))
+        return True
+
+    def mega_aborted(self) -> bool:
+        """True if the last persistent launch gave up on a dependency (after a sync)."""
+        if getattr(self, "_mega_cfg", None) is None:
+            return False
+        return bool(_lib.call("pf_prop_mega_aborted", dev.ptr(self._mega_ctr), self._mega_cfg[0]))
+
     def run_batches(self, body, stream=None) -> None:
         """Call ``body(b0, b1, lane, lane_stream)`` for every plane batch, alternating lanes.
 
@@ -421,6 +473,10 @@ class RsdEngine(GraphedRun):
         if _FGROUP > 1 and self.prop.transposed and self.n_frames == 1:
             self.prop.run_fgroups(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w, vol,
                                   _FGROUP, stream)
+            return vol
+
+        if self.prop.run_mega(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w,
+                              self.n_frames, vol, self.n_voxels, stream):
             return vol
 
         # plane batches outer, frequencies inner: the batch's volume slice stays

@@ -142,5 +142,5 @@ def nufft2(coefficients, points, eps: float):
     out = torch.zeros((L,), dtype=torch.complex64, device=device)
     _lib.call("pf_nufft_interp2_acc", plan.gref, dev.ptr(P.i0), dev.ptr(P.d0), dev.ptr(zero3), L,
               dev.ptr(fine), plan.fine_elems, 1, dev.ptr(ill), 0.0, 0, 1.0, dev.ptr(one), 1,
-              dev.ptr(out), L, 0, dev.stream_ptr())
+              dev.ptr(out), L, 0, None, dev.stream_ptr())
     return out.cpu().numpy().astype(np.complex128)
