@@ -202,7 +202,7 @@ def run_ours(args):
     # are in flight, so step i's upload overlaps step i-1's propagation
     hist_host = torch.empty(hist_shard.shape, dtype=torch.float32, pin_memory=True)
     hist_host.copy_(hist_shard)
-    n_e2e = max(3, min(args.steps, 6))
+    n_e2e = max(8, args.steps)
     for _ in range(2):
         rec.result(rec.submit(hist_host))
     torch.cuda.synchronize()
@@ -210,13 +210,18 @@ def run_ours(args):
         dist.barrier()
     t0 = time.perf_counter()
     handles = [rec.submit(hist_host) for _ in range(2)]
+    done_at = []
     for _ in range(n_e2e - 2):
         rec.result(handles.pop(0))
+        done_at.append(time.perf_counter())
         handles.append(rec.submit(hist_host))
     for h in handles:
         rec.result(h)
+        done_at.append(time.perf_counter())
     torch.cuda.synchronize()
-    e2e = (time.perf_counter() - t0) * 1e3 / n_e2e
+    e2e = (time.perf_counter() - t0) * 1e3 / n_e2e      # whole window, pipeline fill included
+    e2e_steady = (done_at[-1] - done_at[0]) * 1e3 / (len(done_at) - 1)
+    h2d_gbs = _h2d_probe(hist_host, device)
     # single-capture latency through the blocking call, for reference
     for _ in range(2):
         rec(hist_host)
@@ -242,6 +247,8 @@ def run_ours(args):
     if cfg.algorithm == "srsd":   # + per-unit Bluestein x (N rows) and y (P columns) passes
         Q = 2 * P
         s3_flops += units * (cfg.relay.grid.ny + P) * 2 * 5.0 * Q * math.log2(Q)
+    if cfg.algorithm == "nursd1":   # + per-(f, p) type-1 NUFFT: fine-grid FFT + 17x17 spread
+        s3_flops += F * I * (5.0 * (2 * P) ** 2 * math.log2((2 * P) ** 2) + cfg.relay.count * 17 * 17 * 8)
     fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
     clocks = clk.summary()
     roof_k1 = {"bound": "hbm", "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "peak": hbm_peak,
@@ -271,6 +278,9 @@ def run_ours(args):
         "stage_ms": {"k1": k1_ms, "propagation": s3_ms, "step_event": statistics.mean(t_step)},
         "e2e": {"value": cfg.n_voxels / (e2e * 1e-3), "unit": UNIT, "ms_per_step": e2e,
                 "single_capture_latency_ms": e2e_latency, "captures": n_e2e,
+                "steady_ms_per_step": e2e_steady,
+                "h2d_gbs_measured": h2d_gbs,
+                "h2d_floor_ms": hist_host.numel() * 4 / (h2d_gbs * 1e6),
                 "h2d_bytes_per_step": int(hist_host.numel() * 4 * world),
                 "d2h_bytes_per_step": int(cfg.n_voxels * 8),
                 "path": "TransientReconstructor.submit/result stream (pinned host f32 -> chunked "
@@ -313,6 +323,22 @@ def _traffic(kernel_prefix):
 # ---------------------------------------------------------------------------
 # CPU baselines (oracle port of the reference; test infrastructure)
 # ---------------------------------------------------------------------------
+
+
+def _h2d_probe(hist_host, device) -> float:
+    """Pinned host -> device copy bandwidth (GB/s) of one capture-sized transfer: the
+    floor of the e2e step when the capture does not fit the PCIe budget."""
+    dst = torch.empty_like(hist_host, device=device)
+    dst.copy_(hist_host, non_blocking=True)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(2):
+        dst.copy_(hist_host, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    del dst
+    return 2 * hist_host.numel() * 4 / (s.elapsed_time(e) * 1e-3) / 1e9
 
 
 def _cpu_units(cfg, n_f, n_k):

@@ -170,6 +170,12 @@ int pf_prop_mega(const pf_plane* planes, const int32_t* jobs, int njobs, const d
 /* After the stream synchronised: 1 if the launch abandoned a dependency wait. */
 int pf_prop_mega_aborted(const int32_t* counters, int njobs);
 
+/* out (device int32[2]) = {number of non-finite, number of negative} float32
+ * values in x[0..n): the payload checks of reference read_dataset
+ * (core.py:727-728, NaN/inf) and TransientMeasurement (counts >= 0) for
+ * histograms read straight into device memory.  x must be 16-byte aligned. */
+int pf_count_nonfinite(const float* x, int64_t n, int32_t* out, void* stream);
+
 /* ---------------------------------------------------------------- SFFT (Bluestein)
  * Scaled-DFT lines, replacing SfftPlan.apply (spectral.py:160-168) inside
  * sfft_2d_centered (:209-218): per plane b (grid y) the tables chirp[b][M] and

@@ -3,15 +3,20 @@
 Public names mirror the reference package ``phasorfield`` (reference
 ``__init__.py:19-89``) for the hot path: the phasor kernel and temporal
 transform, the eight reconstruction algorithms, the dispatcher, the video
-renderer and the depth projection, plus the boundary types.  Compute runs in
+renderer and the depth projection, the boundary types, and the NLS1
+containers on either side of the path (read straight to device memory,
+volumes written from it).  Compute runs in
 ``libpfgpu.so`` (hand-written sm_100a CUDA); there is no CPU fallback.
 """
 
-from .core import (PROPAGATION_SIGN, SPEED_OF_LIGHT, CuboidGrid, ExplicitVoxels,
-                   FrequencySlices, FrustumGrid, NonPlanarRelay, NonUniformPlanarRelay, PointList,
-                   ReconstructionVolume, TransientMeasurement, UniformGrid2D, UniformGrid3D,
-                   UniformRelay, ValidationError, VoxelPlane, grid_coordinates,
-                   illumination_coordinates)
+from .container import (DeviceTransientMeasurement, read_dataset, read_dataset_device,
+                        read_volume, write_dataset, write_volume)
+from .core import (PROPAGATION_SIGN, SPEED_OF_LIGHT, ContainerFormatError, CuboidGrid,
+                   ExplicitVoxels, FrequencySlices, FrustumGrid, InvalidMagicError,
+                   NonFiniteDataError, NonPlanarRelay, NonUniformPlanarRelay, PointList,
+                   ReconstructionVolume, TransientMeasurement, TruncatedPayloadError,
+                   UniformGrid2D, UniformGrid3D, UniformRelay, UnsupportedVersionError,
+                   ValidationError, VoxelPlane, grid_coordinates, illumination_coordinates)
 from .phasor import (DeviceFrequencySlices, PhasorKernel, build_kernel, to_frequency,
                      to_frequency_device)
 from .reconstruct import (ALGORITHM_NAMES, RsdEngine, light_transport_video, project_max_depth,

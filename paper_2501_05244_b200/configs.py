@@ -4,7 +4,8 @@ Shared conventions: relay lattice cell-centred on [-1, 1]^2, laser at the
 relay centre, scatterers uniform with ``default_rng(1000 + c)``, albedo
 U[0.5, 1], transients per ``sim.simulate_device`` (out-of-window returns
 dropped), Poisson noise at a mean peak of 100 counts, kernel from
-``build_kernel`` (default threshold) -> F = 16/16/16/24/32.
+``build_kernel`` (default threshold) -> F = 16/16/16/24/32.  Config 5 is
+SURVEY 8(d)'s "c4 NURSD1" row (config 4 on 50 % of the lattice nodes).
 """
 
 from __future__ import annotations
@@ -110,6 +111,20 @@ def config(c: int) -> Config:
                                                   g2.y0, 0.5))
         return Config("c4", core.UniformRelay(g2), ill, grid, sc, al, T, dt, lam,
                       0.9 / SPEED_OF_LIGHT, "rsd", seed)
+    if c == 5:
+        # "c4 NURSD1": the config-4 scene seen by 131,072 seeded
+        # lattice nodes (50 %) as a scattered planar relay; nursd1 on these
+        # on-lattice points must equal rsd on the zero-filled lattice (F4)
+        base = config(4)
+        g2 = base.relay.grid
+        keep = np.sort(np.random.default_rng(seed).choice(g2.nx * g2.ny, size=131072,
+                                                          replace=False))
+        pts = core.grid_coordinates(g2).points[keep]
+        relay = core.NonUniformPlanarRelay(core.PointList(pts), g2.z)
+        cfg = Config("c4-nursd1", relay, ill, base.grid, base.scatterers, base.albedo,
+                     base.n_bins, base.delta_t, base.lambda_c, base.t0, "nursd1", seed)
+        cfg.lattice_nodes = keep
+        return cfg
     raise ValueError(f"config {c} is not a bench configuration")
 
 

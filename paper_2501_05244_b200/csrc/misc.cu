@@ -104,3 +104,56 @@ extern "C" int pf_roll(const void* src, void* dst, int64_t nb, int n0, int n1, i
   PF_LAUNCH_CHECK("k_roll3");
   return 0;
 }
+
+// ---- payload check for containers read straight into device memory:
+// out[0] = non-finite count (reference read_dataset core.py:727-728 rejects
+// NaN/inf), out[1] = negative count (TransientMeasurement requires photon
+// counts >= 0).  HBM-bound single pass, 16-byte loads, one atomic per CTA.
+__device__ __forceinline__ int neg(float v) { return v < 0.f; }
+__global__ void k_count_nonfinite(const float* __restrict__ x, long long n, int* out) {
+  int bad = 0, ng = 0;
+  const long long n4 = n >> 2;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = __ldcs(x4 + i);
+    bad += !isfinite(v.x) + !isfinite(v.y) + !isfinite(v.z) + !isfinite(v.w);
+    ng += neg(v.x) + neg(v.y) + neg(v.z) + neg(v.w);
+  }
+  if (blockIdx.x == 0)
+    for (long long i = (n4 << 2) + threadIdx.x; i < n; i += blockDim.x) {
+      bad += !isfinite(x[i]);
+      ng += neg(x[i]);
+    }
+  bad = __reduce_add_sync(0xffffffffu, bad);
+  ng = __reduce_add_sync(0xffffffffu, ng);
+  __shared__ int wsum[2][32];
+  if ((threadIdx.x & 31) == 0) {
+    wsum[0][threadIdx.x >> 5] = bad;
+    wsum[1][threadIdx.x >> 5] = ng;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const bool in = threadIdx.x < (blockDim.x >> 5);
+    const int b = __reduce_add_sync(0xffffffffu, in ? wsum[0][threadIdx.x] : 0);
+    const int g = __reduce_add_sync(0xffffffffu, in ? wsum[1][threadIdx.x] : 0);
+    if (threadIdx.x == 0 && b) atomicAdd(out, b);
+    if (threadIdx.x == 0 && g) atomicAdd(out + 1, g);
+  }
+}
+
+extern "C" int pf_count_nonfinite(const float* x, int64_t n, int32_t* out, void* stream) {
+  PF_ARG_CHECK(n >= 0 && out && (n == 0 || x), "pf_count_nonfinite: bad arguments");
+  PF_ARG_CHECK(((uintptr_t)x & 15) == 0, "pf_count_nonfinite: x must be 16-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(out, 0, 2 * sizeof(int32_t), st);
+  if (n == 0) return 0;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  long long want = ((n >> 2) + 255) / 256;
+  const int grid = (int)(want < 8LL * nsm ? (want > 0 ? want : 1) : 8LL * nsm);
+  k_count_nonfinite<<<grid, 256, 0, st>>>(x, n, out);
+  PF_LAUNCH_CHECK("k_count_nonfinite");
+  return 0;
+}

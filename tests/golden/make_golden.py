@@ -258,7 +258,38 @@ def pfo_literal(sl, voxels):
     return literal_field(sl, voxels)
 
 
+def gen_containers():
+    """NLS1 files written by the reference writers (core.py:676-806): every relay
+    kind and every volume grid kind, static and time-resolved."""
+    from phasorfield import core as C
+    rng = np.random.default_rng(707)
+    d = os.path.join(OUT, "nls1")
+    os.makedirs(d, exist_ok=True)
+    ill = pf.PointList(np.array([[0.0, 0.0], [0.1, -0.05]]))
+    relays = {
+        "uniform": pf.UniformRelay(pf.UniformGrid2D(4, 3, 0.02, 0.025, -0.03, -0.025, 0.0)),
+        "planar": pf.NonUniformPlanarRelay(pf.PointList(rng.uniform(-0.1, 0.1, (5, 2))), 0.01),
+        "nonplanar": pf.NonPlanarRelay(pf.PointList(rng.uniform(-0.1, 0.1, (6, 3)))),
+    }
+    for name, relay in relays.items():
+        hist = rng.poisson(3.0, size=(2, relay.count, 8)).astype(np.float64)
+        m = C.TransientMeasurement(relay, ill, hist, 4e-12, 1.5e-9)
+        C.write_dataset(m, os.path.join(d, f"dataset_{name}.nls1"))
+    cub = pf.CuboidGrid(UniformGrid3D(3, 2, 2, 0.02, 0.025, 0.1, -0.02, -0.0125, 0.5))
+    fru = pf.FrustumGrid(pf.UniformGrid2D(3, 2, 0.02, 0.025, -0.02, -0.0125, 0.0),
+                         np.array([0.5, 0.7]), np.array([1.0, 0.7]), np.array([1.0, 0.6]))
+    exp = pf.ExplicitVoxels((pf.VoxelPlane(0.5, pf.PointList(rng.uniform(-0.1, 0.1, (3, 2)))),
+                             pf.VoxelPlane(0.8, pf.PointList(rng.uniform(-0.1, 0.1, (2, 2))))))
+    for name, grid in (("cuboid", cub), ("frustum", fru), ("explicit", exp)):
+        f = rng.normal(size=grid.count) + 1j * rng.normal(size=grid.count)
+        C.write_volume(C.ReconstructionVolume(grid, f), os.path.join(d, f"volume_{name}.nls1"))
+    times = np.array([0.0, 1e-10, 2.5e-10])
+    fv = rng.normal(size=(3, cub.count)) + 1j * rng.normal(size=(3, cub.count))
+    C.write_volume(C.ReconstructionVolume(cub, fv, times), os.path.join(d, "volume_video.nls1"))
+
+
 if __name__ == "__main__":
     gen_kernel_and_transform()
     gen_spectral()
     gen_reconstruct()
+    gen_containers()
