@@ -328,6 +328,7 @@ def _traffic(kernel_prefix):
 def _h2d_probe(hist_host, device) -> float:
     """Pinned host -> device copy bandwidth (GB/s) of one capture-sized transfer: the
     floor of the e2e step when the capture does not fit the PCIe budget."""
+    import torch
     dst = torch.empty_like(hist_host, device=device)
     dst.copy_(hist_host, non_blocking=True)
     torch.cuda.synchronize()

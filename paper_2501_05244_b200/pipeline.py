@@ -169,6 +169,10 @@ class TransientReconstructor:
             self.engine.run(coeff, sl["vol"], main)
         vol = sl["vol"]
         if self.volume_gather is not None:
+            # the gathered volume lives in one buffer (rank 0): the previous capture's
+            # device->host read of it must finish before this gather overwrites it
+            if self._last_d2h is not None:
+                main.wait_event(self._last_d2h)
             vol = self.volume_gather(sl["vol"])
         done = torch.cuda.Event()
         if vol is not None:
@@ -178,6 +182,7 @@ class TransientReconstructor:
                 sl["host"].copy_(vol, non_blocking=True)
                 sl["vol_free"].record(self.d2h_stream)
                 done.record(self.d2h_stream)
+            self._last_d2h = done
         else:
             sl["vol_free"].record(main)
             done.record(main)
@@ -191,6 +196,7 @@ class TransientReconstructor:
 
     def _init_slots(self, hist_host):
         self.d2h_stream = torch.cuda.Stream(device=self.device)
+        self._last_d2h = None
         self._next = 0
         self._slots = []
         vshape = self.vol.shape
