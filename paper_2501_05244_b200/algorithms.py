@@ -10,6 +10,7 @@ readout (product -> place -> inverse FFT -> interpolate+accumulate).
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 
 import numpy as np
@@ -324,6 +325,9 @@ def _explicit_geo(grid, cx, cy, dx, dy, sx=1.0, sy=1.0):
     return geo
 
 
+_READOUT_BYTES = int(os.environ.get("PF_READOUT_MB", "256")) << 20   # spectra + fine grids per batch
+
+
 class _Type2Readout:
     """cfft2(G_k) * Uhat -> nufft2 at the plane's voxels * scale * illumination phase."""
 
@@ -340,10 +344,13 @@ class _Type2Readout:
         self.include = bool(include_illumination)
         planes = [PlaneSpec(z - z_src, lag_dx, lag_dy, 0, 1, 0, 1, z, 0, i)
                   for i, (*_, z) in enumerate(geo)]
-        self.prop = Propagator(device, px, py, px, py, 0, 0, I, include_illumination, planes,
-                               py * px, batch=1)
-        self.prop.geom.flags = 1      # register path off: generic product-only columns
         self.plan = nu.NufftPlan((py, px), eps, device)
+        # planes per launch: product spectra and fine grids of a whole batch resident
+        per_plane = 8 * I * (self.plan.fine_elems + py * px)
+        self.nb = max(1, min(len(planes), _READOUT_BYTES // per_plane))
+        self.prop = Propagator(device, px, py, px, py, 0, 0, I, include_illumination, planes,
+                               py * px, batch=self.nb)
+        self.prop.geom.flags = 1      # register path off: generic product-only columns
         self.points = []
         for (start, cnt, nux, nuy, pts, z) in geo:
             tor = np.column_stack([2.0 * np.pi * nux / px, 2.0 * np.pi * nuy / py])
@@ -351,8 +358,9 @@ class _Type2Readout:
             xyz = np.column_stack([pts[:, 0], pts[:, 1], np.full(cnt, z)])[npts.order]
             self.points.append((start, cnt, npts,
                                 torch.from_numpy(np.ascontiguousarray(xyz)).to(device)))
-        self.spec = torch.empty((I * py * px,), dtype=torch.complex64, device=device)
-        self.fine = torch.empty((I, self.plan.fine_elems), dtype=torch.complex64, device=device)
+        self.spec = torch.empty((self.nb * I * py * px,), dtype=torch.complex64, device=device)
+        self.fine = torch.empty((self.nb * I, self.plan.fine_elems), dtype=torch.complex64,
+                                device=device)
         self.ill = _ill_tensor(slices, device)
         self.frame_w = _frame_weights(self.freqs, times, device)
 
@@ -361,22 +369,28 @@ class _Type2Readout:
         I, py, px = self.n_illum, self.py, self.px
         gref = ctypes.byref(self.prop.geom)
         base = dev.ptr(self.prop.planes_dev)
+        fine_b = self.plan.fine_elems * 8
+        nplanes = len(self.points)
         for fi in range(self.freqs.size):
             khat = float(self.freqs[fi]) / C
             uhat = uhat_of(fi)
             fw = dev.ptr(self.frame_w) + 8 * fi * self.n_frames
-            for k, (start, cnt, pts, xyz) in enumerate(self.points):
-                pp = base + k * self.prop.plane_size
-                _lib.call("pf_prop_kernel_rows", pp, 1, khat, gref, self.prop.plan_x.ref,
+            for b0 in range(0, nplanes, self.nb):
+                n = min(self.nb, nplanes - b0)
+                pp = base + b0 * self.prop.plane_size
+                _lib.call("pf_prop_kernel_rows", pp, n, khat, gref, self.prop.plan_x.ref,
                           dev.ptr(self.prop.ws_a), s)
-                _lib.call("pf_prop_columns", pp, 1, gref, self.prop.plan_y.ref,
+                _lib.call("pf_prop_columns", pp, n, gref, self.prop.plan_y.ref,
                           dev.ptr(self.prop.ws_a), dev.ptr(uhat), dev.ptr(self.spec), 1, s)
-                nu.place_and_inverse(self.plan, self.spec, I, py * px, self.fine, stream)
-                _lib.call("pf_nufft_interp2_acc", self.plan.gref, dev.ptr(pts.i0),
-                          dev.ptr(pts.d0), dev.ptr(xyz), cnt, dev.ptr(self.fine),
-                          self.plan.fine_elems, I, dev.ptr(self.ill), khat, int(self.include),
-                          1.0 / (px * py), fw, self.n_frames, dev.ptr(vol), self.count, start,
-                          dev.ptr(pts.perm), s)
+                nu.place_and_inverse(self.plan, self.spec, n * I, py * px, self.fine, stream)
+                for k in range(b0, b0 + n):
+                    start, cnt, pts, xyz = self.points[k]
+                    _lib.call("pf_nufft_interp2_acc", self.plan.gref, dev.ptr(pts.i0),
+                              dev.ptr(pts.d0), dev.ptr(xyz), cnt,
+                              dev.ptr(self.fine) + (k - b0) * I * fine_b, self.plan.fine_elems,
+                              I, dev.ptr(self.ill), khat, int(self.include), 1.0 / (px * py), fw,
+                              self.n_frames, dev.ptr(vol), self.count, start, dev.ptr(pts.perm),
+                              s)
         return vol
 
 
@@ -385,34 +399,63 @@ def _readout_setup(slices, grid, times):
     return dev.require_cuda(), _check_times(times)
 
 
+class Nursd2Engine(GraphedRun):
+    """Device plan of :func:`nursd2` (reconstruct.py:413-459) for one geometry; reusable.
+
+    ``slices`` only supplies geometry (uniform relay, frequencies, illuminations);
+    ``run(coeff)`` takes frequency-major device coefficients [F, I, D].
+    """
+
+    def __init__(self, slices, grid, eps: float = 1e-6, times=None,
+                 include_illumination: bool = True, device=None):
+        _require(_kind(grid) == "explicit", "nursd2 reconstructs onto explicit voxels")
+        relay = _uniform_relay(slices)
+        g = relay.grid
+        cx, cy = g.center()
+        geo = _explicit_geo(grid, cx, cy, g.dx, g.dy)
+        _check_depths(np.asarray([t[-1] for t in geo]), g.z)
+        self.times = _check_times(times)
+        self.device = device or dev.require_cuda()
+        jx_lo, jx_hi = -(g.nx // 2), g.nx - g.nx // 2 - 1
+        jy_lo, jy_hi = -(g.ny // 2), g.ny - g.ny // 2 - 1
+        ax = np.concatenate([t[2] for t in geo])
+        ay = np.concatenate([t[3] for t in geo])
+        px = _pad_size(max(ax.max() - jx_lo, jx_hi - ax.min()), max(abs(ax).max(), g.nx // 2),
+                       g.nx)
+        py = _pad_size(max(ay.max() - jy_lo, jy_hi - ay.min()), max(abs(ay).max(), g.ny // 2),
+                       g.ny)
+        self.relay_grid, self.px, self.py = g, px, py
+        self.ro = _Type2Readout(self.device, slices, grid, geo, px, py, g.dx, g.dy, g.z, eps,
+                                include_illumination, self.times)
+        self.freqs, self.n_illum, self.n_frames = self.ro.freqs, self.ro.n_illum, self.ro.n_frames
+        self.n_voxels = grid.count
+        F, I = self.freqs.size, self.n_illum
+        self.uhat = torch.empty((F * I * py * px,), dtype=torch.complex64, device=self.device)
+
+    def relay_spectra(self, coeff, stream=None):
+        """Uhat_f = cfft2(pad_embed(u_f)), natural order (reconstruct.py:441-443)."""
+        g, F, I = self.relay_grid, self.freqs.size, self.n_illum
+        _lib.call("pf_embed_centered", dev.ptr(coeff), F * I, g.ny, g.nx, g.ny * g.nx,
+                  dev.ptr(self.uhat), self.py, self.px, 0, dev.stream_ptr(stream))
+        dev.fft2_natural(self.uhat, self.py, self.px, F * I, -1, 1.0, stream)
+        return self.uhat
+
+    def run(self, coeff, vol=None, stream=None):
+        if vol is None:
+            vol = torch.zeros((self.n_frames, self.n_voxels), dtype=torch.complex64,
+                              device=self.device)
+        else:
+            vol.zero_()
+        uhat = self.relay_spectra(coeff, stream)
+        per_f = self.n_illum * self.py * self.px
+        return self.ro.run(lambda fi: uhat[fi * per_f:], vol, stream)
+
+
 def nursd2(slices, grid, eps: float = 1e-6, times=None, threads: int = 1,
            include_illumination: bool = True):
     """Uniform relay -> explicit voxels (reconstruct.py:413-459)."""
-    _require(_kind(grid) == "explicit", "nursd2 reconstructs onto explicit voxels")
-    relay = _uniform_relay(slices)
-    g = relay.grid
-    cx, cy = g.center()
-    geo = _explicit_geo(grid, cx, cy, g.dx, g.dy)
-    _check_depths(np.asarray([t[-1] for t in geo]), g.z)
-    times = _check_times(times)
-    device = dev.require_cuda()
-    jx_lo, jx_hi = -(g.nx // 2), g.nx - g.nx // 2 - 1
-    jy_lo, jy_hi = -(g.ny // 2), g.ny - g.ny // 2 - 1
-    ax = np.concatenate([t[2] for t in geo])
-    ay = np.concatenate([t[3] for t in geo])
-    px = _pad_size(max(ax.max() - jx_lo, jx_hi - ax.min()), max(abs(ax).max(), g.nx // 2), g.nx)
-    py = _pad_size(max(ay.max() - jy_lo, jy_hi - ay.min()), max(abs(ay).max(), g.ny // 2), g.ny)
-    ro = _Type2Readout(device, slices, grid, geo, px, py, g.dx, g.dy, g.z, eps,
-                       include_illumination, times)
-    coeff = device_coefficients(slices)
-    F, I = ro.freqs.size, ro.n_illum
-    uhat = torch.empty((F * I * py * px,), dtype=torch.complex64, device=device)
-    _lib.call("pf_embed_centered", dev.ptr(coeff), F * I, g.ny, g.nx, g.ny * g.nx, dev.ptr(uhat),
-              py, px, 0, dev.stream_ptr())
-    dev.fft2_natural(uhat, py, px, F * I, -1)
-    vol = torch.zeros((ro.n_frames, grid.count), dtype=torch.complex64, device=device)
-    ro.run(lambda fi: uhat[fi * I * py * px:], vol)
-    return _volume(grid, vol, times)
+    eng = Nursd2Engine(slices, grid, eps, times, include_illumination)
+    return _volume(grid, eng.run(device_coefficients(slices)), eng.times)
 
 
 def nursd3(slices, grid, eps: float = 1e-6, lattice_pitch: float | None = None, times=None,
@@ -649,8 +692,7 @@ def rsd3d(slices, grid, scatter: str = "trilinear", z_pitch: float | None = None
 # ---------------------------------------------------------------------------
 
 
-def nursd3d_explicit(slices, grid, lattice, eps: float = 1e-6, z_pitch: float | None = None,
-                     times=None, threads: int = 1, include_illumination: bool = True):
+class Nursd3dExplicitEngine(GraphedRun):
     """Non-planar relay -> explicit voxels: the paper's 3D NURSD + NURSD-2 fusion.
 
     The reference has no single entry point for this; it is composed
@@ -660,25 +702,44 @@ def nursd3d_explicit(slices, grid, lattice, eps: float = 1e-6, z_pitch: float | 
     (``_lattice_3d``, :594-621); that plane, in the lattice's centred slot
     order, becomes a uniform relay at z0 whose coefficients ``nursd2``
     (:413-459) reads out at the explicit voxels (every voxel plane beyond z0).
+    Geometry-only planning (NUFFT plans, point buckets, pads) happens once here;
+    ``run(coeff)`` is the per-capture work (and can be replayed as a CUDA graph).
     """
-    from .core import FrequencySlices, PointList, UniformGrid2D, UniformRelay
-    _require(_kind(grid) == "explicit", "nursd3d-explicit reconstructs onto explicit voxels")
-    _require(_kind(lattice) == "cuboid", "the stage-1 lattice must be a cuboid grid")
-    eng = Nursd3dEngine(slices, lattice, eps, z_pitch, include_illumination, None)
-    coeff = device_coefficients(slices)
-    F, I = eng.freqs.size, eng.n_illum
-    px, py = eng.px, eng.py
-    planes = eng.virtual_planes(coeff).view(F * I, py, px)
-    # natural -> centred slot order (fftshift) and relay coefficient layout [F][I][py*px]
-    slot = torch.empty_like(planes)
-    _lib.call("pf_roll", dev.ptr(planes), dev.ptr(slot), F * I, 1, py, px, 0, py - py // 2,
-              px - px // 2, dev.stream_ptr())
-    vg = lattice.grid
-    cx = vg.x0 + (vg.nx // 2) * vg.dx
-    cy = vg.y0 + (vg.ny // 2) * vg.dy
-    vrel = UniformRelay(UniformGrid2D(px, py, vg.dx, vg.dy, cx - (px // 2) * vg.dx,
-                                      cy - (py // 2) * vg.dy, eng.z0))
-    from .phasor import DeviceFrequencySlices
-    vs = DeviceFrequencySlices(slices.frequencies, slot.view(F, I, py * px), vrel,
-                               slices.illuminations)
-    return nursd2(vs, grid, eps=eps, times=times, include_illumination=include_illumination)
+
+    def __init__(self, slices, grid, lattice, eps: float = 1e-6, z_pitch: float | None = None,
+                 times=None, include_illumination: bool = True, device=None):
+        from .core import UniformGrid2D, UniformRelay
+        _require(_kind(grid) == "explicit",
+                 "nursd3d-explicit reconstructs onto explicit voxels")
+        _require(_kind(lattice) == "cuboid", "the stage-1 lattice must be a cuboid grid")
+        self.device = device or dev.require_cuda()
+        self.stage1 = Nursd3dEngine(slices, lattice, eps, z_pitch, include_illumination, None,
+                                    device=self.device)
+        px, py = self.stage1.px, self.stage1.py
+        vg = lattice.grid
+        cx = vg.x0 + (vg.nx // 2) * vg.dx
+        cy = vg.y0 + (vg.ny // 2) * vg.dy
+        vrel = UniformRelay(UniformGrid2D(px, py, vg.dx, vg.dy, cx - (px // 2) * vg.dx,
+                                          cy - (py // 2) * vg.dy, self.stage1.z0))
+        meta = type("VirtualSlices", (), dict(frequencies=np.asarray(slices.frequencies),
+                                              relay=vrel, illuminations=slices.illuminations))()
+        self.stage2 = Nursd2Engine(meta, grid, eps, times, include_illumination, self.device)
+        self.times, self.n_frames = self.stage2.times, self.stage2.n_frames
+        F, I = self.stage2.freqs.size, self.stage2.n_illum
+        self.slot = torch.empty((F * I * py * px,), dtype=torch.complex64, device=self.device)
+
+    def run(self, coeff, vol=None, stream=None):
+        st1 = self.stage1
+        F, I, px, py = st1.freqs.size, st1.n_illum, st1.px, st1.py
+        planes = st1.virtual_planes(coeff, stream)
+        # natural -> centred slot order (fftshift) and relay coefficient layout [F][I][py*px]
+        _lib.call("pf_roll", dev.ptr(planes), dev.ptr(self.slot), F * I, 1, py, px, 0,
+                  py - py // 2, px - px // 2, dev.stream_ptr(stream))
+        return self.stage2.run(self.slot.view(F, I, py * px), vol, stream)
+
+
+def nursd3d_explicit(slices, grid, lattice, eps: float = 1e-6, z_pitch: float | None = None,
+                     times=None, threads: int = 1, include_illumination: bool = True):
+    """Config-2 path (see :class:`Nursd3dExplicitEngine`)."""
+    eng = Nursd3dExplicitEngine(slices, grid, lattice, eps, z_pitch, times, include_illumination)
+    return _volume(grid, eng.run(device_coefficients(slices)), eng.times)

@@ -137,6 +137,21 @@ struct Dft<11, DIR> {
 };
 
 // One Stockham stage over `cnt` transforms (transform b at buf + b*ld).
+// Division by a block-invariant divisor d >= 1 for 0 <= x < 2^22:
+// float reciprocal estimate plus one integer correction (exact in that range),
+// instead of the ~20-instruction integer division sequence.
+struct FastDiv {
+  int d;
+  float inv;
+  __device__ __forceinline__ explicit FastDiv(int dd) : d(dd), inv(1.0f / (float)dd) {}
+  __device__ __forceinline__ int div(int x) const {
+    int q = __float2int_rz((float)x * inv);
+    const int r = x - q * d;
+    q += (r >= d) - (r < 0);
+    return q;
+  }
+};
+
 template <int R, int DIR>
 __device__ __forceinline__ void stockham_stage(const float2* __restrict__ src,
                                                float2* __restrict__ dst, int n, int Ns,
@@ -144,14 +159,15 @@ __device__ __forceinline__ void stockham_stage(const float2* __restrict__ src,
   const int nb = n / R;
   const int total = nb * cnt;
   const int twstride = n / (Ns * R);
+  const FastDiv by_nb(nb), by_ns(Ns);
   for (int t = threadIdx.x; t < total; t += blockDim.x) {
-    const int b = t / nb;
+    const int b = by_nb.div(t);
     const int j = t - b * nb;
     const float2* s = src + b * ld;
     float2 v[R];
 #pragma unroll
     for (int r = 0; r < R; r++) v[r] = s[j + r * nb];
-    const int k = j % Ns;
+    const int k = j - by_ns.div(j) * Ns;
     if (k != 0) {
 #pragma unroll
       for (int r = 1; r < R; r++) {

@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(FL_THREADS)
 k_fft_lines(float2* __restrict__ data, pf_fft_plan plan, long long nlines, long long inner,
             long long istr, long long ostr, long long estr, int cnt, float scale) {
   extern __shared__ float2 sm[];
+  __shared__ long long lbase[64];
   const int n = plan.n;
   const int ld = pf_ld(n);
   float2* a = sm;
@@ -31,17 +32,23 @@ k_fft_lines(float2* __restrict__ data, pf_fft_plan plan, long long nlines, long 
   const int nl = (int)(nlines - l0 < cnt ? nlines - l0 : cnt);
   const int tot = nl * n;
   const bool rows = (estr == 1);
+  // per-line base offsets once (64-bit div/mod), element index split by a fast divide
+  for (int c = threadIdx.x; c < nl; c += FL_THREADS) lbase[c] = line_base(l0 + c, inner, istr, ostr);
+  __syncthreads();
+  const FastDiv split(rows ? n : nl);
   for (int e = threadIdx.x; e < tot; e += FL_THREADS) {
+    const int q = split.div(e);
     int c, i;
-    if (rows) { c = e / n; i = e - c * n; } else { i = e / nl; c = e - i * nl; }
-    a[c * ld + i] = data[line_base(l0 + c, inner, istr, ostr) + (long long)i * estr];
+    if (rows) { c = q; i = e - q * n; } else { i = q; c = e - q * nl; }
+    a[c * ld + i] = data[lbase[c] + (long long)i * estr];
   }
   __syncthreads();
   const float2* r = fft_smem<DIR>(a, b, ld, nl, plan);
   for (int e = threadIdx.x; e < tot; e += FL_THREADS) {
+    const int q = split.div(e);
     int c, i;
-    if (rows) { c = e / n; i = e - c * n; } else { i = e / nl; c = e - i * nl; }
-    data[line_base(l0 + c, inner, istr, ostr) + (long long)i * estr] = cscale(r[c * ld + i], scale);
+    if (rows) { c = q; i = e - q * n; } else { i = q; c = e - q * nl; }
+    data[lbase[c] + (long long)i * estr] = cscale(r[c * ld + i], scale);
   }
 }
 
@@ -84,6 +91,7 @@ int launch_lines(float2* data, const pf_fft_plan& p, long long nlines, long long
   const int want = (4 * FL_THREADS + p.n - 1) / p.n;
   if (cnt > want) cnt = want < 1 ? 1 : want;
   if (estr != 1 && cnt < 8 && (size_t)8 * per_line <= FL_SMEM_BUDGET) cnt = 8;  // coalescing
+  if (cnt > 64) cnt = 64;
   if (cnt > nlines) cnt = (int)nlines;
   const int grid = (int)((nlines + cnt - 1) / cnt);
   k_fft_lines<DIR><<<grid, FL_THREADS, cnt * per_line, st>>>(data, p, nlines, inner, istr, ostr,

@@ -24,8 +24,8 @@ constexpr int SP_CHUNK = 32;   // points staged per pass
 constexpr int SP_V = 8;        // value sets (complex) accumulated per CTA
 
 __device__ __forceinline__ int wrap_off(int d, int mr) {
-  // representative of d mod mr in [-mr/2, mr - mr/2)
-  d %= mr;
+  // representative of d mod mr in [-mr/2, mr - mr/2), for d in (-mr, mr)
+  // (cell and anchor are both natural slots: no division needed)
   if (d < -(mr / 2)) d += mr;
   if (d >= mr - mr / 2) d -= mr;
   return d;
@@ -69,7 +69,7 @@ k_spread(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ 
       } else {
         wgt[p][a][o] = 1.0f;
       }
-      if (o == 0) pi0[p][a] = a >= 3 - G.dim ? i0[3 * pt + a] : 0;
+      if (o == 0) pi0[p][a] = a >= 3 - G.dim ? natural(i0[3 * pt + a], G.mr[a]) : 0;
     }
     for (int e = tid; e < nc * nvv; e += NT) {
       const int p = e % nc, v = e / nc;
@@ -172,7 +172,67 @@ __global__ void k_place(pf_nufft_geom G, const float2* __restrict__ S, long long
 }
 
 // type-2 finish (2D): out = sum_stencil fine * wy * wx, then * scale * exp(1j khat r_ill),
-// accumulated into vol[frame][dst0 + l] (frames: exp(1j w t) weights).
+// accumulated into vol[frame][dst0 + perm[l]] (frames: exp(1j w t) weights).
+// One WARP per target point: lane = stencil column (W = 2w+1 <= 32), a loop over
+// the W stencil rows reads one contiguous row segment per step, and a shuffle
+// reduction forms the point's value.  Wrap-around is resolved once per row /
+// column (no per-tap modulo).
+__device__ __forceinline__ int wrap_once(int c, int mr) { return c < 0 ? c + mr : (c >= mr ? c - mr : c); }
+
+__global__ void __launch_bounds__(256)
+k_interp2_warp(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
+               const double* __restrict__ xyz, int npts, const float2* __restrict__ fine,
+               long long fine_stride, int n_illum, const double* __restrict__ ill, double kturns,
+               int include_illum, float scale, const float2* __restrict__ frame_w, int n_frames,
+               float2* __restrict__ vol, long long vol_frame_stride, long long dst0,
+               const int* __restrict__ perm) {
+  const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (l >= npts) return;
+  const int W = 2 * G.w + 1;
+  const int mry = G.mr[1], mrx = G.mr[2];
+  const bool on = lane < W;
+  const float dyl = d0[3 * l + 1], dxl = d0[3 * l + 2];
+  const float dx = dxl + (float)(lane - G.w) * G.h[2];
+  const float wx = on ? __expf(-dx * dx * G.inv4tau[2]) : 0.f;
+  const int cx = wrap_once(natural((long long)i0[3 * l + 2] - G.w, mrx) + (on ? lane : 0), mrx);
+  const int cy0 = natural((long long)i0[3 * l + 1] - G.w, mry);
+  float2 tot = make_float2(0.f, 0.f);
+  for (int p = 0; p < n_illum; p++) {
+    const float2* fp = fine + (long long)p * fine_stride + cx;
+    float2 acc = make_float2(0.f, 0.f);
+    int cy = cy0;
+    for (int oy = 0; oy < W; oy++) {
+      const float dy = dyl + (float)(oy - G.w) * G.h[1];
+      const float w = wx * __expf(-dy * dy * G.inv4tau[1]);
+      const float2 f = __ldg(fp + (long long)cy * mrx);
+      acc.x = fmaf(w, f.x, acc.x);
+      acc.y = fmaf(w, f.y, acc.y);
+      if (++cy == mry) cy = 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    float2 val = cscale(acc, scale);
+    if (include_illum) {
+      const double ex = xyz[3 * l] - ill[3 * p], ey = xyz[3 * l + 1] - ill[3 * p + 1];
+      const double ez = xyz[3 * l + 2] - ill[3 * p + 2];
+      val = cmul(val, expi_reduced(PF_TWO_PI * kturns * sqrt(ex * ex + ey * ey + ez * ez)));
+    }
+    tot = cadd(tot, val);
+  }
+  if (lane == 0) {
+    const long long lo = perm ? perm[l] : l;   // points may be stored cell-sorted
+    for (int f = 0; f < n_frames; f++) {
+      float2* d = vol + f * vol_frame_stride + dst0 + lo;
+      *d = cadd(*d, cmul(tot, frame_w[f]));
+    }
+  }
+}
+
+// w = 16 (W = 33 > 32 lanes): one thread per point.
 __global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
                               const float* __restrict__ d0, const double* __restrict__ xyz,
                               int npts, const float2* __restrict__ fine, long long fine_stride,
@@ -183,39 +243,40 @@ __global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= npts) return;
   const int W = 2 * G.w + 1;
-  float wy[2 * 16 + 1], wx[2 * 16 + 1];
-  for (int o = 0; o < W; o++) {
-    const float dy = d0[3 * l + 1] + (float)(o - G.w) * G.h[1];
-    const float dx = d0[3 * l + 2] + (float)(o - G.w) * G.h[2];
-    wy[o] = __expf(-dy * dy * G.inv4tau[1]);
-    wx[o] = __expf(-dx * dx * G.inv4tau[2]);
-  }
-  const int iy = i0[3 * l + 1], ix = i0[3 * l + 2];
+  const int mry = G.mr[1], mrx = G.mr[2];
+  const int cx0 = natural((long long)i0[3 * l + 2] - G.w, mrx);
+  int cy = natural((long long)i0[3 * l + 1] - G.w, mry);
   float2 tot = make_float2(0.f, 0.f);
   for (int p = 0; p < n_illum; p++) {
     const float2* fp = fine + (long long)p * fine_stride;
     float2 acc = make_float2(0.f, 0.f);
+    int y = cy;
     for (int oy = 0; oy < W; oy++) {
-      const int cy = natural((long long)iy + oy - G.w, G.mr[1]);
+      const float dy = d0[3 * l + 1] + (float)(oy - G.w) * G.h[1];
+      const float wy = __expf(-dy * dy * G.inv4tau[1]);
       float2 row = make_float2(0.f, 0.f);
+      int x = cx0;
       for (int ox = 0; ox < W; ox++) {
-        const int cx = natural((long long)ix + ox - G.w, G.mr[2]);
-        const float2 f = fp[(long long)cy * G.mr[2] + cx];
-        row.x = fmaf(wx[ox], f.x, row.x);
-        row.y = fmaf(wx[ox], f.y, row.y);
+        const float dx = d0[3 * l + 2] + (float)(ox - G.w) * G.h[2];
+        const float wx = __expf(-dx * dx * G.inv4tau[2]);
+        const float2 f = fp[(long long)y * mrx + x];
+        row.x = fmaf(wx, f.x, row.x);
+        row.y = fmaf(wx, f.y, row.y);
+        if (++x == mrx) x = 0;
       }
-      acc.x = fmaf(wy[oy], row.x, acc.x);
-      acc.y = fmaf(wy[oy], row.y, acc.y);
+      acc.x = fmaf(wy, row.x, acc.x);
+      acc.y = fmaf(wy, row.y, acc.y);
+      if (++y == mry) y = 0;
     }
     float2 val = cscale(acc, scale);
     if (include_illum) {
-      const double dx = xyz[3 * l] - ill[3 * p], dy = xyz[3 * l + 1] - ill[3 * p + 1];
-      const double dz = xyz[3 * l + 2] - ill[3 * p + 2];
-      val = cmul(val, expi_reduced(PF_TWO_PI * kturns * sqrt(dx * dx + dy * dy + dz * dz)));
+      const double ex = xyz[3 * l] - ill[3 * p], ey = xyz[3 * l + 1] - ill[3 * p + 1];
+      const double ez = xyz[3 * l + 2] - ill[3 * p + 2];
+      val = cmul(val, expi_reduced(PF_TWO_PI * kturns * sqrt(ex * ex + ey * ey + ez * ez)));
     }
     tot = cadd(tot, val);
   }
-  const long long lo = perm ? perm[l] : l;   // points may be stored cell-sorted
+  const long long lo = perm ? perm[l] : l;
   for (int f = 0; f < n_frames; f++) {
     float2* d = vol + f * vol_frame_stride + dst0 + lo;
     *d = cadd(*d, cmul(tot, frame_w[f]));
@@ -277,6 +338,14 @@ extern "C" int pf_nufft_interp2_acc(const pf_nufft_geom* g, const int32_t* i0, c
                                     void* stream) {
   PF_ARG_CHECK(g && g->dim == 2 && g->w <= 16 && npts >= 0, "pf_nufft_interp2_acc: bad args");
   if (npts == 0) return 0;
+  if (2 * g->w + 1 <= 32) {
+    k_interp2_warp<<<pf_cdiv(npts, 8), 256, 0, (cudaStream_t)stream>>>(
+        *g, i0, d0, xyz, npts, (const float2*)fine, fine_stride, n_illum, ill, khat / PF_TWO_PI,
+        include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride,
+        dst0, perm);
+    PF_LAUNCH_CHECK("k_interp2_warp");
+    return 0;
+  }
   k_interp2_acc<<<pf_cdiv(npts, 128), 128, 0, (cudaStream_t)stream>>>(
       *g, i0, d0, xyz, npts, (const float2*)fine, fine_stride, n_illum, ill, khat / PF_TWO_PI,
       include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride,
