@@ -24,8 +24,9 @@ constexpr int SP_CHUNK = 32;   // points staged per pass
 constexpr int SP_V = 8;        // value sets (complex) accumulated per CTA
 
 __device__ __forceinline__ int wrap_off(int d, int mr) {
-  // representative of d mod mr in [-mr/2, mr - mr/2), for d in (-mr, mr)
-  // (cell and anchor are both natural slots: no division needed)
+  // representative of d mod mr in [-mr/2, mr - mr/2), for d in (-mr, 2 mr)
+  // (offsets between natural slots plus a tile-local index: no division needed)
+  if (d >= mr) d -= mr;
   if (d < -(mr / 2)) d += mr;
   if (d >= mr - mr / 2) d -= mr;
   return d;
@@ -57,19 +58,27 @@ k_spread(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ 
 #pragma unroll
   for (int v = 0; v < SP_V; v++) acc[v] = make_float2(0.f, 0.f);
   const int s0 = tile_start[tile], s1 = tile_start[tile + 1];
+  // tile origin per axis: a point's offset to every cell of the tile is its
+  // offset to the origin (wrapped once, when staged) plus the cell's local index
+  const int tile0[3] = {tz * G.tile[0], ty * G.tile[1], tx * G.tile[2]};
+  const int lz = cz - tile0[0], ly = cy - tile0[1], lx = cx - tile0[2];
   for (int c0 = s0; c0 < s1; c0 += SP_CHUNK) {
     const int nc = min(SP_CHUNK, s1 - c0);
     __syncthreads();
-    for (int e = tid; e < nc * 3 * W; e += NT) {
-      const int p = e / (3 * W), a = (e / W) % 3, o = e % W;
+    for (int e = tid; e < nc * 3; e += NT) {
+      const int p = e / 3, a = e - 3 * p;
       const int pt = tile_pts[c0 + p];
       if (a >= 3 - G.dim) {
-        const float dl = d0[3 * pt + a] + (float)(o - G.w) * G.h[a];
-        wgt[p][a][o] = __expf(-dl * dl * G.inv4tau[a]);
+        const float base = d0[3 * pt + a];
+        for (int o = 0; o < W; o++) {
+          const float dl = base + (float)(o - G.w) * G.h[a];
+          wgt[p][a][o] = __expf(-dl * dl * G.inv4tau[a]);
+        }
+        pi0[p][a] = wrap_off(tile0[a] - natural(i0[3 * pt + a], G.mr[a]), G.mr[a]);
       } else {
-        wgt[p][a][o] = 1.0f;
+        for (int o = 0; o < W; o++) wgt[p][a][o] = 1.0f;
+        pi0[p][a] = 0;      // unused axis of a 2D grid
       }
-      if (o == 0) pi0[p][a] = a >= 3 - G.dim ? natural(i0[3 * pt + a], G.mr[a]) : 0;
     }
     for (int e = tid; e < nc * nvv; e += NT) {
       const int p = e % nc, v = e / nc;
@@ -78,9 +87,10 @@ k_spread(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ 
     __syncthreads();
     if (inside) {
       for (int p = 0; p < nc; p++) {
-        const int ox = wrap_off(cx - pi0[p][2], G.mr[2]);
-        const int oy = wrap_off(cy - pi0[p][1], G.mr[1]);
-        const int oz = G.dim == 3 ? wrap_off(cz - pi0[p][0], G.mr[0]) : 0;
+        // pi0 holds (tile origin - anchor) wrapped; + local index, wrapped once more
+        const int ox = wrap_off(pi0[p][2] + lx, G.mr[2]);
+        const int oy = wrap_off(pi0[p][1] + ly, G.mr[1]);
+        const int oz = G.dim == 3 ? wrap_off(pi0[p][0] + lz, G.mr[0]) : 0;
         if (abs(ox) > G.w || abs(oy) > G.w || abs(oz) > G.w) continue;
         float wv = wgt[p][2][ox + G.w] * wgt[p][1][oy + G.w];
         if (G.dim == 3) wv *= wgt[p][0][oz + G.w];
