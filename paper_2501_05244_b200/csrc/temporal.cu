@@ -12,6 +12,9 @@
 // block then forms every retained bin as an M-term twiddled sum (fp64-built
 // twiddles).  The kernel reads each histogram byte exactly once and writes
 // F complex64 per trace: it is HBM-bound.
+#include <stdint.h>
+#include <stdlib.h>
+
 #include "fft.cuh"
 
 namespace {
@@ -121,6 +124,129 @@ k_temporal_dft_direct(const float* __restrict__ hist, long long n_traces, int T,
   }
 }
 
+// ---- TMA-fed variant (M = 64, i.e. T = 4096, the config 2-4 window) ----------
+// The histograms of G consecutive traces are one contiguous run of G*T*4 bytes:
+// one elected thread moves it into a shared-memory ring with a 1D bulk copy
+// (cp.async.bulk, TMA engine) that completes on the stage's mbarrier, S-1
+// groups ahead of the compute.  The threads never issue global loads for the
+// payload; they wait on the mbarrier, read their stride-M column from shared
+// memory (conflict-free), and phase B uses every thread (two per output).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int G, int S>
+__global__ void __launch_bounds__(G * 64, 1)
+k_temporal_tma(const float* __restrict__ hist, long long n_traces, const int* __restrict__ bins,
+               const float2* __restrict__ twt, int twt_ld, const float2* __restrict__ wphase,
+               int F, float2* __restrict__ out, long long out_stride) {
+  constexpr int M = 64, T = 64 * M, NT = G * M;
+  constexpr int TS = M * K1_KB + 1;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float* ring = reinterpret_cast<float*>(smraw);                  // [S][G*T]
+  float2* xs = reinterpret_cast<float2*>(ring + (size_t)S * G * T);  // [G][TS]
+  float2* tws = xs + G * TS;                                      // [M][F]
+  int* kb = reinterpret_cast<int*>(tws + M * F);                  // [F]
+  __shared__ __align__(8) unsigned long long full[S];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < M * F; e += NT) tws[e] = twt[(e / F) * twt_ld + e % F];
+  for (int e = tid; e < F; e += NT) kb[e] = bins[e] & 63;
+  if (tid == 0) {
+    for (int st = 0; st < S; st++) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long n_groups = (n_traces + G - 1) / G;
+  const long long first = blockIdx.x, step = gridDim.x;
+  auto issue = [&](long long grp, int st) {
+    const long long t0 = grp * G;
+    const long long cnt = n_traces - t0 < G ? n_traces - t0 : G;
+    const unsigned bytes = (unsigned)(cnt * T * sizeof(float));
+    mbar_expect_tx(&full[st], bytes);
+    bulk_g2s(ring + (size_t)st * G * T, hist + t0 * T, bytes, &full[st]);
+  };
+  if (tid == 0) {
+    for (int k = 0; k < S - 1; k++) {
+      const long long grp = first + k * step;
+      if (grp < n_groups) issue(grp, k);
+    }
+  }
+  const int g = tid / M, r = tid - (tid / M) * M;
+  int it = 0;
+  for (long long grp = first; grp < n_groups; grp += step, it++) {
+    const int st = it % S;
+    if (tid == 0) {   // refill the stage consumed in the previous iteration
+      const long long nxt = grp + (long long)(S - 1) * step;
+      if (nxt < n_groups) issue(nxt, (it + S - 1) % S);
+    }
+    mbar_wait(&full[st], (unsigned)((it / S) & 1));
+    const long long trace = grp * G + g;
+    if (trace < n_traces) {
+      const float* h = ring + (size_t)st * G * T + g * T + r;
+      float x[64];
+#pragma unroll
+      for (int q = 0; q < 64; q++) x[q] = h[q * M];
+      float2 X[K1_KB];
+      real_dft64(x, X);
+      float2* dst = xs + g * TS + r * K1_KB;
+#pragma unroll
+      for (int k = 0; k < K1_KB; k++) dst[k] = X[k];
+    }
+    __syncthreads();
+    // phase B: item = (trace, f, half); the two halves of an item are adjacent lanes
+    for (int p = tid; p < G * F * 2; p += NT) {
+      const int half = p & 1, q = p >> 1;
+      const int gg = q % G, f = q / G;
+      const long long tr = grp * G + gg;
+      const int k = kb[f];
+      const bool cj = k > 32;
+      const int kk = cj ? 64 - k : k;
+      const float2* src = xs + gg * TS + kk;
+      float2 acc = make_float2(0.f, 0.f);
+      const int r0 = half * (M / 2);
+#pragma unroll 8
+      for (int rr = r0; rr < r0 + M / 2; rr++) {
+        float2 z = src[rr * K1_KB];
+        if (cj) z.y = -z.y;
+        cacc(acc, z, tws[rr * F + f]);
+      }
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+      if (half == 0 && tr < n_traces) out[(long long)f * out_stride + tr] = cmul(acc, wphase[f]);
+    }
+    __syncthreads();
+  }
+}
+
 constexpr int K1_FCHUNK = 64;  // retained bins per pass (shared-memory bound)
 
 template <int M>
@@ -151,6 +277,52 @@ int launch_k1(const float* hist, long long n_traces, const int* bins, const floa
   return 0;
 }
 
+static int k1_tma_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+int launch_k1_tma(const float* hist, long long n_traces, const int* bins, const float2* twt,
+                  const float2* wphase, int F, float2* out, long long out_stride,
+                  cudaStream_t st) {
+  // G traces per stage, S stages (PF_K1_G / PF_K1_S select the measured variants)
+  const int G = k1_tma_env("PF_K1_G", 4), S = k1_tma_env("PF_K1_S", 2);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const long long groups = (n_traces + G - 1) / G;
+  const size_t smem = (size_t)S * G * 4096 * sizeof(float) +
+                      (size_t)(G * (64 * K1_KB + 1) + 64 * F) * sizeof(float2) + F * sizeof(int);
+  if (smem > 220 * 1024) {
+    pf_set_error("pf_temporal_dft: TMA ring G=%d S=%d needs %zu bytes of shared memory", G, S, smem);
+    return -1;
+  }
+#define K1_TMA(GG, SS)                                                                        \
+  if (G == GG && S == SS) {                                                                   \
+    static bool attr = false;                                                                 \
+    if (!attr) {                                                                              \
+      cudaFuncSetAttribute(k_temporal_tma<GG, SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           220 * 1024);                                                       \
+      attr = true;                                                                            \
+    }                                                                                         \
+    int per = 0;                                                                              \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_temporal_tma<GG, SS>, GG * 64, smem); \
+    if (per < 1) per = 1;                                                                     \
+    const int grid = (int)(groups < (long long)nsm * per ? groups : (long long)nsm * per);   \
+    k_temporal_tma<GG, SS><<<grid, GG * 64, smem, st>>>(hist, n_traces, bins, twt, F, wphase, \
+                                                        F, out, out_stride);                  \
+    PF_LAUNCH_CHECK("k_temporal_tma");                                                        \
+    return 0;                                                                                 \
+  }
+  K1_TMA(4, 2)
+  K1_TMA(2, 2)
+  K1_TMA(2, 3)
+  K1_TMA(1, 4)
+#undef K1_TMA
+  pf_set_error("pf_temporal_dft: unsupported PF_K1_G/PF_K1_S combination");
+  return -1;
+}
+
 }  // namespace
 
 extern "C" int pf_temporal_dft(const float* hist, int64_t n_traces, int n_bins,
@@ -163,6 +335,10 @@ extern "C" int pf_temporal_dft(const float* hist, int64_t n_traces, int n_bins,
   const float2* wp = (const float2*)wphase;
   float2* o = (float2*)out;
   const int M = (n_bins % K1_L == 0) ? n_bins / K1_L : 0;
+  // TMA-fed variant: opt-in (PF_K1_TMA=1); measured 1.44 ms vs 1.35 ms for the load path at
+  // config 4 (K1 is issue-bound, not latency-bound: profiles/r1_k1_variants.json)
+  if (M == 64 && ((uintptr_t)hist & 15) == 0 && n_freq <= K1_FCHUNK && getenv("PF_K1_TMA"))
+    return launch_k1_tma(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
   switch (M) {
     case 1: return launch_k1<1>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
     case 2: return launch_k1<2>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
