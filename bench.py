@@ -151,16 +151,24 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
 
+    # N > 1: the rank's planes run in chunks; each finished chunk is gathered to rank 0
+    # on a side stream while the next chunk computes
+    n_chunks = rec.gather_chunks
+
     def step():
         ev[0].record(stream)
         rec.temporal.run(hist_shard.view(-1, T), local_shard.view(F, -1), stream)
         ev[1].record(stream)
         coeff = sgather(local_shard) if world > 1 else local_shard
         ev[2].record(stream)
-        eng.run_graphed(coeff, rec.vol, stream)
-        ev[3].record(stream)
-        if world > 1:
-            vgather(rec.vol)
+        if n_chunks > 1:
+            rec.propagate_and_gather(coeff, rec.vol, stream)
+            ev[3].record(stream)
+        else:
+            eng.run_graphed(coeff, rec.vol, stream)
+            ev[3].record(stream)
+            if world > 1:
+                vgather(rec.vol)
         ev[4].record(stream)
 
     for _ in range(args.warmup):

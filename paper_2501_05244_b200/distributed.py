@@ -96,3 +96,42 @@ class VolumeGather:
             n = (hi - lo) * self.pv
             self.full[:, lo * self.pv:hi * self.pv].copy_(self.recv[r][:, :n])
         return self.full
+
+    def part_ranges(self, j: int, n_chunks: int):
+        """Per rank: local plane range of chunk j when each shard is cut into n_chunks
+        contiguous pieces (the split ``GraphedRun.chunk_bounds`` uses)."""
+        out = []
+        for lo, hi in self.ranges:
+            n = hi - lo
+            k = max(1, min(n_chunks, n)) if n else 1
+            a = j * (n // k) + min(j, n % k) if j < k else n
+            b = a + (n // k + (1 if j < n % k else 0)) if j < k else n
+            out.append((a, b))
+        return out
+
+    def gather_part(self, local: torch.Tensor, j: int, n_chunks: int):
+        """Gather chunk j of every rank's shard into ``full`` on rank 0 (call on the stream
+        that must order it: after chunk j's planes are final on this rank)."""
+        parts = self.part_ranges(j, n_chunks)
+        maxp = max(b - a for a, b in parts) * self.pv
+        a, b = parts[self.rank]
+        send = self.send[:, :maxp]
+        send[:, :(b - a) * self.pv].copy_(local.view(self.nf, -1)[:, a * self.pv:b * self.pv])
+        send = send.contiguous()
+        recv = [r[:, :maxp].contiguous() for r in self.recv] if self.rank == 0 else None
+        if send.is_cuda and _host_staged(self.group):
+            hs = send.cpu()
+            hr = [torch.empty_like(hs) for _ in range(self.world)] if self.rank == 0 else None
+            dist.gather(_real(hs), [_real(x) for x in hr] if hr else None, dst=0, group=self.group)
+            if self.rank == 0:
+                for d, h in zip(recv, hr):
+                    d.copy_(h)
+        else:
+            dist.gather(_real(send), [_real(x) for x in recv] if recv else None, dst=0,
+                        group=self.group)
+        if self.rank != 0:
+            return None
+        for r, ((lo, _), (pa, pb)) in enumerate(zip(self.ranges, parts)):
+            n = (pb - pa) * self.pv
+            self.full[:, (lo + pa) * self.pv:(lo + pb) * self.pv].copy_(recv[r][:, :n])
+        return self.full

@@ -11,6 +11,8 @@ host memory.  The device-resident sub-steps are exposed for benchmarking.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -76,6 +78,14 @@ class TransientReconstructor:
                                device=self.device)
         self.chunks = max(1, int(chunks))
         self.use_graphs = True
+        # multi-GPU: planes in chunks, each gathered while the next computes
+        nloc = getattr(self.engine, "n_planes_local", 0)
+        want = int(os.environ.get("PF_GATHER_CHUNKS", "4"))
+        self.gather_chunks = 1
+        if volume_gather is not None and hasattr(self.engine, "run_chunk") and want > 1:
+            shards = [hi - lo for lo, hi in volume_gather.ranges]
+            self.gather_chunks = max(1, min(want, min(shards)))
+        self.gather_stream = torch.cuda.Stream(device=self.device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self._hist_dev = None
         self._vol_host = None
@@ -92,6 +102,27 @@ class TransientReconstructor:
         if self.use_graphs:
             return self.engine.run_graphed(coeff, self.vol, stream)
         return self.engine.run(coeff, self.vol, stream)
+
+    def propagate_and_gather(self, coeff: torch.Tensor, vol: torch.Tensor, stream=None,
+                             after=None):
+        """Chunked propagation; chunk j's planes are gathered to rank 0 on the gather
+        stream while chunk j+1 computes.  ``after``: event the first gather must wait
+        for (the previous capture's read of the gathered volume).  Returns the
+        gathered volume on rank 0 (None elsewhere); ``stream`` waits for the gathers."""
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        gs = self.gather_stream
+        if after is not None:
+            gs.wait_event(after)
+        res = None
+        for j in range(self.gather_chunks):
+            self.engine.run_graphed_chunk(coeff, vol, j, self.gather_chunks, main)
+            done = torch.cuda.Event()
+            done.record(main)
+            gs.wait_event(done)
+            with torch.cuda.stream(gs):
+                res = self.volume_gather.gather_part(vol, j, self.gather_chunks)
+        main.wait_stream(gs)
+        return res
 
     # -- host in, host out ------------------------------------------------------
     def __call__(self, hist_host: torch.Tensor) -> torch.Tensor:
@@ -119,13 +150,16 @@ class TransientReconstructor:
             main.wait_event(ev)
             self.temporal.run(dst[c0:c1], out[:, c0:c1], main)
         coeff = self.slice_gather(self.coeff) if self.slice_gather is not None else self.coeff
-        self.propagate(coeff, main)
         vol = self.vol
-        if self.volume_gather is not None:
-            vol = self.volume_gather(self.vol)      # full volume on rank 0, None elsewhere
-            if vol is None:
-                main.synchronize()
-                return None
+        if self.gather_chunks > 1:
+            vol = self.propagate_and_gather(coeff, self.vol, main)
+        else:
+            self.propagate(coeff, main)
+            if self.volume_gather is not None:
+                vol = self.volume_gather(self.vol)      # full volume on rank 0, None elsewhere
+        if self.volume_gather is not None and vol is None:
+            main.synchronize()
+            return None
         self._vol_host.copy_(vol, non_blocking=True)
         main.synchronize()
         return self._vol_host
@@ -163,17 +197,20 @@ class TransientReconstructor:
         sl["hist_free"].record(main)
         coeff = self.slice_gather(sl["coeff"]) if self.slice_gather is not None else sl["coeff"]
         main.wait_event(sl["vol_free"])
-        if self.use_graphs:
-            self.engine.run_graphed(coeff, sl["vol"], main)
-        else:
-            self.engine.run(coeff, sl["vol"], main)
         vol = sl["vol"]
-        if self.volume_gather is not None:
+        if self.gather_chunks > 1:
             # the gathered volume lives in one buffer (rank 0): the previous capture's
-            # device->host read of it must finish before this gather overwrites it
-            if self._last_d2h is not None:
-                main.wait_event(self._last_d2h)
-            vol = self.volume_gather(sl["vol"])
+            # device->host read of it must finish before this capture's gathers write it
+            vol = self.propagate_and_gather(coeff, sl["vol"], main, after=self._last_d2h)
+        else:
+            if self.use_graphs:
+                self.engine.run_graphed(coeff, sl["vol"], main)
+            else:
+                self.engine.run(coeff, sl["vol"], main)
+            if self.volume_gather is not None:
+                if self._last_d2h is not None:
+                    main.wait_event(self._last_d2h)
+                vol = self.volume_gather(sl["vol"])
         done = torch.cuda.Event()
         if vol is not None:
             sl["vol_ready"].record(main)

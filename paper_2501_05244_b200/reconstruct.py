@@ -312,19 +312,19 @@ class Propagator:
             return False
         return bool(_lib.call("pf_prop_mega_aborted", dev.ptr(self._mega_ctr), self._mega_cfg[0]))
 
-    def run_batches(self, body, stream=None) -> None:
-        """Call ``body(b0, b1, lane, lane_stream)`` for every plane batch, alternating lanes.
-
-        Lanes wait for ``stream`` (inputs ready) and ``stream`` waits for every lane.
-        """
+    def run_batches(self, body, stream=None, lo: int = 0, hi: int | None = None) -> None:
+        """Call ``body(b0, b1, lane, lane_stream)`` for every plane batch of [lo, hi),
+        alternating lanes.  Lanes wait for ``stream`` (inputs ready) and ``stream``
+        waits for every lane."""
+        hi = self.nplanes if hi is None else hi
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
         for ls in self.lane_streams:
             ls.wait_stream(main)
-        for i, b0 in enumerate(range(0, self.nplanes, self.batch)):
+        for i, b0 in enumerate(range(lo, hi, self.batch)):
             lane = i % len(self.lane_streams)
             ls = self.lane_streams[lane]
             with torch.cuda.stream(ls):
-                body(b0, min(self.nplanes, b0 + self.batch), lane, ls)
+                body(b0, min(hi, b0 + self.batch), lane, ls)
         for ls in self.lane_streams:
             main.wait_stream(ls)
 
@@ -380,6 +380,42 @@ class GraphedRun:
                 self.run(coeff, vol, side)
             main.wait_stream(side)
             self.graph_kernels = _lib.launch_count - n0   # libpfgpu launches per replay
+            graphs[key] = g
+        with torch.cuda.stream(main):
+            g.replay()
+        return vol
+
+    def chunk_bounds(self, n_chunks: int) -> list:
+        """Contiguous local plane ranges of ``run_chunk`` (at most n_chunks, none empty)."""
+        n = self.n_planes_local
+        n_chunks = max(1, min(int(n_chunks), n))
+        out, lo = [], 0
+        for j in range(n_chunks):
+            hi = lo + n // n_chunks + (1 if j < n % n_chunks else 0)
+            out.append((lo, hi))
+            lo = hi
+        return out
+
+    def run_graphed_chunk(self, coeff: torch.Tensor, vol: torch.Tensor, j: int, n_chunks: int,
+                          stream=None):
+        """Graph replay of chunk j of ``n_chunks``: chunk 0 also builds the relay spectra;
+        chunk j leaves planes ``chunk_bounds(n_chunks)[j]`` of ``vol`` final, so their
+        transfer can start while later chunks compute (multi-GPU volume gather)."""
+        graphs = self.__dict__.setdefault("_chunk_graphs", {})
+        key = (coeff.data_ptr(), vol.data_ptr(), j, n_chunks)
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        lo, hi = self.chunk_bounds(n_chunks)[j]
+        g = graphs.get(key)
+        if g is None:
+            side = torch.cuda.Stream(device=self.device)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self.run_chunk(coeff, vol, lo, hi, j == 0, side)
+            main.wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                self.run_chunk(coeff, vol, lo, hi, j == 0, side)
+            main.wait_stream(side)
             graphs[key] = g
         with torch.cuda.stream(main):
             g.replay()
@@ -444,6 +480,30 @@ class RsdEngine(GraphedRun):
     @property
     def n_voxels(self) -> int:
         return (self.k_hi - self.k_lo) * self.plane_voxels
+
+    @property
+    def n_planes_local(self) -> int:
+        return self.k_hi - self.k_lo
+
+    def run_chunk(self, coeff, vol, lo: int, hi: int, first: bool, stream=None):
+        """Local planes [lo, hi) only (lanes path; chunk 0 builds the spectra)."""
+        if first:
+            self.relay_spectra(coeff, stream)
+        pv = self.plane_voxels
+        vol.view(self.n_frames, -1)[:, lo * pv:hi * pv].zero_()
+        per_f = self.n_illum * self.py * self.px
+        uhat = self.uhat
+
+        def body(b0, b1, lane, ls):
+            for fi in range(self.freqs.size):
+                khat = float(self.freqs[fi]) / SPEED_OF_LIGHT
+                self.prop.run_frequency(dev.ptr(uhat) + 8 * fi * per_f, khat, dev.ptr(self.ill),
+                                        dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
+                                        self.n_frames, vol, self.n_voxels, plane_lo=b0,
+                                        plane_hi=b1, stream=ls, lane=lane)
+
+        self.prop.run_batches(body, stream, lo, hi)
+        return vol
 
     def relay_spectra(self, coeff: torch.Tensor, stream=None) -> torch.Tensor:
         """Uhat_f = cfft2(pad_embed(u_f)) for all (f, p), natural order (reconstruct.py:259-260)."""

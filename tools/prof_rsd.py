@@ -16,7 +16,14 @@ cfg = configs.config(cfg_id)
 k = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
 meta = _Meta(k, cfg.relay, cfg.illuminations)
 meta.frequencies = meta.frequencies[:n_f]
-eng = pf.RsdEngine(meta, cfg.grid)
+if cfg.algorithm == "srsd":
+    from paper_2501_05244_b200.algorithms import SrsdEngine
+    eng = SrsdEngine(meta, cfg.grid)
+elif cfg.algorithm == "nursd1":
+    from paper_2501_05244_b200.algorithms import Nursd1Engine
+    eng = Nursd1Engine(meta, cfg.grid)
+else:
+    eng = pf.RsdEngine(meta, cfg.grid)
 rng = np.random.default_rng(0)
 D = cfg.relay.count
 coeff = torch.from_numpy(np.exp(2j * np.pi * rng.random((n_f, 1, D))).astype(np.complex64)).cuda()
