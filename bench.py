@@ -265,7 +265,7 @@ def run_ours(args):
     roof_k1["frac"] = roof_k1["achieved"] / hbm_peak
     roof_s3 = {"bound": "fp32", "achieved": s3_flops / (s3_ms * 1e-3) / 1e12, "peak": fp32_peak,
                "unit": "TFLOP/s", "traffic": _prop_traffic(F, k_hi - k_lo),
-               "kernel": "propagation k_prop_kernel_rows+k_prop_columns+k_prop_rows_out (S3)",
+               "kernel": "propagation k_pa+k_pb1+k_pb2+k_pc (pf_prop_kernel_rows/columns/rows_out, S3)",
                "ms": s3_ms, "peak_source": "nominal 148 SM x 128 FP32 lanes x 2 x sm_max_mhz "
                                            "(MEASURED_PEAKS.json has no FP32 entry)",
                "flops_model": "(2*F*Nz*I + F*I) * 5 P^2 log2(P^2), P=%d" % P}
@@ -310,11 +310,13 @@ def eng_graph_launches(eng):
 
 
 def _prop_traffic(n_freq, n_planes):
-    """Per-step DRAM bytes of the propagation stage from the committed ncu capture."""
-    per_batch = _traffic("k_prop_per_batch_of_8_planes")
-    if per_batch is None:
+    """Per-step DRAM bytes of the propagation stage from the committed ncu capture
+    (one plane batch of kernels A, B1, B2, C, cold L2), scaled to F x Nz."""
+    per_batch = _traffic("k_prop_per_batch")
+    planes = _traffic("batch_planes")
+    if per_batch is None or not planes:
         return None
-    return per_batch * n_freq * (n_planes / 8.0)
+    return per_batch * n_freq * (n_planes / float(planes))
 
 
 def _traffic(kernel_prefix):

@@ -1,0 +1,24 @@
+#!/bin/bash
+# One GPU call refreshing every round artefact: tests, bench lines (ours + reference arm)
+# for configs 4 (headline), 0, 1, 3, 5, config 2 timing, the c4 launch list and one
+# ncu --set full capture of K1 and the four propagation stages.
+set -x
+mkdir -p gpurun_out/final
+O=gpurun_out/final
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; tail -3 $O/pytest_gpu.log
+python bench.py > $O/bench_c4.json 2> $O/bench_c4.err; tail -c 300 $O/bench_c4.err
+python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref_c4.json 2> $O/bench_ref_c4.err
+for c in 0 1 3 5; do
+  python bench.py --config $c > $O/bench_c$c.json 2> $O/bench_c$c.err
+done
+for c in 0 1 3; do
+  python bench.py --config $c --impl reference --steps 2 --warmup 1 > $O/bench_ref_c$c.json 2> $O/bench_ref_c$c.err
+done
+python tools/run_config2.py > $O/config2.json 2> $O/config2.err
+PF_NF=2 python tools/prof_rsd.py > $O/prof_plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv \
+      --log-file $O/launches_c4.csv python tools/prof_rsd.py > /dev/null 2>&1
+PF_NF=2 ncu --set full --clock-control none --import-source on \
+    -k regex:"k_temporal_dft|k_pa|k_pb1|k_pb2|k_pc" -s 6 -c 5 -o $O/prof_full \
+    python tools/prof_rsd.py > $O/ncu_full.log 2>&1
+tail -2 $O/ncu_full.log
