@@ -95,55 +95,6 @@ k_pa(const pf_plane* __restrict__ planes, double kturns_s, pf_prop_geom g,
   }
 }
 
-template <int L>
-__global__ void __launch_bounds__(FT, 1)
-k_pb(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
-     const float2* __restrict__ tw, const float2* __restrict__ ws_a,
-     const float2* __restrict__ uhat_t, float2* __restrict__ ws_b) {
-  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
-  constexpr int LPW = 32 / L;
-  extern __shared__ float2 sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % L, line = lane / L;
-  const int kx = blockIdx.x;
-  const int b = (blockIdx.y * 8 + warp) * LPW + line;
-  const bool active = b < nplanes;
-  const int bb = active ? b : nplanes - 1;
-  const pf_plane pl = planes[bb];
-  const float2* arow = ws_a + ((long long)bb * NA + kx) * NA;
-  float2 gh[32];
-#pragma unroll
-  for (int m = 0; m < 32; m++) {
-    const int jy = t + L * m;
-    gh[m] = __ldg(arow + (jy <= H ? jy : P - jy));
-  }
-  float2* xch = sm + warp * WFFT_XCH;
-  wfft<L, -1, true>(gh, xch, tw);
-  const int ny = g.ny;
-  for (int p = 0; p < g.n_illum; p++) {
-    const float2* up = uhat_t + pl.uhat_off + (long long)p * g.uhat_illum_stride;
-    float2* outp = ws_b + ((long long)bb * g.n_illum + p) * (long long)P * ny;
-#pragma unroll 1
-    for (int side = 0; side < 2; side++) {
-      const int col = side == 0 ? kx : (P - kx) % P;
-      if (side == 1 && col == kx) break;
-      const float2* ucol = up + (long long)col * P;
-      float2 w[32];
-#pragma unroll
-      for (int m = 0; m < 32; m++) w[m] = cmul(gh[m], __ldg(ucol + t + L * m));
-      wfft<L, 1, true>(w, xch, tw);
-      if (active) {
-        float2* dcol = outp + (long long)col * ny;
-#pragma unroll
-        for (int m = 0; m < 32; m++) {
-          const int i = (t + L * m - g.nu0y) & (P - 1);
-          if (i < ny) dcol[i] = w[m];
-        }
-      }
-    }
-  }
-}
-
 // MULTI: more than one illumination (contributions summed in registers first).
 // PRE: single frame and the CTA's volume rows fit next to the tile: they are
 // prefetched with cp.async at entry so the accumulate is load-free at the end.
@@ -326,15 +277,6 @@ k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
   }
 }
 
-static int pf_splitb_env() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("PF_SPLITB");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v;
-}
-
 // C over all frequencies of the batch in one launch: per (plane, row tile) the
 // ascending-frequency sum is formed in registers and written once.
 template <int L, bool MULTI>
@@ -415,189 +357,6 @@ k_pcf(const pf_plane* __restrict__ planes, pf_prop_geom g, const float2* __restr
   }
 }
 
-// ---- persistent variants: one CTA per SM loops over work items and prefetches
-// the next item's inputs with cp.async while it computes the current one.
-
-// B, persistent: item = (kx, group of 8*LPW planes).  Stage buffers hold the
-// group's At rows and the Uhat^T columns kx, P-kx of every illumination.
-template <int L>
-__global__ void __launch_bounds__(FT, 1)
-k_pbp(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
-      const float2* __restrict__ tw, const float2* __restrict__ ws_a,
-      const float2* __restrict__ uhat_t, float2* __restrict__ ws_b, int n_items) {
-  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
-  constexpr int LPW = 32 / L, PPC = 8 * LPW;
-  extern __shared__ float2 sm[];
-  const int I = g.n_illum;
-  float2* xchb = sm;                                   // [8][WFFT_XCH]
-  float2* abuf = sm + 8 * WFFT_XCH;                    // [2][PPC][NA]
-  float2* ubuf = abuf + 2 * PPC * NA;                  // [2][2][I][P]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % L, line = lane / L;
-  const int lidx = warp * LPW + line;
-  const int ny = g.ny;
-  auto issue = [&](int item, int stage) {
-    const int kx = item % NA, grp = item / NA;
-    float2* ab = abuf + stage * PPC * NA;
-    for (int e = threadIdx.x; e < PPC * NA; e += FT) {
-      const int li = e / NA, jy = e - li * NA;
-      const int b = min(grp * PPC + li, nplanes - 1);
-      cp_async8(ab + e, ws_a + ((long long)b * NA + kx) * NA + jy);
-    }
-    const pf_plane& pl = planes[min(grp * PPC, nplanes - 1)];
-    float2* ub = ubuf + stage * 2 * I * P;
-    for (int e = threadIdx.x; e < 2 * I * P; e += FT) {
-      const int side = e / (I * P), rem = e - side * I * P, p = rem / P, jy = rem - p * P;
-      const int col = side == 0 ? kx : (P - kx) % P;
-      cp_async8(ub + e, uhat_t + pl.uhat_off + (long long)p * g.uhat_illum_stride +
-                            (long long)col * P + jy);
-    }
-    cp_async_commit();
-  };
-  int it = blockIdx.x;
-  if (it < n_items) issue(it, 0);
-  for (int k = 0; it < n_items; it += gridDim.x, k++) {
-    const int stage = k & 1;
-    cp_async_wait_all();
-    __syncthreads();
-    if (it + (int)gridDim.x < n_items) issue(it + gridDim.x, stage ^ 1);
-    const int kx = it % NA, grp = it / NA;
-    const int b = grp * PPC + lidx;
-    const bool active = b < nplanes;
-    const int bb = active ? b : nplanes - 1;
-    const float2* arow = abuf + stage * PPC * NA + lidx * NA;
-    float2 gh[32];
-#pragma unroll
-    for (int m = 0; m < 32; m++) {
-      const int jy = t + L * m;
-      gh[m] = arow[jy <= H ? jy : P - jy];
-    }
-    float2* xch = xchb + warp * WFFT_XCH;
-    wfft<L, -1>(gh, xch, tw);
-    const float2* ub = ubuf + stage * 2 * I * P;
-    for (int p = 0; p < I; p++) {
-      float2* outp = ws_b + ((long long)bb * I + p) * (long long)P * ny;
-#pragma unroll 1
-      for (int side = 0; side < 2; side++) {
-        const int col = side == 0 ? kx : (P - kx) % P;
-        if (side == 1 && col == kx) break;
-        const float2* ucol = ub + (side * I + p) * P;
-        float2 w[32];
-#pragma unroll
-        for (int m = 0; m < 32; m++) w[m] = cmul(gh[m], ucol[t + L * m]);
-        wfft<L, 1>(w, xch, tw);
-        if (active) {
-          float2* dcol = outp + (long long)col * ny;
-#pragma unroll
-          for (int m = 0; m < 32; m++) {
-            const int i = (t + L * m - g.nu0y) & (P - 1);
-            if (i < ny) dcol[i] = w[m];
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// C, persistent: item = (plane, tile of RPC output rows); the next item's
-// transposed tile streams into the other stage while this one is transformed.
-template <int L, bool MULTI>
-__global__ void __launch_bounds__(FT, 1)
-k_pcp(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
-      const float2* __restrict__ tw, const float2* __restrict__ ws_b,
-      const double* __restrict__ ill, const float2* __restrict__ frame_w, int n_frames,
-      float2* __restrict__ vol, long long vol_frame_stride, int n_items) {
-  constexpr int P = 32 * L;
-  constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
-  constexpr int TILE = P * SLD;
-  extern __shared__ float2 sm[];
-  float2* xchb = sm;                          // [8][WFFT_XCH]
-  float2* tiles = sm + 8 * WFFT_XCH;          // [2 * I][TILE]
-  const int I = MULTI ? g.n_illum : 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % L, line = lane / L;
-  const int r = warp * LPW + line;
-  const int ny = g.ny, nx = g.nx;
-  const int tiles_per_plane = (ny + RPC - 1) / RPC;
-  const float scale = 1.0f / ((float)P * (float)P);
-  auto issue = [&](int item, int stage) {
-    const int pb = item / tiles_per_plane, i0 = (item % tiles_per_plane) * RPC;
-    const int nr = min(RPC, ny - i0);
-    for (int p = 0; p < I; p++) {
-      const float2* src = ws_b + ((long long)pb * g.n_illum + p) * (long long)P * ny + i0;
-      float2* dst = tiles + (stage * I + p) * TILE;
-      for (int e = threadIdx.x; e < P * RPC; e += FT) {
-        const int col = e / RPC, rr = e % RPC;
-        if (rr < nr) cp_async8(dst + col * SLD + rr, src + (long long)col * ny + rr);
-      }
-    }
-    cp_async_commit();
-  };
-  int it = blockIdx.x;
-  if (it < n_items) issue(it, 0);
-  for (int k = 0; it < n_items; it += gridDim.x, k++) {
-    const int stage = k & 1;
-    cp_async_wait_all();
-    __syncthreads();
-    if (it + (int)gridDim.x < n_items) issue(it + gridDim.x, stage ^ 1);
-    const int pb = it / tiles_per_plane, i0 = (it % tiles_per_plane) * RPC;
-    const int i = i0 + r;
-    const pf_plane pl = planes[pb];
-    const double yv = pl.y0 + pl.dy * i;
-    const long long off = (pl.vol_plane * ny + i) * (long long)nx;
-    float2 acc[32];
-#pragma unroll 1
-    for (int p = 0; p < I; p++) {
-      float2 v[32];
-      const float2* tl = tiles + (stage * I + p) * TILE;
-#pragma unroll
-      for (int m = 0; m < 32; m++) v[m] = tl[(t + L * m) * SLD + r];
-      wfft<L, 1>(v, xchb + warp * WFFT_XCH, tw);
-      const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
-      const double dy = yv - sy, dz = pl.z - sz;
-      const double byz = fma(dy, dy, dz * dz);
-#pragma unroll
-      for (int m = 0; m < 32; m++) {
-        const int mo = (t + L * m - g.nu0x) & (P - 1);
-        float2 val = cscale(v[m], scale);
-        if (g.include_illum) {
-          const double dx = pl.x0 + pl.dx * mo - sx;
-          val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
-        }
-        acc[m] = p == 0 ? val : cadd(acc[m], val);
-      }
-    }
-    if (i < ny) {
-      for (int fr = 0; fr < n_frames; fr++) {
-        const float2 fw = frame_w[fr];
-        float2* drow = vol + fr * vol_frame_stride + off;
-        float2 old[32];
-#pragma unroll
-        for (int m = 0; m < 32; m++) {
-          const int mo = (t + L * m - g.nu0x) & (P - 1);
-          old[m] = mo < nx ? drow[mo] : make_float2(0.f, 0.f);
-        }
-#pragma unroll
-        for (int m = 0; m < 32; m++) {
-          const int mo = (t + L * m - g.nu0x) & (P - 1);
-          if (mo < nx) drow[mo] = cadd(old[m], cmul(acc[m], fw));
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-static int pf_persist_env() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("PF_PERSIST");
-    v = (e && e[0] == '1') ? 1 : 0;   // off by default: slower on B200
-  }
-  return v;
-}
-
 template <int L, int NW = 8>
 size_t smem_a() {
   constexpr int P = 32 * L, NA = P / 2 + 1, RPC = NW * (32 / L);
@@ -611,61 +370,34 @@ size_t smem_c(int nx, bool pre) {
   return ((x > s ? x : s) + (pre ? (size_t)RPC * nx : 0)) * sizeof(float2);
 }
 
-static int pf_nw_env() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("PF_NW");
-    v = (e && e[0] == '4') ? 4 : 8;
-  }
-  return v;
-}
-
-int nsm() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
-
 template <int L>
 int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const pf_prop_geom& g,
               const float2* tw, const float2* ws_a, float2* ws_a_out, const float2* uhat,
               const float2* ws_b, float2* ws_b_out, const double* ill, const float2* frame_w,
               int n_frames, float2* vol, long long vfs, cudaStream_t st,
               FBatch fb = FBatch{nullptr, 0, 0, 0, 1}) {
-  constexpr int P = 32 * L, NA = P / 2 + 1, RPC = 8 * (32 / L), LPW = 32 / L;
+  constexpr int NA = 32 * L / 2 + 1, RPC = 8 * (32 / L), LPW = 32 / L;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_pa<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_pb<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_pc<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_pc<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_pc<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_pc<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int big = 200 * 1024;
+    cudaFuncSetAttribute(k_pa<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb1<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb2<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb2<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pc<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pc<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pc<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pc<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pcf<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pcf<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     attr = true;
   }
   const double kturns = khat / PF_TWO_PI;
-  if (stage == 0 && pf_nw_env() == 4) {
-    static bool a6 = false;
-    if (!a6) { cudaFuncSetAttribute(k_pa<L, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); a6 = true; }
-    dim3 grid(pf_cdiv(NA, RPC / 2), nplanes, fb.nf);
-    k_pa<L, 4><<<grid, 128, smem_a<L, 4>(), st>>>(planes, kturns, g, tw, ws_a_out, fb);
-    PF_LAUNCH_CHECK("k_pa");
-  } else if (stage == 0) {
+  if (stage == 0) {   // A: kernel rows -> At
     dim3 grid(pf_cdiv(NA, RPC), nplanes, fb.nf);
     k_pa<L><<<grid, FT, smem_a<L>(), st>>>(planes, kturns, g, tw, ws_a_out, fb);
     PF_LAUNCH_CHECK("k_pa");
-  } else if (stage == 1 && pf_splitb_env()) {
-    static bool a4 = false;
-    if (!a4) {
-      cudaFuncSetAttribute(k_pb1<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_pb2<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_pb2<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      a4 = true;
-    }
+  } else if (stage == 1) {   // B1 (Ghat quadrant in place) + B2 (product, y-IFFT, crop)
     const size_t sm = 8 * WFFT_XCH * sizeof(float2);
     dim3 g1(pf_cdiv(NA, 8 * LPW), nplanes, fb.nf);
     k_pb1<L><<<g1, FT, sm, st>>>(nplanes, tw, const_cast<float2*>(ws_a), fb);
@@ -676,34 +408,7 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     else
       k_pb2<L, false><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
     PF_LAUNCH_CHECK("k_pb2");
-  } else if (stage == 1 && pf_persist_env()) {
-    const int I = g.n_illum;
-    const size_t sm = (8 * WFFT_XCH + 2 * (size_t)8 * LPW * NA + 4 * (size_t)I * P) * sizeof(float2);
-    const int items = NA * pf_cdiv(nplanes, 8 * LPW);
-    if (sm <= 220 * 1024) {
-      static bool a2 = false;
-      if (!a2) { cudaFuncSetAttribute(k_pbp<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); a2 = true; }
-      k_pbp<L><<<items < nsm() ? items : nsm(), FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat,
-                                                               ws_b_out, items);
-      PF_LAUNCH_CHECK("k_pbp");
-      return 0;
-    }
-    dim3 grid(NA, pf_cdiv(nplanes, 8 * LPW));
-    k_pb<L><<<grid, FT, 8 * WFFT_XCH * sizeof(float2), st>>>(planes, nplanes, g, tw, ws_a, uhat,
-                                                             ws_b_out);
-    PF_LAUNCH_CHECK("k_pb");
-  } else if (stage == 1) {
-    dim3 grid(NA, pf_cdiv(nplanes, 8 * LPW));
-    k_pb<L><<<grid, FT, 8 * WFFT_XCH * sizeof(float2), st>>>(planes, nplanes, g, tw, ws_a, uhat,
-                                                             ws_b_out);
-    PF_LAUNCH_CHECK("k_pb");
-  } else if (fb.kturns != nullptr) {
-    static bool a5 = false;
-    if (!a5) {
-      cudaFuncSetAttribute(k_pcf<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_pcf<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      a5 = true;
-    }
+  } else if (fb.kturns != nullptr) {   // C over all frequencies of the batch
     dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
     const size_t sm = smem_c<L>(g.nx, false);
     if (g.n_illum > 1)
@@ -711,39 +416,7 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     else
       k_pcf<L, false><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
     PF_LAUNCH_CHECK("k_pcf");
-  } else if (pf_persist_env() &&
-             (8 * WFFT_XCH + 2 * (size_t)g.n_illum * P * (RPC + 1)) * sizeof(float2) <= 220 * 1024) {
-    const size_t sm = (8 * WFFT_XCH + 2 * (size_t)g.n_illum * P * (RPC + 1)) * sizeof(float2);
-    const int items = pf_cdiv(g.ny, RPC) * nplanes;
-    const int grid = items < nsm() ? items : nsm();
-    static bool a3 = false;
-    if (!a3) {
-      cudaFuncSetAttribute(k_pcp<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      cudaFuncSetAttribute(k_pcp<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      a3 = true;
-    }
-    if (g.n_illum > 1)
-      k_pcp<L, true><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames,
-                                           vol, vfs, items);
-    else
-      k_pcp<L, false><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames,
-                                            vol, vfs, items);
-    PF_LAUNCH_CHECK("k_pcp");
-  } else if (pf_nw_env() == 4 && g.n_illum == 1) {
-    static bool a7 = false;
-    if (!a7) {
-      cudaFuncSetAttribute(k_pc<L, false, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_pc<L, false, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      a7 = true;
-    }
-    dim3 grid(pf_cdiv(g.ny, RPC / 2), nplanes);
-    const bool pre = n_frames == 1 && frame_w != nullptr && getenv("PF_NOPRE") == nullptr &&
-                     (size_t)(RPC / 2) * g.nx * 8 <= 64 * 1024;
-    const size_t sm = smem_c<L, 4>(g.nx, pre);
-    if (pre) k_pc<L, false, true, 4><<<grid, 128, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
-    else k_pc<L, false, false, 4><<<grid, 128, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
-    PF_LAUNCH_CHECK("k_pc");
-  } else {
+  } else {   // C: x-IFFT, crop, illumination phase, volume accumulate
     dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
     const bool pre = n_frames == 1 && frame_w != nullptr && (size_t)RPC * g.nx * 8 <= 64 * 1024;
     const size_t sm = smem_c<L>(g.nx, pre);

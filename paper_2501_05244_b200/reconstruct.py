@@ -43,7 +43,6 @@ _BATCH_BYTES = 64 << 20
 _LANES = int(os.environ.get("PF_LANES", "3"))
 _FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "4"))
 _FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
-_FGROUP = int(os.environ.get("PF_FGROUP", "1"))
 _MEGA = os.environ.get("PF_MEGA", "0") == "1"   # measured slower
 _MEGA_LAG = int(os.environ.get("PF_MEGA_LAG", "2"))
 _MEGA_GP = int(os.environ.get("PF_MEGA_GP", "4"))
@@ -231,37 +230,6 @@ class Propagator:
                   nf, ctypes.byref(g), self.plan_x.ref, dev.ptr(self._fb_ws_a), fa, dev.ptr(uhat),
                   uhat_fs, dev.ptr(self._fb_ws_b), fbs, ill_ptr, dev.ptr(frame_w), dev.ptr(vol),
                   dev.stream_ptr(stream))
-
-    def run_fgroups(self, uhat: torch.Tensor, uhat_fs: int, freqs: np.ndarray, ill_ptr: int,
-                    frame_w: torch.Tensor, vol: torch.Tensor, nfg: int, stream=None) -> None:
-        """Plane batches x groups of ``nfg`` frequencies: one launch per stage and group,
-        the group's frequencies summed in registers by kernel C (static volumes)."""
-        g = self.geom
-        na = (g.py // 2 + 1) * (g.px // 2 + 1)
-        nbb = self.batch * g.n_illum * g.ny * g.px
-        if getattr(self, "_fg_key", None) != (nfg, freqs.size):
-            nl = len(self.lane_streams)
-            self._fg_ws = [(torch.empty((nfg * self.batch * na,), dtype=torch.complex64,
-                                        device=self.device),
-                            torch.empty((nfg * nbb,), dtype=torch.complex64, device=self.device))
-                           for _ in range(nl)]
-            self._fg_kt = torch.from_numpy(np.asarray(freqs, dtype=np.float64)
-                                           / (SPEED_OF_LIGHT * 2 * np.pi)).to(self.device)
-            self._fg_key = (nfg, freqs.size)
-        gref = ctypes.byref(g)
-        base = dev.ptr(self.planes_dev)
-
-        def body(b0, b1, lane, ls):
-            wa, wb = self._fg_ws[lane]
-            for f0 in range(0, freqs.size, nfg):
-                nf = min(nfg, freqs.size - f0)
-                _lib.call("pf_prop_fbatch", base + b0 * self.plane_size, b1 - b0,
-                          dev.ptr(self._fg_kt) + 8 * f0, nf, gref, self.plan_x.ref, dev.ptr(wa),
-                          (b1 - b0) * na, dev.ptr(uhat) + 8 * f0 * uhat_fs, uhat_fs, dev.ptr(wb),
-                          nbb, ill_ptr, dev.ptr(frame_w) + 8 * f0, dev.ptr(vol),
-                          dev.stream_ptr(ls))
-
-        self.run_batches(body, stream)
 
     def run_mega(self, uhat: torch.Tensor, uhat_fs: int, freqs: np.ndarray, ill_ptr: int,
                  frame_w: torch.Tensor, n_frames: int, vol: torch.Tensor, vol_frame_stride: int,
@@ -529,10 +497,6 @@ class RsdEngine(GraphedRun):
         if self.prop.fbatch_ok(self.freqs.size, self.n_frames):
             self.prop.run_fbatch(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w, vol,
                                  stream)
-            return vol
-        if _FGROUP > 1 and self.prop.transposed and self.n_frames == 1:
-            self.prop.run_fgroups(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w, vol,
-                                  _FGROUP, stream)
             return vol
 
         if self.prop.run_mega(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w,
