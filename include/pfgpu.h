@@ -176,6 +176,14 @@ int pf_prop_mega_aborted(const int32_t* counters, int njobs);
  * histograms read straight into device memory.  x must be 16-byte aligned. */
 int pf_count_nonfinite(const float* x, int64_t n, int32_t* out, void* stream);
 
+/* rsd3d stage-1 gridding (reconstruct.py:680-707, np.add.at onto the virtual
+ * lattice): for touched cell c, out[v][cells[c]] = sum_{e in [cell_start[c],
+ * cell_start[c+1])} ent_w[e] * vals[v][ent_pt[e]] (fixed order, no atomics).
+ * Cells not listed are left untouched (the caller zeroes the lattice). */
+int pf_scatter_csr(const int32_t* cell_start, const int64_t* cells, const int32_t* ent_pt,
+                   const float* ent_w, int n_cells, const void* vals, int64_t val_stride, int nv,
+                   void* out, int64_t out_stride, void* stream);
+
 /* ---------------------------------------------------------------- SFFT (Bluestein)
  * Scaled-DFT lines, replacing SfftPlan.apply (spectral.py:160-168) inside
  * sfft_2d_centered (:209-218): per plane b (grid y) the tables chirp[b][M] and

@@ -686,6 +686,91 @@ def nursd3d_stage1(slices, grid, eps=1e-6, z_pitch=None):
     return geo, out
 
 
+def rsd3d_scatter(geo, scatter):
+    """Lattice slots and weights of the stage-1 gridding (reconstruct.py:680-703): nearest
+    (1 slot, weight 1) or trilinear (8 corners, products of the per-axis linear weights);
+    slot index j on an axis of length n is the centred lag j - n//2."""
+    px, py, pz = geo["px"], geo["py"], geo["pz"]
+    fx = geo["nu_rx"] + px // 2
+    fy = geo["nu_ry"] + py // 2
+    fz = (geo["rel"][:, 2] - geo["z_min"]) / geo["dz3"] + (pz // 2 - geo["nz3"] // 2)
+    if scatter == "nearest":
+        ix = np.round(fx).astype(np.int64)[:, None]
+        iy = np.round(fy).astype(np.int64)[:, None]
+        iz = np.round(fz).astype(np.int64)[:, None]
+        w = np.ones((fx.size, 1))
+    else:
+        def corners(f):
+            lo = np.floor(f).astype(np.int64)
+            fr = f - lo
+            return np.stack([lo, lo + 1], axis=1), np.stack([1.0 - fr, fr], axis=1)
+        gx, wx = corners(fx)
+        gy, wy = corners(fy)
+        gz, wz = corners(fz)
+        iz = np.broadcast_to(gz[:, :, None, None], (fx.size, 2, 2, 2)).reshape(-1, 8)
+        iy = np.broadcast_to(gy[:, None, :, None], (fx.size, 2, 2, 2)).reshape(-1, 8)
+        ix = np.broadcast_to(gx[:, None, None, :], (fx.size, 2, 2, 2)).reshape(-1, 8)
+        w = (wz[:, :, None, None] * wy[:, None, :, None] * wx[:, None, None, :]).reshape(-1, 8)
+    for idx, n in ((ix, px), (iy, py), (iz, pz)):
+        _need(idx.min() >= 0 and idx.max() < n, "relay scatter indices escaped the lattice")
+    return iz, iy, ix, w
+
+
+def rsd3d_stage1(slices, grid, scatter="trilinear", z_pitch=None):
+    """Per (f, illumination) virtual-plane spectrum of rsd3d (reconstruct.py:705-716):
+    gridding, cfft_n, x cfft_n(G3), cifft_n, slab, cfft_2d."""
+    geo = lattice_3d(slices, grid, z_pitch)
+    vg = grid.grid
+    px, py, pz = geo["px"], geo["py"], geo["pz"]
+    iz, iy, ix, w = rsd3d_scatter(geo, scatter)
+    coeff = np.asarray(slices.coefficients)
+    out = []
+    for fi, om in enumerate(np.asarray(slices.frequencies)):
+        khat = om / C
+        g3 = cfft(kernel_3d(khat, px, py, pz, vg.dx, vg.dy, geo["dz3"]), (-3, -2, -1))
+        per_p = []
+        for p in range(coeff.shape[0]):
+            fine = np.zeros((pz, py, px), dtype=np.complex128)
+            np.add.at(fine, (iz, iy, ix), coeff[p, :, fi][:, None] * w)
+            wave = cifft(cfft(fine, (-3, -2, -1)) * g3, (-3, -2, -1))
+            per_p.append(cfft2(wave[geo["slab"]]))
+        out.append(np.stack(per_p))
+    return geo, out
+
+
+def rsd3d(slices, grid, scatter="trilinear", z_pitch=None, times=None,
+          include_illumination=True):
+    """3D relay -> cuboid by gridding + 3D convolution (reconstruct.py:662-719)."""
+    geo, uplanes = rsd3d_stage1(slices, grid, scatter, z_pitch)
+    return _stage2(slices, grid, geo, uplanes, times, include_illumination)
+
+
+def _stage2(slices, grid, geo, uplanes, times, include_illumination):
+    """Virtual plane z0 -> every output plane (reconstruct.py:641-659)."""
+    vg = grid.grid
+    px, py = geo["px"], geo["py"]
+    zs = vg.z_coords()
+    lag_x = (np.arange(px) - px // 2) * vg.dx
+    lag_y = (np.arange(py) - py // 2) * vg.dy
+    rows = center_slice(py, vg.ny)
+    cols = center_slice(px, vg.nx)
+    xs = vg.x0 + vg.dx * np.arange(vg.nx)
+    ys = vg.y0 + vg.dy * np.arange(vg.ny)
+    ill = ill_coords(slices)
+    freqs = np.asarray(slices.frequencies)
+
+    def term(fi):
+        khat = freqs[fi] / C
+        vol = np.zeros((zs.size, vg.ny, vg.nx), dtype=np.complex128)
+        for p in range(ill.shape[0]):
+            vol += _propagate_planes(uplanes[fi][p], khat, lag_x, lag_y, zs - geo["z0"],
+                                     rows, cols, lambda k: (xs, ys), lambda k: float(zs[k]),
+                                     ill[p], include_illumination)
+        return vol.ravel()
+
+    return _reduce((term(f) for f in range(slices.n_freq)), freqs, grid.count, times)
+
+
 def nursd3d(slices, grid, eps=1e-6, z_pitch=None, times=None, include_illumination=True):
     """3D scattered relay -> cuboid (reconstruct.py:722-765)."""
     rel = np.asarray(slices.relay.points.points)

@@ -590,32 +590,29 @@ def _lattice_3d(slices, grid, z_pitch):
     return rel, dz3, z_min, nz3, pz, z0, nu_rx, nu_ry, px, py, slab
 
 
-class Nursd3dEngine(_UhatPropEngine):
-    """Stage 1: 3D type-1 NUFFT -> x cfft_n(G3) -> cifft_n -> slab -> cfft_2d; stage 2: propagate."""
+class _Lattice3dEngine(_UhatPropEngine):
+    """Shared two-stage structure of nursd3d / rsd3d (reconstruct.py:662-765): stage 1
+    forms the virtual-lattice spectrum (subclass), x cfft_n(G3) -> cifft_n -> slab ->
+    cfft_2d; stage 2 propagates the virtual plane to every output plane."""
 
-    def __init__(self, slices, grid, eps=1e-6, z_pitch=None, include_illumination=True,
-                 times=None, device=None, plane_range=None):
-        _require(_kind(grid) == "cuboid", "nursd3d reconstructs onto a cuboid grid")
-        (rel, dz3, z_min, nz3, pz, z0, nu_rx, nu_ry, px, py, slab) = _lattice_3d(slices, grid,
-                                                                                 z_pitch)
+    def _setup_lattice(self, slices, grid, z_pitch, include_illumination, times, device,
+                       plane_range):
+        _require(_kind(grid) == "cuboid", self.GRID_MSG)
+        geo = _lattice_3d(slices, grid, z_pitch)
+        (rel, dz3, z_min, nz3, pz, z0, nu_rx, nu_ry, px, py, slab) = geo
         self.times = _check_times(times)
         self.device = device or dev.require_cuda()
         vg = grid.grid
         self.vg, self.grid = vg, grid
         self.px, self.py, self.pz, self.dz3, self.z0 = px, py, pz, dz3, z0
         self.slab_nat = (slab - pz // 2) % pz
-        c_z = z_min + (nz3 // 2) * dz3
-        nu_rz = (rel[:, 2] - c_z) / dz3
-        torus = np.column_stack([2.0 * np.pi * nu_rx / px, 2.0 * np.pi * nu_ry / py,
-                                 2.0 * np.pi * nu_rz / pz])
-        self.plan = nu.NufftPlan((pz, py, px), eps, self.device)
-        self.pts = self.plan.points(torus)
         self.freqs = np.asarray(slices.frequencies, dtype=np.float64)
         self.n_illum = int(slices.illuminations.count)
         self._setup_prop(px, py, vg, z0, include_illumination, plane_range or (0, vg.nz))
         self.ill = _ill_tensor(slices, self.device)
         self.frame_w = _frame_weights(self.freqs, self.times, self.device)
         self.n_frames = 1 if self.times is None else self.times.size
+        return geo
 
     def virtual_planes(self, coeff, stream=None):
         """wave[slab] per (f, illumination), natural order [F*I][py][px] (reconstruct.py:741-760)."""
@@ -625,11 +622,9 @@ class Nursd3dEngine(_UhatPropEngine):
         s = dev.stream_ptr(stream)
         uhat3 = torch.empty((I * n3,), dtype=torch.complex64, device=self.device)
         g3 = torch.empty((n3,), dtype=torch.complex64, device=self.device)
-        fine = torch.empty((I, self.plan.fine_elems), dtype=torch.complex64, device=self.device)
         out = torch.empty((F * I * py * px,), dtype=torch.complex64, device=self.device)
         for fi in range(F):
-            nu.type1(self.plan, self.pts, coeff[fi], I, coeff.shape[-1], uhat3, n3, fine,
-                     False, stream)
+            self._lattice_spectrum(coeff[fi], uhat3, n3, stream)
             khat = float(self.freqs[fi]) / C
             _lib.call("pf_kernel3d", dev.ptr(g3), pz, py, px, self.vg.dx, self.vg.dy, self.dz3,
                       khat, s)
@@ -660,6 +655,87 @@ class Nursd3dEngine(_UhatPropEngine):
         return self._propagate(self.relay_spectra(coeff, stream), vol, stream)
 
 
+class Nursd3dEngine(_Lattice3dEngine):
+    """Stage 1 by a 3D type-1 NUFFT of the scattered relay (reconstruct.py:741-760)."""
+
+    GRID_MSG = "nursd3d reconstructs onto a cuboid grid"
+
+    def __init__(self, slices, grid, eps=1e-6, z_pitch=None, include_illumination=True,
+                 times=None, device=None, plane_range=None):
+        (rel, dz3, z_min, nz3, pz, z0, nu_rx, nu_ry, px, py, slab) = self._setup_lattice(
+            slices, grid, z_pitch, include_illumination, times, device, plane_range)
+        c_z = z_min + (nz3 // 2) * dz3
+        nu_rz = (rel[:, 2] - c_z) / dz3
+        torus = np.column_stack([2.0 * np.pi * nu_rx / px, 2.0 * np.pi * nu_ry / py,
+                                 2.0 * np.pi * nu_rz / pz])
+        self.plan = nu.NufftPlan((pz, py, px), eps, self.device)
+        self.pts = self.plan.points(torus)
+        self._fine = torch.empty((self.n_illum, self.plan.fine_elems), dtype=torch.complex64,
+                                 device=self.device)
+
+    def _lattice_spectrum(self, coeff_f, uhat3, n3, stream):
+        nu.type1(self.plan, self.pts, coeff_f, self.n_illum, coeff_f.shape[-1], uhat3, n3,
+                 self._fine, False, stream)
+
+
+class Rsd3dEngine(_Lattice3dEngine):
+    """Stage 1 by gridding the relay onto the virtual lattice (reconstruct.py:662-719):
+    nearest or trilinear weights, duplicate targets summed, then cfft_n."""
+
+    GRID_MSG = "rsd3d reconstructs onto a cuboid grid"
+
+    def __init__(self, slices, grid, scatter="trilinear", z_pitch=None,
+                 include_illumination=True, times=None, device=None, plane_range=None):
+        _require(scatter in ("nearest", "trilinear"), "scatter must be 'nearest' or 'trilinear'")
+        (rel, dz3, z_min, nz3, pz, z0, nu_rx, nu_ry, px, py, slab) = self._setup_lattice(
+            slices, grid, z_pitch, include_illumination, times, device, plane_range)
+        fx = nu_rx + px // 2
+        fy = nu_ry + py // 2
+        fz = (rel[:, 2] - z_min) / dz3 + (pz // 2 - nz3 // 2)
+        n = fx.size
+        if scatter == "nearest":
+            ix = np.round(fx).astype(np.int64)[:, None]
+            iy = np.round(fy).astype(np.int64)[:, None]
+            iz = np.round(fz).astype(np.int64)[:, None]
+            w = np.ones((n, 1))
+        else:
+            def corners(f):
+                lo = np.floor(f).astype(np.int64)
+                fr = f - lo
+                return np.stack([lo, lo + 1], axis=1), np.stack([1.0 - fr, fr], axis=1)
+            gx, wx = corners(fx)
+            gy, wy = corners(fy)
+            gz, wz = corners(fz)
+            iz = np.broadcast_to(gz[:, :, None, None], (n, 2, 2, 2)).reshape(n, 8)
+            iy = np.broadcast_to(gy[:, None, :, None], (n, 2, 2, 2)).reshape(n, 8)
+            ix = np.broadcast_to(gx[:, None, None, :], (n, 2, 2, 2)).reshape(n, 8)
+            w = (wz[:, :, None, None] * wy[:, None, :, None] * wx[:, None, None, :]).reshape(n, 8)
+        for name, idx, bound in (("x", ix, px), ("y", iy, py), ("z", iz, pz)):
+            assert idx.min() >= 0 and idx.max() < bound, \
+                f"relay scatter indices escaped the {name} lattice"
+        # lattice slot j holds centred lag j - n//2: its natural-order cell
+        cell = ((((iz - pz // 2) % pz) * py + (iy - py // 2) % py) * px
+                + (ix - px // 2) % px).ravel()
+        pt = np.repeat(np.arange(n, dtype=np.int64), w.shape[1])
+        order = np.argsort(cell, kind="stable")
+        cell, pt, wf = cell[order], pt[order], w.ravel()[order]
+        uniq, start = np.unique(cell, return_index=True)
+        starts = np.append(start, cell.size).astype(np.int32)
+        d = self.device
+        self._csr = (torch.from_numpy(starts).to(d), torch.from_numpy(uniq.astype(np.int64)).to(d),
+                     torch.from_numpy(pt.astype(np.int32)).to(d),
+                     torch.from_numpy(wf.astype(np.float32)).to(d), int(uniq.size))
+        self.n_relay = n
+
+    def _lattice_spectrum(self, coeff_f, uhat3, n3, stream):
+        st, cells, pts, wts, nc = self._csr
+        uhat3.zero_()
+        _lib.call("pf_scatter_csr", dev.ptr(st), dev.ptr(cells), dev.ptr(pts), dev.ptr(wts), nc,
+                  dev.ptr(coeff_f), coeff_f.shape[-1], self.n_illum, dev.ptr(uhat3), n3,
+                  dev.stream_ptr(stream))
+        dev.fftn_natural(uhat3, (self.pz, self.py, self.px), self.n_illum, -1, 1.0, stream)
+
+
 def nursd3d(slices, grid, eps: float = 1e-6, z_pitch: float | None = None, times=None,
             threads: int = 1, include_illumination: bool = True):
     """Scattered 3D relay -> cuboid (reconstruct.py:722-765)."""
@@ -676,15 +752,9 @@ def nursd3d(slices, grid, eps: float = 1e-6, z_pitch: float | None = None, times
 
 def rsd3d(slices, grid, scatter: str = "trilinear", z_pitch: float | None = None, times=None,
           threads: int = 1, include_illumination: bool = True):
-    """3D trilinear-gridding variant (reference reconstruct.py:662-719).
-
-    Out of the accelerated scope (no config names it); validated here
-    so callers get the reference's errors, then refused explicitly.
-    """
-    _require(_kind(grid) == "cuboid", "rsd3d reconstructs onto a cuboid grid")
-    _require(scatter in ("nearest", "trilinear"), "scatter must be 'nearest' or 'trilinear'")
-    _lattice_3d(slices, grid, z_pitch)
-    raise NotImplementedError("rsd3d is outside the GPU engine's scope (use nursd3d)")
+    """3D relay -> cuboid by gridding + one 3D convolution (reconstruct.py:662-719)."""
+    eng = Rsd3dEngine(slices, grid, scatter, z_pitch, include_illumination, times)
+    return _volume(grid, eng.run(device_coefficients(slices)), eng.times)
 
 
 # ---------------------------------------------------------------------------

@@ -157,3 +157,44 @@ extern "C" int pf_count_nonfinite(const float* x, int64_t n, int32_t* out, void*
   PF_LAUNCH_CHECK("k_count_nonfinite");
   return 0;
 }
+
+// ---- rsd3d stage-1 gridding (reference reconstruct.py:680-707: np.add.at of
+// coefficient x weight onto the virtual lattice; duplicate targets sum).  The
+// geometry-only plan lists, per touched lattice cell, its (point, weight)
+// contributions (CSR, host-built); one thread per touched cell sums them in
+// fixed order for every value set, so the result is deterministic without
+// atomics.  Untouched cells are zeroed by the caller.
+__global__ void k_scatter_csr(const int* __restrict__ cell_start, const long long* __restrict__ cells,
+                              const int* __restrict__ ent_pt, const float* __restrict__ ent_w,
+                              int n_cells, const float2* __restrict__ vals, long long val_stride,
+                              int nv, float2* __restrict__ out, long long out_stride) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += gridDim.x * blockDim.x) {
+    const int e0 = cell_start[c], e1 = cell_start[c + 1];
+    const long long dst = cells[c];
+    for (int v = 0; v < nv; v++) {
+      const float2* vv = vals + (long long)v * val_stride;
+      float2 acc = make_float2(0.f, 0.f);
+      for (int e = e0; e < e1; e++) {
+        const float w = ent_w[e];
+        const float2 x = vv[ent_pt[e]];
+        acc.x = fmaf(w, x.x, acc.x);
+        acc.y = fmaf(w, x.y, acc.y);
+      }
+      out[(long long)v * out_stride + dst] = acc;
+    }
+  }
+}
+
+extern "C" int pf_scatter_csr(const int32_t* cell_start, const int64_t* cells,
+                              const int32_t* ent_pt, const float* ent_w, int n_cells,
+                              const void* vals, int64_t val_stride, int nv, void* out,
+                              int64_t out_stride, void* stream) {
+  PF_ARG_CHECK(n_cells >= 0 && nv >= 1, "pf_scatter_csr: bad sizes");
+  if (n_cells == 0) return 0;
+  const int grid = pf_cdiv(n_cells, 256) < 148 * 16 ? pf_cdiv(n_cells, 256) : 148 * 16;
+  k_scatter_csr<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      cell_start, (const long long*)cells, ent_pt, ent_w, n_cells, (const float2*)vals,
+      val_stride, nv, (float2*)out, out_stride);
+  PF_LAUNCH_CHECK("k_scatter_csr");
+  return 0;
+}

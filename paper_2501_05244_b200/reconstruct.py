@@ -307,7 +307,7 @@ def _frame_weights(freqs: np.ndarray, times, device) -> torch.Tensor:
 
 def _ill_tensor(slices, device) -> torch.Tensor:
     ill = illumination_coordinates(slices.relay, slices.illuminations)
-    return torch.from_numpy(np.ascontiguousarray(ill, dtype=np.float64)).to(device)
+    return torch.from_numpy(np.array(ill, dtype=np.float64, copy=True)).to(device)
 
 
 def _volume(grid, vol: torch.Tensor, times) -> ReconstructionVolume:

@@ -239,6 +239,8 @@ def gen_reconstruct():
     sl_c = two_scatterer(rel_c, pf.PointList(np.array([[0.0, 0.0, 0.0]])))
     g3 = pf.CuboidGrid(UniformGrid3D(8, 8, 2, 0.02, 0.02, 0.08, -0.07, -0.07, 0.86))
     put("nursd3d_curved", sl_c, g3, R.nursd3d(sl_c, g3, eps=1e-6).field)
+    put("rsd3d_curved_tri", sl_c, g3, R.rsd3d(sl_c, g3, scatter="trilinear").field)
+    put("rsd3d_curved_near", sl_c, g3, R.rsd3d(sl_c, g3, scatter="nearest").field)
     # odd relay size (odd pads, centred-index shifts)
     relay9 = pf.UniformRelay(pf.UniformGrid2D(9, 7, 0.02, 0.025, -0.08, -0.075, 0.0))
     sl9 = two_scatterer(relay9)

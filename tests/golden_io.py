@@ -53,6 +53,7 @@ REC_CASES = [
     "chain_srsd_unit", "chain_srsd_08", "chain_nursd1", "chain_nursd2", "chain_nursd3",
     "chain_hybrid", "chain_nursd3d_flat", "nursd1_random", "nursd2_random", "nursd3_random",
     "hybrid_random", "srsd_linear16", "srsd_aniso16", "nursd3d_curved", "rsd_odd", "rsd_odd_none",
+    "rsd3d_curved_tri", "rsd3d_curved_near",
 ]
 
 
@@ -81,5 +82,7 @@ def case_call(name):
         "nursd3d_curved": ("nursd3d", {"eps": 1e-6}),
         "rsd_odd": ("rsd", {}),
         "rsd_odd_none": ("rsd", {"padding": "none"}),
+        "rsd3d_curved_tri": ("rsd3d", {"scatter": "trilinear"}),
+        "rsd3d_curved_near": ("rsd3d", {"scatter": "nearest"}),
     }
     return table[name]

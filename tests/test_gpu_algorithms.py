@@ -1,4 +1,5 @@
-"""GPU parity of srsd / nursd1 / nursd2 / nursd3 / srsd_nursd2 / nursd3d vs reference goldens + oracle."""
+"""GPU parity of srsd / nursd1 / nursd2 / nursd3 / srsd_nursd2 / nursd3d / rsd3d vs reference
+goldens + oracle."""
 
 import numpy as np
 import pytest
@@ -12,7 +13,8 @@ TOL = 1e-4
 
 CASES = ["chain_srsd_unit", "chain_srsd_08", "chain_nursd1", "chain_nursd2", "chain_nursd3",
          "chain_hybrid", "chain_nursd3d_flat", "nursd1_random", "nursd2_random", "nursd3_random",
-         "hybrid_random", "srsd_linear16", "srsd_aniso16", "nursd3d_curved"]
+         "hybrid_random", "srsd_linear16", "srsd_aniso16", "nursd3d_curved", "rsd3d_curved_tri",
+         "rsd3d_curved_near"]
 
 
 @pytest.mark.parametrize("name", CASES)
@@ -123,4 +125,22 @@ def test_config2_composed_small(rng):
     ev = pf.ExplicitVoxels(planes)
     vol = nursd3d_explicit(sl, ev, lattice)
     ref = O.nursd3d_explicit(sl, ev, lattice)
+    assert O.rel_l2(vol.field, ref) < TOL
+
+
+@pytest.mark.parametrize("scatter", ["trilinear", "nearest"])
+def test_rsd3d_random_relay_vs_oracle(rng, scatter):
+    """rsd3d (reconstruct.py:662-719) on a random curved 3D relay with duplicate lattice
+    targets, several frequencies and a time-resolved volume, against the float64 oracle."""
+    xy = rng.uniform(-0.3, 0.3, size=(400, 2))
+    z = 0.02 * np.sin(2 * np.pi * xy[:, 0] / 0.4) * np.cos(2 * np.pi * xy[:, 1] / 0.5)
+    relay = pf.NonPlanarRelay(pf.PointList(np.column_stack([xy, z])))
+    F = 3
+    freqs = 2 * np.pi * 3e8 / 0.06 * (1 + 0.03 * np.arange(F))
+    coeff = rng.normal(size=(1, 400, F)) + 1j * rng.normal(size=(1, 400, F))
+    sl = pf.FrequencySlices(freqs, coeff, relay, pf.PointList(np.zeros((1, 3))))
+    grid = pf.CuboidGrid(pf.UniformGrid3D(24, 20, 3, 0.025, 0.025, 0.1, -0.29, -0.24, 0.6))
+    times = np.array([0.0, 2e-10])
+    vol = pf.reconstruct(sl, grid, "rsd3d", scatter=scatter, times=times)
+    ref = O.rsd3d(sl, grid, scatter=scatter, times=times)
     assert O.rel_l2(vol.field, ref) < TOL

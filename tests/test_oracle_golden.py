@@ -7,7 +7,8 @@ from oracle import pf_oracle as O
 from golden_io import REC_CASES, case_call, grid_from, load, slices_from
 
 ORACLE_FN = {"rsd": O.rsd, "srsd": O.srsd, "nursd1": O.nursd1, "nursd2": O.nursd2,
-             "nursd3": O.nursd3, "srsd-nursd2": O.srsd_nursd2, "nursd3d": O.nursd3d}
+             "nursd3": O.nursd3, "srsd-nursd2": O.srsd_nursd2, "nursd3d": O.nursd3d,
+             "rsd3d": O.rsd3d}
 
 
 def test_build_kernel_kats():
