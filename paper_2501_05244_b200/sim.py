@@ -1,21 +1,129 @@
-"""Seeded synthetic transients (input generation for benches and tests; not the hot path).
+"""Synthetic transient capture (input generation, not the hot path).
 
-Semantics follow reference ``sim.simulate`` (sim.py:67-115): each
-(illumination p, detector c, scatterer s) return arrives at
+Two entry points:
+
+* ``simulate`` / ``add_poisson_noise`` / ``Scene`` / ``Scatterer`` mirror the reference
+  module (``sim.py:37-129``): same arguments, same window and coincidence errors,
+  confocal capture, ambient level, float64 histograms; the deposit runs vectorised on
+  the GPU in float64 (the reference loops in Python: ~10 h for config 4), and the
+  Poisson draw uses the reference's own numpy generator so seeded draws are identical.
+* ``simulate_device`` is the bench generator: float32 histograms left on the device,
+  and returns outside the window DROPPED instead of raising (the config-3/4 scenes span
+  more path length than their windows).
+
+Each (illumination p, detector c, scatterer s) return arrives at
 ``(|x_p - x_s| + |x_s - x_c|)/c``, carries ``albedo/(r1^2 r2^2)`` and is split
-linearly over the two bracketing bins.  Differences, documented in DESIGN.md:
-returns falling outside the time window are DROPPED instead of raising (the
-config-3/4 scenes span more path length than their windows), and
-the deposit runs vectorised on the GPU in float32 (the reference takes ~10 h
-for config 4 on the CPU).
+linearly over the two bracketing bins.
 """
 
 from __future__ import annotations
 
+import math
+from dataclasses import dataclass
+
 import numpy as np
 import torch
 
-from .core import SPEED_OF_LIGHT
+from .core import (SPEED_OF_LIGHT, PointList, TransientMeasurement, ValidationError, _require,
+                   illumination_coordinates)
+
+
+@dataclass(frozen=True)
+class Scatterer:
+    """Isotropic point scatterer (reference sim.py:37-49)."""
+
+    position: tuple
+    albedo: float = 1.0
+
+    def __post_init__(self) -> None:
+        pos = tuple(float(v) for v in self.position)
+        _require(len(pos) == 3 and all(math.isfinite(v) for v in pos),
+                 "scatterer position must be a finite 3D point")
+        _require(self.albedo >= 0 and math.isfinite(self.albedo),
+                 "scatterer albedo must be >= 0")
+        object.__setattr__(self, "position", pos)
+
+
+@dataclass(frozen=True)
+class Scene:
+    """Point scatterers plus a constant ambient level per bin (reference sim.py:52-63)."""
+
+    scatterers: tuple
+    ambient: float = 0.0
+
+    def __post_init__(self) -> None:
+        object.__setattr__(self, "scatterers", tuple(self.scatterers))
+        _require(len(self.scatterers) >= 1, "scene needs at least one scatterer")
+        _require(self.ambient >= 0 and math.isfinite(self.ambient),
+                 "ambient level must be >= 0")
+
+
+def simulate(scene: Scene, relay, illuminations, delta_t: float, n_bins: int, t0: float = 0.0,
+             confocal: bool = False, falloff: bool = True, device=None) -> TransientMeasurement:
+    """Reference ``simulate`` (sim.py:66-115) with the deposit on the GPU in float64."""
+    _require(delta_t > 0, "bin width must be > 0")
+    _require(n_bins >= 2, "need at least two time bins")
+    device = device or torch.device("cuda")
+    det = relay.coordinates()
+    if confocal:
+        ill_points = PointList(det)
+        ill = det
+    else:
+        _require(illuminations is not None,
+                 "non-confocal capture needs explicit illumination points")
+        ill_points = illuminations
+        ill = illumination_coordinates(relay, illuminations)
+    P, D, S = ill.shape[0], det.shape[0], len(scene.scatterers)
+    pos = torch.tensor([s.position for s in scene.scatterers], dtype=torch.float64, device=device)
+    alb = torch.tensor([s.albedo for s in scene.scatterers], dtype=torch.float64, device=device)
+    dt = torch.as_tensor(np.array(det, dtype=np.float64), device=device)
+    it = torch.as_tensor(np.array(ill, dtype=np.float64), device=device)
+    # pair list in the reference's loop order (p-major; confocal: the diagonal)
+    if confocal:
+        pp = torch.arange(D, device=device)
+        cc = pp
+    else:
+        pp = torch.arange(P, device=device).repeat_interleave(D)
+        cc = torch.arange(D, device=device).repeat(P)
+    r1 = torch.linalg.norm(it[pp][:, None, :] - pos[None], dim=2)          # [pairs, S]
+    r2 = torch.linalg.norm(pos[None] - dt[cc][:, None, :], dim=2)
+    bad = (r1 <= 0) | (r2 <= 0)
+    if bool(bad.any()):
+        k = int(torch.nonzero(bad.reshape(-1))[0])
+        si = k % S
+        raise ValidationError(f"scatterer {si} at {scene.scatterers[si].position} coincides "
+                              "with a relay or illumination point")
+    amp = alb[None] / (r1 * r1 * r2 * r2) if falloff else alb[None].expand_as(r1)
+    b = ((r1 + r2) / SPEED_OF_LIGHT - t0) / delta_t
+    b0 = torch.floor(b)
+    frac = b - b0
+    out = (b0 < 0) | (b0 > n_bins - 1) | ((frac > 0) & (b0 + 1 > n_bins - 1))
+    if bool(out.any()):
+        k = int(torch.nonzero(out.reshape(-1))[0])
+        q, si = divmod(k, S)
+        p, c = int(pp[q]), int(cc[q])
+        raise ValidationError(
+            f"scatterer {si} at {scene.scatterers[si].position} arrives at bin "
+            f"{float(b.reshape(-1)[k]):.3f}, outside the {n_bins}-bin window "
+            f"(illumination {p}, detector {c})")
+    hist = torch.zeros((P * D * n_bins,), dtype=torch.float64, device=device)
+    base = ((pp * D + cc) * n_bins)[:, None]
+    idx = base + b0.to(torch.int64)
+    hist.index_add_(0, idx.reshape(-1), (amp * (1.0 - frac)).reshape(-1))
+    nz = (frac > 0).reshape(-1)
+    hist.index_add_(0, (idx + 1).reshape(-1)[nz], (amp * frac).reshape(-1)[nz])
+    hist = hist.view(P, D, n_bins)
+    if scene.ambient > 0:
+        hist[pp, cc, :] += scene.ambient
+    return TransientMeasurement(relay, ill_points, hist.cpu().numpy(), delta_t, t0)
+
+
+def add_poisson_noise(m, scale: float, seed: int) -> TransientMeasurement:
+    """Reference ``add_poisson_noise`` (sim.py:118-129): the same seeded numpy draw."""
+    _require(scale > 0 and math.isfinite(scale), "photon scale must be > 0")
+    rng = np.random.default_rng(seed)
+    noisy = rng.poisson(scale * np.asarray(m.histograms, dtype=np.float64)).astype(np.float64)
+    return TransientMeasurement(m.relay, m.illuminations, noisy, m.delta_t, m.t0)
 
 
 def simulate_device(scatterers: np.ndarray, albedo: np.ndarray, det_xyz: np.ndarray,
