@@ -125,3 +125,29 @@ def test_config4_nursd1_on_lattice_equals_zero_filled_rsd(planes):
     assert O.rel_l2(vol, vr.cpu().numpy()) < 1e-5
     ref = O.rsd(zf.to_host(), base.grid, plane_range=planes)
     _check(vol, ref, (planes[1] - planes[0], 512, 512))
+
+
+def test_config4_full_size_linearity_and_frequency_additivity():
+    """Full config-4 volume (67 M voxels, all 256 planes, 32 frequencies): size-independent
+    properties of the reference operator. (1) Linearity in the wavefront:
+    V(a u1 + b u2) = a V(u1) + b V(u2). (2) The volume is the ascending-frequency sum
+    (reconstruct.py:163-177): V(all f) = V(f < 16) + V(f >= 16)."""
+    cfg = configs.config(4)
+    sl, k = _slices(cfg)
+    c = sl.device_coefficients
+    g = torch.Generator(device="cuda").manual_seed(3)
+    u2 = torch.randn(c.shape, dtype=torch.complex64, device="cuda", generator=g)
+    eng = RsdEngine(sl, cfg.grid)
+    a, b = 0.7 - 0.2j, -1.3 + 0.5j
+    v1 = eng.run(c).clone()
+    v2 = eng.run(u2).clone()
+    v12 = eng.run((a * c + b * u2).contiguous()).clone()
+    lin = ((v12 - (a * v1 + b * v2)).norm() / v12.norm()).item()
+    assert lin < 1e-5, lin
+    lo = c.clone()
+    lo[16:] = 0
+    hi = c - lo
+    vlo = eng.run(lo).clone()
+    vhi = eng.run(hi)
+    add = ((v1 - (vlo + vhi)).norm() / v1.norm()).item()
+    assert add < 1e-6, add
