@@ -151,3 +151,32 @@ def test_config4_full_size_linearity_and_frequency_additivity():
     vhi = eng.run(hi)
     add = ((v1 - (vlo + vhi)).norm() / v1.norm()).item()
     assert add < 1e-6, add
+
+
+def test_config5_full_size_nursd1_equals_zero_filled_rsd():
+    """All 256 planes of the c4-NURSD1 workload: nursd1 on the 131,072 lattice nodes equals rsd
+    on the zero-filled 512x512 lattice over the whole 67 M-voxel volume."""
+    cfg = configs.config(5)
+    sl, k = _slices(cfg)
+    vol = Nursd1Engine(sl, cfg.grid).run(sl.device_coefficients).clone()
+    base = configs.config(4)
+    full = torch.zeros((k.n_freq, 1, base.relay.count), dtype=torch.complex64, device="cuda")
+    full[:, :, torch.from_numpy(cfg.lattice_nodes).cuda()] = sl.device_coefficients
+    zf = pf.DeviceFrequencySlices(k.frequencies, full, base.relay, base.illuminations)
+    vr = RsdEngine(zf, base.grid).run(full)
+    assert ((vol - vr).norm() / vr.norm()).item() < 1e-5
+
+
+def test_config3_full_size_linearity():
+    """srsd over all 128 frustum planes (8.4 M voxels): V(a u1 + b u2) = a V(u1) + b V(u2)."""
+    cfg = configs.config(3)
+    sl, k = _slices(cfg)
+    c = sl.device_coefficients
+    g = torch.Generator(device="cuda").manual_seed(5)
+    u2 = torch.randn(c.shape, dtype=torch.complex64, device="cuda", generator=g)
+    eng = SrsdEngine(sl, cfg.grid)
+    a, b = 1.1 + 0.4j, -0.6 - 0.9j
+    v1 = eng.run(c).clone()
+    v2 = eng.run(u2).clone()
+    v12 = eng.run((a * c + b * u2).contiguous())
+    assert ((v12 - (a * v1 + b * v2)).norm() / v12.norm()).item() < 1e-5
