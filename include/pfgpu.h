@@ -238,6 +238,10 @@ int pf_nufft_deconv(const pf_nufft_geom* g, const void* fine, int64_t fine_strid
 int pf_nufft_place(const pf_nufft_geom* g, const void* S, int64_t s_stride, const float* kz,
                    const float* ky, const float* kx, int nv, void* fine, int64_t fine_stride,
                    int transpose, void* stream);
+/* type-2 finish for any dimension (spectral.py:376-380): out[l] = stencil sum of the
+ * fine grid (after pf_nufft_place + inverse FFT) at point l; stencil width 2w+1 <= 32. */
+int pf_nufft_interp(const pf_nufft_geom* g, const int32_t* i0, const float* d0, int npts,
+                    const void* fine, void* out, void* stream);
 /* type-2 finish (spectral.py:377-380) fused with the per-voxel scale, the
  * illumination phase (reconstruct.py:140-144) and the ascending-frequency
  * accumulation (reconstruct.py:163-177): vol[f][dst0 + perm[l]] += sum_p(...) * frame_w[f]

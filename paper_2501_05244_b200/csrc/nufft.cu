@@ -293,6 +293,54 @@ __global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
   }
 }
 
+// Plain type-2 finish for any dimension (spectral.nufft2, reference spectral.py:376-380):
+// out[l] = sum over the (2w+1)^dim stencil of fine * prod(axis windows).  One warp per
+// point: lane = x tap (W <= 32), loops over the z and y taps (1 for missing axes).
+__global__ void __launch_bounds__(256)
+k_interp_any(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0, int npts,
+             const float2* __restrict__ fine, float2* __restrict__ out) {
+  const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (l >= npts) return;
+  const int W = 2 * G.w + 1;
+  const int Wz = G.dim == 3 ? W : 1, Wy = G.dim >= 2 ? W : 1;
+  const int mrz = G.mr[0], mry = G.mr[1], mrx = G.mr[2];
+  const bool on = lane < W;
+  const float dx = d0[3 * l + 2] + (float)(lane - G.w) * G.h[2];
+  const float wx = on ? __expf(-dx * dx * G.inv4tau[2]) : 0.f;
+  const int cx = wrap_once(natural((long long)i0[3 * l + 2] - G.w, mrx) + (on ? lane : 0), mrx);
+  const int cy0 = Wy > 1 ? natural((long long)i0[3 * l + 1] - G.w, mry) : 0;
+  int cz = Wz > 1 ? natural((long long)i0[3 * l] - G.w, mrz) : 0;
+  float2 acc = make_float2(0.f, 0.f);
+  for (int oz = 0; oz < Wz; oz++) {
+    float wz = 1.f;
+    if (Wz > 1) {
+      const float dz = d0[3 * l] + (float)(oz - G.w) * G.h[0];
+      wz = __expf(-dz * dz * G.inv4tau[0]);
+    }
+    int cy = cy0;
+    for (int oy = 0; oy < Wy; oy++) {
+      float wy = 1.f;
+      if (Wy > 1) {
+        const float dy = d0[3 * l + 1] + (float)(oy - G.w) * G.h[1];
+        wy = __expf(-dy * dy * G.inv4tau[1]);
+      }
+      const float w = wx * wy * wz;
+      const float2 f = __ldg(fine + ((long long)cz * mry + cy) * mrx + cx);
+      acc.x = fmaf(w, f.x, acc.x);
+      acc.y = fmaf(w, f.y, acc.y);
+      if (++cy == mry) cy = 0;
+    }
+    if (++cz == mrz) cz = 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  }
+  if (lane == 0) out[l] = acc;
+}
+
 int grid1d(long long total) {
   long long g = (total + 255) / 256;
   return (int)(g < 148 * 32 ? (g < 1 ? 1 : g) : 148 * 32);
@@ -361,5 +409,16 @@ extern "C" int pf_nufft_interp2_acc(const pf_nufft_geom* g, const int32_t* i0, c
       include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride,
       dst0, perm);
   PF_LAUNCH_CHECK("k_interp2_acc");
+  return 0;
+}
+
+extern "C" int pf_nufft_interp(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                               int npts, const void* fine, void* out, void* stream) {
+  PF_ARG_CHECK(g && g->dim >= 1 && g->dim <= 3 && 2 * g->w + 1 <= 32 && npts >= 0,
+               "pf_nufft_interp: bad args (stencil width must be <= 32)");
+  if (npts == 0) return 0;
+  k_interp_any<<<pf_cdiv(npts, 8), 256, 0, (cudaStream_t)stream>>>(
+      *g, i0, d0, npts, (const float2*)fine, (float2*)out);
+  PF_LAUNCH_CHECK("k_interp_any");
   return 0;
 }

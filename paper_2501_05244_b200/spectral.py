@@ -121,26 +121,21 @@ def nufft1(points, values, modes, eps: float):
 
 
 def nufft2(coefficients, points, eps: float):
-    """Type 2, exponent +1j, centred modes -> points (reference spectral.py:361-381); 1D/2D."""
+    """Type 2, exponent +1j, centred modes -> points (reference spectral.py:361-381); 1D-3D."""
     coeff = np.asarray(coefficients, dtype=np.complex128)
     _require(1 <= coeff.ndim <= 3, "mode array must be 1D, 2D, or 3D")
-    _require(coeff.ndim <= 2, "the GPU type-2 transform supports 1D and 2D modes")
     _require(bool(np.isfinite(coeff).all()), "coefficients must be finite")
     pts = nu.check_points(points, coeff.ndim)
-    c2 = coeff if coeff.ndim == 2 else coeff[None, :]
-    p2 = pts if coeff.ndim == 2 else np.column_stack([pts[:, 0], np.zeros(pts.shape[0])])
+    if coeff.ndim == 1:   # 1D as a single-row 2D problem (as nufft1)
+        coeff = coeff[None, :]
+        pts = np.column_stack([pts[:, 0], np.zeros(pts.shape[0])])   # x pairs with the last axis
     device = dev.require_cuda()
-    plan = nu.NufftPlan(c2.shape, eps, device)
-    S = _to_dev(np.fft.ifftshift(c2))            # centred slots -> natural order
+    plan = nu.NufftPlan(coeff.shape, eps, device)
+    S = _to_dev(np.fft.ifftshift(coeff))         # centred slots -> natural order
     fine = torch.empty((1, plan.fine_elems), dtype=torch.complex64, device=device)
     nu.place_and_inverse(plan, S, 1, plan.mode_elems, fine)
-    P = plan.points(p2)
-    L = p2.shape[0]
-    zero3 = torch.zeros((L, 3), dtype=torch.float64, device=device)
-    one = torch.ones((1,), dtype=torch.complex64, device=device)
-    ill = torch.zeros((1, 3), dtype=torch.float64, device=device)
-    out = torch.zeros((L,), dtype=torch.complex64, device=device)
-    _lib.call("pf_nufft_interp2_acc", plan.gref, dev.ptr(P.i0), dev.ptr(P.d0), dev.ptr(zero3), L,
-              dev.ptr(fine), plan.fine_elems, 1, dev.ptr(ill), 0.0, 0, 1.0, dev.ptr(one), 1,
-              dev.ptr(out), L, 0, None, dev.stream_ptr())
+    P = plan.points(pts)
+    out = torch.zeros((pts.shape[0],), dtype=torch.complex64, device=device)
+    _lib.call("pf_nufft_interp", plan.gref, dev.ptr(P.i0), dev.ptr(P.d0), pts.shape[0],
+              dev.ptr(fine), dev.ptr(out), dev.stream_ptr())
     return out.cpu().numpy().astype(np.complex128)
