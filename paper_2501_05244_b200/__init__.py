@@ -15,8 +15,9 @@ from .core import (PROPAGATION_SIGN, SPEED_OF_LIGHT, ContainerFormatError, Cuboi
                    ExplicitVoxels, FrequencySlices, FrustumGrid, InvalidMagicError,
                    NonFiniteDataError, NonPlanarRelay, NonUniformPlanarRelay, PointList,
                    ReconstructionVolume, TransientMeasurement, TruncatedPayloadError,
-                   UniformGrid2D, UniformGrid3D, UniformRelay, UnsupportedVersionError,
-                   ValidationError, VoxelPlane, grid_coordinates, illumination_coordinates)
+                   TorusMap, UniformGrid2D, UniformGrid3D, UniformRelay, UnsupportedVersionError,
+                   ValidationError, VoxelPlane, grid_coordinates, illumination_coordinates,
+                   rescale_to_torus)
 from .phasor import (DeviceFrequencySlices, PhasorKernel, build_kernel, to_frequency,
                      to_frequency_device)
 from .reconstruct import (ALGORITHM_NAMES, RsdEngine, light_transport_video, project_max_depth,
@@ -32,7 +33,11 @@ def __getattr__(name):
         from . import algorithms
         return getattr(algorithms, name)
     if name in ("cfft_n", "cifft_n", "cfft_2d", "cifft_2d", "sfft_1d", "sfft_2d",
-                "sfft_2d_centered", "nufft1", "nufft2", "next_fast_len"):
+                "sfft_2d_centered", "nufft1", "nufft2", "next_fast_len", "fft_2d", "ifft_2d",
+                "dft_2d", "idft_2d"):
         from . import spectral
         return getattr(spectral, name)
+    if name in ("Scatterer", "Scene", "simulate", "add_poisson_noise"):
+        from . import sim
+        return getattr(sim, name)
     raise AttributeError(name)

@@ -19,7 +19,7 @@ from ._fastlen import next_fast_len
 from .core import _require
 
 __all__ = ["cfft_n", "cifft_n", "cfft_2d", "cifft_2d", "sfft_1d", "sfft_2d", "sfft_2d_centered",
-           "nufft1", "nufft2", "next_fast_len"]
+           "nufft1", "nufft2", "next_fast_len", "fft_2d", "ifft_2d", "dft_2d", "idft_2d"]
 
 
 def _to_dev(a) -> torch.Tensor:
@@ -55,6 +55,39 @@ def cfft_n(u, axes):
 def cifft_n(u, axes):
     """Centred-index inverse DFT over ``axes`` with 1/N (reference spectral.py:112-114)."""
     return _centered(u, axes, +1)
+
+
+def fft_2d(u):
+    """Forward 2D DFT over the last two axes, natural order, unnormalised (spectral.py:97-99)."""
+    u = np.asarray(u, dtype=np.complex128)
+    _require(u.ndim >= 2, "fft_2d takes an array with at least two axes")
+    x = _to_dev(u)
+    dev.fft2_natural(x.view(-1), u.shape[-2], u.shape[-1], int(np.prod(u.shape[:-2])), -1)
+    return x.cpu().numpy().astype(np.complex128)
+
+
+def ifft_2d(u):
+    """Inverse of :func:`fft_2d` with 1/(ny nx) (spectral.py:102-104)."""
+    u = np.asarray(u, dtype=np.complex128)
+    _require(u.ndim >= 2, "ifft_2d takes an array with at least two axes")
+    x = _to_dev(u)
+    ny, nx = u.shape[-2], u.shape[-1]
+    dev.fft2_natural(x.view(-1), ny, nx, int(np.prod(u.shape[:-2])), +1, 1.0 / (ny * nx))
+    return x.cpu().numpy().astype(np.complex128)
+
+
+def dft_2d(u):
+    """2D DFT (spectral.py:77-84; the reference forms it by explicit matrices, same values)."""
+    u = np.asarray(u)
+    _require(u.ndim == 2, "dft_2d takes a 2D array")
+    return fft_2d(u)
+
+
+def idft_2d(u):
+    """Inverse of :func:`dft_2d` scaled by 1/(ny nx) (spectral.py:87-94)."""
+    u = np.asarray(u)
+    _require(u.ndim == 2, "idft_2d takes a 2D array")
+    return ifft_2d(u)
 
 
 def cfft_2d(u):

@@ -74,3 +74,13 @@ def test_nufft2_3d_vs_direct_sum(rng):
     c = rng.normal(size=modes) + 1j * rng.normal(size=modes)
     p = rng.uniform(-np.pi, np.pi, size=(57, 3))
     assert O.rel_l2(S.nufft2(c, p, 1e-6), O.nudft2(c, p)) < 1e-5
+
+
+def test_plain_2d_ffts(rng):
+    """fft_2d / ifft_2d / dft_2d / idft_2d (reference spectral.py:77-104), batched last axes."""
+    from paper_2501_05244_b200 import spectral as S
+    u = rng.normal(size=(3, 12, 10)) + 1j * rng.normal(size=(3, 12, 10))
+    assert O.rel_l2(S.fft_2d(u), np.fft.fft2(u)) < 1e-6
+    assert O.rel_l2(S.ifft_2d(u), np.fft.ifft2(u)) < 1e-6
+    assert O.rel_l2(S.dft_2d(u[0]), np.fft.fft2(u[0])) < 1e-6
+    assert O.rel_l2(S.idft_2d(u[1]), np.fft.ifft2(u[1])) < 1e-6

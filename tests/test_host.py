@@ -104,3 +104,16 @@ def test_no_cpu_fallback():
     grid = pf.CuboidGrid(pf.UniformGrid3D(4, 3, 2, 0.02, 0.02, 0.1, -0.03, -0.01, 0.85))
     with pytest.raises(RuntimeError, match="CUDA"):
         pf.rsd(_slices16(), grid)
+
+
+def test_rescale_to_torus_round_trip_and_errors():
+    """Reference core.py:550-589: box -> [-pi, pi)^d and back; validation messages."""
+    import paper_2501_05244_b200 as pf
+    p = pf.PointList(np.array([[0.0, 1.0], [0.5, 1.9], [0.999, 1.0]]))
+    t, m = pf.rescale_to_torus(p, [0.0, 1.0], [1.0, 2.0])
+    assert np.all(t.points >= -np.pi) and np.all(t.points < np.pi)
+    assert np.allclose(m.inverse(t.points), p.points, atol=1e-15)
+    with pytest.raises(pf.ValidationError, match="inside the half-open box"):
+        pf.rescale_to_torus(p, [0.0, 1.0], [0.5, 2.0])
+    with pytest.raises(pf.ValidationError, match="positive extent"):
+        pf.rescale_to_torus(p, [0.0, 1.0], [0.0, 2.0])
