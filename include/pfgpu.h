@@ -238,6 +238,16 @@ int pf_nufft_deconv(const pf_nufft_geom* g, const void* fine, int64_t fine_strid
 int pf_nufft_place(const pf_nufft_geom* g, const void* S, int64_t s_stride, const float* kz,
                    const float* ky, const float* kx, int nv, void* fine, int64_t fine_stride,
                    int transpose, void* stream);
+/* pf_nufft_interp2_acc for the points of several planes in one launch: point l reads
+ * the fine grids of plane plane_idx[l] (at fine + (plane_idx[l] - plane0) *
+ * fine_plane_stride, illumination p at + p * fine_stride) and accumulates into
+ * vol[f][dst_idx[l]] (nursd2 family readouts, reconstruct.py:453-457). */
+int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                           const double* xyz, const int32_t* plane_idx, const int64_t* dst_idx,
+                           int npts, int plane0, const void* fine, int64_t fine_plane_stride,
+                           int64_t fine_stride, int n_illum, const double* ill, double khat,
+                           int include_illum, float scale, const void* frame_w, int n_frames,
+                           void* vol, int64_t vol_frame_stride, void* stream);
 /* type-2 finish for any dimension (spectral.py:376-380): out[l] = stencil sum of the
  * fine grid (after pf_nufft_place + inverse FFT) at point l; stencil width 2w+1 <= 32. */
 int pf_nufft_interp(const pf_nufft_geom* g, const int32_t* i0, const float* d0, int npts,

@@ -351,13 +351,25 @@ class _Type2Readout:
         self.prop = Propagator(device, px, py, px, py, 0, 0, I, include_illumination, planes,
                                py * px, batch=self.nb)
         self.prop.geom.flags = 1      # register path off: generic product-only columns
-        self.points = []
-        for (start, cnt, nux, nuy, pts, z) in geo:
+        # every plane's points, cell-sorted within the plane, concatenated in plane order:
+        # one interpolation launch serves a whole plane batch
+        i0s, d0s, xyzs, pls, dsts, self.pt_lo = [], [], [], [], [], [0]
+        for k, (start, cnt, nux, nuy, pts, z) in enumerate(geo):
             tor = np.column_stack([2.0 * np.pi * nux / px, 2.0 * np.pi * nuy / py])
             npts = self.plan.points(tor, cell_sorted=True)
             xyz = np.column_stack([pts[:, 0], pts[:, 1], np.full(cnt, z)])[npts.order]
-            self.points.append((start, cnt, npts,
-                                torch.from_numpy(np.ascontiguousarray(xyz)).to(device)))
+            i0s.append(npts.i0)
+            d0s.append(npts.d0)
+            xyzs.append(xyz)
+            pls.append(np.full(cnt, k, dtype=np.int32))
+            dsts.append(start + npts.order.astype(np.int64))
+            self.pt_lo.append(self.pt_lo[-1] + cnt)
+        self.i0_all = torch.cat(i0s)
+        self.d0_all = torch.cat(d0s)
+        self.xyz_all = torch.from_numpy(np.ascontiguousarray(np.vstack(xyzs))).to(device)
+        self.plane_all = torch.from_numpy(np.concatenate(pls)).to(device)
+        self.dst_all = torch.from_numpy(np.concatenate(dsts)).to(device)
+        self.n_planes = len(geo)
         self.spec = torch.empty((self.nb * I * py * px,), dtype=torch.complex64, device=device)
         self.fine = torch.empty((self.nb * I, self.plan.fine_elems), dtype=torch.complex64,
                                 device=device)
@@ -369,8 +381,7 @@ class _Type2Readout:
         I, py, px = self.n_illum, self.py, self.px
         gref = ctypes.byref(self.prop.geom)
         base = dev.ptr(self.prop.planes_dev)
-        fine_b = self.plan.fine_elems * 8
-        nplanes = len(self.points)
+        nplanes = self.n_planes
         for fi in range(self.freqs.size):
             khat = float(self.freqs[fi]) / C
             uhat = uhat_of(fi)
@@ -383,14 +394,14 @@ class _Type2Readout:
                 _lib.call("pf_prop_columns", pp, n, gref, self.prop.plan_y.ref,
                           dev.ptr(self.prop.ws_a), dev.ptr(uhat), dev.ptr(self.spec), 1, s)
                 nu.place_and_inverse(self.plan, self.spec, n * I, py * px, self.fine, stream)
-                for k in range(b0, b0 + n):
-                    start, cnt, pts, xyz = self.points[k]
-                    _lib.call("pf_nufft_interp2_acc", self.plan.gref, dev.ptr(pts.i0),
-                              dev.ptr(pts.d0), dev.ptr(xyz), cnt,
-                              dev.ptr(self.fine) + (k - b0) * I * fine_b, self.plan.fine_elems,
-                              I, dev.ptr(self.ill), khat, int(self.include), 1.0 / (px * py), fw,
-                              self.n_frames, dev.ptr(vol), self.count, start, dev.ptr(pts.perm),
-                              s)
+                lo, hi = self.pt_lo[b0], self.pt_lo[b0 + n]
+                fe = self.plan.fine_elems
+                _lib.call("pf_nufft_interp2_batch", self.plan.gref,
+                          dev.ptr(self.i0_all) + 12 * lo, dev.ptr(self.d0_all) + 12 * lo,
+                          dev.ptr(self.xyz_all) + 24 * lo, dev.ptr(self.plane_all) + 4 * lo,
+                          dev.ptr(self.dst_all) + 8 * lo, hi - lo, b0, dev.ptr(self.fine),
+                          I * fe, fe, I, dev.ptr(self.ill), khat, int(self.include),
+                          1.0 / (px * py), fw, self.n_frames, dev.ptr(vol), self.count, s)
         return vol
 
 

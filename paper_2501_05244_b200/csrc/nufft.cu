@@ -242,6 +242,65 @@ k_interp2_warp(pf_nufft_geom G, const int* __restrict__ i0, const float* __restr
   }
 }
 
+// Batched readout: the points of several planes in one launch.  Point l belongs to
+// plane plane_idx[l] (fine grids of the launch's planes are fine + (plane - plane0) *
+// fine_plane_stride, illumination p at + p * fine_stride) and accumulates into
+// vol[frame][dst_idx[l]].  Same per-point arithmetic as k_interp2_warp.
+__global__ void __launch_bounds__(256)
+k_interp2_batch(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
+                const double* __restrict__ xyz, const int* __restrict__ plane_idx,
+                const long long* __restrict__ dst_idx, int npts, int plane0,
+                const float2* __restrict__ fine, long long fine_plane_stride,
+                long long fine_stride, int n_illum, const double* __restrict__ ill, double kturns,
+                int include_illum, float scale, const float2* __restrict__ frame_w, int n_frames,
+                float2* __restrict__ vol, long long vol_frame_stride) {
+  const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (l >= npts) return;
+  const int W = 2 * G.w + 1;
+  const int mry = G.mr[1], mrx = G.mr[2];
+  const bool on = lane < W;
+  const float dyl = d0[3 * l + 1], dxl = d0[3 * l + 2];
+  const float dx = dxl + (float)(lane - G.w) * G.h[2];
+  const float wx = on ? __expf(-dx * dx * G.inv4tau[2]) : 0.f;
+  const int cx = wrap_once(natural((long long)i0[3 * l + 2] - G.w, mrx) + (on ? lane : 0), mrx);
+  const int cy0 = natural((long long)i0[3 * l + 1] - G.w, mry);
+  const float2* fplane = fine + (long long)(plane_idx[l] - plane0) * fine_plane_stride;
+  float2 tot = make_float2(0.f, 0.f);
+  for (int p = 0; p < n_illum; p++) {
+    const float2* fp = fplane + (long long)p * fine_stride + cx;
+    float2 acc = make_float2(0.f, 0.f);
+    int cy = cy0;
+    for (int oy = 0; oy < W; oy++) {
+      const float dy = dyl + (float)(oy - G.w) * G.h[1];
+      const float w = wx * __expf(-dy * dy * G.inv4tau[1]);
+      const float2 f = __ldg(fp + (long long)cy * mrx);
+      acc.x = fmaf(w, f.x, acc.x);
+      acc.y = fmaf(w, f.y, acc.y);
+      if (++cy == mry) cy = 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    float2 val = cscale(acc, scale);
+    if (include_illum) {
+      const double ex = xyz[3 * l] - ill[3 * p], ey = xyz[3 * l + 1] - ill[3 * p + 1];
+      const double ez = xyz[3 * l + 2] - ill[3 * p + 2];
+      val = cmul(val, expi_reduced(PF_TWO_PI * kturns * sqrt(ex * ex + ey * ey + ez * ez)));
+    }
+    tot = cadd(tot, val);
+  }
+  if (lane == 0) {
+    const long long dst = dst_idx[l];
+    for (int f = 0; f < n_frames; f++) {
+      float2* d = vol + f * vol_frame_stride + dst;
+      *d = cadd(*d, cmul(tot, frame_w[f]));
+    }
+  }
+}
+
 // w = 16 (W = 33 > 32 lanes): one thread per point.
 __global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
                               const float* __restrict__ d0, const double* __restrict__ xyz,
@@ -420,5 +479,24 @@ extern "C" int pf_nufft_interp(const pf_nufft_geom* g, const int32_t* i0, const 
   k_interp_any<<<pf_cdiv(npts, 8), 256, 0, (cudaStream_t)stream>>>(
       *g, i0, d0, npts, (const float2*)fine, (float2*)out);
   PF_LAUNCH_CHECK("k_interp_any");
+  return 0;
+}
+
+extern "C" int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                                      const double* xyz, const int32_t* plane_idx,
+                                      const int64_t* dst_idx, int npts, int plane0,
+                                      const void* fine, int64_t fine_plane_stride,
+                                      int64_t fine_stride, int n_illum, const double* ill,
+                                      double khat, int include_illum, float scale,
+                                      const void* frame_w, int n_frames, void* vol,
+                                      int64_t vol_frame_stride, void* stream) {
+  PF_ARG_CHECK(g && g->dim == 2 && 2 * g->w + 1 <= 32 && npts >= 0,
+               "pf_nufft_interp2_batch: bad args (2D, stencil width <= 32)");
+  if (npts == 0) return 0;
+  k_interp2_batch<<<pf_cdiv(npts, 8), 256, 0, (cudaStream_t)stream>>>(
+      *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine,
+      fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,
+      (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride);
+  PF_LAUNCH_CHECK("k_interp2_batch");
   return 0;
 }
