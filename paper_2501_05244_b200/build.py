@@ -27,20 +27,36 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return OUT
-    nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *sources(), "-o", OUT + ".tmp"]
+def _run(cmd, verbose):
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libpfgpu.so")
+        raise RuntimeError(f"nvcc failed: {' '.join(cmd[-3:])}")
     if verbose:
         sys.stderr.write(r.stderr)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every csrc/*.cu to an object in parallel (one nvcc per file), then link."""
+    if not force and not needs_build():
+        return OUT
+    from concurrent.futures import ThreadPoolExecutor
+    nvcc = os.environ.get("NVCC", "nvcc")
+    comp = [f for f in NVCC_FLAGS if f != "-shared"]
+    if verbose:
+        comp = ["-Xptxas=-v", *comp]
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    srcs = sources()
+    objs = [os.path.join(objdir, os.path.basename(f)[:-3] + ".o") for f in srcs]
+    jobs = max(1, min(len(srcs), os.cpu_count() or 1))
+    with ThreadPoolExecutor(jobs) as ex:
+        list(ex.map(lambda so: _run([nvcc, *comp, "-c", so[0], "-o", so[1]], verbose),
+                    zip(srcs, objs)))
+    _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs,
+          "-o", OUT + ".tmp"], verbose)
     os.replace(OUT + ".tmp", OUT)
     return OUT
 
