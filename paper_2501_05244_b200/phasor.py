@@ -11,6 +11,7 @@ frequency-major complex64 tensor resident on the device for the propagators.
 from __future__ import annotations
 
 import math
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -190,7 +191,10 @@ def to_frequency(measurement, kernel) -> DeviceFrequencySlices:
     if isinstance(h, torch.Tensor):
         ht = h.to(device=device, dtype=torch.float32)
     else:
-        ht = torch.from_numpy(np.ascontiguousarray(h, dtype=np.float32)).to(device)
+        host = np.ascontiguousarray(h, dtype=np.float32)
+        with warnings.catch_warnings():   # read-only payloads are only copied from
+            warnings.simplefilter("ignore", UserWarning)
+            ht = torch.from_numpy(host).to(device)
     coeff = to_frequency_device(ht, kernel, float(measurement.t0))
     return DeviceFrequencySlices(kernel.frequencies, coeff, measurement.relay,
                                  measurement.illuminations)
