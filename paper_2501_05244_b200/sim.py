@@ -132,9 +132,9 @@ def simulate_device(scatterers: np.ndarray, albedo: np.ndarray, det_xyz: np.ndar
     """Float32 histograms [n_illum, n_detect, n_bins] on ``device``."""
     device = device or torch.device("cuda")
     det = torch.as_tensor(np.array(det_xyz, dtype=np.float64), device=device)
-    ill = torch.as_tensor(ill_xyz, dtype=torch.float64, device=device)
-    sc = torch.as_tensor(scatterers, dtype=torch.float64, device=device)
-    al = torch.as_tensor(albedo, dtype=torch.float64, device=device)
+    ill = torch.as_tensor(np.array(ill_xyz, dtype=np.float64), device=device)
+    sc = torch.as_tensor(np.array(scatterers, dtype=np.float64), device=device)
+    al = torch.as_tensor(np.array(albedo, dtype=np.float64), device=device)
     n_ill, n_det = ill.shape[0], det.shape[0]
     hist = torch.zeros((n_ill * n_det * n_bins,), dtype=torch.float32, device=device)
     det_off = torch.arange(n_det, device=device, dtype=torch.int64)[:, None] * n_bins
