@@ -19,8 +19,7 @@
 //
 // Compared with one launch per stage and plane batch, no SM idles at kernel
 // boundaries and the stages of different jobs overlap on every SM.
-#include "prop_math.cuh"
-#include "warp_fft.cuh"
+#include "prop_stages.cuh"
 
 namespace {
 
@@ -72,222 +71,6 @@ __device__ bool wait_geq(const int* p, int target, int* abort_flag) {
     if (it > (1 << 24)) {
       atomicExch(abort_flag, 1);
       return false;
-    }
-  }
-}
-
-// ---- stage bodies (one CTA, tile = task index within the stage) ----------------
-
-template <int L>
-__device__ __forceinline__ void st_a(float2* sm, const pf_plane& pl, double kturns,
-                                     const float2* __restrict__ tw, float2* __restrict__ wa,
-                                     int tile) {
-  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
-  constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % L, line = lane / L;
-  const int r = warp * LPW + line;
-  const int jy0 = tile * RPC;
-  const int jy = jy0 + r;
-  const double ly = (double)jy * pl.lag_dy;
-  const double base = fma(ly, ly, pl.dz * pl.dz);
-  float2 v[32];
-#pragma unroll
-  for (int m = 0; m <= 16; m++) {
-    const double lx = (double)centred(t + L * m, P) * pl.lag_dx;
-    v[m] = g_kernel(fma(lx, lx, base), kturns, (float)kturns);
-  }
-  const int mirror = (lane - t) + ((L - t) & (L - 1));
-#pragma unroll
-  for (int m = 17; m < 32; m++) {
-    const float2 o = make_float2(__shfl_sync(0xffffffffu, v[31 - m].x, mirror),
-                                 __shfl_sync(0xffffffffu, v[31 - m].y, mirror));
-    v[m] = (t == 0) ? v[32 - m] : o;
-  }
-  wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
-  __syncthreads();
-  if (jy <= H) {
-#pragma unroll
-    for (int m = 0; m < 32; m++) {
-      const int kx = t + L * m;
-      if (kx <= H) sm[kx * SLD + r] = v[m];
-    }
-  }
-  __syncthreads();
-  const int nr = min(RPC, NA - jy0);
-  constexpr int KSTEP = MT / RPC;
-  const int rr = threadIdx.x % RPC, k0 = threadIdx.x / RPC;
-  if (rr < nr) {
-    float2* d = wa + (long long)k0 * NA + jy0 + rr;
-    const float2* q = sm + k0 * SLD + rr;
-#pragma unroll 4
-    for (int kx = k0; kx < NA; kx += KSTEP) {
-      *d = *q;
-      d += (long long)KSTEP * NA;
-      q += KSTEP * SLD;
-    }
-  }
-}
-
-template <int L>
-__device__ __forceinline__ void st_b1(float2* sm, const float2* __restrict__ tw,
-                                      float2* __restrict__ wa, int tile) {
-  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
-  constexpr int LPW = 32 / L;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % L, line = lane / L;
-  const int row = (tile * 8 + warp) * LPW + line;
-  const bool active = row < NA;
-  float2* arow = wa + (long long)(active ? row : 0) * NA;
-  float2 v[32];
-#pragma unroll
-  for (int m = 0; m < 32; m++) {
-    const int jy = t + L * m;
-    v[m] = arow[jy <= H ? jy : P - jy];
-  }
-  wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
-  if (active) {
-#pragma unroll
-    for (int m = 0; m <= 16; m++) {
-      const int ky = t + L * m;
-      if (ky <= H) arow[ky] = v[m];
-    }
-  }
-}
-
-template <int L, bool MULTI>
-__device__ __forceinline__ void st_b2(float2* sm, const pf_plane& pl, const pf_prop_geom& g,
-                                      const float2* __restrict__ tw, const float2* __restrict__ wa,
-                                      const float2* __restrict__ uhat_f, float2* __restrict__ wb,
-                                      int tile) {
-  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
-  constexpr int LPW = 32 / L, NL = 8 * LPW;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % L, line = lane / L;
-  const int li = warp * LPW + line;
-  const int kx_raw = tile * (NL / 2) + (li >> 1), side = li & 1;
-  const int kx = min(kx_raw, H);
-  const int col = side == 0 ? kx : (P - kx) % P;
-  const bool active = kx_raw < NA && !(side == 1 && col == kx);
-  const float2* grow = wa + (long long)kx * NA;
-  const int ny = g.ny;
-  const int n_ill = MULTI ? g.n_illum : 1;
-#pragma unroll 1
-  for (int p = 0; p < n_ill; p++) {
-    const float2* ucol = uhat_f + pl.uhat_off + (long long)p * g.uhat_illum_stride +
-                         (long long)col * P;
-    float2 w[32];
-#pragma unroll
-    for (int m = 0; m < 32; m++) {
-      const int ky = t + L * m;
-      w[m] = cmul(grow[ky <= H ? ky : P - ky], __ldg(ucol + ky));
-    }
-    wfft<L, 1>(w, sm + warp * WFFT_XCH, tw);
-    if (active) {
-      float2* dcol = wb + (long long)p * P * ny + (long long)col * ny;
-#pragma unroll
-      for (int m = 0; m < 32; m++) {
-        const int i = (t + L * m - g.nu0y) & (P - 1);
-        if (i < ny) dcol[i] = w[m];
-      }
-    }
-  }
-}
-
-template <int L, bool MULTI, bool PRE>
-__device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double kturns,
-                                     const pf_prop_geom& g, const float2* __restrict__ tw,
-                                     const float2* __restrict__ wb, const double* __restrict__ ill,
-                                     const float2* __restrict__ frame_w, int n_frames,
-                                     float2* __restrict__ vol, long long vfs, int tile) {
-  constexpr int P = 32 * L;
-  constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
-  constexpr int UNION = (8 * WFFT_XCH > P * SLD) ? 8 * WFFT_XCH : P * SLD;
-  float2* volbuf = sm + UNION;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % L, line = lane / L;
-  const int r = warp * LPW + line;
-  const int ny = g.ny, nx = g.nx;
-  const int i0 = tile * RPC;
-  const int i = i0 + r;
-  const int nr = min(RPC, ny - i0);
-  const float scale = 1.0f / ((float)P * (float)P);
-  const long long vol_row0 = (pl.vol_plane * ny + i0) * (long long)nx;
-  if (PRE) {
-    for (int rr = 0; rr < nr; rr++) {
-      const float2* src = vol + vol_row0 + (long long)rr * nx;
-#pragma unroll 4
-      for (int mo = threadIdx.x; mo < nx; mo += MT) cp_async8(volbuf + rr * nx + mo, src + mo);
-    }
-    cp_async_commit();
-  }
-  float2 acc[MULTI ? 32 : 1];
-  float2 v[32];
-  const double yv = pl.y0 + pl.dy * i;
-  const int n_ill = MULTI ? g.n_illum : 1;
-#pragma unroll 1
-  for (int p = 0; p < n_ill; p++) {
-    const float2* src = wb + (long long)p * P * ny + i0;
-    if (p > 0) __syncthreads();
-    {
-      constexpr int CSTEP = MT / RPC;
-      const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
-      if (rr < nr) {
-        const float2* q = src + (long long)c0 * ny + rr;
-        float2* d = sm + c0 * SLD + rr;
-#pragma unroll 8
-        for (int col = c0; col < P; col += CSTEP) {
-          cp_async8(d, q);
-          q += (long long)CSTEP * ny;
-          d += CSTEP * SLD;
-        }
-      }
-    }
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-#pragma unroll
-    for (int m = 0; m < 32; m++) v[m] = sm[(t + L * m) * SLD + r];
-    __syncthreads();
-    wfft<L, 1>(v, sm + warp * WFFT_XCH, tw);
-    const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
-    const double dy = yv - sy, dz = pl.z - sz;
-    const double byz = fma(dy, dy, dz * dz);
-#pragma unroll
-    for (int m = 0; m < 32; m++) {
-      const int mo = (t + L * m - g.nu0x) & (P - 1);
-      float2 val = cscale(v[m], scale);
-      if (g.include_illum && mo < nx) {
-        const double dx = pl.x0 + pl.dx * mo - sx;
-        val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
-      }
-      if (MULTI) {
-        if (p == 0) acc[m] = val; else acc[m] = cadd(acc[m], val);
-      } else {
-        v[m] = val;
-      }
-    }
-  }
-  if (i < ny) {
-    const long long off = vol_row0 + (long long)r * nx;
-    if (PRE) {
-      const float2* old = volbuf + r * nx;
-      const float2 fw = frame_w[0];
-#pragma unroll
-      for (int m = 0; m < 32; m++) {
-        const int mo = (t + L * m - g.nu0x) & (P - 1);
-        if (mo < nx) vol[off + mo] = cadd(old[mo], cmul(MULTI ? acc[m] : v[m], fw));
-      }
-    } else {
-      for (int fr = 0; fr < n_frames; fr++) {
-        const float2 fw = frame_w[fr];
-        float2* drow = vol + fr * vfs + off;
-#pragma unroll
-        for (int m = 0; m < 32; m++) {
-          const int mo = (t + L * m - g.nu0x) & (P - 1);
-          if (mo < nx) drow[mo] = cadd(drow[mo], cmul(MULTI ? acc[m] : v[m], fw));
-        }
-      }
     }
   }
 }

@@ -17,8 +17,7 @@
 // pf_prop_fast() before building it.
 #include <stdlib.h>
 
-#include "prop_math.cuh"
-#include "warp_fft.cuh"
+#include "prop_stages.cuh"
 
 namespace {
 
@@ -32,171 +31,31 @@ struct FBatch {
   int nf;
 };
 
-template <int L, int NW = 8>
-__global__ void __launch_bounds__(NW * 32, 16 / NW)
+// A for every plane of a batch (blockIdx.y) and, batched, every frequency (blockIdx.z).
+template <int L>
+__global__ void __launch_bounds__(FT, 2)
 k_pa(const pf_plane* __restrict__ planes, double kturns_s, pf_prop_geom g,
      const float2* __restrict__ tw, float2* __restrict__ ws_a, FBatch fb) {
-  const double kturns = fb.kturns ? fb.kturns[blockIdx.z] : kturns_s;
-  ws_a += blockIdx.z * fb.ws_a_fs;
-  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
-  constexpr int LPW = 32 / L, RPC = NW * LPW, SLD = RPC + 1;
-  constexpr int NT = NW * 32;
   extern __shared__ float2 sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % L, line = lane / L;
-  const int r = warp * LPW + line;
-  const int jy0 = blockIdx.x * RPC;
-  const int jy = jy0 + r;
-  const pf_plane pl = planes[blockIdx.y];
-  const double ly = (double)jy * pl.lag_dy;
-  const double base = fma(ly, ly, pl.dz * pl.dz);
-  // G is even in x: slots jx and P-jx hold the same value.  Synthesise
-  // m = 0..16 (jx <= P/2 + t) and fetch m = 17..31 from the mirror lane
-  // (L - t, element 31 - m), or from this lane's element 32 - m when t = 0.
-  float2 v[32];
-#pragma unroll
-  for (int m = 0; m <= 16; m++) {
-    const double lx = (double)centred(t + L * m, P) * pl.lag_dx;
-    v[m] = g_kernel(fma(lx, lx, base), kturns, (float)kturns);
-  }
-  const int mirror = (lane - t) + ((L - t) & (L - 1));
-#pragma unroll
-  for (int m = 17; m < 32; m++) {
-    const float2 o = make_float2(__shfl_sync(0xffffffffu, v[31 - m].x, mirror),
-                                 __shfl_sync(0xffffffffu, v[31 - m].y, mirror));
-    v[m] = (t == 0) ? v[32 - m] : o;
-  }
-  wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
-  __syncthreads();
-  if (jy <= H) {
-#pragma unroll
-    for (int m = 0; m < 32; m++) {
-      const int kx = t + L * m;
-      if (kx <= H) sm[kx * SLD + r] = v[m];
-    }
-  }
-  __syncthreads();
-  const int nr = min(RPC, NA - jy0);
-  float2* dst = ws_a + (long long)blockIdx.y * NA * NA + jy0;
-  {
-    // thread -> (kx row within a group of NT/RPC rows, rr); stride NT/RPC rows per step
-    constexpr int KSTEP = NT / RPC;
-    const int rr = threadIdx.x % RPC, k0 = threadIdx.x / RPC;
-    if (rr < nr) {
-      float2* d = dst + (long long)k0 * NA + rr;
-      const float2* q = sm + k0 * SLD + rr;
-#pragma unroll 4
-      for (int kx = k0; kx < NA; kx += KSTEP) {
-        *d = *q;
-        d += (long long)KSTEP * NA;
-        q += KSTEP * SLD;
-      }
-    }
-  }
+  constexpr int NA = 32 * L / 2 + 1;
+  const double kturns = fb.kturns ? fb.kturns[blockIdx.z] : kturns_s;
+  st_a<L>(sm, planes[blockIdx.y], kturns, tw,
+          ws_a + blockIdx.z * fb.ws_a_fs + (long long)blockIdx.y * NA * NA, blockIdx.x);
 }
 
-// MULTI: more than one illumination (contributions summed in registers first).
-// PRE: single frame and the CTA's volume rows fit next to the tile: they are
-// prefetched with cp.async at entry so the accumulate is load-free at the end.
-template <int L, bool MULTI, bool PRE, int NW = 8>
-__global__ void __launch_bounds__(NW * 32, MULTI ? 8 / NW : 16 / NW)
+// C for every plane of a batch (blockIdx.y).  MULTI: more than one illumination
+// (summed in registers first).  PRE: single frame, the CTA's volume rows prefetched
+// with cp.async at entry so the accumulate is load-free at the end.
+template <int L, bool MULTI, bool PRE>
+__global__ void __launch_bounds__(FT, MULTI ? 1 : 2)
 k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
      const float2* __restrict__ tw, const float2* __restrict__ ws_b,
      const double* __restrict__ ill, const float2* __restrict__ frame_w, int n_frames,
      float2* __restrict__ vol, long long vol_frame_stride) {
-  constexpr int P = 32 * L;
-  constexpr int LPW = 32 / L, RPC = NW * LPW, SLD = RPC + 1;
-  constexpr int NT = NW * 32;
-  constexpr int UNION = (NW * WFFT_XCH > P * SLD) ? NW * WFFT_XCH : P * SLD;
   extern __shared__ float2 sm[];
-  float2* volbuf = sm + UNION;   // [RPC][nx] when PRE
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % L, line = lane / L;
-  const int r = warp * LPW + line;
-  const int ny = g.ny, nx = g.nx;
-  const int i0 = blockIdx.x * RPC;
-  const int i = i0 + r;
-  const int nr = min(RPC, ny - i0);
-  const pf_plane pl = planes[blockIdx.y];
-  const float scale = 1.0f / ((float)P * (float)P);
-  const long long vol_row0 = (pl.vol_plane * ny + i0) * (long long)nx;
-  if (PRE) {
-    for (int rr = 0; rr < nr; rr++) {
-      const float2* src = vol + vol_row0 + (long long)rr * nx;
-#pragma unroll 4
-      for (int mo = threadIdx.x; mo < nx; mo += NT) cp_async8(volbuf + rr * nx + mo, src + mo);
-    }
-    cp_async_commit();
-  }
-  float2 acc[MULTI ? 32 : 1];
-  float2 v[32];
-  const double yv = pl.y0 + pl.dy * i;
-  const int n_ill = MULTI ? g.n_illum : 1;
-#pragma unroll 1
-  for (int p = 0; p < n_ill; p++) {
-    const float2* src = ws_b + ((long long)blockIdx.y * g.n_illum + p) * (long long)P * ny + i0;
-    if (p > 0) __syncthreads();
-    {
-      constexpr int CSTEP = NT / RPC;
-      const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
-      if (rr < nr) {
-        const float2* q = src + (long long)c0 * ny + rr;
-        float2* d = sm + c0 * SLD + rr;
-#pragma unroll 8
-        for (int col = c0; col < P; col += CSTEP) {
-          cp_async8(d, q);
-          q += (long long)CSTEP * ny;
-          d += CSTEP * SLD;
-        }
-      }
-    }
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-#pragma unroll
-    for (int m = 0; m < 32; m++) v[m] = sm[(t + L * m) * SLD + r];
-    __syncthreads();
-    wfft<L, 1>(v, sm + warp * WFFT_XCH, tw);
-    const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
-    const double dy = yv - sy, dz = pl.z - sz;
-    const double byz = fma(dy, dy, dz * dz);
-#pragma unroll
-    for (int m = 0; m < 32; m++) {
-      const int mo = (t + L * m - g.nu0x) & (P - 1);
-      float2 val = cscale(v[m], scale);
-      if (g.include_illum && mo < nx) {   // cropped-away columns need no phase
-        const double dx = pl.x0 + pl.dx * mo - sx;
-        val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
-      }
-      if (MULTI) {
-        if (p == 0) acc[m] = val; else acc[m] = cadd(acc[m], val);
-      } else {
-        v[m] = val;
-      }
-    }
-  }
-  if (i < ny) {
-    const long long off = vol_row0 + (long long)r * nx;
-    if (PRE) {
-      const float2* old = volbuf + r * nx;
-      const float2 fw = frame_w[0];
-#pragma unroll
-      for (int m = 0; m < 32; m++) {
-        const int mo = (t + L * m - g.nu0x) & (P - 1);
-        if (mo < nx) vol[off + mo] = cadd(old[mo], cmul(MULTI ? acc[m] : v[m], fw));
-      }
-    } else {
-      for (int fr = 0; fr < n_frames; fr++) {
-        const float2 fw = frame_w[fr];
-        float2* drow = vol + fr * vol_frame_stride + off;
-#pragma unroll
-        for (int m = 0; m < 32; m++) {
-          const int mo = (t + L * m - g.nu0x) & (P - 1);
-          if (mo < nx) drow[mo] = cadd(drow[mo], cmul(MULTI ? acc[m] : v[m], fw));
-        }
-      }
-    }
-  }
+  const long long wb_plane = (long long)g.n_illum * 32 * L * g.ny;
+  st_c<L, MULTI, PRE>(sm, planes[blockIdx.y], kturns, g, tw, ws_b + blockIdx.y * wb_plane, ill,
+                      frame_w, n_frames, vol, vol_frame_stride, blockIdx.x);
 }
 
 // ---- B split in two register-light kernels (128 registers, 16 warps/SM):
@@ -206,30 +65,9 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
 template <int L>
 __global__ void __launch_bounds__(FT, 2)
 k_pb1(int nplanes, const float2* __restrict__ tw, float2* __restrict__ ws_a, FBatch fb) {
-  ws_a += blockIdx.z * fb.ws_a_fs;
-  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
-  constexpr int LPW = 32 / L;
   extern __shared__ float2 sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % L, line = lane / L;
-  const int row = (blockIdx.x * 8 + warp) * LPW + line;     // kx
-  const int b = blockIdx.y;
-  const bool active = row < NA;
-  float2* arow = ws_a + ((long long)b * NA + (active ? row : 0)) * NA;
-  float2 v[32];
-#pragma unroll
-  for (int m = 0; m < 32; m++) {
-    const int jy = t + L * m;
-    v[m] = arow[jy <= H ? jy : P - jy];
-  }
-  wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
-  if (active) {
-#pragma unroll
-    for (int m = 0; m <= 16; m++) {   // ky = t + L m <= P/2 for m < 16 (and m = 16, t = 0)
-      const int ky = t + L * m;
-      if (ky <= H) arow[ky] = v[m];
-    }
-  }
+  constexpr int NA = 32 * L / 2 + 1;
+  st_b1<L>(sm, tw, ws_a + blockIdx.z * fb.ws_a_fs + (long long)blockIdx.y * NA * NA, blockIdx.x);
 }
 
 template <int L, bool MULTI>
