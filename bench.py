@@ -174,6 +174,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    fp32_meas = _fp32_peak(device)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -257,7 +258,8 @@ def run_ours(args):
         s3_flops += units * (cfg.relay.grid.ny + P) * 2 * 5.0 * Q * math.log2(Q)
     if cfg.algorithm == "nursd1":   # + per-(f, p) type-1 NUFFT: fine-grid FFT + 17x17 spread
         s3_flops += F * I * (5.0 * (2 * P) ** 2 * math.log2((2 * P) ** 2) + cfg.relay.count * 17 * 17 * 8)
-    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    fp32_nominal = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    fp32_peak = fp32_meas if fp32_meas > 0 else fp32_nominal
     clocks = clk.summary()
     roof_k1 = {"bound": "hbm", "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "peak": hbm_peak,
                "unit": "GB/s", "traffic": _traffic("k_temporal_dft"), "kernel": "k_temporal_dft (K1)",
@@ -266,9 +268,15 @@ def run_ours(args):
     roof_s3 = {"bound": "fp32", "achieved": s3_flops / (s3_ms * 1e-3) / 1e12, "peak": fp32_peak,
                "unit": "TFLOP/s", "traffic": _prop_traffic(F, k_hi - k_lo),
                "kernel": "propagation k_pa+k_pb1+k_pb2+k_pc (pf_prop_kernel_rows/columns/rows_out, S3)",
-               "ms": s3_ms, "peak_source": "nominal 148 SM x 128 FP32 lanes x 2 x sm_max_mhz "
-                                           "(MEASURED_PEAKS.json has no FP32 entry)",
-               "flops_model": "(2*F*Nz*I + F*I) * 5 P^2 log2(P^2), P=%d" % P}
+               "ms": s3_ms, "peak_source": "measured on this GPU before the timed region: FFMA probe "
+                                           "(pf_fp32_probe, best of 6); nominal %.1f TFLOP/s = "
+                                           "148 SM x 128 lanes x 2 x sm_max_mhz; MEASURED_PEAKS.json "
+                                           "has no FP32 entry" % fp32_nominal,
+               "flops_model": "(2*F*Nz*I + F*I) * 5 P^2 log2(P^2), P=%d" % P,
+               "traffic_note": "DRAM bytes of one plane batch of A+B1+B2+C from an ncu --set "
+                               "full capture (profiles/ncu_traffic.json) scaled to F x Nz; ncu "
+                               "flushes L2 before each kernel, so this counts the L2-resident "
+                               "stage intermediates as DRAM reads: an upper bound"}
     roof_s3["frac"] = roof_s3["achieved"] / fp32_peak
     dominant, other = (roof_s3, roof_k1) if s3_ms >= k1_ms else (roof_k1, roof_s3)
     line = {
@@ -333,6 +341,27 @@ def _traffic(kernel_prefix):
 # ---------------------------------------------------------------------------
 # CPU baselines (oracle port of the reference; test infrastructure)
 # ---------------------------------------------------------------------------
+
+
+def _fp32_peak(device) -> float:
+    """FP32 FFMA throughput measured on this GPU (TFLOP/s; best of 5), the roofline
+    denominator SURVEY 8(d) asks for (MEASURED_PEAKS.json has no FP32 entry)."""
+    import torch
+    from paper_2501_05244_b200 import _device as dev
+    from paper_2501_05244_b200 import _lib
+    nsm = torch.cuda.get_device_properties(device).multi_processor_count
+    blocks, iters = nsm * 8, 2048
+    out = torch.empty(blocks * 256, dtype=torch.float32, device=device)
+    best = 0.0
+    for _ in range(6):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        _lib.call("pf_fp32_probe", dev.ptr(out), blocks, iters, dev.stream_ptr())
+        e.record()
+        torch.cuda.synchronize()
+        flops = 2.0 * 8 * 16 * iters * blocks * 256
+        best = max(best, flops / (s.elapsed_time(e) * 1e-3) / 1e12)
+    return best
 
 
 def _h2d_probe(hist_host, device) -> float:

@@ -184,6 +184,10 @@ int pf_scatter_csr(const int32_t* cell_start, const int64_t* cells, const int32_
                    const float* ent_w, int n_cells, const void* vals, int64_t val_stride, int nv,
                    void* out, int64_t out_stride, void* stream);
 
+/* Measurement helper (bench.py): FP32 FFMA throughput probe, blocks x 256 threads,
+ * 8 chains x 16 unrolled FMAs x iters each; flops = 256 * blocks * iters * 256. */
+int pf_fp32_probe(void* out, int blocks, int iters, void* stream);
+
 /* ---------------------------------------------------------------- SFFT (Bluestein)
  * Scaled-DFT lines, replacing SfftPlan.apply (spectral.py:160-168) inside
  * sfft_2d_centered (:209-218): per plane b (grid y) the tables chirp[b][M] and

@@ -63,6 +63,7 @@ _SIGNATURES = {
     "pf_prop_fbatch": [_vp, _i, _vp, _i, _P(PfPropGeom), _P(PfFftPlan), _vp, _i64, _vp, _i64, _vp,
                        _i64, _vp, _vp, _vp, _vp],
     "pf_count_nonfinite": [_vp, _i64, _vp, _vp],
+    "pf_fp32_probe": [_vp, _i, _i, _vp],
     "pf_nufft_interp": [_P(PfNufftGeom), _vp, _vp, _i, _vp, _vp, _vp],
     "pf_nufft_interp2_batch": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _i64, _i64,
                                _i, _vp, _d, _i, _f, _vp, _i, _vp, _i64, _vp],

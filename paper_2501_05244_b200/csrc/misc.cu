@@ -198,3 +198,26 @@ extern "C" int pf_scatter_csr(const int32_t* cell_start, const int64_t* cells,
   PF_LAUNCH_CHECK("k_scatter_csr");
   return 0;
 }
+
+// ---- FP32 peak probe (bench.py roofline denominator; "FP32 peak measured on
+// the box"): 8 independent FFMA chains per thread, `iters` rounds, result stored so the
+// chains are live.  Flops = 2 * 8 * iters * threads.
+__global__ void __launch_bounds__(256) k_fp32_probe(float* out, int iters, float a, float b) {
+  float c0 = threadIdx.x, c1 = c0 + 1.f, c2 = c0 + 2.f, c3 = c0 + 3.f;
+  float c4 = c0 + 4.f, c5 = c0 + 5.f, c6 = c0 + 6.f, c7 = c0 + 7.f;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      c0 = fmaf(c0, a, b); c1 = fmaf(c1, a, b); c2 = fmaf(c2, a, b); c3 = fmaf(c3, a, b);
+      c4 = fmaf(c4, a, b); c5 = fmaf(c5, a, b); c6 = fmaf(c6, a, b); c7 = fmaf(c7, a, b);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7;
+}
+
+extern "C" int pf_fp32_probe(void* out, int blocks, int iters, void* stream) {
+  PF_ARG_CHECK(out && blocks > 0 && iters > 0, "pf_fp32_probe: bad args");
+  k_fp32_probe<<<blocks, 256, 0, (cudaStream_t)stream>>>((float*)out, iters, 0.9999f, 1e-4f);
+  PF_LAUNCH_CHECK("k_fp32_probe");
+  return 0;
+}
