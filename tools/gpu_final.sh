@@ -19,6 +19,9 @@ PF_NF=2 python tools/prof_rsd.py > $O/prof_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv \
       --log-file $O/launches_c4.csv python tools/prof_rsd.py > /dev/null 2>&1
 PF_NF=2 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_temporal_dft|k_pa|k_pb1|k_pb2|k_pc" -s 6 -c 5 -o $O/prof_full \
+    -k regex:"k_pa|k_pb1|k_pb2|k_pc" -s 4 -c 4 -o $O/prof_full \
     python tools/prof_rsd.py > $O/ncu_full.log 2>&1
-tail -2 $O/ncu_full.log
+PF_NF=2 ncu --set full --clock-control none --import-source on \
+    -k regex:"k_temporal_dft" -s 1 -c 1 -o $O/prof_k1 \
+    python tools/prof_rsd.py > $O/ncu_k1.log 2>&1
+tail -2 $O/ncu_full.log $O/ncu_k1.log
