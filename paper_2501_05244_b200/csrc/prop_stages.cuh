@@ -213,13 +213,19 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
         if (mo < nx) vol[off + mo] = cadd(old[mo], cmul(MULTI ? acc[m] : v[m], fw));
       }
     } else {
-      for (int fr = 0; fr < n_frames; fr++) {
-        const float2 fw = frame_w[fr];
-        float2* drow = vol + fr * vfs + off;
+      // frames innermost: each element's offset is formed once and reused for every
+      // frame (hoisting 32 offsets out of a frame loop spilled)
 #pragma unroll
-        for (int m = 0; m < 32; m++) {
-          const int mo = (t + L * m - g.nu0x) & (P - 1);
-          if (mo < nx) drow[mo] = cadd(drow[mo], cmul(MULTI ? acc[m] : v[m], fw));
+      for (int m = 0; m < 32; m++) {
+        const int mo = (t + L * m - g.nu0x) & (P - 1);
+        if (mo < nx) {
+          const float2 val = MULTI ? acc[m] : v[m];
+          float2* d = vol + off + mo;
+#pragma unroll 1
+          for (int fr = 0; fr < n_frames; fr++) {
+            float2* q = d + fr * vfs;
+            *q = cadd(*q, cmul(val, __ldg(frame_w + fr)));
+          }
         }
       }
     }
