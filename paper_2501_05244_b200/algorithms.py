@@ -20,7 +20,7 @@ from . import _device as dev
 from . import _lib
 from . import nufft as nu
 from ._fastlen import next_fast_len
-from .core import (SPEED_OF_LIGHT, ReconstructionVolume, _require, illumination_coordinates)
+from .core import SPEED_OF_LIGHT, _require
 from .phasor import device_coefficients
 from .reconstruct import (GraphedRun, PlaneSpec, Propagator, _check_depths, _check_times, _close,
                           _exact_pad, _frame_weights, _ill_tensor, _kind, _nonplanar_relay,
