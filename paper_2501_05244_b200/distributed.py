@@ -25,6 +25,24 @@ def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < rem else 0)
 
 
+def chunk_split(n: int, n_chunks: int, unit: int = 1) -> list[tuple[int, int]]:
+    """Cut [0, n) into n_chunks contiguous pieces whose boundaries fall on multiples of
+    ``unit`` (the propagation's lanes x planes-per-batch, so a chunk keeps every stream
+    lane busy); n_chunks must not exceed ceil(n / unit)."""
+    units = -(-n // unit)
+    base, extra = divmod(units, n_chunks)
+    out, u = [], 0
+    for j in range(n_chunks):
+        nu = base + (1 if j < extra else 0)
+        out.append((min(n, u * unit), min(n, (u + nu) * unit)))
+        u += nu
+    return out
+
+
+def max_chunks(n: int, want: int, unit: int = 1) -> int:
+    return max(1, min(int(want), -(-n // unit))) if n else 1
+
+
 def _real(t: torch.Tensor) -> torch.Tensor:
     return torch.view_as_real(t) if t.is_complex() else t
 
@@ -97,23 +115,16 @@ class VolumeGather:
             self.full[:, lo * self.pv:hi * self.pv].copy_(self.recv[r][:, :n])
         return self.full
 
-    def part_ranges(self, j: int, n_chunks: int):
-        """Per rank: local plane range of chunk j when each shard is cut into n_chunks
-        contiguous pieces (the split ``GraphedRun.chunk_bounds`` uses)."""
-        out = []
-        for lo, hi in self.ranges:
-            n = hi - lo
-            k = max(1, min(n_chunks, n)) if n else 1
-            a = j * (n // k) + min(j, n % k) if j < k else n
-            b = a + (n // k + (1 if j < n % k else 0)) if j < k else n
-            out.append((a, b))
-        return out
+    def part_ranges(self, j: int, n_chunks: int, unit: int = 1):
+        """Per rank: local plane range of chunk j when each shard is cut by
+        ``chunk_split(shard, n_chunks, unit)`` (the split ``GraphedRun.chunk_bounds`` uses)."""
+        return [chunk_split(hi - lo, n_chunks, unit)[j] for lo, hi in self.ranges]
 
-    def gather_part(self, local: torch.Tensor, j: int, n_chunks: int):
+    def gather_part(self, local: torch.Tensor, j: int, n_chunks: int, unit: int = 1):
         """Gather chunk j of every rank's shard into ``full`` on rank 0 (call on the stream
         that must order it: after chunk j's planes are final on this rank)."""
-        parts = self.part_ranges(j, n_chunks)
-        maxp = max(b - a for a, b in parts) * self.pv
+        parts = self.part_ranges(j, n_chunks, unit)
+        maxp = max(1, max(b - a for a, b in parts)) * self.pv
         a, b = parts[self.rank]
         send = self.send[:, :maxp]
         send[:, :(b - a) * self.pv].copy_(local.view(self.nf, -1)[:, a * self.pv:b * self.pv])

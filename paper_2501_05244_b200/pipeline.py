@@ -81,10 +81,12 @@ class TransientReconstructor:
         # multi-GPU: planes in chunks, each gathered while the next computes
         nloc = getattr(self.engine, "n_planes_local", 0)
         want = int(os.environ.get("PF_GATHER_CHUNKS", "4"))
-        self.gather_chunks = 1
+        self.gather_chunks, self.chunk_unit = 1, 1
         if volume_gather is not None and hasattr(self.engine, "run_chunk") and want > 1:
-            shards = [hi - lo for lo, hi in volume_gather.ranges]
-            self.gather_chunks = max(1, min(want, min(shards)))
+            from .distributed import max_chunks
+            self.chunk_unit = self.engine.chunk_unit
+            self.gather_chunks = min(max_chunks(hi - lo, want, self.chunk_unit)
+                                     for lo, hi in volume_gather.ranges)
         self.gather_stream = torch.cuda.Stream(device=self.device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self._hist_dev = None
@@ -120,7 +122,8 @@ class TransientReconstructor:
             done.record(main)
             gs.wait_event(done)
             with torch.cuda.stream(gs):
-                res = self.volume_gather.gather_part(vol, j, self.gather_chunks)
+                res = self.volume_gather.gather_part(vol, j, self.gather_chunks,
+                                                     self.chunk_unit)
         main.wait_stream(gs)
         return res
 

@@ -353,16 +353,15 @@ class GraphedRun:
             g.replay()
         return vol
 
+    @property
+    def chunk_unit(self) -> int:
+        """Plane granularity of chunks: one round of plane batches over all stream lanes."""
+        return self.prop.batch * len(self.prop.lane_streams)
+
     def chunk_bounds(self, n_chunks: int) -> list:
-        """Contiguous local plane ranges of ``run_chunk`` (at most n_chunks, none empty)."""
-        n = self.n_planes_local
-        n_chunks = max(1, min(int(n_chunks), n))
-        out, lo = [], 0
-        for j in range(n_chunks):
-            hi = lo + n // n_chunks + (1 if j < n % n_chunks else 0)
-            out.append((lo, hi))
-            lo = hi
-        return out
+        """Contiguous local plane ranges of ``run_chunk`` (distributed.chunk_split)."""
+        from .distributed import chunk_split
+        return chunk_split(self.n_planes_local, n_chunks, self.chunk_unit)
 
     def run_graphed_chunk(self, coeff: torch.Tensor, vol: torch.Tensor, j: int, n_chunks: int,
                           stream=None):

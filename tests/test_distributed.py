@@ -164,8 +164,8 @@ def _part_worker(rank, world, port, out_q):
     full_once = vg(local)
     full_once = None if full_once is None else full_once.clone()
     vg2 = VolumeGather(nz, pv, nf, world, rank, torch.device("cpu"))
-    for j in range(4):
-        res = vg2.gather_part(local, j, 4)
+    for j in range(2):                       # 2 chunks on 2-plane units (uneven shards 4/4/3)
+        res = vg2.gather_part(local, j, 2, 2)
     if rank == 0:
         out_q.put((full_once.numpy(), res.numpy()))
     dist.barrier()
@@ -186,3 +186,15 @@ def test_chunked_volume_gather_equals_single_gather():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert np.array_equal(once, parts)
+
+
+def test_chunk_split_units():
+    from paper_2501_05244_b200.distributed import chunk_split, max_chunks
+    for n, c, u in [(32, 4, 12), (64, 4, 12), (128, 4, 12), (11, 2, 2), (7, 3, 1), (5, 1, 12)]:
+        c = min(c, max_chunks(n, c, u))
+        parts = chunk_split(n, c, u)
+        assert parts[0][0] == 0 and parts[-1][1] == n and len(parts) == c
+        assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+        assert all(b > a for a, b in parts)
+        assert all(b % u == 0 for _, b in parts[:-1])
+    assert chunk_split(32, 3, 12) == [(0, 12), (12, 24), (24, 32)]
