@@ -290,6 +290,63 @@ def gen_containers():
     C.write_volume(C.ReconstructionVolume(cub, fv, times), os.path.join(d, "volume_video.nls1"))
 
 
+def gen_acceptance():
+    """The reference acceptance suite's 20 oracle-consistency scenes (test_acceptance.py:
+    204-266, seeds 6000+i): every algorithm path, one or two illuminations, one or two
+    scatterers.  Stores the slices, grid, the reference reconstruction and the reference
+    oracle.backproject field (the suite's NCC floor: 0.95, 0.9 for the 3D relays)."""
+    from phasorfield import sim as S
+    names = list(pf.ALGORITHM_NAMES)
+    out = {}
+    for i in range(20):
+        rng = np.random.default_rng(6000 + i)
+        algo = names[i % len(names)]
+        lambda_c = (0.04, 0.05, 0.06)[i % 3]
+        z_mid = float(rng.uniform(1.0, 1.2))
+        scat = [S.Scatterer((float(rng.uniform(-0.06, 0.06)), float(rng.uniform(-0.06, 0.06)),
+                             z_mid + float(rng.uniform(-0.05, 0.05))), float(rng.uniform(0.6, 1.0)))
+                for _ in range(1 + i % 2)]
+        scene = S.Scene(tuple(scat))
+        side, pitch = 16, 0.02
+        g2 = pf.UniformGrid2D(side, side, pitch, pitch, -(side - 1) * pitch / 2,
+                              -(side - 1) * pitch / 2, 0.0)
+        inner = pf.UniformGrid2D(12, 12, pitch, pitch, -11 * pitch / 2, -11 * pitch / 2, 0.0)
+        xy = np.column_stack([c.ravel() for c in np.meshgrid(g2.x_coords(), g2.y_coords())])
+        n_ill = 1 + i % 2
+        ill_xy = rng.uniform(-0.08, 0.08, size=(n_ill, 2))
+        if algo in ("rsd", "srsd", "nursd2", "srsd-nursd2"):
+            relay, ill = pf.UniformRelay(g2), pf.PointList(ill_xy)
+        elif algo in ("nursd1", "nursd3"):
+            jit = rng.uniform(-0.006, 0.006, size=xy.shape)
+            relay, ill = pf.NonUniformPlanarRelay(pf.PointList(xy + jit), z=0.0), pf.PointList(ill_xy)
+        else:
+            zs = rng.uniform(0.0, 0.01, size=len(xy))
+            relay = pf.NonPlanarRelay(pf.PointList(np.column_stack([xy, zs])))
+            ill = pf.PointList(np.column_stack([ill_xy, np.zeros(n_ill)]))
+        sl = make_slices(scene, relay, ill, lambda_c=lambda_c, delta_t=32e-12, n_bins=512)
+        z0 = z_mid - 0.09
+        if algo in ("rsd", "rsd3d", "nursd3d", "nursd1"):
+            grid = pf.CuboidGrid(UniformGrid3D(12, 12, 4, pitch, pitch, 0.06, inner.x0, inner.y0, z0))
+        elif algo == "srsd":
+            grid = pf.FrustumGrid(g2, z0 + 0.06 * np.arange(4), np.linspace(1.0, 0.85, 4),
+                                  np.linspace(1.0, 0.85, 4))
+        else:
+            planes = [pf.VoxelPlane(z0 + 0.07 * k, pf.PointList(rng.uniform(-0.1, 0.1, size=(120, 2))))
+                      for k in range(3)]
+            grid = pf.ExplicitVoxels(tuple(planes))
+        opts = {"alpha": 0.8} if algo == "srsd-nursd2" else {}
+        d = _slices_dict(sl)
+        d.update(_grid_dict(grid))
+        d["algo"] = np.array(algo)
+        d["alpha"] = np.array(opts.get("alpha", np.nan))
+        d["field"] = np.asarray(pf.reconstruct(sl, grid, algo, **opts).field)
+        d["backproject"] = np.asarray(pfo.backproject(sl, grid.coordinates()))
+        d["floor"] = np.array(0.9 if algo in ("rsd3d", "nursd3d") else 0.95)
+        out[f"acc{i}"] = d
+    for name, d in out.items():
+        save(f"acc_{name[3:]}", **d)
+
+
 def gen_sim():
     """Reference simulator (sim.py:67-129) on small scenes: non-confocal with ambient,
     confocal, no falloff, and a seeded Poisson draw."""
@@ -311,6 +368,7 @@ def gen_sim():
 
 
 if __name__ == "__main__":
+    gen_acceptance()
     gen_sim()
     gen_kernel_and_transform()
     gen_spectral()

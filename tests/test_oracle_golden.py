@@ -73,3 +73,14 @@ def test_reconstruction_golden(name):
     if "video" in d:
         vid = ORACLE_FN[alg](sl, grid, times=np.array([0.0, 5e-10]))
         assert O.rel_linf(vid, d["video"]) < 1e-11
+
+
+@pytest.mark.parametrize("i", range(20))
+def test_oracle_on_acceptance_scenes(i):
+    """The oracle reproduces the reference on its acceptance-suite scenes (all eight
+    algorithm paths, reference test_acceptance.py:204-266)."""
+    d = load(f"acc_{i}")
+    algo = str(d["algo"])
+    kw = {} if np.isnan(float(d["alpha"])) else {"alpha": float(d["alpha"])}
+    got = ORACLE_FN[algo](slices_from(d), grid_from(d), **kw)
+    assert O.rel_linf(got, d["field"]) < 1e-9, algo
