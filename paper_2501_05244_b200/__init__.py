@@ -18,8 +18,8 @@ from .core import (PROPAGATION_SIGN, SPEED_OF_LIGHT, ContainerFormatError, Cuboi
                    TorusMap, UniformGrid2D, UniformGrid3D, UniformRelay, UnsupportedVersionError,
                    ValidationError, VoxelPlane, grid_coordinates, illumination_coordinates,
                    rescale_to_torus)
-from .phasor import (DeviceFrequencySlices, PhasorKernel, build_kernel, to_frequency,
-                     to_frequency_device)
+from .phasor import (DeviceFrequencySlices, PhasorKernel, build_kernel, lateral_resolution,
+                     to_frequency, to_frequency_device)
 from .reconstruct import (ALGORITHM_NAMES, RsdEngine, light_transport_video, project_max_depth,
                           reconstruct, rsd)
 

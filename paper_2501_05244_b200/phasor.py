@@ -198,3 +198,10 @@ def to_frequency(measurement, kernel) -> DeviceFrequencySlices:
     coeff = to_frequency_device(ht, kernel, float(measurement.t0))
     return DeviceFrequencySlices(kernel.frequencies, coeff, measurement.relay,
                                  measurement.illuminations)
+
+
+def lateral_resolution(lambda_c: float, z: float, aperture: float) -> float:
+    """Diffraction-limited lateral resolution ``1.22 lambda_c z / aperture``
+    (reference phasor.py:130-134)."""
+    _require(lambda_c > 0 and z > 0 and aperture > 0, "wavelength, depth, and aperture must be > 0")
+    return 1.22 * lambda_c * z / aperture
