@@ -179,12 +179,20 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     t_k1, t_s3, t_step = [], [], []
+    # the timing rule: inputs larger than L2, or an L2 flush between timed steps
+    in_bytes = hist_shard.numel() * 4
+    l2_bytes = torch.cuda.get_device_properties(device).L2_cache_size
+    flush = None
+    if in_bytes < 2 * l2_bytes:
+        flush = torch.empty(4 * l2_bytes // 4, dtype=torch.float32, device=device)
     launches0 = _lib.launch_count
     with ClockSampler(local) as clk:
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
         for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1.0)   # evict the previous step's data (not inside ev[0]..ev[4])
             step()
             torch.cuda.synchronize()
             t_k1.append(ev[0].elapsed_time(ev[1]))
@@ -194,7 +202,9 @@ def run_ours(args):
         torch.cuda.synchronize()
     launches = (_lib.launch_count - launches0) // max(1, args.steps)
     launches += eng_graph_launches(eng)
-    total_ms = start.elapsed_time(end)
+    # with flushes between steps the region also holds the flush writes: use the
+    # per-step events (first kernel of the step to its last) instead
+    total_ms = sum(t_step) if flush is not None else start.elapsed_time(end)
     if world > 1:
         dist.barrier()
         tt = torch.tensor([total_ms])
@@ -262,17 +272,18 @@ def run_ours(args):
     fp32_peak = fp32_meas if fp32_meas > 0 else fp32_nominal
     clocks = clk.summary()
     roof_k1 = {"bound": "hbm", "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "peak": hbm_peak,
-               "unit": "GB/s", "traffic": _traffic("k_temporal_dft"), "kernel": "k_temporal_dft (K1)",
+               "unit": "GB/s", "traffic": _traffic("k_temporal_dft", args.config, world),
+               "kernel": "k_temporal_dft (K1)",
                "ms": k1_ms, "peak_source": peak_src}
     roof_k1["frac"] = roof_k1["achieved"] / hbm_peak
     roof_s3 = {"bound": "fp32", "achieved": s3_flops / (s3_ms * 1e-3) / 1e12, "peak": fp32_peak,
-               "unit": "TFLOP/s", "traffic": _prop_traffic(F, k_hi - k_lo),
+               "unit": "TFLOP/s", "traffic": _prop_traffic(F, k_hi - k_lo, args.config),
                "kernel": "propagation k_pa+k_pb1+k_pb2+k_pc (pf_prop_kernel_rows/columns/rows_out, S3)",
                "ms": s3_ms, "peak_source": "measured on this GPU before the timed region: FFMA probe "
                                            "(pf_fp32_probe, best of 6); nominal %.1f TFLOP/s = "
                                            "148 SM x 128 lanes x 2 x sm_max_mhz; MEASURED_PEAKS.json "
                                            "has no FP32 entry" % fp32_nominal,
-               "flops_model": "(2*F*Nz*I + F*I) * 5 P^2 log2(P^2), P=%d" % P,
+               "flops_model": _flops_model(cfg.algorithm, P),
                "traffic_note": "DRAM bytes of one plane batch of A+B1+B2+C from an ncu --set "
                                "full capture (profiles/ncu_traffic.json) scaled to F x Nz; ncu "
                                "flushes L2 before each kernel, so this counts the L2-resident "
@@ -288,7 +299,11 @@ def run_ours(args):
         "config": {"workload": f"config{args.config}-{cfg.algorithm}", "relay": cfg.relay.count,
                    "n_bins": T, "n_freq": F, "planes": nz,
                    "voxels": cfg.n_voxels, "pad": P, "parallelism": f"planes+detectors x{world}",
-                   "l2": "inputs (4.3 GB transients) exceed the 126 MB L2; no flush needed",
+                   "l2": ("inputs (%.2f GB transients) exceed the %d MB L2; no flush needed"
+                          % (in_bytes / 1e9, l2_bytes >> 20)) if flush is None else
+                         ("inputs (%.1f MB transients) fit the %d MB L2: a %d MB buffer is written "
+                          "between timed steps (outside the step events)"
+                          % (in_bytes / 1e6, l2_bytes >> 20, flush.numel() * 4 >> 20)),
                    "timed": "K1 + slice gather + propagation + volume gather"},
         "roofline": dominant, "roofline_other": other,
         "stage_ms": {"k1": k1_ms, "propagation": s3_ms, "step_event": statistics.mean(t_step)},
@@ -317,22 +332,35 @@ def eng_graph_launches(eng):
     return int(getattr(eng, "graph_kernels", 0))
 
 
-def _prop_traffic(n_freq, n_planes):
+def _flops_model(alg, P):
+    base = "(2*F*Nz*I + F*I) * 5 P^2 log2(P^2)"
+    if alg == "srsd":
+        base += " + F*Nz*I * (N + P) * 2 * 5 Q log2(Q), Q=2P (Bluestein x and y passes)"
+    elif alg == "nursd1":
+        base += " + F*I * (5 (2P)^2 log2((2P)^2) + L * 17^2 * 8) (type-1 NUFFT)"
+    return base + ", P=%d" % P
+
+
+def _prop_traffic(n_freq, n_planes, config):
     """Per-step DRAM bytes of the propagation stage from the committed ncu capture
-    (one plane batch of kernels A, B1, B2, C, cold L2), scaled to F x Nz."""
-    per_batch = _traffic("k_prop_per_batch")
-    planes = _traffic("batch_planes")
+    (one plane batch of kernels A, B1, B2, C, cold L2), scaled to F x Nz; only for the
+    configuration the capture was taken on (null otherwise: not measured)."""
+    per_batch = _traffic("k_prop_per_batch", config)
+    planes = _traffic("batch_planes", config)
     if per_batch is None or not planes:
         return None
     return per_batch * n_freq * (n_planes / float(planes))
 
 
-def _traffic(kernel_prefix):
-    """DRAM bytes per launch from the committed ncu capture summary, if present."""
+def _traffic(kernel_prefix, config, world=1):
+    """DRAM bytes per launch from the committed ncu capture summary, when it was taken
+    on this configuration (config 4, one GPU); null otherwise."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             t = json.load(f)
+        if int(t.get("config", 4)) != int(config) or world != 1:
+            return None
         return t.get(kernel_prefix)
     except Exception:
         return None
