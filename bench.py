@@ -219,42 +219,7 @@ def run_ours(args):
     # a stream of captures through TransientReconstructor.submit/result: every step
     # copies its transients host->device and its volume device->host; two captures
     # are in flight, so step i's upload overlaps step i-1's propagation
-    hist_host = torch.empty(hist_shard.shape, dtype=torch.float32, pin_memory=True)
-    hist_host.copy_(hist_shard)
-    n_e2e = max(8, args.steps)
-    for _ in range(2):
-        rec.result(rec.submit(hist_host))
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    handles = [rec.submit(hist_host) for _ in range(2)]
-    done_at = []
-    for _ in range(n_e2e - 2):
-        rec.result(handles.pop(0))
-        done_at.append(time.perf_counter())
-        handles.append(rec.submit(hist_host))
-    for h in handles:
-        rec.result(h)
-        done_at.append(time.perf_counter())
-    torch.cuda.synchronize()
-    e2e = (time.perf_counter() - t0) * 1e3 / n_e2e      # whole window, pipeline fill included
-    e2e_steady = (done_at[-1] - done_at[0]) * 1e3 / (len(done_at) - 1)
-    h2d_gbs = _h2d_probe(hist_host, device)
-    # single-capture latency through the blocking call, for reference
-    for _ in range(2):
-        rec(hist_host)
-    torch.cuda.synchronize()
-    a = time.perf_counter()
-    rec(hist_host)
-    torch.cuda.synchronize()
-    e2e_latency = (time.perf_counter() - a) * 1e3
-    if world > 1:
-        tt = torch.tensor([e2e, e2e_latency])
-        if dist.get_backend() == "nccl":
-            tt = tt.to(device)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e, e2e_latency = float(tt[0].item()), float(tt[1].item())
+    e2e_line = None if args.no_e2e else _e2e_leg(rec, hist_shard, cfg, world, device)
 
     hbm_peak, sm_max, peak_src = _peaks()
     k1_ms = statistics.mean(t_k1)
@@ -307,15 +272,7 @@ def run_ours(args):
                    "timed": "K1 + slice gather + propagation + volume gather"},
         "roofline": dominant, "roofline_other": other,
         "stage_ms": {"k1": k1_ms, "propagation": s3_ms, "step_event": statistics.mean(t_step)},
-        "e2e": {"value": cfg.n_voxels / (e2e * 1e-3), "unit": UNIT, "ms_per_step": e2e,
-                "single_capture_latency_ms": e2e_latency, "captures": n_e2e,
-                "steady_ms_per_step": e2e_steady,
-                "h2d_gbs_measured": h2d_gbs,
-                "h2d_floor_ms": hist_host.numel() * 4 / (h2d_gbs * 1e6),
-                "h2d_bytes_per_step": int(hist_host.numel() * 4 * world),
-                "d2h_bytes_per_step": int(cfg.n_voxels * 8),
-                "path": "TransientReconstructor.submit/result stream (pinned host f32 -> chunked "
-                        "H2D||K1 -> propagation -> D2H; 2 captures in flight; wall clock)"},
+        "e2e": e2e_line,
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
@@ -325,6 +282,60 @@ def run_ours(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def _e2e_leg(rec, hist_shard, cfg, world, device):
+    """Stream of captures through TransientReconstructor.submit/result: every step copies
+    its transients host->device and its volume device->host; two captures are in flight,
+    so step i's upload overlaps step i-1's propagation."""
+    import torch
+    import torch.distributed as dist
+    hist_host = torch.empty(hist_shard.shape, dtype=torch.float32, pin_memory=True)
+    hist_host.copy_(hist_shard)
+    n_e2e = 8   # captures in the timed window
+    for _ in range(2):
+        rec.result(rec.submit(hist_host))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    handles = [rec.submit(hist_host) for _ in range(2)]
+    done_at = []
+    for _ in range(n_e2e - 2):
+        rec.result(handles.pop(0))
+        done_at.append(time.perf_counter())
+        handles.append(rec.submit(hist_host))
+    for h in handles:
+        rec.result(h)
+        done_at.append(time.perf_counter())
+    torch.cuda.synchronize()
+    e2e = (time.perf_counter() - t0) * 1e3 / n_e2e      # whole window, pipeline fill included
+    e2e_steady = (done_at[-1] - done_at[0]) * 1e3 / (len(done_at) - 1)
+    h2d_gbs = _h2d_probe(hist_host, device)
+    # single-capture latency through the blocking call, for reference
+    for _ in range(2):
+        rec(hist_host)
+    torch.cuda.synchronize()
+    a = time.perf_counter()
+    rec(hist_host)
+    torch.cuda.synchronize()
+    e2e_latency = (time.perf_counter() - a) * 1e3
+    if world > 1:
+        tt = torch.tensor([e2e, e2e_latency])
+        if dist.get_backend() == "nccl":
+            tt = tt.to(device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e, e2e_latency = float(tt[0].item()), float(tt[1].item())
+
+    return {"value": cfg.n_voxels / (e2e * 1e-3), "unit": UNIT, "ms_per_step": e2e,
+            "single_capture_latency_ms": e2e_latency, "captures": n_e2e,
+            "steady_ms_per_step": e2e_steady,
+            "h2d_gbs_measured": h2d_gbs,
+            "h2d_floor_ms": hist_host.numel() * 4 / (h2d_gbs * 1e6),
+            "h2d_bytes_per_step": int(hist_host.numel() * 4 * world),
+            "d2h_bytes_per_step": int(cfg.n_voxels * 8),
+            "path": "TransientReconstructor.submit/result stream (pinned host f32 -> chunked "
+                    "H2D||K1 -> propagation -> D2H; 2 captures in flight; wall clock)"}
 
 
 def eng_graph_launches(eng):
@@ -542,6 +553,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="skip the end-to-end leg (for ncu launch lists of the device step)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -53,10 +53,13 @@ int pf_last_error(char* buf, size_t len);
  *   out[f * out_stride + trace] = (sum_t hist[trace][t] W_T^{bins[f] t}) * wphase[f]
  * hist: float32 [n_traces][n_bins]; twiddle: c64 [n_bins/64][n_freq] with
  * entry [r][f] = W_T^{bins[f] r} (fp64-built); wphase: c64 [n_freq] =
- * weight_f * exp(-1j w_f t0).  Requires n_bins = 64*M, M a power of two <= 256. */
+ * weight_f * exp(-1j w_f t0).  Requires n_bins = 64*M, M a power of two <= 256.
+ * n_inner: number of distinct inner bins min(b mod 64, 64 - b mod 64) over the
+ * retained bins (sizes shared memory; 0 = unknown, worst case 33; a count below
+ * the true one traps the kernel). */
 int pf_temporal_dft(const float* hist, int64_t n_traces, int n_bins, const int32_t* bins,
                     const void* twiddle, const void* wphase, int n_freq, void* out,
-                    int64_t out_stride, void* stream);
+                    int64_t out_stride, int n_inner, void* stream);
 /* Same transform for any n_bins (direct sum); unit_roots: c64 [n_bins] W_T^m. */
 int pf_temporal_dft_direct(const float* hist, int64_t n_traces, int n_bins,
                            const int32_t* bins, const void* unit_roots, const void* wphase,
@@ -149,6 +152,17 @@ int pf_prop_fbatch(const pf_plane* planes, int nplanes, const double* kturns, in
                    const pf_prop_geom* g, const pf_fft_plan* plan, void* ws_a, int64_t ws_a_fs,
                    const void* uhat, int64_t uhat_fs, void* ws_b, int64_t ws_b_fs,
                    const double* ill_xyz, const void* frame_w, void* vol, void* stream);
+
+/* pf_prop_fbatch for any pad (Stockham shared-memory path; e.g. the reference's
+ * P = 140 of config 1): khat_f: device float64 [nf] wavenumbers (rad/m); plan_x /
+ * plan_y: length px / py plans; otherwise as pf_prop_fbatch.  Three launches:
+ * A and B over (tiles, planes, frequencies), C looping the frequencies in
+ * ascending order per (row tile, plane) with the sum kept in shared memory. */
+int pf_prop_fbatch_generic(const pf_plane* planes, int nplanes, const double* khat_f, int nf,
+                           const pf_prop_geom* g, const pf_fft_plan* plan_x,
+                           const pf_fft_plan* plan_y, void* ws_a, int64_t ws_a_fs,
+                           const void* uhat, int64_t uhat_fs, void* ws_b, int64_t ws_b_fs,
+                           const double* ill_xyz, const void* frame_w, void* vol, void* stream);
 
 /* Streaming propagation: all (plane, frequency) jobs of a register-path
  * reconstruction in one persistent launch (same stages and results as

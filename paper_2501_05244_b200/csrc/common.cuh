@@ -66,6 +66,18 @@ void pf_set_error(const char* fmt, ...);
 
 static inline int pf_cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// SM count of the current device (grid sizing), queried once per process
+static inline int pf_sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
 // ---------------------------------------------------------------- async copy
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -73,3 +85,4 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) 
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }

@@ -72,17 +72,52 @@ __device__ __forceinline__ void dft_split(float2* v) {
   }
 }
 
+// v * W_N^e (forward, DIR = -1) or v * conj(W_N^e); e is a constant after unrolling,
+// so the quarter-turn cases fold to swaps / negations and cost no instructions
+template <int N, int DIR>
+__device__ __forceinline__ float2 twc(float2 v, int e) {
+  e %= N;
+  if (e == 0) return v;
+  if (2 * e == N) return make_float2(-v.x, -v.y);
+  if (4 * e == N) return DIR < 0 ? make_float2(v.y, -v.x) : make_float2(-v.y, v.x);
+  if (4 * e == 3 * N) return DIR < 0 ? make_float2(-v.y, v.x) : make_float2(v.y, -v.x);
+  return rot<DIR>(v, Unit<N>::c(e), Unit<N>::s(e));
+}
+
+// Cooley-Tukey N = A * B in registers: A-point DFTs over n1 of x[B n1 + n2],
+// twiddles W_N^{n2 k1}, B-point DFTs over n2; X[k1 + A k2] lands in v[k1 + A k2].
+// 4 x 8 for N = 32 takes 432 FP instructions against 470 for the radix-2 split.
+template <int A, int B, int DIR>
+__device__ __forceinline__ void dft_ct(float2* v) {
+  float2 y[B][A];
+#pragma unroll
+  for (int n2 = 0; n2 < B; n2++) {
+#pragma unroll
+    for (int n1 = 0; n1 < A; n1++) y[n2][n1] = v[B * n1 + n2];
+    Dft<A, DIR>::run(y[n2]);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < A; k1++) {
+    float2 z[B];
+#pragma unroll
+    for (int n2 = 0; n2 < B; n2++) z[n2] = twc<A * B, DIR>(y[n2][k1], n2 * k1);
+    Dft<B, DIR>::run(z);
+#pragma unroll
+    for (int k2 = 0; k2 < B; k2++) v[k1 + A * k2] = z[k2];
+  }
+}
+
 template <int DIR>
 struct Dft<8, DIR> {
-  static __device__ __forceinline__ void run(float2* v) { dft_split<8, DIR>(v); }
+  static __device__ __forceinline__ void run(float2* v) { dft_ct<4, 2, DIR>(v); }
 };
 template <int DIR>
 struct Dft<16, DIR> {
-  static __device__ __forceinline__ void run(float2* v) { dft_split<16, DIR>(v); }
+  static __device__ __forceinline__ void run(float2* v) { dft_ct<4, 4, DIR>(v); }
 };
 template <int DIR>
 struct Dft<32, DIR> {
-  static __device__ __forceinline__ void run(float2* v) { dft_split<32, DIR>(v); }
+  static __device__ __forceinline__ void run(float2* v) { dft_ct<4, 8, DIR>(v); }
 };
 
 // odd prime radix: pair j with R-j (real cosine / sine halves)

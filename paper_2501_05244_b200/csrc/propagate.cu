@@ -35,11 +35,17 @@ __device__ __forceinline__ float2 rsd_kernel(double khat, double lx, double ly, 
 }
 
 // (A) kernel rows jy in [0, py/2] -> x-FFT -> keep kx in [0, px/2]
+// Frequency batch (khat_f != nullptr): blockIdx.z is the frequency, ws_a per-f stride ws_a_fs.
 __global__ void __launch_bounds__(PT)
 k_prop_kernel_rows(const pf_plane* __restrict__ planes, double khat, pf_prop_geom g,
-                   pf_fft_plan plan_x, float2* __restrict__ ws_a, int rows_per_cta) {
+                   pf_fft_plan plan_x, float2* __restrict__ ws_a, int rows_per_cta,
+                   const double* __restrict__ khat_f = nullptr, long long ws_a_fs = 0) {
   extern __shared__ float2 sm[];
   const pf_plane pl = planes[blockIdx.y];
+  if (khat_f) {
+    khat = khat_f[blockIdx.z];
+    ws_a += blockIdx.z * ws_a_fs;
+  }
   const int px = g.px, py = g.py;
   const int rows_a = py / 2 + 1, cols_a = px / 2 + 1;
   const int ld = pf_ld(px);
@@ -67,8 +73,12 @@ k_prop_kernel_rows(const pf_plane* __restrict__ planes, double khat, pf_prop_geo
 __global__ void __launch_bounds__(PT)
 k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan plan_y,
                const float2* __restrict__ ws_a, const float2* __restrict__ uhat,
-               float2* __restrict__ ws_b, int cols_per_cta, int product_only) {
+               float2* __restrict__ ws_b, int cols_per_cta, int product_only,
+               long long ws_a_fs = 0, long long uhat_fs = 0, long long ws_b_fs = 0) {
   extern __shared__ float2 sm[];
+  ws_a += blockIdx.z * ws_a_fs;   // frequency batch: blockIdx.z is the frequency
+  uhat += blockIdx.z * uhat_fs;
+  ws_b += blockIdx.z * ws_b_fs;
   const pf_plane pl = planes[blockIdx.y];
   const int px = g.px, py = g.py, ny = g.ny;
   const int rows_a = py / 2 + 1, cols_a = px / 2 + 1;
@@ -171,6 +181,60 @@ k_prop_rows_out(const pf_plane* __restrict__ planes, double khat, pf_prop_geom g
   }
 }
 
+// (C) over all nf frequencies of a batch: per (row tile, plane) the ascending-
+// frequency sum is formed in shared memory (acc, fp32, same operation order as
+// the per-frequency launches) and added to the volume once.  Single frame.
+__global__ void __launch_bounds__(PT)
+k_prop_rows_out_fb(const pf_plane* __restrict__ planes, const double* __restrict__ khat_f, int nf,
+                   pf_prop_geom g, pf_fft_plan plan_x, const float2* __restrict__ ws_b,
+                   long long ws_b_fs, const double* __restrict__ ill,
+                   const float2* __restrict__ frame_w, float2* __restrict__ vol,
+                   int rows_per_cta) {
+  extern __shared__ float2 sm[];
+  const pf_plane pl = planes[blockIdx.y];
+  const int px = g.px, nx = g.nx, ny = g.ny;
+  const int ld = pf_ld(px);
+  const int i0 = blockIdx.x * rows_per_cta;
+  const int nr = min(rows_per_cta, ny - i0);
+  float2* a = sm;
+  float2* b = sm + (size_t)rows_per_cta * ld;
+  float2* acc = sm + (size_t)2 * rows_per_cta * ld;   // [nr][nx]
+  for (int e = threadIdx.x; e < nr * nx; e += PT) acc[e] = make_float2(0.f, 0.f);
+  const float scale = 1.0f / ((float)g.px * (float)g.py);
+  for (int f = 0; f < nf; f++) {
+    const double khat = khat_f[f];
+    const float2 fw = frame_w[f];
+    for (int p = 0; p < g.n_illum; p++) {
+      const float2* src = ws_b + f * ws_b_fs +
+                          (((long long)blockIdx.y * g.n_illum + p) * ny + i0) * (long long)px;
+      for (int e = threadIdx.x; e < nr * px; e += PT) {
+        const int c = e / px, jx = e - c * px;
+        a[c * ld + jx] = src[(long long)c * px + jx];
+      }
+      __syncthreads();
+      const float2* res = fft_smem<1>(a, b, ld, nr, plan_x);
+      const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
+      for (int e = threadIdx.x; e < nr * nx; e += PT) {
+        const int c = e / nx, m = e - c * nx;
+        float2 v = cscale(res[c * ld + natural((long long)g.nu0x + m, px)], scale);
+        if (g.include_illum) {
+          const double dx = pl.x0 + pl.dx * m - sx;
+          const double dy = pl.y0 + pl.dy * (i0 + c) - sy;
+          const double dz = pl.z - sz;
+          v = cmul(v, expi_reduced(khat * sqrt(fma(dx, dx, fma(dy, dy, dz * dz)))));
+        }
+        acc[e] = cadd(acc[e], cmul(v, fw));
+      }
+      __syncthreads();
+    }
+  }
+  for (int e = threadIdx.x; e < nr * nx; e += PT) {
+    const int c = e / nx, m = e - c * nx;
+    float2* d = vol + (pl.vol_plane * ny + i0 + c) * (long long)nx + m;
+    *d = cadd(*d, acc[e]);
+  }
+}
+
 template <typename K>
 void allow_smem(K kern) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PSMEM);
@@ -198,6 +262,57 @@ int pf_prop_fbatch_stage(int stage, const pf_plane* planes, int nplanes, const d
                          long long ws_a_fs, const void* uhat, long long uhat_fs, void* ws_b,
                          long long ws_b_fs, const double* ill, const void* frame_w, void* vol,
                          cudaStream_t st);
+
+// Generic (Stockham) path over all nf frequencies: one launch per stage, blockIdx.z
+// the frequency in A and B; C loops the frequencies (khat_f in rad/m, [nf]).
+static int prop_fbatch_generic(const pf_plane* planes, int nplanes, const double* khat_f, int nf,
+                               const pf_prop_geom* g, const pf_fft_plan* plan_x,
+                               const pf_fft_plan* plan_y, void* ws_a, int64_t ws_a_fs,
+                               const void* uhat, int64_t uhat_fs, void* ws_b, int64_t ws_b_fs,
+                               const double* ill, const void* frame_w, void* vol,
+                               cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    allow_smem(k_prop_kernel_rows);
+    allow_smem(k_prop_columns);
+    allow_smem(k_prop_rows_out_fb);
+    attr = true;
+  }
+  const int rows_a = g->py / 2 + 1, cols_a = g->px / 2 + 1;
+  // many lines per CTA: every Stockham stage then has work for all threads
+  const int rpc = rows_fit(g->px, 2, (8 * PT + g->px - 1) / g->px);
+  const int cpc = rows_fit(g->py, 3, 16);
+  const int rpo = rows_fit(g->px, 3, 8);
+  if (rpc < 1 || cpc < 1 || rpo < 1) { pf_set_error("pf_prop_fbatch: pad too large"); return -1; }
+  k_prop_kernel_rows<<<dim3(pf_cdiv(rows_a, rpc), nplanes, nf), PT,
+                       (size_t)2 * rpc * pf_ld(g->px) * sizeof(float2), st>>>(
+      planes, 0.0, *g, *plan_x, (float2*)ws_a, rpc, khat_f, ws_a_fs);
+  PF_LAUNCH_CHECK("k_prop_kernel_rows");
+  k_prop_columns<<<dim3(pf_cdiv(cols_a, cpc), nplanes, nf), PT,
+                   (size_t)3 * cpc * pf_ld(g->py) * sizeof(float2), st>>>(
+      planes, *g, *plan_y, (const float2*)ws_a, (const float2*)uhat, (float2*)ws_b, cpc, 0,
+      ws_a_fs, uhat_fs, ws_b_fs);
+  PF_LAUNCH_CHECK("k_prop_columns");
+  const size_t smo = ((size_t)2 * rpo * pf_ld(g->px) + (size_t)rpo * g->nx) * sizeof(float2);
+  k_prop_rows_out_fb<<<dim3(pf_cdiv(g->ny, rpo), nplanes), PT, smo, st>>>(
+      planes, khat_f, nf, *g, *plan_x, (const float2*)ws_b, ws_b_fs, ill, (const float2*)frame_w,
+      (float2*)vol, rpo);
+  PF_LAUNCH_CHECK("k_prop_rows_out_fb");
+  return 0;
+}
+
+extern "C" int pf_prop_fbatch_generic(const pf_plane* planes, int nplanes, const double* khat_f,
+                                      int nf, const pf_prop_geom* g, const pf_fft_plan* plan_x,
+                                      const pf_fft_plan* plan_y, void* ws_a, int64_t ws_a_fs,
+                                      const void* uhat, int64_t uhat_fs, void* ws_b,
+                                      int64_t ws_b_fs, const double* ill_xyz,
+                                      const void* frame_w, void* vol, void* stream) {
+  PF_ARG_CHECK(g && plan_x && plan_y && nf >= 1 && nplanes >= 1 && plan_x->n == g->px &&
+                   plan_y->n == g->py,
+               "pf_prop_fbatch_generic: bad args");
+  return prop_fbatch_generic(planes, nplanes, khat_f, nf, g, plan_x, plan_y, ws_a, ws_a_fs, uhat,
+                             uhat_fs, ws_b, ws_b_fs, ill_xyz, frame_w, vol, (cudaStream_t)stream);
+}
 
 extern "C" int pf_prop_fbatch(const pf_plane* planes, int nplanes, const double* kturns, int nf,
                               const pf_prop_geom* g, const pf_fft_plan* plan, void* ws_a,

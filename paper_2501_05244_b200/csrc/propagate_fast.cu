@@ -117,14 +117,19 @@ k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
 
 // C over all frequencies of the batch in one launch: per (plane, row tile) the
 // ascending-frequency sum is formed in registers and written once.
-template <int L, bool MULTI>
-__global__ void __launch_bounds__(FT, 1)
+// NW warps per CTA (RPC = NW * 32/L rows): small volumes (config 0: 64 planes x
+// 64 rows) take fewer rows per CTA so the grid still covers the SMs.  The
+// (frequency, illumination) tiles are double-buffered: the cp.async load of the
+// next tile is in flight while the current one is transformed.
+template <int L, bool MULTI, int NW = 8>
+__global__ void __launch_bounds__(32 * NW, 1)
 k_pcf(const pf_plane* __restrict__ planes, pf_prop_geom g, const float2* __restrict__ tw,
       const float2* __restrict__ ws_b, const double* __restrict__ ill,
       const float2* __restrict__ frame_w, float2* __restrict__ vol, FBatch fb) {
   constexpr int P = 32 * L;
-  constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
+  constexpr int LPW = 32 / L, RPC = NW * LPW, SLD = RPC + 1, TILE = P * SLD;
   extern __shared__ float2 sm[];
+  float2* xch = sm + 2 * TILE;   // per-warp FFT exchange, disjoint from the two tiles
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = lane % L, line = lane / L;
   const int r = warp * LPW + line;
@@ -135,54 +140,60 @@ k_pcf(const pf_plane* __restrict__ planes, pf_prop_geom g, const float2* __restr
   const pf_plane pl = planes[blockIdx.y];
   const float scale = 1.0f / ((float)P * (float)P);
   const double yv = pl.y0 + pl.dy * i;
+  const int n_ill = MULTI ? g.n_illum : 1;
+  const int n_tiles = fb.nf * n_ill;
+  auto load_tile = [&](int idx, float2* dst) {
+    const int f = idx / n_ill, p = idx - f * n_ill;
+    const float2* src = ws_b + f * fb.ws_b_fs +
+                        ((long long)blockIdx.y * g.n_illum + p) * (long long)P * ny + i0;
+    constexpr int CSTEP = 32 * NW / RPC;
+    const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
+    if (rr < nr) {
+      const float2* q = src + (long long)c0 * ny + rr;
+      float2* d = dst + c0 * SLD + rr;
+#pragma unroll 8
+      for (int col = c0; col < P; col += CSTEP) {
+        cp_async8(d, q);
+        q += (long long)CSTEP * ny;
+        d += CSTEP * SLD;
+      }
+    }
+    cp_async_commit();
+  };
   float2 acc[32];
 #pragma unroll
   for (int m = 0; m < 32; m++) acc[m] = make_float2(0.f, 0.f);
-  const int n_ill = MULTI ? g.n_illum : 1;
+  load_tile(0, sm);
 #pragma unroll 1
-  for (int f = 0; f < fb.nf; f++) {
+  for (int idx = 0; idx < n_tiles; idx++) {
+    const int f = idx / n_ill, p = idx - f * n_ill;
+    float2* cur = sm + (idx & 1) * TILE;
+    if (idx + 1 < n_tiles) {
+      load_tile(idx + 1, sm + ((idx + 1) & 1) * TILE);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    float2 v[32];
+#pragma unroll
+    for (int m = 0; m < 32; m++) v[m] = cur[(t + L * m) * SLD + r];
+    __syncthreads();   // the tile is refilled by the load issued in the next iteration
+    wfft<L, 1>(v, xch + warp * WFFT_XCH, tw);
     const double kturns = fb.kturns[f];
     const float2 fw = frame_w[f];
-#pragma unroll 1
-    for (int p = 0; p < n_ill; p++) {
-      const float2* src = ws_b + f * fb.ws_b_fs +
-                          ((long long)blockIdx.y * g.n_illum + p) * (long long)P * ny + i0;
-      __syncthreads();
-      {
-        constexpr int CSTEP = FT / RPC;
-        const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
-        if (rr < nr) {
-          const float2* q = src + (long long)c0 * ny + rr;
-          float2* d = sm + c0 * SLD + rr;
-#pragma unroll 8
-          for (int col = c0; col < P; col += CSTEP) {
-            cp_async8(d, q);
-            q += (long long)CSTEP * ny;
-            d += CSTEP * SLD;
-          }
-        }
-      }
-      cp_async_commit();
-      cp_async_wait_all();
-      __syncthreads();
-      float2 v[32];
+    const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
+    const double dy = yv - sy, dz = pl.z - sz;
+    const double byz = fma(dy, dy, dz * dz);
 #pragma unroll
-      for (int m = 0; m < 32; m++) v[m] = sm[(t + L * m) * SLD + r];
-      __syncthreads();
-      wfft<L, 1>(v, sm + warp * WFFT_XCH, tw);
-      const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
-      const double dy = yv - sy, dz = pl.z - sz;
-      const double byz = fma(dy, dy, dz * dz);
-#pragma unroll
-      for (int m = 0; m < 32; m++) {
-        const int mo = (t + L * m - g.nu0x) & (P - 1);
-        float2 val = cscale(v[m], scale);
-        if (g.include_illum && mo < nx) {
-          const double dx = pl.x0 + pl.dx * mo - sx;
-          val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
-        }
-        acc[m] = cadd(acc[m], cmul(val, fw));
+    for (int m = 0; m < 32; m++) {
+      const int mo = (t + L * m - g.nu0x) & (P - 1);
+      float2 val = cscale(v[m], scale);
+      if (g.include_illum && mo < nx) {
+        const double dx = pl.x0 + pl.dx * mo - sx;
+        val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
       }
+      acc[m] = cadd(acc[m], cmul(val, fw));
     }
   }
   if (i < ny) {
@@ -200,6 +211,12 @@ size_t smem_a() {
   constexpr int P = 32 * L, NA = P / 2 + 1, RPC = NW * (32 / L);
   size_t x = NW * WFFT_XCH, s = (size_t)NA * (RPC + 1);
   return (x > s ? x : s) * sizeof(float2);
+}
+// k_pcf: two tiles + the per-warp exchange buffers
+template <int L, int NW = 8>
+size_t smem_cf() {
+  constexpr int P = 32 * L, RPC = NW * (32 / L);
+  return ((size_t)2 * P * (RPC + 1) + (size_t)NW * WFFT_XCH) * sizeof(float2);
 }
 template <int L, int NW = 8>
 size_t smem_c(int nx, bool pre) {
@@ -226,8 +243,11 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     cudaFuncSetAttribute(k_pc<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_pc<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_pc<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_pcf<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_pcf<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    const int most = 227 * 1024;   // k_pcf at P = 1024 with 8 warps: 215 KB
+    cudaFuncSetAttribute(k_pcf<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+    cudaFuncSetAttribute(k_pcf<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+    cudaFuncSetAttribute(k_pcf<L, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+    cudaFuncSetAttribute(k_pcf<L, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
     attr = true;
   }
   const double kturns = khat / PF_TWO_PI;
@@ -247,12 +267,24 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
       k_pb2<L, false><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
     PF_LAUNCH_CHECK("k_pb2");
   } else if (fb.kturns != nullptr) {   // C over all frequencies of the batch
-    dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
-    const size_t sm = smem_c<L>(g.nx, false);
-    if (g.n_illum > 1)
-      k_pcf<L, true><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
-    else
-      k_pcf<L, false><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+    // 8 warps per CTA unless that leaves fewer than two CTAs per SM; then 2
+    const bool narrow = (long long)pf_cdiv(g.ny, RPC) * nplanes < 2LL * pf_sm_count();
+    if (narrow) {
+      constexpr int RPC2 = 2 * (32 / L);
+      dim3 grid(pf_cdiv(g.ny, RPC2), nplanes);
+      const size_t sm = smem_cf<L, 2>();
+      if (g.n_illum > 1)
+        k_pcf<L, true, 2><<<grid, 64, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+      else
+        k_pcf<L, false, 2><<<grid, 64, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+    } else {
+      dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
+      const size_t sm = smem_cf<L>();
+      if (g.n_illum > 1)
+        k_pcf<L, true><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+      else
+        k_pcf<L, false><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+    }
     PF_LAUNCH_CHECK("k_pcf");
   } else {   // C: x-IFFT, crop, illumination phase, volume accumulate
     dim3 grid(pf_cdiv(g.ny, RPC), nplanes);

@@ -23,40 +23,65 @@ constexpr int K1_THREADS = 256;
 constexpr int K1_L = 64;     // inner DFT length
 constexpr int K1_KB = 33;    // non-redundant bins of a real 64-point DFT
 
-// 64-point real DFT of x[0..63] -> X[0..32]
-__device__ __forceinline__ void real_dft64(const float* x, float2* X) {
+// 64-point real DFT of x[0..63]: the non-redundant bins k in [0, 32] selected by
+// `mask` (bit k; warp-uniform) are stored to dst[0], dst[1], ... in ascending k.
+__device__ __forceinline__ void real_dft64_sel(const float* x, unsigned long long mask,
+                                               float2* dst) {
   float2 z[32];
 #pragma unroll
   for (int q = 0; q < 32; q++) z[q] = make_float2(x[2 * q], x[2 * q + 1]);
   Dft<32, -1>::run(z);
+  int s = 0;
 #pragma unroll
   for (int k = 0; k <= 32; k++) {
-    const float2 a = z[k & 31];
-    const float2 b = cconj(z[(32 - k) & 31]);
-    const float2 e = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y + b.y));
-    // o = (a - b) / (2i)
-    const float2 o = make_float2(0.5f * (a.y - b.y), -0.5f * (a.x - b.x));
-    // W_64^k = exp(-2 pi i k / 64)
-    const float c = Unit<64>::c(k & 63), s = -Unit<64>::s(k & 63);
-    X[k] = make_float2(e.x + o.x * c - o.y * s, e.y + o.x * s + o.y * c);
+    if ((mask >> k) & 1ull) {
+      const float2 a = z[k & 31];
+      const float2 b = cconj(z[(32 - k) & 31]);
+      const float2 e = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y + b.y));
+      // o = (a - b) / (2i)
+      const float2 o = make_float2(0.5f * (a.y - b.y), -0.5f * (a.x - b.x));
+      // W_64^k = exp(-2 pi i k / 64)
+      const float c = Unit<64>::c(k & 63), sn = -Unit<64>::s(k & 63);
+      dst[s++] = make_float2(e.x + o.x * c - o.y * sn, e.y + o.x * sn + o.y * c);
+    }
   }
 }
 
+// all 33 bins (the TMA-fed variant)
+__device__ __forceinline__ void real_dft64(const float* x, float2* X) {
+  real_dft64_sel(x, (1ull << 33) - 1ull, X);
+}
+
+// Only the inner bins k = b mod 64 the retained bins need are formed and
+// parked (config 4: 20 of the 33 non-redundant bins): the split step, the
+// shared-memory stores and the per-trace stride shrink accordingly.
 template <int M>
 __global__ void __launch_bounds__(K1_THREADS)
 k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __restrict__ bins,
                const float2* __restrict__ twt /*[M][twt_ld]*/, int twt_ld,
                const float2* __restrict__ wphase, int F, float2* __restrict__ out,
-               long long out_stride) {
+               long long out_stride, int nkp_cap) {
   constexpr int G = K1_THREADS / M;          // traces per block pass
-  constexpr int TS = M * K1_KB + 1;          // padded per-trace stride (float2)
   constexpr int T = M * K1_L;
   extern __shared__ float2 smem[];
-  float2* xs = smem;                 // [G][M][33] (+1 pad per trace)
-  float2* tws = smem + G * TS;       // [M][F]
-  int* kb = reinterpret_cast<int*>(tws + M * F);  // [F] bin mod 64
+  float2* tws = smem;                        // [M][F]
+  int* ks = reinterpret_cast<int*>(tws + M * F);   // [F] slot | conj << 8
+  float2* xs = reinterpret_cast<float2*>(ks + ((F + 1) & ~1));   // [G][M][nkp] (+1 per trace)
   for (int e = threadIdx.x; e < M * F; e += K1_THREADS) tws[e] = twt[(e / F) * twt_ld + e % F];
-  for (int e = threadIdx.x; e < F; e += K1_THREADS) kb[e] = bins[e] & 63;
+  unsigned long long mask = 0;
+  for (int f = 0; f < F; f++) {
+    const int k = __ldg(bins + f) & 63;
+    mask |= 1ull << (k > 32 ? 64 - k : k);
+  }
+  const int nk = __popcll(mask);
+  const int nkp = nk | 1;            // odd stride: conflict-free parking across r
+  if (nkp > nkp_cap) __trap();       // shared memory was sized for fewer bins (bad n_inner)
+  const int ts = M * nkp + 1;        // per-trace stride
+  for (int f = threadIdx.x; f < F; f += K1_THREADS) {
+    const int k = bins[f] & 63;
+    const int kk = k > 32 ? 64 - k : k;
+    ks[f] = __popcll(mask & ((1ull << kk) - 1ull)) | ((k > 32) << 8);
+  }
   __syncthreads();
 
   const int g = threadIdx.x / M;
@@ -69,25 +94,20 @@ k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __
       float x[64];
 #pragma unroll
       for (int q = 0; q < 64; q++) x[q] = __ldg(h + q * M);
-      float2 X[K1_KB];
-      real_dft64(x, X);
-      float2* dst = xs + g * TS + r * K1_KB;
-#pragma unroll
-      for (int k = 0; k < K1_KB; k++) dst[k] = X[k];
+      real_dft64_sel(x, mask, xs + g * ts + r * nkp);
     }
     __syncthreads();
     for (int p = threadIdx.x; p < G * F; p += K1_THREADS) {
       const int gg = p % G, f = p / G;
       const long long tr = grp * G + gg;
       if (tr >= n_traces) continue;
-      const int k = kb[f];
-      const bool cj = k > 32;
-      const int kk = cj ? 64 - k : k;
-      const float2* src = xs + gg * TS + kk;
+      const int kv = ks[f];
+      const bool cj = kv >> 8;
+      const float2* src = xs + gg * ts + (kv & 255);
       float2 acc = make_float2(0.f, 0.f);
 #pragma unroll 8
       for (int rr = 0; rr < M; rr++) {
-        float2 z = src[rr * K1_KB];
+        float2 z = src[rr * nkp];
         if (cj) z.y = -z.y;
         cacc(acc, z, tws[rr * F + f]);
       }
@@ -252,10 +272,16 @@ constexpr int K1_FCHUNK = 64;  // retained bins per pass (shared-memory bound)
 template <int M>
 int launch_k1(const float* hist, long long n_traces, const int* bins, const float2* twt,
               const float2* wphase, int F_total, float2* out, long long out_stride,
-              cudaStream_t st) {
+              int n_inner, cudaStream_t st) {
   constexpr int G = K1_THREADS / M;
   const int FC = F_total < K1_FCHUNK ? F_total : K1_FCHUNK;
-  const size_t smem = (size_t)(G * (M * K1_KB + 1) + M * FC) * sizeof(float2) + FC * sizeof(int);
+  // parked bins per column: the caller's count of distinct inner bins (bins mod 64
+  // folded to [0, 32]) when given, else the worst case
+  int nk = (n_inner >= 1 && n_inner <= K1_KB) ? n_inner : K1_KB;
+  if (nk > FC) nk = FC;
+  const int nkp = nk | 1;
+  const size_t smem = (size_t)(G * (M * nkp + 1) + M * FC) * sizeof(float2) +
+                      ((FC + 1) & ~1) * sizeof(int);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_temporal_dft<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -265,13 +291,17 @@ int launch_k1(const float* hist, long long n_traces, const int* bins, const floa
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const long long groups = (n_traces + G - 1) / G;
-  const int grid = (int)(groups < (long long)nsm * 8 ? groups : (long long)nsm * 8);
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_temporal_dft<M>, K1_THREADS, smem);
+  if (per < 1) per = 1;
+  const long long cap = (long long)nsm * per;
+  const int grid_k1 = (int)(groups < cap ? groups : cap);
   for (int f0 = 0; f0 < F_total; f0 += FC) {
     const int F = F_total - f0 < FC ? F_total - f0 : FC;
-    k_temporal_dft<M><<<grid, K1_THREADS, smem, st>>>(hist, n_traces, bins + f0, twt + f0,
+    k_temporal_dft<M><<<grid_k1, K1_THREADS, smem, st>>>(hist, n_traces, bins + f0, twt + f0,
                                                        F_total, wphase + f0, F,
                                                        out + (long long)f0 * out_stride,
-                                                       out_stride);
+                                                       out_stride, nkp);
     PF_LAUNCH_CHECK("k_temporal_dft");
   }
   return 0;
@@ -327,7 +357,8 @@ int launch_k1_tma(const float* hist, long long n_traces, const int* bins, const 
 
 extern "C" int pf_temporal_dft(const float* hist, int64_t n_traces, int n_bins,
                                const int32_t* bins, const void* twiddle, const void* wphase,
-                               int n_freq, void* out, int64_t out_stride, void* stream) {
+                               int n_freq, void* out, int64_t out_stride, int n_inner,
+                               void* stream) {
   PF_ARG_CHECK(n_traces >= 0 && n_freq >= 1 && n_bins >= 1, "pf_temporal_dft: bad sizes");
   if (n_traces == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
@@ -340,15 +371,15 @@ extern "C" int pf_temporal_dft(const float* hist, int64_t n_traces, int n_bins,
   if (M == 64 && ((uintptr_t)hist & 15) == 0 && n_freq <= K1_FCHUNK && getenv("PF_K1_TMA"))
     return launch_k1_tma(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
   switch (M) {
-    case 1: return launch_k1<1>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
-    case 2: return launch_k1<2>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
-    case 4: return launch_k1<4>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
-    case 8: return launch_k1<8>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
-    case 16: return launch_k1<16>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
-    case 32: return launch_k1<32>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
-    case 64: return launch_k1<64>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
-    case 128: return launch_k1<128>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
-    case 256: return launch_k1<256>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
+    case 1: return launch_k1<1>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
+    case 2: return launch_k1<2>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
+    case 4: return launch_k1<4>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
+    case 8: return launch_k1<8>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
+    case 16: return launch_k1<16>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
+    case 32: return launch_k1<32>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
+    case 64: return launch_k1<64>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
+    case 128: return launch_k1<128>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
+    case 256: return launch_k1<256>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
     default: break;
   }
   pf_set_error("pf_temporal_dft: n_bins must be 64*M with M a power of two <= 256 "

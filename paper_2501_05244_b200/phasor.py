@@ -148,6 +148,8 @@ class TemporalPlan:
             r = np.arange(m, dtype=np.int64)
             ph = (np.outer(r, bins) % T).astype(np.float64) / T   # [M, F], exact integer reduction
             self.tw = torch.from_numpy(np.exp(-2j * np.pi * ph).astype(np.complex64)).to(device)
+            k = bins % 64
+            self.n_inner = int(np.unique(np.minimum(k, 64 - k)).size)
         else:
             ph = np.arange(T, dtype=np.float64) / T
             self.tw = torch.from_numpy(np.exp(-2j * np.pi * ph).astype(np.complex64)).to(device)
@@ -155,10 +157,14 @@ class TemporalPlan:
     def run(self, hist: torch.Tensor, out: torch.Tensor, stream=None) -> None:
         """hist float32 [n_traces, T] (contiguous) -> out complex64 [F, n_traces]."""
         n_traces = hist.shape[0]
-        name = "pf_temporal_dft" if self.fast else "pf_temporal_dft_direct"
-        _lib.call(name, dev.ptr(hist), n_traces, self.n_bins, dev.ptr(self.bins), dev.ptr(self.tw),
-                  dev.ptr(self.wphase), self.n_freq, dev.ptr(out), out.stride(0),
-                  dev.stream_ptr(stream))
+        if self.fast:
+            _lib.call("pf_temporal_dft", dev.ptr(hist), n_traces, self.n_bins, dev.ptr(self.bins),
+                      dev.ptr(self.tw), dev.ptr(self.wphase), self.n_freq, dev.ptr(out),
+                      out.stride(0), self.n_inner, dev.stream_ptr(stream))
+        else:
+            _lib.call("pf_temporal_dft_direct", dev.ptr(hist), n_traces, self.n_bins,
+                      dev.ptr(self.bins), dev.ptr(self.tw), dev.ptr(self.wphase), self.n_freq,
+                      dev.ptr(out), out.stride(0), dev.stream_ptr(stream))
 
 
 def to_frequency_device(histograms: torch.Tensor, kernel, t0: float = 0.0,

@@ -43,6 +43,7 @@ _BATCH_BYTES = 64 << 20
 _LANES = int(os.environ.get("PF_LANES", "3"))
 _FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "4"))
 _FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
+_FBATCH_GENERIC = os.environ.get("PF_FBATCH_GENERIC", "1") != "0"
 _MEGA = os.environ.get("PF_MEGA", "0") == "1"   # measured slower
 _MEGA_LAG = int(os.environ.get("PF_MEGA_LAG", "2"))
 _MEGA_GP = int(os.environ.get("PF_MEGA_GP", "4"))
@@ -203,8 +204,9 @@ class Propagator:
                       frame_w_ptr, n_frames, dev.ptr(vol), vol_frame_stride, s)
 
     def fbatch_ok(self, n_freq: int, n_frames: int) -> bool:
-        """All frequencies in one launch per stage (small configs, static volume)."""
-        if not self.transposed or n_frames != 1:
+        """All frequencies in one launch per stage (small configs, static volume);
+        register path or, for other pads (config 1's P = 140), the Stockham path."""
+        if n_frames != 1 or (not self.transposed and not _FBATCH_GENERIC):
             return False
         g = self.geom
         per = 8 * ((g.py // 2 + 1) * (g.px // 2 + 1) + g.n_illum * g.ny * g.px)
@@ -223,9 +225,18 @@ class Propagator:
             self._fb_ws_b = torch.empty((nf * nb,), dtype=torch.complex64, device=self.device)
             self._fb_kt = torch.from_numpy(np.asarray(freqs, dtype=np.float64)
                                            / (SPEED_OF_LIGHT * 2 * np.pi)).to(self.device)
+            # rad/m, formed exactly as the per-frequency launches form khat
+            self._fb_kh = torch.tensor([float(f) / SPEED_OF_LIGHT for f in freqs],
+                                       dtype=torch.float64).to(self.device)
             self._fb_strides = (self.nplanes * na, nb)
             self._fb_key = key
         fa, fbs = self._fb_strides
+        if not self.transposed:
+            _lib.call("pf_prop_fbatch_generic", dev.ptr(self.planes_dev), self.nplanes,
+                      dev.ptr(self._fb_kh), nf, ctypes.byref(g), self.plan_x.ref, self.plan_y.ref,
+                      dev.ptr(self._fb_ws_a), fa, dev.ptr(uhat), uhat_fs, dev.ptr(self._fb_ws_b),
+                      fbs, ill_ptr, dev.ptr(frame_w), dev.ptr(vol), dev.stream_ptr(stream))
+            return
         _lib.call("pf_prop_fbatch", dev.ptr(self.planes_dev), self.nplanes, dev.ptr(self._fb_kt),
                   nf, ctypes.byref(g), self.plan_x.ref, dev.ptr(self._fb_ws_a), fa, dev.ptr(uhat),
                   uhat_fs, dev.ptr(self._fb_ws_b), fbs, ill_ptr, dev.ptr(frame_w), dev.ptr(vol),

@@ -3,6 +3,7 @@ goldens + oracle."""
 
 import numpy as np
 import pytest
+import torch
 
 import paper_2501_05244_b200 as pf
 from oracle import pf_oracle as O
@@ -60,6 +61,32 @@ def test_nursd1_c1_like(rng):
     vol = pf.nursd1(sl, grid)
     ref = O.nursd1(sl, grid)
     assert O.rel_l2(vol.field, ref) < TOL
+
+
+@pytest.mark.parametrize("n_ill", [1, 2])
+def test_generic_fbatch_matches_per_frequency(rng, monkeypatch, n_ill):
+    """Frequency-batched Stockham path (pf_prop_fbatch_generic, P = 140) reproduces the
+    per-frequency launches bit for bit, and both match the oracle."""
+    import importlib
+    R = importlib.import_module("paper_2501_05244_b200.reconstruct")
+    from paper_2501_05244_b200.algorithms import Nursd1Engine
+    pts = rng.uniform(-1.0, 1.0, size=(2048, 2))
+    sl = _rand_slices(rng, pf.NonUniformPlanarRelay(pf.PointList(pts), 0.0), n_freq=4,
+                      n_ill=n_ill)
+    p = 2.0 / 64
+    grid = pf.CuboidGrid(pf.UniformGrid3D(64, 64, 5, p, p, 0.3, -1 + p / 2, -1 + p / 2, 0.5))
+    eng = Nursd1Engine(sl, grid)
+    assert not eng.prop.transposed and eng.px == 140
+    coeff = pf.phasor.device_coefficients(sl)
+    assert eng.prop.fbatch_ok(sl.n_freq, 1)
+    batched = eng.run(coeff).clone()
+    monkeypatch.setattr(R, "_FBATCH_GENERIC", False)
+    assert not eng.prop.fbatch_ok(sl.n_freq, 1)
+    per_f = eng.run(coeff)
+    torch.cuda.synchronize()
+    assert torch.equal(batched, per_f)
+    ref = O.nursd1(sl, grid)
+    assert O.rel_l2(batched.cpu().numpy().reshape(ref.shape), ref) < TOL
 
 
 def test_nursd1_on_lattice_register_path(rng):
