@@ -10,8 +10,8 @@ readout (product -> place -> inverse FFT -> interpolate+accumulate).
 from __future__ import annotations
 
 import ctypes
-import os
 import math
+import os
 
 import numpy as np
 import torch
@@ -27,7 +27,8 @@ from .reconstruct import (GraphedRun, PlaneSpec, Propagator, _check_depths, _che
                           _pad_size, _planar_relay, _uniform_relay, _volume, rsd)
 
 C = SPEED_OF_LIGHT
-_BATCH_BYTES = 96 << 20
+_BATCH_BYTES = int(os.environ.get("PF_SRSD_BATCH_MB", "96")) << 20
+_SRSD_MINQ = int(os.environ.get("PF_SRSD_MINQ", "8"))   # plane multiple (x 32/L)
 
 
 def _center_nu0(n: int) -> int:
@@ -149,7 +150,7 @@ class SrsdEngine(GraphedRun):
         per_plane = 8 * (2 * I * py * px + I * g.ny * px)
         batch = max(1, min(len(ks), _BATCH_BYTES // per_plane))
         if self.transposed:
-            q = 8 * (32 // (px // 32))
+            q = _SRSD_MINQ * (32 // (px // 32))
             batch = min(len(ks), max(q, (batch // q) * q))
         self.batch = batch
         for i, k in enumerate(ks):
