@@ -147,6 +147,7 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
   const int nr = min(RPC, ny - i0);
   const float scale = 1.0f / ((float)P * (float)P);
   const long long vol_row0 = (pl.vol_plane * ny + i0) * (long long)nx;
+  const bool aligned = ((g.nu0x | nx) & (L - 1)) == 0;   // column crop uniform per m
   if (PRE) {
     for (int rr = 0; rr < nr; rr++) {
       const float2* src = vol + vol_row0 + (long long)rr * nx;
@@ -187,11 +188,19 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
     const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
     const double dy = yv - sy, dz = pl.z - sz;
     const double byz = fma(dy, dy, dz * dz);
+    // x of output column t + base(m) (aligned crop): x0 - sx + dx * t once per lane
+    const double xt = pl.x0 - sx + pl.dx * t;
 #pragma unroll
     for (int m = 0; m < 32; m++) {
       const int mo = (t + L * m - g.nu0x) & (P - 1);
       float2 val = cscale(v[m], scale);
-      if (g.include_illum && mo < nx) {
+      if (aligned) {
+        const int base = (L * m - g.nu0x) & (P - 1);
+        if (g.include_illum && base < nx) {
+          const double dx = fma(pl.dx, (double)base, xt);
+          val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
+        }
+      } else if (g.include_illum && mo < nx) {
         const double dx = pl.x0 + pl.dx * mo - sx;
         val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
       }
@@ -207,10 +216,20 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
     if (PRE) {
       const float2* old = volbuf + r * nx;
       const float2 fw = frame_w[0];
+      if (aligned) {
+        float2* dt = vol + off + t;
+        const float2* ot = old + t;
 #pragma unroll
-      for (int m = 0; m < 32; m++) {
-        const int mo = (t + L * m - g.nu0x) & (P - 1);
-        if (mo < nx) vol[off + mo] = cadd(old[mo], cmul(MULTI ? acc[m] : v[m], fw));
+        for (int m = 0; m < 32; m++) {
+          const int base = (L * m - g.nu0x) & (P - 1);
+          if (base < nx) dt[base] = cadd(ot[base], cmul(MULTI ? acc[m] : v[m], fw));
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < 32; m++) {
+          const int mo = (t + L * m - g.nu0x) & (P - 1);
+          if (mo < nx) vol[off + mo] = cadd(old[mo], cmul(MULTI ? acc[m] : v[m], fw));
+        }
       }
     } else {
       // frames innermost: each element's offset is formed once and reused for every

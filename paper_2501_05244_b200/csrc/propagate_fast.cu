@@ -93,6 +93,8 @@ k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
   const float2* grow = ws_a + ((long long)bb * NA + kx) * NA;
   const int ny = g.ny;
   const int n_ill = MULTI ? g.n_illum : 1;
+  // crop offset and height multiples of L: row i = t + base(m), kept iff base(m) < ny
+  const bool aligned = ((g.nu0y | ny) & (L - 1)) == 0;
 #pragma unroll 1
   for (int p = 0; p < n_ill; p++) {
     const float2* ucol = uhat_t + pl.uhat_off + (long long)p * g.uhat_illum_stride +
@@ -106,10 +108,19 @@ k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
     wfft<L, 1>(w, sm + warp * WFFT_XCH, tw);
     if (active) {
       float2* dcol = ws_b + ((long long)bb * g.n_illum + p) * (long long)P * ny + (long long)col * ny;
+      if (aligned) {   // crop decided per m for the whole warp: no per-lane index math
+        float2* dt = dcol + t;
 #pragma unroll
-      for (int m = 0; m < 32; m++) {
-        const int i = (t + L * m - g.nu0y) & (P - 1);
-        if (i < ny) dcol[i] = w[m];
+        for (int m = 0; m < 32; m++) {
+          const int base = (L * m - g.nu0y) & (P - 1);
+          if (base < ny) dt[base] = w[m];
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < 32; m++) {
+          const int i = (t + L * m - g.nu0y) & (P - 1);
+          if (i < ny) dcol[i] = w[m];
+        }
       }
     }
   }
