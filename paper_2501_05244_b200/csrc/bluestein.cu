@@ -126,13 +126,27 @@ k_bluestein_w(const float2* __restrict__ src, long long src_ps, long long src_ls
   const float2* kh = khat + (long long)b * Q;
   const float2* s = src + b * src_ps + (long long)(active ? l : 0) * src_ls;
   float2 v[32];
+  // input window and output length on lane-multiple boundaries (the SRSD pads):
+  // element m is inside or outside for the whole warp
+  const bool aligned = ((o_in | n_in | M) & (L - 1)) == 0;
+  if (aligned) {
+    const float2* st = s + t - o_in;
+    const float2* ct = ch + t;
 #pragma unroll
-  for (int m = 0; m < 32; m++) {
-    const int q = t + L * m;
-    const int i = q - o_in;
-    float2 x = make_float2(0.f, 0.f);
-    if (q < M && i >= 0 && i < n_in) x = cmul(__ldg(s + i), __ldg(ch + q));
-    v[m] = x;
+    for (int m = 0; m < 32; m++) {
+      const int base = L * m;
+      v[m] = (base < M && base >= o_in && base < o_in + n_in)
+                 ? cmul(__ldg(st + base), __ldg(ct + base)) : make_float2(0.f, 0.f);
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < 32; m++) {
+      const int q = t + L * m;
+      const int i = q - o_in;
+      float2 x = make_float2(0.f, 0.f);
+      if (q < M && i >= 0 && i < n_in) x = cmul(__ldg(s + i), __ldg(ch + q));
+      v[m] = x;
+    }
   }
   float2* xch = sm + warp * WFFT_XCH;
   wfft<L, -1>(v, xch, tw);
@@ -152,16 +166,29 @@ k_bluestein_w(const float2* __restrict__ src, long long src_ps, long long src_ls
     __syncthreads();
     const int nl = min(LPC, nlines - l0);
     float2* d = dst + b * dst_ps + l0;
+    const bool pow2 = (M & (M - 1)) == 0;   // natural(k - M/2) = k ^ M/2
     for (int e = threadIdx.x; e < M * LPC; e += 256) {
       const int k = e / LPC, rr = e % LPC;
-      if (rr < nl) d[(long long)natural((long long)k - M / 2, M) * dst_ls + rr] = sm[k * SLD + rr];
+      const int kn = pow2 ? (k ^ (M >> 1)) : natural((long long)k - M / 2, M);
+      if (rr < nl) d[(long long)kn * dst_ls + rr] = sm[k * SLD + rr];
     }
   } else if (active) {
     float2* d = dst + b * dst_ps + (long long)l * dst_ls;
+    if (aligned && (M & (M - 1)) == 0) {
+      // k = t + L m < M: natural(k - M/2) = k ^ M/2 = t + (L m ^ M/2)
+      float2* dt = d + t;
+      const float2* ct = ch + t;
 #pragma unroll
-    for (int m = 0; m < 32; m++) {
-      const int k = t + L * m;
-      if (k < M) d[natural((long long)k - M / 2, M)] = cscale(cmul(v[m], __ldg(ch + k)), inv_q);
+      for (int m = 0; m < 32; m++) {
+        const int base = L * m;
+        if (base < M) dt[base ^ (M >> 1)] = cscale(cmul(v[m], __ldg(ct + base)), inv_q);
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < 32; m++) {
+        const int k = t + L * m;
+        if (k < M) d[natural((long long)k - M / 2, M)] = cscale(cmul(v[m], __ldg(ch + k)), inv_q);
+      }
     }
   }
 }

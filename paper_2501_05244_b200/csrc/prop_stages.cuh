@@ -26,9 +26,11 @@ __device__ __forceinline__ void st_a(float2* sm, const pf_plane& pl, double ktur
   const double ly = (double)jy * pl.lag_dy;
   const double base = fma(ly, ly, pl.dz * pl.dz);
   float2 v[32];
+  const double lx_t = (double)t * pl.lag_dx;
 #pragma unroll
   for (int m = 0; m <= 16; m++) {
-    const double lx = (double)centred(t + L * m, P) * pl.lag_dx;
+    // lag of centred(t + L m, P): t + L m below P/2 for m < 16, t - P/2 at m = 16
+    const double lx = fma((double)(m < 16 ? L * m : -H), pl.lag_dx, lx_t);
     v[m] = g_kernel(fma(lx, lx, base), kturns, (float)kturns);
   }
   const int mirror = (lane - t) + ((L - t) & (L - 1));
@@ -77,7 +79,7 @@ __device__ __forceinline__ void st_b1(float2* sm, const float2* __restrict__ tw,
 #pragma unroll
   for (int m = 0; m < 32; m++) {
     const int jy = t + L * m;
-    v[m] = arow[jy <= H ? jy : P - jy];
+    v[m] = m < 16 ? arow[jy] : arow[P - jy];   // jy <= P/2 iff m < 16 (or m = 16, t = 0)
   }
   wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
   if (active) {
@@ -114,7 +116,7 @@ __device__ __forceinline__ void st_b2(float2* sm, const pf_plane& pl, const pf_p
 #pragma unroll
     for (int m = 0; m < 32; m++) {
       const int ky = t + L * m;
-      w[m] = cmul(grow[ky <= H ? ky : P - ky], __ldg(ucol + ky));
+      w[m] = cmul(m < 16 ? grow[ky] : grow[P - ky], __ldg(ucol + ky));
     }
     wfft<L, 1>(w, sm + warp * WFFT_XCH, tw);
     if (active) {

@@ -103,7 +103,9 @@ k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
 #pragma unroll
     for (int m = 0; m < 32; m++) {
       const int ky = t + L * m;
-      w[m] = cmul(__ldg(grow + (ky <= H ? ky : P - ky)), __ldg(ucol + ky));
+      // mirrored row: ky <= P/2 exactly for m < 16 (m = 16 only at t = 0, where
+      // P - ky = ky), so the index form is fixed per unrolled m
+      w[m] = cmul(__ldg(m < 16 ? grow + ky : grow + (P - ky)), __ldg(ucol + ky));
     }
     wfft<L, 1>(w, sm + warp * WFFT_XCH, tw);
     if (active) {
