@@ -38,6 +38,12 @@ __device__ __forceinline__ float2 expi_reduced(double phase) {
 __device__ __forceinline__ int centred(int j, int n) { return j < n - n / 2 ? j : j - n; }
 // natural slot of centred index c (any integer) on a length-n axis
 __device__ __forceinline__ int natural(long long c, int n) {
+  if (c >= -(long long)n && c < 2LL * n) {   // every hot call site: no 64-bit division
+    int m = (int)c;
+    m += m < 0 ? n : 0;
+    m -= m >= n ? n : 0;
+    return m;
+  }
   long long m = c % n;
   return (int)(m < 0 ? m + n : m);
 }

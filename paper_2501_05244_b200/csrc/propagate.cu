@@ -53,8 +53,9 @@ k_prop_kernel_rows(const pf_plane* __restrict__ planes, double khat, pf_prop_geo
   const int nr = min(rows_per_cta, rows_a - r0);
   float2* a = sm;
   float2* b = sm + (size_t)rows_per_cta * ld;
+  const FastDiv dpx(px), dca(cols_a);
   for (int e = threadIdx.x; e < nr * px; e += PT) {
-    const int c = e / px, jx = e - c * px;
+    const int c = dpx.div(e), jx = e - c * px;
     const double lx = (double)centred(jx, px) * pl.lag_dx;
     const double ly = (double)(r0 + c) * pl.lag_dy;
     a[c * ld + jx] = rsd_kernel(khat, lx, ly, pl.dz);
@@ -63,7 +64,7 @@ k_prop_kernel_rows(const pf_plane* __restrict__ planes, double khat, pf_prop_geo
   const float2* res = fft_smem<-1>(a, b, ld, nr, plan_x);
   float2* dst = ws_a + ((long long)blockIdx.y * rows_a + r0) * cols_a;
   for (int e = threadIdx.x; e < nr * cols_a; e += PT) {
-    const int c = e / cols_a, kx = e - c * cols_a;
+    const int c = dca.div(e), kx = e - c * cols_a;
     dst[(long long)c * cols_a + kx] = res[c * ld + kx];
   }
 }
@@ -90,8 +91,9 @@ k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan 
   float2* buf1 = sm + (size_t)C * ld;
   float2* buf2 = sm + (size_t)2 * C * ld;
   const float2* src = ws_a + (long long)blockIdx.y * rows_a * cols_a + k0;
+  const FastDiv dnc(nc);
   for (int e = threadIdx.x; e < nc * py; e += PT) {
-    const int jy = e / nc, c = e - jy * nc;
+    const int jy = dnc.div(e), c = e - jy * nc;
     const int sy = jy < rows_a ? jy : py - jy;
     buf0[c * ld + jy] = src[(long long)sy * cols_a + c];
   }
@@ -106,18 +108,18 @@ k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan 
     for (int side = 0; side < 2; side++) {
       // column handled by slot c on this side; mirrors that coincide are skipped
       for (int e = threadIdx.x; e < nc * py; e += PT) {
-        const int jy = e / nc, c = e - jy * nc;
+        const int jy = dnc.div(e), c = e - jy * nc;
         const int kx = k0 + c;
-        const int col = side == 0 ? kx : (px - kx) % px;
+        const int col = (side == 0 || kx == 0) ? kx : px - kx;
         w0[c * ld + jy] = cmul(gh[c * ld + jy], u[(long long)jy * px + col]);
       }
       __syncthreads();
       if (product_only) {   // full spectrum column for a type-2 readout: [plane][p][py][px]
         float2* sp = ws_b + ((long long)blockIdx.y * g.n_illum + p) * (long long)py * px;
         for (int e = threadIdx.x; e < nc * py; e += PT) {
-          const int jy = e / nc, c = e - jy * nc;
+          const int jy = dnc.div(e), c = e - jy * nc;
           const int kx = k0 + c;
-          const int col = side == 0 ? kx : (px - kx) % px;
+          const int col = (side == 0 || kx == 0) ? kx : px - kx;
           if (side == 1 && col == kx) continue;
           sp[(long long)jy * px + col] = w0[c * ld + jy];
         }
@@ -126,9 +128,9 @@ k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan 
       }
       const float2* res = fft_smem<1>(w0, w1, ld, nc, plan_y);
       for (int e = threadIdx.x; e < nc * ny; e += PT) {
-        const int i = e / nc, c = e - i * nc;
+        const int i = dnc.div(e), c = e - i * nc;
         const int kx = k0 + c;
-        const int col = side == 0 ? kx : (px - kx) % px;
+        const int col = (side == 0 || kx == 0) ? kx : px - kx;
         if (side == 1 && col == kx) continue;
         const int jy = natural((long long)g.nu0y + i, py);
         outp[(long long)i * px + col] = res[c * ld + jy];
@@ -153,17 +155,18 @@ k_prop_rows_out(const pf_plane* __restrict__ planes, double khat, pf_prop_geom g
   float2* a = sm;
   float2* b = sm + (size_t)rows_per_cta * ld;
   const float scale = 1.0f / ((float)g.px * (float)g.py);
+  const FastDiv dpx(px), dnx(nx);
   for (int p = 0; p < g.n_illum; p++) {
     const float2* src = ws_b + (((long long)blockIdx.y * g.n_illum + p) * ny + i0) * (long long)px;
     for (int e = threadIdx.x; e < nr * px; e += PT) {
-      const int c = e / px, jx = e - c * px;
+      const int c = dpx.div(e), jx = e - c * px;
       a[c * ld + jx] = src[(long long)c * px + jx];
     }
     __syncthreads();
     const float2* res = fft_smem<1>(a, b, ld, nr, plan_x);
     const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
     for (int e = threadIdx.x; e < nr * nx; e += PT) {
-      const int c = e / nx, m = e - c * nx;
+      const int c = dnx.div(e), m = e - c * nx;
       float2 v = cscale(res[c * ld + natural((long long)g.nu0x + m, px)], scale);
       if (g.include_illum) {
         const double dx = pl.x0 + pl.dx * m - sx;
@@ -201,6 +204,7 @@ k_prop_rows_out_fb(const pf_plane* __restrict__ planes, const double* __restrict
   float2* acc = sm + (size_t)2 * rows_per_cta * ld;   // [nr][nx]
   for (int e = threadIdx.x; e < nr * nx; e += PT) acc[e] = make_float2(0.f, 0.f);
   const float scale = 1.0f / ((float)g.px * (float)g.py);
+  const FastDiv dpx(px), dnx(nx);
   for (int f = 0; f < nf; f++) {
     const double khat = khat_f[f];
     const float2 fw = frame_w[f];
@@ -208,14 +212,14 @@ k_prop_rows_out_fb(const pf_plane* __restrict__ planes, const double* __restrict
       const float2* src = ws_b + f * ws_b_fs +
                           (((long long)blockIdx.y * g.n_illum + p) * ny + i0) * (long long)px;
       for (int e = threadIdx.x; e < nr * px; e += PT) {
-        const int c = e / px, jx = e - c * px;
+        const int c = dpx.div(e), jx = e - c * px;
         a[c * ld + jx] = src[(long long)c * px + jx];
       }
       __syncthreads();
       const float2* res = fft_smem<1>(a, b, ld, nr, plan_x);
       const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
       for (int e = threadIdx.x; e < nr * nx; e += PT) {
-        const int c = e / nx, m = e - c * nx;
+        const int c = dnx.div(e), m = e - c * nx;
         float2 v = cscale(res[c * ld + natural((long long)g.nu0x + m, px)], scale);
         if (g.include_illum) {
           const double dx = pl.x0 + pl.dx * m - sx;
@@ -229,7 +233,7 @@ k_prop_rows_out_fb(const pf_plane* __restrict__ planes, const double* __restrict
     }
   }
   for (int e = threadIdx.x; e < nr * nx; e += PT) {
-    const int c = e / nx, m = e - c * nx;
+    const int c = dnx.div(e), m = e - c * nx;
     float2* d = vol + (pl.vol_plane * ny + i0 + c) * (long long)nx + m;
     *d = cadd(*d, acc[e]);
   }

@@ -138,7 +138,8 @@ template <int L, bool MULTI, int NW = 8>
 __global__ void __launch_bounds__(32 * NW, 1)
 k_pcf(const pf_plane* __restrict__ planes, pf_prop_geom g, const float2* __restrict__ tw,
       const float2* __restrict__ ws_b, const double* __restrict__ ill,
-      const float2* __restrict__ frame_w, float2* __restrict__ vol, FBatch fb) {
+      const float2* __restrict__ frame_w, float2* __restrict__ vol, FBatch fb,
+      float2* __restrict__ part) {
   constexpr int P = 32 * L;
   constexpr int LPW = 32 / L, RPC = NW * LPW, SLD = RPC + 1, TILE = P * SLD;
   extern __shared__ float2 sm[];
@@ -154,9 +155,12 @@ k_pcf(const pf_plane* __restrict__ planes, pf_prop_geom g, const float2* __restr
   const float scale = 1.0f / ((float)P * (float)P);
   const double yv = pl.y0 + pl.dy * i;
   const int n_ill = MULTI ? g.n_illum : 1;
-  const int n_tiles = fb.nf * n_ill;
+  // frequency group blockIdx.z of gridDim.z (part != nullptr: partial sums)
+  const int f_lo = (int)((long long)blockIdx.z * fb.nf / gridDim.z);
+  const int f_hi = (int)((long long)(blockIdx.z + 1) * fb.nf / gridDim.z);
+  const int n_tiles = (f_hi - f_lo) * n_ill;
   auto load_tile = [&](int idx, float2* dst) {
-    const int f = idx / n_ill, p = idx - f * n_ill;
+    const int f = f_lo + idx / n_ill, p = idx % n_ill;
     const float2* src = ws_b + f * fb.ws_b_fs +
                         ((long long)blockIdx.y * g.n_illum + p) * (long long)P * ny + i0;
     constexpr int CSTEP = 32 * NW / RPC;
@@ -179,7 +183,7 @@ k_pcf(const pf_plane* __restrict__ planes, pf_prop_geom g, const float2* __restr
   load_tile(0, sm);
 #pragma unroll 1
   for (int idx = 0; idx < n_tiles; idx++) {
-    const int f = idx / n_ill, p = idx - f * n_ill;
+    const int f = f_lo + idx / n_ill, p = idx % n_ill;
     float2* cur = sm + (idx & 1) * TILE;
     if (idx + 1 < n_tiles) {
       load_tile(idx + 1, sm + ((idx + 1) & 1) * TILE);
@@ -210,12 +214,36 @@ k_pcf(const pf_plane* __restrict__ planes, pf_prop_geom g, const float2* __restr
     }
   }
   if (i < ny) {
+    if (part) {
+      float2* prow = part + (((long long)blockIdx.z * gridDim.y + blockIdx.y) * ny + i) * nx;
+#pragma unroll
+      for (int m = 0; m < 32; m++) {
+        const int mo = (t + L * m - g.nu0x) & (P - 1);
+        if (mo < nx) prow[mo] = acc[m];
+      }
+      return;
+    }
     float2* drow = vol + (pl.vol_plane * ny + i) * (long long)nx;
 #pragma unroll
     for (int m = 0; m < 32; m++) {
       const int mo = (t + L * m - g.nu0x) & (P - 1);
       if (mo < nx) drow[mo] = cadd(drow[mo], acc[m]);
     }
+  }
+}
+
+// vol[plane] += sum over groups z (ascending) of part[z][plane]
+__global__ void k_pcf_sum(const pf_plane* __restrict__ planes, int nplanes, int ny, int nx,
+                          const float2* __restrict__ part, int groups, float2* __restrict__ vol) {
+  const long long per = (long long)ny * nx, total = per * nplanes;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(e / per);
+    const long long o = e - b * per;
+    float2 s = part[e];
+    for (int z = 1; z < groups; z++) s = cadd(s, part[z * total + e]);
+    float2* d = vol + planes[b].vol_plane * per + o;
+    *d = cadd(*d, s);
   }
 }
 
@@ -284,19 +312,35 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     const bool narrow = (long long)pf_cdiv(g.ny, RPC) * nplanes < 2LL * pf_sm_count();
     if (narrow) {
       constexpr int RPC2 = 2 * (32 / L);
-      dim3 grid(pf_cdiv(g.ny, RPC2), nplanes);
+      // few (plane, row tile) CTAs: split the frequencies into groups whose partial
+      // sums go to the (now free) kernel-spectrum workspace, then add them in order
+      const long long ctas = (long long)pf_cdiv(g.ny, RPC2) * nplanes;
+      int groups = (int)((8LL * pf_sm_count() + ctas - 1) / ctas);
+      if (groups > fb.nf) groups = fb.nf;
+      if (groups > 8) groups = 8;
+      const long long need = (long long)groups * nplanes * g.ny * g.nx;
+      if (groups < 2 || need > (long long)fb.nf * fb.ws_a_fs) groups = 1;
+      float2* part = groups > 1 ? const_cast<float2*>(ws_a) : nullptr;
+      dim3 grid(pf_cdiv(g.ny, RPC2), nplanes, groups);
       const size_t sm = smem_cf<L, 2>();
       if (g.n_illum > 1)
-        k_pcf<L, true, 2><<<grid, 64, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+        k_pcf<L, true, 2><<<grid, 64, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb, part);
       else
-        k_pcf<L, false, 2><<<grid, 64, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+        k_pcf<L, false, 2><<<grid, 64, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb, part);
+      PF_LAUNCH_CHECK("k_pcf");
+      if (part) {
+        const long long total = (long long)nplanes * g.ny * g.nx;
+        const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+        k_pcf_sum<<<blocks, 256, 0, st>>>(planes, nplanes, g.ny, g.nx, part, groups, vol);
+        PF_LAUNCH_CHECK("k_pcf_sum");
+      }
     } else {
       dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
       const size_t sm = smem_cf<L>();
       if (g.n_illum > 1)
-        k_pcf<L, true><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+        k_pcf<L, true><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb, nullptr);
       else
-        k_pcf<L, false><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb);
+        k_pcf<L, false><<<grid, FT, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb, nullptr);
     }
     PF_LAUNCH_CHECK("k_pcf");
   } else {   // C: x-IFFT, crop, illumination phase, volume accumulate
