@@ -130,7 +130,13 @@ __device__ __forceinline__ void st_b2(float2* sm, const pf_plane& pl, const pf_p
   }
 }
 
-template <int L, bool MULTI, bool PRE>
+// Centred crop (the output lattice is the relay lattice: n = P/2, nu0 = -n/2): the
+// kept outputs of lane t are t + L ((m + 8) mod 32) for m in [0, 8) and [24, 32),
+// known at compile time, so the crop and its addresses need no per-element tests.
+__host__ __device__ constexpr bool cent_keep(int m) { return ((m + 8) & 31) < 16; }
+__host__ __device__ constexpr int cent_base(int m) { return (m + 8) & 31; }
+
+template <int L, bool MULTI, bool PRE, bool CENT = false>
 __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double kturns,
                                      const pf_prop_geom& g, const float2* __restrict__ tw,
                                      const float2* __restrict__ wb, const double* __restrict__ ill,
@@ -192,6 +198,22 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
     const double byz = fma(dy, dy, dz * dz);
     // x of output column t + base(m) (aligned crop): x0 - sx + dx * t once per lane
     const double xt = pl.x0 - sx + pl.dx * t;
+    if (CENT && g.include_illum) {
+#pragma unroll
+      for (int m = 0; m < 32; m++) {
+        float2 val = cscale(v[m], scale);
+        if (cent_keep(m)) {
+          const double dx = fma(pl.dx, (double)(L * cent_base(m)), xt);
+          val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
+        }
+        if (MULTI) {
+          if (p == 0) acc[m] = val; else acc[m] = cadd(acc[m], val);
+        } else {
+          v[m] = val;
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int m = 0; m < 32; m++) {
       const int mo = (t + L * m - g.nu0x) & (P - 1);
@@ -218,7 +240,17 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
     if (PRE) {
       const float2* old = volbuf + r * nx;
       const float2 fw = frame_w[0];
-      if (aligned) {
+      if (CENT) {
+        float2* dt = vol + off + t;
+        const float2* ot = old + t;
+#pragma unroll
+        for (int m = 0; m < 32; m++) {
+          if (cent_keep(m)) {
+            const int base = L * cent_base(m);
+            dt[base] = cadd(ot[base], cmul(MULTI ? acc[m] : v[m], fw));
+          }
+        }
+      } else if (aligned) {
         float2* dt = vol + off + t;
         const float2* ot = old + t;
 #pragma unroll

@@ -46,7 +46,7 @@ k_pa(const pf_plane* __restrict__ planes, double kturns_s, pf_prop_geom g,
 // C for every plane of a batch (blockIdx.y).  MULTI: more than one illumination
 // (summed in registers first).  PRE: single frame, the CTA's volume rows prefetched
 // with cp.async at entry so the accumulate is load-free at the end.
-template <int L, bool MULTI, bool PRE>
+template <int L, bool MULTI, bool PRE, bool CENT>
 __global__ void __launch_bounds__(FT, MULTI ? 1 : 2)
 k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
      const float2* __restrict__ tw, const float2* __restrict__ ws_b,
@@ -54,7 +54,7 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
      float2* __restrict__ vol, long long vol_frame_stride) {
   extern __shared__ float2 sm[];
   const long long wb_plane = (long long)g.n_illum * 32 * L * g.ny;
-  st_c<L, MULTI, PRE>(sm, planes[blockIdx.y], kturns, g, tw, ws_b + blockIdx.y * wb_plane, ill,
+  st_c<L, MULTI, PRE, CENT>(sm, planes[blockIdx.y], kturns, g, tw, ws_b + blockIdx.y * wb_plane, ill,
                       frame_w, n_frames, vol, vol_frame_stride, blockIdx.x);
 }
 
@@ -70,7 +70,7 @@ k_pb1(int nplanes, const float2* __restrict__ tw, float2* __restrict__ ws_a, FBa
   st_b1<L>(sm, tw, ws_a + blockIdx.z * fb.ws_a_fs + (long long)blockIdx.y * NA * NA, blockIdx.x);
 }
 
-template <int L, bool MULTI>
+template <int L, bool MULTI, bool CENT>
 __global__ void __launch_bounds__(FT, 2)
 k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
       const float2* __restrict__ tw, const float2* __restrict__ ws_a,
@@ -110,7 +110,12 @@ k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
     wfft<L, 1>(w, sm + warp * WFFT_XCH, tw);
     if (active) {
       float2* dcol = ws_b + ((long long)bb * g.n_illum + p) * (long long)P * ny + (long long)col * ny;
-      if (aligned) {   // crop decided per m for the whole warp: no per-lane index math
+      if (CENT) {      // centred crop: kept rows t + L ((m + 8) mod 32), compile time
+        float2* dt = dcol + t;
+#pragma unroll
+        for (int m = 0; m < 32; m++)
+          if (cent_keep(m)) dt[L * cent_base(m)] = w[m];
+      } else if (aligned) {   // crop decided per m for the whole warp: no per-lane index math
         float2* dt = dcol + t;
 #pragma unroll
         for (int m = 0; m < 32; m++) {
@@ -278,12 +283,17 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     const int big = 200 * 1024;
     cudaFuncSetAttribute(k_pa<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_pb1<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_pb2<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_pb2<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_pc<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_pc<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_pc<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_pc<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb2<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb2<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb2<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb2<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+#define PF_PC_ATTR(M, PR, C) \
+    cudaFuncSetAttribute(k_pc<L, M, PR, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    PF_PC_ATTR(false, false, false) PF_PC_ATTR(true, false, false)
+    PF_PC_ATTR(false, true, false) PF_PC_ATTR(true, true, false)
+    PF_PC_ATTR(false, false, true) PF_PC_ATTR(true, false, true)
+    PF_PC_ATTR(false, true, true) PF_PC_ATTR(true, true, true)
+#undef PF_PC_ATTR
     const int most = 227 * 1024;   // k_pcf at P = 1024 with 8 warps: 215 KB
     cudaFuncSetAttribute(k_pcf<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
     cudaFuncSetAttribute(k_pcf<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
@@ -302,10 +312,15 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     k_pb1<L><<<g1, FT, sm, st>>>(nplanes, tw, const_cast<float2*>(ws_a), fb);
     PF_LAUNCH_CHECK("k_pb1");
     dim3 g2(NA, pf_cdiv(2 * nplanes, 8 * LPW), fb.nf);
-    if (g.n_illum > 1)
-      k_pb2<L, true><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
-    else
-      k_pb2<L, false><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
+    // centred row crop (output lattice = relay lattice): compile-time kept rows
+    const bool cent_y = 2 * g.ny == 32 * L && 2 * g.nu0y == -g.ny;
+    if (g.n_illum > 1) {
+      if (cent_y) k_pb2<L, true, true><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
+      else k_pb2<L, true, false><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
+    } else {
+      if (cent_y) k_pb2<L, false, true><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
+      else k_pb2<L, false, false><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
+    }
     PF_LAUNCH_CHECK("k_pb2");
   } else if (fb.kturns != nullptr) {   // C over all frequencies of the batch
     // 8 warps per CTA unless that leaves fewer than two CTAs per SM; then 2
@@ -347,13 +362,22 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     dim3 grid(pf_cdiv(g.ny, RPC), nplanes);
     const bool pre = n_frames == 1 && frame_w != nullptr && (size_t)RPC * g.nx * 8 <= 64 * 1024;
     const size_t sm = smem_c<L>(g.nx, pre);
+    // centred column crop: compile-time kept columns
+    const bool cent_x = 2 * g.nx == 32 * L && 2 * g.nu0x == -g.nx;
+#define PF_PC_LAUNCH(M)                                                                        \
+  if (pre) {                                                                                   \
+    if (cent_x) k_pc<L, M, true, true><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs); \
+    else k_pc<L, M, true, false><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs); \
+  } else {                                                                                     \
+    if (cent_x) k_pc<L, M, false, true><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs); \
+    else k_pc<L, M, false, false><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs); \
+  }
     if (g.n_illum > 1) {
-      if (pre) k_pc<L, true, true><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
-      else k_pc<L, true, false><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
+      PF_PC_LAUNCH(true)
     } else {
-      if (pre) k_pc<L, false, true><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
-      else k_pc<L, false, false><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs);
+      PF_PC_LAUNCH(false)
     }
+#undef PF_PC_LAUNCH
     PF_LAUNCH_CHECK("k_pc");
   }
   return 0;
