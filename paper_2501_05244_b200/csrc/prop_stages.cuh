@@ -44,9 +44,9 @@ __device__ __forceinline__ void st_a(float2* sm, const pf_plane& pl, double ktur
   __syncthreads();
   if (jy <= H) {
 #pragma unroll
-    for (int m = 0; m < 32; m++) {
-      const int kx = t + L * m;
-      if (kx <= H) sm[kx * SLD + r] = v[m];
+    for (int m = 0; m <= 16; m++) {
+      // kx = t + L m <= P/2: every m < 16, and m = 16 at t = 0 only
+      if (m < 16 || t == 0) sm[(t + L * m) * SLD + r] = v[m];
     }
   }
   __syncthreads();
@@ -85,8 +85,7 @@ __device__ __forceinline__ void st_b1(float2* sm, const float2* __restrict__ tw,
   if (active) {
 #pragma unroll
     for (int m = 0; m <= 16; m++) {
-      const int ky = t + L * m;
-      if (ky <= H) arow[ky] = v[m];
+      if (m < 16 || t == 0) arow[t + L * m] = v[m];   // ky <= P/2
     }
   }
 }
@@ -149,14 +148,20 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = lane % L, line = lane / L;
   const int r = warp * LPW + line;
-  const int ny = g.ny, nx = g.nx;
+  // CENT: both crops centred, so ny = nx = P/2 at compile time (RPC divides P/2)
+  const int ny = CENT ? P / 2 : g.ny, nx = CENT ? P / 2 : g.nx;
   const int i0 = tile * RPC;
   const int i = i0 + r;
-  const int nr = min(RPC, ny - i0);
+  const int nr = CENT ? RPC : min(RPC, ny - i0);
   const float scale = 1.0f / ((float)P * (float)P);
   const long long vol_row0 = (pl.vol_plane * ny + i0) * (long long)nx;
   const bool aligned = ((g.nu0x | nx) & (L - 1)) == 0;   // column crop uniform per m
-  if (PRE) {
+  if (PRE && CENT) {
+    const float2* src = vol + vol_row0;
+#pragma unroll
+    for (int e = threadIdx.x; e < RPC * (P / 2); e += PROP_MT) cp_async8(volbuf + e, src + e);
+    cp_async_commit();
+  } else if (PRE) {
     for (int rr = 0; rr < nr; rr++) {
       const float2* src = vol + vol_row0 + (long long)rr * nx;
 #pragma unroll 4
@@ -175,7 +180,12 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
     {
       constexpr int CSTEP = PROP_MT / RPC;
       const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
-      if (rr < nr) {
+      if (CENT) {   // compile-time strides: every copy is base + immediate offset
+        const float2* q = src + c0 * (P / 2) + rr;
+        float2* d = sm + c0 * SLD + rr;
+#pragma unroll
+        for (int k = 0; k < P / CSTEP; k++) cp_async8(d + k * CSTEP * SLD, q + k * CSTEP * (P / 2));
+      } else if (rr < nr) {
         const float2* q = src + (long long)c0 * ny + rr;
         float2* d = sm + c0 * SLD + rr;
 #pragma unroll 8

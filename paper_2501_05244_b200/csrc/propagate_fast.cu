@@ -363,7 +363,8 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     const bool pre = n_frames == 1 && frame_w != nullptr && (size_t)RPC * g.nx * 8 <= 64 * 1024;
     const size_t sm = smem_c<L>(g.nx, pre);
     // centred column crop: compile-time kept columns
-    const bool cent_x = 2 * g.nx == 32 * L && 2 * g.nu0x == -g.nx;
+    const bool cent_x = 2 * g.nx == 32 * L && 2 * g.nu0x == -g.nx &&
+                        2 * g.ny == 32 * L && 2 * g.nu0y == -g.ny;   // both crops centred
 #define PF_PC_LAUNCH(M)                                                                        \
   if (pre) {                                                                                   \
     if (cent_x) k_pc<L, M, true, true><<<grid, FT, sm, st>>>(planes, kturns, g, tw, ws_b, ill, frame_w, n_frames, vol, vfs); \
