@@ -211,7 +211,7 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
     if (CENT && g.include_illum) {
 #pragma unroll
       for (int m = 0; m < 32; m++) {
-        float2 val = cscale(v[m], scale);
+        float2 val = v[m];   // 1/P^2 (a power of two: exact) is folded into the frame weight
         if (cent_keep(m)) {
           const double dx = fma(pl.dx, (double)(L * cent_base(m)), xt);
           val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
@@ -227,7 +227,7 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
 #pragma unroll
     for (int m = 0; m < 32; m++) {
       const int mo = (t + L * m - g.nu0x) & (P - 1);
-      float2 val = cscale(v[m], scale);
+      float2 val = v[m];   // 1/P^2 (a power of two: exact) is folded into the frame weight
       if (aligned) {
         const int base = (L * m - g.nu0x) & (P - 1);
         if (g.include_illum && base < nx) {
@@ -249,7 +249,7 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
     const long long off = vol_row0 + (long long)r * nx;
     if (PRE) {
       const float2* old = volbuf + r * nx;
-      const float2 fw = frame_w[0];
+      const float2 fw = cscale(frame_w[0], scale);
       if (CENT) {
         float2* dt = vol + off + t;
         const float2* ot = old + t;
@@ -287,7 +287,7 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
 #pragma unroll 1
           for (int fr = 0; fr < n_frames; fr++) {
             float2* q = d + fr * vfs;
-            *q = cadd(*q, cmul(val, __ldg(frame_w + fr)));
+            *q = cadd(*q, cmul(val, cscale(__ldg(frame_w + fr), scale)));
           }
         }
       }
