@@ -26,12 +26,11 @@ constexpr int K1_KB = 33;    // non-redundant bins of a real 64-point DFT
 // 64-point real DFT of x[0..63]: the non-redundant bins k in [0, 32] selected by
 // `mask` (bit k; warp-uniform) are stored to dst[0], dst[1], ... in ascending k.
 __device__ __forceinline__ void real_dft64_sel(const float* x, unsigned long long mask,
-                                               float2* dst) {
+                                               float2* dst, int stride = 1) {
   float2 z[32];
 #pragma unroll
   for (int q = 0; q < 32; q++) z[q] = make_float2(x[2 * q], x[2 * q + 1]);
   Dft<32, -1>::run(z);
-  int s = 0;
 #pragma unroll
   for (int k = 0; k <= 32; k++) {
     if ((mask >> k) & 1ull) {
@@ -42,7 +41,8 @@ __device__ __forceinline__ void real_dft64_sel(const float* x, unsigned long lon
       const float2 o = make_float2(0.5f * (a.y - b.y), -0.5f * (a.x - b.x));
       // W_64^k = exp(-2 pi i k / 64)
       const float c = Unit<64>::c(k & 63), sn = -Unit<64>::s(k & 63);
-      dst[s++] = make_float2(e.x + o.x * c - o.y * sn, e.y + o.x * sn + o.y * c);
+      *dst = make_float2(e.x + o.x * c - o.y * sn, e.y + o.x * sn + o.y * c);
+      dst += stride;
     }
   }
 }
@@ -53,34 +53,43 @@ __device__ __forceinline__ void real_dft64(const float* x, float2* X) {
 }
 
 // Only the inner bins k = b mod 64 the retained bins need are formed and
-// parked (config 4: 20 of the 33 non-redundant bins): the split step, the
-// shared-memory stores and the per-trace stride shrink accordingly.
+// parked (config 4: 20 of the 33 non-redundant bins), slot-major with the
+// column index r fastest: xs[g][slot][r] (row stride MP).  Phase B gives each
+// retained bin two threads (even / odd r, combined by one shuffle); the bins
+// that fold to 64 - k read conjugated twiddles and conjugate the sum instead
+// of every term.  Strides MP = M + 2 and TS = 4 (mod 16) keep the parking
+// stores and the phase-B loads free of shared-memory bank conflicts.
 template <int M>
 __global__ void __launch_bounds__(K1_THREADS)
 k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __restrict__ bins,
                const float2* __restrict__ twt /*[M][twt_ld]*/, int twt_ld,
                const float2* __restrict__ wphase, int F, float2* __restrict__ out,
-               long long out_stride, int nkp_cap) {
+               long long out_stride, int ts_cap) {
   constexpr int G = K1_THREADS / M;          // traces per block pass
   constexpr int T = M * K1_L;
+  constexpr int MP = M + 2 - (M & 1);
   extern __shared__ float2 smem[];
-  float2* tws = smem;                        // [M][F]
-  int* ks = reinterpret_cast<int*>(tws + M * F);   // [F] slot | conj << 8
-  float2* xs = reinterpret_cast<float2*>(ks + ((F + 1) & ~1));   // [G][M][nkp] (+1 per trace)
-  for (int e = threadIdx.x; e < M * F; e += K1_THREADS) tws[e] = twt[(e / F) * twt_ld + e % F];
+  float2* tws = smem;                                   // [F][MP]
+  int* ks = reinterpret_cast<int*>(tws + F * MP);       // [F] slot | conj << 8
+  float2* xs = reinterpret_cast<float2*>(ks + ((F + 1) & ~1));   // [G][TS]
   unsigned long long mask = 0;
   for (int f = 0; f < F; f++) {
     const int k = __ldg(bins + f) & 63;
     mask |= 1ull << (k > 32 ? 64 - k : k);
   }
   const int nk = __popcll(mask);
-  const int nkp = nk | 1;            // odd stride: conflict-free parking across r
-  if (nkp > nkp_cap) __trap();       // shared memory was sized for fewer bins (bad n_inner)
-  const int ts = M * nkp + 1;        // per-trace stride
+  const int ts = nk * MP + (((4 - nk * MP) % 16) + 16) % 16;
+  if (ts > ts_cap) __trap();         // shared memory was sized for fewer bins (bad n_inner)
   for (int f = threadIdx.x; f < F; f += K1_THREADS) {
     const int k = bins[f] & 63;
     const int kk = k > 32 ? 64 - k : k;
     ks[f] = __popcll(mask & ((1ull << kk) - 1ull)) | ((k > 32) << 8);
+  }
+  for (int e = threadIdx.x; e < M * F; e += K1_THREADS) {
+    const int rr = e / F, f = e - rr * F;
+    float2 w = twt[rr * twt_ld + f];
+    if ((bins[f] & 63) > 32) w.y = -w.y;
+    tws[f * MP + rr] = w;
   }
   __syncthreads();
 
@@ -94,24 +103,33 @@ k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __
       float x[64];
 #pragma unroll
       for (int q = 0; q < 64; q++) x[q] = __ldg(h + q * M);
-      real_dft64_sel(x, mask, xs + g * ts + r * nkp);
+      real_dft64_sel(x, mask, xs + g * ts + r, MP);
     }
     __syncthreads();
-    for (int p = threadIdx.x; p < G * F; p += K1_THREADS) {
-      const int gg = p % G, f = p / G;
-      const long long tr = grp * G + gg;
-      if (tr >= n_traces) continue;
+    for (int p0 = 0; p0 < 2 * G * F; p0 += K1_THREADS) {
+      const int p = p0 + threadIdx.x;
+      const bool valid = p < 2 * G * F;
+      const int hh = p & 1, o = p >> 1;
+      const int gg = o % G, f = valid ? o / G : 0;
       const int kv = ks[f];
-      const bool cj = kv >> 8;
-      const float2* src = xs + gg * ts + (kv & 255);
       float2 acc = make_float2(0.f, 0.f);
-#pragma unroll 8
-      for (int rr = 0; rr < M; rr++) {
-        float2 z = src[rr * nkp];
-        if (cj) z.y = -z.y;
-        cacc(acc, z, tws[rr * F + f]);
+      if (valid) {
+        const float2* src = xs + gg * ts + (kv & 255) * MP + hh;
+        const float2* tw = tws + f * MP + hh;
+        if (M == 1) {
+          if (hh == 0) cacc(acc, src[0], tw[0]);
+        } else {
+#pragma unroll 16
+          for (int j = 0; j < M / 2; j++) cacc(acc, src[2 * j], tw[2 * j]);
+        }
       }
-      out[(long long)f * out_stride + tr] = cmul(acc, wphase[f]);
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+      const long long tr = grp * G + gg;
+      if (valid && hh == 0 && tr < n_traces) {
+        if (kv >> 8) acc.y = -acc.y;
+        out[(long long)f * out_stride + tr] = cmul(acc, wphase[f]);
+      }
     }
     __syncthreads();
   }
@@ -279,12 +297,13 @@ int launch_k1(const float* hist, long long n_traces, const int* bins, const floa
   // folded to [0, 32]) when given, else the worst case
   int nk = (n_inner >= 1 && n_inner <= K1_KB) ? n_inner : K1_KB;
   if (nk > FC) nk = FC;
-  const int nkp = nk | 1;
-  const size_t smem = (size_t)(G * (M * nkp + 1) + M * FC) * sizeof(float2) +
+  constexpr int MP = M + 2 - (M & 1);
+  const int ts_cap = nk * MP + 15;   // per-trace stride incl. the bank-alignment pad
+  const size_t smem = ((size_t)G * ts_cap + (size_t)FC * MP) * sizeof(float2) +
                       ((FC + 1) & ~1) * sizeof(int);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_temporal_dft<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_temporal_dft<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   int dev = 0, nsm = 148;
@@ -301,7 +320,7 @@ int launch_k1(const float* hist, long long n_traces, const int* bins, const floa
     k_temporal_dft<M><<<grid_k1, K1_THREADS, smem, st>>>(hist, n_traces, bins + f0, twt + f0,
                                                        F_total, wphase + f0, F,
                                                        out + (long long)f0 * out_stride,
-                                                       out_stride, nkp);
+                                                       out_stride, ts_cap);
     PF_LAUNCH_CHECK("k_temporal_dft");
   }
   return 0;
