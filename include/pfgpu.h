@@ -54,12 +54,12 @@ int pf_last_error(char* buf, size_t len);
  * hist: float32 [n_traces][n_bins]; twiddle: c64 [n_bins/64][n_freq] with
  * entry [r][f] = W_T^{bins[f] r} (fp64-built); wphase: c64 [n_freq] =
  * weight_f * exp(-1j w_f t0).  Requires n_bins = 64*M, M a power of two <= 256.
- * n_inner: number of distinct inner bins min(b mod 64, 64 - b mod 64) over the
- * retained bins (sizes shared memory; 0 = unknown, worst case 33; a count below
- * the true one traps the kernel). */
+ * inner_mask: bit k set for every inner bin k = min(b mod 64, 64 - b mod 64) of the
+ * retained bins (sizes shared memory and selects the bins formed; 0 = unknown:
+ * the kernel derives it, shared memory for all 33; a set missing a bin traps). */
 int pf_temporal_dft(const float* hist, int64_t n_traces, int n_bins, const int32_t* bins,
                     const void* twiddle, const void* wphase, int n_freq, void* out,
-                    int64_t out_stride, int n_inner, void* stream);
+                    int64_t out_stride, uint64_t inner_mask, void* stream);
 /* Same transform for any n_bins (direct sum); unit_roots: c64 [n_bins] W_T^m. */
 int pf_temporal_dft_direct(const float* hist, int64_t n_traces, int n_bins,
                            const int32_t* bins, const void* unit_roots, const void* wphase,

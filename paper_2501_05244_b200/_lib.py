@@ -50,7 +50,7 @@ _P = ctypes.POINTER
 _SIGNATURES = {
     "pf_version": [],
     "pf_last_error": [ctypes.c_char_p, ctypes.c_size_t],
-    "pf_temporal_dft": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp],
+    "pf_temporal_dft": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, ctypes.c_uint64, _vp],
     "pf_temporal_dft_direct": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, _vp],
     "pf_fft_lines": [_vp, _P(PfFftPlan), _i64, _i64, _i64, _i64, _i64, _i, _f, _vp],
     "pf_embed_centered": [_vp, _i64, _i, _i, _i64, _vp, _i, _i, _i, _vp],

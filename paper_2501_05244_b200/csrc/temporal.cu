@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(K1_THREADS)
 k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __restrict__ bins,
                const float2* __restrict__ twt /*[M][twt_ld]*/, int twt_ld,
                const float2* __restrict__ wphase, int F, float2* __restrict__ out,
-               long long out_stride, int ts_cap) {
+               long long out_stride, int ts_cap, unsigned long long inner_mask) {
   constexpr int G = K1_THREADS / M;          // traces per block pass
   constexpr int T = M * K1_L;
   constexpr int MP = M + 2 - (M & 1);
@@ -72,10 +72,14 @@ k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __
   float2* tws = smem;                                   // [F][MP]
   int* ks = reinterpret_cast<int*>(tws + F * MP);       // [F] slot | conj << 8
   float2* xs = reinterpret_cast<float2*>(ks + ((F + 1) & ~1));   // [G][TS]
-  unsigned long long mask = 0;
-  for (int f = 0; f < F; f++) {
-    const int k = __ldg(bins + f) & 63;
-    mask |= 1ull << (k > 32 ? 64 - k : k);
+  // the caller's inner-bin set (a kernel argument: warp-uniform branches in the
+  // parking loop) or, if not given, the set of this chunk's bins
+  unsigned long long mask = inner_mask;
+  if (mask == 0) {
+    for (int f = 0; f < F; f++) {
+      const int k = __ldg(bins + f) & 63;
+      mask |= 1ull << (k > 32 ? 64 - k : k);
+    }
   }
   const int nk = __popcll(mask);
   const int ts = nk * MP + (((4 - nk * MP) % 16) + 16) % 16;
@@ -290,11 +294,13 @@ constexpr int K1_FCHUNK = 64;  // retained bins per pass (shared-memory bound)
 template <int M>
 int launch_k1(const float* hist, long long n_traces, const int* bins, const float2* twt,
               const float2* wphase, int F_total, float2* out, long long out_stride,
-              int n_inner, cudaStream_t st) {
+              unsigned long long inner_mask, cudaStream_t st) {
   constexpr int G = K1_THREADS / M;
   const int FC = F_total < K1_FCHUNK ? F_total : K1_FCHUNK;
-  // parked bins per column: the caller's count of distinct inner bins (bins mod 64
-  // folded to [0, 32]) when given, else the worst case
+  // parked bins per column: the caller's set of inner bins (bins mod 64 folded to
+  // [0, 32]) when given, else the worst case
+  inner_mask &= (1ull << 33) - 1ull;
+  const int n_inner = __builtin_popcountll(inner_mask);
   int nk = (n_inner >= 1 && n_inner <= K1_KB) ? n_inner : K1_KB;
   if (nk > FC) nk = FC;
   constexpr int MP = M + 2 - (M & 1);
@@ -320,7 +326,7 @@ int launch_k1(const float* hist, long long n_traces, const int* bins, const floa
     k_temporal_dft<M><<<grid_k1, K1_THREADS, smem, st>>>(hist, n_traces, bins + f0, twt + f0,
                                                        F_total, wphase + f0, F,
                                                        out + (long long)f0 * out_stride,
-                                                       out_stride, ts_cap);
+                                                       out_stride, ts_cap, inner_mask);
     PF_LAUNCH_CHECK("k_temporal_dft");
   }
   return 0;
@@ -376,8 +382,8 @@ int launch_k1_tma(const float* hist, long long n_traces, const int* bins, const 
 
 extern "C" int pf_temporal_dft(const float* hist, int64_t n_traces, int n_bins,
                                const int32_t* bins, const void* twiddle, const void* wphase,
-                               int n_freq, void* out, int64_t out_stride, int n_inner,
-                               void* stream) {
+                               int n_freq, void* out, int64_t out_stride,
+                               uint64_t inner_mask, void* stream) {
   PF_ARG_CHECK(n_traces >= 0 && n_freq >= 1 && n_bins >= 1, "pf_temporal_dft: bad sizes");
   if (n_traces == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
@@ -390,15 +396,15 @@ extern "C" int pf_temporal_dft(const float* hist, int64_t n_traces, int n_bins,
   if (M == 64 && ((uintptr_t)hist & 15) == 0 && n_freq <= K1_FCHUNK && getenv("PF_K1_TMA"))
     return launch_k1_tma(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, st);
   switch (M) {
-    case 1: return launch_k1<1>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
-    case 2: return launch_k1<2>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
-    case 4: return launch_k1<4>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
-    case 8: return launch_k1<8>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
-    case 16: return launch_k1<16>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
-    case 32: return launch_k1<32>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
-    case 64: return launch_k1<64>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
-    case 128: return launch_k1<128>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
-    case 256: return launch_k1<256>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, n_inner, st);
+    case 1: return launch_k1<1>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, inner_mask, st);
+    case 2: return launch_k1<2>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, inner_mask, st);
+    case 4: return launch_k1<4>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, inner_mask, st);
+    case 8: return launch_k1<8>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, inner_mask, st);
+    case 16: return launch_k1<16>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, inner_mask, st);
+    case 32: return launch_k1<32>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, inner_mask, st);
+    case 64: return launch_k1<64>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, inner_mask, st);
+    case 128: return launch_k1<128>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, inner_mask, st);
+    case 256: return launch_k1<256>(hist, n_traces, bins, tw, wp, n_freq, o, out_stride, inner_mask, st);
     default: break;
   }
   pf_set_error("pf_temporal_dft: n_bins must be 64*M with M a power of two <= 256 "

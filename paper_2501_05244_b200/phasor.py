@@ -149,7 +149,8 @@ class TemporalPlan:
             ph = (np.outer(r, bins) % T).astype(np.float64) / T   # [M, F], exact integer reduction
             self.tw = torch.from_numpy(np.exp(-2j * np.pi * ph).astype(np.complex64)).to(device)
             k = bins % 64
-            self.n_inner = int(np.unique(np.minimum(k, 64 - k)).size)
+            # inner bins the retained bins fold to (K1 forms and parks only these)
+            self.inner_mask = sum(1 << int(j) for j in set(np.minimum(k, 64 - k).tolist()))
         else:
             ph = np.arange(T, dtype=np.float64) / T
             self.tw = torch.from_numpy(np.exp(-2j * np.pi * ph).astype(np.complex64)).to(device)
@@ -160,7 +161,7 @@ class TemporalPlan:
         if self.fast:
             _lib.call("pf_temporal_dft", dev.ptr(hist), n_traces, self.n_bins, dev.ptr(self.bins),
                       dev.ptr(self.tw), dev.ptr(self.wphase), self.n_freq, dev.ptr(out),
-                      out.stride(0), self.n_inner, dev.stream_ptr(stream))
+                      out.stride(0), self.inner_mask, dev.stream_ptr(stream))
         else:
             _lib.call("pf_temporal_dft_direct", dev.ptr(hist), n_traces, self.n_bins,
                       dev.ptr(self.bins), dev.ptr(self.tw), dev.ptr(self.wphase), self.n_freq,
