@@ -84,6 +84,15 @@ int pf_fft_lines(void* data, const pf_fft_plan* plan, int64_t nlines, int64_t in
 int pf_embed_centered(const void* src, int64_t nb, int ny, int nx, int64_t src_batch_stride,
                       void* dst, int py, int px, int transpose, void* stream);
 
+/* Register-path relay spectra (replaces _pad_embed + cfft_2d, reference
+ * reconstruct.py:113-119,259-260): dst[b][kx][ky] = the TRANSPOSED natural-order
+ * forward 2D FFT of src[b] (ny x nx, row-major) embedded centred in P x P, for
+ * P in {128, 256, 512, 1024} (plan: pf_fft_plan of length P).  Only the ny relay
+ * rows are transformed; the zero rows cost nothing.  Two launches. */
+int pf_relay_spectra_fast(const void* src, int64_t nb, int ny, int nx,
+                          int64_t src_batch_stride, void* dst, int P,
+                          const pf_fft_plan* plan, void* stream);
+
 /* ---------------------------------------------------------------- propagation
  * Plane-to-plane RSD propagation, the per-(frequency, plane) inner loop of
  * rsd (reconstruct.py:254-266), srsd (:312-325), nursd1 (:372-383) and the

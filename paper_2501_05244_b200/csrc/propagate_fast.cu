@@ -384,6 +384,98 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
   return 0;
 }
 
+// ---- Relay spectra on the register path (reference reconstruct.py:259-260:
+// Uhat = cfft2(_pad_embed(u)), with the centred embed of :113-119 as an index map).
+// Output TRANSPOSED natural-order spectrum Uhat^T[b][kx][ky] (what B2 consumes).
+// Rows: only the ny relay rows are transformed (zero rows transform to zero) and
+// stored transposed through a padded shared tile; columns: one line per kx,
+// reading only the relay rows' slots (the rest are zero), contiguous in ky.
+template <int L>
+__global__ void __launch_bounds__(FT, 2)
+k_us_rows(const float2* __restrict__ src, int ny, int nx, long long sbs,
+          const float2* __restrict__ tw, float2* __restrict__ dst) {
+  constexpr int P = 32 * L, LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
+  extern __shared__ float2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int r = warp * LPW + line;
+  const int jy0 = blockIdx.x * RPC;
+  // rows jy0 .. jy0 + RPC - 1 hold relay rows iff centred(jy) + ny/2 in [0, ny);
+  // a tile without any is never read by the column pass (uniform exit, before syncs)
+  bool any = false;
+#pragma unroll 1
+  for (int q = 0; q < RPC; q++) any |= (unsigned)(centred(jy0 + q, P) + ny / 2) < (unsigned)ny;
+  if (!any) return;
+  const int iy = centred(jy0 + r, P) + ny / 2;
+  const bool vrow = (unsigned)iy < (unsigned)ny;
+  const float2* row = src + blockIdx.y * sbs + (long long)(vrow ? iy : 0) * nx;
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 32; m++) {
+    const int ix = centred(t + L * m, P) + nx / 2;
+    v[m] = (vrow && (unsigned)ix < (unsigned)nx) ? __ldg(row + ix) : make_float2(0.f, 0.f);
+  }
+  wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < 32; m++) sm[(t + L * m) * SLD + r] = v[m];
+  __syncthreads();
+  constexpr int KSTEP = FT / RPC;
+  const int rr = threadIdx.x % RPC, k0 = threadIdx.x / RPC;
+  float2* d = dst + (long long)blockIdx.y * P * P + (long long)k0 * P + jy0 + rr;
+  const float2* q = sm + k0 * SLD + rr;
+#pragma unroll 4
+  for (int kx = k0; kx < P; kx += KSTEP) {
+    *d = *q;
+    d += (long long)KSTEP * P;
+    q += KSTEP * SLD;
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(FT, 2)
+k_us_cols(int ny, const float2* __restrict__ tw, float2* __restrict__ dst) {
+  constexpr int P = 32 * L, LPW = 32 / L;
+  extern __shared__ float2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int kx = (blockIdx.x * 8 + warp) * LPW + line;
+  float2* col = dst + blockIdx.y * (long long)P * P + (long long)kx * P;
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 32; m++) {
+    const int jy = t + L * m;
+    v[m] = (unsigned)(centred(jy, P) + ny / 2) < (unsigned)ny ? col[jy] : make_float2(0.f, 0.f);
+  }
+  wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
+#pragma unroll
+  for (int m = 0; m < 32; m++) col[t + L * m] = v[m];
+}
+
+template <int L>
+int run_relay_spectra(const float2* src, long long nb, int ny, int nx, long long sbs,
+                      const float2* tw, float2* dst, cudaStream_t st) {
+  constexpr int P = 32 * L, LPW = 32 / L, RPC = 8 * LPW;
+  const size_t sm_r = (size_t)(8 * WFFT_XCH > P * (RPC + 1) ? 8 * WFFT_XCH : P * (RPC + 1)) *
+                      sizeof(float2);
+  const size_t sm_c = 8 * WFFT_XCH * sizeof(float2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_us_rows<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_us_cols<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  for (long long b0 = 0; b0 < nb; b0 += 65535) {
+    const int n = (int)(nb - b0 < 65535 ? nb - b0 : 65535);
+    k_us_rows<L><<<dim3(P / RPC, n), FT, sm_r, st>>>(src + b0 * sbs, ny, nx, sbs, tw,
+                                                     dst + b0 * (long long)P * P);
+    PF_LAUNCH_CHECK("k_us_rows");
+    k_us_cols<L><<<dim3(P / (8 * LPW), n), FT, sm_c, st>>>(ny, tw, dst + b0 * (long long)P * P);
+    PF_LAUNCH_CHECK("k_us_cols");
+  }
+  return 0;
+}
+
 }  // namespace
 
 // 32*L when the register path applies (square power-of-two pad 128..1024), else 0
@@ -446,5 +538,27 @@ int pf_prop_fbatch_stage(int stage, const pf_plane* planes, int nplanes, const d
   }
 #undef PF_FB_CASE
   pf_set_error("pf_prop_fbatch: geometry not eligible for the register path");
+  return -1;
+}
+
+// Transposed relay spectra for the register path: dst[b][kx][ky] = cfft2 of the
+// centred embed of src[b] (ny x nx, row-major) into P x P (P = pf_prop_fast).
+extern "C" int pf_relay_spectra_fast(const void* src, int64_t nb, int ny, int nx,
+                                     int64_t src_batch_stride, void* dst, int P,
+                                     const pf_fft_plan* plan, void* stream) {
+  PF_ARG_CHECK(plan != nullptr && plan->n == P, "pf_relay_spectra_fast: plan length != P");
+  PF_ARG_CHECK(nb >= 0 && ny >= 1 && nx >= 1 && ny <= P && nx <= P,
+               "pf_relay_spectra_fast: bad sizes");
+  if (nb == 0) return 0;
+  const float2* tw = (const float2*)plan->tw;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (P) {
+    case 128: return run_relay_spectra<4>((const float2*)src, nb, ny, nx, src_batch_stride, tw, (float2*)dst, st);
+    case 256: return run_relay_spectra<8>((const float2*)src, nb, ny, nx, src_batch_stride, tw, (float2*)dst, st);
+    case 512: return run_relay_spectra<16>((const float2*)src, nb, ny, nx, src_batch_stride, tw, (float2*)dst, st);
+    case 1024: return run_relay_spectra<32>((const float2*)src, nb, ny, nx, src_batch_stride, tw, (float2*)dst, st);
+    default: break;
+  }
+  pf_set_error("pf_relay_spectra_fast: P must be 128, 256, 512 or 1024");
   return -1;
 }

@@ -487,13 +487,13 @@ class RsdEngine(GraphedRun):
         """Uhat_f = cfft2(pad_embed(u_f)) for all (f, p), natural order (reconstruct.py:259-260)."""
         g = self.relay_grid
         F, I = self.freqs.size, self.n_illum
-        tr = self.prop.transposed
+        if self.prop.transposed:   # register path: embed + row FFT + column FFT, Uhat^T
+            _lib.call("pf_relay_spectra_fast", dev.ptr(coeff), F * I, g.ny, g.nx, g.ny * g.nx,
+                      dev.ptr(self.uhat), self.px, self.prop.plan_x.ref, dev.stream_ptr(stream))
+            return self.uhat
         _lib.call("pf_embed_centered", dev.ptr(coeff), F * I, g.ny, g.nx, g.ny * g.nx,
-                  dev.ptr(self.uhat), self.py, self.px, int(tr), dev.stream_ptr(stream))
-        if tr:   # FFT2 of the transposed grid is the transposed spectrum
-            dev.fft2_natural(self.uhat, self.px, self.py, F * I, -1, 1.0, stream)
-        else:
-            dev.fft2_natural(self.uhat, self.py, self.px, F * I, -1, 1.0, stream)
+                  dev.ptr(self.uhat), self.py, self.px, 0, dev.stream_ptr(stream))
+        dev.fft2_natural(self.uhat, self.py, self.px, F * I, -1, 1.0, stream)
         return self.uhat
 
     def run(self, coeff: torch.Tensor, vol: torch.Tensor | None = None, stream=None):

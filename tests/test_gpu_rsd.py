@@ -86,6 +86,28 @@ def test_fftn_vs_numpy(rng, shape):
     assert O.rel_l2(t.cpu().numpy(), ref) < 2e-6
 
 
+@pytest.mark.parametrize("P,ny,nx,nb", [(128, 64, 64, 3), (128, 37, 50, 2), (256, 128, 128, 1),
+                                         (512, 256, 256, 2), (512, 255, 3, 1), (1024, 512, 512, 2),
+                                         (1024, 1024, 1000, 1), (128, 1, 1, 1)])
+def test_relay_spectra_fast_vs_numpy(rng, P, ny, nx, nb):
+    """pf_relay_spectra_fast (register path) = transposed cfft2 of the centred embed
+    (reference reconstruct.py:113-119,259-260), natural order, float64 numpy reference."""
+    from paper_2501_05244_b200 import _device as dev, _lib
+    x = (rng.normal(size=(nb, ny, nx)) + 1j * rng.normal(size=(nb, ny, nx))).astype(np.complex64)
+    emb = np.zeros((nb, P, P), np.complex128)
+    iy = (np.arange(ny) - ny // 2) % P
+    ix = (np.arange(nx) - nx // 2) % P
+    emb[:, iy[:, None], ix[None, :]] = x
+    ref = np.fft.fft2(emb).transpose(0, 2, 1)
+    src = torch.from_numpy(x).cuda()
+    out = torch.full((nb, P, P), complex(np.nan, np.nan), dtype=torch.complex64, device="cuda")
+    plan = dev.fft_plan(P, src.device)
+    _lib.call("pf_relay_spectra_fast", dev.ptr(src), nb, ny, nx, ny * nx, dev.ptr(out), P,
+              plan.ref, dev.stream_ptr())
+    torch.cuda.synchronize()
+    assert O.rel_l2(out.cpu().numpy(), ref) < 2e-6
+
+
 RSD_CASES = ["rsd_small", "rsd_small_noill", "rsd_full16", "rsd_none16", "rsd_video",
              "chain_rsd", "rsd_odd", "rsd_odd_none"]
 
