@@ -156,10 +156,11 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
   const float scale = 1.0f / ((float)P * (float)P);
   const long long vol_row0 = (pl.vol_plane * ny + i0) * (long long)nx;
   const bool aligned = ((g.nu0x | nx) & (L - 1)) == 0;   // column crop uniform per m
-  if (PRE && CENT) {
-    const float2* src = vol + vol_row0;
+  if (PRE && CENT) {   // rows of P/2 elements starting at a multiple of P/2: 16-byte aligned
+    const float4* src = reinterpret_cast<const float4*>(vol + vol_row0);
+    float4* dst = reinterpret_cast<float4*>(volbuf);
 #pragma unroll
-    for (int e = threadIdx.x; e < RPC * (P / 2); e += PROP_MT) cp_async8(volbuf + e, src + e);
+    for (int e = threadIdx.x; e < RPC * (P / 4); e += PROP_MT) cp_async16(dst + e, src + e);
     cp_async_commit();
   } else if (PRE) {
     for (int rr = 0; rr < nr; rr++) {
