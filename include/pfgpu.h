@@ -258,6 +258,15 @@ int pf_nufft_spread(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
                     int64_t val_stride, int nv, void* fine, int64_t fine_stride, void* stream);
 /* type-1 finish (spectral.py:357-358): centred modes / discrete deconvolution,
  * written in natural order on the mode grid ([x][y] when transpose, 2D). */
+/* Type-1 finish on the register path (replaces the fine-grid fftn + pf_nufft_deconv,
+ * reference spectral.py:356-358) for 2D plans with square modes m in {128, 256, 512,
+ * 1024} and fine grid mr = 2m: out[v][c_x][c_y] (TRANSPOSED natural-order modes) =
+ * FFT(fine[v]) at the centred modes / (ker_y * ker_x).  rt: scratch of nv * m * 2m
+ * complex64.  plan_mr / plan_h: pf_fft_plan of lengths 2m and m.  Two launches. */
+int pf_nufft_type1_finish_pow2(const pf_nufft_geom* g, const void* fine, int64_t fine_stride,
+                               int nv, void* rt, const pf_fft_plan* plan_mr,
+                               const pf_fft_plan* plan_h, const float* ky, const float* kx,
+                               void* out, int64_t out_stride, void* stream);
 int pf_nufft_deconv(const pf_nufft_geom* g, const void* fine, int64_t fine_stride,
                     const float* kz, const float* ky, const float* kx, int nv, void* out,
                     int64_t out_stride, int transpose, void* stream);

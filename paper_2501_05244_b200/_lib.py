@@ -55,6 +55,8 @@ _SIGNATURES = {
     "pf_fft_lines": [_vp, _P(PfFftPlan), _i64, _i64, _i64, _i64, _i64, _i, _f, _vp],
     "pf_embed_centered": [_vp, _i64, _i, _i, _i64, _vp, _i, _i, _i, _vp],
     "pf_prop_fast": [_P(PfPropGeom)],
+    "pf_nufft_type1_finish_pow2": [_P(PfNufftGeom), _vp, _i64, _i, _vp, _P(PfFftPlan),
+                                   _P(PfFftPlan), _vp, _vp, _vp, _i64, _vp],
     "pf_relay_spectra_fast": [_vp, _i64, _i, _i, _i64, _vp, _i, _P(PfFftPlan), _vp],
     "pf_prop_ws_a": [_P(PfPropGeom), _i],
     "pf_prop_ws_b": [_P(PfPropGeom), _i],
@@ -99,7 +101,7 @@ _lib = None
 
 # calls that enqueue kernels (bench.py reports how many ran in its timed region)
 _LAUNCHERS = {"pf_temporal_dft", "pf_temporal_dft_direct", "pf_fft_lines", "pf_embed_centered",
-              "pf_relay_spectra_fast",
+              "pf_relay_spectra_fast", "pf_nufft_type1_finish_pow2",
               "pf_prop_kernel_rows", "pf_prop_columns", "pf_prop_rows_out", "pf_prop_fbatch", "pf_prop_fbatch_generic", "pf_prop_mega", "pf_count_nonfinite", "pf_scatter_csr", "pf_nufft_interp", "pf_nufft_interp2_batch", "pf_bluestein_lines", "pf_bluestein_warp",
               "pf_nufft_spread", "pf_nufft_deconv", "pf_nufft_place", "pf_nufft_interp2_acc",
               "pf_kernel3d", "pf_cmul", "pf_copy_planes", "pf_roll"}

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -77,6 +78,12 @@ class NufftPlan:
         self.kers = [torch.from_numpy(k.astype(np.float32)).to(device) for k in kers]
         self.fine_elems = int(np.prod(self.mrs))
         self.mode_elems = int(np.prod(self.modes3))
+        # type-1 finish on the register path: square 2D modes m in 128..1024, mr = 2m
+        m2 = self.modes3[2]
+        self.pow2_finish = (self.dim == 2 and self.modes3[1] == m2 and m2 in (128, 256, 512, 1024)
+                            and self.mrs[1] == 2 * m2 and self.mrs[2] == 2 * m2
+                            and os.environ.get("PF_NUFFT_FAST", "1") != "0")
+        self._rt = None
 
     @property
     def gref(self):
@@ -189,9 +196,21 @@ def type1(plan: NufftPlan, pts: NufftPoints, vals: torch.Tensor, nv: int, val_st
     s = dev.stream_ptr(stream)
     _lib.call("pf_nufft_spread", plan.gref, dev.ptr(pts.i0), dev.ptr(pts.d0), dev.ptr(ts),
               dev.ptr(tp), dev.ptr(vals), val_stride, nv, dev.ptr(fine), plan.fine_elems, s)
+    kz, ky, kx = plan.kers
+    if transpose and plan.pow2_finish:
+        # register path: split fine-grid FFT that forms only the kept modes, fused
+        # with the deconvolution (pf_nufft_type1_finish_pow2)
+        m = plan.modes3[2]
+        need = nv * m * 2 * m
+        if plan._rt is None or plan._rt.numel() < need:
+            plan._rt = torch.empty((need,), dtype=torch.complex64, device=plan.device)
+        _lib.call("pf_nufft_type1_finish_pow2", plan.gref, dev.ptr(fine), plan.fine_elems, nv,
+                  dev.ptr(plan._rt), dev.fft_plan(2 * m, plan.device).ref,
+                  dev.fft_plan(m, plan.device).ref, dev.ptr(ky), dev.ptr(kx), dev.ptr(out),
+                  out_stride, s)
+        return out
     shape = tuple(m for m in plan.mrs if True)[3 - plan.dim:]
     dev.fftn_natural(fine, shape, nv, -1, 1.0, stream)
-    kz, ky, kx = plan.kers
     _lib.call("pf_nufft_deconv", plan.gref, dev.ptr(fine), plan.fine_elems, dev.ptr(kz),
               dev.ptr(ky), dev.ptr(kx), nv, dev.ptr(out), out_stride, int(transpose), s)
     return out

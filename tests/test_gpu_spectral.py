@@ -84,3 +84,32 @@ def test_plain_2d_ffts(rng):
     assert O.rel_l2(S.ifft_2d(u), np.fft.ifft2(u)) < 1e-6
     assert O.rel_l2(S.dft_2d(u[0]), np.fft.fft2(u[0])) < 1e-6
     assert O.rel_l2(S.idft_2d(u[1]), np.fft.ifft2(u[1])) < 1e-6
+
+
+@pytest.mark.parametrize("m,eps", [(128, 1e-6), (256, 1e-4), (1024, 1e-6)])
+def test_type1_register_finish_vs_oracle(rng, m, eps):
+    """Split register-FFT type-1 finish (pf_nufft_type1_finish_pow2, mr = 2m) against the
+    float64 oracle nufft1 (reference spectral.py:336-358) and the generic fftn + deconv."""
+    import torch
+    from paper_2501_05244_b200 import nufft as nu
+    dev = torch.device("cuda")
+    L, nv = 2000, 3
+    pts = rng.uniform(-np.pi, np.pi, size=(L, 2))
+    pts[:500] = -np.pi + 2 * np.pi * rng.integers(0, m, size=(500, 2)) / m   # on-lattice nodes
+    vals = (rng.normal(size=(nv, L)) + 1j * rng.normal(size=(nv, L))).astype(np.complex64)
+    plan = nu.NufftPlan((m, m), eps, dev)
+    assert plan.pow2_finish and plan.mrs[1:] == (2 * m, 2 * m)
+    p = plan.points(pts)
+    v = torch.from_numpy(vals).to(dev)
+    out = torch.full((nv, m, m), complex(np.nan, np.nan), dtype=torch.complex64, device=dev)
+    nu.type1(plan, p, v, nv, L, out, m * m, transpose=True)
+    plan.pow2_finish = False
+    gen = torch.empty_like(out)
+    nu.type1(plan, p, v, nv, L, gen, m * m, transpose=True)
+    got, ref_gpu = out.cpu().numpy(), gen.cpu().numpy()
+    assert O.rel_l2(got, ref_gpu) < 2e-6
+    for i in range(nv if m <= 256 else 1):
+        ref = O.nufft1(pts, vals[i].astype(np.complex128), (m, m), eps)
+        # natural-order modes, transposed [x][y]; the oracle returns centred [y][x]
+        ref_nat = np.fft.ifftshift(ref).T
+        assert O.rel_l2(got[i], ref_nat) < 2e-6
