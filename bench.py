@@ -185,7 +185,7 @@ def run_ours(args):
     flush = None
     if in_bytes < 2 * l2_bytes:
         flush = torch.empty(4 * l2_bytes // 4, dtype=torch.float32, device=device)
-    launches0 = _lib.launch_count
+    launches0 = _lib.launches()
     with ClockSampler(local) as clk:
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
@@ -200,8 +200,8 @@ def run_ours(args):
             t_step.append(ev[0].elapsed_time(ev[4]))
         end.record(stream)
         torch.cuda.synchronize()
-    launches = (_lib.launch_count - launches0) // max(1, args.steps)
-    launches += eng_graph_launches(eng)
+    launches = (_lib.launches() - launches0) // max(1, args.steps)
+    launches += eng_graph_launches(eng, n_chunks)
     # with flushes between steps the region also holds the flush writes: use the
     # per-step events (first kernel of the step to its last) instead
     total_ms = sum(t_step) if flush is not None else start.elapsed_time(end)
@@ -338,8 +338,11 @@ def _e2e_leg(rec, hist_shard, cfg, world, device):
                     "H2D||K1 -> propagation -> D2H; 2 captures in flight; wall clock)"}
 
 
-def eng_graph_launches(eng):
-    """libpfgpu kernels replayed per step from the engine's captured CUDA graph."""
+def eng_graph_launches(eng, n_chunks=1):
+    """libpfgpu kernels replayed per step from the engine's captured CUDA graph(s)."""
+    if n_chunks > 1:
+        per = getattr(eng, "chunk_graph_kernels", {})
+        return int(sum(per.get((j, n_chunks), 0) for j in range(n_chunks)))
     return int(getattr(eng, "graph_kernels", 0))
 
 

@@ -46,6 +46,9 @@ typedef struct pf_fft_plan {
 int pf_version(void);
 /* Copy the calling thread's last error message into buf (always NUL-terminated). */
 int pf_last_error(char* buf, size_t len);
+/* Kernels launched by this library in this process (a stream-captured launch counts
+ * once, at capture).  Used by the bench's gpu_launches figure. */
+int64_t pf_launch_count(void);
 
 /* ---------------------------------------------------------------- K1
  * Temporal phasor transform: replaces phasor.to_frequency (phasor.py:107-127,

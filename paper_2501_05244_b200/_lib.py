@@ -50,6 +50,7 @@ _P = ctypes.POINTER
 _SIGNATURES = {
     "pf_version": [],
     "pf_last_error": [ctypes.c_char_p, ctypes.c_size_t],
+    "pf_launch_count": [],
     "pf_temporal_dft": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, ctypes.c_uint64, _vp],
     "pf_temporal_dft_direct": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, _vp],
     "pf_fft_lines": [_vp, _P(PfFftPlan), _i64, _i64, _i64, _i64, _i64, _i, _f, _vp],
@@ -93,19 +94,18 @@ _SIGNATURES = {
     "pf_prop_rows_out": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp,
                          _i64, _vp],
 }
-_RESTYPES = {"pf_prop_mega_ws": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
+_RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_mega_ws": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
              "pf_prop_ws_spectrum": ctypes.c_int64,
              "pf_prop_fast": ctypes.c_int}
 
 _lib = None
 
-# calls that enqueue kernels (bench.py reports how many ran in its timed region)
-_LAUNCHERS = {"pf_temporal_dft", "pf_temporal_dft_direct", "pf_fft_lines", "pf_embed_centered",
-              "pf_relay_spectra_fast", "pf_nufft_type1_finish_pow2",
-              "pf_prop_kernel_rows", "pf_prop_columns", "pf_prop_rows_out", "pf_prop_fbatch", "pf_prop_fbatch_generic", "pf_prop_mega", "pf_count_nonfinite", "pf_scatter_csr", "pf_nufft_interp", "pf_nufft_interp2_batch", "pf_bluestein_lines", "pf_bluestein_warp",
-              "pf_nufft_spread", "pf_nufft_deconv", "pf_nufft_place", "pf_nufft_interp2_acc",
-              "pf_kernel3d", "pf_cmul", "pf_copy_planes", "pf_roll"}
-launch_count = 0
+
+
+def launches() -> int:
+    """Kernels libpfgpu has launched in this process (native counter, one per launch
+    site that ran; a launch captured into a CUDA graph counts once, at capture)."""
+    return int(load().pf_launch_count())
 
 
 class PfError(RuntimeError):
@@ -139,10 +139,7 @@ def last_error() -> str:
 
 
 def call(name: str, *args) -> int:
-    global launch_count
     rc = getattr(load(), name)(*args)
-    if name in _LAUNCHERS:
-        launch_count += 1
     if name in _RESTYPES:
         return rc
     if rc != 0:

@@ -52,9 +52,12 @@ __device__ __forceinline__ int natural(long long c, int n) {
 // Thread-local last-error message; every extern "C" entry point returns 0 on
 // success, <0 for an argument error, >0 for a CUDA error.
 void pf_set_error(const char* fmt, ...);
+// process-wide count of kernel launches (one per PF_LAUNCH_CHECK; pf_launch_count)
+void pf_note_launch();
 
 #define PF_LAUNCH_CHECK(what)                                              \
   do {                                                                     \
+    pf_note_launch();                                                      \
     cudaError_t e__ = cudaGetLastError();                                  \
     if (e__ != cudaSuccess) {                                              \
       pf_set_error("%s: %s", what, cudaGetErrorString(e__));               \

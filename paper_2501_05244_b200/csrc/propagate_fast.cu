@@ -342,7 +342,6 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
         k_pcf<L, true, 2><<<grid, 64, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb, part);
       else
         k_pcf<L, false, 2><<<grid, 64, sm, st>>>(planes, g, tw, ws_b, ill, frame_w, vol, fb, part);
-      PF_LAUNCH_CHECK("k_pcf");
       if (part) {
         const long long total = (long long)nplanes * g.ny * g.nx;
         const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);

@@ -40,7 +40,7 @@ ALGORITHM_NAMES = ("rsd", "srsd", "nursd1", "nursd2", "nursd3", "rsd3d", "nursd3
 
 # workspace budget per propagation batch: keep ws_a + ws_b L2-resident (126 MB L2)
 _BATCH_BYTES = 64 << 20
-_LANES = int(os.environ.get("PF_LANES", "3"))
+_LANES = int(os.environ.get("PF_LANES", "2"))
 _FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "4"))
 _FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
 _FBATCH_GENERIC = os.environ.get("PF_FBATCH_GENERIC", "1") != "0"
@@ -354,11 +354,11 @@ class GraphedRun:
                 self.run(coeff, vol, side)          # warm-up: plans, attributes, caches
             main.wait_stream(side)
             g = torch.cuda.CUDAGraph()
-            n0 = _lib.launch_count
+            n0 = _lib.launches()
             with torch.cuda.graph(g, stream=side):
                 self.run(coeff, vol, side)
             main.wait_stream(side)
-            self.graph_kernels = _lib.launch_count - n0   # libpfgpu launches per replay
+            self.graph_kernels = _lib.launches() - n0   # libpfgpu launches per replay
             graphs[key] = g
         with torch.cuda.stream(main):
             g.replay()
@@ -391,9 +391,13 @@ class GraphedRun:
                 self.run_chunk(coeff, vol, lo, hi, j == 0, side)
             main.wait_stream(side)
             g = torch.cuda.CUDAGraph()
+            n0 = _lib.launches()
             with torch.cuda.graph(g, stream=side):
                 self.run_chunk(coeff, vol, lo, hi, j == 0, side)
             main.wait_stream(side)
+            # libpfgpu launches per replay of chunk j of n_chunks
+            self.__dict__.setdefault("chunk_graph_kernels", {})[(j, n_chunks)] = \
+                _lib.launches() - n0
             graphs[key] = g
         with torch.cuda.stream(main):
             g.replay()
