@@ -21,7 +21,8 @@ namespace {
 
 constexpr int NT = 256;
 constexpr int SP_CHUNK = 32;   // points staged per pass
-constexpr int SP_V = 8;        // value sets (complex) accumulated per CTA
+// value sets (complex) accumulated per CTA: 16 when there are at least 16 (every
+// frequency of a capture shares one staging of the tile's points), else 8
 
 __device__ __forceinline__ int wrap_off(int d, int mr) {
   // representative of d mod mr in [-mr/2, mr - mr/2), for d in (-mr, 2 mr)
@@ -33,6 +34,7 @@ __device__ __forceinline__ int wrap_off(int d, int mr) {
 }
 
 // grid: (total tiles, ceil(nv / SP_V)); block: tile cells (<= 256 threads)
+template <int SP_V>
 __global__ void __launch_bounds__(NT)
 k_spread(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
          const int* __restrict__ tile_start, const int* __restrict__ tile_pts,
@@ -60,8 +62,8 @@ k_spread(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ 
   const int s0 = tile_start[tile], s1 = tile_start[tile + 1];
   // tile origin per axis: a point's offset to every cell of the tile is its
   // offset to the origin (wrapped once, when staged) plus the cell's local index
-  const int tile0[3] = {tz * G.tile[0], ty * G.tile[1], tx * G.tile[2]};
-  const int lz = cz - tile0[0], ly = cy - tile0[1], lx = cx - tile0[2];
+  const int tile0z = tz * G.tile[0], tile0y = ty * G.tile[1], tile0x = tx * G.tile[2];
+  const int lz = cz - tile0z, ly = cy - tile0y, lx = cx - tile0x;
   for (int c0 = s0; c0 < s1; c0 += SP_CHUNK) {
     const int nc = min(SP_CHUNK, s1 - c0);
     __syncthreads();
@@ -74,7 +76,8 @@ k_spread(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ 
           const float dl = base + (float)(o - G.w) * G.h[a];
           wgt[p][a][o] = __expf(-dl * dl * G.inv4tau[a]);
         }
-        pi0[p][a] = wrap_off(tile0[a] - natural(i0[3 * pt + a], G.mr[a]), G.mr[a]);
+        const int t0 = a == 0 ? tile0z : (a == 1 ? tile0y : tile0x);
+        pi0[p][a] = wrap_off(t0 - natural(i0[3 * pt + a], G.mr[a]), G.mr[a]);
       } else {
         for (int o = 0; o < W; o++) wgt[p][a][o] = 1.0f;
         pi0[p][a] = 0;      // unused axis of a 2D grid
@@ -106,7 +109,9 @@ k_spread(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ 
   }
   if (inside) {
     const long long cell = ((long long)cz * G.mr[1] + cy) * G.mr[2] + cx;
-    for (int v = 0; v < nvv; v++) fine[(long long)(v0 + v) * fine_stride + cell] = acc[v];
+#pragma unroll
+    for (int v = 0; v < SP_V; v++)   // constant indices: acc stays in registers
+      if (v < nvv) fine[(long long)(v0 + v) * fine_stride + cell] = acc[v];
   }
 }
 
@@ -415,10 +420,15 @@ extern "C" int pf_nufft_spread(const pf_nufft_geom* g, const int32_t* i0, const 
                "pf_nufft_spread: bad geometry");
   PF_ARG_CHECK(g->tile[0] * g->tile[1] * g->tile[2] <= NT, "pf_nufft_spread: tile too large");
   const int ntiles = g->ntiles[0] * g->ntiles[1] * g->ntiles[2];
-  dim3 grid(ntiles, pf_cdiv(nv, SP_V));
-  k_spread<<<grid, NT, 0, (cudaStream_t)stream>>>(*g, i0, d0, tile_start, tile_pts,
-                                                  (const float2*)vals, val_stride, nv,
-                                                  (float2*)fine, fine_stride);
+  if (nv >= 16) {
+    k_spread<16><<<dim3(ntiles, pf_cdiv(nv, 16)), NT, 0, (cudaStream_t)stream>>>(
+        *g, i0, d0, tile_start, tile_pts, (const float2*)vals, val_stride, nv, (float2*)fine,
+        fine_stride);
+  } else {
+    k_spread<8><<<dim3(ntiles, pf_cdiv(nv, 8)), NT, 0, (cudaStream_t)stream>>>(
+        *g, i0, d0, tile_start, tile_pts, (const float2*)vals, val_stride, nv, (float2*)fine,
+        fine_stride);
+  }
   PF_LAUNCH_CHECK("k_spread");
   return 0;
 }

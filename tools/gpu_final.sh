@@ -24,4 +24,5 @@ PF_NF=2 ncu --set full --clock-control none --import-source on \
 PF_NF=2 ncu --set full --clock-control none --import-source on \
     -k regex:"k_temporal_dft" -s 1 -c 1 -o $O/prof_k1 \
     python tools/prof_rsd.py > $O/ncu_k1.log 2>&1
-tail -2 $O/ncu_full.log $O/ncu_k1.log
+tail -n 2 $O/ncu_full.log $O/ncu_k1.log
+timeout 600 python tools/chunk_prof.py > $O/chunk_prof.txt 2>&1; cat $O/chunk_prof.txt
