@@ -132,6 +132,57 @@ def fftn_natural(buf: torch.Tensor, shape: tuple[int, ...], nbatch: int, directi
         buf.mul_(scale)
 
 
+def kept_ranges(m: int, mr: int) -> list[tuple[int, int]]:
+    """Natural slots on a length-mr axis holding the centred modes [-m//2, m - m//2):
+    (start, length) runs (reference NufftPlan.slots, spectral.py:287-295)."""
+    if m >= mr:
+        return [(0, mr)]
+    return [(0, m - m // 2), (mr - m // 2, m // 2)] if m // 2 else [(0, m - m // 2)]
+
+
+def fftn_pruned(buf: torch.Tensor, shape: tuple[int, ...], nbatch: int, direction: int,
+                kept: list, outputs: bool, stream=None) -> None:
+    """In-place 2D/3D FFT of ``nbatch`` contiguous arrays computing only the lines a
+    NUFFT needs.  ``kept[a]``: (start, length) runs of the kept slots on axis a.
+    outputs=True (type 1, forward): only kept outputs are read afterwards, so an axis
+    is transformed only along lines whose already-transformed coordinates are kept.
+    outputs=False (type 2, inverse): the input is zero off the kept slots, so an axis
+    is transformed only along lines whose not-yet-transformed coordinates are kept
+    (the other lines are zero and stay zero).  Axes run last to first, as in
+    ``fftn_natural``; line sets map onto pf_fft_lines' (inner, istr, ostr) indexing."""
+    d = len(shape)
+    assert d in (2, 3)
+    strides = [int(np.prod(shape[a + 1:])) for a in range(d)]
+    total = int(np.prod(shape))
+    base = ptr(buf)
+
+    def run(off, n, nl, inner, istr, ostr, estr):
+        if nl > 0:
+            _lib.call("pf_fft_lines", base + 8 * off, fft_plan(n, buf.device).ref, nl, inner,
+                      istr, ostr, estr, direction, 1.0, stream_ptr(stream))
+
+    for ax in range(d - 1, -1, -1):
+        n = shape[ax]
+        if n == 1:
+            continue
+        others = [a for a in range(d) if a != ax]
+        runs = [kept[a] if (a > ax) == outputs else [(0, shape[a])] for a in others]
+        if d == 2:
+            (o,) = others
+            for s0, ln in runs[0]:
+                # lines along the other axis o, batches folded in with stride `total`
+                run(s0 * strides[o], n, nbatch * ln, ln, strides[o], total, strides[ax])
+            continue
+        oa, ia = others
+        for so, lo in runs[0]:
+            for si, li in runs[1]:
+                fold = oa == 0 and lo == shape[0]   # a full leading axis runs into the next batch
+                for b in ([0] if fold else range(nbatch)):
+                    nl = (nbatch if fold else 1) * lo * li
+                    run(b * total + so * strides[oa] + si * strides[ia], n, nl, li, strides[ia],
+                        strides[oa], strides[ax])
+
+
 def c64(t: torch.Tensor) -> torch.Tensor:
     """View a complex64 tensor; ensures contiguity."""
     assert t.dtype == torch.complex64

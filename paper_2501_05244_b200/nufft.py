@@ -84,6 +84,9 @@ class NufftPlan:
                             and self.mrs[1] == 2 * m2 and self.mrs[2] == 2 * m2
                             and os.environ.get("PF_NUFFT_FAST", "1") != "0")
         self._rt = None
+        # natural fine-grid slots of the centred modes per transformed axis
+        self.kept = [dev.kept_ranges(m, mr) for m, mr in
+                     zip(self.modes3[3 - self.dim:], self.mrs[3 - self.dim:])]
 
     @property
     def gref(self):
@@ -209,8 +212,9 @@ def type1(plan: NufftPlan, pts: NufftPoints, vals: torch.Tensor, nv: int, val_st
                   dev.fft_plan(m, plan.device).ref, dev.ptr(ky), dev.ptr(kx), dev.ptr(out),
                   out_stride, s)
         return out
-    shape = tuple(m for m in plan.mrs if True)[3 - plan.dim:]
-    dev.fftn_natural(fine, shape, nv, -1, 1.0, stream)
+    shape = plan.mrs[3 - plan.dim:]
+    # only the kept modes are gathered: transform only the lines that reach them
+    dev.fftn_pruned(fine, shape, nv, -1, plan.kept, True, stream)
     _lib.call("pf_nufft_deconv", plan.gref, dev.ptr(fine), plan.fine_elems, dev.ptr(kz),
               dev.ptr(ky), dev.ptr(kx), nv, dev.ptr(out), out_stride, int(transpose), s)
     return out
@@ -223,5 +227,6 @@ def place_and_inverse(plan: NufftPlan, S: torch.Tensor, nv: int, s_stride: int,
     _lib.call("pf_nufft_place", plan.gref, dev.ptr(S), s_stride, dev.ptr(kz), dev.ptr(ky),
               dev.ptr(kx), nv, dev.ptr(fine), plan.fine_elems, 0, dev.stream_ptr(stream))
     shape = plan.mrs[3 - plan.dim:]
-    dev.fftn_natural(fine, shape, nv, +1, 1.0, stream)
+    # the placed grid is zero off the mode slots: skip the lines that are all zero
+    dev.fftn_pruned(fine, shape, nv, +1, plan.kept, False, stream)
     return fine

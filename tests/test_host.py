@@ -117,3 +117,49 @@ def test_rescale_to_torus_round_trip_and_errors():
         pf.rescale_to_torus(p, [0.0, 1.0], [0.5, 2.0])
     with pytest.raises(pf.ValidationError, match="positive extent"):
         pf.rescale_to_torus(p, [0.0, 1.0], [0.0, 2.0])
+
+
+@pytest.mark.parametrize("shape,modes,nb", [((12, 10), (5, 6), 2), ((8, 12, 10), (3, 5, 6), 2),
+                                            ((6, 9, 8), (6, 4, 3), 1)])
+def test_fftn_pruned_line_sets(monkeypatch, shape, modes, nb):
+    """The NUFFT's pruned fftn (host line-set logic) against numpy: type 1 keeps every
+    kept output, type 2 (zero off the kept slots) is exact everywhere.  pf_fft_lines is
+    emulated on the CPU buffer from its (inner, istr, ostr, estr) line indexing."""
+    import torch
+    from paper_2501_05244_b200 import _device as dev
+    rng = np.random.default_rng(5)
+    x = (rng.normal(size=(nb,) + shape) + 1j * rng.normal(size=(nb,) + shape)).astype(np.complex64)
+    kept = [dev.kept_ranges(m, n) for m, n in zip(modes, shape)]
+    t = torch.from_numpy(x.copy())
+    flat = t.view(-1).numpy()
+    base = t.data_ptr()
+
+    def fake(name, p, planref, nl, inner, istr, ostr, estr, direction, scale, stream):
+        assert name == "pf_fft_lines"
+        n = planref._obj.n
+        off = (p - base) // 8
+        for ln in range(nl):
+            idx = off + (ln // inner) * ostr + (ln % inner) * istr + np.arange(n) * estr
+            v = flat[idx].astype(np.complex128)
+            flat[idx] = np.fft.fft(v) if direction < 0 else np.fft.ifft(v) * n
+        return 0
+
+    monkeypatch.setattr(dev._lib, "call", fake)
+    axes = tuple(range(1, len(shape) + 1))
+    sel = np.ix_(*[np.concatenate([np.arange(s0, s0 + ln) for s0, ln in k]) for k in kept])
+    st = type("S", (), {"cuda_stream": 0})()   # no device: the emulated call ignores it
+    dev.fftn_pruned(t, shape, nb, -1, kept, True, st)
+    ref = np.fft.fftn(x.astype(np.complex128), axes=axes)
+    for b in range(nb):
+        np.testing.assert_allclose(flat.reshape((nb,) + shape)[b][sel], ref[b][sel], rtol=1e-4,
+                                   atol=1e-4)
+    # type 2: input zero off the kept slots, full inverse everywhere
+    z = np.zeros_like(x)
+    for b in range(nb):
+        z[b][sel] = x[b][sel]
+    t2 = torch.from_numpy(z.copy())
+    flat = t2.view(-1).numpy()
+    base = t2.data_ptr()
+    dev.fftn_pruned(t2, shape, nb, +1, kept, False, st)
+    ref2 = np.fft.ifftn(z.astype(np.complex128), axes=axes) * np.prod(shape)
+    np.testing.assert_allclose(flat.reshape((nb,) + shape), ref2, rtol=1e-4, atol=1e-4)
