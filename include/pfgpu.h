@@ -309,6 +309,11 @@ int pf_kernel3d(void* out, int pz, int py, int px, double dx, double dy, double 
 /* a[i] = a[i] * b[i % b_period] * scale */
 int pf_cmul(void* a, const void* b, int64_t n, int64_t b_period, float scale, void* stream);
 /* dst[b][:] = src[b*src_stride + plane_off + :plane_elems] (slab extraction, :760) */
+/* One output plane of an inverse DFT along the leading axis: dst[b][j] = scale *
+ * sum_z src[b][z][j] * w[z] (w = exp(+2 pi i z slab / nz), complex64, host-built in
+ * float64); replaces the z pass of cifft_n + slab extraction (reconstruct.py:758-759). */
+int pf_zslab(const void* src, int nb, int nz, int64_t nyx, const void* w, float scale,
+             void* dst, void* stream);
 int pf_copy_planes(const void* src, int nb, int64_t src_stride, int64_t plane_off,
                    int64_t plane_elems, void* dst, void* stream);
 

@@ -618,6 +618,8 @@ class _Lattice3dEngine(_UhatPropEngine):
         self.vg, self.grid = vg, grid
         self.px, self.py, self.pz, self.dz3, self.z0 = px, py, pz, dz3, z0
         self.slab_nat = (slab - pz // 2) % pz
+        zw = np.exp(2j * np.pi * ((np.arange(pz) * self.slab_nat) % pz) / pz)   # float64 phases
+        self._zslab_w = torch.from_numpy(zw.astype(np.complex64)).to(self.device)
         self.freqs = np.asarray(slices.frequencies, dtype=np.float64)
         self.n_illum = int(slices.illuminations.count)
         self._setup_prop(px, py, vg, z0, include_illumination, plane_range or (0, vg.nz))
@@ -642,9 +644,12 @@ class _Lattice3dEngine(_UhatPropEngine):
                       khat, s)
             dev.fftn_natural(g3, (pz, py, px), 1, -1, 1.0, stream)
             _lib.call("pf_cmul", dev.ptr(uhat3), dev.ptr(g3), I * n3, n3, 1.0, s)
-            dev.fftn_natural(uhat3, (pz, py, px), I, +1, 1.0 / n3, stream)
-            _lib.call("pf_copy_planes", dev.ptr(uhat3), I, n3, self.slab_nat * py * px, py * px,
-                      dev.ptr(out) + 8 * fi * I * py * px, s)
+            # cifft_n, then the slab plane: the z pass is evaluated at the slab only, then
+            # the plane's y/x inverse transforms (the 3D inverse is never formed)
+            out_f = out[fi * I * py * px:(fi + 1) * I * py * px]
+            _lib.call("pf_zslab", dev.ptr(uhat3), I, pz, py * px, dev.ptr(self._zslab_w),
+                      1.0 / n3, dev.ptr(out_f), s)
+            dev.fft2_natural(out_f, py, px, I, +1, 1.0, stream)
         return out
 
     def relay_spectra(self, coeff, stream=None):

@@ -77,6 +77,36 @@ extern "C" int pf_copy_planes(const void* src, int nb, int64_t src_stride, int64
   return 0;
 }
 
+// One output plane of an inverse DFT along the leading axis (nursd3d stage 1,
+// reference reconstruct.py:758-759: cifft_n over (z, y, x), then the slab plane):
+// dst[b][j] = scale * sum_z src[b][z][j] * w[z], w[z] = exp(+2 pi i z slab / nz) built
+// in float64 on the host.  The y/x inverse transforms of that one plane follow, so the
+// full 3D inverse transform is never formed.
+namespace {
+__global__ void k_zslab(const float2* __restrict__ src, int nb, int nz, long long nyx,
+                        const float2* __restrict__ w, float scale, float2* __restrict__ dst) {
+  const long long total = (long long)nb * nyx;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / nyx, j = e - b * nyx;
+    const float2* s = src + b * nz * nyx + j;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int z = 0; z < nz; z++) acc = cadd(acc, cmul(s[(long long)z * nyx], __ldg(w + z)));
+    dst[e] = make_float2(acc.x * scale, acc.y * scale);
+  }
+}
+}  // namespace
+
+extern "C" int pf_zslab(const void* src, int nb, int nz, int64_t nyx, const void* w, float scale,
+                        void* dst, void* stream) {
+  PF_ARG_CHECK(nb >= 0 && nz >= 1 && nyx >= 0, "pf_zslab: bad sizes");
+  if (nb == 0 || nyx == 0) return 0;
+  k_zslab<<<grid_for((long long)nb * nyx), 256, 0, (cudaStream_t)stream>>>(
+      (const float2*)src, nb, nz, nyx, (const float2*)w, scale, (float2*)dst);
+  PF_LAUNCH_CHECK("k_zslab");
+  return 0;
+}
+
 // circular shift of the trailing (up to 3) axes: dst[b][j] = src[b][(j + s) mod n]
 // per axis -- ifftshift uses s = n/2, fftshift s = n - n/2 (spectral.py:107-114)
 namespace {
