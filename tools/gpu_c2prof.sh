@@ -1,0 +1,4 @@
+mkdir -p gpurun_out/c2
+O=gpurun_out/c2
+python tools/prof_c2.py > $O/c2plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2.csv python tools/prof_c2.py > $O/ncu_c2.log 2>&1
+python tools/launches.py $O/launches_c2.csv > $O/launches_c2.txt 2>&1; head -16 $O/launches_c2.txt
