@@ -602,6 +602,9 @@ def _lattice_3d(slices, grid, z_pitch):
     return rel, dz3, z_min, nz3, pz, z0, nu_rx, nu_ry, px, py, slab
 
 
+_GROUP_FINE_BYTES = 4 << 30   # type-1 fine grids of one nursd3d frequency group
+
+
 class _Lattice3dEngine(_UhatPropEngine):
     """Shared two-stage structure of nursd3d / rsd3d (reconstruct.py:662-765): stage 1
     forms the virtual-lattice spectrum (subclass), x cfft_n(G3) -> cifft_n -> slab ->
@@ -634,11 +637,14 @@ class _Lattice3dEngine(_UhatPropEngine):
         px, py, pz = self.px, self.py, self.pz
         n3 = pz * py * px
         s = dev.stream_ptr(stream)
-        uhat3 = torch.empty((I * n3,), dtype=torch.complex64, device=self.device)
+        gf = max(1, min(F, getattr(self, "group_f", 1)))   # frequencies per lattice-spectrum call
+        uhat3g = torch.empty((gf * I * n3,), dtype=torch.complex64, device=self.device)
         g3 = torch.empty((n3,), dtype=torch.complex64, device=self.device)
         out = torch.empty((F * I * py * px,), dtype=torch.complex64, device=self.device)
         for fi in range(F):
-            self._lattice_spectrum(coeff[fi], uhat3, n3, stream)
+            if fi % gf == 0:
+                self._lattice_spectra(coeff, fi, min(F, fi + gf), uhat3g, n3, stream)
+            uhat3 = uhat3g[(fi % gf) * I * n3:(fi % gf + 1) * I * n3]
             khat = float(self.freqs[fi]) / C
             _lib.call("pf_kernel3d", dev.ptr(g3), pz, py, px, self.vg.dx, self.vg.dy, self.dz3,
                       khat, s)
@@ -651,6 +657,13 @@ class _Lattice3dEngine(_UhatPropEngine):
                       1.0 / n3, dev.ptr(out_f), s)
             dev.fft2_natural(out_f, py, px, I, +1, 1.0, stream)
         return out
+
+    def _lattice_spectra(self, coeff, f0, f1, uhat3g, n3, stream):
+        """Lattice spectra of frequencies [f0, f1) into uhat3g ([f][I][n3]); one call per
+        frequency unless the subclass batches them."""
+        I = self.n_illum
+        for j, fi in enumerate(range(f0, f1)):
+            self._lattice_spectrum(coeff[fi], uhat3g[j * I * n3:(j + 1) * I * n3], n3, stream)
 
     def relay_spectra(self, coeff, stream=None):
         F, I = self.freqs.size, self.n_illum
@@ -687,12 +700,23 @@ class Nursd3dEngine(_Lattice3dEngine):
                                  2.0 * np.pi * nu_rz / pz])
         self.plan = nu.NufftPlan((pz, py, px), eps, self.device)
         self.pts = self.plan.points(torus)
-        self._fine = torch.empty((self.n_illum, self.plan.fine_elems), dtype=torch.complex64,
-                                 device=self.device)
+        # the frequencies of a group share one spreading pass (a tile's points and window
+        # weights are staged once for up to 16 value sets); their fine grids stay within
+        # _GROUP_FINE_BYTES
+        per = 8 * self.n_illum * self.plan.fine_elems
+        self.group_f = max(1, min(self.freqs.size, _GROUP_FINE_BYTES // per))
+        self._fine = torch.empty((self.group_f * self.n_illum, self.plan.fine_elems),
+                                 dtype=torch.complex64, device=self.device)
 
     def _lattice_spectrum(self, coeff_f, uhat3, n3, stream):
         nu.type1(self.plan, self.pts, coeff_f, self.n_illum, coeff_f.shape[-1], uhat3, n3,
                  self._fine, False, stream)
+
+    def _lattice_spectra(self, coeff, f0, f1, uhat3g, n3, stream):
+        nv = (f1 - f0) * self.n_illum
+        vals = coeff[f0:f1].reshape(nv, coeff.shape[-1])
+        nu.type1(self.plan, self.pts, vals, nv, coeff.shape[-1], uhat3g, n3, self._fine, False,
+                 stream)
 
 
 class Rsd3dEngine(_Lattice3dEngine):
