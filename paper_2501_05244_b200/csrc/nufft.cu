@@ -210,6 +210,9 @@ k_interp2_warp(pf_nufft_geom G, const int* __restrict__ i0, const float* __restr
   const float dyl = d0[3 * l + 1], dxl = d0[3 * l + 2];
   const float dx = dxl + (float)(lane - G.w) * G.h[2];
   const float wx = on ? __expf(-dx * dx * G.inv4tau[2]) : 0.f;
+  // row weights: lane o forms row o's weight once; the row loop broadcasts it
+  const float dyo = dyl + (float)(lane - G.w) * G.h[1];
+  const float wy_lane = on ? __expf(-dyo * dyo * G.inv4tau[1]) : 0.f;
   const int cx = wrap_once(natural((long long)i0[3 * l + 2] - G.w, mrx) + (on ? lane : 0), mrx);
   const int cy0 = natural((long long)i0[3 * l + 1] - G.w, mry);
   float2 tot = make_float2(0.f, 0.f);
@@ -218,8 +221,7 @@ k_interp2_warp(pf_nufft_geom G, const int* __restrict__ i0, const float* __restr
     float2 acc = make_float2(0.f, 0.f);
     int cy = cy0;
     for (int oy = 0; oy < W; oy++) {
-      const float dy = dyl + (float)(oy - G.w) * G.h[1];
-      const float w = wx * __expf(-dy * dy * G.inv4tau[1]);
+      const float w = wx * __shfl_sync(0xffffffffu, wy_lane, oy);
       const float2 f = __ldg(fp + (long long)cy * mrx);
       acc.x = fmaf(w, f.x, acc.x);
       acc.y = fmaf(w, f.y, acc.y);
@@ -268,6 +270,9 @@ k_interp2_batch(pf_nufft_geom G, const int* __restrict__ i0, const float* __rest
   const float dyl = d0[3 * l + 1], dxl = d0[3 * l + 2];
   const float dx = dxl + (float)(lane - G.w) * G.h[2];
   const float wx = on ? __expf(-dx * dx * G.inv4tau[2]) : 0.f;
+  // row weights: lane o forms row o's weight once; the row loop broadcasts it
+  const float dyo = dyl + (float)(lane - G.w) * G.h[1];
+  const float wy_lane = on ? __expf(-dyo * dyo * G.inv4tau[1]) : 0.f;
   const int cx = wrap_once(natural((long long)i0[3 * l + 2] - G.w, mrx) + (on ? lane : 0), mrx);
   const int cy0 = natural((long long)i0[3 * l + 1] - G.w, mry);
   const float2* fplane = fine + (long long)(plane_idx[l] - plane0) * fine_plane_stride;
@@ -277,8 +282,7 @@ k_interp2_batch(pf_nufft_geom G, const int* __restrict__ i0, const float* __rest
     float2 acc = make_float2(0.f, 0.f);
     int cy = cy0;
     for (int oy = 0; oy < W; oy++) {
-      const float dy = dyl + (float)(oy - G.w) * G.h[1];
-      const float w = wx * __expf(-dy * dy * G.inv4tau[1]);
+      const float w = wx * __shfl_sync(0xffffffffu, wy_lane, oy);
       const float2 f = __ldg(fp + (long long)cy * mrx);
       acc.x = fmaf(w, f.x, acc.x);
       acc.y = fmaf(w, f.y, acc.y);
