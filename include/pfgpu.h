@@ -154,6 +154,17 @@ int pf_prop_rows_out(const pf_plane* planes, int nplanes, double khat,
                      const double* ill_xyz, const void* frame_w, int n_frames, void* vol,
                      int64_t vol_frame_stride, void* stream);
 
+/* Stage C with the illumination phase by Horner's rule (register path, both crops
+ * centred, one illumination, single frame): call it for the frequencies in DESCENDING
+ * order, last = 1 on the lowest (khat = k_0); dkhat = the uniform frequency spacing in
+ * rad/m.  vol <- vol * exp(i dk d) + v_f, and on the last call the sum is multiplied by
+ * exp(i k_0 d): the same sum as reconstruct.py:160-168 (ascending f, per-frequency
+ * phases) in nested order.  Returns 1 without work when the geometry is not eligible. */
+int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, double khat, double dkhat,
+                            int last, const pf_prop_geom* g, const pf_fft_plan* plan_x,
+                            const void* ws_b, const double* ill_xyz, const void* frame_w,
+                            void* vol, void* stream);
+
 /* All nf frequencies of a plane batch at once (register path, static volume):
  * kturns: device float64 [nf] = khat_f / (2 pi); ws_a / uhat / ws_b advance by
  * the given per-frequency strides (elements); frame_w: device c64 [nf] weights

@@ -185,7 +185,8 @@ class SrsdEngine(GraphedRun):
         def body(b0, b1, lane, ls):
             nb = b1 - b0
             uhat, xbuf = self.uhat_l[lane], self.xbuf_l[lane]
-            for fi in range(self.freqs.size):
+            order, dk = self.prop.freq_order(self.freqs, self.n_frames)
+            for fi in order:
                 for p in range(I):
                     _scaled_spectra(coeff[fi, p], g.ny, g.nx, py, px, self.tabs, b0, nb, xbuf,
                                     uhat[p * py * px:], I * py * px, self.transposed, ls)
@@ -193,7 +194,8 @@ class SrsdEngine(GraphedRun):
                 self.prop.run_frequency(dev.ptr(uhat), khat, dev.ptr(self.ill),
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
-                                        plane_hi=b1, stream=ls, lane=lane)
+                                        plane_hi=b1, stream=ls, lane=lane,
+                                        horner=None if dk is None else (dk, fi == order[-1]))
 
         self.prop.run_batches(body, stream)
         return vol
@@ -234,12 +236,14 @@ class _UhatPropEngine(GraphedRun):
             return vol
 
         def body(b0, b1, lane, ls):
-            for fi in range(self.freqs.size):
+            order, dk = self.prop.freq_order(self.freqs, self.n_frames)
+            for fi in order:
                 khat = float(self.freqs[fi]) / C
                 self.prop.run_frequency(dev.ptr(uhat) + 8 * fi * per_f, khat, dev.ptr(self.ill),
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
-                                        plane_hi=b1, stream=ls, lane=lane)
+                                        plane_hi=b1, stream=ls, lane=lane,
+                                        horner=None if dk is None else (dk, fi == order[-1]))
 
         self.prop.run_batches(body, stream)
         return vol

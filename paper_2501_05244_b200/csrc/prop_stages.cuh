@@ -135,12 +135,21 @@ __device__ __forceinline__ void st_b2(float2* sm, const pf_plane& pl, const pf_p
 __host__ __device__ constexpr bool cent_keep(int m) { return ((m + 8) & 31) < 16; }
 __host__ __device__ constexpr int cent_base(int m) { return (m + 8) & 31; }
 
-template <int L, bool MULTI, bool PRE, bool CENT = false>
+// HOR (single illumination, centred crop, prefetched single-frame volume): frequencies
+// arrive in DESCENDING order and the illumination phase exp(i k_f d) is applied by
+// Horner's rule, vol <- vol * z + v_f with z = exp(i dk d) (uniformly spaced k_f; dk d
+// is a few radians, so z is formed in float32), and on the last step (f = 0, HOR = 2,
+// kturns = k_0 / 2 pi) the sum is multiplied by exp(i k_0 d) in the float64-reduced form.
+// Same sum as the ascending per-frequency phases, in nested order.
+template <int L, bool MULTI, bool PRE, bool CENT = false, int HOR = 0>
 __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double kturns,
                                      const pf_prop_geom& g, const float2* __restrict__ tw,
                                      const float2* __restrict__ wb, const double* __restrict__ ill,
                                      const float2* __restrict__ frame_w, int n_frames,
-                                     float2* __restrict__ vol, long long vfs, int tile) {
+                                     float2* __restrict__ vol, long long vfs, int tile,
+                                     float dturns = 0.f) {
+  static_assert(HOR == 0 || (!MULTI && PRE && CENT), "Horner variant: one illumination, "
+                "centred crop, prefetched volume");
   constexpr int P = 32 * L;
   constexpr int LPW = 32 / L, RPC = 8 * LPW, SLD = RPC + 1;
   constexpr int UNION = (8 * WFFT_XCH > P * SLD) ? 8 * WFFT_XCH : P * SLD;
@@ -213,7 +222,7 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
 #pragma unroll
       for (int m = 0; m < 32; m++) {
         float2 val = v[m];   // 1/P^2 (a power of two: exact) is folded into the frame weight
-        if (cent_keep(m)) {
+        if (HOR == 0 && cent_keep(m)) {
           const double dx = fma(pl.dx, (double)(L * cent_base(m)), xt);
           val = cmul(val, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
         }
@@ -251,7 +260,29 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
     if (PRE) {
       const float2* old = volbuf + r * nx;
       const float2 fw = cscale(frame_w[0], scale);
-      if (CENT) {
+      if (CENT && HOR) {
+        float2* dt = vol + off + t;
+        const float2* ot = old + t;
+        const double dy = yv - ill[1], dz = pl.z - ill[2];
+        const double byz = fma(dy, dy, dz * dz);
+        const double xt = pl.x0 - ill[0] + pl.dx * t;
+        const float byzf = (float)byz;
+#pragma unroll
+        for (int m = 0; m < 32; m++) {
+          if (cent_keep(m)) {
+            const int base = L * cent_base(m);
+            const double dx = fma(pl.dx, (double)base, xt);
+            const float dxf = (float)dx;
+            const float d2 = fmaf(dxf, dxf, byzf);
+            const float tz = dturns * (d2 * rsqrtf(d2));
+            float zs, zc;
+            __sincosf(6.28318530717958647692f * (tz - rintf(tz)), &zs, &zc);
+            float2 nv = cadd(cmul(ot[base], make_float2(zc, zs)), cmul(v[m], fw));
+            if (HOR == 2) nv = cmul(nv, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
+            dt[base] = nv;
+          }
+        }
+      } else if (CENT) {
         float2* dt = vol + off + t;
         const float2* ot = old + t;
 #pragma unroll

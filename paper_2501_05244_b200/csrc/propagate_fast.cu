@@ -58,6 +58,20 @@ k_pc(const pf_plane* __restrict__ planes, double kturns, pf_prop_geom g,
                       frame_w, n_frames, vol, vol_frame_stride, blockIdx.x);
 }
 
+// C with the illumination phase by Horner's rule over descending frequencies (st_c HOR)
+template <int L, int HOR>
+__global__ void __launch_bounds__(FT, 2)
+k_pc_h(const pf_plane* __restrict__ planes, double kturns, float dturns, pf_prop_geom g,
+       const float2* __restrict__ tw, const float2* __restrict__ ws_b,
+       const double* __restrict__ ill, const float2* __restrict__ frame_w,
+       float2* __restrict__ vol) {
+  extern __shared__ float2 sm[];
+  const long long wb_plane = 32LL * L * g.ny;
+  st_c<L, false, true, true, HOR>(sm, planes[blockIdx.y], kturns, g, tw,
+                                  ws_b + blockIdx.y * wb_plane, ill, frame_w, 1, vol, 0,
+                                  blockIdx.x, dturns);
+}
+
 // ---- B split in two register-light kernels (128 registers, 16 warps/SM):
 // B1: in place on ws_a, each line = one At row (plane b, kx): mirror, y-FFT,
 //     keep ky <= P/2  ->  Ghat quadrant Gq[b][kx][ky] (Ghat is even in ky too).
@@ -560,4 +574,55 @@ extern "C" int pf_relay_spectra_fast(const void* src, int64_t nb, int ny, int nx
   }
   pf_set_error("pf_relay_spectra_fast: P must be 128, 256, 512 or 1024");
   return -1;
+}
+
+// Stage C with Horner's rule (see st_c): frequencies must be visited in descending order,
+// last = 1 on the lowest one (khat = k_0); dkhat = k_{f+1} - k_f (uniform spacing).
+// Eligible: register path, both crops centred, one illumination, illumination phase on,
+// single frame.  Returns 1 (and does nothing) when the geometry is not eligible.
+extern "C" int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, double khat,
+                                       double dkhat, int last, const pf_prop_geom* g,
+                                       const pf_fft_plan* plan_x, const void* ws_b,
+                                       const double* ill_xyz, const void* frame_w, void* vol,
+                                       void* stream) {
+  PF_ARG_CHECK(g && plan_x && plan_x->n == g->px && nplanes >= 1 && frame_w && vol,
+               "pf_prop_rows_out_horner: bad args");
+  const int L = pf_prop_fast_L(g);
+  const int P = 32 * L;
+  if (L == 0 || g->n_illum != 1 || !g->include_illum || 2 * g->nx != P || 2 * g->ny != P ||
+      2 * g->nu0x != -g->nx || 2 * g->nu0y != -g->ny)
+    return 1;
+  const float2* tw = (const float2*)plan_x->tw;
+  const double kturns = khat / PF_TWO_PI;
+  const float dturns = (float)(dkhat / PF_TWO_PI);
+  cudaStream_t st = (cudaStream_t)stream;
+#define PF_H_CASE(LL)                                                                          \
+  case LL: {                                                                                   \
+    constexpr int RPC = 8 * (32 / LL);                                                         \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      cudaFuncSetAttribute(k_pc_h<LL, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+      cudaFuncSetAttribute(k_pc_h<LL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+      attr = true;                                                                             \
+    }                                                                                          \
+    dim3 grid(pf_cdiv(g->ny, RPC), nplanes);                                                   \
+    const size_t sm = smem_c<LL>(g->nx, true);                                                 \
+    if (last)                                                                                  \
+      k_pc_h<LL, 2><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, (const float2*)ws_b, \
+                                          ill_xyz, (const float2*)frame_w, (float2*)vol);      \
+    else                                                                                       \
+      k_pc_h<LL, 1><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, (const float2*)ws_b, \
+                                          ill_xyz, (const float2*)frame_w, (float2*)vol);      \
+    PF_LAUNCH_CHECK("k_pc_h");                                                                 \
+    return 0;                                                                                  \
+  }
+  switch (L) {
+    PF_H_CASE(4)
+    PF_H_CASE(8)
+    PF_H_CASE(16)
+    PF_H_CASE(32)
+    default: break;
+  }
+#undef PF_H_CASE
+  return 1;
 }

@@ -44,6 +44,7 @@ _LANES = int(os.environ.get("PF_LANES", "2"))
 _FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "4"))
 _FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
 _FBATCH_GENERIC = os.environ.get("PF_FBATCH_GENERIC", "1") != "0"
+_HORNER = os.environ.get("PF_HORNER", "1") != "0"   # kernel C phases by Horner's rule
 _MEGA = os.environ.get("PF_MEGA", "0") == "1"   # measured slower
 _MEGA_LAG = int(os.environ.get("PF_MEGA_LAG", "2"))
 _MEGA_GP = int(os.environ.get("PF_MEGA_GP", "4"))
@@ -185,10 +186,30 @@ class Propagator:
         # register-FFT path (square power-of-two pads) consumes Uhat transposed
         self.transposed = bool(_lib.call("pf_prop_fast", ctypes.byref(g)))
 
+    def freq_order(self, freqs: np.ndarray, n_frames: int):
+        """(frequency visiting order, Horner spacing): descending with kernel C applying the
+        illumination phase by Horner's rule (pf_prop_rows_out_horner) when the geometry
+        allows it (register path, centred crops, one illumination, one frame, uniformly
+        spaced frequencies), else ascending and None."""
+        F = int(freqs.size)
+        g = self.geom
+        P = g.px
+        ok = (_HORNER and self.transposed and F >= 2 and n_frames == 1 and g.n_illum == 1
+              and g.include_illum and 2 * g.nx == P and 2 * g.ny == P
+              and 2 * g.nu0x == -g.nx and 2 * g.nu0y == -g.ny)
+        if ok:
+            d = np.diff(np.asarray(freqs, dtype=np.float64))
+            ok = bool(np.all(np.abs(d - d[0]) <= 1e-9 * abs(d[0])))
+        if not ok:
+            return list(range(F)), None
+        return list(range(F - 1, -1, -1)), float(d[0]) / SPEED_OF_LIGHT
+
     def run_frequency(self, uhat_ptr: int, khat: float, ill_ptr: int, frame_w_ptr: int,
                       n_frames: int, vol: torch.Tensor, vol_frame_stride: int,
                       plane_lo: int = 0, plane_hi: int | None = None, stream=None,
-                      uhat_ptr_for_batch=None, lane: int = 0) -> None:
+                      uhat_ptr_for_batch=None, lane: int = 0, horner=None) -> None:
+        """One frequency over planes [plane_lo, plane_hi).  horner=(dkhat, last): kernel C
+        by Horner's rule (frequencies visited in ``freq_order``)."""
         plane_hi = self.nplanes if plane_hi is None else plane_hi
         s = dev.stream_ptr(stream)
         gref = ctypes.byref(self.geom)
@@ -200,6 +221,13 @@ class Propagator:
             up = uhat_ptr if uhat_ptr_for_batch is None else uhat_ptr_for_batch(b0, nb)
             _lib.call("pf_prop_kernel_rows", pp, nb, khat, gref, self.plan_x.ref, wa, s)
             _lib.call("pf_prop_columns", pp, nb, gref, self.plan_y.ref, wa, up, wb, 0, s)
+            if horner is not None:
+                rc = _lib.call("pf_prop_rows_out_horner", pp, nb, khat, horner[0],
+                               int(horner[1]), gref, self.plan_x.ref, wb, ill_ptr, frame_w_ptr,
+                               dev.ptr(vol), s)
+                if rc != 0:
+                    raise _lib.PfError(f"pf_prop_rows_out_horner: not eligible ({rc})")
+                continue
             _lib.call("pf_prop_rows_out", pp, nb, khat, gref, self.plan_x.ref, wb, ill_ptr,
                       frame_w_ptr, n_frames, dev.ptr(vol), vol_frame_stride, s)
 
@@ -477,12 +505,14 @@ class RsdEngine(GraphedRun):
         uhat = self.uhat
 
         def body(b0, b1, lane, ls):
-            for fi in range(self.freqs.size):
+            order, dk = self.prop.freq_order(self.freqs, self.n_frames)
+            for fi in order:
                 khat = float(self.freqs[fi]) / SPEED_OF_LIGHT
                 self.prop.run_frequency(dev.ptr(uhat) + 8 * fi * per_f, khat, dev.ptr(self.ill),
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
-                                        plane_hi=b1, stream=ls, lane=lane)
+                                        plane_hi=b1, stream=ls, lane=lane,
+                                        horner=None if dk is None else (dk, fi == order[-1]))
 
         self.prop.run_batches(body, stream, lo, hi)
         return vol
@@ -520,12 +550,14 @@ class RsdEngine(GraphedRun):
         # plane batches outer, frequencies inner: the batch's volume slice stays
         # L2-resident across its ascending-frequency accumulation
         def body(b0, b1, lane, ls):
-            for fi in range(self.freqs.size):
+            order, dk = self.prop.freq_order(self.freqs, self.n_frames)
+            for fi in order:
                 khat = float(self.freqs[fi]) / SPEED_OF_LIGHT
                 self.prop.run_frequency(dev.ptr(uhat) + 8 * fi * per_f, khat, dev.ptr(self.ill),
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
-                                        plane_hi=b1, stream=ls, lane=lane)
+                                        plane_hi=b1, stream=ls, lane=lane,
+                                        horner=None if dk is None else (dk, fi == order[-1]))
 
         self.prop.run_batches(body, stream)
         return vol

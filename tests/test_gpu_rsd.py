@@ -244,6 +244,7 @@ def test_streaming_launch_matches_stage_launches(rng, monkeypatch, n, nz, n_ill,
     import importlib
     R = importlib.import_module("paper_2501_05244_b200.reconstruct")
     monkeypatch.setattr(R, "_FBATCH_BYTES", 0)
+    monkeypatch.setattr(R, "_HORNER", False)   # the streaming kernel uses per-frequency phases
     monkeypatch.setattr(R, "_MEGA_LAG", lag)
     monkeypatch.setattr(R, "_MEGA_GP", gp)
     p = 2.0 / n
@@ -264,3 +265,31 @@ def test_streaming_launch_matches_stage_launches(rng, monkeypatch, n, nz, n_ill,
     if n <= 128:
         ref = O.rsd(sl, grid, times=times)
         assert O.rel_l2(vol.cpu().numpy().reshape(ref.shape), ref) < TOL
+
+
+@pytest.mark.parametrize("n,nz,n_freq", [(64, 6, 5), (256, 4, 9), (512, 4, 32)])
+def test_horner_phases_match_per_frequency_phases(rng, monkeypatch, n, nz, n_freq):
+    """Kernel C with the illumination phase by Horner's rule over descending frequencies
+    (pf_prop_rows_out_horner) = the ascending per-frequency phases (reference
+    reconstruct.py:160-168), and both = the float64 oracle."""
+    import importlib
+    R = importlib.import_module("paper_2501_05244_b200.reconstruct")
+    monkeypatch.setattr(R, "_FBATCH_BYTES", 0)
+    p = 2.0 / n
+    g = pf.UniformGrid2D(n, n, p, p, -1 + p / 2, -1 + p / 2, 0.0)
+    sl = _random_slices(rng, pf.UniformRelay(g), n_freq=n_freq)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(n, n, nz, p, p, 0.4, g.x0, g.y0, 0.5))
+    eng = R.RsdEngine(sl, grid)
+    order, dk = eng.prop.freq_order(eng.freqs, 1)
+    assert dk is not None and order[0] == n_freq - 1
+    coeff = pf.phasor.device_coefficients(sl)
+    hor = eng.run(coeff).clone()
+    monkeypatch.setattr(R, "_HORNER", False)
+    asc = eng.run(coeff)
+    torch.cuda.synchronize()
+    # z = exp(i dk d) is formed in float32 and raised to the 31st power by the recurrence:
+    # ~4e-6 at 32 frequencies, 25x inside the 1e-4 gate
+    assert O.rel_l2(hor.cpu().numpy(), asc.cpu().numpy()) < 1e-5
+    if n <= 256:
+        ref = O.rsd(sl, grid)
+        assert O.rel_l2(hor.cpu().numpy().reshape(ref.shape), ref) < TOL
