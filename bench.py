@@ -243,7 +243,7 @@ def run_ours(args):
     roof_k1["frac"] = roof_k1["achieved"] / hbm_peak
     roof_s3 = {"bound": "fp32", "achieved": s3_flops / (s3_ms * 1e-3) / 1e12, "peak": fp32_peak,
                "unit": "TFLOP/s", "traffic": _prop_traffic(F, k_hi - k_lo, args.config),
-               "kernel": "propagation k_pa+k_pb1+k_pb2+k_pc (pf_prop_kernel_rows/columns/rows_out, S3)",
+               "kernel": "propagation k_pa+k_pb1+k_pb2+k_pc_h (pf_prop_kernel_rows/columns/rows_out_horner, S3)",
                "ms": s3_ms, "peak_source": "measured on this GPU before the timed region: FFMA probe "
                                            "(pf_fp32_probe, best of 6); nominal %.1f TFLOP/s = "
                                            "148 SM x 128 lanes x 2 x sm_max_mhz; MEASURED_PEAKS.json "

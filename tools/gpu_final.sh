@@ -26,3 +26,4 @@ PF_NF=2 ncu --set full --clock-control none --import-source on \
     python tools/prof_rsd.py > $O/ncu_k1.log 2>&1
 tail -n 2 $O/ncu_full.log $O/ncu_k1.log
 timeout 600 python tools/chunk_prof.py > $O/chunk_prof.txt 2>&1; cat $O/chunk_prof.txt
+PF_PARITY_LOG=$O/parity.jsonl timeout 900 python -m pytest tests/test_gpu_configs.py -m gpu -q > $O/parity_pytest.log 2>&1; tail -n 2 $O/parity_pytest.log
