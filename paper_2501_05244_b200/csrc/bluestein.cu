@@ -107,13 +107,17 @@ extern "C" int pf_bluestein_lines(const void* src, int64_t src_ps, int64_t src_l
 
 namespace {
 
-template <int L, bool XPASS>
+// CW: the SRSD window at compile time (M = Q/2 outputs, n_in = Q/4 inputs at o_in = Q/8:
+// the centred N-of-2N relay in a Q = 4N transform), so the zero inputs and the unused
+// outputs are constants the compiler folds out of the first and last radix-32 stages.
+template <int L, bool XPASS, bool CW = false>
 __global__ void __launch_bounds__(256, 2)
-k_bluestein_w(const float2* __restrict__ src, long long src_ps, long long src_ls, int n_in,
-              int o_in, float2* __restrict__ dst, long long dst_ps, long long dst_ls, int M,
+k_bluestein_w(const float2* __restrict__ src, long long src_ps, long long src_ls, int n_in_rt,
+              int o_in_rt, float2* __restrict__ dst, long long dst_ps, long long dst_ls, int M_rt,
               int nlines, int n_out_lines, const float2* __restrict__ tw,
               const float2* __restrict__ chirp, const float2* __restrict__ khat) {
   constexpr int Q = 32 * L, LPW = 32 / L, LPC = 8 * LPW;
+  const int M = CW ? Q / 2 : M_rt, n_in = CW ? Q / 4 : n_in_rt, o_in = CW ? Q / 8 : o_in_rt;
   extern __shared__ float2 sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = lane % L, line = lane / L;
@@ -202,16 +206,26 @@ int launch_bw(int xpass, const float2* src, long long src_ps, long long src_ls, 
   if (!attr) {
     cudaFuncSetAttribute(k_bluestein_w<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_bluestein_w<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_bluestein_w<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_bluestein_w<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   size_t sm = 8 * WFFT_XCH;
   if (xpass && (size_t)M * (LPC + 1) > sm) sm = (size_t)M * (LPC + 1);
   sm *= sizeof(float2);
   dim3 grid(pf_cdiv(nlines, LPC), nplanes);
-  (void)Q;
-  if (xpass)
+  const bool cw = 2 * M == Q && 4 * n_in == Q && 8 * o_in == Q;
+  if (xpass && cw)
+    k_bluestein_w<L, true, true><<<grid, 256, sm, st>>>(src, src_ps, src_ls, n_in, o_in, dst,
+                                                        dst_ps, dst_ls, M, nlines, 0, tw, chirp,
+                                                        khat);
+  else if (xpass)
     k_bluestein_w<L, true><<<grid, 256, sm, st>>>(src, src_ps, src_ls, n_in, o_in, dst, dst_ps,
                                                   dst_ls, M, nlines, 0, tw, chirp, khat);
+  else if (cw)
+    k_bluestein_w<L, false, true><<<grid, 256, sm, st>>>(src, src_ps, src_ls, n_in, o_in, dst,
+                                                         dst_ps, dst_ls, M, nlines, 0, tw, chirp,
+                                                         khat);
   else
     k_bluestein_w<L, false><<<grid, 256, sm, st>>>(src, src_ps, src_ls, n_in, o_in, dst, dst_ps,
                                                    dst_ls, M, nlines, 0, tw, chirp, khat);
