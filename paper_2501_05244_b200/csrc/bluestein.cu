@@ -153,7 +153,8 @@ k_bluestein_w(const float2* __restrict__ src, long long src_ps, long long src_ls
     }
   }
   float2* xch = sm + warp * WFFT_XCH;
-  wfft<L, -1>(v, xch, tw);
+  // CW: inputs only at q in [o_in, o_in + n_in) = [4L, 12L): m in [4, 12) for every lane
+  wfft<L, -1, false, CW>(v, xch, tw);
 #pragma unroll
   for (int m = 0; m < 32; m++) v[m] = cmul(v[m], __ldg(kh + t + L * m));
   wfft<L, 1>(v, xch, tw);

@@ -22,7 +22,31 @@ constexpr int WFFT_XCH = 32 * 33;  // float2 per warp exchange buffer
 // tw2[k1 * L + t] = W_n^{t k1} (one contiguous run per k1 across the lanes).
 // EARLY: issue the 31 twiddle loads before the first 32-point DFT so their
 // latency hides behind it (costs 62 registers; for kernels with headroom).
-template <int L, int DIR, bool EARLY = false>
+// 32-point DFT of a line whose only nonzero inputs are v[4..11] (the SRSD Bluestein
+// window: N relay samples centred in a 4N transform).  Same 4 x 8 factorisation as
+// Dft<32>: each radix-4 sub-DFT has a single nonzero input, so it is a broadcast with
+// quarter-turn rotations and costs nothing; the twiddles and the radix-8 level remain.
+template <int DIR>
+__device__ __forceinline__ void dft32_in4_12(float2 (&v)[32]) {
+  float2 out[32];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; k1++) {
+    float2 z[8];
+#pragma unroll
+    for (int n2 = 0; n2 < 8; n2++) {
+      const float2 y = n2 >= 4 ? v[n2] : twc<4, DIR>(v[8 + n2], k1);
+      z[n2] = twc<32, DIR>(y, n2 * k1);
+    }
+    Dft<8, DIR>::run(z);
+#pragma unroll
+    for (int k2 = 0; k2 < 8; k2++) out[k1 + 4 * k2] = z[k2];
+  }
+#pragma unroll
+  for (int m = 0; m < 32; m++) v[m] = out[m];
+}
+
+// PRUNE_IN: v[m] is zero for m outside [4, 12) (dft32_in4_12 for the first stage)
+template <int L, int DIR, bool EARLY = false, bool PRUNE_IN = false>
 __device__ __forceinline__ void wfft(float2 (&v)[32], float2* __restrict__ xch,
                                      const float2* __restrict__ tw_plan) {
   static_assert(L == 4 || L == 8 || L == 16 || L == 32, "L must be 4, 8, 16 or 32");
@@ -37,7 +61,7 @@ __device__ __forceinline__ void wfft(float2 (&v)[32], float2* __restrict__ xch,
 #pragma unroll
     for (int k1 = 1; k1 < 32; k1++) v[k1] = DIR < 0 ? cmul(v[k1], w[k1]) : cmulc(v[k1], w[k1]);
   } else {
-    Dft<32, DIR>::run(v);
+    if (PRUNE_IN) dft32_in4_12<DIR>(v); else Dft<32, DIR>::run(v);
     if (t != 0) {
 #pragma unroll
       for (int k1 = 1; k1 < 32; k1++) {
