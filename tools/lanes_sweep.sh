@@ -1,7 +1,7 @@
 # config-4 device step for stream-lane / plane-batch variants (PF_LANES, PF_BATCH_CAP)
 mkdir -p gpurun_out/lanes
 O=gpurun_out/lanes
-for c in "3 4" "2 4" "4 4" "2 8" "3 8" "2 6"; do
+for c in "2 4" "3 4" "1 4" "2 2" "3 2" "1 8"; do
   set -- $c
   PF_LANES=$1 PF_BATCH_CAP=$2 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e > $O/b_$1_$2.json 2> $O/b_$1_$2.err
   python -c "import json; d=json.load(open('$O/b_$1_$2.json')); print('lanes=$1 cap=$2', round(d['ms_per_step'],3), round(d['stage_ms']['propagation'],3))" || tail -3 $O/b_$1_$2.err
