@@ -190,11 +190,17 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
     {
       constexpr int CSTEP = PROP_MT / RPC;
       const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
-      if (CENT) {   // compile-time strides: every copy is base + immediate offset
-        const float2* q = src + c0 * (P / 2) + rr;
-        float2* d = sm + c0 * SLD + rr;
+      if (CENT) {
+        // 16-byte copies of row pairs: odd columns sit one slot later in the padded tile
+        // (col * SLD + (col & 1) + row), so every pair is 16-byte aligned on both sides;
+        // compile-time strides, every copy is base + immediate offset
+        constexpr int PSTEP = PROP_MT / (RPC / 2);
+        const int pr = threadIdx.x % (RPC / 2), c0p = threadIdx.x / (RPC / 2);
+        const float4* q = reinterpret_cast<const float4*>(src + c0p * (P / 2) + 2 * pr);
+        float4* d = reinterpret_cast<float4*>(sm + c0p * SLD + (c0p & 1) + 2 * pr);
 #pragma unroll
-        for (int k = 0; k < P / CSTEP; k++) cp_async8(d + k * CSTEP * SLD, q + k * CSTEP * (P / 2));
+        for (int k = 0; k < P / PSTEP; k++)
+          cp_async16(d + k * PSTEP * SLD / 2, q + k * PSTEP * (P / 2) / 2);
       } else if (rr < nr) {
         const float2* q = src + (long long)c0 * ny + rr;
         float2* d = sm + c0 * SLD + rr;
@@ -210,7 +216,7 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
     cp_async_wait_all();
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < 32; m++) v[m] = sm[(t + L * m) * SLD + r];
+    for (int m = 0; m < 32; m++) v[m] = sm[(t + L * m) * SLD + (CENT ? (t & 1) : 0) + r];
     __syncthreads();
     wfft<L, 1>(v, sm + warp * WFFT_XCH, tw);
     const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
