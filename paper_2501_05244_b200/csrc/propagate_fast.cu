@@ -178,20 +178,38 @@ k_pcf(const pf_plane* __restrict__ planes, pf_prop_geom g, const float2* __restr
   const int f_lo = (int)((long long)blockIdx.z * fb.nf / gridDim.z);
   const int f_hi = (int)((long long)(blockIdx.z + 1) * fb.nf / gridDim.z);
   const int n_tiles = (f_hi - f_lo) * n_ill;
+  // full tile of an even-height crop at even offsets: 16-byte copies (see load_tile)
+  const bool pairs = nr == RPC && (ny & 1) == 0 && (fb.ws_b_fs & 1) == 0;
+  const int sh = pairs ? (t & 1) : 0;   // (t + L m) & 1 == t & 1 (L even)
   auto load_tile = [&](int idx, float2* dst) {
     const int f = f_lo + idx / n_ill, p = idx % n_ill;
     const float2* src = ws_b + f * fb.ws_b_fs +
                         ((long long)blockIdx.y * g.n_illum + p) * (long long)P * ny + i0;
-    constexpr int CSTEP = 32 * NW / RPC;
-    const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
-    if (rr < nr) {
-      const float2* q = src + (long long)c0 * ny + rr;
-      float2* d = dst + c0 * SLD + rr;
+    if (pairs) {
+      // 16-byte row pairs; odd columns sit one slot later in the padded tile so both
+      // sides stay 16-byte aligned (the reads below add the same offset)
+      constexpr int PSTEP = 32 * NW / (RPC / 2);
+      const int pr = threadIdx.x % (RPC / 2), c0p = threadIdx.x / (RPC / 2);
+      const float4* q = reinterpret_cast<const float4*>(src + (long long)c0p * ny + 2 * pr);
+      float4* d = reinterpret_cast<float4*>(dst + c0p * SLD + (c0p & 1) + 2 * pr);
 #pragma unroll 8
-      for (int col = c0; col < P; col += CSTEP) {
-        cp_async8(d, q);
-        q += (long long)CSTEP * ny;
-        d += CSTEP * SLD;
+      for (int col = c0p; col < P; col += PSTEP) {
+        cp_async16(d, q);
+        q += (long long)PSTEP * ny / 2;
+        d += PSTEP * SLD / 2;
+      }
+    } else {
+      constexpr int CSTEP = 32 * NW / RPC;
+      const int rr = threadIdx.x % RPC, c0 = threadIdx.x / RPC;
+      if (rr < nr) {
+        const float2* q = src + (long long)c0 * ny + rr;
+        float2* d = dst + c0 * SLD + rr;
+#pragma unroll 8
+        for (int col = c0; col < P; col += CSTEP) {
+          cp_async8(d, q);
+          q += (long long)CSTEP * ny;
+          d += CSTEP * SLD;
+        }
       }
     }
     cp_async_commit();
@@ -213,7 +231,7 @@ k_pcf(const pf_plane* __restrict__ planes, pf_prop_geom g, const float2* __restr
     __syncthreads();
     float2 v[32];
 #pragma unroll
-    for (int m = 0; m < 32; m++) v[m] = cur[(t + L * m) * SLD + r];
+    for (int m = 0; m < 32; m++) v[m] = cur[(t + L * m) * SLD + sh + r];
     __syncthreads();   // the tile is refilled by the load issued in the next iteration
     wfft<L, 1>(v, xch + warp * WFFT_XCH, tw);
     const double kturns = fb.kturns[f];
