@@ -165,13 +165,20 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
   const float scale = 1.0f / ((float)P * (float)P);
   const long long vol_row0 = (pl.vol_plane * ny + i0) * (long long)nx;
   const bool aligned = ((g.nu0x | nx) & (L - 1)) == 0;   // column crop uniform per m
-  if (PRE && CENT) {   // rows of P/2 elements starting at a multiple of P/2: 16-byte aligned
+  // rows of P/2 elements starting at a multiple of P/2: 16-byte copies.  One illumination:
+  // issued after the tile (LATE_VOL), so the transform waits only for the tile and the
+  // volume rows arrive while it runs
+  constexpr bool LATE_VOL = PRE && CENT && !MULTI;
+  auto prefetch_vol = [&]() {
     const float4* src = reinterpret_cast<const float4*>(vol + vol_row0);
     float4* dst = reinterpret_cast<float4*>(volbuf);
 #pragma unroll
     for (int e = threadIdx.x; e < RPC * (P / 4); e += PROP_MT) cp_async16(dst + e, src + e);
     cp_async_commit();
-  } else if (PRE) {
+  };
+  if (PRE && CENT && !LATE_VOL) {
+    prefetch_vol();
+  } else if (PRE && !CENT) {
     for (int rr = 0; rr < nr; rr++) {
       const float2* src = vol + vol_row0 + (long long)rr * nx;
 #pragma unroll 4
@@ -213,7 +220,12 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
       }
     }
     cp_async_commit();
-    cp_async_wait_all();
+    if (LATE_VOL) {
+      prefetch_vol();
+      cp_async_wait_1();   // the tile group; the volume group stays in flight
+    } else {
+      cp_async_wait_all();
+    }
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < 32; m++) v[m] = sm[(t + L * m) * SLD + (CENT ? (t & 1) : 0) + r];
@@ -260,6 +272,10 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
         v[m] = val;
       }
     }
+  }
+  if (LATE_VOL) {   // volume rows copied by other threads: complete and visible
+    cp_async_wait_all();
+    __syncthreads();
   }
   if (i < ny) {
     const long long off = vol_row0 + (long long)r * nx;
