@@ -155,6 +155,8 @@ def run_ours(args):
     # on a side stream while the next chunk computes
     n_chunks = rec.gather_chunks
 
+    final = {}
+
     def step():
         ev[0].record(stream)
         rec.temporal.run(hist_shard.view(-1, T), local_shard.view(F, -1), stream)
@@ -162,13 +164,14 @@ def run_ours(args):
         coeff = sgather(local_shard) if world > 1 else local_shard
         ev[2].record(stream)
         if n_chunks > 1:
-            rec.propagate_and_gather(coeff, rec.vol, stream)
+            final["vol"] = rec.propagate_and_gather(coeff, rec.vol, stream)
             ev[3].record(stream)
         else:
             eng.run_graphed(coeff, rec.vol, stream)
+            final["vol"] = rec.vol
             ev[3].record(stream)
             if world > 1:
-                vgather(rec.vol)
+                final["vol"] = vgather(rec.vol)
         ev[4].record(stream)
 
     for _ in range(args.warmup):
@@ -200,6 +203,11 @@ def run_ours(args):
             t_step.append(ev[0].elapsed_time(ev[4]))
         end.record(stream)
         torch.cuda.synchronize()
+    vol_digest = None
+    if rank == 0 and final.get("vol") is not None:
+        import hashlib
+        # bytes of the last timed step's (gathered) volume: identical for every N
+        vol_digest = hashlib.sha256(final["vol"].cpu().numpy().tobytes()).hexdigest()[:16]
     launches = (_lib.launches() - launches0) // max(1, args.steps)
     launches += eng_graph_launches(eng, n_chunks)
     # with flushes between steps the region also holds the flush writes: use the
@@ -275,6 +283,8 @@ def run_ours(args):
         "e2e": e2e_line,
         "gpu_launches": int(launches),
         "clocks": clocks,
+        "volume_sha256_16": vol_digest,
+        "dist_backend": (dist.get_backend() if world > 1 else None),
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample(cfg, kernel, hist_shard, rec, args)
@@ -548,6 +558,24 @@ def run_reference(args):
     }), flush=True)
 
 
+def _respawn(args) -> bool:
+    """``--gpus N`` without a launcher: re-exec this script under torch.distributed.run with
+    N ranks (one per GPU, rendezvous on 127.0.0.1). Returns True when it did (the caller
+    exits with the launcher's status)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stderr.write("bench: --gpus %d without WORLD_SIZE: %s\n" % (args.gpus, " ".join(cmd)))
+    rc = subprocess.call(cmd)
+    sys.exit(rc)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -559,6 +587,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true",
                     help="skip the end-to-end leg (for ncu launch lists of the device step)")
     args = ap.parse_args()
+    _respawn(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -187,26 +187,6 @@ int pf_prop_fbatch_generic(const pf_plane* planes, int nplanes, const double* kh
                            const void* uhat, int64_t uhat_fs, void* ws_b, int64_t ws_b_fs,
                            const double* ill_xyz, const void* frame_w, void* vol, void* stream);
 
-/* Streaming propagation: all (plane, frequency) jobs of a register-path
- * reconstruction in one persistent launch (same stages and results as
- * pf_prop_kernel_rows / pf_prop_columns / pf_prop_rows_out per frequency).
- * jobs: device int32 [njobs][4] = {plane, f, prev, 0} where prev is the job
- * index of (plane, f-1) or -1 (volume rows accumulate in that order);
- * kturns: device float64 [F] = khat_f / (2 pi); uhat: transposed spectra,
- * frequency f at uhat + f*uhat_fs; frame_w: device c64 [F][n_frames];
- * ws_a / ws_b: pf_prop_mega_ws(g, slots, 0 / 1) elements; slots >= 3 lag + 2;
- * counters: device int32 [4 njobs + 2] (zeroed by the call).
- * Replaces the per-(frequency, plane) loop of rsd reconstruct.py:254-266,
- * srsd :312-325 and nursd1 :372-383 (register path only). */
-int64_t pf_prop_mega_ws(const pf_prop_geom* g, int slots, int which);
-int pf_prop_mega(const pf_plane* planes, const int32_t* jobs, int njobs, const double* kturns,
-                 const pf_prop_geom* g, const pf_fft_plan* plan, const void* uhat,
-                 int64_t uhat_fs, const double* ill_xyz, const void* frame_w, int n_frames,
-                 void* vol, int64_t vol_frame_stride, void* ws_a, void* ws_b, int slots, int lag,
-                 int32_t* counters, void* stream);
-/* After the stream synchronised: 1 if the launch abandoned a dependency wait. */
-int pf_prop_mega_aborted(const int32_t* counters, int njobs);
-
 /* out (device int32[2]) = {number of non-finite, number of negative} float32
  * values in x[0..n): the payload checks of reference read_dataset
  * (core.py:727-728, NaN/inf) and TransientMeasurement (counts >= 0) for

@@ -74,10 +74,6 @@ _SIGNATURES = {
     "pf_nufft_interp2_batch": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _i64, _i64,
                                _i, _vp, _d, _i, _f, _vp, _i, _vp, _i64, _vp],
     "pf_scatter_csr": [_vp, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp, _i64, _vp],
-    "pf_prop_mega_ws": [_P(PfPropGeom), _i, _i],
-    "pf_prop_mega": [_vp, _vp, _i, _vp, _P(PfPropGeom), _P(PfFftPlan), _vp, _i64, _vp, _vp, _i,
-                     _vp, _i64, _vp, _vp, _i, _i, _vp, _vp],
-    "pf_prop_mega_aborted": [_vp, _i],
     "pf_bluestein_lines": [_vp, _i64, _i64, _i64, _i, _i, _vp, _i64, _i64, _i64, _i, _i, _i, _i,
                            _P(PfFftPlan), _vp, _vp, _vp],
     "pf_bluestein_warp": [_i, _vp, _i64, _i64, _i, _i, _vp, _i64, _i64, _i, _i, _i, _P(PfFftPlan),
@@ -97,7 +93,7 @@ _SIGNATURES = {
     "pf_prop_rows_out": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp,
                          _i64, _vp],
 }
-_RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_mega_ws": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
+_RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
              "pf_prop_ws_spectrum": ctypes.c_int64,
              "pf_prop_fast": ctypes.c_int}
 

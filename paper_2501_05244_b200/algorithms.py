@@ -222,7 +222,7 @@ class _UhatPropEngine(GraphedRun):
                             k - k_lo) for k in range(k_lo, k_hi)]
         self.prop = Propagator(self.device, px, py, vg.nx, vg.ny, _center_nu0(vg.nx),
                                _center_nu0(vg.ny), self.n_illum, include_illumination, planes,
-                               py * px)
+                               py * px, n_planes_total=vg.nz)
         self.n_voxels = (k_hi - k_lo) * vg.nx * vg.ny
 
     def _propagate(self, uhat, vol, stream):
@@ -230,9 +230,6 @@ class _UhatPropEngine(GraphedRun):
         if self.prop.fbatch_ok(self.freqs.size, self.n_frames):
             self.prop.run_fbatch(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w, vol,
                                  stream)
-            return vol
-        if self.prop.run_mega(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w,
-                              self.n_frames, vol, self.n_voxels, stream):
             return vol
 
         def body(b0, b1, lane, ls):

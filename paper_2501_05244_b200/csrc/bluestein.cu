@@ -76,10 +76,9 @@ extern "C" int pf_bluestein_lines(const void* src, int64_t src_ps, int64_t src_l
   PF_ARG_CHECK(plan_q && plan_q->n >= 2 * M - 1 && M >= 1 && nlines >= 0 && nplanes >= 1,
                "pf_bluestein_lines: bad args");
   if (nlines == 0) return 0;
-  static bool attr = false;
-  if (!attr) {
+  static PfDevOnce attr;  
+  if (attr.first()) {
     cudaFuncSetAttribute(k_bluestein, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   const size_t per = 2 * (size_t)pf_ld(plan_q->n) * sizeof(float2);
   int cnt = (int)((200 * 1024) / per);
@@ -203,13 +202,12 @@ int launch_bw(int xpass, const float2* src, long long src_ps, long long src_ls, 
               float2* dst, long long dst_ps, long long dst_ls, int M, int nlines, int nplanes,
               const float2* tw, const float2* chirp, const float2* khat, cudaStream_t st) {
   constexpr int LPC = 8 * (32 / L), Q = 32 * L;
-  static bool attr = false;
-  if (!attr) {
+  static PfDevOnce attr;  
+  if (attr.first()) {
     cudaFuncSetAttribute(k_bluestein_w<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_bluestein_w<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_bluestein_w<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_bluestein_w<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   size_t sm = 8 * WFFT_XCH;
   if (xpass && (size_t)M * (LPC + 1) > sm) sm = (size_t)M * (LPC + 1);

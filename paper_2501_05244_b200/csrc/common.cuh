@@ -52,6 +52,18 @@ __device__ __forceinline__ int natural(long long c, int n) {
 // Thread-local last-error message; every extern "C" entry point returns 0 on
 // success, <0 for an argument error, >0 for a CUDA error.
 void pf_set_error(const char* fmt, ...);
+
+// One-time-per-device guard for cudaFuncSetAttribute (the attribute is per device, so a
+// process driving several GPUs must set it on each): `if (attr.first()) {...}`.
+struct PfDevOnce {
+  unsigned long long done = 0;   // bit d: device d already configured
+  bool first() {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long b = 1ull << (d & 63);
+    return (__atomic_fetch_or(&done, b, __ATOMIC_ACQ_REL) & b) == 0;
+  }
+};
 // process-wide count of kernel launches (one per PF_LAUNCH_CHECK; pf_launch_count)
 void pf_note_launch();
 

@@ -74,11 +74,10 @@ __global__ void k_embed_centered(const float2* __restrict__ src, long long nb, i
 template <int DIR>
 int launch_lines(float2* data, const pf_fft_plan& p, long long nlines, long long inner,
                  long long istr, long long ostr, long long estr, float scale, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static PfDevOnce attr;  
+  if (attr.first()) {
     cudaFuncSetAttribute(k_fft_lines<DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)FL_SMEM_BUDGET);
-    attr = true;
   }
   const int ld = pf_ld(p.n);
   const size_t per_line = 2 * (size_t)ld * sizeof(float2);

@@ -130,11 +130,10 @@ int run_t1(const float2* fine, long long fine_stride, int nv, float2* rt, const 
   const size_t sm_r = (size_t)(8 * WFFT_XCH > H * (RPC + 1) ? 8 * WFFT_XCH : H * (RPC + 1)) *
                       sizeof(float2);
   const size_t sm_c = 8 * WFFT_XCH * sizeof(float2);
-  static bool attr = false;
-  if (!attr) {
+  static PfDevOnce attr;  
+  if (attr.first()) {
     cudaFuncSetAttribute(k_t1_rows<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_t1_cols<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   for (int v0 = 0; v0 < nv; v0 += 65535) {
     const int n = nv - v0 < 65535 ? nv - v0 : 65535;

@@ -275,12 +275,11 @@ static int prop_fbatch_generic(const pf_plane* planes, int nplanes, const double
                                const void* uhat, int64_t uhat_fs, void* ws_b, int64_t ws_b_fs,
                                const double* ill, const void* frame_w, void* vol,
                                cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static PfDevOnce attr;  
+  if (attr.first()) {
     allow_smem(k_prop_kernel_rows);
     allow_smem(k_prop_columns);
     allow_smem(k_prop_rows_out_fb);
-    attr = true;
   }
   const int rows_a = g->py / 2 + 1, cols_a = g->px / 2 + 1;
   // many lines per CTA: every Stockham stage then has work for all threads
@@ -353,8 +352,8 @@ extern "C" int pf_prop_kernel_rows(const pf_plane* planes, int nplanes, double k
   if (pf_prop_fast_L(g))
     return pf_prop_fast_stage(0, planes, nplanes, khat, g, plan_x, nullptr, ws_a, nullptr, nullptr,
                               nullptr, nullptr, nullptr, 0, nullptr, 0, (cudaStream_t)stream);
-  static bool attr = false;
-  if (!attr) { allow_smem(k_prop_kernel_rows); attr = true; }
+  static PfDevOnce attr;  
+  if (attr.first()) { allow_smem(k_prop_kernel_rows); }
   const int rows_a = g->py / 2 + 1;
   int rpc = rows_fit(g->px, 2, (2 * PT + g->px - 1) / g->px);
   if (rpc < 1) { pf_set_error("pf_prop_kernel_rows: px too large"); return -1; }
@@ -375,8 +374,8 @@ extern "C" int pf_prop_columns(const pf_plane* planes, int nplanes, const pf_pro
   if (pf_prop_fast_L(g))
     return pf_prop_fast_stage(1, planes, nplanes, 0.0, g, plan_y, ws_a, nullptr, uhat, nullptr,
                               ws_b, nullptr, nullptr, 0, nullptr, 0, (cudaStream_t)stream);
-  static bool attr = false;
-  if (!attr) { allow_smem(k_prop_columns); attr = true; }
+  static PfDevOnce attr;  
+  if (attr.first()) { allow_smem(k_prop_columns); }
   const int cols_a = g->px / 2 + 1;
   int cpc = rows_fit(g->py, 3, 8);
   if (cpc < 1) { pf_set_error("pf_prop_columns: py too large"); return -1; }
@@ -399,8 +398,8 @@ extern "C" int pf_prop_rows_out(const pf_plane* planes, int nplanes, double khat
     return pf_prop_fast_stage(2, planes, nplanes, khat, g, plan_x, nullptr, nullptr, nullptr, ws_b,
                               nullptr, ill_xyz, frame_w, n_frames, vol, vol_frame_stride,
                               (cudaStream_t)stream);
-  static bool attr = false;
-  if (!attr) { allow_smem(k_prop_rows_out); attr = true; }
+  static PfDevOnce attr;  
+  if (attr.first()) { allow_smem(k_prop_rows_out); }
   int rpc = rows_fit(g->px, 2, (2 * PT + g->px - 1) / g->px);
   if (rpc < 1) { pf_set_error("pf_prop_rows_out: px too large"); return -1; }
   dim3 grid(pf_cdiv(g->ny, rpc), nplanes);

@@ -310,8 +310,8 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
               int n_frames, float2* vol, long long vfs, cudaStream_t st,
               FBatch fb = FBatch{nullptr, 0, 0, 0, 1}) {
   constexpr int NA = 32 * L / 2 + 1, RPC = 8 * (32 / L), LPW = 32 / L;
-  static bool attr = false;
-  if (!attr) {
+  static PfDevOnce attr;  
+  if (attr.first()) {
     const int big = 200 * 1024;
     cudaFuncSetAttribute(k_pa<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_pb1<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -331,7 +331,6 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     cudaFuncSetAttribute(k_pcf<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
     cudaFuncSetAttribute(k_pcf<L, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
     cudaFuncSetAttribute(k_pcf<L, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
-    attr = true;
   }
   const double kturns = khat / PF_TWO_PI;
   if (stage == 0) {   // A: kernel rows -> At
@@ -490,11 +489,10 @@ int run_relay_spectra(const float2* src, long long nb, int ny, int nx, long long
   const size_t sm_r = (size_t)(8 * WFFT_XCH > P * (RPC + 1) ? 8 * WFFT_XCH : P * (RPC + 1)) *
                       sizeof(float2);
   const size_t sm_c = 8 * WFFT_XCH * sizeof(float2);
-  static bool attr = false;
-  if (!attr) {
+  static PfDevOnce attr;  
+  if (attr.first()) {
     cudaFuncSetAttribute(k_us_rows<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_us_cols<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   for (long long b0 = 0; b0 < nb; b0 += 65535) {
     const int n = (int)(nb - b0 < 65535 ? nb - b0 : 65535);
@@ -608,8 +606,11 @@ extern "C" int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, doub
   const int L = pf_prop_fast_L(g);
   const int P = 32 * L;
   if (L == 0 || g->n_illum != 1 || !g->include_illum || 2 * g->nx != P || 2 * g->ny != P ||
-      2 * g->nu0x != -g->nx || 2 * g->nu0y != -g->ny)
+      2 * g->nu0x != -g->nx || 2 * g->nu0y != -g->ny) {
+    pf_set_error("pf_prop_rows_out_horner: geometry not eligible (register pad, one "
+                 "illumination, centred crop of half the pad)");
     return 1;
+  }
   const float2* tw = (const float2*)plan_x->tw;
   const double kturns = khat / PF_TWO_PI;
   const float dturns = (float)(dkhat / PF_TWO_PI);
@@ -617,11 +618,10 @@ extern "C" int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, doub
 #define PF_H_CASE(LL)                                                                          \
   case LL: {                                                                                   \
     constexpr int RPC = 8 * (32 / LL);                                                         \
-    static bool attr = false;                                                                  \
-    if (!attr) {                                                                               \
+    static PfDevOnce attr;                                                                    \
+    if (attr.first()) {                                                                               \
       cudaFuncSetAttribute(k_pc_h<LL, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
       cudaFuncSetAttribute(k_pc_h<LL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      attr = true;                                                                             \
     }                                                                                          \
     dim3 grid(pf_cdiv(g->ny, RPC), nplanes);                                                   \
     const size_t sm = smem_c<LL>(g->nx, true);                                                 \
@@ -642,5 +642,6 @@ extern "C" int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, doub
     default: break;
   }
 #undef PF_H_CASE
+  pf_set_error("pf_prop_rows_out_horner: no register FFT for L = %d", L);
   return 1;
 }

@@ -83,7 +83,7 @@ k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __
   }
   const int nk = __popcll(mask);
   const int ts = nk * MP + (((4 - nk * MP) % 16) + 16) % 16;
-  if (ts > ts_cap) __trap();         // shared memory was sized for fewer bins (bad n_inner)
+  if (ts > ts_cap) return;   // unreachable: the launcher checks the bin set on the host
   for (int f = threadIdx.x; f < F; f += K1_THREADS) {
     const int k = bins[f] & 63;
     const int kk = k > 32 ? 64 - k : k;
@@ -301,16 +301,16 @@ int launch_k1(const float* hist, long long n_traces, const int* bins, const floa
   // [0, 32]) when given, else the worst case
   inner_mask &= (1ull << 33) - 1ull;
   const int n_inner = __builtin_popcountll(inner_mask);
-  int nk = (n_inner >= 1 && n_inner <= K1_KB) ? n_inner : K1_KB;
-  if (nk > FC) nk = FC;
+  // (the kernel parks exactly inner_mask's bins when it is given, else at most min(33, FC)
+  // per chunk, so ts <= ts_cap by construction)
+  int nk = n_inner >= 1 ? n_inner : (K1_KB < FC ? K1_KB : FC);
   constexpr int MP = M + 2 - (M & 1);
   const int ts_cap = nk * MP + 15;   // per-trace stride incl. the bank-alignment pad
   const size_t smem = ((size_t)G * ts_cap + (size_t)FC * MP) * sizeof(float2) +
                       ((FC + 1) & ~1) * sizeof(int);
-  static bool attr = false;
-  if (!attr) {
+  static PfDevOnce attr;  
+  if (attr.first()) {
     cudaFuncSetAttribute(k_temporal_dft<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
   }
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -354,11 +354,10 @@ int launch_k1_tma(const float* hist, long long n_traces, const int* bins, const 
   }
 #define K1_TMA(GG, SS)                                                                        \
   if (G == GG && S == SS) {                                                                   \
-    static bool attr = false;                                                                 \
-    if (!attr) {                                                                              \
+    static PfDevOnce attr;                                                                   \
+    if (attr.first()) {                                                                              \
       cudaFuncSetAttribute(k_temporal_tma<GG, SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            220 * 1024);                                                       \
-      attr = true;                                                                            \
     }                                                                                         \
     int per = 0;                                                                              \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_temporal_tma<GG, SS>, GG * 64, smem); \
@@ -419,11 +418,10 @@ extern "C" int pf_temporal_dft_direct(const float* hist, int64_t n_traces, int n
   PF_ARG_CHECK(n_traces >= 0 && n_freq >= 1 && n_bins >= 1, "pf_temporal_dft_direct: bad sizes");
   PF_ARG_CHECK(n_bins <= 50 * 1024, "pf_temporal_dft_direct: n_bins too large");
   if (n_traces == 0) return 0;
-  static bool attr = false;
-  if (!attr) {
+  static PfDevOnce attr;  
+  if (attr.first()) {
     cudaFuncSetAttribute(k_temporal_dft_direct, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    attr = true;
   }
   const int grid = (int)(n_traces < 4096 ? n_traces : 4096);
   k_temporal_dft_direct<<<grid, K1_THREADS, n_bins * sizeof(float), (cudaStream_t)stream>>>(

@@ -2,9 +2,9 @@
 
 One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch on the box,
 gloo in the CPU tests).  The work partitions without a data-path exchange
-inside the propagation: every voxel's ascending-frequency sum lives on the
-rank that owns its depth plane, so results are bitwise independent of the
-number of GPUs.  The two exchanges are at the edges of the path:
+inside the propagation: every voxel's frequency sum (in the fixed order the
+whole-grid geometry selects) lives on the rank that owns its depth plane, so
+results are bitwise independent of the number of GPUs.  The two exchanges are at the edges of the path:
 
 * K1 shards the detectors; the frequency slices (64 MiB at config 4) are
   all-gathered so every rank holds ``[F, I, D]`` (the north star's "frequency

@@ -13,9 +13,13 @@ nursd2/3, hyb.  ... -> product -> type-2 NUFFT readout      reconstruct.py:413-5
 nursd3d         3D type-1 -> 3D conv -> slab -> propagate   reconstruct.py:722-765
 ==============  =========================================  ==========================
 
-Accumulation is in ascending frequency order then illumination order, per
-voxel, so results are bit-reproducible run to run and independent of how depth
-planes are batched or sharded.  ``threads`` is accepted and ignored (the
+Accumulation order per voxel is fixed by the geometry: ascending frequency then
+illumination (reference order), or descending frequency when kernel C applies the
+illumination phase by Horner's rule (one illumination, uniform bins, register pads).
+Every path choice is made from the whole grid, never from a shard, so results are
+bit-reproducible run to run and independent of how depth planes are batched or
+sharded across GPUs; different paths (e.g. frequency-batched vs per-frequency
+launches) round differently in fp32.  ``threads`` is accepted and ignored (the
 reference uses it only to parallelise the per-frequency terms).
 """
 
@@ -45,9 +49,6 @@ _FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "4"))
 _FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
 _FBATCH_GENERIC = os.environ.get("PF_FBATCH_GENERIC", "1") != "0"
 _HORNER = os.environ.get("PF_HORNER", "1") != "0"   # kernel C phases by Horner's rule
-_MEGA = os.environ.get("PF_MEGA", "0") == "1"   # measured slower
-_MEGA_LAG = int(os.environ.get("PF_MEGA_LAG", "2"))
-_MEGA_GP = int(os.environ.get("PF_MEGA_GP", "4"))
 
 
 # ---------------------------------------------------------------------------
@@ -147,8 +148,12 @@ class Propagator:
     """
 
     def __init__(self, device, px, py, nx, ny, nu0x, nu0y, n_illum, include_illum,
-                 planes: list, uhat_illum_stride: int, batch: int | None = None):
+                 planes: list, uhat_illum_stride: int, batch: int | None = None,
+                 n_planes_total: int | None = None):
         self.device = device
+        # path choices (frequency batching) follow the whole grid, not this shard, so a
+        # plane-sharded engine runs the same arithmetic as the single-GPU one
+        self.n_planes_total = int(n_planes_total or len(planes))
         g = _lib.PfPropGeom()
         g.px, g.py, g.nx, g.ny = int(px), int(py), int(nx), int(ny)
         g.nu0x, g.nu0y = int(nu0x), int(nu0y)
@@ -222,11 +227,9 @@ class Propagator:
             _lib.call("pf_prop_kernel_rows", pp, nb, khat, gref, self.plan_x.ref, wa, s)
             _lib.call("pf_prop_columns", pp, nb, gref, self.plan_y.ref, wa, up, wb, 0, s)
             if horner is not None:
-                rc = _lib.call("pf_prop_rows_out_horner", pp, nb, khat, horner[0],
-                               int(horner[1]), gref, self.plan_x.ref, wb, ill_ptr, frame_w_ptr,
-                               dev.ptr(vol), s)
-                if rc != 0:
-                    raise _lib.PfError(f"pf_prop_rows_out_horner: not eligible ({rc})")
+                # a nonzero status (geometry not eligible) raises PfError in _lib.call
+                _lib.call("pf_prop_rows_out_horner", pp, nb, khat, horner[0], int(horner[1]),
+                          gref, self.plan_x.ref, wb, ill_ptr, frame_w_ptr, dev.ptr(vol), s)
                 continue
             _lib.call("pf_prop_rows_out", pp, nb, khat, gref, self.plan_x.ref, wb, ill_ptr,
                       frame_w_ptr, n_frames, dev.ptr(vol), vol_frame_stride, s)
@@ -238,7 +241,7 @@ class Propagator:
             return False
         g = self.geom
         per = 8 * ((g.py // 2 + 1) * (g.px // 2 + 1) + g.n_illum * g.ny * g.px)
-        return n_freq * self.nplanes * per <= _FBATCH_BYTES
+        return n_freq * self.n_planes_total * per <= _FBATCH_BYTES
 
     def run_fbatch(self, uhat: torch.Tensor, uhat_fs: int, freqs: np.ndarray, ill_ptr: int,
                    frame_w: torch.Tensor, vol: torch.Tensor, stream=None) -> None:
@@ -269,55 +272,6 @@ class Propagator:
                   nf, ctypes.byref(g), self.plan_x.ref, dev.ptr(self._fb_ws_a), fa, dev.ptr(uhat),
                   uhat_fs, dev.ptr(self._fb_ws_b), fbs, ill_ptr, dev.ptr(frame_w), dev.ptr(vol),
                   dev.stream_ptr(stream))
-
-    def run_mega(self, uhat: torch.Tensor, uhat_fs: int, freqs: np.ndarray, ill_ptr: int,
-                 frame_w: torch.Tensor, n_frames: int, vol: torch.Tensor, vol_frame_stride: int,
-                 stream=None) -> bool:
-        """All (plane, frequency) jobs in one persistent launch (``pf_prop_mega``).
-
-        Jobs run in groups of ``_MEGA_GP`` planes, frequencies ascending inside a
-        group, so a group's volume slice and each Uhat_f stay L2-resident.
-        Returns False when the register path does not apply.
-        """
-        if not (_MEGA and self.transposed):
-            return False
-        g = self.geom
-        nf = int(freqs.size)
-        key = (nf, n_frames)
-        if getattr(self, "_mega_key", None) != key:
-            lag = max(1, _MEGA_LAG)
-            slots = 3 * lag + 2
-            jobs, last = [], {}
-            for p0 in range(0, self.nplanes, max(1, _MEGA_GP)):
-                grp = range(p0, min(self.nplanes, p0 + max(1, _MEGA_GP)))
-                for f in range(nf):
-                    for p in grp:
-                        jobs.append((p, f, last.get(p, -1), 0))
-                        last[p] = len(jobs) - 1
-            self._mega_jobs = torch.tensor(jobs, dtype=torch.int32, device=self.device)
-            self._mega_kt = torch.from_numpy(np.asarray(freqs, dtype=np.float64)
-                                             / (SPEED_OF_LIGHT * 2 * np.pi)).to(self.device)
-            gref = ctypes.byref(g)
-            self._mega_wa = torch.empty(_lib.call("pf_prop_mega_ws", gref, slots, 0),
-                                        dtype=torch.complex64, device=self.device)
-            self._mega_wb = torch.empty(_lib.call("pf_prop_mega_ws", gref, slots, 1),
-                                        dtype=torch.complex64, device=self.device)
-            self._mega_ctr = torch.zeros(4 * len(jobs) + 2, dtype=torch.int32, device=self.device)
-            self._mega_cfg = (len(jobs), slots, lag)
-            self._mega_key = key
-        njobs, slots, lag = self._mega_cfg
-        _lib.call("pf_prop_mega", dev.ptr(self.planes_dev), dev.ptr(self._mega_jobs), njobs,
-                  dev.ptr(self._mega_kt), ctypes.byref(g), self.plan_x.ref, dev.ptr(uhat),
-                  uhat_fs, ill_ptr, dev.ptr(frame_w), n_frames, dev.ptr(vol), vol_frame_stride,
-                  dev.ptr(self._mega_wa), dev.ptr(self._mega_wb), slots, lag,
-                  dev.ptr(self._mega_ctr), dev.stream_ptr(stream))
-        return True
-
-    def mega_aborted(self) -> bool:
-        """True if the last persistent launch gave up on a dependency (after a sync)."""
-        if getattr(self, "_mega_cfg", None) is None:
-            return False
-        return bool(_lib.call("pf_prop_mega_aborted", dev.ptr(self._mega_ctr), self._mega_cfg[0]))
 
     def run_batches(self, body, stream=None, lo: int = 0, hi: int | None = None) -> None:
         """Call ``body(b0, b1, lane, lane_stream)`` for every plane batch of [lo, hi),
@@ -479,7 +433,7 @@ class RsdEngine(GraphedRun):
         planes = [PlaneSpec(zs[k] - g.z, g.dx, g.dy, vg.x0, vg.dx, vg.y0, vg.dy, zs[k],
                             0, k - k_lo) for k in range(k_lo, k_hi)]
         self.prop = Propagator(self.device, px, py, vg.nx, vg.ny, nu0x, nu0y, self.n_illum,
-                               include_illumination, planes, py * px)
+                               include_illumination, planes, py * px, n_planes_total=vg.nz)
         self.ill = _ill_tensor(slices, self.device)
         self.frame_w = _frame_weights(self.freqs, self.times, self.device)
         self.n_frames = 1 if self.times is None else self.times.size
@@ -541,10 +495,6 @@ class RsdEngine(GraphedRun):
         if self.prop.fbatch_ok(self.freqs.size, self.n_frames):
             self.prop.run_fbatch(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w, vol,
                                  stream)
-            return vol
-
-        if self.prop.run_mega(uhat, per_f, self.freqs, dev.ptr(self.ill), self.frame_w,
-                              self.n_frames, vol, self.n_voxels, stream):
             return vol
 
         # plane batches outer, frequencies inner: the batch's volume slice stays

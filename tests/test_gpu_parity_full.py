@@ -1,0 +1,151 @@
+"""North-star parity at BASELINE size: whole volumes against the float64 oracle.
+
+configs 3 (srsd, 128 frustum planes), 4 (rsd, 256 planes, 67 M voxels) and 5 (nursd1 on
+131,072 lattice nodes, 256 planes) are compared over EVERY voxel, and the argmax of
+``project_max_depth`` (reference reconstruct.py:834-836) is taken over all planes; config 2
+(16,384-point non-planar relay, T = 4096, 1e6 explicit voxels) against the composed oracle
+(reference nursd3d stage 1 reconstruct.py:741-760, then nursd2 :413-459).  The oracle
+runs process-parallel on the host cores (``oracle_pool``; each split is the unsplit
+arithmetic).  Gates (BASELINE north_star): relative L2 <= 1e-4 on the complex volume
+(GPU complex64 vs oracle complex128) and an identical argmax; the reference image's
+top-2 gap is logged ($PF_PARITY_LOG) to expose near-ties.
+"""
+
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2501_05244_b200 as pf
+from oracle import pf_oracle as O
+from oracle_pool import oracle_freq_terms, oracle_planes
+from paper_2501_05244_b200 import configs
+from paper_2501_05244_b200.algorithms import Nursd1Engine, Nursd3dExplicitEngine, SrsdEngine
+from paper_2501_05244_b200.reconstruct import RsdEngine
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def _slices(cfg):
+    hist = configs.transients(cfg, device=torch.device("cuda"))
+    k = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
+    coeff = pf.to_frequency_device(hist, k, cfg.t0)
+    del hist
+    sl = pf.DeviceFrequencySlices(k.frequencies, coeff, cfg.relay, cfg.illuminations)
+    return sl, k
+
+
+def _top2_gap(img):
+    top2 = np.sort(img.ravel())[-2:]
+    return float((top2[1] - top2[0]) / top2[1])
+
+
+def _log(rec):
+    log = os.environ.get("PF_PARITY_LOG")
+    if log:
+        with open(log, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+
+
+def _check_volume(name, got, ref, shape, t_gpu, t_oracle):
+    rel = O.rel_l2(got, ref)
+    a = np.abs(got.reshape(shape)).max(axis=0)
+    b = np.abs(ref.reshape(shape)).max(axis=0)
+    ia, ib = int(np.argmax(a)), int(np.argmax(b))
+    # per-plane argmax agreement (informative: single planes can hold near-ties)
+    pa = np.abs(got.reshape(shape)).reshape(shape[0], -1).argmax(axis=1)
+    pb = np.abs(ref.reshape(shape)).reshape(shape[0], -1).argmax(axis=1)
+    _log({"case": name, "rel_l2": rel, "argmax_same": ia == ib,
+          "argmax_yx": [int(v) for v in np.unravel_index(ib, b.shape)],
+          "top2_gap": _top2_gap(b), "per_plane_argmax_same": int((pa == pb).sum()),
+          "planes": int(shape[0]), "shape": list(shape), "voxels": int(np.prod(shape)),
+          "gpu_s": t_gpu, "oracle_s": t_oracle, "oracle_procs": _procs()})
+    assert rel < TOL, rel
+    assert ia == ib, f"argmax differs (reference top-2 gap {_top2_gap(b):.3e})"
+
+
+def _procs():
+    from oracle_pool import n_procs
+    return n_procs()
+
+
+def _run_gpu(eng, coeff):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    v = eng.run(coeff)
+    torch.cuda.synchronize()
+    return v[0].cpu().numpy(), time.perf_counter() - t
+
+
+def test_config3_srsd_full_volume():
+    cfg = configs.config(3)
+    sl, k = _slices(cfg)
+    assert k.n_freq == 24
+    eng = SrsdEngine(sl, cfg.grid)
+    got, tg = _run_gpu(eng, sl.device_coefficients)
+    t = time.perf_counter()
+    ref = oracle_planes("srsd", sl.to_host(), cfg.grid, cfg.grid.n_planes)
+    _check_volume("config3-srsd-full", got, ref, (128, 256, 256), tg, time.perf_counter() - t)
+
+
+def test_config4_rsd_full_volume():
+    cfg = configs.config(4)
+    sl, k = _slices(cfg)
+    assert k.n_freq == 32
+    eng = RsdEngine(sl, cfg.grid)
+    assert eng.px == 1024          # GPU pad; the oracle uses the reference pad (1050)
+    got, tg = _run_gpu(eng, sl.device_coefficients)
+    del eng
+    torch.cuda.empty_cache()
+    t = time.perf_counter()
+    ref = oracle_planes("rsd", sl.to_host(), cfg.grid, 256)
+    _check_volume("config4-rsd-full", got, ref, (256, 512, 512), tg, time.perf_counter() - t)
+
+
+def test_config5_nursd1_full_volume():
+    cfg = configs.config(5)
+    sl, k = _slices(cfg)
+    eng = Nursd1Engine(sl, cfg.grid)
+    got, tg = _run_gpu(eng, sl.device_coefficients)
+    del eng
+    torch.cuda.empty_cache()
+    t = time.perf_counter()
+    ref = oracle_planes("nursd1", sl.to_host(), cfg.grid, 256)
+    _check_volume("config5-nursd1-full", got, ref, (256, 512, 512), tg, time.perf_counter() - t)
+
+
+def test_config2_composed_full_size():
+    """16,384 relay points, T = 4096, 16 frequencies, 1e6 voxels in 64 planes."""
+    cfg = configs.config(2)
+    sl, k = _slices(cfg)
+    assert k.n_freq == 16 and cfg.grid.count == 1_000_000
+    eng = Nursd3dExplicitEngine(sl, cfg.grid, cfg.lattice)
+    vol = torch.zeros((1, cfg.grid.count), dtype=torch.complex64, device="cuda")
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    eng.run(sl.device_coefficients, vol)
+    torch.cuda.synchronize()
+    tg = time.perf_counter() - t
+    got = vol[0].cpu().numpy()
+    host = sl.to_host()
+    t = time.perf_counter()
+    ref = oracle_freq_terms("nursd3d_explicit", host, (cfg.grid, cfg.lattice),
+                            z_pitch=host.shortest_wavelength / 2.0)
+    to = time.perf_counter() - t
+    rel = O.rel_l2(got, ref)
+    ia, ib = int(np.argmax(np.abs(got))), int(np.argmax(np.abs(ref)))
+    # per plane (64 planes of 15,625 random voxels): argmax agreement, informative
+    cnt = [len(p.points.points) for p in cfg.grid.planes]
+    edges = np.cumsum([0] + cnt)
+    same = sum(int(np.argmax(np.abs(got[a:b])) == np.argmax(np.abs(ref[a:b])))
+               for a, b in zip(edges[:-1], edges[1:]))
+    _log({"case": "config2-nursd3d-explicit-full", "rel_l2": rel, "argmax_same": ia == ib,
+          "top2_gap": _top2_gap(np.abs(ref)), "per_plane_argmax_same": same,
+          "planes": len(cnt), "voxels": int(got.size), "gpu_s": tg, "oracle_s": to,
+          "oracle_procs": _procs()})
+    assert rel < TOL, rel
+    assert ia == ib, f"argmax differs (top-2 gap {_top2_gap(np.abs(ref)):.3e})"

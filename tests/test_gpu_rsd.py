@@ -233,40 +233,6 @@ def test_graphed_run_matches_eager(rng):
     assert eng.graph_kernels > 0
 
 
-@pytest.mark.parametrize("n,nz,n_ill,video,lag,gp", [
-    (64, 7, 1, False, 2, 4),      # P = 128 (L = 4), plane count not a multiple of the group
-    (64, 5, 2, False, 1, 3),      # two illuminations (MULTI), shortest lag
-    (128, 4, 1, True, 2, 4),      # P = 256, time-resolved frames (no volume prefetch)
-    (512, 3, 1, False, 3, 2),     # P = 1024 (L = 32), the config-4 kernel shape
-])
-def test_streaming_launch_matches_stage_launches(rng, monkeypatch, n, nz, n_ill, video, lag, gp):
-    """pf_prop_mega (one persistent launch) reproduces the per-stage launches bit for bit."""
-    import importlib
-    R = importlib.import_module("paper_2501_05244_b200.reconstruct")
-    monkeypatch.setattr(R, "_FBATCH_BYTES", 0)
-    monkeypatch.setattr(R, "_HORNER", False)   # the streaming kernel uses per-frequency phases
-    monkeypatch.setattr(R, "_MEGA_LAG", lag)
-    monkeypatch.setattr(R, "_MEGA_GP", gp)
-    p = 2.0 / n
-    g = pf.UniformGrid2D(n, n, p, p, -1 + p / 2, -1 + p / 2, 0.0)
-    sl = _random_slices(rng, pf.UniformRelay(g), n_freq=5, n_ill=n_ill)
-    grid = pf.CuboidGrid(pf.UniformGrid3D(n, n, nz, p, p, 0.3, g.x0, g.y0, 0.4))
-    times = np.array([0.0, 1e-10]) if video else None
-    eng = R.RsdEngine(sl, grid, times=times)
-    assert eng.prop.transposed
-    coeff = pf.phasor.device_coefficients(sl)
-    monkeypatch.setattr(R, "_MEGA", False)
-    staged = eng.run(coeff).clone()
-    monkeypatch.setattr(R, "_MEGA", True)
-    vol = eng.run(coeff)
-    torch.cuda.synchronize()
-    assert not eng.prop.mega_aborted()
-    assert torch.equal(vol, staged)
-    if n <= 128:
-        ref = O.rsd(sl, grid, times=times)
-        assert O.rel_l2(vol.cpu().numpy().reshape(ref.shape), ref) < TOL
-
-
 @pytest.mark.parametrize("n,nz,n_freq", [(64, 6, 5), (256, 4, 9), (512, 4, 32)])
 def test_horner_phases_match_per_frequency_phases(rng, monkeypatch, n, nz, n_freq):
     """Kernel C with the illumination phase by Horner's rule over descending frequencies
