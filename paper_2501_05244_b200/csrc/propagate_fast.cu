@@ -147,6 +147,114 @@ k_pb2(const pf_plane* __restrict__ planes, int nplanes, pf_prop_geom g,
   }
 }
 
+// B1 and B2 fused: line = (plane b, kx) of the kernel quadrant.  The mirrored At row is
+// y-transformed to the Ghat column kx (even in ky: lanes keep the ky <= P/2 outputs and
+// take the rest from the mirror lane by shuffle), then for each illumination and each of
+// the output columns kx and P - kx it is multiplied by the Uhat^T column, y-inverted and
+// stored row-cropped to Tt.  The Ghat quadrant never leaves the SM (B1's in-place
+// quadrant write and B2's two mirrored reads of it are gone, and so is one launch).
+// CTA lines: pbc planes x (NL / pbc) consecutive kx, so the lines of one kx (same Uhat^T
+// columns) run in the same CTA.
+template <int L, bool MULTI, bool CENT>
+__global__ void __launch_bounds__(FT, 2)
+k_pb12(const pf_plane* __restrict__ planes, int nplanes, int pbc, pf_prop_geom g,
+       const float2* __restrict__ tw, const float2* __restrict__ ws_a,
+       const float2* __restrict__ uhat_t, float2* __restrict__ ws_b, FBatch fb) {
+  ws_a += blockIdx.z * fb.ws_a_fs;
+  uhat_t += blockIdx.z * fb.uhat_fs;
+  ws_b += blockIdx.z * fb.ws_b_fs;
+  constexpr int P = 32 * L, H = P / 2, NA = H + 1;
+  constexpr int LPW = 32 / L, NL = 8 * LPW;
+  extern __shared__ float2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const int li = warp * LPW + line;
+  const int kxc = NL / pbc;
+  const int bl = li % pbc, kxl = li / pbc;
+  const int b = blockIdx.y * pbc + bl;
+  const int kx_raw = blockIdx.x * kxc + kxl;
+  const bool valid = b < nplanes && kxl < kxc && kx_raw < NA;
+  const int bb = b < nplanes ? b : nplanes - 1;
+  const int kx = kx_raw < H ? kx_raw : H;
+  const pf_plane pl = planes[bb];
+  float2 gq[17];   // Ghat[t + L m], m <= 16 (ky <= P/2 for m < 16, and m = 16 at t = 0)
+  {
+    const float2* arow = ws_a + ((long long)bb * NA + kx) * NA;
+    float2 v[32];
+#pragma unroll
+    for (int m = 0; m < 32; m++) {
+      const int jy = t + L * m;
+      v[m] = __ldg(m < 16 ? arow + jy : arow + (P - jy));
+    }
+    wfft<L, -1>(v, sm + warp * WFFT_XCH, tw);
+#pragma unroll
+    for (int m = 0; m <= 16; m++) gq[m] = v[m];
+  }
+  // Ghat[t + L m] for m > 16 = Ghat[P - t - L m] = lane (L - t)'s gq[31 - m] (t > 0), or
+  // this lane's gq[32 - m] (t = 0)
+  const int mirror = (lane - t) + ((L - t) & (L - 1));
+  const int ny = g.ny;
+  const int n_ill = MULTI ? g.n_illum : 1;
+  const bool aligned = ((g.nu0y | ny) & (L - 1)) == 0;
+#pragma unroll 1
+  for (int p = 0; p < n_ill; p++) {
+#pragma unroll 1
+    for (int side = 0; side < 2; side++) {
+      const int col = side == 0 ? kx : (P - kx) & (P - 1);
+      if (LPW == 1 && side == 1 && col == kx) break;   // warp-uniform (one line per warp)
+      const bool active = valid && !(side == 1 && col == kx);
+      const float2* ucol = uhat_t + pl.uhat_off + (long long)p * g.uhat_illum_stride +
+                           (long long)col * P;
+      float2 w[32];
+#pragma unroll
+      for (int m = 0; m < 32; m++) {
+        float2 gm;
+        if (m <= 16) {
+          gm = gq[m];
+        } else {
+          const float2 o = make_float2(__shfl_sync(0xffffffffu, gq[31 - m].x, mirror),
+                                       __shfl_sync(0xffffffffu, gq[31 - m].y, mirror));
+          gm = t == 0 ? gq[32 - m] : o;
+        }
+        w[m] = cmul(gm, __ldg(ucol + t + L * m));
+      }
+      wfft<L, 1>(w, sm + warp * WFFT_XCH, tw);
+      if (active) {
+        float2* dcol = ws_b + ((long long)bb * g.n_illum + p) * (long long)P * ny +
+                       (long long)col * ny;
+        if (CENT) {
+          float2* dt = dcol + t;
+#pragma unroll
+          for (int m = 0; m < 32; m++)
+            if (cent_keep(m)) dt[L * cent_base(m)] = w[m];
+        } else if (aligned) {
+          float2* dt = dcol + t;
+#pragma unroll
+          for (int m = 0; m < 32; m++) {
+            const int base = (L * m - g.nu0y) & (P - 1);
+            if (base < ny) dt[base] = w[m];
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < 32; m++) {
+            const int i = (t + L * m - g.nu0y) & (P - 1);
+            if (i < ny) dcol[i] = w[m];
+          }
+        }
+      }
+    }
+  }
+}
+
+static bool b12_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PF_B12");
+    on = (e == nullptr || atoi(e) != 0) ? 1 : 0;
+  }
+  return on == 1;
+}
+
 // C over all frequencies of the batch in one launch: per (plane, row tile) the
 // ascending-frequency sum is formed in registers and written once.
 // NW warps per CTA (RPC = NW * 32/L rows): small volumes (config 0: 64 planes x
@@ -319,6 +427,10 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     cudaFuncSetAttribute(k_pb2<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_pb2<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_pb2<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb12<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb12<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb12<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_pb12<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
 #define PF_PC_ATTR(M, PR, C) \
     cudaFuncSetAttribute(k_pc<L, M, PR, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     PF_PC_ATTR(false, false, false) PF_PC_ATTR(true, false, false)
@@ -339,12 +451,25 @@ int run_stage(int stage, const pf_plane* planes, int nplanes, double khat, const
     PF_LAUNCH_CHECK("k_pa");
   } else if (stage == 1) {   // B1 (Ghat quadrant in place) + B2 (product, y-IFFT, crop)
     const size_t sm = 8 * WFFT_XCH * sizeof(float2);
+    const bool cent_y = 2 * g.ny == 32 * L && 2 * g.nu0y == -g.ny;
+    if (b12_enabled()) {   // B1 + B2 fused
+      const int pbc = nplanes < 8 * LPW ? nplanes : 8 * LPW;
+      dim3 g12(pf_cdiv(NA, (8 * LPW) / pbc), pf_cdiv(nplanes, pbc), fb.nf);
+      if (g.n_illum > 1) {
+        if (cent_y) k_pb12<L, true, true><<<g12, FT, sm, st>>>(planes, nplanes, pbc, g, tw, ws_a, uhat, ws_b_out, fb);
+        else k_pb12<L, true, false><<<g12, FT, sm, st>>>(planes, nplanes, pbc, g, tw, ws_a, uhat, ws_b_out, fb);
+      } else {
+        if (cent_y) k_pb12<L, false, true><<<g12, FT, sm, st>>>(planes, nplanes, pbc, g, tw, ws_a, uhat, ws_b_out, fb);
+        else k_pb12<L, false, false><<<g12, FT, sm, st>>>(planes, nplanes, pbc, g, tw, ws_a, uhat, ws_b_out, fb);
+      }
+      PF_LAUNCH_CHECK("k_pb12");
+      return 0;
+    }
     dim3 g1(pf_cdiv(NA, 8 * LPW), nplanes, fb.nf);
     k_pb1<L><<<g1, FT, sm, st>>>(nplanes, tw, const_cast<float2*>(ws_a), fb);
     PF_LAUNCH_CHECK("k_pb1");
     dim3 g2(NA, pf_cdiv(2 * nplanes, 8 * LPW), fb.nf);
     // centred row crop (output lattice = relay lattice): compile-time kept rows
-    const bool cent_y = 2 * g.ny == 32 * L && 2 * g.nu0y == -g.ny;
     if (g.n_illum > 1) {
       if (cent_y) k_pb2<L, true, true><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
       else k_pb2<L, true, false><<<g2, FT, sm, st>>>(planes, nplanes, g, tw, ws_a, uhat, ws_b_out, fb);
