@@ -44,7 +44,7 @@ ALGORITHM_NAMES = ("rsd", "srsd", "nursd1", "nursd2", "nursd3", "rsd3d", "nursd3
 
 # workspace budget per propagation batch: keep ws_a + ws_b L2-resident (126 MB L2)
 _BATCH_BYTES = 64 << 20
-_LANES = int(os.environ.get("PF_LANES", "2"))
+_LANES = int(os.environ.get("PF_LANES", "3"))
 _FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "4"))
 _FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
 _FBATCH_GENERIC = os.environ.get("PF_FBATCH_GENERIC", "1") != "0"
