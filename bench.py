@@ -95,6 +95,11 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def _n_planes(grid):
+    return {"frustum": lambda g: g.n_planes, "explicit": lambda g: len(g.planes)}.get(
+        grid.kind, lambda g: g.grid.nz)(grid)
+
+
 def _dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -131,7 +136,10 @@ def run_ours(args):
     hist = configs.transients(cfg, device=device)            # [1, D, T] float32, identical per rank
     I, D, T = hist.shape
     F = kernel.n_freq
-    nz = cfg.grid.n_planes if cfg.grid.kind == "frustum" else cfg.grid.grid.nz
+    nz = _n_planes(cfg.grid)
+    explicit = cfg.grid.kind == "explicit"
+    if explicit and world > 1:
+        raise SystemExit("bench: config %d (explicit voxels) runs on one GPU" % args.config)
     d_lo, d_hi = shard_range(D, world, rank)
     k_lo, k_hi = shard_range(nz, world, rank)
     hist_shard = hist[:, d_lo:d_hi].contiguous()
@@ -145,7 +153,8 @@ def run_ours(args):
     rec = TransientReconstructor(kernel, cfg.relay, cfg.illuminations, cfg.grid, t0=cfg.t0,
                                  plane_range=(k_lo, k_hi), device=device,
                                  trace_range=(d_lo, d_hi), slice_gather=sgather,
-                                 volume_gather=vgather, algorithm=cfg.algorithm)
+                                 volume_gather=vgather, algorithm=cfg.algorithm,
+                                 lattice=getattr(cfg, "lattice", None))
     eng = rec.engine
     local_shard = rec.coeff
     stream = torch.cuda.current_stream()
@@ -467,7 +476,7 @@ def cpu_baseline_sample(cfg, kernel, hist_dev, rec, args):
     from oracle import pf_oracle as O
 
     F = kernel.n_freq
-    nz = cfg.grid.n_planes if cfg.grid.kind == "frustum" else cfg.grid.grid.nz
+    nz = _n_planes(cfg.grid)
     n_tr = 4096
     h = hist_dev.view(-1, cfg.n_bins)[:n_tr].cpu().numpy().astype(np.float64)
     t = time.perf_counter()
@@ -475,6 +484,18 @@ def cpu_baseline_sample(cfg, kernel, hist_dev, rec, args):
     t1 = (time.perf_counter() - t) * (hist_dev.shape[1] / n_tr)
     coeff = rec.coeff.permute(1, 2, 0).cpu().numpy().astype(np.complex128)
     sl = _HostSlices(kernel.frequencies, coeff, cfg.relay, cfg.illuminations)
+    if cfg.algorithm == "nursd3d-explicit":
+        # composed oracle (stage 1 + nursd2) on one frequency, single core, times F
+        from oracle.pool import _OneFreq
+        t = time.perf_counter()
+        O.nursd3d_explicit(_OneFreq(sl, 0), cfg.grid, cfg.lattice,
+                           z_pitch=sl.shortest_wavelength / 2.0)
+        t3 = (time.perf_counter() - t) * F
+        return {"value": cfg.n_voxels / (t1 + t3), "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"oracle.to_frequency on {n_tr} of {hist_dev.shape[1]} traces + the "
+                          f"composed oracle (nursd3d stage 1 + nursd2) for 1 of {F} frequencies; "
+                          f"per-trace and per-frequency linear extrapolation",
+                "s1_s": t1, "s3_s": t3}
     fn = {"rsd": O.rsd, "srsd": O.srsd, "nursd1": O.nursd1}[cfg.algorithm]
     # per-frequency setup (relay spectrum / NUFFT) and per-plane cost separated by
     # timing 1 and 3 planes per frequency, then extrapolated to F x Nz
@@ -505,6 +526,10 @@ class _HostSlices:
         self.relay = relay
         self.illuminations = ill
         self.n_freq = self.frequencies.size
+
+    @property
+    def shortest_wavelength(self):
+        return 2.0 * math.pi * 299792458.0 / float(self.frequencies.max())
 
 
 _REF_STATE = {}
@@ -539,13 +564,15 @@ def run_reference(args):
     cfg = configs.config(args.config)
     kernel = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
     F = kernel.n_freq
-    nz = cfg.grid.n_planes if cfg.grid.kind == "frustum" else cfg.grid.grid.nz
+    nz = _n_planes(cfg.grid)
     D = cfg.relay.count
     rng = np.random.default_rng(cfg.seed)
     # S3 cost is data-independent FFT work: seeded random-phase coefficients stand in
     coeff = np.exp(2j * np.pi * rng.random((1, D, F)))
     sl = _HostSlices(kernel.frequencies, coeff, cfg.relay, cfg.illuminations)
     ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    if cfg.algorithm == "nursd3d-explicit":
+        return _run_reference_explicit(args, cfg, kernel, sl, ncores, world)
     n_tr = 2048
     h = rng.poisson(2.0, size=(n_tr, cfg.n_bins)).astype(np.float64)
     units = [(i % F, (3 * i) % max(1, nz - 3)) for i in range(ncores)]
@@ -599,6 +626,44 @@ def _respawn(args) -> bool:
     sys.stderr.write("bench: --gpus %d without WORLD_SIZE: %s\n" % (args.gpus, " ".join(cmd)))
     rc = subprocess.call(cmd)
     sys.exit(rc)
+
+
+def _run_reference_explicit(args, cfg, kernel, sl, ncores, world):
+    """Config 2: the whole composed oracle (nursd3d stage 1 + nursd2, every frequency,
+    every voxel) per step, frequencies spread over the host cores and added in ascending
+    order (oracle.pool); plus to_frequency on a trace sample."""
+    from oracle import pf_oracle as O
+    from oracle.pool import oracle_freq_terms
+    F, D = kernel.n_freq, cfg.relay.count
+    n_tr = 2048
+    h = np.random.default_rng(1).poisson(2.0, size=(n_tr, cfg.n_bins)).astype(np.float64)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        oracle_freq_terms("nursd3d_explicit", sl, (cfg.grid, cfg.lattice), procs=ncores,
+                          z_pitch=sl.shortest_wavelength / 2.0)
+        t3 = time.perf_counter() - t
+        t = time.perf_counter()
+        O.to_frequency(h, kernel.bin_indices, kernel.frequencies, kernel.weights, cfg.t0)
+        t1 = (time.perf_counter() - t) * D / n_tr / ncores
+        if it >= args.warmup:
+            times.append(t3 + t1)
+    est = statistics.mean(times)
+    value = cfg.n_voxels / est
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c128 (float64)", "data": "synthetic (seeded random-phase slices, Poisson hist)",
+        "config": {"workload": f"config{args.config}-{cfg.algorithm}", "voxels": cfg.n_voxels,
+                   "pad": "reference pad rules"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
+                         "sample": f"per step: the full composed oracle over all {F} frequencies "
+                                   f"and {cfg.n_voxels} voxels ({min(ncores, F)} processes, one "
+                                   f"frequency each) + to_frequency on {n_tr} traces, "
+                                   f"extrapolated to {D} traces"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
 
 
 def main():

@@ -1,4 +1,5 @@
-"""Process-parallel CPU oracle for the full-size parity tests (test infrastructure).
+"""Process-parallel CPU oracle (TEST INFRASTRUCTURE: the full-size parity tests and the
+reference arm of bench.py; never imported by the product package).
 
 The float64 oracle (``oracle/pf_oracle.py``) computes every (frequency, plane) unit
 independently, so a full BASELINE-size volume is split across the host cores:

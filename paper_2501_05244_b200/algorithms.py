@@ -837,6 +837,8 @@ class Nursd3dExplicitEngine(GraphedRun):
                                               relay=vrel, illuminations=slices.illuminations))()
         self.stage2 = Nursd2Engine(meta, grid, eps, times, include_illumination, self.device)
         self.times, self.n_frames = self.stage2.times, self.stage2.n_frames
+        self.n_voxels = self.stage2.n_voxels
+        self.px, self.py = px, py
         F, I = self.stage2.freqs.size, self.stage2.n_illum
         self.slot = torch.empty((F * I * py * px,), dtype=torch.complex64, device=self.device)
 

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _device as dev
-from .core import ReconstructionVolume
+from .core import SPEED_OF_LIGHT, ReconstructionVolume
 from .phasor import TemporalPlan
 from .reconstruct import RsdEngine
 
@@ -31,11 +31,23 @@ class _Meta:
         self.illuminations = illuminations
         self.n_freq = int(self.frequencies.size)
 
+    @property
+    def shortest_wavelength(self) -> float:
+        return 2.0 * np.pi * SPEED_OF_LIGHT / float(self.frequencies.max())
+
 
 def make_engine(algorithm, meta, grid, device, plane_range=None, times=None,
-                include_illumination=True, padding="exact", eps=1e-6):
-    """Device engine (``run(coeff, vol, stream)``) for a cuboid/frustum algorithm."""
+                include_illumination=True, padding="exact", eps=1e-6, lattice=None):
+    """Device engine (``run(coeff, vol, stream)``) for a cuboid/frustum algorithm, or the
+    non-planar relay -> explicit voxels composition ("nursd3d-explicit", needs the stage-1
+    ``lattice``; one GPU, no plane sharding)."""
     name = algorithm.replace("_", "-").lower()
+    if name == "nursd3d-explicit":
+        from .algorithms import Nursd3dExplicitEngine
+        if plane_range is not None and tuple(plane_range) != (0, len(grid.planes)):
+            raise ValueError("nursd3d-explicit does not shard depth planes")
+        return Nursd3dExplicitEngine(meta, grid, lattice, eps, None, times,
+                                     include_illumination, device=device)
     if name == "rsd":
         return RsdEngine(meta, grid, padding, include_illumination, times, device=device,
                          plane_range=plane_range)
@@ -59,13 +71,13 @@ class TransientReconstructor:
     def __init__(self, kernel, relay, illuminations, grid, t0: float = 0.0, padding="exact",
                  include_illumination=True, times=None, plane_range=None, chunks: int = 8,
                  device=None, trace_range=None, slice_gather=None, volume_gather=None,
-                 algorithm="rsd", eps=1e-6):
+                 algorithm="rsd", eps=1e-6, lattice=None):
         self.device = device or dev.require_cuda()
         self.kernel = kernel
         self.grid = grid
         self.meta = _Meta(kernel, relay, illuminations)
         self.engine = make_engine(algorithm, self.meta, grid, self.device, plane_range, times,
-                                  include_illumination, padding, eps)
+                                  include_illumination, padding, eps, lattice)
         self.temporal = TemporalPlan(kernel, t0, self.device)
         self.n_illum = illuminations.count
         self.n_det = relay.count

@@ -21,7 +21,7 @@ import torch
 
 import paper_2501_05244_b200 as pf
 from oracle import pf_oracle as O
-from oracle_pool import oracle_freq_terms, oracle_planes
+from oracle.pool import oracle_freq_terms, oracle_planes
 from paper_2501_05244_b200 import configs
 from paper_2501_05244_b200.algorithms import Nursd1Engine, Nursd3dExplicitEngine, SrsdEngine
 from paper_2501_05244_b200.reconstruct import RsdEngine
@@ -69,7 +69,7 @@ def _check_volume(name, got, ref, shape, t_gpu, t_oracle):
 
 
 def _procs():
-    from oracle_pool import n_procs
+    from oracle.pool import n_procs
     return n_procs()
 
 

@@ -6,7 +6,7 @@ import numpy as np
 
 import paper_2501_05244_b200 as pf
 from oracle import pf_oracle as O
-from oracle_pool import oracle_freq_terms, oracle_planes
+from oracle.pool import oracle_freq_terms, oracle_planes
 
 
 def _uniform_slices(rng, n=12, F=3):
