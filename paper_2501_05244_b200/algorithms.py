@@ -24,7 +24,7 @@ from .core import SPEED_OF_LIGHT, _require
 from .phasor import device_coefficients
 from .reconstruct import (GraphedRun, PlaneSpec, Propagator, _check_depths, _check_times, _close,
                           _exact_pad, _frame_weights, _ill_tensor, _kind, _nonplanar_relay,
-                          _pad_size, _planar_relay, _uniform_relay, _volume, rsd)
+                          _pad_size, _planar_relay, _uniform_relay, _volume, cached_engine, rsd)
 
 C = SPEED_OF_LIGHT
 _BATCH_BYTES = int(os.environ.get("PF_SRSD_BATCH_MB", "96")) << 20
@@ -203,8 +203,10 @@ class SrsdEngine(GraphedRun):
 
 def srsd(slices, grid, times=None, threads: int = 1, include_illumination: bool = True):
     """Scaled propagation onto a depth-widening frustum (reconstruct.py:276-327)."""
-    eng = SrsdEngine(slices, grid, include_illumination, times)
-    return _volume(grid, eng.run(device_coefficients(slices)), eng.times)
+    eng = cached_engine("srsd", slices, grid, (bool(include_illumination),
+                                               None if times is None else np.asarray(times)),
+                        lambda: SrsdEngine(slices, grid, include_illumination, times))
+    return _volume(grid, eng.run_dropin(device_coefficients(slices)), eng.times)
 
 
 # ---------------------------------------------------------------------------
@@ -307,8 +309,10 @@ class Nursd1Engine(_UhatPropEngine):
 def nursd1(slices, grid, eps: float = 1e-6, times=None, threads: int = 1,
            include_illumination: bool = True):
     """Scattered planar relay -> cuboid via type-1 NUFFT (reconstruct.py:335-385)."""
-    eng = Nursd1Engine(slices, grid, eps, include_illumination, times)
-    return _volume(grid, eng.run(device_coefficients(slices)), eng.times)
+    eng = cached_engine("nursd1", slices, grid, (float(eps), bool(include_illumination),
+                                                 None if times is None else np.asarray(times)),
+                        lambda: Nursd1Engine(slices, grid, eps, include_illumination, times))
+    return _volume(grid, eng.run_dropin(device_coefficients(slices)), eng.times)
 
 
 # ---------------------------------------------------------------------------

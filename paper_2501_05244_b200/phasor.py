@@ -11,7 +11,6 @@ frequency-major complex64 tensor resident on the device for the propagators.
 from __future__ import annotations
 
 import math
-import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -168,6 +167,72 @@ class TemporalPlan:
                       dev.ptr(out), out.stride(0), dev.stream_ptr(stream))
 
 
+_PLANS: dict = {}
+
+
+def _plan_for(kernel, t0: float, device) -> "TemporalPlan":
+    """TemporalPlan cache keyed by the kernel's bins / frequencies / weights and t0."""
+    key = (int(kernel.n_bins), np.asarray(kernel.bin_indices).tobytes(),
+           np.asarray(kernel.frequencies, dtype=np.float64).tobytes(),
+           np.asarray(kernel.weights, dtype=np.float64).tobytes(), float(t0), str(device))
+    plan = _PLANS.pop(key, None) or TemporalPlan(kernel, t0, device)
+    _PLANS[key] = plan
+    while len(_PLANS) > 4:
+        _PLANS.pop(next(iter(_PLANS)))
+    return plan
+
+
+class _HostStager:
+    """Host histograms -> K1 without a pageable copy: the rows are cut into chunks; host
+    threads copy chunk c into pinned buffer c % 2 (numpy releases the GIL) while chunk c - 1
+    is in flight host->device on the copy stream and chunk c - 2 is in K1, whose device
+    ring slot c % 2 is reused once its K1 has run.  Float64 payloads are narrowed to
+    float32 by the same copy."""
+
+    CHUNK_BYTES = 64 << 20
+    THREADS = 8
+
+    def __init__(self, device):
+        from concurrent.futures import ThreadPoolExecutor
+        self.device = device
+        n = self.CHUNK_BYTES // 4
+        self.pinned = [torch.empty((n,), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        self.ring = [torch.empty((n,), dtype=torch.float32, device=device) for _ in range(2)]
+        self.h2d_done = [torch.cuda.Event() for _ in range(2)]
+        self.k1_done = [torch.cuda.Event() for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(device=device)
+        self.pool = ThreadPoolExecutor(self.THREADS)
+
+    def run(self, host: np.ndarray, plan: "TemporalPlan", out: torch.Tensor) -> None:
+        n_tr, T = host.shape
+        rows = max(1, self.CHUNK_BYTES // (4 * T))
+        main = torch.cuda.current_stream(self.device)
+        th = self.THREADS
+        for c, r0 in enumerate(range(0, n_tr, rows)):
+            k = c & 1
+            r1 = min(n_tr, r0 + rows)
+            n = (r1 - r0) * T
+            # pinned[k] no longer read by an earlier transfer (this call's or the previous
+            # call's; an event never recorded returns at once)
+            self.h2d_done[k].synchronize()
+            dst = self.pinned[k].numpy()[:n].reshape(r1 - r0, T)
+            src = host[r0:r1]
+            edges = np.linspace(0, r1 - r0, th + 1).astype(np.int64)
+            list(self.pool.map(lambda i: np.copyto(dst[edges[i]:edges[i + 1]],
+                                                   src[edges[i]:edges[i + 1]],
+                                                   casting="same_kind"), range(th)))
+            self.copy_stream.wait_event(self.k1_done[k])   # ring[k] consumed by its K1
+            with torch.cuda.stream(self.copy_stream):
+                self.ring[k][:n].copy_(self.pinned[k][:n], non_blocking=True)
+                self.h2d_done[k].record(self.copy_stream)
+            main.wait_event(self.h2d_done[k])
+            plan.run(self.ring[k][:n].view(r1 - r0, T), out[:, r0:r1], main)
+            self.k1_done[k].record(main)
+
+
+_STAGERS: dict = {}
+
+
 def to_frequency_device(histograms: torch.Tensor, kernel, t0: float = 0.0,
                         out: torch.Tensor | None = None, plan: TemporalPlan | None = None,
                         stream=None) -> torch.Tensor:
@@ -195,14 +260,23 @@ def to_frequency(measurement, kernel) -> DeviceFrequencySlices:
              "measurement and kernel disagree on the bin width")
     device = dev.require_cuda()
     h = measurement.histograms
+    plan = _plan_for(kernel, float(measurement.t0), device)
     if isinstance(h, torch.Tensor):
         ht = h.to(device=device, dtype=torch.float32)
+        coeff = to_frequency_device(ht, kernel, float(measurement.t0), plan=plan)
     else:
-        host = np.ascontiguousarray(h, dtype=np.float32)
-        with warnings.catch_warnings():   # read-only payloads are only copied from
-            warnings.simplefilter("ignore", UserWarning)
-            ht = torch.from_numpy(host).to(device)
-    coeff = to_frequency_device(ht, kernel, float(measurement.t0))
+        # host payload: staged through pinned chunks straight into K1 (no device copy of
+        # the whole capture, no pageable transfer)
+        host = np.asarray(h)
+        i_n, d_n, t_n = host.shape
+        host2 = host.reshape(i_n * d_n, t_n)
+        if not host2.flags.c_contiguous:
+            host2 = np.ascontiguousarray(host2)
+        coeff = torch.empty((plan.n_freq, i_n, d_n), dtype=torch.complex64, device=device)
+        st = _STAGERS.get(str(device))
+        if st is None:
+            st = _STAGERS[str(device)] = _HostStager(device)
+        st.run(host2, plan, coeff.view(plan.n_freq, i_n * d_n))
     return DeviceFrequencySlices(kernel.frequencies, coeff, measurement.relay,
                                  measurement.illuminations)
 

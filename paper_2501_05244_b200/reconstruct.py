@@ -303,11 +303,118 @@ def _ill_tensor(slices, device) -> torch.Tensor:
     return torch.from_numpy(np.array(ill, dtype=np.float64, copy=True)).to(device)
 
 
+_PINNED: dict = {}
+
+
+_D2H_CHUNK = 1 << 22     # complex64 elements per device->host chunk (32 MB)
+
+
+def _host_c128(vol: torch.Tensor) -> np.ndarray:
+    """Device complex64 [frames, V] -> fresh host complex128 array (the reference's field
+    dtype).  The volume goes device->host in 32 MB chunks into a cached pinned buffer on a
+    side stream; host threads upcast each chunk into the output as soon as its copy lands
+    (numpy releases the GIL), so the transfer and the upcast overlap."""
+    n = vol.numel()
+    buf = _PINNED.get("vol")
+    if buf is None or buf.numel() < n:
+        _PINNED.pop("vol", None)
+        buf = torch.empty((n,), dtype=torch.complex64, pin_memory=True)
+        _PINNED["vol"] = buf
+    if "pool" not in _PINNED:
+        from concurrent.futures import ThreadPoolExecutor
+        _PINNED["pool"] = ThreadPoolExecutor(8)
+        _PINNED["stream"] = {}
+    side = _PINNED["stream"].get(vol.device.index)
+    if side is None:
+        side = _PINNED["stream"][vol.device.index] = torch.cuda.Stream(device=vol.device)
+    side.wait_stream(torch.cuda.current_stream(vol.device))
+    flat_dev = vol.reshape(-1)
+    edges = list(range(0, n, _D2H_CHUNK)) + [n]
+    events = []
+    with torch.cuda.stream(side):
+        for a, b in zip(edges[:-1], edges[1:]):
+            buf[a:b].copy_(flat_dev[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            events.append(ev)
+    src = buf[:n].numpy()
+    out = np.empty(vol.shape, dtype=np.complex128)
+    flat = out.reshape(-1)
+
+    def upcast(j):
+        events[j].synchronize()
+        flat[edges[j]:edges[j + 1]] = src[edges[j]:edges[j + 1]]
+
+    list(_PINNED["pool"].map(upcast, range(len(events))))
+    return out
+
+
 def _volume(grid, vol: torch.Tensor, times) -> ReconstructionVolume:
-    field = vol.cpu().numpy().astype(np.complex128)
+    """ReconstructionVolume from the device result (reference semantics: complex128, finite,
+    read-only).  The finiteness check runs on the device; the host array is freshly made
+    here and handed over without the defensive copy."""
+    _require(bool(torch.isfinite(torch.view_as_real(vol)).all()), "field must be finite")
+    field = _host_c128(vol)
     if times is None:
         field = field[0]
-    return ReconstructionVolume(grid, field, times)
+    return ReconstructionVolume._owned(grid, field, times)
+
+
+# ---------------------------------------------------------------------------
+# engine cache: the drop-in functions plan once per geometry (like an FFT plan cache)
+# ---------------------------------------------------------------------------
+
+_ENGINES: "dict" = {}
+_ENGINE_CACHE = int(os.environ.get("PF_ENGINE_CACHE", "2"))
+
+
+def _fingerprint(obj):
+    """Hashable value-identity of geometry objects (dataclasses of scalars / arrays)."""
+    import dataclasses
+    import hashlib
+    if obj is None or isinstance(obj, (bool, int, float, str)):
+        return obj
+    if isinstance(obj, (np.floating, np.integer)):
+        return obj.item()
+    if isinstance(obj, np.ndarray):
+        a = np.ascontiguousarray(obj)
+        return ("nd", a.shape, a.dtype.str, hashlib.sha1(a.tobytes()).hexdigest())
+    if isinstance(obj, (list, tuple)):
+        return tuple(_fingerprint(x) for x in obj)
+    if dataclasses.is_dataclass(obj):
+        return (type(obj).__name__,) + tuple(
+            (f.name, _fingerprint(getattr(obj, f.name))) for f in dataclasses.fields(obj))
+    return ("id", id(obj))
+
+
+def _slices_geometry(slices):
+    return (_fingerprint(np.asarray(slices.frequencies, dtype=np.float64)),
+            _fingerprint(slices.relay), _fingerprint(slices.illuminations))
+
+
+def cached_engine(kind: str, slices, grid, options: tuple, factory):
+    """Engine for (kind, slices geometry, grid, options) from a small LRU cache; ``factory``
+    builds it on a miss.  Engines hold only geometry-derived plans and workspaces, so a
+    hit is exactly what a rebuild would produce."""
+    if _ENGINE_CACHE <= 0:
+        return factory()
+    # the module's path switches are part of the key: an engine captured under other
+    # switches would replay their launch sequence
+    flags = (_LANES, _FAST_BATCH_CAP, _FBATCH_BYTES, _FBATCH_GENERIC, _HORNER, _BATCH_BYTES)
+    devi = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    key = (kind, devi, _slices_geometry(slices), _fingerprint(grid),
+           _fingerprint(options), flags)
+    eng = _ENGINES.pop(key, None)
+    if eng is None:
+        eng = factory()
+    _ENGINES[key] = eng
+    while len(_ENGINES) > _ENGINE_CACHE:
+        _ENGINES.pop(next(iter(_ENGINES)))
+    return eng
+
+
+def clear_engine_cache() -> None:
+    _ENGINES.clear()
 
 
 # ---------------------------------------------------------------------------
@@ -345,6 +452,21 @@ class GraphedRun:
         with torch.cuda.stream(main):
             g.replay()
         return vol
+
+    def run_dropin(self, coeff: torch.Tensor, stream=None) -> torch.Tensor:
+        """Graph replay on engine-owned input/output buffers (the drop-in functions' path:
+        ``coeff`` is copied into the captured input, the returned volume is reused by the
+        next call)."""
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        inp = self.__dict__.get("_dropin_in")
+        if inp is None or inp.shape != coeff.shape:
+            inp = torch.empty_like(coeff, device=self.device)
+            self._dropin_in = inp
+            self._dropin_out = torch.zeros((self.n_frames, self.n_voxels),
+                                           dtype=torch.complex64, device=self.device)
+        with torch.cuda.stream(main):
+            inp.copy_(coeff, non_blocking=True)
+        return self.run_graphed(inp, self._dropin_out, main)
 
     @property
     def chunk_unit(self) -> int:
@@ -516,8 +638,10 @@ class RsdEngine(GraphedRun):
 def rsd(slices, grid, padding: str = "exact", times=None, threads: int = 1,
         include_illumination: bool = True) -> ReconstructionVolume:
     """Plane-to-plane propagation onto a cuboid sharing the relay pitch (reconstruct.py:208-268)."""
-    eng = RsdEngine(slices, grid, padding, include_illumination, times)
-    vol = eng.run(device_coefficients(slices))
+    eng = cached_engine("rsd", slices, grid, (padding, bool(include_illumination),
+                                              None if times is None else np.asarray(times)),
+                        lambda: RsdEngine(slices, grid, padding, include_illumination, times))
+    vol = eng.run_dropin(device_coefficients(slices))
     return _volume(grid, vol, eng.times)
 
 
