@@ -132,7 +132,7 @@ def run_ours(args):
         else:   # gloo: CPU-staged collectives (used to exercise N>1 logic on one GPU)
             dist.init_process_group(backend)
     cfg = configs.config(args.config)
-    kernel = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
+    kernel = configs.kernel(cfg)
     hist = configs.transients(cfg, device=device)            # [1, D, T] float32, identical per rank
     I, D, T = hist.shape
     F = kernel.n_freq
@@ -600,7 +600,7 @@ def run_reference(args):
     from paper_2501_05244_b200 import configs
 
     cfg = configs.config(args.config)
-    kernel = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
+    kernel = configs.kernel(cfg)
     F = kernel.n_freq
     nz = _n_planes(cfg.grid)
     D = cfg.relay.count

@@ -156,14 +156,20 @@ int pf_prop_rows_out(const pf_plane* planes, int nplanes, double khat,
 
 /* Stage C with the illumination phase by Horner's rule (register path, both crops
  * centred, one illumination, single frame): call it for the frequencies in DESCENDING
- * order, last = 1 on the lowest (khat = k_0); dkhat = the uniform frequency spacing in
- * rad/m.  vol <- vol * exp(i dk d) + v_f, and on the last call the sum is multiplied by
- * exp(i k_0 d): the same sum as reconstruct.py:160-168 (ascending f, per-frequency
- * phases) in nested order.  Returns 1 without work when the geometry is not eligible. */
+ * order; dkhat = the uniform frequency spacing in rad/m.  vol <- vol * exp(i dk d) + v_f,
+ * and at f = 0 the sum is multiplied by exp(i k_0 d): the same sum as
+ * reconstruct.py:160-168 (ascending f, per-frequency phases) in nested order.
+ * mode 1: inner step; 2: f = 0 of a single-block sum (khat = k_0).  Sums longer than a
+ * block of B frequencies restart the nesting per block (z is raised to at most B - 1) and
+ * chain the blocks with Z = exp(i B dk d) from a float64-reduced phase: mode 3 at the
+ * lowest frequency of a block other than the first (o <- o Z + (vol z + v), vol <- 0),
+ * mode 4 at f = 0 (vol <- (o Z + (vol z + v)) exp(i k_0 d)); ws_o = the batch's outer
+ * accumulator (nplanes x ny x nx complex64), zkhat = B dkhat.
+ * Returns 1 without work when the geometry is not eligible. */
 int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, double khat, double dkhat,
-                            int last, const pf_prop_geom* g, const pf_fft_plan* plan_x,
+                            int mode, const pf_prop_geom* g, const pf_fft_plan* plan_x,
                             const void* ws_b, const double* ill_xyz, const void* frame_w,
-                            void* vol, void* stream);
+                            void* vol, void* ws_o, double zkhat, void* stream);
 
 /* All nf frequencies of a plane batch at once (register path, static volume):
  * kturns: device float64 [nf] = khat_f / (2 pi); ws_a / uhat / ws_b advance by

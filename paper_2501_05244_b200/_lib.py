@@ -89,7 +89,7 @@ _SIGNATURES = {
     "pf_zslab": [_vp, _i, _i, _i64, _vp, _f, _vp, _vp],
     "pf_roll": [_vp, _vp, _i64, _i, _i, _i, _i, _i, _i, _vp],
     "pf_prop_rows_out_horner": [_vp, _i, _d, _d, _i, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp,
-                                _vp, _vp, _vp],
+                                _vp, _vp, _vp, _d, _vp],
     "pf_prop_rows_out": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp,
                          _i64, _vp],
 }

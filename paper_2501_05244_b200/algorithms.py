@@ -195,7 +195,7 @@ class SrsdEngine(GraphedRun):
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
                                         plane_hi=b1, stream=ls, lane=lane,
-                                        horner=None if dk is None else (dk, fi == order[-1]))
+                                        horner=None if dk is None else (dk, fi, len(order)))
 
         self.prop.run_batches(body, stream)
         return vol
@@ -242,7 +242,7 @@ class _UhatPropEngine(GraphedRun):
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
                                         plane_hi=b1, stream=ls, lane=lane,
-                                        horner=None if dk is None else (dk, fi == order[-1]))
+                                        horner=None if dk is None else (dk, fi, len(order)))
 
         self.prop.run_batches(body, stream)
         return vol

@@ -125,7 +125,47 @@ def config(c: int) -> Config:
                      base.n_bins, base.delta_t, base.lambda_c, base.t0, "nursd1", seed)
         cfg.lattice_nodes = keep
         return cfg
+    if c == 6:
+        # "config 4 heavy": BASELINE config 4 states "~400 frequency bins in the wavelet
+        # band", which the reference's build_kernel (sigma = c / (5 lambda)) cannot give at
+        # T = 4096, 4 ps (it keeps 32).  Same capture and volume as config 4 with
+        # a hand-built PhasorKernel (reference phasor.py:42-69): the Gaussian packet about
+        # the same carrier, sigma widened so that exactly the 400 lowest positive bins reach
+        # the 0.01 retention threshold
+        base = config(4)
+        cfg = Config("c4-heavy", base.relay, base.illuminations, base.grid, base.scatterers,
+                     base.albedo, base.n_bins, base.delta_t, base.lambda_c, base.t0, "rsd", seed)
+        cfg.kernel = heavy_kernel(base, 400)
+        return cfg
     raise ValueError(f"config {c} is not a bench configuration")
+
+
+def heavy_kernel(cfg: Config, n_freq: int, threshold: float = 0.01):
+    """PhasorKernel over bins 1..n_freq: weights exp(-(w - w_c)^2 / (2 s^2)) with s chosen
+    so that the farthest retained bin sits exactly at ``threshold`` (weights in
+    [threshold, 1], every bin contributes)."""
+    import math
+
+    from .core import _readonly
+    from .phasor import PhasorKernel
+    T, dt = cfg.n_bins, cfg.delta_t
+    omega_c = 2.0 * math.pi * SPEED_OF_LIGHT / cfg.lambda_c
+    k = np.arange(1, n_freq + 1)
+    om = 2.0 * math.pi * k / (T * dt)
+    span = float(np.abs(om - omega_c).max())
+    sigma = span / math.sqrt(2.0 * math.log(1.0 / threshold))
+    wt = np.exp(-((om - omega_c) ** 2) / (2.0 * sigma * sigma))
+    return PhasorKernel(float(cfg.lambda_c), float(dt), int(T), float(threshold), omega_c,
+                        sigma, _readonly(k), _readonly(om), _readonly(wt))
+
+
+def kernel(cfg: Config):
+    """The configuration's phasor kernel: the reference build_kernel unless hand-built."""
+    k = getattr(cfg, "kernel", None)
+    if k is not None:
+        return k
+    from .phasor import build_kernel
+    return build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
 
 
 def transients(cfg: Config, device=None, noise: bool = True):

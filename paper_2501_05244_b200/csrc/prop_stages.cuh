@@ -141,13 +141,19 @@ __host__ __device__ constexpr int cent_base(int m) { return (m + 8) & 31; }
 // is a few radians, so z is formed in float32), and on the last step (f = 0, HOR = 2,
 // kturns = k_0 / 2 pi) the sum is multiplied by exp(i k_0 d) in the float64-reduced form.
 // Same sum as the ascending per-frequency phases, in nested order.
+// Many frequencies (F > block): the nesting restarts every block of B frequencies so z is
+// raised to at most B - 1, and the blocks are chained by Z = exp(i B dk d) formed from a
+// float64-reduced phase (the outer accumulator o lives in ws_o, one row set per plane of
+// the batch):  HOR = 3 at a block's lowest frequency: o <- o Z + (h z + v), h <- 0;
+// HOR = 4 at f = 0: vol <- (o Z + (h z + v)) exp(i k_0 d).
 template <int L, bool MULTI, bool PRE, bool CENT = false, int HOR = 0>
 __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double kturns,
                                      const pf_prop_geom& g, const float2* __restrict__ tw,
                                      const float2* __restrict__ wb, const double* __restrict__ ill,
                                      const float2* __restrict__ frame_w, int n_frames,
                                      float2* __restrict__ vol, long long vfs, int tile,
-                                     float dturns = 0.f) {
+                                     float dturns = 0.f, float2* __restrict__ ws_o = nullptr,
+                                     double zturns = 0.0) {
   static_assert(HOR == 0 || (!MULTI && PRE && CENT), "Horner variant: one illumination, "
                 "centred crop, prefetched volume");
   constexpr int P = 32 * L;
@@ -300,6 +306,17 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
             float zs, zc;
             __sincosf(6.28318530717958647692f * (tz - rintf(tz)), &zs, &zc);
             float2 nv = cadd(cmul(ot[base], make_float2(zc, zs)), cmul(v[m], fw));
+            if (HOR >= 3) {   // chain the block: o Z + h (o row of this batch plane)
+              const double d2 = fma(dx, dx, byz);
+              float2* op = ws_o + ((long long)blockIdx.y * ny + i) * nx + t + base;
+              nv = cadd(cmul(*op, phase_turns(d2, zturns, (float)zturns)), nv);
+              if (HOR == 3) {
+                *op = nv;
+                nv = make_float2(0.f, 0.f);
+              } else {
+                nv = cmul(nv, phase_turns(d2, kturns, (float)kturns));
+              }
+            }
             if (HOR == 2) nv = cmul(nv, phase_turns(fma(dx, dx, byz), kturns, (float)kturns));
             dt[base] = nv;
           }

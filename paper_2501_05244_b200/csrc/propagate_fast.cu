@@ -64,12 +64,12 @@ __global__ void __launch_bounds__(FT, 2)
 k_pc_h(const pf_plane* __restrict__ planes, double kturns, float dturns, pf_prop_geom g,
        const float2* __restrict__ tw, const float2* __restrict__ ws_b,
        const double* __restrict__ ill, const float2* __restrict__ frame_w,
-       float2* __restrict__ vol) {
+       float2* __restrict__ vol, float2* __restrict__ ws_o, double zturns) {
   extern __shared__ float2 sm[];
   const long long wb_plane = 32LL * L * g.ny;
   st_c<L, false, true, true, HOR>(sm, planes[blockIdx.y], kturns, g, tw,
                                   ws_b + blockIdx.y * wb_plane, ill, frame_w, 1, vol, 0,
-                                  blockIdx.x, dturns);
+                                  blockIdx.x, dturns, ws_o, zturns);
 }
 
 // ---- B split in two register-light kernels (128 registers, 16 warps/SM):
@@ -717,16 +717,20 @@ extern "C" int pf_relay_spectra_fast(const void* src, int64_t nb, int ny, int nx
   return -1;
 }
 
-// Stage C with Horner's rule (see st_c): frequencies must be visited in descending order,
-// last = 1 on the lowest one (khat = k_0); dkhat = k_{f+1} - k_f (uniform spacing).
+// Stage C with Horner's rule (see st_c): frequencies must be visited in descending order;
+// dkhat = k_{f+1} - k_f (uniform spacing).  mode: 1 inner step, 2 last step of a
+// single-block sum (f = 0, khat = k_0), 3 lowest frequency of a block (not f = 0),
+// 4 f = 0 of a multi-block sum; modes 3/4 use ws_o (nplanes x ny x nx complex64, the
+// batch's outer accumulator) and zkhat = B dkhat (B = block length).
 // Eligible: register path, both crops centred, one illumination, illumination phase on,
 // single frame.  Returns 1 (and does nothing) when the geometry is not eligible.
 extern "C" int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, double khat,
-                                       double dkhat, int last, const pf_prop_geom* g,
+                                       double dkhat, int mode, const pf_prop_geom* g,
                                        const pf_fft_plan* plan_x, const void* ws_b,
                                        const double* ill_xyz, const void* frame_w, void* vol,
-                                       void* stream) {
-  PF_ARG_CHECK(g && plan_x && plan_x->n == g->px && nplanes >= 1 && frame_w && vol,
+                                       void* ws_o, double zkhat, void* stream) {
+  PF_ARG_CHECK(g && plan_x && plan_x->n == g->px && nplanes >= 1 && frame_w && vol &&
+               mode >= 1 && mode <= 4 && (mode < 3 || ws_o),
                "pf_prop_rows_out_horner: bad args");
   const int L = pf_prop_fast_L(g);
   const int P = 32 * L;
@@ -739,6 +743,7 @@ extern "C" int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, doub
   const float2* tw = (const float2*)plan_x->tw;
   const double kturns = khat / PF_TWO_PI;
   const float dturns = (float)(dkhat / PF_TWO_PI);
+  const double zturns = zkhat / PF_TWO_PI;
   cudaStream_t st = (cudaStream_t)stream;
 #define PF_H_CASE(LL)                                                                          \
   case LL: {                                                                                   \
@@ -747,15 +752,21 @@ extern "C" int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, doub
     if (attr.first()) {                                                                               \
       cudaFuncSetAttribute(k_pc_h<LL, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
       cudaFuncSetAttribute(k_pc_h<LL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+      cudaFuncSetAttribute(k_pc_h<LL, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+      cudaFuncSetAttribute(k_pc_h<LL, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
     }                                                                                          \
     dim3 grid(pf_cdiv(g->ny, RPC), nplanes);                                                   \
     const size_t sm = smem_c<LL>(g->nx, true);                                                 \
-    if (last)                                                                                  \
-      k_pc_h<LL, 2><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, (const float2*)ws_b, \
-                                          ill_xyz, (const float2*)frame_w, (float2*)vol);      \
-    else                                                                                       \
-      k_pc_h<LL, 1><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, (const float2*)ws_b, \
-                                          ill_xyz, (const float2*)frame_w, (float2*)vol);      \
+    const float2* wb = (const float2*)ws_b;                                                    \
+    const float2* fw = (const float2*)frame_w;                                                 \
+    float2* vo = (float2*)vol;                                                                 \
+    float2* wo = (float2*)ws_o;                                                                \
+    switch (mode) {                                                                            \
+      case 1: k_pc_h<LL, 1><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns); break; \
+      case 2: k_pc_h<LL, 2><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns); break; \
+      case 3: k_pc_h<LL, 3><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns); break; \
+      default: k_pc_h<LL, 4><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns); break; \
+    }                                                                                          \
     PF_LAUNCH_CHECK("k_pc_h");                                                                 \
     return 0;                                                                                  \
   }

@@ -49,6 +49,7 @@ _FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "4"))
 _FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
 _FBATCH_GENERIC = os.environ.get("PF_FBATCH_GENERIC", "1") != "0"
 _HORNER = os.environ.get("PF_HORNER", "1") != "0"   # kernel C phases by Horner's rule
+_HORNER_BLOCK = int(os.environ.get("PF_HORNER_BLOCK", "32"))   # frequencies per nested block
 
 
 # ---------------------------------------------------------------------------
@@ -213,7 +214,7 @@ class Propagator:
                       n_frames: int, vol: torch.Tensor, vol_frame_stride: int,
                       plane_lo: int = 0, plane_hi: int | None = None, stream=None,
                       uhat_ptr_for_batch=None, lane: int = 0, horner=None) -> None:
-        """One frequency over planes [plane_lo, plane_hi).  horner=(dkhat, last): kernel C
+        """One frequency over planes [plane_lo, plane_hi).  horner=(dkhat, f, F): kernel C
         by Horner's rule (frequencies visited in ``freq_order``)."""
         plane_hi = self.nplanes if plane_hi is None else plane_hi
         s = dev.stream_ptr(stream)
@@ -227,12 +228,31 @@ class Propagator:
             _lib.call("pf_prop_kernel_rows", pp, nb, khat, gref, self.plan_x.ref, wa, s)
             _lib.call("pf_prop_columns", pp, nb, gref, self.plan_y.ref, wa, up, wb, 0, s)
             if horner is not None:
+                dk, fi, nf = horner
+                B = _HORNER_BLOCK
+                if nf <= B:
+                    mode, wo = (2 if fi == 0 else 1), 0
+                else:   # blocks of B frequencies chained through the outer accumulator
+                    mode = 4 if fi == 0 else (3 if fi % B == 0 else 1)
+                    wo_t = self._ws_o(lane, nb)
+                    if fi == nf - 1:
+                        wo_t.zero_()
+                    wo = dev.ptr(wo_t)
                 # a nonzero status (geometry not eligible) raises PfError in _lib.call
-                _lib.call("pf_prop_rows_out_horner", pp, nb, khat, horner[0], int(horner[1]),
-                          gref, self.plan_x.ref, wb, ill_ptr, frame_w_ptr, dev.ptr(vol), s)
+                _lib.call("pf_prop_rows_out_horner", pp, nb, khat, dk, mode, gref,
+                          self.plan_x.ref, wb, ill_ptr, frame_w_ptr, dev.ptr(vol), wo, B * dk, s)
                 continue
             _lib.call("pf_prop_rows_out", pp, nb, khat, gref, self.plan_x.ref, wb, ill_ptr,
                       frame_w_ptr, n_frames, dev.ptr(vol), vol_frame_stride, s)
+
+    def _ws_o(self, lane: int, nb: int) -> torch.Tensor:
+        """Outer Horner accumulator of a lane's plane batch (nb x ny x nx complex64)."""
+        lst = self.__dict__.setdefault("ws_o_l", {})
+        t = lst.get(lane)
+        if t is None:
+            t = lst[lane] = torch.empty((self.batch * self.geom.ny * self.geom.nx,),
+                                        dtype=torch.complex64, device=self.device)
+        return t[:nb * self.geom.ny * self.geom.nx]
 
     def fbatch_ok(self, n_freq: int, n_frames: int) -> bool:
         """All frequencies in one launch per stage (small configs, static volume);
@@ -400,7 +420,8 @@ def cached_engine(kind: str, slices, grid, options: tuple, factory):
         return factory()
     # the module's path switches are part of the key: an engine captured under other
     # switches would replay their launch sequence
-    flags = (_LANES, _FAST_BATCH_CAP, _FBATCH_BYTES, _FBATCH_GENERIC, _HORNER, _BATCH_BYTES)
+    flags = (_LANES, _FAST_BATCH_CAP, _FBATCH_BYTES, _FBATCH_GENERIC, _HORNER, _HORNER_BLOCK,
+             _BATCH_BYTES)
     devi = torch.cuda.current_device() if torch.cuda.is_available() else -1
     key = (kind, devi, _slices_geometry(slices), _fingerprint(grid),
            _fingerprint(options), flags)
@@ -588,7 +609,7 @@ class RsdEngine(GraphedRun):
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
                                         plane_hi=b1, stream=ls, lane=lane,
-                                        horner=None if dk is None else (dk, fi == order[-1]))
+                                        horner=None if dk is None else (dk, fi, len(order)))
 
         self.prop.run_batches(body, stream, lo, hi)
         return vol
@@ -629,7 +650,7 @@ class RsdEngine(GraphedRun):
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
                                         plane_hi=b1, stream=ls, lane=lane,
-                                        horner=None if dk is None else (dk, fi == order[-1]))
+                                        horner=None if dk is None else (dk, fi, len(order)))
 
         self.prop.run_batches(body, stream)
         return vol

@@ -24,8 +24,8 @@ from paper_2501_05244_b200.phasor import device_coefficients
 pytestmark = pytest.mark.gpu
 R = importlib.import_module("paper_2501_05244_b200.reconstruct")
 
-_WS = ("ws_a_l", "ws_b_l", "uhat", "uhat_l", "xbuf_l", "fine", "spec", "_fb_ws_a", "_fb_ws_b",
-       "_fine", "slot")
+_WS = ("ws_a_l", "ws_b_l", "ws_o_l", "uhat", "uhat_l", "xbuf_l", "fine", "spec", "_fb_ws_a",
+       "_fb_ws_b", "_fine", "slot")
 _SUB = ("prop", "ro", "stage1", "stage2")
 GUARD = 1 << 16
 
@@ -38,7 +38,7 @@ def _poison(obj, seen=None):
     n = 0
     for name in _WS:
         v = getattr(obj, name, None)
-        for t in (v if isinstance(v, list) else [v]):
+        for t in (v if isinstance(v, list) else list(v.values()) if isinstance(v, dict) else [v]):
             if isinstance(t, torch.Tensor) and t.is_cuda and t.is_floating_point() | t.is_complex():
                 (torch.view_as_real(t) if t.is_complex() else t).fill_(float("nan"))
                 n += 1
@@ -83,14 +83,15 @@ def _lattice(n):
     return pf.UniformGrid2D(n, n, p, p, -1 + p / 2, -1 + p / 2, 0.0)
 
 
-@pytest.mark.parametrize("n,nz,n_ill,video,fbatch", [
-    (64, 6, 1, False, True), (64, 6, 1, False, False), (64, 5, 2, False, False),
-    (128, 4, 1, True, False), (96, 3, 1, False, False), (512, 3, 1, False, False)])
-def test_rsd_workspaces_and_guards(rng, monkeypatch, n, nz, n_ill, video, fbatch):
+@pytest.mark.parametrize("n,nz,n_ill,video,fbatch,F", [
+    (64, 6, 1, False, True, 5), (64, 6, 1, False, False, 5), (64, 5, 2, False, False, 5),
+    (64, 5, 1, False, False, 70),
+    (128, 4, 1, True, False, 5), (96, 3, 1, False, False, 5), (512, 3, 1, False, False, 5)])
+def test_rsd_workspaces_and_guards(rng, monkeypatch, n, nz, n_ill, video, fbatch, F):
     if not fbatch:
         monkeypatch.setattr(R, "_FBATCH_BYTES", 0)
     g = _lattice(n)
-    sl = _slices(rng, pf.UniformRelay(g), n_ill=n_ill)
+    sl = _slices(rng, pf.UniformRelay(g), F=F, n_ill=n_ill)
     grid = pf.CuboidGrid(pf.UniformGrid3D(n, n, nz, g.dx, g.dy, 0.2, g.x0, g.y0, 0.5))
     times = np.array([0.0, 1e-10, 2e-10]) if video else None
     eng = R.RsdEngine(sl, grid, times=times)

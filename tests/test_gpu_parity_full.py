@@ -32,7 +32,7 @@ TOL = 1e-4
 
 def _slices(cfg):
     hist = configs.transients(cfg, device=torch.device("cuda"))
-    k = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
+    k = configs.kernel(cfg)
     coeff = pf.to_frequency_device(hist, k, cfg.t0)
     del hist
     sl = pf.DeviceFrequencySlices(k.frequencies, coeff, cfg.relay, cfg.illuminations)
@@ -149,3 +149,21 @@ def test_config2_composed_full_size():
           "oracle_procs": _procs()})
     assert rel < TOL, rel
     assert ia == ib, f"argmax differs (top-2 gap {_top2_gap(np.abs(ref)):.3e})"
+
+
+@pytest.mark.parametrize("planes", [(0, 2), (128, 130), (254, 256)])
+def test_config6_heavy_400_bins_plane_subsets(planes):
+    """Config 4 with 400 frequency bins (BASELINE "~400 bins"; hand-built kernel): Horner's
+    rule in 32-frequency blocks chained by float64-reduced phases keeps the sum within the
+    gate; the oracle's 400 frequency terms run in parallel and are added in ascending order
+    (reference _reduce)."""
+    cfg = configs.config(6)
+    sl, k = _slices(cfg)
+    assert k.n_freq == 400
+    eng = RsdEngine(sl, cfg.grid, plane_range=planes)
+    assert eng.prop.freq_order(eng.freqs, 1)[1] is not None      # Horner path
+    got, tg = _run_gpu(eng, sl.device_coefficients)
+    t = time.perf_counter()
+    ref = oracle_freq_terms("rsd", sl.to_host(), (cfg.grid,), plane_range=planes)
+    _check_volume("config6-heavy-planes-%d-%d" % planes, got, ref,
+                  (planes[1] - planes[0], 512, 512), tg, time.perf_counter() - t)

@@ -233,7 +233,9 @@ def test_graphed_run_matches_eager(rng):
     assert eng.graph_kernels > 0
 
 
-@pytest.mark.parametrize("n,nz,n_freq", [(64, 6, 5), (256, 4, 9), (512, 4, 32)])
+@pytest.mark.parametrize("n,nz,n_freq", [(64, 6, 5), (256, 4, 9), (512, 4, 32),
+                                         (64, 5, 33), (64, 3, 64), (64, 4, 100),
+                                         (128, 3, 400)])
 def test_horner_phases_match_per_frequency_phases(rng, monkeypatch, n, nz, n_freq):
     """Kernel C with the illumination phase by Horner's rule over descending frequencies
     (pf_prop_rows_out_horner) = the ascending per-frequency phases (reference
@@ -253,8 +255,9 @@ def test_horner_phases_match_per_frequency_phases(rng, monkeypatch, n, nz, n_fre
     monkeypatch.setattr(R, "_HORNER", False)
     asc = eng.run(coeff)
     torch.cuda.synchronize()
-    # z = exp(i dk d) is formed in float32 and raised to the 31st power by the recurrence:
-    # ~4e-6 at 32 frequencies, 25x inside the 1e-4 gate
+    # z = exp(i dk d) is formed in float32 and raised to at most the 31st power (blocks of
+    # 32 frequencies chained by a float64-reduced exp(i 32 dk d) beyond that): ~4e-6 at any
+    # frequency count, 25x inside the 1e-4 gate
     assert O.rel_l2(hor.cpu().numpy(), asc.cpu().numpy()) < 1e-5
     if n <= 256:
         ref = O.rsd(sl, grid)

@@ -13,7 +13,7 @@ from paper_2501_05244_b200.pipeline import _Meta  # noqa: E402
 cfg_id = int(os.environ.get("PF_CFG", "4"))
 n_f = int(os.environ.get("PF_NF", "2"))
 cfg = configs.config(cfg_id)
-k = pf.build_kernel(cfg.lambda_c, cfg.n_bins, cfg.delta_t)
+k = configs.kernel(cfg)
 meta = _Meta(k, cfg.relay, cfg.illuminations)
 meta.frequencies = meta.frequencies[:n_f]
 if cfg.algorithm == "srsd":
