@@ -269,10 +269,11 @@ def run_ours(args):
                                            "148 SM x 128 lanes x 2 x sm_max_mhz; MEASURED_PEAKS.json "
                                            "has no FP32 entry" % fp32_nominal,
                "flops_model": _flops_model(cfg.algorithm, P),
-               "traffic_note": "DRAM bytes of one plane batch of A+B1+B2+C from an ncu --set "
-                               "full capture (profiles/ncu_traffic.json) scaled to F x Nz; ncu "
-                               "flushes L2 before each kernel, so this counts the L2-resident "
-                               "stage intermediates as DRAM reads: an upper bound"}
+               "traffic_note": "steady-state DRAM bytes per step of the propagation kernels "
+                               "(ncu application replay, no cache control, kernels serialised "
+                               "by the profiler; profiles/r2_traffic_steady.json): ~70x the "
+                               "0.6 GB compulsory (slices in, volume out), mostly write-back "
+                               "of the per-batch stage workspaces and the volume slices"}
     roof_s3["frac"] = roof_s3["achieved"] / fp32_peak
     ex = _executed_flops(cfg, eng, F, k_hi - k_lo, I)
     if ex is not None:
@@ -437,29 +438,34 @@ def _flops_model(alg, P):
     return base + ", P=%d" % P
 
 
-def _prop_traffic(n_freq, n_planes, config):
-    """Per-step DRAM bytes of the propagation stage from the committed ncu capture
-    (one plane batch of kernels A, B1, B2, C, cold L2), scaled to F x Nz; only for the
-    configuration the capture was taken on (null otherwise: not measured)."""
-    per_batch = _traffic("k_prop_per_batch", config)
-    planes = _traffic("batch_planes", config)
-    if per_batch is None or not planes:
+def _steady():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic_steady.json")) as f:
+            return json.load(f)
+    except Exception:
         return None
-    return per_batch * n_freq * (n_planes / float(planes))
+
+
+def _prop_traffic(n_freq, n_planes, config):
+    """Steady-state DRAM bytes per step of the propagation kernels (A, fused B, C and the
+    relay spectra) from the committed ncu application-replay capture without cache control
+    (profiles/r2_traffic_steady.json, config 4, F = 32, all 256 planes); null for other
+    configurations (not measured)."""
+    t = _steady()
+    if t is None or int(config) != 4 or n_freq != 32 or n_planes != 256:
+        return None
+    return t["propagation_dram_bytes_per_step"]
 
 
 def _traffic(kernel_prefix, config, world=1):
-    """DRAM bytes per launch from the committed ncu capture summary, when it was taken
-    on this configuration (config 4, one GPU); null otherwise."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    try:
-        with open(path) as f:
-            t = json.load(f)
-        if int(t.get("config", 4)) != int(config) or world != 1:
-            return None
-        return t.get(kernel_prefix)
-    except Exception:
+    """K1's DRAM bytes per launch from the same capture (config 4, one GPU)."""
+    t = _steady()
+    if t is None or int(config) != 4 or world != 1:
         return None
+    for name, d in t["kernels"].items():
+        if name.startswith(kernel_prefix):
+            return d["dram_read_bytes_per_step"] + d["dram_write_bytes_per_step"]
+    return None
 
 
 # ---------------------------------------------------------------------------

@@ -320,6 +320,37 @@ int pf_copy_planes(const void* src, int nb, int64_t src_stride, int64_t plane_of
 int pf_roll(const void* src, void* dst, int64_t nb, int n0, int n1, int n2, int s0, int s1, int s2,
             void* stream);
 
+/* ---------------------------------------------------------------- whole algorithm
+ * rsd (reference reconstruct.py:208-268, rsd(slices, grid, padding, times, threads,
+ * include_illumination)) in one call: relay lattice and output cuboid as the reference's
+ * UniformGrid2D / UniformGrid3D fields (x0/y0 = first sample, not the centre); host
+ * arrays frequencies [n_freq] (rad/s, ascending, FrequencySlices.frequencies),
+ * ill_xyz [n_illum][3] (illumination_coordinates, core.py), times [n_frames] or
+ * n_frames = 0 for a static volume.  slices: device c64 [n_freq][n_illum][relay_ny *
+ * relay_nx] (frequency-major, row-major lattice); vol: device c64 [max(1, n_frames)]
+ * [nz * ny * nx], x fastest (written, not accumulated); ws: device scratch of at least
+ * pf_rsd_workspace_bytes(args) bytes.  Validation errors (status -1, pf_last_error) carry
+ * the reference's ValidationError messages ("pitch", "origin", "beyond the relay",
+ * "padding='none'").  Asynchronous on `stream`; plane batches run on three internal
+ * lanes forked from and joined back to it. */
+typedef struct pf_rsd_args {
+  int relay_nx, relay_ny;
+  double relay_dx, relay_dy, relay_x0, relay_y0, relay_z;
+  int nx, ny, nz;
+  double dx, dy, dz, x0, y0, z0;
+  int n_freq, n_illum;
+  const double* frequencies;
+  const double* ill_xyz;
+  int n_frames;
+  const double* times;
+  int padding_none;
+  int include_illum;
+} pf_rsd_args;
+
+int64_t pf_rsd_workspace_bytes(const pf_rsd_args* args);
+int pf_rsd(const pf_rsd_args* args, const void* slices, void* vol, void* ws, int64_t ws_bytes,
+           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

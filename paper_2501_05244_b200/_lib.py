@@ -43,6 +43,20 @@ class PfNufftGeom(ctypes.Structure):
                 ("ntiles", ctypes.c_int * 3)]
 
 
+class PfRsdArgs(ctypes.Structure):
+    _fields_ = [("relay_nx", ctypes.c_int), ("relay_ny", ctypes.c_int),
+                ("relay_dx", ctypes.c_double), ("relay_dy", ctypes.c_double),
+                ("relay_x0", ctypes.c_double), ("relay_y0", ctypes.c_double),
+                ("relay_z", ctypes.c_double),
+                ("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int),
+                ("dx", ctypes.c_double), ("dy", ctypes.c_double), ("dz", ctypes.c_double),
+                ("x0", ctypes.c_double), ("y0", ctypes.c_double), ("z0", ctypes.c_double),
+                ("n_freq", ctypes.c_int), ("n_illum", ctypes.c_int),
+                ("frequencies", ctypes.c_void_p), ("ill_xyz", ctypes.c_void_p),
+                ("n_frames", ctypes.c_int), ("times", ctypes.c_void_p),
+                ("padding_none", ctypes.c_int), ("include_illum", ctypes.c_int)]
+
+
 _vp, _i, _i64, _d, _f = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_float
 _P = ctypes.POINTER
 
@@ -56,6 +70,8 @@ _SIGNATURES = {
     "pf_fft_lines": [_vp, _P(PfFftPlan), _i64, _i64, _i64, _i64, _i64, _i, _f, _vp],
     "pf_embed_centered": [_vp, _i64, _i, _i, _i64, _vp, _i, _i, _i, _vp],
     "pf_prop_fast": [_P(PfPropGeom)],
+    "pf_rsd_workspace_bytes": [_P(PfRsdArgs)],
+    "pf_rsd": [_P(PfRsdArgs), _vp, _vp, _vp, _i64, _vp],
     "pf_nufft_type1_finish_pow2": [_P(PfNufftGeom), _vp, _i64, _i, _vp, _P(PfFftPlan),
                                    _P(PfFftPlan), _vp, _vp, _vp, _i64, _vp],
     "pf_relay_spectra_fast": [_vp, _i64, _i, _i, _i64, _vp, _i, _P(PfFftPlan), _vp],
@@ -94,7 +110,7 @@ _SIGNATURES = {
                          _i64, _vp],
 }
 _RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
-             "pf_prop_ws_spectrum": ctypes.c_int64,
+             "pf_prop_ws_spectrum": ctypes.c_int64, "pf_rsd_workspace_bytes": ctypes.c_int64,
              "pf_prop_fast": ctypes.c_int}
 
 _lib = None

@@ -1,0 +1,367 @@
+// Whole-algorithm C entry point for rsd (reference reconstruct.py:208-268): the same
+// plan and launch sequence as the Python engine (reconstruct.RsdEngine), in C++ behind
+// the C-ABI, for a caller that binds the library directly.
+//
+//   pf_rsd_workspace_bytes(args)            device scratch the call needs
+//   pf_rsd(args, slices, vol, ws, bytes, s) slices [F][I][ny*nx] c64 -> vol [frames][V] c64
+//
+// Host side: validation with the reference's messages, pad sizes (reference pad rule
+// without the +8 margin, a power of two when within 1.6x: rsd is pad independent once no
+// lag wraps), fp64 twiddle tables, plane specs, frame weights; all of it is copied into
+// the caller's workspace.  Device side: relay spectra, then per plane batch and frequency
+// the A / fused B / C kernels (Horner's rule in C when the geometry allows), with plane
+// batches spread over three lanes (streams forked from and joined back to the caller's
+// stream).  No allocation, no global mutable state; not capturable into a CUDA graph
+// (the tables are uploaded from pageable host memory).
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <vector>
+
+#include "common.cuh"
+#include "../../include/pfgpu.h"
+
+namespace {
+
+constexpr double C_LIGHT = 299792458.0;
+constexpr int LANES = 3;
+constexpr int HORNER_BLOCK = 32;
+constexpr int64_t BATCH_BYTES = 64LL << 20;
+
+bool close_rel(double a, double b) {
+  return fabs(a - b) <= fmax(1e-9 * fmax(fabs(a), fabs(b)), 1e-12);
+}
+
+bool smooth11(long n) {
+  if (n < 1) return false;
+  const int ps[5] = {2, 3, 5, 7, 11};
+  for (int p : ps)
+    while (n % p == 0) n /= p;
+  return n == 1;
+}
+
+long next_fast_len(long n) {
+  if (n < 1) n = 1;
+  while (!smooth11(n)) n++;
+  return n;
+}
+
+long exact_pad(double lag_max, double nu_max, long n_min) {
+  long need = 2 * (long)ceil(fmax(lag_max, nu_max)) + 2;
+  if (need < n_min) need = n_min;
+  long p2 = 1;
+  while (p2 < need) p2 *= 2;
+  if (64 < need && p2 <= 1024 && p2 * 5 <= need * 8) return p2;
+  return next_fast_len(need);
+}
+
+// stage radices: powers of two merged into as few even stages as possible, then odd primes
+// in descending order (_device.radices_for)
+int radices(long n, int* out) {
+  std::vector<int> f;
+  long m = n;
+  for (int p : {2, 3, 5, 7, 11})
+    while (m % p == 0) {
+      f.push_back(p);
+      m /= p;
+    }
+  if (m != 1) return -1;
+  int k = 0;
+  std::vector<int> odd;
+  for (int p : f) (p == 2 ? k++ : (odd.push_back(p), 0));
+  int ns = 0;
+  if (k) {
+    const int s = (k + 3) / 4;
+    for (int i = 0; i < s; i++) out[ns++] = 1 << (k / s + (i < k % s ? 1 : 0));
+  }
+  for (int i = (int)odd.size() - 1; i >= 0; i--) out[ns++] = odd[i];   // descending
+  return ns;
+}
+
+// unit roots exp(-2 pi i m / n) in fp64, rounded to c64; the register-FFT lengths append
+// the k1-major twiddles [k1][t] = exp(-2 pi i ((k1 t) mod n) / n), n = 32 L
+std::vector<float2> twiddles(long n) {
+  std::vector<float2> w;
+  for (long m = 0; m < n; m++) {
+    const double a = -2.0 * M_PI * (double)m / (double)n;
+    w.push_back(make_float2((float)cos(a), (float)sin(a)));
+  }
+  if (n == 128 || n == 256 || n == 512 || n == 1024) {
+    const long L = n / 32;
+    for (long k1 = 0; k1 < 32; k1++)
+      for (long t = 0; t < L; t++) {
+        const double a = -2.0 * M_PI * (double)((k1 * t) % n) / (double)n;
+        w.push_back(make_float2((float)cos(a), (float)sin(a)));
+      }
+  }
+  return w;
+}
+
+struct Layout {
+  int px, py, nu0x, nu0y, batch, lanes;
+  bool fast, horner;
+  double dkhat;
+  int64_t off_twx, off_twy, off_planes, off_ill, off_fw, off_uhat, off_wa, off_wb, off_wo, total;
+  int64_t n_twx, n_twy;
+};
+
+int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+// validation + plan; returns 0 or -1 with pf_set_error
+int plan(const pf_rsd_args* a, Layout* L) {
+  if (!a || a->n_freq < 1 || a->n_illum < 1 || a->relay_nx < 1 || a->relay_ny < 1 ||
+      a->nx < 1 || a->ny < 1 || a->nz < 1 || !a->frequencies || !a->ill_xyz ||
+      (a->n_frames > 0 && !a->times)) {
+    pf_set_error("pf_rsd: bad arguments");
+    return -1;
+  }
+  if (!(close_rel(a->dx, a->relay_dx) && close_rel(a->dy, a->relay_dy))) {
+    pf_set_error("output lateral pitch must equal the relay pitch");
+    return -1;
+  }
+  const double cx = a->relay_x0 + (a->relay_nx / 2) * a->relay_dx;
+  const double cy = a->relay_y0 + (a->relay_ny / 2) * a->relay_dy;
+  const double qx = (a->x0 - cx) / a->relay_dx, qy = (a->y0 - cy) / a->relay_dy;
+  const double rx = nearbyint(qx), ry = nearbyint(qy);
+  if (fabs(qx - rx) > 1e-9 * fmax(1.0, fabs(qx))) {
+    pf_set_error("output grid x origin offset must be an integer multiple of the lattice pitch");
+    return -1;
+  }
+  if (fabs(qy - ry) > 1e-9 * fmax(1.0, fabs(qy))) {
+    pf_set_error("output grid y origin offset must be an integer multiple of the lattice pitch");
+    return -1;
+  }
+  for (int k = 0; k < a->nz; k++)
+    if (!(a->z0 + k * a->dz > a->relay_z)) {
+      pf_set_error("every voxel plane must lie strictly beyond the relay plane");
+      return -1;
+    }
+  const int nu0x = (int)rx, nu0y = (int)ry;
+  const int gx = a->relay_nx, gy = a->relay_ny;
+  const int jx_lo = -(gx / 2), jx_hi = gx - gx / 2 - 1, jy_lo = -(gy / 2), jy_hi = gy - gy / 2 - 1;
+  const int nux_lo = nu0x, nux_hi = nu0x + a->nx - 1, nuy_lo = nu0y, nuy_hi = nu0y + a->ny - 1;
+  long px, py;
+  if (a->padding_none) {
+    if (!(a->nx == gx && a->ny == gy && nu0x == jx_lo && nu0y == jy_lo)) {
+      pf_set_error("padding='none' requires the output lattice to coincide with the relay "
+                   "lattice");
+      return -1;
+    }
+    px = gx;
+    py = gy;
+  } else {
+    const double lx = fmax(abs(nux_lo - jx_hi), abs(nux_hi - jx_lo));
+    const double ly = fmax(abs(nuy_lo - jy_hi), abs(nuy_hi - jy_lo));
+    px = exact_pad(lx, fmax(fmax(abs(nux_lo), abs(nux_hi)), gx / 2), gx);
+    py = exact_pad(ly, fmax(fmax(abs(nuy_lo), abs(nuy_hi)), gy / 2), gy);
+  }
+  int rad[PF_MAX_STAGES];
+  if (radices(px, rad) < 0 || radices(py, rad) < 0) {
+    pf_set_error("pf_rsd: pad is not 11-smooth");
+    return -1;
+  }
+  pf_prop_geom g{};
+  g.px = (int)px;
+  g.py = (int)py;
+  g.nx = a->nx;
+  g.ny = a->ny;
+  g.nu0x = nu0x;
+  g.nu0y = nu0y;
+  g.n_illum = a->n_illum;
+  g.include_illum = a->include_illum ? 1 : 0;
+  g.uhat_illum_stride = px * py;
+  L->px = (int)px;
+  L->py = (int)py;
+  L->nu0x = nu0x;
+  L->nu0y = nu0y;
+  L->fast = pf_prop_fast(&g) != 0;
+  // plane batch (reconstruct.Propagator): ws_a + ws_b within 64 MB; register path: a
+  // multiple of 4 (32 / L) planes, at most 4 (32 / L)
+  const int64_t per = 8 * ((int64_t)(py / 2 + 1) * (px / 2 + 1) + (int64_t)a->n_illum * a->ny * px);
+  int batch = (int)fmax(1.0, fmin((double)a->nz, (double)(BATCH_BYTES / per)));
+  if (L->fast) {
+    const int l = (int)(px / 32), q = 4 * (32 / l);
+    int b = (batch / q) * q;
+    if (b < q) b = q;
+    batch = b;
+    if (batch > 4 * (32 / l)) batch = 4 * (32 / l);
+    if (batch > a->nz) batch = a->nz;
+  }
+  L->batch = batch;
+  const int nb = (a->nz + batch - 1) / batch;
+  L->lanes = nb < LANES ? nb : LANES;
+  // Horner's rule in C: register path, centred crops, one illumination, one frame,
+  // uniformly spaced frequencies
+  const int F = a->n_freq;
+  L->horner = L->fast && F >= 2 && a->n_frames <= 1 && a->n_illum == 1 && a->include_illum &&
+              2 * a->nx == px && 2 * a->ny == py && 2 * nu0x == -a->nx && 2 * nu0y == -a->ny;
+  if (L->horner) {
+    const double d0 = a->frequencies[1] - a->frequencies[0];
+    for (int f = 1; f < F; f++)
+      if (fabs((a->frequencies[f] - a->frequencies[f - 1]) - d0) > 1e-9 * fabs(d0))
+        L->horner = false;
+    L->dkhat = d0 / C_LIGHT;
+  }
+  const int frames = a->n_frames > 0 ? a->n_frames : 1;
+  L->n_twx = (int64_t)twiddles(px).size();
+  L->n_twy = py == px ? 0 : (int64_t)twiddles(py).size();
+  int64_t o = 0;
+  L->off_twx = o; o = align256(o + 8 * L->n_twx);
+  L->off_twy = o; o = align256(o + 8 * L->n_twy);
+  L->off_planes = o; o = align256(o + (int64_t)sizeof(pf_plane) * a->nz);
+  L->off_ill = o; o = align256(o + 8 * 3 * a->n_illum);
+  L->off_fw = o; o = align256(o + 8 * (int64_t)F * frames);
+  L->off_uhat = o; o = align256(o + 8 * (int64_t)F * a->n_illum * px * py);
+  L->off_wa = o; o = align256(o + 8 * L->lanes * pf_prop_ws_a(&g, batch));
+  L->off_wb = o; o = align256(o + 8 * L->lanes * pf_prop_ws_b(&g, batch));
+  L->off_wo = o;
+  if (L->horner && F > HORNER_BLOCK) o = align256(o + 8 * (int64_t)L->lanes * batch * a->nx * a->ny);
+  L->total = o;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" int64_t pf_rsd_workspace_bytes(const pf_rsd_args* a) {
+  Layout L;
+  if (plan(a, &L) != 0) return -1;
+  return L.total;
+}
+
+extern "C" int pf_rsd(const pf_rsd_args* a, const void* slices, void* vol, void* ws,
+                      int64_t ws_bytes, void* stream) {
+  Layout L;
+  if (plan(a, &L) != 0) return -1;
+  PF_ARG_CHECK(slices && vol && ws && ws_bytes >= L.total,
+               "pf_rsd: null buffer or workspace smaller than pf_rsd_workspace_bytes");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  const int F = a->n_freq, I = a->n_illum, frames = a->n_frames > 0 ? a->n_frames : 1;
+  const int64_t V = (int64_t)a->nz * a->ny * a->nx;
+  // ---- tables (host, fp64) -> workspace
+  pf_fft_plan plx{}, ply{};
+  {
+    std::vector<float2> tx = twiddles(L.px);
+    PF_CUDA_CHECK(cudaMemcpyAsync(w + L.off_twx, tx.data(), 8 * tx.size(),
+                                  cudaMemcpyHostToDevice, st), "pf_rsd: upload");
+    plx.n = L.px;
+    plx.nst = radices(L.px, plx.radix);
+    plx.tw = w + L.off_twx;
+    if (L.py != L.px) {
+      std::vector<float2> ty = twiddles(L.py);
+      PF_CUDA_CHECK(cudaMemcpyAsync(w + L.off_twy, ty.data(), 8 * ty.size(),
+                                    cudaMemcpyHostToDevice, st), "pf_rsd: upload");
+      ply.n = L.py;
+      ply.nst = radices(L.py, ply.radix);
+      ply.tw = w + L.off_twy;
+    } else {
+      ply = plx;
+    }
+  }
+  std::vector<pf_plane> planes(a->nz);
+  for (int k = 0; k < a->nz; k++) {
+    const double z = a->z0 + k * a->dz;
+    planes[k] = pf_plane{z - a->relay_z, a->relay_dx, a->relay_dy, a->x0, a->dx, a->y0, a->dy,
+                         z, 0, k};
+  }
+  PF_CUDA_CHECK(cudaMemcpyAsync(w + L.off_planes, planes.data(), sizeof(pf_plane) * a->nz,
+                                cudaMemcpyHostToDevice, st), "pf_rsd: upload");
+  PF_CUDA_CHECK(cudaMemcpyAsync(w + L.off_ill, a->ill_xyz, 8 * 3 * I, cudaMemcpyHostToDevice, st),
+                "pf_rsd: upload");
+  std::vector<float2> fw((size_t)F * frames);
+  for (int f = 0; f < F; f++)
+    for (int j = 0; j < frames; j++) {
+      const double ph = a->n_frames > 0 ? a->frequencies[f] * a->times[j] : 0.0;
+      fw[(size_t)f * frames + j] = make_float2((float)cos(ph), (float)sin(ph));
+    }
+  PF_CUDA_CHECK(cudaMemcpyAsync(w + L.off_fw, fw.data(), 8 * fw.size(), cudaMemcpyHostToDevice, st),
+                "pf_rsd: upload");
+  PF_CUDA_CHECK(cudaMemsetAsync(vol, 0, 8 * (size_t)frames * V, st), "pf_rsd: zero volume");
+
+  pf_prop_geom g{};
+  g.px = L.px;
+  g.py = L.py;
+  g.nx = a->nx;
+  g.ny = a->ny;
+  g.nu0x = L.nu0x;
+  g.nu0y = L.nu0y;
+  g.n_illum = I;
+  g.include_illum = a->include_illum ? 1 : 0;
+  g.uhat_illum_stride = (int64_t)L.px * L.py;
+  float2* uhat = (float2*)(w + L.off_uhat);
+  // ---- relay spectra Uhat_f = cfft2(pad_embed(u_f)) (transposed on the register path)
+  int rc;
+  if (L.fast) {
+    rc = pf_relay_spectra_fast(slices, (int64_t)F * I, a->relay_ny, a->relay_nx,
+                               (int64_t)a->relay_ny * a->relay_nx, uhat, L.px, &plx, stream);
+  } else {
+    rc = pf_embed_centered(slices, (int64_t)F * I, a->relay_ny, a->relay_nx,
+                           (int64_t)a->relay_ny * a->relay_nx, uhat, L.py, L.px, 0, stream);
+    if (rc == 0)
+      rc = pf_fft_lines(uhat, &plx, (int64_t)F * I * L.py, 1, 0, L.px, 1, -1, 1.0f, stream);
+    if (rc == 0)
+      rc = pf_fft_lines(uhat, &ply, (int64_t)F * I * L.px, L.px, 1, (int64_t)L.py * L.px, L.px,
+                        -1, 1.0f, stream);
+  }
+  if (rc != 0) return rc;
+  // ---- lanes forked from the caller's stream
+  cudaStream_t lane_st[LANES];
+  cudaEvent_t ev_fork, ev_join[LANES];
+  PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "pf_rsd: event");
+  PF_CUDA_CHECK(cudaEventRecord(ev_fork, st), "pf_rsd: event");
+  for (int l = 0; l < L.lanes; l++) {
+    PF_CUDA_CHECK(cudaStreamCreateWithFlags(&lane_st[l], cudaStreamNonBlocking), "pf_rsd: stream");
+    PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join[l], cudaEventDisableTiming), "pf_rsd: event");
+    PF_CUDA_CHECK(cudaStreamWaitEvent(lane_st[l], ev_fork, 0), "pf_rsd: fork");
+  }
+  const pf_plane* planes_d = (const pf_plane*)(w + L.off_planes);
+  const double* ill_d = (const double*)(w + L.off_ill);
+  const float2* fw_d = (const float2*)(w + L.off_fw);
+  const int64_t per_f = (int64_t)I * L.px * L.py;
+  const int64_t wa_n = pf_prop_ws_a(&g, L.batch), wb_n = pf_prop_ws_b(&g, L.batch);
+  const int64_t wo_n = (int64_t)L.batch * a->nx * a->ny;
+  rc = 0;
+  for (int b0 = 0, bi = 0; b0 < a->nz && rc == 0; b0 += L.batch, bi++) {
+    const int lane = bi % L.lanes;
+    void* ls = (void*)lane_st[lane];
+    const int nb = a->nz - b0 < L.batch ? a->nz - b0 : L.batch;
+    const pf_plane* pp = planes_d + b0;
+    float2* wa = (float2*)(w + L.off_wa) + lane * wa_n;
+    float2* wb = (float2*)(w + L.off_wb) + lane * wb_n;
+    float2* wo = (float2*)(w + L.off_wo) + lane * wo_n;
+    for (int s = 0; s < F && rc == 0; s++) {
+      const int f = L.horner ? F - 1 - s : s;   // Horner: descending frequencies
+      const double khat = a->frequencies[f] / C_LIGHT;
+      const float2* uh = uhat + f * per_f;
+      rc = pf_prop_kernel_rows(pp, nb, khat, &g, &plx, wa, ls);
+      if (rc == 0) rc = pf_prop_columns(pp, nb, &g, &ply, wa, uh, wb, 0, ls);
+      if (rc != 0) break;
+      if (L.horner) {
+        int mode;
+        if (F <= HORNER_BLOCK) {
+          mode = f == 0 ? 2 : 1;
+        } else {
+          mode = f == 0 ? 4 : (f % HORNER_BLOCK == 0 ? 3 : 1);
+          if (f == F - 1)
+            PF_CUDA_CHECK(cudaMemsetAsync(wo, 0, 8 * (size_t)nb * a->nx * a->ny, lane_st[lane]),
+                          "pf_rsd: zero");
+        }
+        rc = pf_prop_rows_out_horner(pp, nb, khat, L.dkhat, mode, &g, &plx, wb, ill_d,
+                                     fw_d + (int64_t)f * frames, vol, wo,
+                                     HORNER_BLOCK * L.dkhat, ls);
+      } else {
+        rc = pf_prop_rows_out(pp, nb, khat, &g, &plx, wb, ill_d, fw_d + (int64_t)f * frames,
+                              frames, vol, V, ls);
+      }
+    }
+  }
+  for (int l = 0; l < L.lanes; l++) {
+    cudaEventRecord(ev_join[l], lane_st[l]);
+    cudaStreamWaitEvent(st, ev_join[l], 0);
+    cudaEventDestroy(ev_join[l]);
+    cudaStreamDestroy(lane_st[l]);
+  }
+  cudaEventDestroy(ev_fork);
+  return rc;
+}

@@ -77,6 +77,15 @@ void pf_note_launch();
     }                                                                      \
   } while (0)
 
+#define PF_CUDA_CHECK(call, what)                                          \
+  do {                                                                     \
+    cudaError_t e__ = (call);                                              \
+    if (e__ != cudaSuccess) {                                              \
+      pf_set_error("%s: %s", what, cudaGetErrorString(e__));               \
+      return (int)e__;                                                     \
+    }                                                                      \
+  } while (0)
+
 #define PF_ARG_CHECK(cond, msg)                                            \
   do {                                                                     \
     if (!(cond)) {                                                         \

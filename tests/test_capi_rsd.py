@@ -1,0 +1,123 @@
+"""The whole-algorithm C entry point pf_rsd (include/pfgpu.h), called the way a reference-side
+ctypes binding would call it: host geometry and frequency arrays, device
+slices / volume / workspace pointers, the caller's stream.  CPU tests cover the planning
+and the reference's validation messages (no device needed); GPU tests compare the result
+with the float64 oracle (reference rsd, reconstruct.py:208-268) and with the Python engine.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2501_05244_b200 as pf
+from oracle import pf_oracle as O
+from paper_2501_05244_b200 import _lib
+from paper_2501_05244_b200.core import illumination_coordinates
+
+TOL = 1e-4
+
+
+def rsd_args(slices, grid, padding="exact", times=None, include_illumination=True):
+    """pf_rsd_args from reference objects (the binding a maintainer would add); the host
+    arrays are returned too so they outlive the call."""
+    g, vg = slices.relay.grid, grid.grid
+    freqs = np.ascontiguousarray(slices.frequencies, dtype=np.float64)
+    ill = np.ascontiguousarray(illumination_coordinates(slices.relay, slices.illuminations),
+                               dtype=np.float64)
+    t = None if times is None else np.ascontiguousarray(times, dtype=np.float64)
+    a = _lib.PfRsdArgs(relay_nx=g.nx, relay_ny=g.ny, relay_dx=g.dx, relay_dy=g.dy,
+                       relay_x0=g.x0, relay_y0=g.y0, relay_z=g.z, nx=vg.nx, ny=vg.ny, nz=vg.nz,
+                       dx=vg.dx, dy=vg.dy, dz=vg.dz, x0=vg.x0, y0=vg.y0, z0=vg.z0,
+                       n_freq=freqs.size, n_illum=ill.shape[0],
+                       frequencies=freqs.ctypes.data, ill_xyz=ill.ctypes.data,
+                       n_frames=0 if t is None else t.size,
+                       times=None if t is None else t.ctypes.data,
+                       padding_none=int(padding == "none"),
+                       include_illum=int(bool(include_illumination)))
+    return a, (freqs, ill, t)
+
+
+def capi_rsd(slices, grid, **kw):
+    import torch
+    a, keep = rsd_args(slices, grid, **kw)
+    lib = _lib.load()
+    nbytes = lib.pf_rsd_workspace_bytes(ctypes.byref(a))
+    assert nbytes > 0, _lib.last_error()
+    c = np.asarray(slices.coefficients)                       # [I, D, F]
+    coeff = torch.from_numpy(np.ascontiguousarray(c.transpose(2, 0, 1)).astype(np.complex64)).cuda()
+    frames = max(1, a.n_frames)
+    vol = torch.empty((frames, grid.count), dtype=torch.complex64, device="cuda")
+    ws = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    rc = lib.pf_rsd(ctypes.byref(a), coeff.data_ptr(), vol.data_ptr(), ws.data_ptr(), nbytes, s)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    return vol.cpu().numpy()
+
+
+def _scene(rng, n, F=4, n_ill=1, nz=3, off=0, nx=None, ny=None, dz=0.25, spacing=0.02):
+    p = 2.0 / n
+    g = pf.UniformGrid2D(n, n, p, p, -1 + p / 2, -1 + p / 2, 0.0)
+    freqs = 2 * np.pi * 3e8 / 0.06 * (1 + spacing * np.arange(F))
+    c = rng.normal(size=(n_ill, n * n, F)) + 1j * rng.normal(size=(n_ill, n * n, F))
+    ill = pf.PointList(rng.uniform(-0.3, 0.3, size=(n_ill, 2)))
+    sl = pf.FrequencySlices(freqs, c, pf.UniformRelay(g), ill)
+    nx, ny = nx or n, ny or n
+    grid = pf.CuboidGrid(pf.UniformGrid3D(nx, ny, nz, p, p, dz, g.x0 + off * p, g.y0 + off * p, 0.5))
+    return sl, grid
+
+
+# ---------------------------------------------------------------- CPU: planning + validation
+
+def test_workspace_bytes_config4_geometry():
+    from paper_2501_05244_b200 import configs
+    cfg = configs.config(4)
+    k = configs.kernel(cfg)
+    sl = type("S", (), dict(frequencies=k.frequencies, relay=cfg.relay,
+                            illuminations=cfg.illuminations))()
+    a, _ = rsd_args(sl, cfg.grid)
+    nbytes = _lib.load().pf_rsd_workspace_bytes(ctypes.byref(a))
+    # Uhat (32 x 1024^2 c64 = 256 MiB) + 3 lanes x 4 planes of A and B workspaces
+    assert 256 << 20 < nbytes < 512 << 20
+
+
+@pytest.mark.parametrize("change,match", [
+    (dict(dx=0.05), "pitch"), (dict(x0=0.013), "origin"), (dict(z0=-0.2), "beyond the relay"),
+    (dict(nx=20), "padding='none'")])
+def test_validation_messages(rng, change, match):
+    sl, grid = _scene(rng, 32)
+    a, keep = rsd_args(sl, grid, padding="none" if match == "padding='none'" else "exact")
+    for k, v in change.items():
+        setattr(a, k, v)
+    assert _lib.load().pf_rsd_workspace_bytes(ctypes.byref(a)) == -1
+    assert match in _lib.last_error()
+
+
+# ---------------------------------------------------------------- GPU: results
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [
+    dict(n=64),                                 # P = 128 register path, Horner C
+    dict(n=64, F=40),                           # Horner in 32-frequency blocks
+    dict(n=64, n_ill=2),                        # two illuminations (per-frequency phases)
+    dict(n=40, nx=30, ny=24, off=3),            # generic pad, offset window
+    dict(n=128, nz=5),                          # P = 256
+])
+def test_pf_rsd_matches_oracle_and_engine(rng, case):
+    sl, grid = _scene(rng, **case)
+    got = capi_rsd(sl, grid)[0]
+    ref = O.rsd(sl, grid)
+    assert O.rel_l2(got, ref) < TOL
+    eng = pf.rsd(sl, grid).field
+    assert O.rel_l2(got, eng) < 1e-5
+
+
+@pytest.mark.gpu
+def test_pf_rsd_video_and_no_padding(rng):
+    sl, grid = _scene(rng, 32, F=3)
+    times = np.array([0.0, 1.5e-10, 4e-10])
+    got = capi_rsd(sl, grid, times=times)
+    assert O.rel_l2(got, O.rsd(sl, grid, times=times)) < TOL
+    got = capi_rsd(sl, grid, padding="none", include_illumination=False)[0]
+    assert O.rel_l2(got, O.rsd(sl, grid, padding="none", include_illumination=False)) < TOL
