@@ -36,6 +36,10 @@ extern "C" {
 /* Mixed-radix plan for one transform length (host struct, passed by pointer).
  * radix[] lists the stage radices (2,3,4,5,7,8,11,16); tw is a DEVICE table of
  * n complex64 unit roots W_n^m = exp(-2 pi i m / n) built in float64. */
+/* A plan whose radix[PF_MAX_STAGES - 1] holds PF_XFFT_TAG carries, after its n unit
+ * roots, the k1-major twiddle table [35][L] (W_n^{k1 t}) of the mixed-radix register FFT
+ * for n = 35 L, L in {4, 5, 8, 10, 15, 20, 30} (pf_fft_lines then takes that kernel). */
+#define PF_XFFT_TAG 0x35F7
 typedef struct pf_fft_plan {
   int n;
   int nst;

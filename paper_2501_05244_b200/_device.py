@@ -50,6 +50,18 @@ def radices_for(n: int) -> list[int]:
     return pow2 + sorted(odd, reverse=True)
 
 
+PF_MAX_STAGES = 24
+PF_XFFT_TAG = 0x35F7     # include/pfgpu.h
+
+
+def xfft_L(n: int) -> int:
+    """Lanes of the mixed-radix register FFT for n = 35 L (xfft.cuh), else 0."""
+    if n % 35:
+        return 0
+    L = n // 35
+    return L if L in (4, 5, 8, 10, 15, 20, 30) else 0
+
+
 class FftPlan:
     """Mixed-radix plan for one length on one device (twiddles built in float64)."""
 
@@ -65,6 +77,12 @@ class FftPlan:
             k1 = np.arange(32)[:, None]
             t = np.arange(L)[None, :]
             w = np.concatenate([w, np.exp(-2j * np.pi * ((k1 * t) % self.n) / self.n).ravel()])
+        xl = xfft_L(self.n)
+        if xl:
+            # mixed-radix register FFT (n = 35 L): k1-major table [35][L] after the roots
+            k1 = np.arange(35)[:, None]
+            t = np.arange(xl)[None, :]
+            w = np.concatenate([w, np.exp(-2j * np.pi * ((k1 * t) % self.n) / self.n).ravel()])
         self.tw = torch.from_numpy(w.astype(np.complex64)).to(device)
         self.c = _lib.PfFftPlan()
         self.c.n = self.n
@@ -72,6 +90,8 @@ class FftPlan:
         for i, r in enumerate(rad):
             self.c.radix[i] = r
         self.c.tw = ctypes.c_void_p(ptr(self.tw))
+        if xl:
+            self.c.radix[PF_MAX_STAGES - 1] = PF_XFFT_TAG
 
     @property
     def ref(self):

@@ -19,8 +19,7 @@
 
 #include <vector>
 
-#include "common.cuh"
-#include "../../include/pfgpu.h"
+#include "xfft.cuh"
 
 namespace {
 
@@ -86,6 +85,14 @@ std::vector<float2> twiddles(long n) {
   for (long m = 0; m < n; m++) {
     const double a = -2.0 * M_PI * (double)m / (double)n;
     w.push_back(make_float2((float)cos(a), (float)sin(a)));
+  }
+  const long xl = xfft_L((int)n);
+  if (xl) {   // mixed-radix register FFT: k1-major [35][L]
+    for (long k1 = 0; k1 < 35; k1++)
+      for (long t = 0; t < xl; t++) {
+        const double a = -2.0 * M_PI * (double)((k1 * t) % n) / (double)n;
+        w.push_back(make_float2((float)cos(a), (float)sin(a)));
+      }
   }
   if (n == 128 || n == 256 || n == 512 || n == 1024) {
     const long L = n / 32;
@@ -248,6 +255,7 @@ extern "C" int pf_rsd(const pf_rsd_args* a, const void* slices, void* vol, void*
     plx.n = L.px;
     plx.nst = radices(L.px, plx.radix);
     plx.tw = w + L.off_twx;
+    if (xfft_L(L.px)) plx.radix[PF_MAX_STAGES - 1] = PF_XFFT_TAG;
     if (L.py != L.px) {
       std::vector<float2> ty = twiddles(L.py);
       PF_CUDA_CHECK(cudaMemcpyAsync(w + L.off_twy, ty.data(), 8 * ty.size(),
@@ -255,6 +263,7 @@ extern "C" int pf_rsd(const pf_rsd_args* a, const void* slices, void* vol, void*
       ply.n = L.py;
       ply.nst = radices(L.py, ply.radix);
       ply.tw = w + L.off_twy;
+      if (xfft_L(L.py)) ply.radix[PF_MAX_STAGES - 1] = PF_XFFT_TAG;
     } else {
       ply = plx;
     }

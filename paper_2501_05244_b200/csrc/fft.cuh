@@ -195,6 +195,32 @@ struct Dft<11, DIR> {
   static __device__ __forceinline__ void run(float2* v) { dft_odd<11, DIR>(v); }
 };
 
+// composite odd / mixed lengths of the mixed-radix register FFT (xfft.cuh)
+template <int DIR>
+struct Dft<6, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_ct<2, 3, DIR>(v); }
+};
+template <int DIR>
+struct Dft<10, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_ct<2, 5, DIR>(v); }
+};
+template <int DIR>
+struct Dft<15, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_ct<3, 5, DIR>(v); }
+};
+template <int DIR>
+struct Dft<20, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_ct<4, 5, DIR>(v); }
+};
+template <int DIR>
+struct Dft<30, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_ct<5, 6, DIR>(v); }
+};
+template <int DIR>
+struct Dft<35, DIR> {
+  static __device__ __forceinline__ void run(float2* v) { dft_ct<5, 7, DIR>(v); }
+};
+
 // One Stockham stage over `cnt` transforms (transform b at buf + b*ld).
 // Division by a block-invariant divisor d >= 1 for 0 <= x < 2^22:
 // float reciprocal estimate plus one integer correction (exact in that range),

@@ -6,7 +6,7 @@
 // `cnt` lines in shared memory with coalesced loads (element-major when the
 // lines are columns, line-major when they are rows), runs the Stockham
 // transform (fft.cuh), and writes them back in place.
-#include "fft.cuh"
+#include "xfft.cuh"
 
 namespace {
 
@@ -50,6 +50,101 @@ k_fft_lines(float2* __restrict__ data, pf_fft_plan plan, long long nlines, long 
     if (rows) { c = q; i = e - q * n; } else { i = q; c = e - q * nl; }
     data[lbase[c] + (long long)i * estr] = cscale(r[c * ld + i], scale);
   }
+}
+
+// Lengths n = 35 L (xfft.cuh): the same staging (coalesced tile of lines in shared
+// memory), then each warp transforms 32 / L lines in registers, using each line's own
+// tile row as its exchange buffer, and writes the result back into the row in natural
+// order before the coalesced store.
+template <int L, int DIR>
+__global__ void __launch_bounds__(FL_THREADS, 2)
+k_xfft_lines(float2* __restrict__ data, const float2* __restrict__ tw2, long long nlines,
+             long long inner, long long istr, long long ostr, long long estr, float scale) {
+  constexpr int N = XFFT_R * L, LD = N + ((N % 16) == 0 ? 1 : 0), LPW = 32 / L;
+  constexpr int CNT = 8 * LPW, J = xfft_J(L);
+  extern __shared__ float2 sm[];
+  __shared__ long long lbase[CNT];
+  const long long l0 = (long long)blockIdx.x * CNT;
+  const int nl = (int)(nlines - l0 < CNT ? nlines - l0 : CNT);
+  const int tot = nl * N;
+  const bool rows = (estr == 1);
+  for (int c = threadIdx.x; c < nl; c += FL_THREADS) lbase[c] = line_base(l0 + c, inner, istr, ostr);
+  __syncthreads();
+  const FastDiv split(rows ? N : nl);
+  for (int e = threadIdx.x; e < tot; e += FL_THREADS) {
+    const int q = split.div(e);
+    int c, i;
+    if (rows) { c = q; i = e - q * N; } else { i = q; c = e - q * nl; }
+    sm[c * LD + i] = data[lbase[c] + (long long)i * estr];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane % L, line = lane / L;
+  const bool active = line < LPW && warp * LPW + line < nl;
+  float2* row = sm + (warp * LPW + (line < LPW ? line : 0)) * LD;
+  float2 v[XFFT_R];
+#pragma unroll
+  for (int m = 0; m < XFFT_R; m++) v[m] = row[t + L * m];
+  float2 w[J][L];
+  xfft<L, DIR>(v, w, row, tw2, t, active);
+  if (active) {
+#pragma unroll
+    for (int j = 0; j < J; j++) {
+      const int k1 = t + L * j;
+      if (J * L == XFFT_R || k1 < XFFT_R) {
+#pragma unroll
+        for (int k2 = 0; k2 < L; k2++) row[k1 + XFFT_R * k2] = w[j][k2];
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < tot; e += FL_THREADS) {
+    const int q = split.div(e);
+    int c, i;
+    if (rows) { c = q; i = e - q * N; } else { i = q; c = e - q * nl; }
+    data[lbase[c] + (long long)i * estr] = cscale(sm[c * LD + i], scale);
+  }
+}
+
+template <int L, int DIR>
+int launch_xlines(float2* data, const pf_fft_plan& p, long long nlines, long long inner,
+                  long long istr, long long ostr, long long estr, float scale, cudaStream_t st) {
+  constexpr int N = XFFT_R * L, LD = N + ((N % 16) == 0 ? 1 : 0), CNT = 8 * (32 / L);
+  const size_t smem = (size_t)CNT * LD * sizeof(float2);
+  static PfDevOnce attr;
+  if (attr.first())
+    cudaFuncSetAttribute(k_xfft_lines<L, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  const long long grid = (nlines + CNT - 1) / CNT;
+  const float2* tw2 = reinterpret_cast<const float2*>(p.tw) + N;   // after the n unit roots
+  k_xfft_lines<L, DIR><<<(unsigned)grid, FL_THREADS, smem, st>>>(data, tw2, nlines, inner, istr,
+                                                                  ostr, estr, scale);
+  PF_LAUNCH_CHECK("k_xfft_lines");
+  return 0;
+}
+
+template <int DIR>
+int launch_xfft(float2* data, const pf_fft_plan& p, long long nlines, long long inner,
+                long long istr, long long ostr, long long estr, float scale, cudaStream_t st) {
+  switch (xfft_L(p.n)) {
+    case 4: return launch_xlines<4, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
+    case 5: return launch_xlines<5, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
+    case 8: return launch_xlines<8, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
+    case 10: return launch_xlines<10, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
+    case 15: return launch_xlines<15, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
+    case 20: return launch_xlines<20, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
+    case 30: return launch_xlines<30, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
+    default: return 1;
+  }
+}
+
+static bool xfft_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PF_XFFT");
+    on = (e == nullptr || atoi(e) != 0) ? 1 : 0;
+  }
+  return on == 1;
 }
 
 // transpose=1 writes dst[bb][jx][jy] (the transposed grid, px rows of py)
@@ -109,6 +204,13 @@ extern "C" int pf_fft_lines(void* data, const pf_fft_plan* plan, int64_t nlines,
   PF_ARG_CHECK(inner >= 1 && nlines >= 0, "pf_fft_lines: bad line layout");
   if (nlines == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
+  // 35 L lengths: the register mixed-radix kernel (the plan carries its twiddle table)
+  if (xfft_L(plan->n) && plan->radix[PF_MAX_STAGES - 1] == PF_XFFT_TAG && xfft_enabled()) {
+    return dir < 0 ? launch_xfft<-1>((float2*)data, *plan, nlines, inner, inner_stride,
+                                     outer_stride, elem_stride, scale, st)
+                   : launch_xfft<1>((float2*)data, *plan, nlines, inner, inner_stride,
+                                    outer_stride, elem_stride, scale, st);
+  }
   if (dir < 0)
     return launch_lines<-1>((float2*)data, *plan, nlines, inner, inner_stride, outer_stride,
                             elem_stride, scale, st);

@@ -64,8 +64,8 @@ def test_to_frequency_sizes(rng, T):
     assert O.rel_l2(sl.coefficients, ref) < 2e-6
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 8, 11, 12, 13, 16, 17, 30, 49, 64, 97, 121, 128, 140, 194, 280,
-                               512, 525, 1024, 1050, 2048, 2100])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 8, 11, 12, 13, 16, 17, 30, 49, 64, 97, 121, 128, 140, 175,
+                               194, 280, 350, 512, 525, 700, 1024, 1050, 2048, 2100])
 def test_fft_lines_vs_numpy(rng, n):
     from paper_2501_05244_b200 import _device as dev
     x = (rng.normal(size=(3, n)) + 1j * rng.normal(size=(3, n))).astype(np.complex64)
@@ -76,7 +76,8 @@ def test_fft_lines_vs_numpy(rng, n):
     assert O.rel_l2(t.cpu().numpy(), x) < 2e-6
 
 
-@pytest.mark.parametrize("shape", [(6, 10), (9, 7), (64, 64), (140, 140), (20, 16, 8)])
+@pytest.mark.parametrize("shape", [(6, 10), (9, 7), (64, 64), (140, 140), (20, 16, 8),
+                                   (350, 12), (700, 5), (1050, 3), (3, 140, 280), (41, 175)])
 def test_fftn_vs_numpy(rng, shape):
     from paper_2501_05244_b200 import _device as dev
     x = (rng.normal(size=(2,) + shape) + 1j * rng.normal(size=(2,) + shape)).astype(np.complex64)
