@@ -253,6 +253,10 @@ def run_ours(args):
         s3_flops += units * (cfg.relay.grid.ny + P) * 2 * 5.0 * Q * math.log2(Q)
     if cfg.algorithm == "nursd1":   # + per-(f, p) type-1 NUFFT: fine-grid FFT + 17x17 spread
         s3_flops += F * I * (5.0 * (2 * P) ** 2 * math.log2((2 * P) ** 2) + cfg.relay.count * 17 * 17 * 8)
+    kernel_name = ("propagation k_pa + k_pb12 + k_pc_h (pf_prop_kernel_rows / columns / "
+                   "rows_out_horner, S3)")
+    if explicit:
+        s3_flops, kernel_name = _explicit_flops(eng, F, I, cfg)
     fp32_nominal = 148 * 128 * 2 * sm_max * 1e6 / 1e12
     fp32_peak = fp32_meas if fp32_meas > 0 else fp32_nominal
     clocks = clk.summary()
@@ -263,7 +267,7 @@ def run_ours(args):
     roof_k1["frac"] = roof_k1["achieved"] / hbm_peak
     roof_s3 = {"bound": "fp32", "achieved": s3_flops / (s3_ms * 1e-3) / 1e12, "peak": fp32_peak,
                "unit": "TFLOP/s", "traffic": _prop_traffic(F, k_hi - k_lo, args.config),
-               "kernel": "propagation k_pa+k_pb1+k_pb2+k_pc_h (pf_prop_kernel_rows/columns/rows_out_horner, S3)",
+               "kernel": kernel_name,
                "ms": s3_ms, "peak_source": "measured on this GPU before the timed region: FFMA probe "
                                            "(pf_fp32_probe, best of 6); nominal %.1f TFLOP/s = "
                                            "148 SM x 128 lanes x 2 x sm_max_mhz; MEASURED_PEAKS.json "
@@ -427,6 +431,23 @@ def _executed_flops(cfg, eng, F, nz, I):
     return flops, ("(F*Nz*I*((P/2+1) + (P/2+1) + (P) + ny) + F*I*(ny + P)) * 5 P log2 P, "
                    "P=%d, ny=%d: executed line-FFTs after the kernel symmetry and crop "
                    "pruning" % (P, ny))
+
+
+def _explicit_flops(eng, F, I, cfg):
+    """Config 2 (nursd3d stage 1 + nursd2 readout), standard counts: stage 1 per frequency
+    = 3D type-1 spreading (L points x 17^3 x 8) + the 3D fine-grid FFT; stage 2 per
+    (frequency, plane) = the kernel's 2D FFT on the P x P pad + the fine-grid inverse FFT
+    + the 17 x 17 interpolation of every voxel (8 flops per tap)."""
+    s1, s2 = eng.stage1, eng.stage2.ro
+    fine3 = int(s1.plan.fine_elems) if hasattr(s1, "plan") else 0
+    f1 = F * I * (cfg.relay.count * 17 ** 3 * 8 + (5.0 * fine3 * math.log2(fine3) if fine3 else 0))
+    P2 = s2.px * s2.py
+    fine2 = s2.plan.fine_elems
+    nplanes = s2.n_planes
+    f2 = F * I * nplanes * (5.0 * P2 * math.log2(P2) + 5.0 * fine2 * math.log2(fine2))
+    f2 += F * I * cfg.n_voxels * 17 * 17 * 8
+    return f1 + f2, ("stage 1 + stage 2 (type-1 spread + 3D FFT; kernel 2D FFT + fine-grid "
+                     "IFFT + 17x17 interpolation; 5 n log2 n per FFT, 8 flops per tap)")
 
 
 def _flops_model(alg, P):
