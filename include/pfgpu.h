@@ -317,6 +317,11 @@ int pf_zslab(const void* src, int nb, int nz, int64_t nyx, const void* w, float 
              void* dst, void* stream);
 int pf_copy_planes(const void* src, int nb, int64_t src_stride, int64_t plane_off,
                    int64_t plane_elems, void* dst, void* stream);
+/* Centred nx x ny window of nb natural-order py x px planes (inverse of the centred
+ * embed): dst[b][i][j] = src[b][(i - ny/2) mod py][(j - nx/2) mod px]; the virtual plane
+ * of the 3D stage 1 on the frustum-base lattice (3D RSD / NURSD + SRSD). */
+int pf_crop_centered(const void* src, int64_t nb, int py, int px, void* dst, int ny, int nx,
+                     void* stream);
 
 /* circular shift of the trailing axes (n0, n1, n2) of nb arrays:
  * dst[b][j] = src[b][(j + s) mod n] per axis (ifftshift: s = n/2, fftshift: s = n - n/2;

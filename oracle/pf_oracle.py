@@ -825,6 +825,35 @@ def nursd3d_explicit(slices, grid, lattice, eps=1e-6, z_pitch=None, times=None,
     return nursd2(vs, grid, eps=eps, times=times, include_illumination=include_illumination)
 
 
+def lattice_srsd(slices, frustum, stage1="nursd3d", eps=1e-6, scatter="trilinear",
+                 z_pitch=None, times=None, include_illumination=True):
+    """Composed oracle of the paper's "3D RSD / 3D NURSD + SRSD":
+    nursd3d stage 1 (reconstruct.py:741-760) or rsd3d stage 1 (:705-716) on the lattice of
+    the frustum base, the wave slab at z0 cropped to the base window (the centred rows /
+    columns of reconstruct.py:650-651), then srsd (:276-327) from that uniform relay at z0."""
+    b = frustum.base
+    zs = np.asarray(frustum.zs, dtype=np.float64)
+    vg = type("G", (), dict(nx=b.nx, ny=b.ny, dx=b.dx, dy=b.dy, x0=b.x0, y0=b.y0,
+                            z_coords=lambda self: zs))()
+    lattice = type("L", (), dict(grid=vg))()
+    if stage1 == "nursd3d":
+        geo, uplanes = nursd3d_stage1(slices, lattice, eps, z_pitch)
+    else:
+        geo, uplanes = rsd3d_stage1(slices, lattice, scatter, z_pitch)
+    rows = center_slice(geo["py"], b.ny)
+    cols = center_slice(geo["px"], b.nx)
+    waves = [cifft2(u)[:, rows, cols] for u in uplanes]          # [I, ny, nx] per f
+    coeff = np.stack([w.reshape(w.shape[0], -1) for w in waves], axis=-1)   # [I, D, F]
+    grid2 = type("G2", (), dict(nx=b.nx, ny=b.ny, dx=b.dx, dy=b.dy, x0=b.x0, y0=b.y0,
+                                z=geo["z0"], center=lambda self: (
+                                    b.x0 + (b.nx // 2) * b.dx, b.y0 + (b.ny // 2) * b.dy)))()
+    relay = type("R", (), dict(kind="uniform", grid=grid2, z=geo["z0"], count=b.nx * b.ny))()
+    vs = type("S", (), dict(frequencies=slices.frequencies, coefficients=coeff, relay=relay,
+                            illuminations=slices.illuminations,
+                            n_freq=int(np.asarray(slices.frequencies).size)))()
+    return srsd(vs, frustum, times=times, include_illumination=include_illumination)
+
+
 class _FlatView:
     """A 3D relay whose points share one z, viewed as a planar relay (reconstruct.py:735-740)."""
 

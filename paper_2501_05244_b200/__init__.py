@@ -29,7 +29,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # the non-rsd algorithms live in .algorithms (loaded on first use)
     if name in ("srsd", "nursd1", "nursd2", "nursd3", "nursd3d", "srsd_nursd2", "rsd3d",
-                "nursd3d_explicit"):
+                "nursd3d_explicit", "nursd3d_srsd", "rsd3d_srsd"):
         from . import algorithms
         return getattr(algorithms, name)
     if name in ("cfft_n", "cifft_n", "cfft_2d", "cifft_2d", "sfft_1d", "sfft_2d",

@@ -71,6 +71,7 @@ _SIGNATURES = {
     "pf_embed_centered": [_vp, _i64, _i, _i, _i64, _vp, _i, _i, _i, _vp],
     "pf_prop_fast": [_P(PfPropGeom)],
     "pf_rsd_workspace_bytes": [_P(PfRsdArgs)],
+    "pf_crop_centered": [_vp, _i64, _i, _i, _vp, _i, _i, _vp],
     "pf_rsd": [_P(PfRsdArgs), _vp, _vp, _vp, _i64, _vp],
     "pf_nufft_type1_finish_pow2": [_P(PfNufftGeom), _vp, _i64, _i, _vp, _P(PfFftPlan),
                                    _P(PfFftPlan), _vp, _vp, _vp, _i64, _vp],

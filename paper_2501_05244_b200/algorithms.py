@@ -782,6 +782,75 @@ class Rsd3dEngine(_Lattice3dEngine):
         dev.fftn_natural(uhat3, (self.pz, self.py, self.px), self.n_illum, -1, 1.0, stream)
 
 
+class Lattice3dSrsdEngine(GraphedRun):
+    """The paper's "3D RSD / 3D NURSD + SRSD" ("the second stage is
+    simply the standard RSD algorithm, so it can be replaced by SRSD"): stage 1 of nursd3d
+    (reconstruct.py:741-760, 3D type-1 NUFFT) or rsd3d (:705-716, gridding) propagates the
+    scattered 3D relay to the virtual plane z0 beyond its far face, on the lattice of the
+    frustum's base (the lattice the cuboid grid supplies in nursd3d); the wave there,
+    sampled on the base window (the centred crop of reconstruct.py:650-651), is a uniform
+    relay at z0 whose coefficients srsd (:276-327) propagates onto the frustum, so the
+    voxel pitch grows with depth.  No reference entry point exists; the oracle composes the
+    same reference pieces (``oracle.lattice_srsd``)."""
+
+    def __init__(self, slices, grid, stage1: str = "nursd3d", eps: float = 1e-6,
+                 scatter: str = "trilinear", z_pitch: float | None = None, times=None,
+                 include_illumination: bool = True, device=None):
+        from .core import CuboidGrid, UniformGrid2D, UniformGrid3D, UniformRelay
+        _require(_kind(grid) == "frustum", "this algorithm reconstructs onto a frustum grid")
+        _require(stage1 in ("nursd3d", "rsd3d"), "stage 1 must be 'nursd3d' or 'rsd3d'")
+        _nonplanar_relay(slices)
+        self.device = device or dev.require_cuda()
+        b = grid.base
+        zs = np.asarray(grid.zs, dtype=np.float64)
+        # stage-1 lattice: the frustum base's lateral lattice; its one plane at the nearest
+        # frustum depth makes _lattice_3d check every depth against the far face z0
+        lattice = CuboidGrid(UniformGrid3D(b.nx, b.ny, 1, b.dx, b.dy, 1.0, b.x0, b.y0,
+                                           float(zs.min())))
+        if stage1 == "nursd3d":
+            self.stage1 = Nursd3dEngine(slices, lattice, eps, z_pitch, include_illumination,
+                                        None, device=self.device)
+        else:
+            self.stage1 = Rsd3dEngine(slices, lattice, scatter, z_pitch, include_illumination,
+                                      None, device=self.device)
+        z0 = self.stage1.z0
+        vrel = UniformRelay(UniformGrid2D(b.nx, b.ny, b.dx, b.dy, b.x0, b.y0, z0))
+        meta = type("VirtualSlices", (), dict(frequencies=np.asarray(slices.frequencies),
+                                              relay=vrel, illuminations=slices.illuminations))()
+        self.stage2 = SrsdEngine(meta, grid, include_illumination, times, device=self.device)
+        self.times, self.n_frames = self.stage2.times, self.stage2.n_frames
+        self.n_voxels = self.stage2.n_voxels
+        self.px, self.py = self.stage2.px, self.stage2.py
+        F, I = self.stage2.freqs.size, self.stage2.n_illum
+        self.window = torch.empty((F * I * b.ny * b.nx,), dtype=torch.complex64,
+                                  device=self.device)
+
+    def run(self, coeff, vol=None, stream=None):
+        st1 = self.stage1
+        F, I = st1.freqs.size, st1.n_illum
+        b = self.stage2.g
+        planes = st1.virtual_planes(coeff, stream)          # natural order [F*I][py][px]
+        _lib.call("pf_crop_centered", dev.ptr(planes), F * I, st1.py, st1.px,
+                  dev.ptr(self.window), b.ny, b.nx, dev.stream_ptr(stream))
+        return self.stage2.run(self.window.view(F, I, b.ny * b.nx), vol, stream)
+
+
+def nursd3d_srsd(slices, grid, eps: float = 1e-6, z_pitch: float | None = None, times=None,
+                 threads: int = 1, include_illumination: bool = True):
+    """3D NURSD stage 1 + SRSD stage 2 onto a frustum (see :class:`Lattice3dSrsdEngine`)."""
+    eng = Lattice3dSrsdEngine(slices, grid, "nursd3d", eps, "trilinear", z_pitch, times,
+                              include_illumination)
+    return _volume(grid, eng.run(device_coefficients(slices)), eng.times)
+
+
+def rsd3d_srsd(slices, grid, scatter: str = "trilinear", z_pitch: float | None = None,
+               times=None, threads: int = 1, include_illumination: bool = True):
+    """3D RSD (gridded) stage 1 + SRSD stage 2 onto a frustum (:class:`Lattice3dSrsdEngine`)."""
+    eng = Lattice3dSrsdEngine(slices, grid, "rsd3d", 1e-6, scatter, z_pitch, times,
+                              include_illumination)
+    return _volume(grid, eng.run(device_coefficients(slices)), eng.times)
+
+
 def nursd3d(slices, grid, eps: float = 1e-6, z_pitch: float | None = None, times=None,
             threads: int = 1, include_illumination: bool = True):
     """Scattered 3D relay -> cuboid (reconstruct.py:722-765)."""

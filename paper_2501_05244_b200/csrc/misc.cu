@@ -77,6 +77,35 @@ extern "C" int pf_copy_planes(const void* src, int nb, int64_t src_stride, int64
   return 0;
 }
 
+// Centred window of natural-order planes (the inverse of the centred embed):
+// dst[b][i][j] = src[b][(i - ny/2) mod py][(j - nx/2) mod px] -- the virtual plane of the
+// 3D stages sampled on an nx x ny lattice window (the crop of reconstruct.py:650-651).
+namespace {
+__global__ void k_crop_centered(const float2* __restrict__ src, long long nb, int py, int px,
+                                float2* __restrict__ dst, int ny, int nx) {
+  const long long total = nb * (long long)ny * nx;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / ((long long)ny * nx);
+    const int rem = (int)(e - b * (long long)ny * nx);
+    const int i = rem / nx, j = rem - i * nx;
+    const int sy = natural(i - ny / 2, py), sx = natural(j - nx / 2, px);
+    dst[e] = src[(b * py + sy) * (long long)px + sx];
+  }
+}
+}  // namespace
+
+extern "C" int pf_crop_centered(const void* src, int64_t nb, int py, int px, void* dst, int ny,
+                                int nx, void* stream) {
+  PF_ARG_CHECK(nb >= 0 && ny >= 1 && nx >= 1 && ny <= py && nx <= px,
+               "pf_crop_centered: bad sizes");
+  if (nb == 0) return 0;
+  k_crop_centered<<<grid_for(nb * (long long)ny * nx), 256, 0, (cudaStream_t)stream>>>(
+      (const float2*)src, nb, py, px, (float2*)dst, ny, nx);
+  PF_LAUNCH_CHECK("k_crop_centered");
+  return 0;
+}
+
 // One output plane of an inverse DFT along the leading axis (nursd3d stage 1,
 // reference reconstruct.py:758-759: cifft_n over (z, y, x), then the slab plane):
 // dst[b][j] = scale * sum_z src[b][z][j] * w[z], w[z] = exp(+2 pi i z slab / nz) built

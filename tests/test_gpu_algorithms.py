@@ -171,3 +171,26 @@ def test_rsd3d_random_relay_vs_oracle(rng, scatter):
     vol = pf.reconstruct(sl, grid, "rsd3d", scatter=scatter, times=times)
     ref = O.rsd3d(sl, grid, scatter=scatter, times=times)
     assert O.rel_l2(vol.field, ref) < TOL
+
+
+@pytest.mark.parametrize("stage1,video", [("nursd3d", False), ("rsd3d", False), ("nursd3d", True)])
+def test_3d_relay_plus_srsd_vs_composed_oracle(rng, stage1, video):
+    """The paper's "3D RSD / 3D NURSD + SRSD": stage 1 of the 3D
+    algorithms to the virtual plane, then srsd onto a depth-widening frustum; against the
+    composed oracle (reference stage 1 + reference srsd)."""
+    xy = rng.uniform(-0.3, 0.3, size=(500, 2))
+    zz = 0.03 * np.sin(2 * np.pi * xy[:, 0] / 0.6) * np.cos(2 * np.pi * xy[:, 1] / 0.9)
+    relay = pf.NonPlanarRelay(pf.PointList(np.column_stack([xy, zz])))
+    F = 3
+    freqs = 2 * np.pi * 299792458.0 / 0.06 * (1.0 + 0.03 * np.arange(F))
+    coeff = rng.normal(size=(1, 500, F)) + 1j * rng.normal(size=(1, 500, F))
+    sl = pf.FrequencySlices(freqs, coeff, relay, pf.PointList(np.array([[0.0, 0.0, 0.0]])))
+    n, p = 24, 0.6 / 24
+    base = pf.UniformGrid2D(n, n, p, p, -0.3 + p / 2, -0.3 + p / 2, 0.0)
+    zs = np.linspace(0.5, 1.1, 4)
+    frustum = pf.FrustumGrid(base, zs, zs[0] / zs, zs[0] / zs)
+    times = np.array([0.0, 2e-10]) if video else None
+    fn = pf.nursd3d_srsd if stage1 == "nursd3d" else pf.rsd3d_srsd
+    vol = fn(sl, frustum, times=times)
+    ref = O.lattice_srsd(sl, frustum, stage1=stage1, times=times)
+    assert O.rel_l2(vol.field, ref) < TOL
