@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -62,6 +63,18 @@ def xfft_L(n: int) -> int:
     return L if L in (4, 5, 8, 10, 15, 20, 30) else 0
 
 
+def xfft_plan_L(n: int) -> int:
+    """Lanes of the register FFT a plan of length n is tagged for (0: Stockham stages).
+    PF_XFFT = "large" (default): only L >= 20 (n = 700, 1050), where it measured faster
+    (config 2's 700-point fine-grid lines); "all": every 35 L length (slower at 140 and 280:
+    the generic propagation kernels drop to one CTA per SM); "0": never."""
+    mode = os.environ.get("PF_XFFT", "large")
+    L = xfft_L(n)
+    if mode == "0" or (mode != "all" and L < 20):
+        return 0
+    return L
+
+
 class FftPlan:
     """Mixed-radix plan for one length on one device (twiddles built in float64)."""
 
@@ -77,7 +90,7 @@ class FftPlan:
             k1 = np.arange(32)[:, None]
             t = np.arange(L)[None, :]
             w = np.concatenate([w, np.exp(-2j * np.pi * ((k1 * t) % self.n) / self.n).ravel()])
-        xl = xfft_L(self.n)
+        xl = xfft_plan_L(self.n)
         if xl:
             # mixed-radix register FFT (n = 35 L): k1-major table [35][L] after the roots
             k1 = np.arange(35)[:, None]

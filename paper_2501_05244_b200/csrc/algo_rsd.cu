@@ -15,6 +15,7 @@
 // (the tables are uploaded from pageable host memory).
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -86,7 +87,11 @@ std::vector<float2> twiddles(long n) {
     const double a = -2.0 * M_PI * (double)m / (double)n;
     w.push_back(make_float2((float)cos(a), (float)sin(a)));
   }
-  const long xl = xfft_L((int)n);
+  // register FFT tables as the Python plans (_device.xfft_plan_L): L >= 20 by default
+  const char* ev = getenv("PF_XFFT");
+  long xl = xfft_L((int)n);
+  if (ev && strcmp(ev, "0") == 0) xl = 0;
+  if (!(ev && strcmp(ev, "all") == 0) && xl < 20) xl = 0;
   if (xl) {   // mixed-radix register FFT: k1-major [35][L]
     for (long k1 = 0; k1 < 35; k1++)
       for (long t = 0; t < xl; t++) {
@@ -255,7 +260,8 @@ extern "C" int pf_rsd(const pf_rsd_args* a, const void* slices, void* vol, void*
     plx.n = L.px;
     plx.nst = radices(L.px, plx.radix);
     plx.tw = w + L.off_twx;
-    if (xfft_L(L.px)) plx.radix[PF_MAX_STAGES - 1] = PF_XFFT_TAG;
+    if (L.n_twx > L.px && !(L.px == 128 || L.px == 256 || L.px == 512 || L.px == 1024))
+      plx.radix[PF_MAX_STAGES - 1] = PF_XFFT_TAG;
     if (L.py != L.px) {
       std::vector<float2> ty = twiddles(L.py);
       PF_CUDA_CHECK(cudaMemcpyAsync(w + L.off_twy, ty.data(), 8 * ty.size(),
@@ -263,7 +269,8 @@ extern "C" int pf_rsd(const pf_rsd_args* a, const void* slices, void* vol, void*
       ply.n = L.py;
       ply.nst = radices(L.py, ply.radix);
       ply.tw = w + L.off_twy;
-      if (xfft_L(L.py)) ply.radix[PF_MAX_STAGES - 1] = PF_XFFT_TAG;
+      if (L.n_twy > L.py && !(L.py == 128 || L.py == 256 || L.py == 512 || L.py == 1024))
+        ply.radix[PF_MAX_STAGES - 1] = PF_XFFT_TAG;
     } else {
       ply = plx;
     }

@@ -298,6 +298,86 @@ __device__ __noinline__ void stockham_stage_any(const float2* __restrict__ src,
   }
 }
 
+// ---- mixed-radix register FFT for n = 35 L (see xfft.cuh for the algorithm notes) ----
+constexpr int XFFT_R = 35;
+
+__host__ __device__ constexpr int xfft_J(int L) { return (XFFT_R + L - 1) / L; }
+
+// supported lane counts; 0 when n is not 35 L with such an L
+__host__ __device__ inline int xfft_L(int n) {
+  if (n % XFFT_R) return 0;
+  const int L = n / XFFT_R;
+  return (L == 4 || L == 5 || L == 8 || L == 10 || L == 15 || L == 20 || L == 30) ? L : 0;
+}
+
+// v: the lane's R inputs; row: the line's exchange row base in shared memory (>= L R
+// elements, the line's own, written and read by this line's lanes only); tw2: the plan's
+// k1-major twiddle table [R][L] (W_n^{k1 t}); t: lane within the line.
+template <int L, int DIR>
+__device__ __forceinline__ void xfft(float2 (&v)[XFFT_R], float2 (&w)[xfft_J(L)][L],
+                                     float2* __restrict__ row, const float2* __restrict__ tw2,
+                                     int t, bool active) {
+  constexpr int R = XFFT_R, J = xfft_J(L);
+  Dft<R, DIR>::run(v);
+  if (t != 0) {
+#pragma unroll
+    for (int k1 = 1; k1 < R; k1++) {
+      const float2 c = __ldg(tw2 + k1 * L + t);
+      v[k1] = DIR < 0 ? cmul(v[k1], c) : cmulc(v[k1], c);
+    }
+  }
+  __syncwarp();
+  if (active) {
+#pragma unroll
+    for (int k1 = 0; k1 < R; k1++) row[t * R + k1] = v[k1];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < J; j++) {
+    const int k1 = t + L * j;
+    if (J * L == R || k1 < R) {
+#pragma unroll
+      for (int tp = 0; tp < L; tp++) w[j][tp] = row[tp * R + k1];
+      Dft<L, DIR>::run(w[j]);
+    }
+  }
+  __syncwarp();
+}
+
+// All `cnt` lines of a shared-memory tile (row stride ld >= n) by the register FFT, in
+// place, natural order in and out; each warp owns 32 / L lines at a time and uses their
+// own rows as the exchange buffer.  Block-wide: every thread calls it; synchronised on
+// return.
+template <int L, int DIR>
+__device__ __forceinline__ void xfft_tile(float2* __restrict__ a, int ld, int cnt,
+                                       const float2* __restrict__ tw2) {
+  constexpr int LPW = 32 / L, J = xfft_J(L);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int t = lane % L, line = lane / L;
+  for (int c0 = warp * LPW; c0 < cnt; c0 += nw * LPW) {
+    const int c = c0 + (line < LPW ? line : 0);
+    const bool active = line < LPW && c < cnt;
+    float2* row = a + (size_t)(c < cnt ? c : c0) * ld;
+    float2 v[XFFT_R];
+#pragma unroll
+    for (int m = 0; m < XFFT_R; m++) v[m] = row[t + L * m];
+    float2 w[J][L];
+    xfft<L, DIR>(v, w, row, tw2, t, active);
+    if (active) {
+#pragma unroll
+      for (int j = 0; j < J; j++) {
+        const int k1 = t + L * j;
+        if (J * L == XFFT_R || k1 < XFFT_R) {
+#pragma unroll
+          for (int k2 = 0; k2 < L; k2++) row[k1 + XFFT_R * k2] = w[j][k2];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
 // Run the full transform on `cnt` length-n lines held in `a` (scratch `b`).
 // Caller must __syncthreads() after filling `a`.  Returns the buffer holding
 // the natural-order result; all threads are synchronised on return.
@@ -327,6 +407,24 @@ __device__ float2* fft_smem(float2* a, float2* b, int ld, int cnt, const pf_fft_
     dst = t;
   }
   return src;
+}
+
+// XL = 0: the Stockham stages (scratch b); XL = L: the 35 L register FFT in place (the
+// plan carries its twiddle table, PF_XFFT_TAG).  Returns the buffer holding the result.
+template <int XL, int DIR>
+__device__ __forceinline__ float2* fft_any(float2* a, float2* b, int ld, int cnt,
+                                           const pf_fft_plan& p) {
+  if constexpr (XL > 0) {
+    xfft_tile<XL, DIR>(a, ld, cnt, reinterpret_cast<const float2*>(p.tw) + p.n);
+    return a;
+  } else {
+    return fft_smem<DIR>(a, b, ld, cnt, p);
+  }
+}
+
+// XL for a plan: the register FFT's lane count when the plan is tagged, else 0
+__host__ __device__ inline int plan_xl(const pf_fft_plan& p) {
+  return p.radix[PF_MAX_STAGES - 1] == PF_XFFT_TAG ? xfft_L(p.n) : 0;
 }
 
 // padded leading dimension for `cnt` lines of length n in shared memory

@@ -138,15 +138,6 @@ int launch_xfft(float2* data, const pf_fft_plan& p, long long nlines, long long 
   }
 }
 
-static bool xfft_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("PF_XFFT");
-    on = (e == nullptr || atoi(e) != 0) ? 1 : 0;
-  }
-  return on == 1;
-}
-
 // transpose=1 writes dst[bb][jx][jy] (the transposed grid, px rows of py)
 __global__ void k_embed_centered(const float2* __restrict__ src, long long nb, int ny, int nx,
                                  long long sbs, float2* __restrict__ dst, int py, int px,
@@ -205,7 +196,8 @@ extern "C" int pf_fft_lines(void* data, const pf_fft_plan* plan, int64_t nlines,
   if (nlines == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   // 35 L lengths: the register mixed-radix kernel (the plan carries its twiddle table)
-  if (xfft_L(plan->n) && plan->radix[PF_MAX_STAGES - 1] == PF_XFFT_TAG && xfft_enabled()) {
+  // (the plan builder decides: it tags a plan only where the register FFT is wanted)
+  if (plan_xl(*plan)) {
     return dir < 0 ? launch_xfft<-1>((float2*)data, *plan, nlines, inner, inner_stride,
                                      outer_stride, elem_stride, scale, st)
                    : launch_xfft<1>((float2*)data, *plan, nlines, inner, inner_stride,

@@ -36,6 +36,7 @@ __device__ __forceinline__ float2 rsd_kernel(double khat, double lx, double ly, 
 
 // (A) kernel rows jy in [0, py/2] -> x-FFT -> keep kx in [0, px/2]
 // Frequency batch (khat_f != nullptr): blockIdx.z is the frequency, ws_a per-f stride ws_a_fs.
+template <int XL>
 __global__ void __launch_bounds__(PT)
 k_prop_kernel_rows(const pf_plane* __restrict__ planes, double khat, pf_prop_geom g,
                    pf_fft_plan plan_x, float2* __restrict__ ws_a, int rows_per_cta,
@@ -61,7 +62,7 @@ k_prop_kernel_rows(const pf_plane* __restrict__ planes, double khat, pf_prop_geo
     a[c * ld + jx] = rsd_kernel(khat, lx, ly, pl.dz);
   }
   __syncthreads();
-  const float2* res = fft_smem<-1>(a, b, ld, nr, plan_x);
+  const float2* res = fft_any<XL, -1>(a, b, ld, nr, plan_x);
   float2* dst = ws_a + ((long long)blockIdx.y * rows_a + r0) * cols_a;
   for (int e = threadIdx.x; e < nr * cols_a; e += PT) {
     const int c = dca.div(e), kx = e - c * cols_a;
@@ -71,6 +72,7 @@ k_prop_kernel_rows(const pf_plane* __restrict__ planes, double khat, pf_prop_geo
 
 // (B) per column kx in [0, px/2]: mirror -> y-FFT (Ghat column) -> for each
 // illumination and for columns kx and px-kx: * Uhat column -> y-IFFT -> crop rows
+template <int XL>
 __global__ void __launch_bounds__(PT)
 k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan plan_y,
                const float2* __restrict__ ws_a, const float2* __restrict__ uhat,
@@ -98,7 +100,7 @@ k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan 
     buf0[c * ld + jy] = src[(long long)sy * cols_a + c];
   }
   __syncthreads();
-  float2* gh = fft_smem<-1>(buf0, buf1, ld, nc, plan_y);
+  float2* gh = fft_any<XL, -1>(buf0, buf1, ld, nc, plan_y);
   float2* w0 = (gh == buf0) ? buf1 : buf0;
   float2* w1 = buf2;
   const float2* up = uhat + pl.uhat_off;
@@ -126,7 +128,7 @@ k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan 
         __syncthreads();
         continue;
       }
-      const float2* res = fft_smem<1>(w0, w1, ld, nc, plan_y);
+      const float2* res = fft_any<XL, 1>(w0, w1, ld, nc, plan_y);
       for (int e = threadIdx.x; e < nc * ny; e += PT) {
         const int i = dnc.div(e), c = e - i * nc;
         const int kx = k0 + c;
@@ -141,6 +143,7 @@ k_prop_columns(const pf_plane* __restrict__ planes, pf_prop_geom g, pf_fft_plan 
 }
 
 // (C) per output row: x-IFFT -> crop columns -> scale -> illumination phase -> accumulate
+template <int XL>
 __global__ void __launch_bounds__(PT)
 k_prop_rows_out(const pf_plane* __restrict__ planes, double khat, pf_prop_geom g,
                 pf_fft_plan plan_x, const float2* __restrict__ ws_b,
@@ -163,7 +166,7 @@ k_prop_rows_out(const pf_plane* __restrict__ planes, double khat, pf_prop_geom g
       a[c * ld + jx] = src[(long long)c * px + jx];
     }
     __syncthreads();
-    const float2* res = fft_smem<1>(a, b, ld, nr, plan_x);
+    const float2* res = fft_any<XL, 1>(a, b, ld, nr, plan_x);
     const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
     for (int e = threadIdx.x; e < nr * nx; e += PT) {
       const int c = dnx.div(e), m = e - c * nx;
@@ -187,6 +190,7 @@ k_prop_rows_out(const pf_plane* __restrict__ planes, double khat, pf_prop_geom g
 // (C) over all nf frequencies of a batch: per (row tile, plane) the ascending-
 // frequency sum is formed in shared memory (acc, fp32, same operation order as
 // the per-frequency launches) and added to the volume once.  Single frame.
+template <int XL>
 __global__ void __launch_bounds__(PT)
 k_prop_rows_out_fb(const pf_plane* __restrict__ planes, const double* __restrict__ khat_f, int nf,
                    pf_prop_geom g, pf_fft_plan plan_x, const float2* __restrict__ ws_b,
@@ -216,7 +220,7 @@ k_prop_rows_out_fb(const pf_plane* __restrict__ planes, const double* __restrict
         a[c * ld + jx] = src[(long long)c * px + jx];
       }
       __syncthreads();
-      const float2* res = fft_smem<1>(a, b, ld, nr, plan_x);
+      const float2* res = fft_any<XL, 1>(a, b, ld, nr, plan_x);
       const double sx = ill[3 * p], sy = ill[3 * p + 1], sz = ill[3 * p + 2];
       for (int e = threadIdx.x; e < nr * nx; e += PT) {
         const int c = dnx.div(e), m = e - c * nx;
@@ -250,6 +254,40 @@ int rows_fit(int n, int bufs, int want) {
   return r < want ? r : want;
 }
 
+// lines per CTA for a stage: the Stockham path wants enough lines to keep every thread of
+// every stage busy; the register FFT (xl > 0) wants 32 / xl lines per warp of the CTA (the
+// kernels keep their buffer layout, so the shared-memory budget is the same)
+int lines_for(int n, int bufs, int want_stockham, int xl) {
+  if (xl > 0) return rows_fit(n, bufs, (PT / 32) * (32 / xl));
+  return rows_fit(n, bufs, want_stockham);
+}
+
+// instantiate kernel K<XL> for the plan's register-FFT lane count
+#define PF_XL_DISPATCH(xl, CALL)                                                            \
+  switch (xl) {                                                                             \
+    case 4: { constexpr int XL = 4; CALL; } break;                                          \
+    case 5: { constexpr int XL = 5; CALL; } break;                                          \
+    case 8: { constexpr int XL = 8; CALL; } break;                                          \
+    case 10: { constexpr int XL = 10; CALL; } break;                                        \
+    case 15: { constexpr int XL = 15; CALL; } break;                                        \
+    case 20: { constexpr int XL = 20; CALL; } break;                                        \
+    case 30: { constexpr int XL = 30; CALL; } break;                                        \
+    default: { constexpr int XL = 0; CALL; } break;                                         \
+  }
+
+template <int XL>
+void allow_generic() {
+  allow_smem(k_prop_kernel_rows<XL>);
+  allow_smem(k_prop_columns<XL>);
+  allow_smem(k_prop_rows_out_fb<XL>);
+  allow_smem(k_prop_rows_out<XL>);
+}
+
+void allow_all_generic() {
+  allow_generic<0>(); allow_generic<4>(); allow_generic<5>(); allow_generic<8>();
+  allow_generic<10>(); allow_generic<15>(); allow_generic<20>(); allow_generic<30>();
+}
+
 }  // namespace
 
 int pf_prop_fast_L(const pf_prop_geom* g);
@@ -275,31 +313,28 @@ static int prop_fbatch_generic(const pf_plane* planes, int nplanes, const double
                                const void* uhat, int64_t uhat_fs, void* ws_b, int64_t ws_b_fs,
                                const double* ill, const void* frame_w, void* vol,
                                cudaStream_t st) {
-  static PfDevOnce attr;  
-  if (attr.first()) {
-    allow_smem(k_prop_kernel_rows);
-    allow_smem(k_prop_columns);
-    allow_smem(k_prop_rows_out_fb);
-  }
+  static PfDevOnce attr;
+  if (attr.first()) allow_all_generic();
   const int rows_a = g->py / 2 + 1, cols_a = g->px / 2 + 1;
-  // many lines per CTA: every Stockham stage then has work for all threads
-  const int rpc = rows_fit(g->px, 2, (8 * PT + g->px - 1) / g->px);
-  const int cpc = rows_fit(g->py, 3, 16);
-  const int rpo = rows_fit(g->px, 3, 8);
+  const int xlx = plan_xl(*plan_x), xly = plan_xl(*plan_y);
+  // many lines per CTA: every Stockham stage (or every warp of the register FFT) has work
+  const int rpc = lines_for(g->px, 2, (8 * PT + g->px - 1) / g->px, xlx);
+  const int cpc = lines_for(g->py, 3, 16, xly);
+  const int rpo = xlx ? rows_fit(g->px, 3, (PT / 32) * (32 / xlx)) : rows_fit(g->px, 3, 8);
   if (rpc < 1 || cpc < 1 || rpo < 1) { pf_set_error("pf_prop_fbatch: pad too large"); return -1; }
-  k_prop_kernel_rows<<<dim3(pf_cdiv(rows_a, rpc), nplanes, nf), PT,
+  PF_XL_DISPATCH(xlx, (k_prop_kernel_rows<XL><<<dim3(pf_cdiv(rows_a, rpc), nplanes, nf), PT,
                        (size_t)2 * rpc * pf_ld(g->px) * sizeof(float2), st>>>(
-      planes, 0.0, *g, *plan_x, (float2*)ws_a, rpc, khat_f, ws_a_fs);
+      planes, 0.0, *g, *plan_x, (float2*)ws_a, rpc, khat_f, ws_a_fs)))
   PF_LAUNCH_CHECK("k_prop_kernel_rows");
-  k_prop_columns<<<dim3(pf_cdiv(cols_a, cpc), nplanes, nf), PT,
+  PF_XL_DISPATCH(xly, (k_prop_columns<XL><<<dim3(pf_cdiv(cols_a, cpc), nplanes, nf), PT,
                    (size_t)3 * cpc * pf_ld(g->py) * sizeof(float2), st>>>(
       planes, *g, *plan_y, (const float2*)ws_a, (const float2*)uhat, (float2*)ws_b, cpc, 0,
-      ws_a_fs, uhat_fs, ws_b_fs);
+      ws_a_fs, uhat_fs, ws_b_fs)))
   PF_LAUNCH_CHECK("k_prop_columns");
   const size_t smo = ((size_t)2 * rpo * pf_ld(g->px) + (size_t)rpo * g->nx) * sizeof(float2);
-  k_prop_rows_out_fb<<<dim3(pf_cdiv(g->ny, rpo), nplanes), PT, smo, st>>>(
+  PF_XL_DISPATCH(xlx, (k_prop_rows_out_fb<XL><<<dim3(pf_cdiv(g->ny, rpo), nplanes), PT, smo, st>>>(
       planes, khat_f, nf, *g, *plan_x, (const float2*)ws_b, ws_b_fs, ill, (const float2*)frame_w,
-      (float2*)vol, rpo);
+      (float2*)vol, rpo)))
   PF_LAUNCH_CHECK("k_prop_rows_out_fb");
   return 0;
 }
@@ -352,15 +387,16 @@ extern "C" int pf_prop_kernel_rows(const pf_plane* planes, int nplanes, double k
   if (pf_prop_fast_L(g))
     return pf_prop_fast_stage(0, planes, nplanes, khat, g, plan_x, nullptr, ws_a, nullptr, nullptr,
                               nullptr, nullptr, nullptr, 0, nullptr, 0, (cudaStream_t)stream);
-  static PfDevOnce attr;  
-  if (attr.first()) { allow_smem(k_prop_kernel_rows); }
+  static PfDevOnce attr;
+  if (attr.first()) allow_all_generic();
   const int rows_a = g->py / 2 + 1;
-  int rpc = rows_fit(g->px, 2, (2 * PT + g->px - 1) / g->px);
+  const int xl = plan_xl(*plan_x);
+  int rpc = lines_for(g->px, 2, (2 * PT + g->px - 1) / g->px, xl);
   if (rpc < 1) { pf_set_error("pf_prop_kernel_rows: px too large"); return -1; }
   dim3 grid(pf_cdiv(rows_a, rpc), nplanes);
   const size_t smem = (size_t)2 * rpc * pf_ld(g->px) * sizeof(float2);
-  k_prop_kernel_rows<<<grid, PT, smem, (cudaStream_t)stream>>>(planes, khat, *g, *plan_x,
-                                                               (float2*)ws_a, rpc);
+  PF_XL_DISPATCH(xl, (k_prop_kernel_rows<XL><<<grid, PT, smem, (cudaStream_t)stream>>>(
+      planes, khat, *g, *plan_x, (float2*)ws_a, rpc)))
   PF_LAUNCH_CHECK("k_prop_kernel_rows");
   return 0;
 }
@@ -374,16 +410,17 @@ extern "C" int pf_prop_columns(const pf_plane* planes, int nplanes, const pf_pro
   if (pf_prop_fast_L(g))
     return pf_prop_fast_stage(1, planes, nplanes, 0.0, g, plan_y, ws_a, nullptr, uhat, nullptr,
                               ws_b, nullptr, nullptr, 0, nullptr, 0, (cudaStream_t)stream);
-  static PfDevOnce attr;  
-  if (attr.first()) { allow_smem(k_prop_columns); }
+  static PfDevOnce attr;
+  if (attr.first()) allow_all_generic();
   const int cols_a = g->px / 2 + 1;
-  int cpc = rows_fit(g->py, 3, 8);
+  const int xl = plan_xl(*plan_y);
+  int cpc = lines_for(g->py, 3, 8, xl);
   if (cpc < 1) { pf_set_error("pf_prop_columns: py too large"); return -1; }
   dim3 grid(pf_cdiv(cols_a, cpc), nplanes);
   const size_t smem = (size_t)3 * cpc * pf_ld(g->py) * sizeof(float2);
-  k_prop_columns<<<grid, PT, smem, (cudaStream_t)stream>>>(
+  PF_XL_DISPATCH(xl, (k_prop_columns<XL><<<grid, PT, smem, (cudaStream_t)stream>>>(
       planes, *g, *plan_y, (const float2*)ws_a, (const float2*)uhat, (float2*)ws_b, cpc,
-      product_only);
+      product_only)))
   PF_LAUNCH_CHECK("k_prop_columns");
   return 0;
 }
@@ -398,15 +435,16 @@ extern "C" int pf_prop_rows_out(const pf_plane* planes, int nplanes, double khat
     return pf_prop_fast_stage(2, planes, nplanes, khat, g, plan_x, nullptr, nullptr, nullptr, ws_b,
                               nullptr, ill_xyz, frame_w, n_frames, vol, vol_frame_stride,
                               (cudaStream_t)stream);
-  static PfDevOnce attr;  
-  if (attr.first()) { allow_smem(k_prop_rows_out); }
-  int rpc = rows_fit(g->px, 2, (2 * PT + g->px - 1) / g->px);
+  static PfDevOnce attr;
+  if (attr.first()) allow_all_generic();
+  const int xl = plan_xl(*plan_x);
+  int rpc = lines_for(g->px, 2, (2 * PT + g->px - 1) / g->px, xl);
   if (rpc < 1) { pf_set_error("pf_prop_rows_out: px too large"); return -1; }
   dim3 grid(pf_cdiv(g->ny, rpc), nplanes);
   const size_t smem = (size_t)2 * rpc * pf_ld(g->px) * sizeof(float2);
-  k_prop_rows_out<<<grid, PT, smem, (cudaStream_t)stream>>>(
+  PF_XL_DISPATCH(xl, (k_prop_rows_out<XL><<<grid, PT, smem, (cudaStream_t)stream>>>(
       planes, khat, *g, *plan_x, (const float2*)ws_b, ill_xyz, (const float2*)frame_w, n_frames,
-      (float2*)vol, vol_frame_stride, rpc);
+      (float2*)vol, vol_frame_stride, rpc)))
   PF_LAUNCH_CHECK("k_prop_rows_out");
   return 0;
 }
