@@ -139,6 +139,99 @@ k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __
   }
 }
 
+// Same transform with the traces of a CTA decoupled: the M threads of a trace (M >= 32)
+// synchronise among themselves only (a named barrier per trace, or the warp for M = 32)
+// and form their own trace's bins in phase B, so one trace's loads overlap another's
+// arithmetic instead of every trace of the CTA moving in lock step through
+// load -> transform -> park -> sum.
+__device__ __forceinline__ void trace_sync(int id, int nthreads) {
+  if (nthreads == 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(K1_THREADS)
+k_temporal_dft_pair(const float* __restrict__ hist, long long n_traces,
+                    const int* __restrict__ bins, const float2* __restrict__ twt, int twt_ld,
+                    const float2* __restrict__ wphase, int F, float2* __restrict__ out,
+                    long long out_stride, int ts_cap, unsigned long long inner_mask) {
+  static_assert(M >= 32, "one or more whole warps per trace");
+  constexpr int G = K1_THREADS / M;
+  constexpr int T = M * K1_L;
+  constexpr int MP = M + 2 - (M & 1);
+  extern __shared__ float2 smem[];
+  float2* tws = smem;
+  int* ks = reinterpret_cast<int*>(tws + F * MP);
+  float2* xs = reinterpret_cast<float2*>(ks + ((F + 1) & ~1));
+  unsigned long long mask = inner_mask;
+  if (mask == 0) {
+    for (int f = 0; f < F; f++) {
+      const int k = __ldg(bins + f) & 63;
+      mask |= 1ull << (k > 32 ? 64 - k : k);
+    }
+  }
+  const int nk = __popcll(mask);
+  const int ts = nk * MP + (((4 - nk * MP) % 16) + 16) % 16;
+  if (ts > ts_cap) return;
+  for (int f = threadIdx.x; f < F; f += K1_THREADS) {
+    const int k = bins[f] & 63;
+    const int kk = k > 32 ? 64 - k : k;
+    ks[f] = __popcll(mask & ((1ull << kk) - 1ull)) | ((k > 32) << 8);
+  }
+  for (int e = threadIdx.x; e < M * F; e += K1_THREADS) {
+    const int rr = e / F, f = e - rr * F;
+    float2 w = twt[rr * twt_ld + f];
+    if ((bins[f] & 63) > 32) w.y = -w.y;
+    tws[f * MP + rr] = w;
+  }
+  __syncthreads();
+  const int g = threadIdx.x / M;
+  const int r = threadIdx.x - g * M;
+  float2* xg = xs + g * ts;
+  // trace g of CTA b takes traces g*nb + b, g*nb + b + stride, ... (independent streams)
+  for (long long trace = (long long)blockIdx.x * G + g; trace < n_traces;
+       trace += (long long)gridDim.x * G) {
+    const float* h = hist + trace * (long long)T + r;
+    float x[64];
+#pragma unroll
+    for (int q = 0; q < 64; q++) x[q] = __ldg(h + q * M);
+    real_dft64_sel(x, mask, xg + r, MP);
+    trace_sync(1 + g, M);
+    for (int q0 = 0; q0 < 2 * F; q0 += M) {
+      const int q = q0 + r;
+      const bool valid = q < 2 * F;
+      const int hh = q & 1, f = valid ? q >> 1 : 0;
+      const int kv = ks[f];
+      float2 acc = make_float2(0.f, 0.f);
+      if (valid) {
+        const float2* src = xg + (kv & 255) * MP + hh;
+        const float2* tw = tws + f * MP + hh;
+#pragma unroll 16
+        for (int j = 0; j < M / 2; j++) cacc(acc, src[2 * j], tw[2 * j]);
+      }
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+      if (valid && hh == 0) {
+        if (kv >> 8) acc.y = -acc.y;
+        out[(long long)f * out_stride + trace] = cmul(acc, wphase[f]);
+      }
+    }
+    trace_sync(1 + g, M);
+  }
+}
+
+static int k1_pair_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PF_K1_PAIR");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 // Any T: one thread per (trace, bin), trace staged in shared memory.
 __global__ void __launch_bounds__(K1_THREADS)
 k_temporal_dft_direct(const float* __restrict__ hist, long long n_traces, int T,
@@ -321,13 +414,28 @@ int launch_k1(const float* hist, long long n_traces, const int* bins, const floa
   if (per < 1) per = 1;
   const long long cap = (long long)nsm * per;
   const int grid_k1 = (int)(groups < cap ? groups : cap);
+  constexpr int MPAIR = M >= 32 ? M : 32;
+  const bool pair = M >= 32 && k1_pair_mode() != 0;
+  if (pair) {
+    static PfDevOnce attr2;
+    if (attr2.first())
+      cudaFuncSetAttribute(k_temporal_dft_pair<MPAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           227 * 1024);
+  }
   for (int f0 = 0; f0 < F_total; f0 += FC) {
     const int F = F_total - f0 < FC ? F_total - f0 : FC;
-    k_temporal_dft<M><<<grid_k1, K1_THREADS, smem, st>>>(hist, n_traces, bins + f0, twt + f0,
-                                                       F_total, wphase + f0, F,
-                                                       out + (long long)f0 * out_stride,
-                                                       out_stride, ts_cap, inner_mask);
-    PF_LAUNCH_CHECK("k_temporal_dft");
+    if (pair) {
+      k_temporal_dft_pair<MPAIR><<<grid_k1, K1_THREADS, smem, st>>>(
+          hist, n_traces, bins + f0, twt + f0, F_total, wphase + f0, F,
+          out + (long long)f0 * out_stride, out_stride, ts_cap, inner_mask);
+      PF_LAUNCH_CHECK("k_temporal_dft_pair");
+    } else {
+      k_temporal_dft<M><<<grid_k1, K1_THREADS, smem, st>>>(hist, n_traces, bins + f0, twt + f0,
+                                                         F_total, wphase + f0, F,
+                                                         out + (long long)f0 * out_stride,
+                                                         out_stride, ts_cap, inner_mask);
+      PF_LAUNCH_CHECK("k_temporal_dft");
+    }
   }
   return 0;
 }
