@@ -13,6 +13,8 @@
 // its own cell in fixed point order (no atomics, bit-reproducible).  It then
 // writes every cell of its tile exactly once, so no zero-fill pass is needed.
 // Type 2 (spectral.py:374-380) interpolates with one thread per target point.
+#include <stdlib.h>
+
 #include "fft.cuh"
 
 // pf_nufft_geom: see include/pfgpu.h
@@ -310,6 +312,89 @@ k_interp2_batch(pf_nufft_geom G, const int* __restrict__ i0, const float* __rest
   }
 }
 
+// The batched readout with a half-warp per point (W = 2w + 1 <= 32): lane c of a half
+// serves stencil columns c and c + 16 (when c + 16 < W), so a warp interpolates two
+// points where the warp-per-point kernel left 32 - W lanes idle; per-point arithmetic
+// and summation order per column pair as k_interp2_batch (the column partial sums of a
+// row are combined in a different order, fp32 rounding only).
+__global__ void __launch_bounds__(256)
+k_interp2_batch_h(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
+                  const double* __restrict__ xyz, const int* __restrict__ plane_idx,
+                  const long long* __restrict__ dst_idx, int npts, int plane0,
+                  const float2* __restrict__ fine, long long fine_plane_stride,
+                  long long fine_stride, int n_illum, const double* __restrict__ ill,
+                  double kturns, int include_illum, float scale,
+                  const float2* __restrict__ frame_w, int n_frames, float2* __restrict__ vol,
+                  long long vol_frame_stride) {
+  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+  const int l = blockIdx.x * (blockDim.x >> 4) + ((threadIdx.x >> 5) << 1) + half;
+  const bool live = l < npts;
+  const int lc = live ? l : 0;
+  const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+  const int W = 2 * G.w + 1;
+  const int mry = G.mr[1], mrx = G.mr[2];
+  const bool on1 = hl < W, on2 = hl + 16 < W;
+  const float dyl = d0[3 * lc + 1], dxl = d0[3 * lc + 2];
+  const float dx1 = dxl + (float)(hl - G.w) * G.h[2];
+  const float dx2 = dxl + (float)(hl + 16 - G.w) * G.h[2];
+  const float wx1 = on1 ? __expf(-dx1 * dx1 * G.inv4tau[2]) : 0.f;
+  const float wx2 = on2 ? __expf(-dx2 * dx2 * G.inv4tau[2]) : 0.f;
+  // row weights: lane c forms rows c and c + 16; the row loop broadcasts them
+  const float dy1 = dyl + (float)(hl - G.w) * G.h[1];
+  const float dy2 = dyl + (float)(hl + 16 - G.w) * G.h[1];
+  const float wy1 = on1 ? __expf(-dy1 * dy1 * G.inv4tau[1]) : 0.f;
+  const float wy2 = on2 ? __expf(-dy2 * dy2 * G.inv4tau[1]) : 0.f;
+  const int cxb = natural((long long)i0[3 * lc + 2] - G.w, mrx);
+  const int cx1 = wrap_once(cxb + (on1 ? hl : 0), mrx);
+  const int cx2 = wrap_once(cxb + (on2 ? hl + 16 : 0), mrx);
+  const int cy0 = natural((long long)i0[3 * lc + 1] - G.w, mry);
+  const float2* fplane = fine + (long long)(plane_idx[lc] - plane0) * fine_plane_stride;
+  float2 tot = make_float2(0.f, 0.f);
+  for (int p = 0; p < n_illum; p++) {
+    const float2* fp = fplane + (long long)p * fine_stride;
+    float2 acc = make_float2(0.f, 0.f);
+    int cy = cy0;
+    for (int oy = 0; oy < W; oy++) {
+      const int src = (half << 4) + (oy & 15);
+      const float wa = __shfl_sync(0xffffffffu, wy1, src);
+      const float wb = __shfl_sync(0xffffffffu, wy2, src);
+      const float wy = oy < 16 ? wa : wb;
+      const float2* rowp = fp + (long long)cy * mrx;
+      const float2 f1 = __ldg(rowp + cx1);
+      const float w1 = wx1 * wy;
+      acc.x = fmaf(w1, f1.x, acc.x);
+      acc.y = fmaf(w1, f1.y, acc.y);
+      if (on2) {
+        const float2 f2 = __ldg(rowp + cx2);
+        const float w2 = wx2 * wy;
+        acc.x = fmaf(w2, f2.x, acc.x);
+        acc.y = fmaf(w2, f2.y, acc.y);
+      }
+      if (++cy == mry) cy = 0;
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    float2 val = cscale(acc, scale);
+    if (include_illum && hl == 0) {
+      const double ex = xyz[3 * lc] - ill[3 * p], ey = xyz[3 * lc + 1] - ill[3 * p + 1];
+      const double ez = xyz[3 * lc + 2] - ill[3 * p + 2];
+      val = cmul(val, expi_reduced(PF_TWO_PI * kturns * sqrt(ex * ex + ey * ey + ez * ez)));
+    }
+    tot = cadd(tot, val);
+  }
+  (void)hmask;
+  if (hl == 0 && live) {
+    const long long dst = dst_idx[l];
+    for (int f = 0; f < n_frames; f++) {
+      float2* d = vol + f * vol_frame_stride + dst;
+      *d = cadd(*d, cmul(tot, frame_w[f]));
+    }
+  }
+}
+
 // w = 16 (W = 33 > 32 lanes): one thread per point.
 __global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
                               const float* __restrict__ d0, const double* __restrict__ xyz,
@@ -507,6 +592,19 @@ extern "C" int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0,
   PF_ARG_CHECK(g && g->dim == 2 && 2 * g->w + 1 <= 32 && npts >= 0,
                "pf_nufft_interp2_batch: bad args (2D, stencil width <= 32)");
   if (npts == 0) return 0;
+  static int half = -1;
+  if (half < 0) {
+    const char* e = getenv("PF_INTERP_HALF");
+    half = (e == nullptr || atoi(e) != 0) ? 1 : 0;
+  }
+  if (half) {   // two points per warp (half a warp each)
+    k_interp2_batch_h<<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
+        *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine,
+        fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,
+        (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride);
+    PF_LAUNCH_CHECK("k_interp2_batch_h");
+    return 0;
+  }
   k_interp2_batch<<<pf_cdiv(npts, 8), 256, 0, (cudaStream_t)stream>>>(
       *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine,
       fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,
