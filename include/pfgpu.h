@@ -360,6 +360,30 @@ int64_t pf_rsd_workspace_bytes(const pf_rsd_args* args);
 int pf_rsd(const pf_rsd_args* args, const void* slices, void* vol, void* ws, int64_t ws_bytes,
            void* stream);
 
+/* srsd (reference reconstruct.py:276-327, srsd(slices, grid, times, threads,
+ * include_illumination)) in one call.  The frustum's base is the relay lattice (the
+ * reference requires them to coincide, :291-294); zs / alphas / betas (host, [nz]) are
+ * FrustumGrid.zs / alphas / betas.  Same conventions as pf_rsd otherwise; the output
+ * planes keep nx x ny samples at pitch dx / alpha_k about the base centre. */
+typedef struct pf_srsd_args {
+  int nx, ny;
+  double relay_dx, relay_dy, relay_x0, relay_y0, relay_z;
+  int nz;
+  const double* zs;
+  const double* alphas;
+  const double* betas;
+  int n_freq, n_illum;
+  const double* frequencies;
+  const double* ill_xyz;
+  int n_frames;
+  const double* times;
+  int include_illum;
+} pf_srsd_args;
+
+int64_t pf_srsd_workspace_bytes(const pf_srsd_args* args);
+int pf_srsd(const pf_srsd_args* args, const void* slices, void* vol, void* ws, int64_t ws_bytes,
+            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,18 @@ class PfRsdArgs(ctypes.Structure):
                 ("padding_none", ctypes.c_int), ("include_illum", ctypes.c_int)]
 
 
+class PfSrsdArgs(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int),
+                ("relay_dx", ctypes.c_double), ("relay_dy", ctypes.c_double),
+                ("relay_x0", ctypes.c_double), ("relay_y0", ctypes.c_double),
+                ("relay_z", ctypes.c_double), ("nz", ctypes.c_int),
+                ("zs", ctypes.c_void_p), ("alphas", ctypes.c_void_p), ("betas", ctypes.c_void_p),
+                ("n_freq", ctypes.c_int), ("n_illum", ctypes.c_int),
+                ("frequencies", ctypes.c_void_p), ("ill_xyz", ctypes.c_void_p),
+                ("n_frames", ctypes.c_int), ("times", ctypes.c_void_p),
+                ("include_illum", ctypes.c_int)]
+
+
 _vp, _i, _i64, _d, _f = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_float
 _P = ctypes.POINTER
 
@@ -73,6 +85,8 @@ _SIGNATURES = {
     "pf_rsd_workspace_bytes": [_P(PfRsdArgs)],
     "pf_crop_centered": [_vp, _i64, _i, _i, _vp, _i, _i, _vp],
     "pf_rsd": [_P(PfRsdArgs), _vp, _vp, _vp, _i64, _vp],
+    "pf_srsd_workspace_bytes": [_P(PfSrsdArgs)],
+    "pf_srsd": [_P(PfSrsdArgs), _vp, _vp, _vp, _i64, _vp],
     "pf_nufft_type1_finish_pow2": [_P(PfNufftGeom), _vp, _i64, _i, _vp, _P(PfFftPlan),
                                    _P(PfFftPlan), _vp, _vp, _vp, _i64, _vp],
     "pf_relay_spectra_fast": [_vp, _i64, _i, _i, _i64, _vp, _i, _P(PfFftPlan), _vp],
@@ -112,6 +126,7 @@ _SIGNATURES = {
 }
 _RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
              "pf_prop_ws_spectrum": ctypes.c_int64, "pf_rsd_workspace_bytes": ctypes.c_int64,
+             "pf_srsd_workspace_bytes": ctypes.c_int64,
              "pf_prop_fast": ctypes.c_int}
 
 _lib = None

@@ -20,95 +20,11 @@
 
 #include <vector>
 
-#include "xfft.cuh"
+#include "algo_host.cuh"
 
 namespace {
 
-constexpr double C_LIGHT = 299792458.0;
-constexpr int LANES = 3;
-constexpr int HORNER_BLOCK = 32;
-constexpr int64_t BATCH_BYTES = 64LL << 20;
-
-bool close_rel(double a, double b) {
-  return fabs(a - b) <= fmax(1e-9 * fmax(fabs(a), fabs(b)), 1e-12);
-}
-
-bool smooth11(long n) {
-  if (n < 1) return false;
-  const int ps[5] = {2, 3, 5, 7, 11};
-  for (int p : ps)
-    while (n % p == 0) n /= p;
-  return n == 1;
-}
-
-long next_fast_len(long n) {
-  if (n < 1) n = 1;
-  while (!smooth11(n)) n++;
-  return n;
-}
-
-long exact_pad(double lag_max, double nu_max, long n_min) {
-  long need = 2 * (long)ceil(fmax(lag_max, nu_max)) + 2;
-  if (need < n_min) need = n_min;
-  long p2 = 1;
-  while (p2 < need) p2 *= 2;
-  if (64 < need && p2 <= 1024 && p2 * 5 <= need * 8) return p2;
-  return next_fast_len(need);
-}
-
-// stage radices: powers of two merged into as few even stages as possible, then odd primes
-// in descending order (_device.radices_for)
-int radices(long n, int* out) {
-  std::vector<int> f;
-  long m = n;
-  for (int p : {2, 3, 5, 7, 11})
-    while (m % p == 0) {
-      f.push_back(p);
-      m /= p;
-    }
-  if (m != 1) return -1;
-  int k = 0;
-  std::vector<int> odd;
-  for (int p : f) (p == 2 ? k++ : (odd.push_back(p), 0));
-  int ns = 0;
-  if (k) {
-    const int s = (k + 3) / 4;
-    for (int i = 0; i < s; i++) out[ns++] = 1 << (k / s + (i < k % s ? 1 : 0));
-  }
-  for (int i = (int)odd.size() - 1; i >= 0; i--) out[ns++] = odd[i];   // descending
-  return ns;
-}
-
-// unit roots exp(-2 pi i m / n) in fp64, rounded to c64; the register-FFT lengths append
-// the k1-major twiddles [k1][t] = exp(-2 pi i ((k1 t) mod n) / n), n = 32 L
-std::vector<float2> twiddles(long n) {
-  std::vector<float2> w;
-  for (long m = 0; m < n; m++) {
-    const double a = -2.0 * M_PI * (double)m / (double)n;
-    w.push_back(make_float2((float)cos(a), (float)sin(a)));
-  }
-  // register FFT tables as the Python plans (_device.xfft_plan_L): L >= 20 by default
-  const char* ev = getenv("PF_XFFT");
-  long xl = xfft_L((int)n);
-  if (ev && strcmp(ev, "0") == 0) xl = 0;
-  if (!(ev && strcmp(ev, "all") == 0) && xl < 20) xl = 0;
-  if (xl) {   // mixed-radix register FFT: k1-major [35][L]
-    for (long k1 = 0; k1 < 35; k1++)
-      for (long t = 0; t < xl; t++) {
-        const double a = -2.0 * M_PI * (double)((k1 * t) % n) / (double)n;
-        w.push_back(make_float2((float)cos(a), (float)sin(a)));
-      }
-  }
-  if (n == 128 || n == 256 || n == 512 || n == 1024) {
-    const long L = n / 32;
-    for (long k1 = 0; k1 < 32; k1++)
-      for (long t = 0; t < L; t++) {
-        const double a = -2.0 * M_PI * (double)((k1 * t) % n) / (double)n;
-        w.push_back(make_float2((float)cos(a), (float)sin(a)));
-      }
-  }
-  return w;
-}
+using namespace pfalgo;
 
 struct Layout {
   int px, py, nu0x, nu0y, batch, lanes;
@@ -118,7 +34,6 @@ struct Layout {
   int64_t n_twx, n_twy;
 };
 
-int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
 // validation + plan; returns 0 or -1 with pf_set_error
 int plan(const pf_rsd_args* a, Layout* L) {

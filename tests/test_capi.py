@@ -1,4 +1,4 @@
-"""The whole-algorithm C entry point pf_rsd (include/pfgpu.h), called the way a reference-side
+"""The whole-algorithm C entry points pf_rsd and pf_srsd (include/pfgpu.h), called the way a reference-side
 ctypes binding would call it: host geometry and frequency arrays, device
 slices / volume / workspace pointers, the caller's stream.  CPU tests cover the planning
 and the reference's validation messages (no device needed); GPU tests compare the result
@@ -121,3 +121,83 @@ def test_pf_rsd_video_and_no_padding(rng):
     assert O.rel_l2(got, O.rsd(sl, grid, times=times)) < TOL
     got = capi_rsd(sl, grid, padding="none", include_illumination=False)[0]
     assert O.rel_l2(got, O.rsd(sl, grid, padding="none", include_illumination=False)) < TOL
+
+
+# ---------------------------------------------------------------- pf_srsd
+
+def srsd_args(slices, frustum, times=None, include_illumination=True):
+    g = slices.relay.grid
+    zs = np.ascontiguousarray(frustum.zs, dtype=np.float64)
+    al = np.ascontiguousarray(frustum.alphas, dtype=np.float64)
+    be = np.ascontiguousarray(frustum.betas, dtype=np.float64)
+    freqs = np.ascontiguousarray(slices.frequencies, dtype=np.float64)
+    ill = np.ascontiguousarray(illumination_coordinates(slices.relay, slices.illuminations),
+                               dtype=np.float64)
+    t = None if times is None else np.ascontiguousarray(times, dtype=np.float64)
+    a = _lib.PfSrsdArgs(nx=g.nx, ny=g.ny, relay_dx=g.dx, relay_dy=g.dy, relay_x0=g.x0,
+                        relay_y0=g.y0, relay_z=g.z, nz=zs.size, zs=zs.ctypes.data,
+                        alphas=al.ctypes.data, betas=be.ctypes.data, n_freq=freqs.size,
+                        n_illum=ill.shape[0], frequencies=freqs.ctypes.data,
+                        ill_xyz=ill.ctypes.data, n_frames=0 if t is None else t.size,
+                        times=None if t is None else t.ctypes.data,
+                        include_illum=int(bool(include_illumination)))
+    return a, (zs, al, be, freqs, ill, t)
+
+
+def capi_srsd(slices, frustum, **kw):
+    import torch
+    a, keep = srsd_args(slices, frustum, **kw)
+    lib = _lib.load()
+    nbytes = lib.pf_srsd_workspace_bytes(ctypes.byref(a))
+    assert nbytes > 0, _lib.last_error()
+    c = np.asarray(slices.coefficients)
+    coeff = torch.from_numpy(np.ascontiguousarray(c.transpose(2, 0, 1)).astype(np.complex64)).cuda()
+    vol = torch.empty((max(1, a.n_frames), frustum.count), dtype=torch.complex64, device="cuda")
+    ws = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+    rc = lib.pf_srsd(ctypes.byref(a), coeff.data_ptr(), vol.data_ptr(), ws.data_ptr(), nbytes,
+                     torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    return vol.cpu().numpy()
+
+
+def _frustum(g, nz=4, z0=0.6, z1=1.8):
+    zs = np.linspace(z0, z1, nz)
+    return pf.FrustumGrid(g, zs, zs[0] / zs, zs[0] / zs)
+
+
+def test_srsd_workspace_and_validation(rng):
+    sl, _ = _scene(rng, 32)
+    fr = _frustum(sl.relay.grid)
+    a, keep = srsd_args(sl, fr)
+    assert _lib.load().pf_srsd_workspace_bytes(ctypes.byref(a)) > 0
+    a.relay_z = 1.0                                       # planes no longer beyond the relay
+    assert _lib.load().pf_srsd_workspace_bytes(ctypes.byref(a)) == -1
+    assert "beyond the relay" in _lib.last_error()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [
+    dict(n=32),                 # P = 64 generic Stockham pad, Q = 128
+    dict(n=64),                 # P = 128 register path, Q = 256 register Bluestein, Horner C
+    dict(n=64, F=40),           # Horner blocks
+    dict(n=48, n_ill=2),        # P = 96 generic, two illuminations
+    dict(n=128, nz=3),          # P = 256, Q = 512
+])
+def test_pf_srsd_matches_oracle_and_engine(rng, case):
+    nz = case.pop("nz", 4)
+    sl, _ = _scene(rng, **case)
+    fr = _frustum(sl.relay.grid, nz=nz)
+    got = capi_srsd(sl, fr)[0]
+    ref = O.srsd(sl, fr)
+    assert O.rel_l2(got, ref) < TOL
+    assert O.rel_l2(got, pf.srsd(sl, fr).field) < 1e-5
+
+
+@pytest.mark.gpu
+def test_pf_srsd_video(rng):
+    sl, _ = _scene(rng, 32, F=3)
+    fr = _frustum(sl.relay.grid, nz=3)
+    times = np.array([0.0, 2e-10])
+    got = capi_srsd(sl, fr, times=times)
+    assert O.rel_l2(got, O.srsd(sl, fr, times=times)) < TOL

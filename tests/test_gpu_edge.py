@@ -82,3 +82,28 @@ def test_to_frequency_single_trace_and_short_window(rng):
         sl = pf.to_frequency(pf.TransientMeasurement(relay, ill, h, 16e-12), k)
         ref = O.to_frequency(h, k.bin_indices, k.frequencies, k.weights, 0.0)
         assert O.rel_l2(sl.coefficients, ref) < 1e-5
+
+
+def test_dropin_engine_cache_and_graph_replay(rng):
+    """The drop-in functions plan once per geometry (engine cache + graph replay on the
+    engine's own buffers): repeated calls with new data, alternating geometries and the
+    same geometry after other calls all match the oracle; results returned earlier are not
+    overwritten by later calls (fresh host arrays)."""
+    import importlib
+    R = importlib.import_module("paper_2501_05244_b200.reconstruct")
+    R.clear_engine_cache()
+    g1 = pf.UniformGrid2D(24, 24, 0.02, 0.02, -0.23, -0.23, 0.0)
+    g2 = pf.UniformGrid2D(20, 16, 0.03, 0.03, -0.285, -0.225, 0.0)
+    grids = {1: pf.CuboidGrid(pf.UniformGrid3D(24, 24, 3, 0.02, 0.02, 0.2, g1.x0, g1.y0, 0.4)),
+             2: pf.CuboidGrid(pf.UniformGrid3D(20, 16, 2, 0.03, 0.03, 0.3, g2.x0, g2.y0, 0.5))}
+    relays = {1: pf.UniformRelay(g1), 2: pf.UniformRelay(g2)}
+    kept = []
+    for key in (1, 2, 1, 1, 2):
+        sl = _sl(rng, relays[key], n_freq=3)
+        vol = pf.rsd(sl, grids[key])
+        ref = O.rsd(sl, grids[key])
+        assert O.rel_l2(vol.field, ref) < TOL
+        kept.append((vol, ref))
+    for vol, ref in kept:
+        assert O.rel_l2(vol.field, ref) < TOL
+    assert len(R._ENGINES) <= R._ENGINE_CACHE
