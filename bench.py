@@ -120,7 +120,8 @@ class ClockSampler:
 
 
 def _n_planes(grid):
-    return {"frustum": lambda g: g.n_planes, "explicit": lambda g: len(g.planes)}.get(
+    return {"frustum": lambda g: g.n_planes, "explicit": lambda g: len(g.planes),
+            "voxels": lambda g: 1}.get(
         grid.kind, lambda g: g.grid.nz)(grid)
 
 
@@ -161,7 +162,7 @@ def run_ours(args):
     I, D, T = hist.shape
     F = kernel.n_freq
     nz = _n_planes(cfg.grid)
-    explicit = cfg.grid.kind == "explicit"
+    explicit = cfg.grid.kind in ("explicit", "voxels")
     if explicit and world > 1:
         raise SystemExit("bench: config %d (explicit voxels) runs on one GPU" % args.config)
     d_lo, d_hi = shard_range(D, world, rank)
@@ -484,9 +485,11 @@ def _explicit_flops(eng, F, I, cfg):
     f1 = F * I * (cfg.relay.count * 17 ** 3 * 8 + (5.0 * fine3 * math.log2(fine3) if fine3 else 0))
     P2 = s2.px * s2.py
     fine2 = s2.plan.fine_elems
-    nplanes = s2.n_planes
+    # voxel clouds: every slab's Chebyshev node is a plane, every voxel reads all its nodes
+    nodes = getattr(s2, "nodes", 1)
+    nplanes = s2.n_slabs * nodes if hasattr(s2, "n_slabs") else s2.n_planes
     f2 = F * I * nplanes * (5.0 * P2 * math.log2(P2) + 5.0 * fine2 * math.log2(fine2))
-    f2 += F * I * cfg.n_voxels * 17 * 17 * 8
+    f2 += F * I * cfg.n_voxels * 17 * 17 * 8 * nodes
     return f1 + f2, ("stage 1 + stage 2 (type-1 spread + 3D FFT; kernel 2D FFT + fine-grid "
                      "IFFT + 17x17 interpolation; 5 n log2 n per FFT, 8 flops per tap)")
 
@@ -591,16 +594,20 @@ def cpu_baseline_sample(cfg, kernel, hist_dev, rec, args):
     coeff = rec.coeff.permute(1, 2, 0).cpu().numpy().astype(np.complex128)
     sl = _HostSlices(kernel.frequencies, coeff, cfg.relay, cfg.illuminations)
     if cfg.algorithm == "nursd3d-explicit":
-        # composed oracle (stage 1 + nursd2) on one frequency, single core, times F
+        # composed oracle (stage 1 + nursd2) on one frequency, single core, times F; a voxel
+        # cloud is one reference plane per voxel: a voxel subsample, extrapolated per voxel
         from oracle.pool import _OneFreq
+        grid, scale = _oracle_voxels(cfg.grid, 200)
         t = time.perf_counter()
-        O.nursd3d_explicit(_OneFreq(sl, 0), cfg.grid, cfg.lattice,
+        O.nursd3d_explicit(_OneFreq(sl, 0), grid, cfg.lattice,
                            z_pitch=sl.shortest_wavelength / 2.0)
-        t3 = (time.perf_counter() - t) * F
+        t3 = (time.perf_counter() - t) * F * scale
         return {"value": cfg.n_voxels / (t1 + t3), "unit": UNIT, "cores": 1, "kind": "port",
                 "sample": f"oracle.to_frequency on {n_tr} of {hist_dev.shape[1]} traces + the "
-                          f"composed oracle (nursd3d stage 1 + nursd2) for 1 of {F} frequencies; "
-                          f"per-trace and per-frequency linear extrapolation",
+                          f"composed oracle (nursd3d stage 1 + nursd2) for 1 of {F} frequencies"
+                          + (f" on {grid.count} of {cfg.n_voxels} voxels (one plane each)"
+                             if scale != 1.0 else "") +
+                          "; per-trace, per-frequency (and per-voxel) linear extrapolation",
                 "s1_s": t1, "s3_s": t3}
     fn = {"rsd": O.rsd, "srsd": O.srsd, "nursd1": O.nursd1}[cfg.algorithm]
     # per-frequency setup (relay spectrum / NUFFT) and per-plane cost separated by
@@ -734,6 +741,22 @@ def _respawn(args) -> bool:
     sys.exit(rc)
 
 
+def _oracle_voxels(grid, n):
+    """The oracle's view of an output grid: explicit planes as they are; a voxel cloud as
+    one reference plane per voxel (reconstruct.py:393-410), subsampled to n voxels plus the
+    lateral extremes (the nursd2 pad depends on them) -> (grid, extrapolation factor)."""
+    if grid.kind != "voxels":
+        return grid, 1.0
+    from paper_2501_05244_b200.core import VoxelCloud
+    pts = np.asarray(grid.points)
+    rng = np.random.default_rng(11)
+    keep = np.unique(np.concatenate([rng.choice(pts.shape[0], size=min(n, pts.shape[0]),
+                                                replace=False),
+                                     [pts[:, 0].argmin(), pts[:, 0].argmax(),
+                                      pts[:, 1].argmin(), pts[:, 1].argmax()]]))
+    return VoxelCloud(pts[keep]).as_explicit(), pts.shape[0] / keep.size
+
+
 def _run_reference_explicit(args, cfg, kernel, sl, ncores, world):
     """Config 2: the whole composed oracle (nursd3d stage 1 + nursd2, every frequency,
     every voxel) per step, frequencies spread over the host cores and added in ascending
@@ -743,12 +766,13 @@ def _run_reference_explicit(args, cfg, kernel, sl, ncores, world):
     F, D = kernel.n_freq, cfg.relay.count
     n_tr = 2048
     h = np.random.default_rng(1).poisson(2.0, size=(n_tr, cfg.n_bins)).astype(np.float64)
+    grid, scale = _oracle_voxels(cfg.grid, 400)
     times = []
     for it in range(args.warmup + args.steps):
         t = time.perf_counter()
-        oracle_freq_terms("nursd3d_explicit", sl, (cfg.grid, cfg.lattice), procs=ncores,
+        oracle_freq_terms("nursd3d_explicit", sl, (grid, cfg.lattice), procs=ncores,
                           z_pitch=sl.shortest_wavelength / 2.0)
-        t3 = time.perf_counter() - t
+        t3 = (time.perf_counter() - t) * scale
         t = time.perf_counter()
         O.to_frequency(h, kernel.bin_indices, kernel.frequencies, kernel.weights, cfg.t0)
         t1 = (time.perf_counter() - t) * D / n_tr / ncores
@@ -764,10 +788,13 @@ def _run_reference_explicit(args, cfg, kernel, sl, ncores, world):
         "config": {"workload": f"config{args.config}-{cfg.algorithm}", "voxels": cfg.n_voxels,
                    "pad": "reference pad rules"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
-                         "sample": f"per step: the full composed oracle over all {F} frequencies "
-                                   f"and {cfg.n_voxels} voxels ({min(ncores, F)} processes, one "
-                                   f"frequency each) + to_frequency on {n_tr} traces, "
-                                   f"extrapolated to {D} traces"},
+                         "sample": (f"per step: the full composed oracle over all {F} frequencies "
+                                    f"and {cfg.n_voxels} voxels " if scale == 1.0 else
+                                    f"per step: the composed oracle over all {F} frequencies on "
+                                    f"{grid.count} of {cfg.n_voxels} voxels (one reference plane "
+                                    f"each), extrapolated per voxel, ") +
+                                   f"({min(ncores, F)} processes, one frequency each) + "
+                                   f"to_frequency on {n_tr} traces, extrapolated to {D} traces"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

@@ -288,6 +288,17 @@ int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0, const floa
                            int64_t fine_stride, int n_illum, const double* ill, double khat,
                            int include_illum, float scale, const void* frame_w, int n_frames,
                            void* vol, int64_t vol_frame_stride, void* stream);
+/* The same readout for voxels at arbitrary depths (z-Chebyshev): voxel l takes the
+ * Lagrange-weighted sum lw[l][m] over its slab's `nodes` consecutive fine grids (the
+ * first at plane_idx[l]) of the same stencil; nodes = 1, lw = NULL is
+ * pf_nufft_interp2_batch.  One half warp per point. */
+int pf_nufft_interp2_nodes(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                           const double* xyz, const int32_t* plane_idx, const int64_t* dst_idx,
+                           int npts, int plane0, const void* fine, int64_t fine_plane_stride,
+                           int64_t fine_stride, int n_illum, const double* ill, double khat,
+                           int include_illum, float scale, const void* frame_w, int n_frames,
+                           void* vol, int64_t vol_frame_stride, int nodes, const float* lw,
+                           void* stream);
 /* type-2 finish for any dimension (spectral.py:376-380): out[l] = stencil sum of the
  * fine grid (after pf_nufft_place + inverse FFT) at point l; stencil width 2w+1 <= 32. */
 int pf_nufft_interp(const pf_nufft_geom* g, const int32_t* i0, const float* d0, int npts,

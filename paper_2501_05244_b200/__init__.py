@@ -16,7 +16,8 @@ from .core import (PROPAGATION_SIGN, SPEED_OF_LIGHT, ContainerFormatError, Cuboi
                    NonFiniteDataError, NonPlanarRelay, NonUniformPlanarRelay, PointList,
                    ReconstructionVolume, TransientMeasurement, TruncatedPayloadError,
                    TorusMap, UniformGrid2D, UniformGrid3D, UniformRelay, UnsupportedVersionError,
-                   ValidationError, VoxelPlane, grid_coordinates, illumination_coordinates,
+                   ValidationError, VoxelCloud, VoxelPlane, grid_coordinates,
+                   illumination_coordinates,
                    rescale_to_torus)
 from .phasor import (DeviceFrequencySlices, PhasorKernel, build_kernel, lateral_resolution,
                      to_frequency, to_frequency_device)
@@ -29,7 +30,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # the non-rsd algorithms live in .algorithms (loaded on first use)
     if name in ("srsd", "nursd1", "nursd2", "nursd3", "nursd3d", "srsd_nursd2", "rsd3d",
-                "nursd3d_explicit", "nursd3d_srsd", "rsd3d_srsd"):
+                "nursd3d_explicit", "nursd3d_srsd", "rsd3d_srsd", "nursd2_voxels"):
         from . import algorithms
         return getattr(algorithms, name)
     if name in ("cfft_n", "cifft_n", "cfft_2d", "cifft_2d", "sfft_1d", "sfft_2d",

@@ -104,6 +104,8 @@ _SIGNATURES = {
     "pf_nufft_interp": [_P(PfNufftGeom), _vp, _vp, _i, _vp, _vp, _vp],
     "pf_nufft_interp2_batch": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _i64, _i64,
                                _i, _vp, _d, _i, _f, _vp, _i, _vp, _i64, _vp],
+    "pf_nufft_interp2_nodes": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _i64, _i64,
+                               _i, _vp, _d, _i, _f, _vp, _i, _vp, _i64, _i, _vp, _vp],
     "pf_scatter_csr": [_vp, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp, _i64, _vp],
     "pf_bluestein_lines": [_vp, _i64, _i64, _i64, _i, _i, _vp, _i64, _i64, _i64, _i, _i, _i, _i,
                            _P(PfFftPlan), _vp, _vp, _vp],

@@ -125,6 +125,17 @@ def config(c: int) -> Config:
                      base.n_bins, base.delta_t, base.lambda_c, base.t0, "nursd1", seed)
         cfg.lattice_nodes = keep
         return cfg
+    if c == 7:
+        # config 2 with BASELINE's literal output: 1,000,000 seeded random voxel positions
+        # in the 1 m^3 box (arbitrary depths: the z-Chebyshev readout)
+        base = config(2)
+        vox = np.column_stack([rng.uniform(-0.5, 0.5, size=(1_000_000, 2)),
+                               rng.uniform(1.0, 2.0, size=1_000_000)])
+        cfg = Config("c2-voxels", base.relay, base.illuminations, core.VoxelCloud(vox),
+                     base.scatterers, base.albedo, base.n_bins, base.delta_t, base.lambda_c,
+                     base.t0, "nursd3d-explicit", seed)
+        cfg.lattice = base.lattice
+        return cfg
     if c == 6:
         # "config 4 heavy": BASELINE config 4 states "~400 frequency bins in the wavelet
         # band", which the reference's build_kernel (sigma = c / (5 lambda)) cannot give at

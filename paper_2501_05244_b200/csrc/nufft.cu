@@ -317,6 +317,9 @@ k_interp2_batch(pf_nufft_geom G, const int* __restrict__ i0, const float* __rest
 // points where the warp-per-point kernel left 32 - W lanes idle; per-point arithmetic
 // and summation order per column pair as k_interp2_batch (the column partial sums of a
 // row are combined in a different order, fp32 rounding only).
+// nodes > 1 (arbitrary voxel depths, z-Chebyshev readout): the voxel's value is the sum
+// over its slab's `nodes` consecutive fine grids (first at plane_idx[l]) weighted by its
+// Lagrange weights lw[l][m] -- the same stencil on every node grid.
 __global__ void __launch_bounds__(256)
 k_interp2_batch_h(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
                   const double* __restrict__ xyz, const int* __restrict__ plane_idx,
@@ -325,7 +328,8 @@ k_interp2_batch_h(pf_nufft_geom G, const int* __restrict__ i0, const float* __re
                   long long fine_stride, int n_illum, const double* __restrict__ ill,
                   double kturns, int include_illum, float scale,
                   const float2* __restrict__ frame_w, int n_frames, float2* __restrict__ vol,
-                  long long vol_frame_stride) {
+                  long long vol_frame_stride, int nodes = 1,
+                  const float* __restrict__ lw = nullptr) {
   const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
   const int l = blockIdx.x * (blockDim.x >> 4) + ((threadIdx.x >> 5) << 1) + half;
   const bool live = l < npts;
@@ -351,26 +355,30 @@ k_interp2_batch_h(pf_nufft_geom G, const int* __restrict__ i0, const float* __re
   const float2* fplane = fine + (long long)(plane_idx[lc] - plane0) * fine_plane_stride;
   float2 tot = make_float2(0.f, 0.f);
   for (int p = 0; p < n_illum; p++) {
-    const float2* fp = fplane + (long long)p * fine_stride;
     float2 acc = make_float2(0.f, 0.f);
-    int cy = cy0;
-    for (int oy = 0; oy < W; oy++) {
-      const int src = (half << 4) + (oy & 15);
-      const float wa = __shfl_sync(0xffffffffu, wy1, src);
-      const float wb = __shfl_sync(0xffffffffu, wy2, src);
-      const float wy = oy < 16 ? wa : wb;
-      const float2* rowp = fp + (long long)cy * mrx;
-      const float2 f1 = __ldg(rowp + cx1);
-      const float w1 = wx1 * wy;
-      acc.x = fmaf(w1, f1.x, acc.x);
-      acc.y = fmaf(w1, f1.y, acc.y);
-      if (on2) {
-        const float2 f2 = __ldg(rowp + cx2);
-        const float w2 = wx2 * wy;
-        acc.x = fmaf(w2, f2.x, acc.x);
-        acc.y = fmaf(w2, f2.y, acc.y);
+    for (int m = 0; m < nodes; m++) {
+      const float2* fp = fplane + (long long)m * fine_plane_stride + (long long)p * fine_stride;
+      const float lwm = lw ? __ldg(lw + (long long)lc * nodes + m) : 1.0f;
+      const float wx1m = wx1 * lwm, wx2m = wx2 * lwm;
+      int cy = cy0;
+      for (int oy = 0; oy < W; oy++) {
+        const int src = (half << 4) + (oy & 15);
+        const float wa = __shfl_sync(0xffffffffu, wy1, src);
+        const float wb = __shfl_sync(0xffffffffu, wy2, src);
+        const float wy = oy < 16 ? wa : wb;
+        const float2* rowp = fp + (long long)cy * mrx;
+        const float2 f1 = __ldg(rowp + cx1);
+        const float w1 = wx1m * wy;
+        acc.x = fmaf(w1, f1.x, acc.x);
+        acc.y = fmaf(w1, f1.y, acc.y);
+        if (on2) {
+          const float2 f2 = __ldg(rowp + cx2);
+          const float w2 = wx2m * wy;
+          acc.x = fmaf(w2, f2.x, acc.x);
+          acc.y = fmaf(w2, f2.y, acc.y);
+        }
+        if (++cy == mry) cy = 0;
       }
-      if (++cy == mry) cy = 0;
     }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) {
@@ -394,6 +402,16 @@ k_interp2_batch_h(pf_nufft_geom G, const int* __restrict__ i0, const float* __re
     }
   }
 }
+
+extern "C" int pf_nufft_interp2_nodes(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                                      const double* xyz, const int32_t* plane_idx,
+                                      const int64_t* dst_idx, int npts, int plane0,
+                                      const void* fine, int64_t fine_plane_stride,
+                                      int64_t fine_stride, int n_illum, const double* ill,
+                                      double khat, int include_illum, float scale,
+                                      const void* frame_w, int n_frames, void* vol,
+                                      int64_t vol_frame_stride, int nodes, const float* lw,
+                                      void* stream);
 
 // w = 16 (W = 33 > 32 lanes): one thread per point.
 __global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
@@ -610,5 +628,26 @@ extern "C" int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0,
       fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,
       (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride);
   PF_LAUNCH_CHECK("k_interp2_batch");
+  return 0;
+}
+
+extern "C" int pf_nufft_interp2_nodes(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                                      const double* xyz, const int32_t* plane_idx,
+                                      const int64_t* dst_idx, int npts, int plane0,
+                                      const void* fine, int64_t fine_plane_stride,
+                                      int64_t fine_stride, int n_illum, const double* ill,
+                                      double khat, int include_illum, float scale,
+                                      const void* frame_w, int n_frames, void* vol,
+                                      int64_t vol_frame_stride, int nodes, const float* lw,
+                                      void* stream) {
+  PF_ARG_CHECK(g && g->dim == 2 && 2 * g->w + 1 <= 32 && npts >= 0 && nodes >= 1 &&
+                   (nodes == 1 || lw != nullptr),
+               "pf_nufft_interp2_nodes: bad args (2D, stencil width <= 32, weights for nodes > 1)");
+  if (npts == 0) return 0;
+  k_interp2_batch_h<<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
+      *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine,
+      fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,
+      (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride, nodes, lw);
+  PF_LAUNCH_CHECK("k_interp2_nodes");
   return 0;
 }

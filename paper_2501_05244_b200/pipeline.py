@@ -44,7 +44,8 @@ def make_engine(algorithm, meta, grid, device, plane_range=None, times=None,
     name = algorithm.replace("_", "-").lower()
     if name == "nursd3d-explicit":
         from .algorithms import Nursd3dExplicitEngine
-        if plane_range is not None and tuple(plane_range) != (0, len(grid.planes)):
+        n_pl = len(grid.planes) if grid.kind == "explicit" else 1
+        if plane_range is not None and tuple(plane_range) != (0, n_pl):
             raise ValueError("nursd3d-explicit does not shard depth planes")
         return Nursd3dExplicitEngine(meta, grid, lattice, eps, None, times,
                                      include_illumination, device=device)

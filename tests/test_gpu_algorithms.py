@@ -194,3 +194,38 @@ def test_3d_relay_plus_srsd_vs_composed_oracle(rng, stage1, video):
     vol = fn(sl, frustum, times=times)
     ref = O.lattice_srsd(sl, frustum, stage1=stage1, times=times)
     assert O.rel_l2(vol.field, ref) < TOL
+
+
+@pytest.mark.parametrize("video", [False, True])
+def test_nursd2_voxels_arbitrary_depths_vs_per_voxel_planes(rng, video):
+    """Voxels at arbitrary depths (VoxelCloud, z-Chebyshev readout) = the reference's nursd2
+    on one plane per voxel (reconstruct.py:413-459)."""
+    n = 24
+    p = 0.02
+    g = pf.UniformGrid2D(n, n, p, p, -(n - 1) * p / 2, -(n - 1) * p / 2, 0.0)
+    sl = _rand_slices(rng, pf.UniformRelay(g), n_freq=3, n_ill=1)
+    pts = np.column_stack([rng.uniform(-0.2, 0.2, size=(150, 2)), rng.uniform(0.5, 1.3, 150)])
+    cloud = pf.VoxelCloud(pts)
+    times = np.array([0.0, 1.5e-10]) if video else None
+    vol = pf.nursd2_voxels(sl, cloud, times=times)
+    ref = O.nursd2(sl, cloud.as_explicit(), times=times)
+    assert O.rel_l2(vol.field, ref) < TOL
+
+
+def test_config2_family_voxel_cloud_vs_composed_oracle(rng):
+    """Non-planar relay -> voxels at arbitrary depths (config 7 family): nursd3d stage 1 +
+    the z-Chebyshev nursd2 readout against the composed oracle with one plane per voxel."""
+    from paper_2501_05244_b200.algorithms import nursd3d_explicit
+    xy = rng.uniform(-0.3, 0.3, size=(500, 2))
+    zz = 0.03 * np.sin(2 * np.pi * xy[:, 0] / 0.6) * np.cos(2 * np.pi * xy[:, 1] / 0.9)
+    relay = pf.NonPlanarRelay(pf.PointList(np.column_stack([xy, zz])))
+    freqs = 2 * np.pi * 299792458.0 / 0.06 * (1.0 + 0.03 * np.arange(2))
+    coeff = rng.normal(size=(1, 500, 2)) + 1j * rng.normal(size=(1, 500, 2))
+    sl = pf.FrequencySlices(freqs, coeff, relay, pf.PointList(np.array([[0.0, 0.0, 0.0]])))
+    p = 0.6 / 24
+    lattice = pf.CuboidGrid(pf.UniformGrid3D(24, 24, 1, p, p, 0.1, -0.3 + p / 2, -0.3 + p / 2, 0.6))
+    pts = np.column_stack([rng.uniform(-0.15, 0.15, size=(120, 2)), rng.uniform(0.5, 0.9, 120)])
+    cloud = pf.VoxelCloud(pts)
+    vol = nursd3d_explicit(sl, cloud, lattice)
+    ref = O.nursd3d_explicit(sl, cloud.as_explicit(), lattice)
+    assert O.rel_l2(vol.field, ref) < TOL

@@ -167,3 +167,37 @@ def test_config6_heavy_400_bins_plane_subsets(planes):
     ref = oracle_freq_terms("rsd", sl.to_host(), (cfg.grid,), plane_range=planes)
     _check_volume("config6-heavy-planes-%d-%d" % planes, got, ref,
                   (planes[1] - planes[0], 512, 512), tg, time.perf_counter() - t)
+
+
+def test_config7_arbitrary_depth_voxels_subsample():
+    """Config 2 with BASELINE's literal output -- 1,000,000 seeded random (x, y, z) voxel
+    positions in the box -- through the z-Chebyshev readout, against the composed oracle
+    with one plane per voxel (reference nursd3d stage 1, then nursd2 :413-459) on a
+    2,000-voxel subsample that keeps the lateral extremes (the nursd2 pad depends on them)."""
+    cfg = configs.config(7)
+    sl, k = _slices(cfg)
+    eng = Nursd3dExplicitEngine(sl, cfg.grid, cfg.lattice)
+    vol = torch.zeros((1, cfg.grid.count), dtype=torch.complex64, device="cuda")
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    eng.run(sl.device_coefficients, vol)
+    torch.cuda.synchronize()
+    tg = time.perf_counter() - t
+    got_all = vol[0].cpu().numpy()
+    pts = np.asarray(cfg.grid.points)
+    rng = np.random.default_rng(77)
+    keep = np.unique(np.concatenate([
+        rng.choice(pts.shape[0], size=2000, replace=False),
+        [pts[:, 0].argmin(), pts[:, 0].argmax(), pts[:, 1].argmin(), pts[:, 1].argmax()]]))
+    sub = pf.VoxelCloud(pts[keep]).as_explicit()
+    host = sl.to_host()
+    t = time.perf_counter()
+    ref = oracle_freq_terms("nursd3d_explicit", host, (sub, cfg.lattice),
+                            z_pitch=host.shortest_wavelength / 2.0)
+    to = time.perf_counter() - t
+    got = got_all[keep]
+    rel = O.rel_l2(got, ref)
+    _log({"case": "config7-voxels-subsample", "rel_l2": rel, "voxels_checked": int(keep.size),
+          "voxels": int(got_all.size), "node_planes": int(eng.stage2.ro.n_slabs * eng.stage2.ro.nodes),
+          "gpu_s": tg, "oracle_s": to, "oracle_procs": _procs()})
+    assert rel < TOL, rel
