@@ -189,9 +189,34 @@ def run_ours(args):
     # on a side stream while the next chunk computes
     n_chunks = rec.gather_chunks
 
+    # N > 1 on the Horner register path: the collectives fused into the kernels over peer
+    # memory (K1 stores every rank's slices, kernel C stores rank 0's volume; CUDA IPC over
+    # NVLink / NVSwitch) -- no NCCL data transfer, two one-element all-reduces for order
+    peer = None
+    if (world > 1 and os.environ.get("PF_PEER", "1") != "0" and I == 1 and T % 2048 == 0
+            and hasattr(eng, "fused_gather_ok") and eng.fused_gather_ok()):
+        from paper_2501_05244_b200.distributed import PeerSlices, PeerVolume
+        from paper_2501_05244_b200.phasor import temporal_peers
+        peer = (PeerSlices(F, I, D, world, rank, device), PeerVolume(nz, plane_vox, world, rank,
+                                                                     device))
+
     final = {}
 
+    def step_peer():
+        ps, pv = peer
+        ev[0].record(stream)
+        temporal_peers(rec.temporal, hist_shard.view(-1, T), ps, stream)
+        ev[1].record(stream)
+        ps.sync(stream)
+        ev[2].record(stream)
+        eng.run_graphed(ps.full, rec.vol, stream, vol_out=pv.out_ptr)
+        ev[3].record(stream)
+        final["vol"] = pv.sync(stream)
+        ev[4].record(stream)
+
     def step():
+        if peer is not None:
+            return step_peer()
         ev[0].record(stream)
         rec.temporal.run(hist_shard.view(-1, T), local_shard.view(F, -1), stream)
         ev[1].record(stream)
@@ -351,9 +376,17 @@ def run_ours(args):
         "clocks": clocks,
         "volume_sha256_16": vol_digest,
         "dist_backend": (dist.get_backend() if world > 1 else None),
+        "collectives": (None if world == 1 else
+                        "fused into K1 and kernel C over peer memory (CUDA IPC)" if peer is not None
+                        else "NCCL all-gather + chunked gather"),
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample(cfg, kernel, hist_shard, rec, args)
+    if peer is not None:
+        torch.cuda.synchronize()
+        dist.barrier()
+        for pb in peer:
+            pb.close()
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:

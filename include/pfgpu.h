@@ -168,12 +168,14 @@ int pf_prop_rows_out(const pf_plane* planes, int nplanes, double khat,
  * chain the blocks with Z = exp(i B dk d) from a float64-reduced phase: mode 3 at the
  * lowest frequency of a block other than the first (o <- o Z + (vol z + v), vol <- 0),
  * mode 4 at f = 0 (vol <- (o Z + (vol z + v)) exp(i k_0 d)); ws_o = the batch's outer
- * accumulator (nplanes x ny x nx complex64), zkhat = B dkhat.
+ * accumulator (nplanes x ny x nx complex64), zkhat = B dkhat.  vol_out (NULL: vol) receives the
+ * finished planes of the final step (modes 2 and 4) at the same offsets: the fused volume
+ * gather points it at rank 0's volume (peer memory, distributed.PeerVolume).
  * Returns 1 without work when the geometry is not eligible. */
 int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, double khat, double dkhat,
                             int mode, const pf_prop_geom* g, const pf_fft_plan* plan_x,
                             const void* ws_b, const double* ill_xyz, const void* frame_w,
-                            void* vol, void* ws_o, double zkhat, void* stream);
+                            void* vol, void* ws_o, double zkhat, void* vol_out, void* stream);
 
 /* All nf frequencies of a plane batch at once (register path, static volume):
  * kturns: device float64 [nf] = khat_f / (2 pi); ws_a / uhat / ws_b advance by
@@ -196,6 +198,22 @@ int pf_prop_fbatch_generic(const pf_plane* planes, int nplanes, const double* kh
                            const pf_fft_plan* plan_y, void* ws_a, int64_t ws_a_fs,
                            const void* uhat, int64_t uhat_fs, void* ws_b, int64_t ws_b_fs,
                            const double* ill_xyz, const void* frame_w, void* vol, void* stream);
+
+/* K1 with the slice all-gather fused into its store (distributed.PeerSlices): each retained
+ * bin of this rank's traces is written to peers[j][f * peer_stride + peer_col + trace] for
+ * every rank's full [F][I][D] slice buffer (device array of n_peers device pointers, peer
+ * memory mapped with pf_ipc_open); n_bins = 64 M with M in {32, 64, 128, 256}. */
+int pf_temporal_dft_peers(const float* hist, int64_t n_traces, int n_bins, const int32_t* bins,
+                          const void* twiddle, const void* wphase, int n_freq,
+                          uint64_t inner_mask, const uint64_t* peers, int n_peers,
+                          int64_t peer_stride, int64_t peer_col, void* stream);
+/* CUDA IPC for the peer-memory collectives: the 64-byte handle of the allocation holding
+ * ptr plus ptr's offset in it; the mapping of that allocation in another process (same
+ * device, or a peer over NVLink / NVSwitch) with the offset applied; unmapping (pass the
+ * mapped pointer minus its offset). */
+int pf_ipc_handle(const void* ptr, void* handle_out, int64_t* offset_out);
+int pf_ipc_open(const void* handle, int64_t offset, void** ptr_out);
+int pf_ipc_close(void* base);
 
 /* out (device int32[2]) = {number of non-finite, number of negative} float32
  * values in x[0..n): the payload checks of reference read_dataset

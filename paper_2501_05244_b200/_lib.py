@@ -122,7 +122,12 @@ _SIGNATURES = {
     "pf_zslab": [_vp, _i, _i, _i64, _vp, _f, _vp, _vp],
     "pf_roll": [_vp, _vp, _i64, _i, _i, _i, _i, _i, _i, _vp],
     "pf_prop_rows_out_horner": [_vp, _i, _d, _d, _i, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp,
-                                _vp, _vp, _vp, _d, _vp],
+                                _vp, _vp, _vp, _d, _vp, _vp],
+    "pf_temporal_dft_peers": [_vp, _i64, _i, _vp, _vp, _vp, _i, ctypes.c_uint64, _vp, _i,
+                              _i64, _i64, _vp],
+    "pf_ipc_handle": [_vp, _vp, _P(ctypes.c_int64)],
+    "pf_ipc_open": [_vp, _i64, _P(ctypes.c_void_p)],
+    "pf_ipc_close": [_vp],
     "pf_prop_rows_out": [_vp, _i, _d, _P(PfPropGeom), _P(PfFftPlan), _vp, _vp, _vp, _i, _vp,
                          _i64, _vp],
 }

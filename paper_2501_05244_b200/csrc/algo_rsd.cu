@@ -280,7 +280,7 @@ extern "C" int pf_rsd(const pf_rsd_args* a, const void* slices, void* vol, void*
         }
         rc = pf_prop_rows_out_horner(pp, nb, khat, L.dkhat, mode, &g, &plx, wb, ill_d,
                                      fw_d + (int64_t)f * frames, vol, wo,
-                                     HORNER_BLOCK * L.dkhat, ls);
+                                     HORNER_BLOCK * L.dkhat, nullptr, ls);
       } else {
         rc = pf_prop_rows_out(pp, nb, khat, &g, &plx, wb, ill_d, fw_d + (int64_t)f * frames,
                               frames, vol, V, ls);

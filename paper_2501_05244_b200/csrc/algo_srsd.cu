@@ -297,7 +297,7 @@ extern "C" int pf_srsd(const pf_srsd_args* a, const void* slices, void* vol, voi
                           "pf_srsd: zero");
         }
         rc = pf_prop_rows_out_horner(pp, nb, khat, L.dkhat, mode, &g, &plans[0], wb, ill_d,
-                                     fw_d + (int64_t)f * frames, vol, wo, 32 * L.dkhat, ls);
+                                     fw_d + (int64_t)f * frames, vol, wo, 32 * L.dkhat, nullptr, ls);
       } else {
         rc = pf_prop_rows_out(pp, nb, khat, &g, &plans[0], wb, ill_d, fw_d + (int64_t)f * frames,
                               frames, vol, V, ls);

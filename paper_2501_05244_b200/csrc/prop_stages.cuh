@@ -153,7 +153,7 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
                                      const float2* __restrict__ frame_w, int n_frames,
                                      float2* __restrict__ vol, long long vfs, int tile,
                                      float dturns = 0.f, float2* __restrict__ ws_o = nullptr,
-                                     double zturns = 0.0) {
+                                     double zturns = 0.0, float2* __restrict__ vol_out = nullptr) {
   static_assert(HOR == 0 || (!MULTI && PRE && CENT), "Horner variant: one illumination, "
                 "centred crop, prefetched volume");
   constexpr int P = 32 * L;
@@ -289,7 +289,9 @@ __device__ __forceinline__ void st_c(float2* sm, const pf_plane& pl, double ktur
       const float2* old = volbuf + r * nx;
       const float2 fw = cscale(frame_w[0], scale);
       if (CENT && HOR) {
-        float2* dt = vol + off + t;
+        // the final step (HOR 2 / 4) may store the finished plane elsewhere: the fused
+        // volume gather writes it straight into rank 0's volume (peer memory)
+        float2* dt = ((HOR == 2 || HOR == 4) && vol_out ? vol_out : vol) + off + t;
         const float2* ot = old + t;
         const double dy = yv - ill[1], dz = pl.z - ill[2];
         const double byz = fma(dy, dy, dz * dz);

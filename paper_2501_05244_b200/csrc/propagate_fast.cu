@@ -64,12 +64,14 @@ __global__ void __launch_bounds__(FT, 2)
 k_pc_h(const pf_plane* __restrict__ planes, double kturns, float dturns, pf_prop_geom g,
        const float2* __restrict__ tw, const float2* __restrict__ ws_b,
        const double* __restrict__ ill, const float2* __restrict__ frame_w,
-       float2* __restrict__ vol, float2* __restrict__ ws_o, double zturns) {
+       float2* __restrict__ vol, float2* __restrict__ ws_o, double zturns,
+       float2* __restrict__ vol_out) {
   extern __shared__ float2 sm[];
   const long long wb_plane = 32LL * L * g.ny;
   st_c<L, false, true, true, HOR>(sm, planes[blockIdx.y], kturns, g, tw,
                                   ws_b + blockIdx.y * wb_plane, ill, frame_w, 1, vol, 0,
-                                  blockIdx.x, dturns, ws_o, zturns);
+                                  blockIdx.x, dturns, ws_o, zturns, vol_out);
+  if ((HOR == 2 || HOR == 4) && vol_out) __threadfence_system();
 }
 
 // ---- B split in two register-light kernels (128 registers, 16 warps/SM):
@@ -728,7 +730,7 @@ extern "C" int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, doub
                                        double dkhat, int mode, const pf_prop_geom* g,
                                        const pf_fft_plan* plan_x, const void* ws_b,
                                        const double* ill_xyz, const void* frame_w, void* vol,
-                                       void* ws_o, double zkhat, void* stream) {
+                                       void* ws_o, double zkhat, void* vol_out, void* stream) {
   PF_ARG_CHECK(g && plan_x && plan_x->n == g->px && nplanes >= 1 && frame_w && vol &&
                mode >= 1 && mode <= 4 && (mode < 3 || ws_o),
                "pf_prop_rows_out_horner: bad args");
@@ -761,11 +763,12 @@ extern "C" int pf_prop_rows_out_horner(const pf_plane* planes, int nplanes, doub
     const float2* fw = (const float2*)frame_w;                                                 \
     float2* vo = (float2*)vol;                                                                 \
     float2* wo = (float2*)ws_o;                                                                \
+    float2* vout = (float2*)vol_out;                                                           \
     switch (mode) {                                                                            \
-      case 1: k_pc_h<LL, 1><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns); break; \
-      case 2: k_pc_h<LL, 2><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns); break; \
-      case 3: k_pc_h<LL, 3><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns); break; \
-      default: k_pc_h<LL, 4><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns); break; \
+      case 1: k_pc_h<LL, 1><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns, vout); break; \
+      case 2: k_pc_h<LL, 2><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns, vout); break; \
+      case 3: k_pc_h<LL, 3><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns, vout); break; \
+      default: k_pc_h<LL, 4><<<grid, FT, sm, st>>>(planes, kturns, dturns, *g, tw, wb, ill_xyz, fw, vo, wo, zturns, vout); break; \
     }                                                                                          \
     PF_LAUNCH_CHECK("k_pc_h");                                                                 \
     return 0;                                                                                  \

@@ -157,7 +157,9 @@ __global__ void __launch_bounds__(K1_THREADS)
 k_temporal_dft_pair(const float* __restrict__ hist, long long n_traces,
                     const int* __restrict__ bins, const float2* __restrict__ twt, int twt_ld,
                     const float2* __restrict__ wphase, int F, float2* __restrict__ out,
-                    long long out_stride, int ts_cap, unsigned long long inner_mask) {
+                    long long out_stride, int ts_cap, unsigned long long inner_mask,
+                    const unsigned long long* __restrict__ peers = nullptr, int n_peers = 0,
+                    long long peer_stride = 0, long long peer_col = 0) {
   static_assert(M >= 32, "one or more whole warps per trace");
   constexpr int G = K1_THREADS / M;
   constexpr int T = M * K1_L;
@@ -216,11 +218,20 @@ k_temporal_dft_pair(const float* __restrict__ hist, long long n_traces,
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
       if (valid && hh == 0) {
         if (kv >> 8) acc.y = -acc.y;
-        out[(long long)f * out_stride + trace] = cmul(acc, wphase[f]);
+        const float2 val = cmul(acc, wphase[f]);
+        if (n_peers == 0) {
+          out[(long long)f * out_stride + trace] = val;
+        } else {
+          // fused all-gather: this rank's detector shard straight into every rank's full
+          // [F][I][D] slice buffer (peer memory over NVLink / NVSwitch)
+          const long long o = (long long)f * peer_stride + peer_col + trace;
+          for (int j = 0; j < n_peers; j++) reinterpret_cast<float2*>(peers[j])[o] = val;
+        }
       }
     }
     trace_sync(1 + g, M);
   }
+  if (n_peers) __threadfence_system();   // peer stores visible before the kernel retires
 }
 
 static int k1_pair_mode() {
@@ -387,7 +398,9 @@ constexpr int K1_FCHUNK = 64;  // retained bins per pass (shared-memory bound)
 template <int M>
 int launch_k1(const float* hist, long long n_traces, const int* bins, const float2* twt,
               const float2* wphase, int F_total, float2* out, long long out_stride,
-              unsigned long long inner_mask, cudaStream_t st) {
+              unsigned long long inner_mask, cudaStream_t st,
+              const unsigned long long* peers = nullptr, int n_peers = 0,
+              long long peer_stride = 0, long long peer_col = 0) {
   constexpr int G = K1_THREADS / M;
   const int FC = F_total < K1_FCHUNK ? F_total : K1_FCHUNK;
   // parked bins per column: the caller's set of inner bins (bins mod 64 folded to
@@ -415,7 +428,11 @@ int launch_k1(const float* hist, long long n_traces, const int* bins, const floa
   const long long cap = (long long)nsm * per;
   const int grid_k1 = (int)(groups < cap ? groups : cap);
   constexpr int MPAIR = M >= 32 ? M : 32;
-  const bool pair = M >= 32 && k1_pair_mode() != 0;
+  const bool pair = M >= 32 && (k1_pair_mode() != 0 || n_peers > 0);
+  if (n_peers > 0 && !pair) {
+    pf_set_error("pf_temporal_dft_peers: needs n_bins = 64 M with M >= 32");
+    return -1;
+  }
   if (pair) {
     static PfDevOnce attr2;
     if (attr2.first())
@@ -427,7 +444,8 @@ int launch_k1(const float* hist, long long n_traces, const int* bins, const floa
     if (pair) {
       k_temporal_dft_pair<MPAIR><<<grid_k1, K1_THREADS, smem, st>>>(
           hist, n_traces, bins + f0, twt + f0, F_total, wphase + f0, F,
-          out + (long long)f0 * out_stride, out_stride, ts_cap, inner_mask);
+          out + (long long)f0 * out_stride, out_stride, ts_cap, inner_mask, peers, n_peers,
+          peer_stride, peer_col + (long long)f0 * peer_stride);
       PF_LAUNCH_CHECK("k_temporal_dft_pair");
     } else {
       k_temporal_dft<M><<<grid_k1, K1_THREADS, smem, st>>>(hist, n_traces, bins + f0, twt + f0,
@@ -537,4 +555,31 @@ extern "C" int pf_temporal_dft_direct(const float* hist, int64_t n_traces, int n
       (float2*)out, out_stride);
   PF_LAUNCH_CHECK("k_temporal_dft_direct");
   return 0;
+}
+
+// K1 with the slice all-gather fused into its store (multi-GPU, distributed.PeerSlices):
+// every retained bin of this rank's traces goes to peers[j][f * peer_stride + peer_col +
+// trace] for each of the n_peers ranks' full slice buffers (this rank's own included).
+extern "C" int pf_temporal_dft_peers(const float* hist, int64_t n_traces, int n_bins,
+                                     const int32_t* bins, const void* twiddle,
+                                     const void* wphase, int n_freq, uint64_t inner_mask,
+                                     const uint64_t* peers, int n_peers, int64_t peer_stride,
+                                     int64_t peer_col, void* stream) {
+  PF_ARG_CHECK(n_traces >= 0 && n_freq >= 1 && peers && n_peers >= 1,
+               "pf_temporal_dft_peers: bad arguments");
+  if (n_traces == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const float2* tw = (const float2*)twiddle;
+  const float2* wp = (const float2*)wphase;
+  const unsigned long long* pp = (const unsigned long long*)peers;
+  const int M = (n_bins % K1_L == 0) ? n_bins / K1_L : 0;
+  switch (M) {
+    case 32: return launch_k1<32>(hist, n_traces, bins, tw, wp, n_freq, nullptr, 0, inner_mask, st, pp, n_peers, peer_stride, peer_col);
+    case 64: return launch_k1<64>(hist, n_traces, bins, tw, wp, n_freq, nullptr, 0, inner_mask, st, pp, n_peers, peer_stride, peer_col);
+    case 128: return launch_k1<128>(hist, n_traces, bins, tw, wp, n_freq, nullptr, 0, inner_mask, st, pp, n_peers, peer_stride, peer_col);
+    case 256: return launch_k1<256>(hist, n_traces, bins, tw, wp, n_freq, nullptr, 0, inner_mask, st, pp, n_peers, peer_stride, peer_col);
+    default: break;
+  }
+  pf_set_error("pf_temporal_dft_peers: n_bins must be 64 M with M in {32, 64, 128, 256}");
+  return -1;
 }

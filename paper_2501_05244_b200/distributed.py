@@ -146,3 +146,127 @@ class VolumeGather:
             n = (pb - pa) * self.pv
             self.full[:, (lo + pa) * self.pv:(lo + pb) * self.pv].copy_(recv[r][:, :n])
         return self.full
+
+
+# ---------------------------------------------------------------------------
+# peer-memory collectives: the exchange is fused into the producing kernel
+# ---------------------------------------------------------------------------
+
+
+def _ipc_handle(t: torch.Tensor) -> tuple:
+    """(64-byte handle of the allocation holding t, t's offset in it)."""
+    import ctypes
+
+    from . import _lib
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    _lib.call("pf_ipc_handle", t.data_ptr(), buf, ctypes.byref(off))
+    return buf.raw, int(off.value)
+
+
+def _ipc_open(h: tuple) -> tuple:
+    """Map a peer's allocation: (pointer to the peer tensor, mapping base to close)."""
+    import ctypes
+
+    from . import _lib
+    p = ctypes.c_void_p()
+    _lib.call("pf_ipc_open", ctypes.create_string_buffer(h[0], 64), h[1], ctypes.byref(p))
+    return int(p.value), int(p.value) - h[1]
+
+
+def stream_barrier(group=None, device=None, stream=None) -> None:
+    """Order every rank's later device work after every rank's earlier device work without
+    a host round trip: a one-element all-reduce enqueued on the stream (NCCL).  gloo (CPU
+    tests, one GPU shared by the ranks): drain the device, then a host barrier."""
+    if dist.get_backend(group) == "gloo":
+        torch.cuda.synchronize(device)
+        dist.barrier(group=group)
+        return
+    flag = torch.ones(1, dtype=torch.float32, device=device)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    with torch.cuda.stream(s):
+        dist.all_reduce(flag, group=group)
+
+
+class PeerSlices:
+    """The slice all-gather fused into K1: every rank owns a full
+    ``[F, I, D]`` slice buffer; the ranks exchange CUDA IPC handles of those buffers once,
+    and each rank's K1 (``pf_temporal_dft_peers``) writes its detector shard's bins
+    straight into all of them over NVLink / NVSwitch (peer stores tile by tile, no NCCL
+    transfer); ``sync`` orders the reads after every rank's K1."""
+
+    def __init__(self, n_freq: int, n_illum: int, n_det: int, world: int, rank: int, device,
+                 group=None):
+        if n_illum != 1:   # a rank's traces are contiguous columns only for one illumination
+            raise ValueError("the fused slice all-gather takes one illumination")
+        self.F, self.I, self.D = n_freq, n_illum, n_det
+        self.world, self.rank, self.group, self.device = world, rank, group, device
+        self.ranges = [shard_range(n_det, world, r) for r in range(world)]
+        self.full = torch.zeros((n_freq, n_illum, n_det), dtype=torch.complex64, device=device)
+        torch.cuda.synchronize(device)   # zeroed before any peer can write into it
+        handles = [None] * world
+        dist.all_gather_object(handles, _ipc_handle(self.full), group=group)
+        self._opened = []
+        ptrs = []
+        for r, h in enumerate(handles):
+            if r == rank:
+                ptrs.append(self.full.data_ptr())
+            else:
+                p, base = _ipc_open(h)
+                self._opened.append(base)
+                ptrs.append(p)
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=device)
+        lo, _ = self.ranges[rank]
+        # column of this rank's first trace in the [F][I*D] view (illumination-major rows)
+        self.peer_stride = n_illum * n_det
+        self.col = lo
+
+    def sync(self, stream=None):
+        stream_barrier(self.group, self.device, stream)
+        return self.full
+
+    def close(self):
+        from . import _lib
+        for p in self._opened:
+            _lib.call("pf_ipc_close", p)
+        self._opened = []
+
+
+class PeerVolume:
+    """The volume gather fused into kernel C: rank 0 owns the full
+    volume; the other ranks map it once (CUDA IPC) and their final Horner step of every
+    plane batch stores the finished planes straight into it (``vol_out`` of
+    ``pf_prop_rows_out_horner``), so each plane batch's transfer overlaps the rest of the
+    propagation with no separate gather; ``sync`` orders rank 0's reads after every
+    rank's last store."""
+
+    def __init__(self, n_planes: int, plane_voxels: int, world: int, rank: int, device,
+                 group=None):
+        self.world, self.rank, self.group, self.device = world, rank, group, device
+        self.ranges = [shard_range(n_planes, world, r) for r in range(world)]
+        self.pv = plane_voxels
+        full = torch.zeros((1, n_planes * plane_voxels), dtype=torch.complex64, device=device) \
+            if rank == 0 else torch.zeros(1, dtype=torch.complex64, device=device)
+        self.full = full if rank == 0 else None
+        torch.cuda.synchronize(device)   # zeroed before any peer can write into it
+        handles = [None]
+        if rank == 0:
+            handles = [_ipc_handle(full)]
+        dist.broadcast_object_list(handles, src=0, group=group)
+        self._opened = None
+        if rank == 0:
+            base = full.data_ptr()
+        else:
+            base, self._opened = _ipc_open(handles[0])
+        lo, _ = self.ranges[rank]
+        self.out_ptr = base + 8 * lo * plane_voxels     # this shard's first plane in rank 0
+
+    def sync(self, stream=None):
+        stream_barrier(self.group, self.device, stream)
+        return self.full
+
+    def close(self):
+        from . import _lib
+        if self._opened:
+            _lib.call("pf_ipc_close", self._opened)
+            self._opened = None

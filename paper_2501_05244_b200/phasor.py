@@ -233,6 +233,15 @@ class _HostStager:
 _STAGERS: dict = {}
 
 
+def temporal_peers(plan: "TemporalPlan", hist: torch.Tensor, peers, stream=None) -> None:
+    """K1 of this rank's traces with the slice all-gather fused into its store
+    (``distributed.PeerSlices``): hist float32 [n_traces, T] of the rank's detectors."""
+    _lib.call("pf_temporal_dft_peers", dev.ptr(hist), hist.shape[0], plan.n_bins,
+              dev.ptr(plan.bins), dev.ptr(plan.tw), dev.ptr(plan.wphase), plan.n_freq,
+              plan.inner_mask, dev.ptr(peers.peers), peers.world, peers.peer_stride, peers.col,
+              dev.stream_ptr(stream))
+
+
 def to_frequency_device(histograms: torch.Tensor, kernel, t0: float = 0.0,
                         out: torch.Tensor | None = None, plan: TemporalPlan | None = None,
                         stream=None) -> torch.Tensor:

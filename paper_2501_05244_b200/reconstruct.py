@@ -213,7 +213,8 @@ class Propagator:
     def run_frequency(self, uhat_ptr: int, khat: float, ill_ptr: int, frame_w_ptr: int,
                       n_frames: int, vol: torch.Tensor, vol_frame_stride: int,
                       plane_lo: int = 0, plane_hi: int | None = None, stream=None,
-                      uhat_ptr_for_batch=None, lane: int = 0, horner=None) -> None:
+                      uhat_ptr_for_batch=None, lane: int = 0, horner=None,
+                      vol_out=None) -> None:
         """One frequency over planes [plane_lo, plane_hi).  horner=(dkhat, f, F): kernel C
         by Horner's rule (frequencies visited in ``freq_order``)."""
         plane_hi = self.nplanes if plane_hi is None else plane_hi
@@ -240,7 +241,8 @@ class Propagator:
                     wo = dev.ptr(wo_t)
                 # a nonzero status (geometry not eligible) raises PfError in _lib.call
                 _lib.call("pf_prop_rows_out_horner", pp, nb, khat, dk, mode, gref,
-                          self.plan_x.ref, wb, ill_ptr, frame_w_ptr, dev.ptr(vol), wo, B * dk, s)
+                          self.plan_x.ref, wb, ill_ptr, frame_w_ptr, dev.ptr(vol), wo, B * dk,
+                          vol_out, s)
                 continue
             _lib.call("pf_prop_rows_out", pp, nb, khat, gref, self.plan_x.ref, wb, ill_ptr,
                       frame_w_ptr, n_frames, dev.ptr(vol), vol_frame_stride, s)
@@ -452,21 +454,22 @@ class GraphedRun:
     pair; inputs and outputs are used in place.
     """
 
-    def run_graphed(self, coeff: torch.Tensor, vol: torch.Tensor, stream=None):
+    def run_graphed(self, coeff: torch.Tensor, vol: torch.Tensor, stream=None, vol_out=None):
         graphs = self.__dict__.setdefault("_graphs", {})
-        key = (coeff.data_ptr(), vol.data_ptr())
+        key = (coeff.data_ptr(), vol.data_ptr(), vol_out)
+        kw = {} if vol_out is None else {"vol_out": vol_out}
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
         g = graphs.get(key)
         if g is None:
             side = torch.cuda.Stream(device=self.device)
             side.wait_stream(main)
             with torch.cuda.stream(side):
-                self.run(coeff, vol, side)          # warm-up: plans, attributes, caches
+                self.run(coeff, vol, side, **kw)    # warm-up: plans, attributes, caches
             main.wait_stream(side)
             g = torch.cuda.CUDAGraph()
             n0 = _lib.launches()
             with torch.cuda.graph(g, stream=side):
-                self.run(coeff, vol, side)
+                self.run(coeff, vol, side, **kw)
             main.wait_stream(side)
             self.graph_kernels = _lib.launches() - n0   # libpfgpu launches per replay
             graphs[key] = g
@@ -627,12 +630,24 @@ class RsdEngine(GraphedRun):
         dev.fft2_natural(self.uhat, self.py, self.px, F * I, -1, 1.0, stream)
         return self.uhat
 
-    def run(self, coeff: torch.Tensor, vol: torch.Tensor | None = None, stream=None):
+    def fused_gather_ok(self) -> bool:
+        """Kernel C's final Horner step can store the finished planes elsewhere (the fused
+        volume gather of distributed.PeerVolume): register path, Horner geometry, no
+        frequency-batched launches."""
+        return (not self.prop.fbatch_ok(self.freqs.size, self.n_frames)
+                and self.prop.freq_order(self.freqs, self.n_frames)[1] is not None)
+
+    def run(self, coeff: torch.Tensor, vol: torch.Tensor | None = None, stream=None,
+            vol_out: int | None = None):
+        """``vol_out``: device address the finished planes go to instead of ``vol`` (rank 0's
+        volume at this shard's first plane, peer memory); ``vol`` then only accumulates."""
         if vol is None:
             vol = torch.zeros((self.n_frames, self.n_voxels), dtype=torch.complex64,
                               device=self.device)
         else:
             vol.zero_()
+        if vol_out is not None and not self.fused_gather_ok():
+            raise ValueError("the fused volume gather needs the Horner register path")
         uhat = self.relay_spectra(coeff, stream)
         per_f = self.n_illum * self.py * self.px
         if self.prop.fbatch_ok(self.freqs.size, self.n_frames):
@@ -650,7 +665,8 @@ class RsdEngine(GraphedRun):
                                         dev.ptr(self.frame_w) + 8 * fi * self.n_frames,
                                         self.n_frames, vol, self.n_voxels, plane_lo=b0,
                                         plane_hi=b1, stream=ls, lane=lane,
-                                        horner=None if dk is None else (dk, fi, len(order)))
+                                        horner=None if dk is None else (dk, fi, len(order)),
+                                        vol_out=vol_out)
 
         self.prop.run_batches(body, stream)
         return vol

@@ -198,3 +198,88 @@ def test_chunk_split_units():
         assert all(b > a for a, b in parts)
         assert all(b % u == 0 for _, b in parts[:-1])
     assert chunk_split(32, 3, 12) == [(0, 12), (12, 24), (24, 32)]
+
+
+def _peer_worker(rank, world, port, out_q):
+    """Two ranks on cuda:0 exchanging CUDA IPC mappings (the mechanism NVLink peers use):
+    K1 with the slice all-gather fused into its store, kernel C storing the finished planes
+    straight into rank 0's volume."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import importlib
+    R = importlib.import_module("paper_2501_05244_b200.reconstruct")
+    R._FBATCH_BYTES = 0                      # per-frequency launches (the config-4 sequence)
+    from paper_2501_05244_b200.distributed import PeerSlices, PeerVolume
+    from paper_2501_05244_b200.phasor import TemporalPlan, temporal_peers
+    from paper_2501_05244_b200.pipeline import _Meta
+    pf, g, hist, k, grid = _peer_scene()
+    dev = torch.device("cuda", 0)
+    D, nz, T = g.count, grid.grid.nz, hist.shape[-1]
+    d_lo, d_hi = shard_range(D, world, rank)
+    k_lo, k_hi = shard_range(nz, world, rank)
+    ps = PeerSlices(k.n_freq, 1, D, world, rank, dev)
+    pv = PeerVolume(nz, g.count, world, rank, dev)
+    h = torch.from_numpy(hist[0, d_lo:d_hi].copy()).to(dev)
+    temporal_peers(TemporalPlan(k, 1e-10, dev), h, ps)
+    full = ps.sync()
+    ill = pf.PointList(np.zeros((1, 2)))
+    eng = R.RsdEngine(_Meta(k, pf.UniformRelay(g), ill), grid, plane_range=(k_lo, k_hi),
+                      device=dev)
+    assert eng.fused_gather_ok()
+    vol = torch.zeros((1, eng.n_voxels), dtype=torch.complex64, device=dev)
+    eng.run_graphed(full, vol, vol_out=pv.out_ptr)
+    out = pv.sync()
+    if rank == 0:
+        out_q.put((full.cpu().numpy(), out.cpu().numpy()))
+    dist.barrier()
+    ps.close()
+    pv.close()
+    dist.destroy_process_group()
+
+
+def _peer_scene():
+    import paper_2501_05244_b200 as pf
+    rng = np.random.default_rng(9)
+    n, T, dt = 64, 2048, 8e-12
+    p = 2.0 / n
+    g = pf.UniformGrid2D(n, n, p, p, -1 + p / 2, -1 + p / 2, 0.0)
+    hist = rng.poisson(2.0, size=(1, n * n, T)).astype(np.float32)
+    k = pf.build_kernel(0.06, T, dt)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(n, n, 6, p, p, 0.2, g.x0, g.y0, 0.5))
+    return pf, g, hist, k, grid
+
+
+@pytest.mark.gpu
+def test_two_rank_peer_memory_collectives_match_single_gpu():
+    """The fused collectives (K1 writing every rank's slice buffer, kernel C writing rank 0's
+    volume, CUDA IPC mappings; two gloo ranks on cuda:0 only for the host handshake and the
+    barriers) give the single-process slices and volume bit for bit."""
+    import importlib
+    R = importlib.import_module("paper_2501_05244_b200.reconstruct")
+    from paper_2501_05244_b200.phasor import to_frequency_device
+    from paper_2501_05244_b200.pipeline import _Meta
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    full, vol = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    pf, g, hist, k, grid = _peer_scene()
+    dev = torch.device("cuda", 0)
+    coeff = to_frequency_device(torch.from_numpy(hist).to(dev), k, 1e-10)
+    ref_c = coeff.cpu().numpy()
+    bad = np.argwhere(full != ref_c)
+    assert bad.size == 0, (bad[:5].tolist(), len(bad), np.abs(full - ref_c).max())
+    keep = R._FBATCH_BYTES
+    R._FBATCH_BYTES = 0
+    try:
+        eng = R.RsdEngine(_Meta(k, pf.UniformRelay(g), pf.PointList(np.zeros((1, 2)))), grid,
+                          device=dev)
+        ref = eng.run(coeff).cpu().numpy()
+    finally:
+        R._FBATCH_BYTES = keep
+    assert np.array_equal(vol, ref)
