@@ -11,6 +11,7 @@ frequency-major complex64 tensor resident on the device for the propagators.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -189,17 +190,19 @@ class _HostStager:
     ring slot c % 2 is reused once its K1 has run.  Float64 payloads are narrowed to
     float32 by the same copy."""
 
-    CHUNK_BYTES = 64 << 20
-    THREADS = 8
+    CHUNK_BYTES = int(os.environ.get("PF_STAGE_MB", "64")) << 20
+    BUFS = int(os.environ.get("PF_STAGE_BUFS", "2"))
+    THREADS = int(os.environ.get("PF_STAGE_THREADS", "8"))
 
     def __init__(self, device):
         from concurrent.futures import ThreadPoolExecutor
         self.device = device
         n = self.CHUNK_BYTES // 4
-        self.pinned = [torch.empty((n,), dtype=torch.float32, pin_memory=True) for _ in range(2)]
-        self.ring = [torch.empty((n,), dtype=torch.float32, device=device) for _ in range(2)]
-        self.h2d_done = [torch.cuda.Event() for _ in range(2)]
-        self.k1_done = [torch.cuda.Event() for _ in range(2)]
+        nb = self.BUFS
+        self.pinned = [torch.empty((n,), dtype=torch.float32, pin_memory=True) for _ in range(nb)]
+        self.ring = [torch.empty((n,), dtype=torch.float32, device=device) for _ in range(nb)]
+        self.h2d_done = [torch.cuda.Event() for _ in range(nb)]
+        self.k1_done = [torch.cuda.Event() for _ in range(nb)]
         self.copy_stream = torch.cuda.Stream(device=device)
         self.pool = ThreadPoolExecutor(self.THREADS)
 
@@ -209,7 +212,7 @@ class _HostStager:
         main = torch.cuda.current_stream(self.device)
         th = self.THREADS
         for c, r0 in enumerate(range(0, n_tr, rows)):
-            k = c & 1
+            k = c % self.BUFS
             r1 = min(n_tr, r0 + rows)
             n = (r1 - r0) * T
             # pinned[k] no longer read by an earlier transfer (this call's or the previous
