@@ -195,10 +195,11 @@ def run_ours(args):
     peer = None
     if (world > 1 and os.environ.get("PF_PEER", "1") != "0" and I == 1 and T % 2048 == 0
             and hasattr(eng, "fused_gather_ok") and eng.fused_gather_ok()):
-        from paper_2501_05244_b200.distributed import PeerSlices, PeerVolume
+        from paper_2501_05244_b200.distributed import open_peer_collectives
         from paper_2501_05244_b200.phasor import temporal_peers
-        peer = (PeerSlices(F, I, D, world, rank, device), PeerVolume(nz, plane_vox, world, rank,
-                                                                     device))
+        # every rank maps the others' buffers; if any rank cannot (no peer access), all fall
+        # back to the NCCL gathers together
+        peer = open_peer_collectives(F, I, D, nz, plane_vox, world, rank, device)
 
     final = {}
 

@@ -204,17 +204,32 @@ class PeerSlices:
         self.ranges = [shard_range(n_det, world, r) for r in range(world)]
         self.full = torch.zeros((n_freq, n_illum, n_det), dtype=torch.complex64, device=device)
         torch.cuda.synchronize(device)   # zeroed before any peer can write into it
+        # every rank reaches every collective of the handshake; failures only clear self.ok
+        # (open_peer_collectives agrees on the outcome across ranks)
+        self.ok, self.error = True, None
+        try:
+            mine = _ipc_handle(self.full)
+        except Exception as e:
+            mine, self.ok, self.error = None, False, e
         handles = [None] * world
-        dist.all_gather_object(handles, _ipc_handle(self.full), group=group)
+        dist.all_gather_object(handles, mine, group=group)
         self._opened = []
         ptrs = []
         for r, h in enumerate(handles):
             if r == rank:
                 ptrs.append(self.full.data_ptr())
-            else:
+                continue
+            if h is None or not self.ok:
+                self.ok = False
+                ptrs.append(0)
+                continue
+            try:
                 p, base = _ipc_open(h)
                 self._opened.append(base)
                 ptrs.append(p)
+            except Exception as e:
+                self.ok, self.error = False, e
+                ptrs.append(0)
         self.peers = torch.tensor(ptrs, dtype=torch.int64, device=device)
         lo, _ = self.ranges[rank]
         # column of this rank's first trace in the [F][I*D] view (illumination-major rows)
@@ -249,15 +264,25 @@ class PeerVolume:
             if rank == 0 else torch.zeros(1, dtype=torch.complex64, device=device)
         self.full = full if rank == 0 else None
         torch.cuda.synchronize(device)   # zeroed before any peer can write into it
+        self.ok, self.error = True, None
         handles = [None]
         if rank == 0:
-            handles = [_ipc_handle(full)]
+            try:
+                handles = [_ipc_handle(full)]
+            except Exception as e:
+                self.ok, self.error = False, e
         dist.broadcast_object_list(handles, src=0, group=group)
         self._opened = None
+        base = 0
         if rank == 0:
             base = full.data_ptr()
+        elif handles[0] is None:
+            self.ok = False
         else:
-            base, self._opened = _ipc_open(handles[0])
+            try:
+                base, self._opened = _ipc_open(handles[0])
+            except Exception as e:
+                self.ok, self.error = False, e
         lo, _ = self.ranges[rank]
         self.out_ptr = base + 8 * lo * plane_voxels     # this shard's first plane in rank 0
 
@@ -270,3 +295,26 @@ class PeerVolume:
         if self._opened:
             _lib.call("pf_ipc_close", self._opened)
             self._opened = None
+
+
+def open_peer_collectives(n_freq, n_illum, n_det, n_planes, plane_voxels, world, rank, device,
+                          group=None):
+    """(PeerSlices, PeerVolume) when every rank can map the others' buffers, else None on
+    every rank (the decision is all-reduced so no rank is left waiting in a collective the
+    others skipped).  The reason a rank failed is printed once."""
+    made = (PeerSlices(n_freq, n_illum, n_det, world, rank, device, group),
+            PeerVolume(n_planes, plane_voxels, world, rank, device, group))
+    good = all(m.ok for m in made)
+    err = next((m.error for m in made if m.error is not None), None)
+    ok = torch.tensor([1 if good else 0], dtype=torch.int32)
+    if dist.get_backend(group) != "gloo":
+        ok = ok.to(device)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    if int(ok.item()) == 1:
+        return made
+    for m in made:
+        m.close()
+    if err is not None:
+        print(f"peer-memory collectives unavailable on rank {rank}: {err}; using NCCL",
+              flush=True)
+    return None
