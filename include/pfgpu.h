@@ -413,6 +413,33 @@ int64_t pf_srsd_workspace_bytes(const pf_srsd_args* args);
 int pf_srsd(const pf_srsd_args* args, const void* slices, void* vol, void* ws, int64_t ws_bytes,
             void* stream);
 
+/* nursd1 (reference reconstruct.py:335-385, nursd1(slices, grid, eps, times, threads,
+ * include_illumination)) in one call: detections scattered on the plane z = relay_z
+ * (relay_xy host [n_points][2], x then y) -> cuboid grid, via a type-1 NUFFT at accuracy
+ * eps onto the padded lattice spectrum and the rsd propagation.  slices: device
+ * [F][I][n_points] c64 (a frequency-major transpose of FrequencySlices.coefficients);
+ * vol: device [frames][nz*ny*nx] c64.  Pad: the reference rule when a detection is off
+ * the voxel lattice (the result depends on it), else the exact pad.  Same conventions
+ * as pf_rsd otherwise. */
+typedef struct pf_nursd1_args {
+  int n_points;
+  const double* relay_xy;
+  double relay_z;
+  int nx, ny, nz;
+  double dx, dy, dz, x0, y0, z0;
+  int n_freq, n_illum;
+  const double* frequencies;
+  const double* ill_xyz;
+  int n_frames;
+  const double* times;
+  double eps;
+  int include_illum;
+} pf_nursd1_args;
+
+int64_t pf_nursd1_workspace_bytes(const pf_nursd1_args* args);
+int pf_nursd1(const pf_nursd1_args* args, const void* slices, void* vol, void* ws,
+              int64_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,6 +69,17 @@ class PfSrsdArgs(ctypes.Structure):
                 ("include_illum", ctypes.c_int)]
 
 
+class PfNursd1Args(ctypes.Structure):
+    _fields_ = [("n_points", ctypes.c_int), ("relay_xy", ctypes.c_void_p),
+                ("relay_z", ctypes.c_double), ("nx", ctypes.c_int), ("ny", ctypes.c_int),
+                ("nz", ctypes.c_int), ("dx", ctypes.c_double), ("dy", ctypes.c_double),
+                ("dz", ctypes.c_double), ("x0", ctypes.c_double), ("y0", ctypes.c_double),
+                ("z0", ctypes.c_double), ("n_freq", ctypes.c_int), ("n_illum", ctypes.c_int),
+                ("frequencies", ctypes.c_void_p), ("ill_xyz", ctypes.c_void_p),
+                ("n_frames", ctypes.c_int), ("times", ctypes.c_void_p),
+                ("eps", ctypes.c_double), ("include_illum", ctypes.c_int)]
+
+
 _vp, _i, _i64, _d, _f = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_float
 _P = ctypes.POINTER
 
@@ -87,6 +98,8 @@ _SIGNATURES = {
     "pf_rsd": [_P(PfRsdArgs), _vp, _vp, _vp, _i64, _vp],
     "pf_srsd_workspace_bytes": [_P(PfSrsdArgs)],
     "pf_srsd": [_P(PfSrsdArgs), _vp, _vp, _vp, _i64, _vp],
+    "pf_nursd1_workspace_bytes": [_P(PfNursd1Args)],
+    "pf_nursd1": [_P(PfNursd1Args), _vp, _vp, _vp, _i64, _vp],
     "pf_nufft_type1_finish_pow2": [_P(PfNufftGeom), _vp, _i64, _i, _vp, _P(PfFftPlan),
                                    _P(PfFftPlan), _vp, _vp, _vp, _i64, _vp],
     "pf_relay_spectra_fast": [_vp, _i64, _i, _i, _i64, _vp, _i, _P(PfFftPlan), _vp],
@@ -133,7 +146,7 @@ _SIGNATURES = {
 }
 _RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
              "pf_prop_ws_spectrum": ctypes.c_int64, "pf_rsd_workspace_bytes": ctypes.c_int64,
-             "pf_srsd_workspace_bytes": ctypes.c_int64,
+             "pf_srsd_workspace_bytes": ctypes.c_int64, "pf_nursd1_workspace_bytes": ctypes.c_int64,
              "pf_prop_fast": ctypes.c_int}
 
 _lib = None

@@ -114,3 +114,117 @@ inline pf_fft_plan make_plan(long n, const void* tw_dev, size_t n_tw) {
 }
 
 }  // namespace pfalgo
+
+namespace pfalgo {
+
+// plane batch of the propagation loop (reconstruct.Propagator): ws_a + ws_b within
+// BATCH_BYTES; register path: a multiple of 4 (32 / L) planes, at most 4 (32 / L)
+inline int prop_batch(const pf_prop_geom* g, int nz, bool fast) {
+  const int64_t per = 8 * ((int64_t)(g->py / 2 + 1) * (g->px / 2 + 1) +
+                           (int64_t)g->n_illum * g->ny * g->px);
+  int batch = (int)fmax(1.0, fmin((double)nz, (double)(BATCH_BYTES / per)));
+  if (fast) {
+    const int l = g->px / 32, q = 4 * (32 / l);
+    int b = (batch / q) * q;
+    if (b < q) b = q;
+    batch = b;
+    if (batch > 4 * (32 / l)) batch = 4 * (32 / l);
+    if (batch > nz) batch = nz;
+  }
+  return batch;
+}
+
+// Horner's rule in kernel C: register path, centred crops, one illumination, one frame,
+// uniformly spaced frequencies (reconstruct.Propagator.freq_order); *dkhat = spacing / c
+inline bool horner_ok(const pf_prop_geom* g, bool fast, const double* freqs, int F,
+                      int n_frames, int include_illum, double* dkhat) {
+  if (!(fast && F >= 2 && n_frames <= 1 && g->n_illum == 1 && include_illum &&
+        2 * g->nx == g->px && 2 * g->ny == g->py && 2 * g->nu0x == -g->nx &&
+        2 * g->nu0y == -g->ny))
+    return false;
+  const double d0 = freqs[1] - freqs[0];
+  for (int f = 1; f < F; f++)
+    if (fabs((freqs[f] - freqs[f - 1]) - d0) > 1e-9 * fabs(d0)) return false;
+  *dkhat = d0 / C_LIGHT;
+  return true;
+}
+
+// The per plane batch, per frequency A / fused B / C launches of the propagation, plane
+// batches round-robin over `lanes` streams forked from and joined back to `st`.
+// uhat: [F][I][P^2] relay spectra; vol: [frames][V] (accumulated into, zeroed by the caller).
+struct PropLoop {
+  const pf_prop_geom* g;
+  const pf_fft_plan* plx;
+  const pf_fft_plan* ply;
+  const pf_plane* planes;   // device [nz]
+  int nz, batch, lanes, frames;
+  const double* ill;        // device [I][3]
+  const float2* fw;         // device [F][frames]
+  bool horner;
+  double dkhat;
+  char* wa;                 // device lanes x pf_prop_ws_a(g, batch) c64
+  char* wb;                 // device lanes x pf_prop_ws_b(g, batch) c64
+  char* wo;                 // device lanes x batch x nx x ny c64 (Horner blocks), or null
+};
+
+inline int prop_loop(const PropLoop& p, const float2* uhat, const double* freqs, int F,
+                     void* vol, int64_t V, cudaStream_t st) {
+  const pf_prop_geom& g = *p.g;
+  cudaStream_t lane_st[LANES];
+  cudaEvent_t ev_fork, ev_join[LANES];
+  PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "prop: event");
+  PF_CUDA_CHECK(cudaEventRecord(ev_fork, st), "prop: event");
+  for (int l = 0; l < p.lanes; l++) {
+    PF_CUDA_CHECK(cudaStreamCreateWithFlags(&lane_st[l], cudaStreamNonBlocking), "prop: stream");
+    PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join[l], cudaEventDisableTiming), "prop: event");
+    PF_CUDA_CHECK(cudaStreamWaitEvent(lane_st[l], ev_fork, 0), "prop: fork");
+  }
+  const int64_t per_f = (int64_t)g.n_illum * g.px * g.py;
+  const int64_t wa_n = pf_prop_ws_a(&g, p.batch), wb_n = pf_prop_ws_b(&g, p.batch);
+  const int64_t wo_n = (int64_t)p.batch * g.nx * g.ny;
+  int rc = 0;
+  for (int b0 = 0, bi = 0; b0 < p.nz && rc == 0; b0 += p.batch, bi++) {
+    const int lane = bi % p.lanes;
+    void* ls = (void*)lane_st[lane];
+    const int nb = p.nz - b0 < p.batch ? p.nz - b0 : p.batch;
+    const pf_plane* pp = p.planes + b0;
+    float2* wa = (float2*)p.wa + lane * wa_n;
+    float2* wb = (float2*)p.wb + lane * wb_n;
+    float2* wo = p.wo ? (float2*)p.wo + lane * wo_n : nullptr;
+    for (int s = 0; s < F && rc == 0; s++) {
+      const int f = p.horner ? F - 1 - s : s;   // Horner: descending frequencies
+      const double khat = freqs[f] / C_LIGHT;
+      const float2* uh = uhat + f * per_f;
+      rc = pf_prop_kernel_rows(pp, nb, khat, &g, p.plx, wa, ls);
+      if (rc == 0) rc = pf_prop_columns(pp, nb, &g, p.ply, wa, uh, wb, 0, ls);
+      if (rc != 0) break;
+      if (p.horner) {
+        int mode;
+        if (F <= HORNER_BLOCK) {
+          mode = f == 0 ? 2 : 1;
+        } else {
+          mode = f == 0 ? 4 : (f % HORNER_BLOCK == 0 ? 3 : 1);
+          if (f == F - 1)
+            PF_CUDA_CHECK(cudaMemsetAsync(wo, 0, 8 * (size_t)nb * g.nx * g.ny, lane_st[lane]),
+                          "prop: zero");
+        }
+        rc = pf_prop_rows_out_horner(pp, nb, khat, p.dkhat, mode, &g, p.plx, wb, p.ill,
+                                     p.fw + (int64_t)f * p.frames, vol, wo,
+                                     HORNER_BLOCK * p.dkhat, nullptr, ls);
+      } else {
+        rc = pf_prop_rows_out(pp, nb, khat, &g, p.plx, wb, p.ill, p.fw + (int64_t)f * p.frames,
+                              p.frames, vol, V, ls);
+      }
+    }
+  }
+  for (int l = 0; l < p.lanes; l++) {
+    cudaEventRecord(ev_join[l], lane_st[l]);
+    cudaStreamWaitEvent(st, ev_join[l], 0);
+    cudaEventDestroy(ev_join[l]);
+    cudaStreamDestroy(lane_st[l]);
+  }
+  cudaEventDestroy(ev_fork);
+  return rc;
+}
+
+}  // namespace pfalgo

@@ -103,33 +103,13 @@ int plan(const pf_rsd_args* a, Layout* L) {
   L->nu0x = nu0x;
   L->nu0y = nu0y;
   L->fast = pf_prop_fast(&g) != 0;
-  // plane batch (reconstruct.Propagator): ws_a + ws_b within 64 MB; register path: a
-  // multiple of 4 (32 / L) planes, at most 4 (32 / L)
-  const int64_t per = 8 * ((int64_t)(py / 2 + 1) * (px / 2 + 1) + (int64_t)a->n_illum * a->ny * px);
-  int batch = (int)fmax(1.0, fmin((double)a->nz, (double)(BATCH_BYTES / per)));
-  if (L->fast) {
-    const int l = (int)(px / 32), q = 4 * (32 / l);
-    int b = (batch / q) * q;
-    if (b < q) b = q;
-    batch = b;
-    if (batch > 4 * (32 / l)) batch = 4 * (32 / l);
-    if (batch > a->nz) batch = a->nz;
-  }
-  L->batch = batch;
-  const int nb = (a->nz + batch - 1) / batch;
+  L->batch = prop_batch(&g, a->nz, L->fast);
+  const int nb = (a->nz + L->batch - 1) / L->batch;
   L->lanes = nb < LANES ? nb : LANES;
-  // Horner's rule in C: register path, centred crops, one illumination, one frame,
-  // uniformly spaced frequencies
   const int F = a->n_freq;
-  L->horner = L->fast && F >= 2 && a->n_frames <= 1 && a->n_illum == 1 && a->include_illum &&
-              2 * a->nx == px && 2 * a->ny == py && 2 * nu0x == -a->nx && 2 * nu0y == -a->ny;
-  if (L->horner) {
-    const double d0 = a->frequencies[1] - a->frequencies[0];
-    for (int f = 1; f < F; f++)
-      if (fabs((a->frequencies[f] - a->frequencies[f - 1]) - d0) > 1e-9 * fabs(d0))
-        L->horner = false;
-    L->dkhat = d0 / C_LIGHT;
-  }
+  L->dkhat = 0.0;
+  L->horner = horner_ok(&g, L->fast, a->frequencies, F, a->n_frames, a->include_illum, &L->dkhat);
+  const int batch = L->batch;
   const int frames = a->n_frames > 0 ? a->n_frames : 1;
   L->n_twx = (int64_t)twiddles(px).size();
   L->n_twy = py == px ? 0 : (int64_t)twiddles(py).size();
@@ -236,63 +216,9 @@ extern "C" int pf_rsd(const pf_rsd_args* a, const void* slices, void* vol, void*
                         -1, 1.0f, stream);
   }
   if (rc != 0) return rc;
-  // ---- lanes forked from the caller's stream
-  cudaStream_t lane_st[LANES];
-  cudaEvent_t ev_fork, ev_join[LANES];
-  PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "pf_rsd: event");
-  PF_CUDA_CHECK(cudaEventRecord(ev_fork, st), "pf_rsd: event");
-  for (int l = 0; l < L.lanes; l++) {
-    PF_CUDA_CHECK(cudaStreamCreateWithFlags(&lane_st[l], cudaStreamNonBlocking), "pf_rsd: stream");
-    PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join[l], cudaEventDisableTiming), "pf_rsd: event");
-    PF_CUDA_CHECK(cudaStreamWaitEvent(lane_st[l], ev_fork, 0), "pf_rsd: fork");
-  }
-  const pf_plane* planes_d = (const pf_plane*)(w + L.off_planes);
-  const double* ill_d = (const double*)(w + L.off_ill);
-  const float2* fw_d = (const float2*)(w + L.off_fw);
-  const int64_t per_f = (int64_t)I * L.px * L.py;
-  const int64_t wa_n = pf_prop_ws_a(&g, L.batch), wb_n = pf_prop_ws_b(&g, L.batch);
-  const int64_t wo_n = (int64_t)L.batch * a->nx * a->ny;
-  rc = 0;
-  for (int b0 = 0, bi = 0; b0 < a->nz && rc == 0; b0 += L.batch, bi++) {
-    const int lane = bi % L.lanes;
-    void* ls = (void*)lane_st[lane];
-    const int nb = a->nz - b0 < L.batch ? a->nz - b0 : L.batch;
-    const pf_plane* pp = planes_d + b0;
-    float2* wa = (float2*)(w + L.off_wa) + lane * wa_n;
-    float2* wb = (float2*)(w + L.off_wb) + lane * wb_n;
-    float2* wo = (float2*)(w + L.off_wo) + lane * wo_n;
-    for (int s = 0; s < F && rc == 0; s++) {
-      const int f = L.horner ? F - 1 - s : s;   // Horner: descending frequencies
-      const double khat = a->frequencies[f] / C_LIGHT;
-      const float2* uh = uhat + f * per_f;
-      rc = pf_prop_kernel_rows(pp, nb, khat, &g, &plx, wa, ls);
-      if (rc == 0) rc = pf_prop_columns(pp, nb, &g, &ply, wa, uh, wb, 0, ls);
-      if (rc != 0) break;
-      if (L.horner) {
-        int mode;
-        if (F <= HORNER_BLOCK) {
-          mode = f == 0 ? 2 : 1;
-        } else {
-          mode = f == 0 ? 4 : (f % HORNER_BLOCK == 0 ? 3 : 1);
-          if (f == F - 1)
-            PF_CUDA_CHECK(cudaMemsetAsync(wo, 0, 8 * (size_t)nb * a->nx * a->ny, lane_st[lane]),
-                          "pf_rsd: zero");
-        }
-        rc = pf_prop_rows_out_horner(pp, nb, khat, L.dkhat, mode, &g, &plx, wb, ill_d,
-                                     fw_d + (int64_t)f * frames, vol, wo,
-                                     HORNER_BLOCK * L.dkhat, nullptr, ls);
-      } else {
-        rc = pf_prop_rows_out(pp, nb, khat, &g, &plx, wb, ill_d, fw_d + (int64_t)f * frames,
-                              frames, vol, V, ls);
-      }
-    }
-  }
-  for (int l = 0; l < L.lanes; l++) {
-    cudaEventRecord(ev_join[l], lane_st[l]);
-    cudaStreamWaitEvent(st, ev_join[l], 0);
-    cudaEventDestroy(ev_join[l]);
-    cudaStreamDestroy(lane_st[l]);
-  }
-  cudaEventDestroy(ev_fork);
-  return rc;
+  PropLoop p{&g, &plx, &ply, (const pf_plane*)(w + L.off_planes), a->nz, L.batch, L.lanes,
+             frames, (const double*)(w + L.off_ill), (const float2*)(w + L.off_fw), L.horner,
+             L.dkhat, w + L.off_wa, w + L.off_wb,
+             (L.horner && F > HORNER_BLOCK) ? w + L.off_wo : nullptr};
+  return prop_loop(p, uhat, a->frequencies, F, vol, V, st);
 }

@@ -1,8 +1,9 @@
-"""The whole-algorithm C entry points pf_rsd and pf_srsd (include/pfgpu.h), called the way a reference-side
+"""The whole-algorithm C entry points pf_rsd, pf_srsd and pf_nursd1 (include/pfgpu.h), called the way a reference-side
 ctypes binding would call it: host geometry and frequency arrays, device
 slices / volume / workspace pointers, the caller's stream.  CPU tests cover the planning
 and the reference's validation messages (no device needed); GPU tests compare the result
-with the float64 oracle (reference rsd, reconstruct.py:208-268) and with the Python engine.
+with the float64 oracle (reference rsd / srsd / nursd1, reconstruct.py:208-385) and with
+the Python engine.
 """
 
 import ctypes
@@ -201,3 +202,97 @@ def test_pf_srsd_video(rng):
     times = np.array([0.0, 2e-10])
     got = capi_srsd(sl, fr, times=times)
     assert O.rel_l2(got, O.srsd(sl, fr, times=times)) < TOL
+
+
+# ---------------------------------------------------------------- pf_nursd1
+
+def nursd1_args(slices, grid, eps=1e-6, times=None, include_illumination=True):
+    vg = grid.grid
+    xy = np.ascontiguousarray(np.asarray(slices.relay.points.points)[:, :2], dtype=np.float64)
+    freqs = np.ascontiguousarray(slices.frequencies, dtype=np.float64)
+    ill = np.ascontiguousarray(illumination_coordinates(slices.relay, slices.illuminations),
+                               dtype=np.float64)
+    t = None if times is None else np.ascontiguousarray(times, dtype=np.float64)
+    a = _lib.PfNursd1Args(n_points=xy.shape[0], relay_xy=xy.ctypes.data, relay_z=slices.relay.z,
+                          nx=vg.nx, ny=vg.ny, nz=vg.nz, dx=vg.dx, dy=vg.dy, dz=vg.dz, x0=vg.x0,
+                          y0=vg.y0, z0=vg.z0, n_freq=freqs.size, n_illum=ill.shape[0],
+                          frequencies=freqs.ctypes.data, ill_xyz=ill.ctypes.data,
+                          n_frames=0 if t is None else t.size,
+                          times=None if t is None else t.ctypes.data, eps=eps,
+                          include_illum=int(bool(include_illumination)))
+    return a, (xy, freqs, ill, t)
+
+
+def capi_nursd1(slices, grid, **kw):
+    import torch
+    a, keep = nursd1_args(slices, grid, **kw)
+    lib = _lib.load()
+    nbytes = lib.pf_nursd1_workspace_bytes(ctypes.byref(a))
+    assert nbytes > 0, _lib.last_error()
+    c = np.asarray(slices.coefficients)
+    coeff = torch.from_numpy(np.ascontiguousarray(c.transpose(2, 0, 1)).astype(np.complex64)).cuda()
+    vol = torch.empty((max(1, a.n_frames), grid.count), dtype=torch.complex64, device="cuda")
+    ws = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+    rc = lib.pf_nursd1(ctypes.byref(a), coeff.data_ptr(), vol.data_ptr(), ws.data_ptr(), nbytes,
+                       torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    return vol.cpu().numpy()
+
+
+def _scatter_scene(rng, n=64, n_pts=2048, F=2, n_ill=1, nz=3, lattice=False):
+    p = 2.0 / n
+    if lattice:
+        g = pf.UniformGrid2D(n, n, p, p, -1 + p / 2, -1 + p / 2, 0.0)
+        xy = pf.grid_coordinates(g).points
+        xy = xy[rng.random(xy.shape[0]) < 0.5]
+    else:
+        xy = rng.uniform(-1.0, 1.0, size=(n_pts, 2))
+    relay = pf.NonUniformPlanarRelay(pf.PointList(xy), 0.0)
+    freqs = 2 * np.pi * 3e8 / 0.06 * (1 + 0.02 * np.arange(F))
+    c = rng.normal(size=(n_ill, relay.count, F)) + 1j * rng.normal(size=(n_ill, relay.count, F))
+    ill = pf.PointList(rng.uniform(-0.3, 0.3, size=(n_ill, 2)))
+    sl = pf.FrequencySlices(freqs, c, relay, ill)
+    grid = pf.CuboidGrid(pf.UniformGrid3D(n, n, nz, p, p, 0.3, -1 + p / 2, -1 + p / 2, 0.5))
+    return sl, grid
+
+
+def test_nursd1_workspace_and_validation(rng):
+    sl, grid = _scatter_scene(rng)
+    a, keep = nursd1_args(sl, grid)
+    lib = _lib.load()
+    n = lib.pf_nursd1_workspace_bytes(ctypes.byref(a))
+    # off-lattice points: the reference pad P = 140, fine grid 280 x 280, F x I = 2
+    assert n > 2 * 8 * (280 * 280 + 140 * 140)
+    a.eps = 1.0
+    assert lib.pf_nursd1_workspace_bytes(ctypes.byref(a)) == -1
+    assert "accuracy target" in _lib.last_error()
+    a.eps = 1e-6
+    a.z0 = -0.5
+    assert lib.pf_nursd1_workspace_bytes(ctypes.byref(a)) == -1
+    assert "beyond the relay" in _lib.last_error()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [
+    dict(),                           # off-lattice: reference pad P = 140, generic path
+    dict(n_ill=2, F=3),               # two illuminations
+    dict(lattice=True),               # on-lattice: P = 128 register path, pow2 type-1 finish, Horner C
+    dict(lattice=True, F=40),         # Horner in 32-frequency blocks
+    dict(kw=dict(eps=1e-9)),          # tighter stencil (w = 11)
+])
+def test_pf_nursd1_matches_oracle_and_engine(rng, case):
+    kw = case.pop("kw", {})
+    sl, grid = _scatter_scene(rng, **case)
+    got = capi_nursd1(sl, grid, **kw)[0]
+    assert O.rel_l2(got, O.nursd1(sl, grid, **kw)) < TOL
+    assert O.rel_l2(got, pf.nursd1(sl, grid, **kw).field) < 1e-5
+
+
+@pytest.mark.gpu
+def test_pf_nursd1_video_without_illumination(rng):
+    sl, grid = _scatter_scene(rng, n=32, n_pts=512, F=3)
+    times = np.array([0.0, 2e-10])
+    got = capi_nursd1(sl, grid, times=times, include_illumination=False)
+    ref = O.nursd1(sl, grid, times=times, include_illumination=False)
+    assert O.rel_l2(got, ref) < TOL
