@@ -6,6 +6,7 @@ arithmetic kernel on the path lives in ``libpfgpu.so``.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import math
 import os
@@ -229,3 +230,14 @@ def phase_factors(omega: np.ndarray, times: np.ndarray) -> np.ndarray:
 
 def pow2_ceil(x: int) -> int:
     return 1 << max(0, math.ceil(math.log2(max(1, x))))
+
+
+@contextlib.contextmanager
+def nvtx(name: str):
+    """NVTX range around a host scope (pipeline stages show up named in a profiler's
+    timeline; free when none is attached)."""
+    torch.cuda.nvtx.range_push(name)
+    try:
+        yield
+    finally:
+        torch.cuda.nvtx.range_pop()

@@ -8,6 +8,8 @@
 
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "xfft.cuh"
 
 namespace pfalgo {
@@ -98,6 +100,13 @@ inline std::vector<float2> twiddles(long n) {
   return w;
 }
 
+
+// NVTX range over a host scope (a profiler shows the C entry points' phases; no cost
+// without one attached)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
 

@@ -260,6 +260,7 @@ extern "C" int64_t pf_nursd1_workspace_bytes(const pf_nursd1_args* a) {
 
 extern "C" int pf_nursd1(const pf_nursd1_args* a, const void* slices, void* vol, void* ws,
                          int64_t ws_bytes, void* stream) {
+  Nvtx range("pf_nursd1");
   Plan P;
   if (plan(a, &P) != 0) return -1;
   PF_ARG_CHECK(slices && vol && ws && ws_bytes >= P.total,

@@ -138,6 +138,7 @@ extern "C" int64_t pf_rsd_workspace_bytes(const pf_rsd_args* a) {
 
 extern "C" int pf_rsd(const pf_rsd_args* a, const void* slices, void* vol, void* ws,
                       int64_t ws_bytes, void* stream) {
+  Nvtx range("pf_rsd");
   Layout L;
   if (plan(a, &L) != 0) return -1;
   PF_ARG_CHECK(slices && vol && ws && ws_bytes >= L.total,

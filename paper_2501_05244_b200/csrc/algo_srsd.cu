@@ -155,6 +155,7 @@ extern "C" int64_t pf_srsd_workspace_bytes(const pf_srsd_args* a) {
 
 extern "C" int pf_srsd(const pf_srsd_args* a, const void* slices, void* vol, void* ws,
                        int64_t ws_bytes, void* stream) {
+  Nvtx range("pf_srsd");
   SLayout L;
   if (splan(a, &L) != 0) return -1;
   PF_ARG_CHECK(slices && vol && ws && ws_bytes >= L.total,

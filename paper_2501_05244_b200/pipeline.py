@@ -157,27 +157,31 @@ class TransientReconstructor:
         out = self.coeff.view(self.kernel.n_freq, n_tr)
         main = torch.cuda.current_stream(self.device)
         step = (n_tr + self.chunks - 1) // self.chunks
-        for c0 in range(0, n_tr, step):
-            c1 = min(n_tr, c0 + step)
-            with torch.cuda.stream(self.copy_stream):
-                dst[c0:c1].copy_(src[c0:c1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(self.copy_stream)
-            main.wait_event(ev)
-            self.temporal.run(dst[c0:c1], out[:, c0:c1], main)
-        coeff = self.slice_gather(self.coeff) if self.slice_gather is not None else self.coeff
+        with dev.nvtx("pf: h2d + K1"):
+            for c0 in range(0, n_tr, step):
+                c1 = min(n_tr, c0 + step)
+                with torch.cuda.stream(self.copy_stream):
+                    dst[c0:c1].copy_(src[c0:c1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(self.copy_stream)
+                main.wait_event(ev)
+                self.temporal.run(dst[c0:c1], out[:, c0:c1], main)
+        with dev.nvtx("pf: slice gather"):
+            coeff = self.slice_gather(self.coeff) if self.slice_gather is not None else self.coeff
         vol = self.vol
-        if self.gather_chunks > 1:
-            vol = self.propagate_and_gather(coeff, self.vol, main)
-        else:
-            self.propagate(coeff, main)
-            if self.volume_gather is not None:
-                vol = self.volume_gather(self.vol)      # full volume on rank 0, None elsewhere
+        with dev.nvtx("pf: propagation + volume gather"):
+            if self.gather_chunks > 1:
+                vol = self.propagate_and_gather(coeff, self.vol, main)
+            else:
+                self.propagate(coeff, main)
+                if self.volume_gather is not None:
+                    vol = self.volume_gather(self.vol)   # full volume on rank 0, None elsewhere
         if self.volume_gather is not None and vol is None:
             main.synchronize()
             return None
-        self._vol_host.copy_(vol, non_blocking=True)
-        main.synchronize()
+        with dev.nvtx("pf: d2h"):
+            self._vol_host.copy_(vol, non_blocking=True)
+            main.synchronize()
         return self._vol_host
 
     # -- pipelined streaming of successive captures -----------------------------------
