@@ -440,6 +440,33 @@ int64_t pf_nursd1_workspace_bytes(const pf_nursd1_args* args);
 int pf_nursd1(const pf_nursd1_args* args, const void* slices, void* vol, void* ws,
               int64_t ws_bytes, void* stream);
 
+/* nursd2 (reference reconstruct.py:413-459, nursd2(slices, grid, eps, times, threads,
+ * include_illumination)) in one call: detections on a uniform relay lattice -> explicit
+ * voxels on planes of constant depth (ExplicitGrid: plane_z / plane_count host
+ * [n_planes], voxel_xy host [sum plane_count][2], plane-major, x then y).  slices:
+ * device [F][I][relay_ny*relay_nx] c64; vol: device [frames][sum plane_count] c64 in
+ * the grid's voxel order.  Reference pad rule; type-2 NUFFT at accuracy eps.  Same
+ * conventions as pf_rsd otherwise. */
+typedef struct pf_nursd2_args {
+  int relay_nx, relay_ny;
+  double relay_dx, relay_dy, relay_x0, relay_y0, relay_z;
+  int n_planes;
+  const double* plane_z;
+  const int64_t* plane_count;
+  const double* voxel_xy;
+  int n_freq, n_illum;
+  const double* frequencies;
+  const double* ill_xyz;
+  int n_frames;
+  const double* times;
+  double eps;
+  int include_illum;
+} pf_nursd2_args;
+
+int64_t pf_nursd2_workspace_bytes(const pf_nursd2_args* args);
+int pf_nursd2(const pf_nursd2_args* args, const void* slices, void* vol, void* ws,
+              int64_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

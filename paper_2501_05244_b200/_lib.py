@@ -80,6 +80,19 @@ class PfNursd1Args(ctypes.Structure):
                 ("eps", ctypes.c_double), ("include_illum", ctypes.c_int)]
 
 
+class PfNursd2Args(ctypes.Structure):
+    _fields_ = [("relay_nx", ctypes.c_int), ("relay_ny", ctypes.c_int),
+                ("relay_dx", ctypes.c_double), ("relay_dy", ctypes.c_double),
+                ("relay_x0", ctypes.c_double), ("relay_y0", ctypes.c_double),
+                ("relay_z", ctypes.c_double), ("n_planes", ctypes.c_int),
+                ("plane_z", ctypes.c_void_p), ("plane_count", ctypes.c_void_p),
+                ("voxel_xy", ctypes.c_void_p), ("n_freq", ctypes.c_int),
+                ("n_illum", ctypes.c_int), ("frequencies", ctypes.c_void_p),
+                ("ill_xyz", ctypes.c_void_p), ("n_frames", ctypes.c_int),
+                ("times", ctypes.c_void_p), ("eps", ctypes.c_double),
+                ("include_illum", ctypes.c_int)]
+
+
 _vp, _i, _i64, _d, _f = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_float
 _P = ctypes.POINTER
 
@@ -100,6 +113,8 @@ _SIGNATURES = {
     "pf_srsd": [_P(PfSrsdArgs), _vp, _vp, _vp, _i64, _vp],
     "pf_nursd1_workspace_bytes": [_P(PfNursd1Args)],
     "pf_nursd1": [_P(PfNursd1Args), _vp, _vp, _vp, _i64, _vp],
+    "pf_nursd2_workspace_bytes": [_P(PfNursd2Args)],
+    "pf_nursd2": [_P(PfNursd2Args), _vp, _vp, _vp, _i64, _vp],
     "pf_nufft_type1_finish_pow2": [_P(PfNufftGeom), _vp, _i64, _i, _vp, _P(PfFftPlan),
                                    _P(PfFftPlan), _vp, _vp, _vp, _i64, _vp],
     "pf_relay_spectra_fast": [_vp, _i64, _i, _i, _i64, _vp, _i, _P(PfFftPlan), _vp],
@@ -147,6 +162,7 @@ _SIGNATURES = {
 _RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, "pf_prop_ws_b": ctypes.c_int64,
              "pf_prop_ws_spectrum": ctypes.c_int64, "pf_rsd_workspace_bytes": ctypes.c_int64,
              "pf_srsd_workspace_bytes": ctypes.c_int64, "pf_nursd1_workspace_bytes": ctypes.c_int64,
+             "pf_nursd2_workspace_bytes": ctypes.c_int64,
              "pf_prop_fast": ctypes.c_int}
 
 _lib = None

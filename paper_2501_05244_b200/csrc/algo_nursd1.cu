@@ -25,40 +25,22 @@
 #include <algorithm>
 #include <vector>
 
-#include "algo_host.cuh"
+#include "nufft_host.cuh"
 
 namespace {
 
 using namespace pfalgo;
 
-constexpr double EPS_MIN = 1e-14, EPS_MAX = 1e-1, COORD_TOL = 1e-9;
-constexpr int TILE = 16;   // nufft.TILE_2D = (1, 16, 16)
-
-// reference pad rule (reconstruct.py:102-110), used when results depend on it
-long ref_pad(double lag_max, double nu_max, long n_min) {
-  const long need = 2 * (long)ceil(fmax(lag_max, nu_max)) + 2;
-  return next_fast_len(n_min > need + 8 ? n_min : need + 8);
-}
-
-// kept natural slots of the centred modes on a length-mr axis (_device.kept_ranges)
-std::vector<std::pair<int, int>> kept_ranges(int m, int mr) {
-  if (m >= mr) return {{0, mr}};
-  if (m / 2) return {{0, m - m / 2}, {mr - m / 2, m / 2}};
-  return {{0, m - m / 2}};
-}
-
 struct Plan {
   // propagation
   int px, py, batch, lanes;
-  bool fast, horner, pow2_finish;
+  bool fast, horner;
   double dkhat;
   pf_prop_geom g;
   // NUFFT (modes (py, px), 2D)
-  pf_nufft_geom ng;
-  std::vector<float> ker[3];
+  Nufft2Plan nu;
   std::vector<int32_t> i0, tstart, tpts;
   std::vector<float> d0;
-  int64_t fine_elems;
   // workspace
   int64_t n_tw[4];   // px, py, mry, mrx tables (0 = shared with an earlier one)
   int64_t off_tw[4], off_planes, off_ill, off_fw, off_ker[3], off_i0, off_d0, off_ts, off_tp,
@@ -75,8 +57,6 @@ int plan(const pf_nursd1_args* a, Plan* P) {
       a->nz < 1 || !a->frequencies || !a->ill_xyz || !a->relay_xy ||
       (a->n_frames > 0 && !a->times))
     return fail("pf_nursd1: bad arguments");
-  if (!(isfinite(a->eps) && a->eps >= EPS_MIN && a->eps <= EPS_MAX))
-    return fail("accuracy target must lie in [1e-14, 0.1]");
   for (int k = 0; k < a->nz; k++)
     if (!(a->z0 + k * a->dz > a->relay_z))
       return fail("every voxel plane must lie strictly beyond the relay plane");
@@ -108,89 +88,19 @@ int plan(const pf_nursd1_args* a, Plan* P) {
   if (radices(px, rad) < 0 || radices(py, rad) < 0) return fail("pf_nursd1: pad is not 11-smooth");
   P->px = (int)px;
   P->py = (int)py;
-  // ---- NUFFT plan (nufft.NufftPlan, modes (1, py, px))
-  const int w = std::max(2, (int)ceil(log10(1.0 / a->eps)) + 2);
-  if (w > 16) return fail("accuracy target too tight for the GPU stencil (w <= 16)");
-  pf_nufft_geom& ng = P->ng;
-  ng = pf_nufft_geom{};
-  ng.dim = 2;
-  ng.w = w;
-  const int modes[3] = {1, (int)py, (int)px};
-  for (int ax3 = 0; ax3 < 3; ax3++) {
-    const int m = modes[ax3];
-    int mr;
-    double tau;
-    if (ax3 == 0) {
-      mr = 1;
-      tau = 1.0;
-      P->ker[0].assign(1, 1.0f);
-    } else {
-      mr = (int)next_fast_len(std::max(2 * m, 2 * w + 2));
-      const double s = (double)mr / m;
-      tau = M_PI * w / (s * (s - 0.5) * m * m);
-      const double h = 2.0 * M_PI / mr;
-      P->ker[ax3].resize(m);
-      for (int i = 0; i < m; i++) {
-        const double k = i - m / 2;
-        double acc = 0.0;
-        for (int j = 1; j <= w; j++)
-          acc += exp(-(j * h) * (j * h) / (4.0 * tau)) * cos(k * (j * h));
-        P->ker[ax3][i] = (float)(1.0 + 2.0 * acc);
-      }
+  // ---- NUFFT plan (nufft.NufftPlan, modes (py, px)), anchors and tile buckets
+  if (nufft2_plan((int)py, (int)px, a->eps, &P->nu) != 0) return -1;
+  {
+    std::vector<double> tx(Lp), ty(Lp);
+    for (int l = 0; l < Lp; l++) {
+      tx[l] = 2.0 * M_PI * nux[l] / px;
+      ty[l] = 2.0 * M_PI * nuy[l] / py;
     }
-    ng.mr[ax3] = mr;
-    ng.m[ax3] = m;
-    ng.h[ax3] = (float)(2.0 * M_PI / mr);
-    ng.inv4tau[ax3] = (float)(1.0 / (4.0 * tau));
-    ng.tile[ax3] = ax3 == 0 ? 1 : TILE;
-    ng.ntiles[ax3] = (mr + ng.tile[ax3] - 1) / ng.tile[ax3];
+    if (nufft2_points(P->nu, tx.data(), ty.data(), Lp, false, &P->i0, &P->d0, nullptr) != 0)
+      return -1;
   }
-  P->fine_elems = (int64_t)ng.mr[1] * ng.mr[2];
-  const int mrx = ng.mr[2], mry = ng.mr[1];
-  P->pow2_finish = px == py && (px == 128 || px == 256 || px == 512 || px == 1024) &&
-                   mry == 2 * py && mrx == 2 * px;
-  // ---- per-point stencil anchors (NufftPoints): torus coordinates 2 pi nu / P
-  P->i0.assign(3 * (size_t)Lp, 0);
-  P->d0.assign(3 * (size_t)Lp, 0.0f);
-  for (int l = 0; l < Lp; l++) {
-    const double tor[2] = {2.0 * M_PI * nux[l] / px, 2.0 * M_PI * nuy[l] / py};   // (x, y)
-    for (int c = 0; c < 2; c++)
-      if (!(tor[c] >= -M_PI - COORD_TOL && tor[c] < M_PI + COORD_TOL))
-        return fail("point coordinates must lie in [-pi, pi)");
-    for (int ax3 = 1; ax3 < 3; ax3++) {
-      const double x = tor[2 - ax3];   // mode axis a pairs with point column 2 - a
-      const double h = 2.0 * M_PI / ng.mr[ax3];
-      const double xi = x - 2.0 * M_PI * floor(x / (2.0 * M_PI));
-      const long k = (long)floor(xi / h + 0.5);
-      P->i0[3 * (size_t)l + ax3] = (int32_t)k;
-      P->d0[3 * (size_t)l + ax3] = (float)(k * h - xi);
-    }
-  }
-  // ---- tile buckets (NufftPoints.tiles): CSR over tiles, points ascending per tile
-  const int nty = ng.ntiles[1], ntx = ng.ntiles[2];
-  std::vector<std::vector<int>> per_pt_tiles(Lp);
-  std::vector<int32_t> count((size_t)nty * ntx + 1, 0);
-  for (int l = 0; l < Lp; l++) {
-    int ty[64], tx[64], ny_ = 0, nx_ = 0;
-    for (int j = -w; j <= w; j++) {
-      const int cy_ = (int)(((P->i0[3 * (size_t)l + 1] + j) % mry + mry) % mry) / TILE;
-      const int cx_ = (int)(((P->i0[3 * (size_t)l + 2] + j) % mrx + mrx) % mrx) / TILE;
-      if (std::find(ty, ty + ny_, cy_) == ty + ny_) ty[ny_++] = cy_;
-      if (std::find(tx, tx + nx_, cx_) == tx + nx_) tx[nx_++] = cx_;
-    }
-    for (int i = 0; i < ny_; i++)
-      for (int k = 0; k < nx_; k++) {
-        const int t = ty[i] * ntx + tx[k];
-        per_pt_tiles[l].push_back(t);
-        count[t + 1]++;
-      }
-  }
-  P->tstart.assign((size_t)nty * ntx + 1, 0);
-  for (size_t t = 0; t < (size_t)nty * ntx; t++) P->tstart[t + 1] = P->tstart[t] + count[t + 1];
-  P->tpts.assign(P->tstart.back(), 0);
-  std::vector<int32_t> fill(P->tstart.begin(), P->tstart.end() - 1);
-  for (int l = 0; l < Lp; l++)
-    for (int t : per_pt_tiles[l]) P->tpts[fill[t]++] = l;
+  nufft2_tiles(P->nu, P->i0, Lp, &P->tstart, &P->tpts);
+  const int mry = P->nu.g.mr[1], mrx = P->nu.g.mr[2];
   // ---- propagation geometry (algorithms._UhatPropEngine: centred output windows)
   pf_prop_geom& g = P->g;
   g = pf_prop_geom{};
@@ -227,15 +137,15 @@ int plan(const pf_nursd1_args* a, Plan* P) {
   P->off_fw = o; o = align256(o + 8 * (int64_t)F * frames);
   for (int i = 0; i < 3; i++) {
     P->off_ker[i] = o;
-    o = align256(o + 4 * (int64_t)P->ker[i].size());
+    o = align256(o + 4 * (int64_t)P->nu.ker[i].size());
   }
   P->off_i0 = o; o = align256(o + 4 * (int64_t)P->i0.size());
   P->off_d0 = o; o = align256(o + 4 * (int64_t)P->d0.size());
   P->off_ts = o; o = align256(o + 4 * (int64_t)P->tstart.size());
   P->off_tp = o; o = align256(o + 4 * (int64_t)std::max<size_t>(1, P->tpts.size()));
-  P->off_fine = o; o = align256(o + 8 * (int64_t)F * I * P->fine_elems);
+  P->off_fine = o; o = align256(o + 8 * (int64_t)F * I * P->nu.fine_elems);
   P->off_rt = o;
-  if (P->fast && P->pow2_finish) o = align256(o + 8 * (int64_t)F * I * px * 2 * px);
+  if (P->fast && P->nu.pow2_finish) o = align256(o + 8 * (int64_t)F * I * px * 2 * px);
   P->off_uhat = o; o = align256(o + 8 * (int64_t)F * I * px * py);
   P->off_wa = o; o = align256(o + 8 * P->lanes * pf_prop_ws_a(&g, P->batch));
   P->off_wb = o; o = align256(o + 8 * P->lanes * pf_prop_ws_b(&g, P->batch));
@@ -271,7 +181,7 @@ extern "C" int pf_nursd1(const pf_nursd1_args* a, const void* slices, void* vol,
   const int64_t V = (int64_t)a->nz * a->ny * a->nx;
   const int nv = F * I;
   // ---- tables (host, fp64 twiddles) -> workspace; plans px, py, mry, mrx
-  const long lens[4] = {P.px, P.py, P.ng.mr[1], P.ng.mr[2]};
+  const long lens[4] = {P.px, P.py, P.nu.g.mr[1], P.nu.g.mr[2]};
   pf_fft_plan pl[4];
   for (int i = 0; i < 4; i++) {
     int src = i;
@@ -302,7 +212,7 @@ extern "C" int pf_nursd1(const pf_nursd1_args* a, const void* slices, void* vol,
       fw[(size_t)f * frames + j] = make_float2((float)cos(ph), (float)sin(ph));
     }
   UPLOAD(P.off_fw, fw.data(), 8 * fw.size());
-  for (int i = 0; i < 3; i++) UPLOAD(P.off_ker[i], P.ker[i].data(), 4 * P.ker[i].size());
+  for (int i = 0; i < 3; i++) UPLOAD(P.off_ker[i], P.nu.ker[i].data(), 4 * P.nu.ker[i].size());
   UPLOAD(P.off_i0, P.i0.data(), 4 * P.i0.size());
   UPLOAD(P.off_d0, P.d0.data(), 4 * P.d0.size());
   UPLOAD(P.off_ts, P.tstart.data(), 4 * P.tstart.size());
@@ -314,27 +224,27 @@ extern "C" int pf_nursd1(const pf_nursd1_args* a, const void* slices, void* vol,
   const float* kz = (const float*)(w + P.off_ker[0]);
   const float* ky = (const float*)(w + P.off_ker[1]);
   const float* kx = (const float*)(w + P.off_ker[2]);
-  int rc = pf_nufft_spread(&P.ng, (const int32_t*)(w + P.off_i0), (const float*)(w + P.off_d0),
+  int rc = pf_nufft_spread(&P.nu.g, (const int32_t*)(w + P.off_i0), (const float*)(w + P.off_d0),
                            (const int32_t*)(w + P.off_ts), (const int32_t*)(w + P.off_tp), slices,
-                           a->n_points, nv, fine, P.fine_elems, stream);
+                           a->n_points, nv, fine, P.nu.fine_elems, stream);
   if (rc != 0) return rc;
   const int64_t out_stride = (int64_t)P.px * P.py;
-  if (P.fast && P.pow2_finish) {
-    rc = pf_nufft_type1_finish_pow2(&P.ng, fine, P.fine_elems, nv, w + P.off_rt, &pl[3], &pl[0],
+  if (P.fast && P.nu.pow2_finish) {
+    rc = pf_nufft_type1_finish_pow2(&P.nu.g, fine, P.nu.fine_elems, nv, w + P.off_rt, &pl[3], &pl[0],
                                     ky, kx, uhat, out_stride, stream);
   } else {
     // pruned fine-grid FFT (_device.fftn_pruned, outputs=True): every row along x, then
     // along y only the columns holding kept modes
-    const int mry = P.ng.mr[1], mrx = P.ng.mr[2];
-    rc = pf_fft_lines(fine, &pl[3], (int64_t)nv * mry, mry, mrx, P.fine_elems, 1, -1, 1.0f,
+    const int mry = P.nu.g.mr[1], mrx = P.nu.g.mr[2];
+    rc = pf_fft_lines(fine, &pl[3], (int64_t)nv * mry, mry, mrx, P.nu.fine_elems, 1, -1, 1.0f,
                       stream);
     for (auto r : kept_ranges(P.px, mrx)) {
       if (rc != 0 || r.second == 0) continue;
       rc = pf_fft_lines(fine + r.first, &pl[2], (int64_t)nv * r.second, r.second, 1,
-                        P.fine_elems, mrx, -1, 1.0f, stream);
+                        P.nu.fine_elems, mrx, -1, 1.0f, stream);
     }
     if (rc == 0)
-      rc = pf_nufft_deconv(&P.ng, fine, P.fine_elems, kz, ky, kx, nv, uhat, out_stride,
+      rc = pf_nufft_deconv(&P.nu.g, fine, P.nu.fine_elems, kz, ky, kx, nv, uhat, out_stride,
                            P.fast ? 1 : 0, stream);
   }
   if (rc != 0) return rc;

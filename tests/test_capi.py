@@ -1,8 +1,8 @@
-"""The whole-algorithm C entry points pf_rsd, pf_srsd and pf_nursd1 (include/pfgpu.h), called the way a reference-side
+"""The whole-algorithm C entry points pf_rsd, pf_srsd, pf_nursd1 and pf_nursd2 (include/pfgpu.h), called the way a reference-side
 ctypes binding would call it: host geometry and frequency arrays, device
 slices / volume / workspace pointers, the caller's stream.  CPU tests cover the planning
 and the reference's validation messages (no device needed); GPU tests compare the result
-with the float64 oracle (reference rsd / srsd / nursd1, reconstruct.py:208-385) and with
+with the float64 oracle (reference rsd / srsd / nursd1 / nursd2, reconstruct.py:208-459) and with
 the Python engine.
 """
 
@@ -295,4 +295,93 @@ def test_pf_nursd1_video_without_illumination(rng):
     times = np.array([0.0, 2e-10])
     got = capi_nursd1(sl, grid, times=times, include_illumination=False)
     ref = O.nursd1(sl, grid, times=times, include_illumination=False)
+    assert O.rel_l2(got, ref) < TOL
+
+
+# ---------------------------------------------------------------- pf_nursd2
+
+def nursd2_args(slices, voxels, eps=1e-6, times=None, include_illumination=True):
+    g = slices.relay.grid
+    zs = np.ascontiguousarray([p.z for p in voxels.planes], dtype=np.float64)
+    cnt = np.ascontiguousarray([p.points.count for p in voxels.planes], dtype=np.int64)
+    xy = np.ascontiguousarray(np.vstack([np.asarray(p.points.points) for p in voxels.planes]),
+                              dtype=np.float64)
+    freqs = np.ascontiguousarray(slices.frequencies, dtype=np.float64)
+    ill = np.ascontiguousarray(illumination_coordinates(slices.relay, slices.illuminations),
+                               dtype=np.float64)
+    t = None if times is None else np.ascontiguousarray(times, dtype=np.float64)
+    a = _lib.PfNursd2Args(relay_nx=g.nx, relay_ny=g.ny, relay_dx=g.dx, relay_dy=g.dy,
+                          relay_x0=g.x0, relay_y0=g.y0, relay_z=g.z, n_planes=zs.size,
+                          plane_z=zs.ctypes.data, plane_count=cnt.ctypes.data,
+                          voxel_xy=xy.ctypes.data, n_freq=freqs.size, n_illum=ill.shape[0],
+                          frequencies=freqs.ctypes.data, ill_xyz=ill.ctypes.data,
+                          n_frames=0 if t is None else t.size,
+                          times=None if t is None else t.ctypes.data, eps=eps,
+                          include_illum=int(bool(include_illumination)))
+    return a, (zs, cnt, xy, freqs, ill, t)
+
+
+def capi_nursd2(slices, voxels, **kw):
+    import torch
+    a, keep = nursd2_args(slices, voxels, **kw)
+    lib = _lib.load()
+    nbytes = lib.pf_nursd2_workspace_bytes(ctypes.byref(a))
+    assert nbytes > 0, _lib.last_error()
+    c = np.asarray(slices.coefficients)
+    coeff = torch.from_numpy(np.ascontiguousarray(c.transpose(2, 0, 1)).astype(np.complex64)).cuda()
+    vol = torch.empty((max(1, a.n_frames), voxels.count), dtype=torch.complex64, device="cuda")
+    ws = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+    rc = lib.pf_nursd2(ctypes.byref(a), coeff.data_ptr(), vol.data_ptr(), ws.data_ptr(), nbytes,
+                       torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    return vol.cpu().numpy()
+
+
+def _voxel_scene(rng, n=24, F=2, n_ill=1, zs=(0.7, 0.9), per_plane=50):
+    p = 0.02
+    g = pf.UniformGrid2D(n, n, p, p, -(n - 1) * p / 2, -(n - 1) * p / 2, 0.0)
+    freqs = 2 * np.pi * 3e8 / 0.06 * (1 + 0.02 * np.arange(F))
+    c = rng.normal(size=(n_ill, n * n, F)) + 1j * rng.normal(size=(n_ill, n * n, F))
+    ill = pf.PointList(rng.uniform(-0.1, 0.1, size=(n_ill, 2)))
+    sl = pf.FrequencySlices(freqs, c, pf.UniformRelay(g), ill)
+    planes = tuple(pf.VoxelPlane(z, pf.PointList(rng.uniform(-0.2, 0.2, size=(per_plane, 2))))
+                   for z in zs)
+    return sl, pf.ExplicitVoxels(planes)
+
+
+def test_nursd2_workspace_and_validation(rng):
+    sl, ev = _voxel_scene(rng)
+    a, keep = nursd2_args(sl, ev)
+    lib = _lib.load()
+    assert lib.pf_nursd2_workspace_bytes(ctypes.byref(a)) > 0
+    a.relay_z = 0.8                                       # plane 0.7 no longer beyond the relay
+    assert lib.pf_nursd2_workspace_bytes(ctypes.byref(a)) == -1
+    assert "beyond the relay" in _lib.last_error()
+    a.relay_z = 0.0
+    a.eps = 0.5
+    assert lib.pf_nursd2_workspace_bytes(ctypes.byref(a)) == -1
+    assert "accuracy target" in _lib.last_error()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [
+    dict(),                                       # two planes, one illumination
+    dict(n_ill=2, F=3),                           # two illuminations
+    dict(zs=(0.5, 0.6, 0.8, 1.1), per_plane=200),
+    dict(n=64, zs=(0.9,), per_plane=3000),        # larger pad, one plane
+])
+def test_pf_nursd2_matches_oracle_and_engine(rng, case):
+    sl, ev = _voxel_scene(rng, **case)
+    got = capi_nursd2(sl, ev)[0]
+    assert O.rel_l2(got, O.nursd2(sl, ev)) < TOL
+    assert O.rel_l2(got, pf.nursd2(sl, ev).field) < 1e-5
+
+
+@pytest.mark.gpu
+def test_pf_nursd2_video_without_illumination(rng):
+    sl, ev = _voxel_scene(rng, F=3)
+    times = np.array([0.0, 2e-10])
+    got = capi_nursd2(sl, ev, times=times, include_illumination=False)
+    ref = O.nursd2(sl, ev, times=times, include_illumination=False)
     assert O.rel_l2(got, ref) < TOL
