@@ -292,6 +292,15 @@ int pf_nufft_type1_finish_pow2(const pf_nufft_geom* g, const void* fine, int64_t
 int pf_nufft_deconv(const pf_nufft_geom* g, const void* fine, int64_t fine_stride,
                     const float* kz, const float* ky, const float* kx, int nv, void* out,
                     int64_t out_stride, int transpose, void* stream);
+/* Type-2 start for 2D plans in two fused passes (spectral.py:373-375, = pf_nufft_place +
+ * the pruned inverse fine-grid FFT, bit for bit): fine[v] = unnormalised inverse FFT of
+ * S[v] / (ker_y ker_x) placed on the fine slots, S natural order [v][my][mx].  The x pass
+ * builds each kept fine row from S in shared memory; the y pass reads only the kept rows.
+ * plan_x / plan_y: pf_fft_plan of lengths mr[2] / mr[1]. */
+int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, int64_t s_stride,
+                            const float* ky, const float* kx, int nv, void* fine,
+                            int64_t fine_stride, const pf_fft_plan* plan_x,
+                            const pf_fft_plan* plan_y, void* stream);
 /* type-2 start (spectral.py:374): modes / deconvolution onto their fine slots, 0 elsewhere. */
 int pf_nufft_place(const pf_nufft_geom* g, const void* S, int64_t s_stride, const float* kz,
                    const float* ky, const float* kx, int nv, void* fine, int64_t fine_stride,

@@ -13,9 +13,9 @@
 // concatenated in plane order, each carrying (x, y, z), its plane and its output slot;
 // all of it copied into the caller's workspace.  Device side: relay spectra (embed +
 // natural-order 2D FFT), then per frequency and plane batch: kernel rows, product-only
-// columns (Uhat * Ghat_k), place / deconvolution onto the fine grid, the pruned inverse
-// fine-grid FFT and one interpolation launch for the batch's voxels (scale 1 / (px py),
-// illumination phase at each voxel, frame weights).
+// columns (Uhat * Ghat_k), the fused place / deconvolution + inverse fine-grid FFT
+// (pf_nufft_type2_start_2d) and one interpolation launch for the batch's voxels (scale
+// 1 / (px py), illumination phase at each voxel, frame weights).
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -232,14 +232,12 @@ extern "C" int pf_nursd2(const pf_nursd2_args* a, const void* slices, void* vol,
                       stream);
   if (rc != 0) return rc;
   const pf_plane* planes_d = (const pf_plane*)(w + P.off_planes);
-  const float* kz = (const float*)(w + P.off_ker[0]);
   const float* ky = (const float*)(w + P.off_ker[1]);
   const float* kx = (const float*)(w + P.off_ker[2]);
   float2* wa = (float2*)(w + P.off_wa);
   float2* spec = (float2*)(w + P.off_spec);
   float2* fine = (float2*)(w + P.off_fine);
   const int64_t per_f = (int64_t)I * px * py;
-  const auto kept_y = kept_ranges(py, mry);
   for (int f = 0; f < F && rc == 0; f++) {
     const double khat = a->frequencies[f] / C_LIGHT;
     for (int b0 = 0; b0 < a->n_planes && rc == 0; b0 += P.nb) {
@@ -248,17 +246,11 @@ extern "C" int pf_nursd2(const pf_nursd2_args* a, const void* slices, void* vol,
       const int nv = n * I;
       rc = pf_prop_kernel_rows(pp, n, khat, &P.g, &pl[0], wa, stream);
       if (rc == 0) rc = pf_prop_columns(pp, n, &P.g, &pl[1], wa, uhat + f * per_f, spec, 1, stream);
-      // type-2 first half (spectral.py:373-375): place (spectrum / deconvolution), then the
-      // inverse fine-grid FFT skipping the all-zero lines (_device.fftn_pruned, outputs=False)
+      // type-2 first half (spectral.py:373-375): place (spectrum / deconvolution) and the
+      // inverse fine-grid FFT, fused (pf_nufft_type2_start_2d)
       if (rc == 0)
-        rc = pf_nufft_place(&P.nu.g, spec, (int64_t)py * px, kz, ky, kx, nv, fine, fe, 0, stream);
-      for (auto r : kept_y) {
-        if (rc != 0 || r.second == 0) continue;
-        rc = pf_fft_lines(fine + (int64_t)r.first * mrx, &pl[3], (int64_t)nv * r.second, r.second,
-                          mrx, fe, 1, +1, 1.0f, stream);
-      }
-      if (rc == 0)
-        rc = pf_fft_lines(fine, &pl[2], (int64_t)nv * mrx, mrx, 1, fe, mrx, +1, 1.0f, stream);
+        rc = pf_nufft_type2_start_2d(&P.nu.g, spec, (int64_t)py * px, ky, kx, nv, fine, fe,
+                                     &pl[3], &pl[2], stream);
       const int64_t lo = P.pt_lo[b0], hi = P.pt_lo[b0 + n];
       if (rc == 0 && hi > lo)
         rc = pf_nufft_interp2_batch(

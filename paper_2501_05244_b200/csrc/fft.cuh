@@ -427,5 +427,18 @@ __host__ __device__ inline int plan_xl(const pf_fft_plan& p) {
   return p.radix[PF_MAX_STAGES - 1] == PF_XFFT_TAG ? xfft_L(p.n) : 0;
 }
 
+// instantiate CALL with constexpr XL = the plan's register-FFT lane count (0: Stockham)
+#define PF_XL_DISPATCH(xl, CALL)                                                            \
+  switch (xl) {                                                                             \
+    case 4: { constexpr int XL = 4; CALL; } break;                                          \
+    case 5: { constexpr int XL = 5; CALL; } break;                                          \
+    case 8: { constexpr int XL = 8; CALL; } break;                                          \
+    case 10: { constexpr int XL = 10; CALL; } break;                                        \
+    case 15: { constexpr int XL = 15; CALL; } break;                                        \
+    case 20: { constexpr int XL = 20; CALL; } break;                                        \
+    case 30: { constexpr int XL = 30; CALL; } break;                                        \
+    default: { constexpr int XL = 0; CALL; } break;                                         \
+  }
+
 // padded leading dimension for `cnt` lines of length n in shared memory
 __host__ __device__ __forceinline__ int pf_ld(int n) { return n + ((n % 16) == 0 ? 1 : 0); }

@@ -1,0 +1,163 @@
+// Type-2 NUFFT start for 2D plans, fused (reference spectral.py:373-375):
+//   fine = ifftn(place(S / (ker_y ker_x)))       (unnormalised inverse, natural order)
+// in two passes instead of place + two pruned line passes (pf_nufft_place + pf_fft_lines):
+//
+//   rows:    for every KEPT fine row (the my slots holding centred modes) build the row
+//            in shared memory straight from the mode grid -- S / deconvolution on the mx
+//            kept slots, zero elsewhere -- inverse-transform it along x and store it;
+//   columns: for every fine column read only the kept rows (the other rows are zero by
+//            construction and are never written nor read), inverse-transform along y and
+//            store the whole column.
+//
+// Per fine grid this moves S (my mx) + kept rows (my mrx, written then read) + the grid
+// (mry mrx, written) instead of S + a zero-filled grid written + kept rows read / written
+// + the grid read / written: 9 instead of 17 bytes-units at mr = 2m.  Same arithmetic and
+// operation order as the unfused sequence (the FFT kernels are the same), so the fine
+// grid is bit-identical to it.
+#include "fft.cuh"
+
+namespace {
+
+constexpr int T2_THREADS = 256;
+constexpr size_t T2_SMEM = 200 * 1024;
+
+template <int XL>
+__global__ void __launch_bounds__(T2_THREADS, XL > 0 ? 2 : 1)
+k_t2_rows(pf_nufft_geom G, const float2* __restrict__ S, long long s_stride,
+          const float* __restrict__ ky, const float* __restrict__ kx, int nv,
+          float2* __restrict__ fine, long long fine_stride, pf_fft_plan plan_x, int cnt) {
+  extern __shared__ float2 sm[];
+  const int mrx = G.mr[2], mx = G.m[2], my = G.m[1], mry = G.mr[1];
+  const int ld = pf_ld(mrx);
+  float2* a = sm;
+  float2* b = sm + (size_t)cnt * ld;
+  const long long nlines = (long long)nv * my;
+  const long long l0 = (long long)blockIdx.x * cnt;
+  const int nl = (int)(nlines - l0 < cnt ? nlines - l0 : cnt);
+  const FastDiv dmrx(mrx);
+  for (int e = threadIdx.x; e < nl * mrx; e += T2_THREADS) {
+    const int c = dmrx.div(e), fx = e - c * mrx;
+    const long long l = l0 + c;
+    const int v = (int)(l / my), i = (int)(l - (long long)v * my);
+    const int cy = i - my / 2;
+    const int cx = fx < mrx - mrx / 2 ? fx : fx - mrx;
+    float2 val = make_float2(0.f, 0.f);
+    if (cx >= -(mx / 2) && cx < mx - mx / 2) {
+      const int jy = natural(cy, my), jx = natural(cx, mx);
+      // k_place's denominator: kz[0] (= 1) * ky * kx
+      const float den = 1.0f * ky[cy + my / 2] * kx[cx + mx / 2];
+      const float2 s = S[(long long)v * s_stride + (long long)jy * mx + jx];
+      val = make_float2(s.x / den, s.y / den);
+    }
+    a[c * ld + fx] = val;
+  }
+  __syncthreads();
+  const float2* res = fft_any<XL, 1>(a, b, ld, nl, plan_x);
+  for (int e = threadIdx.x; e < nl * mrx; e += T2_THREADS) {
+    const int c = dmrx.div(e), fx = e - c * mrx;
+    const long long l = l0 + c;
+    const int v = (int)(l / my), i = (int)(l - (long long)v * my);
+    const int cy = i - my / 2;
+    const int fy = cy < 0 ? cy + mry : cy;
+    fine[(long long)v * fine_stride + (long long)fy * mrx + fx] = res[c * ld + fx];
+  }
+}
+
+template <int XL>
+__global__ void __launch_bounds__(T2_THREADS, XL > 0 ? 2 : 1)
+k_t2_cols(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fine_stride,
+          pf_fft_plan plan_y, int cnt) {
+  extern __shared__ float2 sm[];
+  __shared__ long long lbase[64];
+  const int mrx = G.mr[2], my = G.m[1], mry = G.mr[1];
+  const int ld = pf_ld(mry);
+  float2* a = sm;
+  float2* b = sm + (size_t)cnt * ld;
+  const long long nlines = (long long)nv * mrx;
+  const long long l0 = (long long)blockIdx.x * cnt;
+  const int nl = (int)(nlines - l0 < cnt ? nlines - l0 : cnt);
+  for (int c = threadIdx.x; c < nl; c += T2_THREADS) {
+    const long long l = l0 + c;
+    const long long v = l / mrx;
+    lbase[c] = v * fine_stride + (l - v * mrx);
+  }
+  __syncthreads();
+  const FastDiv dnl(nl);
+  const int lo_hi = my - my / 2;          // kept slots [0, lo_hi) and [mry - my/2, mry)
+  const int hi_lo = mry - my / 2;
+  for (int e = threadIdx.x; e < nl * mry; e += T2_THREADS) {
+    const int fy = dnl.div(e), c = e - fy * nl;
+    float2 val = make_float2(0.f, 0.f);
+    if (fy < lo_hi || fy >= hi_lo) val = fine[lbase[c] + (long long)fy * mrx];
+    a[c * ld + fy] = val;
+  }
+  __syncthreads();
+  const float2* res = fft_any<XL, 1>(a, b, ld, nl, plan_y);
+  for (int e = threadIdx.x; e < nl * mry; e += T2_THREADS) {
+    const int fy = dnl.div(e), c = e - fy * nl;
+    fine[lbase[c] + (long long)fy * mrx] = res[c * ld + fy];
+  }
+}
+
+// lines per CTA: register FFT: 32 / L lines per warp, `rounds` passes of the 8 warps;
+// Stockham: enough lines to keep the 256 threads busy.  Both within the smem budget.
+size_t t2_per_line(int n, int xl) { return (xl ? 1 : 2) * (size_t)pf_ld(n) * sizeof(float2); }
+
+int t2_cnt(int n, int xl, int rounds, int want_min) {
+  const size_t per = t2_per_line(n, xl);
+  int cnt = xl ? rounds * (T2_THREADS / 32) * (32 / xl) : (4 * T2_THREADS + n - 1) / n;
+  if (cnt < want_min) cnt = want_min;
+  const int fit = (int)(T2_SMEM / per);
+  if (cnt > fit) cnt = fit;
+  if (cnt > 64) cnt = 64;
+  return cnt < 1 ? 1 : cnt;
+}
+
+template <typename K>
+void t2_allow(K k) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T2_SMEM);
+}
+
+template <int XL>
+void t2_allow_all() {
+  t2_allow(k_t2_rows<XL>);
+  t2_allow(k_t2_cols<XL>);
+}
+
+}  // namespace
+
+extern "C" int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, int64_t s_stride,
+                                       const float* ky, const float* kx, int nv, void* fine,
+                                       int64_t fine_stride, const pf_fft_plan* plan_x,
+                                       const pf_fft_plan* plan_y, void* stream) {
+  PF_ARG_CHECK(g && g->dim == 2 && g->mr[0] == 1 && nv >= 1 && plan_x && plan_y &&
+                   plan_x->n == g->mr[2] && plan_y->n == g->mr[1] && g->m[2] <= g->mr[2] &&
+                   g->m[1] <= g->mr[1],
+               "pf_nufft_type2_start_2d: bad args (2D plan, plans of the fine-grid lengths)");
+  PF_ARG_CHECK(S && fine && ky && kx, "pf_nufft_type2_start_2d: null buffer");
+  static PfDevOnce attr;
+  if (attr.first()) {   // every instantiation: later calls may take other lengths
+    for (int xl : {0, 4, 5, 8, 10, 15, 20, 30}) PF_XL_DISPATCH(xl, (t2_allow_all<XL>()));
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int xlx = plan_xl(*plan_x), xly = plan_xl(*plan_y);
+  {
+    const int cnt = t2_cnt(g->mr[2], xlx, 1, 1);
+    const long long nl = (long long)nv * g->m[1];
+    const size_t smem = cnt * t2_per_line(g->mr[2], xlx);
+    PF_XL_DISPATCH(xlx, (k_t2_rows<XL><<<(unsigned)((nl + cnt - 1) / cnt), T2_THREADS, smem, st>>>(
+                             *g, (const float2*)S, s_stride, ky, kx, nv, (float2*)fine,
+                             fine_stride, *plan_x, cnt)));
+    PF_LAUNCH_CHECK("k_t2_rows");
+  }
+  {
+    // columns: >= 16 adjacent columns per CTA for 128-byte row segments
+    const int cnt = t2_cnt(g->mr[1], xly, 2, 16);
+    const long long nl = (long long)nv * g->mr[2];
+    const size_t smem = cnt * t2_per_line(g->mr[1], xly);
+    PF_XL_DISPATCH(xly, (k_t2_cols<XL><<<(unsigned)((nl + cnt - 1) / cnt), T2_THREADS, smem, st>>>(
+                             *g, nv, (float2*)fine, fine_stride, *plan_y, cnt)));
+    PF_LAUNCH_CHECK("k_t2_cols");
+  }
+  return 0;
+}

@@ -263,17 +263,6 @@ int lines_for(int n, int bufs, int want_stockham, int xl) {
 }
 
 // instantiate kernel K<XL> for the plan's register-FFT lane count
-#define PF_XL_DISPATCH(xl, CALL)                                                            \
-  switch (xl) {                                                                             \
-    case 4: { constexpr int XL = 4; CALL; } break;                                          \
-    case 5: { constexpr int XL = 5; CALL; } break;                                          \
-    case 8: { constexpr int XL = 8; CALL; } break;                                          \
-    case 10: { constexpr int XL = 10; CALL; } break;                                        \
-    case 15: { constexpr int XL = 15; CALL; } break;                                        \
-    case 20: { constexpr int XL = 20; CALL; } break;                                        \
-    case 30: { constexpr int XL = 30; CALL; } break;                                        \
-    default: { constexpr int XL = 0; CALL; } break;                                         \
-  }
 
 template <int XL>
 void allow_generic() {

@@ -27,6 +27,7 @@ _EPS_MIN, _EPS_MAX = 1e-14, 1e-1
 _COORD_TOL = 1e-9
 TILE_2D = (1, 16, 16)
 TILE_3D = (4, 8, 8)
+_T2_FUSED = os.environ.get("PF_T2_FUSED", "1") != "0"
 
 
 class NufftPlan:
@@ -224,6 +225,13 @@ def place_and_inverse(plan: NufftPlan, S: torch.Tensor, nv: int, s_stride: int,
                       fine: torch.Tensor, stream=None) -> torch.Tensor:
     """Type-2 first half (spectral.py:373-375): fine = ifftn(place(S / ker)) * prod(mr)."""
     kz, ky, kx = plan.kers
+    if plan.dim == 2 and _T2_FUSED:
+        # place + pruned inverse FFT in two fused passes (bit-identical)
+        _lib.call("pf_nufft_type2_start_2d", plan.gref, dev.ptr(S), s_stride, dev.ptr(ky),
+                  dev.ptr(kx), nv, dev.ptr(fine), plan.fine_elems,
+                  dev.fft_plan(plan.mrs[2], plan.device).ref,
+                  dev.fft_plan(plan.mrs[1], plan.device).ref, dev.stream_ptr(stream))
+        return fine
     _lib.call("pf_nufft_place", plan.gref, dev.ptr(S), s_stride, dev.ptr(kz), dev.ptr(ky),
               dev.ptr(kx), nv, dev.ptr(fine), plan.fine_elems, 0, dev.stream_ptr(stream))
     shape = plan.mrs[3 - plan.dim:]

@@ -113,3 +113,39 @@ def test_type1_register_finish_vs_oracle(rng, m, eps):
         # natural-order modes, transposed [x][y]; the oracle returns centred [y][x]
         ref_nat = np.fft.ifftshift(ref).T
         assert O.rel_l2(got[i], ref_nat) < 2e-6
+
+
+@pytest.mark.parametrize("modes,nv", [((350, 350), 3),    # fine 700: register FFT (35 x 20)
+                                      ((64, 64), 2),      # fine 128: Stockham
+                                      ((45, 63), 2),      # odd modes, fine 90 x 126
+                                      ((140, 140), 5)])   # fine 280 (Stockham by default)
+def test_type2_start_fused_equals_place_and_pruned_fft(rng, monkeypatch, modes, nv):
+    """pf_nufft_type2_start_2d (place + inverse fine-grid FFT in two fused passes) writes
+    the same fine grid as pf_nufft_place + the pruned line passes, bit for bit."""
+    import torch
+    from paper_2501_05244_b200 import nufft as nu
+    plan = nu.NufftPlan(modes, 1e-6, torch.device("cuda"))
+    my, mx = modes
+    S = torch.from_numpy((rng.normal(size=(nv, my * mx)) + 1j * rng.normal(size=(nv, my * mx)))
+                         .astype(np.complex64)).cuda()
+    fine_a = torch.full((nv, plan.fine_elems), complex(np.nan, np.nan), dtype=torch.complex64,
+                        device="cuda")
+    fine_b = torch.empty_like(fine_a)
+    monkeypatch.setattr(nu, "_T2_FUSED", True)
+    nu.place_and_inverse(plan, S, nv, my * mx, fine_a)
+    monkeypatch.setattr(nu, "_T2_FUSED", False)
+    nu.place_and_inverse(plan, S, nv, my * mx, fine_b)
+    torch.cuda.synchronize()
+    assert torch.equal(fine_a, fine_b)
+    # and it is the inverse DFT of the placed spectrum
+    mry, mrx = plan.mrs[1], plan.mrs[2]
+    ky, kx = (k.cpu().numpy().astype(np.float64) for k in plan.kers[1:])
+    grid = np.zeros((mry, mrx), complex)
+    s0 = S[0].cpu().numpy().reshape(my, mx).astype(complex)
+    cy = np.arange(my) - my // 2
+    cx = np.arange(mx) - mx // 2
+    sc = s0[np.ix_(cy % my, cx % mx)] / np.outer(ky, kx)
+    grid[np.ix_(cy % mry, cx % mrx)] = sc
+    ref = np.fft.ifft2(grid) * mry * mrx
+    got = fine_a[0].cpu().numpy().reshape(mry, mrx)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5
