@@ -6,6 +6,8 @@
 // `cnt` lines in shared memory with coalesced loads (element-major when the
 // lines are columns, line-major when they are rows), runs the Stockham
 // transform (fft.cuh), and writes them back in place.
+#include <stdlib.h>
+
 #include "xfft.cuh"
 
 namespace {
@@ -172,8 +174,21 @@ int launch_lines(float2* data, const pf_fft_plan& p, long long nlines, long long
     pf_set_error("pf_fft_lines: length %d does not fit shared memory", p.n);
     return -1;
   }
-  // enough lines per CTA to keep 256 threads busy, but leave work for all SMs
-  const int want = (4 * FL_THREADS + p.n - 1) / p.n;
+  // enough lines per CTA to keep 256 threads busy (4 elements per thread), more (up to
+  // 16) while the grid still gives every SM 4 CTAs: fewer barriers per line
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm < 1) nsm = 148;
+  }
+  const long long w_small = (4 * FL_THREADS + p.n - 1) / p.n;
+  const long long w_big = (16 * FL_THREADS + p.n - 1) / p.n;
+  long long wl = nlines / (4LL * nsm);
+  if (wl < w_small) wl = w_small;
+  if (wl > w_big) wl = w_big;
+  const int want = (int)wl;
   if (cnt > want) cnt = want < 1 ? 1 : want;
   if (estr != 1 && cnt < 8 && (size_t)8 * per_line <= FL_SMEM_BUDGET) cnt = 8;  // coalescing
   if (cnt > 64) cnt = 64;

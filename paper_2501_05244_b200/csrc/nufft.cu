@@ -403,6 +403,118 @@ k_interp2_batch_h(pf_nufft_geom G, const int* __restrict__ i0, const float* __re
   }
 }
 
+
+// The half-warp readout specialised for W = 17 (w = 8: the reference's default accuracy
+// eps = 1e-6), trimmed to the instructions a tap needs: lane c owns stencil column c for
+// rows 0..15 (row weights broadcast by shuffle) and row 16 (its weight formed in every
+// lane); column 16 is spread over the lanes after the row loop (lane r takes tap (r, 16),
+// lane 0 also (16, 16)) instead of a predicated second column in every row.  32-bit cell
+// offsets (the fine grid has < 2^31 cells), the torus wrap-around by one compare per row.
+// Same weights as k_interp2_batch_h; the column-16 taps join each lane's sum last (fp32
+// summation order only).
+__global__ void __launch_bounds__(256)
+k_interp2_h17(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
+              const double* __restrict__ xyz, const int* __restrict__ plane_idx,
+              const long long* __restrict__ dst_idx, int npts, int plane0,
+              const float2* __restrict__ fine, long long fine_plane_stride,
+              long long fine_stride, int n_illum, const double* __restrict__ ill,
+              double kturns, int include_illum, float scale,
+              const float2* __restrict__ frame_w, int n_frames, float2* __restrict__ vol,
+              long long vol_frame_stride, int nodes, const float* __restrict__ lw) {
+  constexpr int w = 8;
+  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+  const int l = blockIdx.x * (blockDim.x >> 4) + ((threadIdx.x >> 5) << 1) + half;
+  const bool live = l < npts;
+  const int lc = live ? l : 0;
+  const int mry = G.mr[1], mrx = G.mr[2], fe = mry * mrx;
+  const float dyl = d0[3 * lc + 1], dxl = d0[3 * lc + 2];
+  const float dx = dxl + (float)(hl - w) * G.h[2];
+  const float wx = __expf(-dx * dx * G.inv4tau[2]);
+  const float dx16 = dxl + (float)(16 - w) * G.h[2];
+  const float wx16 = __expf(-dx16 * dx16 * G.inv4tau[2]);
+  const float dy = dyl + (float)(hl - w) * G.h[1];
+  const float wy_own = __expf(-dy * dy * G.inv4tau[1]);
+  const float dy16 = dyl + (float)(16 - w) * G.h[1];
+  const float wy16 = __expf(-dy16 * dy16 * G.inv4tau[1]);
+  // anchors lie in [0, mr]: the stencil origin wraps at most once
+  const int cxb = wrap_once(i0[3 * lc + 2] - w, mrx);
+  const int cx = wrap_once(cxb + hl, mrx), cx16 = wrap_once(cxb + 16, mrx);
+  const int cy0 = wrap_once(i0[3 * lc + 1] - w, mry);
+  const int r0 = cy0 * mrx;                                   // row 0's offset
+  const int r_own = wrap_once(cy0 + hl, mry) * mrx;           // this lane's row (column 16)
+  const int r16 = wrap_once(cy0 + 16, mry) * mrx;
+  const float2* fplane = fine + (long long)(plane_idx[lc] - plane0) * fine_plane_stride;
+  float2 tot = make_float2(0.f, 0.f);
+  for (int p = 0; p < n_illum; p++) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int m = 0; m < nodes; m++) {
+      const float2* g = fplane + (long long)m * fine_plane_stride + (long long)p * fine_stride;
+      const float lwm = lw ? __ldg(lw + (long long)lc * nodes + m) : 1.0f;
+      const float wxm = wx * lwm;
+      const float2* col = g + cx;
+      int ro = r0;
+#pragma unroll 4
+      for (int oy = 0; oy < 16; oy++) {
+        const float wy = __shfl_sync(0xffffffffu, wy_own, (half << 4) + oy);
+        const float2 f = __ldg(col + ro);
+        const float ww = wxm * wy;
+        acc.x = fmaf(ww, f.x, acc.x);
+        acc.y = fmaf(ww, f.y, acc.y);
+        ro += mrx;
+        if (ro >= fe) ro -= fe;
+      }
+      {
+        const float2 f = __ldg(col + ro);                      // row 16
+        const float ww = wxm * wy16;
+        acc.x = fmaf(ww, f.x, acc.x);
+        acc.y = fmaf(ww, f.y, acc.y);
+      }
+      const float wx16m = wx16 * lwm;
+      {   // column 16: lane r takes row r, lane 0 also row 16
+        const float2 f = __ldg(g + r_own + cx16);
+        const float ww = wx16m * wy_own;
+        acc.x = fmaf(ww, f.x, acc.x);
+        acc.y = fmaf(ww, f.y, acc.y);
+        if (hl == 0) {
+          const float2 f2 = __ldg(g + r16 + cx16);
+          const float w2 = wx16m * wy16;
+          acc.x = fmaf(w2, f2.x, acc.x);
+          acc.y = fmaf(w2, f2.y, acc.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    float2 val = cscale(acc, scale);
+    if (include_illum && hl == 0) {
+      const double ex = xyz[3 * lc] - ill[3 * p], ey = xyz[3 * lc + 1] - ill[3 * p + 1];
+      const double ez = xyz[3 * lc + 2] - ill[3 * p + 2];
+      val = cmul(val, expi_reduced(PF_TWO_PI * kturns * sqrt(ex * ex + ey * ey + ez * ez)));
+    }
+    tot = cadd(tot, val);
+  }
+  if (hl == 0 && live) {
+    const long long dst = dst_idx[l];
+    for (int f = 0; f < n_frames; f++) {
+      float2* d = vol + f * vol_frame_stride + dst;
+      *d = cadd(*d, cmul(tot, frame_w[f]));
+    }
+  }
+}
+
+// PF_INTERP_H17=0 keeps the general half-warp kernel for W = 17 (A/B measurements)
+bool interp_h17_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PF_INTERP_H17");
+    on = (e == nullptr || atoi(e) != 0) ? 1 : 0;
+  }
+  return on != 0;
+}
+
 extern "C" int pf_nufft_interp2_nodes(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
                                       const double* xyz, const int32_t* plane_idx,
                                       const int64_t* dst_idx, int npts, int plane0,
@@ -615,6 +727,15 @@ extern "C" int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0,
     const char* e = getenv("PF_INTERP_HALF");
     half = (e == nullptr || atoi(e) != 0) ? 1 : 0;
   }
+  if (half && g->w == 8 && (long long)g->mr[1] * g->mr[2] < (1LL << 31) &&
+      interp_h17_enabled()) {   // W = 17
+    k_interp2_h17<<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
+        *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine,
+        fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,
+        (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride, 1, nullptr);
+    PF_LAUNCH_CHECK("k_interp2_h17");
+    return 0;
+  }
   if (half) {   // two points per warp (half a warp each)
     k_interp2_batch_h<<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
         *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine,
@@ -644,6 +765,14 @@ extern "C" int pf_nufft_interp2_nodes(const pf_nufft_geom* g, const int32_t* i0,
                    (nodes == 1 || lw != nullptr),
                "pf_nufft_interp2_nodes: bad args (2D, stencil width <= 32, weights for nodes > 1)");
   if (npts == 0) return 0;
+  if (g->w == 8 && (long long)g->mr[1] * g->mr[2] < (1LL << 31) && interp_h17_enabled()) {
+    k_interp2_h17<<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
+        *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine,
+        fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,
+        (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride, nodes, lw);
+    PF_LAUNCH_CHECK("k_interp2_h17");
+    return 0;
+  }
   k_interp2_batch_h<<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
       *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine,
       fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,
