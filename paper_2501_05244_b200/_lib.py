@@ -127,6 +127,9 @@ _SIGNATURES = {
                        _i64, _vp, _vp, _vp, _vp],
     "pf_prop_fbatch_generic": [_vp, _i, _vp, _i, _P(PfPropGeom), _P(PfFftPlan), _P(PfFftPlan),
                                _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp],
+    "pf_prop_onchip_ok": [_P(PfPropGeom)],
+    "pf_prop_fbatch_onchip": [_vp, _i, _vp, _i, _P(PfPropGeom), _vp, _vp, _i64, _vp, _vp, _vp,
+                              _vp, _i, _vp],
     "pf_count_nonfinite": [_vp, _i64, _vp, _vp],
     "pf_fp32_probe": [_vp, _i, _i, _vp],
     "pf_nufft_interp": [_P(PfNufftGeom), _vp, _vp, _i, _vp, _vp, _vp],
@@ -164,7 +167,7 @@ _RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, 
              "pf_prop_ws_spectrum": ctypes.c_int64, "pf_rsd_workspace_bytes": ctypes.c_int64,
              "pf_srsd_workspace_bytes": ctypes.c_int64, "pf_nursd1_workspace_bytes": ctypes.c_int64,
              "pf_nursd2_workspace_bytes": ctypes.c_int64,
-             "pf_prop_fast": ctypes.c_int}
+             "pf_prop_fast": ctypes.c_int, "pf_prop_onchip_ok": ctypes.c_int}
 
 _lib = None
 

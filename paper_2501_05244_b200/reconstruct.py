@@ -48,6 +48,8 @@ _LANES = int(os.environ.get("PF_LANES", "3"))
 _FAST_BATCH_CAP = int(os.environ.get("PF_BATCH_CAP", "4"))
 _FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
 _FBATCH_GENERIC = os.environ.get("PF_FBATCH_GENERIC", "1") != "0"
+_ONCHIP = os.environ.get("PF_ONCHIP", "1") != "0"   # P = 140: whole units in shared memory
+_ONCHIP_GROUPS = int(os.environ.get("PF_ONCHIP_GROUPS", "0"))   # 0: from the geometry
 _HORNER = os.environ.get("PF_HORNER", "1") != "0"   # kernel C phases by Horner's rule
 _HORNER_BLOCK = int(os.environ.get("PF_HORNER_BLOCK", "32"))   # frequencies per nested block
 
@@ -191,6 +193,9 @@ class Propagator:
         self.plan_y = dev.fft_plan(py, device)
         # register-FFT path (square power-of-two pads) consumes Uhat transposed
         self.transposed = bool(_lib.call("pf_prop_fast", ctypes.byref(g)))
+        # P = 140 (config 1's reference pad): every stage of a unit in one CTA's shared memory
+        self.onchip = (_ONCHIP and not self.transposed
+                       and bool(_lib.call("pf_prop_onchip_ok", ctypes.byref(g))))
 
     def freq_order(self, freqs: np.ndarray, n_frames: int):
         """(frequency visiting order, Horner spacing): descending with kernel C applying the
@@ -265,6 +270,20 @@ class Propagator:
         per = 8 * ((g.py // 2 + 1) * (g.px // 2 + 1) + g.n_illum * g.ny * g.px)
         return n_freq * self.n_planes_total * per <= _FBATCH_BYTES
 
+    def onchip_groups(self, nf: int) -> int:
+        """Frequency groups of the on-chip path: the count minimising (CTA waves over 148
+        SMs) x (frequencies per CTA), fewest groups on ties; from the whole grid's plane
+        count, so a plane-sharded engine sums each plane in the same order."""
+        if _ONCHIP_GROUPS > 0:
+            return max(1, min(nf, _ONCHIP_GROUPS))
+        best = None
+        for gr in range(1, nf + 1):
+            fpc = -(-nf // gr)
+            cost = -(-self.n_planes_total * (-(-nf // fpc)) // 148) * fpc
+            if best is None or cost < best[0]:
+                best = (cost, gr)
+        return best[1]
+
     def run_fbatch(self, uhat: torch.Tensor, uhat_fs: int, freqs: np.ndarray, ill_ptr: int,
                    frame_w: torch.Tensor, vol: torch.Tensor, stream=None) -> None:
         g = self.geom
@@ -284,6 +303,24 @@ class Propagator:
             self._fb_strides = (self.nplanes * na, nb)
             self._fb_key = key
         fa, fbs = self._fb_strides
+        if self.onchip:
+            groups = self.onchip_groups(nf)
+            if getattr(self, "_oc_key", None) != (nf, groups):
+                k1 = np.arange(35)[:, None]
+                t = np.arange(4)[None, :]
+                tw = np.exp(-2j * np.pi * ((k1 * t) % 140) / 140.0).astype(np.complex64)
+                self._oc_tw = torch.from_numpy(tw.ravel().copy()).to(self.device)
+                ng = -(-nf // -(-nf // groups))
+                self._oc_part = (torch.empty((ng * self.nplanes * g.ny * g.nx,),
+                                             dtype=torch.complex64, device=self.device)
+                                 if ng > 1 else None)
+                self._oc_key = (nf, groups)
+            part = 0 if self._oc_part is None else dev.ptr(self._oc_part)
+            _lib.call("pf_prop_fbatch_onchip", dev.ptr(self.planes_dev), self.nplanes,
+                      dev.ptr(self._fb_kt), nf, ctypes.byref(g), dev.ptr(self._oc_tw),
+                      dev.ptr(uhat), uhat_fs, ill_ptr, dev.ptr(frame_w), dev.ptr(vol), part,
+                      groups, dev.stream_ptr(stream))
+            return
         if not self.transposed:
             _lib.call("pf_prop_fbatch_generic", dev.ptr(self.planes_dev), self.nplanes,
                       dev.ptr(self._fb_kh), nf, ctypes.byref(g), self.plan_x.ref, self.plan_y.ref,
@@ -423,7 +460,7 @@ def cached_engine(kind: str, slices, grid, options: tuple, factory):
     # the module's path switches are part of the key: an engine captured under other
     # switches would replay their launch sequence
     flags = (_LANES, _FAST_BATCH_CAP, _FBATCH_BYTES, _FBATCH_GENERIC, _HORNER, _HORNER_BLOCK,
-             _BATCH_BYTES)
+             _BATCH_BYTES, _ONCHIP, _ONCHIP_GROUPS)
     devi = torch.cuda.current_device() if torch.cuda.is_available() else -1
     key = (kind, devi, _slices_geometry(slices), _fingerprint(grid),
            _fingerprint(options), flags)
