@@ -205,15 +205,15 @@ int pf_prop_fbatch_generic(const pf_plane* planes, int nplanes, const double* kh
  * CTA sums its contiguous range of ceil(nf / groups) frequencies in ascending order;
  * with groups > 1 the partial planes go to ws_part ([groups][nplanes][ny][nx] c64) and a
  * second launch adds them to vol in ascending group order.  kturns: device float64 [nf]
- * = khat_f / (2 pi); tw2: device c64 [35][4] = W_140^{k1 t} (k1-major); uhat natural
- * layout [py][px] per plane offset, uhat_fs elements per frequency; frame_w: device c64
- * [nf].  Requires pf_prop_onchip_ok(g) (px = py = 140, one illumination, output plane
- * within the shared-memory budget). */
+ * = khat_f / (2 pi); uhat natural layout [py][px] per plane offset, uhat_fs elements per
+ * frequency; frame_w: device c64 [nf]; warps: warps per CTA (12 or 16; 0 = default).
+ * Requires pf_prop_onchip_ok(g) (px = py = 140, one illumination, output plane within the
+ * shared-memory budget). */
 int pf_prop_onchip_ok(const pf_prop_geom* g);
 int pf_prop_fbatch_onchip(const pf_plane* planes, int nplanes, const double* kturns, int nf,
-                          const pf_prop_geom* g, const void* tw2, const void* uhat,
-                          int64_t uhat_fs, const double* ill_xyz, const void* frame_w, void* vol,
-                          void* ws_part, int groups, void* stream);
+                          const pf_prop_geom* g, const void* uhat, int64_t uhat_fs,
+                          const double* ill_xyz, const void* frame_w, void* vol, void* ws_part,
+                          int groups, int warps, void* stream);
 
 /* K1 with the slice all-gather fused into its store (distributed.PeerSlices): each retained
  * bin of this rank's traces is written to peers[j][f * peer_stride + peer_col + trace] for

@@ -128,8 +128,8 @@ _SIGNATURES = {
     "pf_prop_fbatch_generic": [_vp, _i, _vp, _i, _P(PfPropGeom), _P(PfFftPlan), _P(PfFftPlan),
                                _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp],
     "pf_prop_onchip_ok": [_P(PfPropGeom)],
-    "pf_prop_fbatch_onchip": [_vp, _i, _vp, _i, _P(PfPropGeom), _vp, _vp, _i64, _vp, _vp, _vp,
-                              _vp, _i, _vp],
+    "pf_prop_fbatch_onchip": [_vp, _i, _vp, _i, _P(PfPropGeom), _vp, _i64, _vp, _vp, _vp, _vp,
+                              _i, _i, _vp],
     "pf_count_nonfinite": [_vp, _i64, _vp, _vp],
     "pf_fp32_probe": [_vp, _i, _i, _vp],
     "pf_nufft_interp": [_P(PfNufftGeom), _vp, _vp, _i, _vp, _vp, _vp],

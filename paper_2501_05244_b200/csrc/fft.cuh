@@ -195,30 +195,61 @@ struct Dft<11, DIR> {
   static __device__ __forceinline__ void run(float2* v) { dft_odd<11, DIR>(v); }
 };
 
+// Prime-factor (Good-Thomas) N = A * B for coprime A, B: no twiddles between the two
+// passes.  Input x[n] with n = n1 (mod A), n = n2 (mod B) (CRT map) -> A-point DFTs over n1,
+// B-point DFTs over n2 -> X[(B k1 + A k2) mod N], since W_N^{n B k1} = W_A^{n1 k1} and
+// W_N^{n A k2} = W_B^{n2 k2}.  Both index maps are compile-time register renamings.
+__host__ __device__ constexpr int pf_inv_mod(int a, int m) {
+  int r = 1;
+  while ((a * r) % m != 1) r++;
+  return r;
+}
+template <int A, int B, int DIR>
+__device__ __forceinline__ void dft_pfa(float2* v) {
+  constexpr int N = A * B;
+  constexpr int CA = B * pf_inv_mod(B % A, A), CB = A * pf_inv_mod(A % B, B);
+  float2 y[B][A];
+#pragma unroll
+  for (int n2 = 0; n2 < B; n2++) {
+#pragma unroll
+    for (int n1 = 0; n1 < A; n1++) y[n2][n1] = v[(n1 * CA + n2 * CB) % N];
+    Dft<A, DIR>::run(y[n2]);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < A; k1++) {
+    float2 z[B];
+#pragma unroll
+    for (int n2 = 0; n2 < B; n2++) z[n2] = y[n2][k1];
+    Dft<B, DIR>::run(z);
+#pragma unroll
+    for (int k2 = 0; k2 < B; k2++) v[(B * k1 + A * k2) % N] = z[k2];
+  }
+}
+
 // composite odd / mixed lengths of the mixed-radix register FFT (xfft.cuh)
 template <int DIR>
 struct Dft<6, DIR> {
-  static __device__ __forceinline__ void run(float2* v) { dft_ct<2, 3, DIR>(v); }
+  static __device__ __forceinline__ void run(float2* v) { dft_pfa<2, 3, DIR>(v); }
 };
 template <int DIR>
 struct Dft<10, DIR> {
-  static __device__ __forceinline__ void run(float2* v) { dft_ct<2, 5, DIR>(v); }
+  static __device__ __forceinline__ void run(float2* v) { dft_pfa<2, 5, DIR>(v); }
 };
 template <int DIR>
 struct Dft<15, DIR> {
-  static __device__ __forceinline__ void run(float2* v) { dft_ct<3, 5, DIR>(v); }
+  static __device__ __forceinline__ void run(float2* v) { dft_pfa<3, 5, DIR>(v); }
 };
 template <int DIR>
 struct Dft<20, DIR> {
-  static __device__ __forceinline__ void run(float2* v) { dft_ct<4, 5, DIR>(v); }
+  static __device__ __forceinline__ void run(float2* v) { dft_pfa<4, 5, DIR>(v); }
 };
 template <int DIR>
 struct Dft<30, DIR> {
-  static __device__ __forceinline__ void run(float2* v) { dft_ct<5, 6, DIR>(v); }
+  static __device__ __forceinline__ void run(float2* v) { dft_pfa<5, 6, DIR>(v); }
 };
 template <int DIR>
 struct Dft<35, DIR> {
-  static __device__ __forceinline__ void run(float2* v) { dft_ct<5, 7, DIR>(v); }
+  static __device__ __forceinline__ void run(float2* v) { dft_pfa<5, 7, DIR>(v); }
 };
 
 // One Stockham stage over `cnt` transforms (transform b at buf + b*ld).

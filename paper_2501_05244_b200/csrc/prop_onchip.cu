@@ -42,13 +42,27 @@ __device__ __forceinline__ int oc_wrap(int c) {
   return c - (c >= OC_P ? OC_P : 0);
 }
 
-// 35 x 4 line transform; element e of the line at row[e * ES], the line's own storage is
-// the exchange buffer.  v: the lane's inputs x[t + 4 m]; on return w[j][k2] = X[(t + 4 j)
-// + 35 k2] for t + 4 j < 35.  `active` lanes write the exchange; all lanes call it.
+// 140-point line transform, Cooley-Tukey 35 x 4 in natural order (the prime-factor form
+// has no twiddles but its CRT / Ruritanian index maps put the 4 lanes of a line on the same
+// bank quad for either the loads or the stores: measured slower): lane t of the line holds
+// v[m] = x[t + 4 m]; 35-point DFT in registers (itself prime-factor 5 x 7), twiddles
+// W_140^{k1 t} (tw, shared memory), one exchange through the line's own storage (element e
+// at row[e * ES]), 4-point DFTs; on return w[j][k2] = X[k1 + 35 k2] with k1 = t + 4 j < 35.
+// `active` lanes write the exchange; every lane calls it.
+// lane within the line, re-read per stage (volatile: the compiler cannot hoist the 35
+// t-dependent element offsets of every stage out of the frequency loop, which would pin
+// ~70 registers for the whole kernel)
+__device__ __forceinline__ int oc_t() {
+  unsigned l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return (int)(l & (OC_L - 1));
+}
+__device__ __forceinline__ int oc_in(int m, int t) { return t + OC_L * m; }
+__device__ __forceinline__ int oc_out(int k1, int k2) { return k1 + OC_R * k2; }
+
 template <int DIR, int ES>
 __device__ __forceinline__ void oc_fft(float2 (&v)[OC_R], float2 (&w)[OC_J][OC_L],
-                                       float2* row, const float2* __restrict__ tw, int t,
-                                       bool active) {
+                                       float2* row, const float2* tw, int t, bool active) {
   Dft<OC_R, DIR>::run(v);
   if (t != 0) {
 #pragma unroll
@@ -76,51 +90,60 @@ __device__ __forceinline__ void oc_fft(float2 (&v)[OC_R], float2 (&w)[OC_J][OC_L
 }
 
 template <int NW>
-__global__ void __launch_bounds__(NW * 32, 1)
-k_prop_onchip(const pf_plane* __restrict__ planes, const double* __restrict__ kturns_f, int nf,
-              int fpc, pf_prop_geom g, const float2* __restrict__ tw_g,
-              const float2* __restrict__ uhat, long long uhat_fs, const double* __restrict__ ill,
-              const float2* __restrict__ frame_w, float2* __restrict__ vol,
-              float2* __restrict__ ws_part, int acc_ld) {
+__device__ __forceinline__ void oc_body(const pf_plane* __restrict__ planes,
+                                        const double* __restrict__ kturns_f, int nf, int fpc,
+                                        const pf_prop_geom& g, const float2* __restrict__ uhat,
+                                        long long uhat_fs, const double* __restrict__ ill,
+                                        const float2* __restrict__ frame_w,
+                                        float2* __restrict__ vol, float2* __restrict__ ws_part,
+                                        int acc_ld) {
   extern __shared__ float2 sm[];
   const int nx = g.nx, ny = g.ny;
   float2* S = sm;                               // [OC_ROWS][OC_LD]
   float2* acc = sm + OC_ROWS * OC_LD;           // [nx][acc_ld]: acc[m][i]
   float2* tw = acc + (size_t)nx * acc_ld;       // [35][4] = W_140^{k1 t}
+  for (int e = threadIdx.x; e < OC_R * OC_L; e += NW * 32) {
+    double sn, cs;
+    sincospi(-2.0 * (double)((e / OC_L) * (e % OC_L)) / OC_P, &sn, &cs);
+    tw[e] = make_float2((float)cs, (float)sn);
+  }
   const pf_plane pl = planes[blockIdx.x];
   const int f0 = blockIdx.y * fpc, f1 = min(nf, f0 + fpc);
-  for (int e = threadIdx.x; e < OC_R * OC_L; e += NW * 32) tw[e] = tw_g[e];
   for (int e = threadIdx.x; e < nx * acc_ld; e += NW * 32) acc[e] = make_float2(0.f, 0.f);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = lane % OC_L, line = lane / OC_L;
-  const int slot = warp * OC_LPW + line;
+  const int line = lane / OC_L;
   const float scale = 1.0f / ((float)OC_P * (float)OC_P);
   const double sx = ill[0], sy = ill[1], sz = ill[2];
   const float2* up = uhat + pl.uhat_off;
   for (int f = f0; f < f1; f++) {
     const double kt = kturns_f[f];
     const float ktf = (float)kt;
-    __syncthreads();   // previous frequency's stage 4 is done with S (and tw / acc ready)
+    __syncthreads();   // previous frequency's stage 4 is done with S (and acc zeroed)
     // ---- 1: kernel columns jx = slot <= P/2, synthesised along y, y-FFT
-    if (warp * OC_LPW <= OC_H) {   // warp-uniform: slots 0 .. 71
-      const bool act = slot <= OC_H;
-      const int jx = act ? slot : OC_H;
+    for (int s0 = warp * OC_LPW; s0 <= OC_H; s0 += NW * OC_LPW) {   // warp-uniform
+      const int t = oc_t();
+      const int sl = s0 + line;
+      const bool act = sl <= OC_H;
+      const int jx = act ? sl : OC_H;
       const double lx = (double)centred(jx, OC_P) * pl.lag_dx;
       const double bx = fma(lx, lx, pl.dz * pl.dz);
-      // synthesised into the line's exchange row first (a rolled loop: the float64
-      // radius of 35 points at once would not fit the register budget)
-      float2* xrow = S + (OC_H + 1 + min(slot, OC_H)) * OC_LD;
+      // synthesised into the line's exchange row (rows P/2+1 .. P+1) first, lags 0..P/2
+      // once each (G is even in the y lag): the float64 radius of 35 points at once in
+      // registers would not fit the register budget
+      float2* xrow = S + (OC_H + 1 + jx) * OC_LD;
       if (act) {
-#pragma unroll 5
-        for (int m = 0; m < OC_R; m++) {
-          const double ly = (double)centred(t + OC_L * m, OC_P) * pl.lag_dy;
-          xrow[t + OC_L * m] = g_kernel(fma(ly, ly, bx), kt, ktf);
+#pragma unroll 3
+        for (int jy = t; jy <= OC_H; jy += OC_L) {
+          const double ly = (double)jy * pl.lag_dy;
+          const float2 gv = g_kernel(fma(ly, ly, bx), kt, ktf);
+          xrow[jy] = gv;
+          if (jy != 0 && jy != OC_H) xrow[OC_P - jy] = gv;
         }
       }
       __syncwarp();
       float2 v[OC_R];
 #pragma unroll
-      for (int m = 0; m < OC_R; m++) v[m] = xrow[t + OC_L * m];
+      for (int n1 = 0; n1 < OC_R; n1++) v[n1] = xrow[oc_in(n1, t)];
       float2 w[OC_J][OC_L];
       oc_fft<-1, 1>(v, w, xrow, tw, t, act);
       if (act) {
@@ -129,8 +152,8 @@ k_prop_onchip(const pf_plane* __restrict__ planes, const double* __restrict__ kt
         for (int j = 0; j < OC_J; j++) {
           const int k1 = t + OC_L * j;
 #pragma unroll
-          for (int k2 = 0; k2 < 3; k2++) {
-            const int ky = k1 + OC_R * k2;
+          for (int k2 = 0; k2 < OC_L; k2++) {
+            const int ky = oc_out(k1, k2);
             if (k1 < OC_R && ky <= OC_H) {
               S[ky * OC_LD + jx] = w[j][k2];
               if (mir) S[ky * OC_LD + OC_P - jx] = w[j][k2];
@@ -141,12 +164,14 @@ k_prop_onchip(const pf_plane* __restrict__ planes, const double* __restrict__ kt
     }
     __syncthreads();
     // ---- 2: x-FFT of rows ky <= P/2 in place
-    if (warp * OC_LPW <= OC_H) {
-      const bool act = slot <= OC_H;
-      float2* row = S + min(slot, OC_H) * OC_LD;
+    for (int s0 = warp * OC_LPW; s0 <= OC_H; s0 += NW * OC_LPW) {
+      const int t = oc_t();
+      const int sl = s0 + line;
+      const bool act = sl <= OC_H;
+      float2* row = S + min(sl, OC_H) * OC_LD;
       float2 v[OC_R];
 #pragma unroll
-      for (int m = 0; m < OC_R; m++) v[m] = row[t + OC_L * m];
+      for (int n1 = 0; n1 < OC_R; n1++) v[n1] = row[oc_in(n1, t)];
       float2 w[OC_J][OC_L];
       oc_fft<-1, 1>(v, w, row, tw, t, act);
       if (act) {
@@ -155,7 +180,7 @@ k_prop_onchip(const pf_plane* __restrict__ planes, const double* __restrict__ kt
           const int k1 = t + OC_L * j;
           if (k1 < OC_R) {
 #pragma unroll
-            for (int k2 = 0; k2 < OC_L; k2++) row[k1 + OC_R * k2] = w[j][k2];
+            for (int k2 = 0; k2 < OC_L; k2++) row[oc_out(k1, k2)] = w[j][k2];
           }
         }
       }
@@ -163,6 +188,7 @@ k_prop_onchip(const pf_plane* __restrict__ planes, const double* __restrict__ kt
     __syncthreads();
     // ---- 3: rows ky, P - ky: * Uhat, x-IFFT, keep the cropped columns (pairs in one warp)
     for (int s0 = warp * OC_LPW; s0 < 2 * (OC_H + 1); s0 += NW * OC_LPW) {   // warp-uniform
+      const int t = oc_t();
       const int s = min(s0 + line, 2 * OC_H + 1);
       const int q = s >> 1, side = s & 1;
       const bool act = s0 + line <= 2 * OC_H + 1 && (side == 0 || (q != 0 && q != OC_H));
@@ -172,9 +198,9 @@ k_prop_onchip(const pf_plane* __restrict__ planes, const double* __restrict__ kt
       const float2* urow = up + (long long)f * uhat_fs + (long long)(act ? ky : q) * OC_P;
       float2 v[OC_R];
 #pragma unroll
-      for (int m = 0; m < OC_R; m++) v[m] = __ldg(urow + t + OC_L * m);
+      for (int n1 = 0; n1 < OC_R; n1++) v[n1] = __ldg(urow + oc_in(n1, t));
 #pragma unroll
-      for (int m = 0; m < OC_R; m++) v[m] = cmul(grow[t + OC_L * m], v[m]);
+      for (int n1 = 0; n1 < OC_R; n1++) v[n1] = cmul(grow[oc_in(n1, t)], v[n1]);
       float2 w[OC_J][OC_L];
       oc_fft<1, 1>(v, w, row, tw, t, act);
       if (act) {
@@ -183,7 +209,7 @@ k_prop_onchip(const pf_plane* __restrict__ planes, const double* __restrict__ kt
           const int k1 = t + OC_L * j;
 #pragma unroll
           for (int k2 = 0; k2 < OC_L; k2++) {
-            const int xn = k1 + OC_R * k2;
+            const int xn = oc_out(k1, k2);
             if (k1 < OC_R && oc_wrap(xn - g.nu0x) < nx) row[xn] = w[j][k2];
           }
         }
@@ -193,13 +219,14 @@ k_prop_onchip(const pf_plane* __restrict__ planes, const double* __restrict__ kt
     // ---- 4: y-IFFT of output column m (x = nu0x + m), rows cropped, acc += (ascending f)
     const float2 fw = cscale(frame_w[f], scale);
     for (int m0 = warp * OC_LPW; m0 < nx; m0 += NW * OC_LPW) {
+      const int t = oc_t();
       const int mr = m0 + line;
       const bool act = mr < nx;
       const int m = act ? mr : m0;
       float2* col = S + oc_wrap(g.nu0x + m);
       float2 v[OC_R];
 #pragma unroll
-      for (int e = 0; e < OC_R; e++) v[e] = col[(t + OC_L * e) * OC_LD];
+      for (int n1 = 0; n1 < OC_R; n1++) v[n1] = col[oc_in(n1, t) * OC_LD];
       float2 w[OC_J][OC_L];
       oc_fft<1, OC_LD>(v, w, col, tw, t, act);
       if (act) {
@@ -211,7 +238,7 @@ k_prop_onchip(const pf_plane* __restrict__ planes, const double* __restrict__ kt
           const int k1 = t + OC_L * j;
 #pragma unroll
           for (int k2 = 0; k2 < OC_L; k2++) {
-            const int i = oc_wrap(k1 + OC_R * k2 - g.nu0y);
+            const int i = oc_wrap(oc_out(k1, k2) - g.nu0y);
             if (k1 < OC_R && i < ny) {
               float2 val = w[j][k2];
               if (g.include_illum) {
@@ -230,17 +257,32 @@ k_prop_onchip(const pf_plane* __restrict__ planes, const double* __restrict__ kt
   // the plane's sum over this CTA's frequencies: straight into the volume (one group) or
   // into the group's partial plane (k_onchip_sum adds the groups in ascending order)
   const long long plane_elems = (long long)ny * nx;
-  for (int e = threadIdx.x; e < ny * nx; e += NW * 32) {
-    const int i = e / nx, m = e - i * nx;
-    const float2 a = acc[m * acc_ld + i];
-    if (gridDim.y == 1) {
-      float2* d = vol + pl.vol_plane * plane_elems + e;
-      *d = cadd(*d, a);
-    } else {
-      ws_part[((long long)blockIdx.y * gridDim.x + blockIdx.x) * plane_elems + e] = a;
+  for (int i = warp; i < ny; i += NW) {
+    for (int m = lane; m < nx; m += 32) {
+      const float2 a = acc[m * acc_ld + i];
+      const long long e = (long long)i * nx + m;
+      if (gridDim.y == 1) {
+        float2* d = vol + pl.vol_plane * plane_elems + e;
+        *d = cadd(*d, a);
+      } else {
+        ws_part[((long long)blockIdx.y * gridDim.x + blockIdx.x) * plane_elems + e] = a;
+      }
     }
   }
 }
+
+#define OC_KARGS                                                                              \
+  const pf_plane *__restrict__ planes, const double *__restrict__ kturns_f, int nf, int fpc,  \
+      pf_prop_geom g, const float2 *__restrict__ uhat, long long uhat_fs,                      \
+      const double *__restrict__ ill, const float2 *__restrict__ frame_w,                      \
+      float2 *__restrict__ vol, float2 *__restrict__ ws_part, int acc_ld
+// 12 / 16 warps: the launch bound caps registers at 168 / 128 (fewer warps cannot use more
+// registers: each SM sub-partition holds 16 K registers for its share of the warps)
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_prop_onchip(OC_KARGS) {
+  oc_body<NW>(planes, kturns_f, nf, fpc, g, uhat, uhat_fs, ill, frame_w, vol, ws_part, acc_ld);
+}
+#undef OC_KARGS
 
 // vol[plane k] += sum over groups g (ascending) of ws_part[g][k]
 __global__ void k_onchip_sum(const pf_plane* __restrict__ planes, int nplanes, int groups,
@@ -267,7 +309,8 @@ int acc_pitch(int ny) {
 }
 
 size_t onchip_smem(const pf_prop_geom& g) {
-  return ((size_t)OC_ROWS * OC_LD + (size_t)g.nx * acc_pitch(g.ny) + OC_R * OC_L) * sizeof(float2);
+  return ((size_t)OC_ROWS * OC_LD + (size_t)g.nx * acc_pitch(g.ny) + OC_R * OC_L) *
+         sizeof(float2);
 }
 
 }  // namespace
@@ -283,16 +326,19 @@ extern "C" int pf_prop_onchip_ok(const pf_prop_geom* g) {
 }
 
 extern "C" int pf_prop_fbatch_onchip(const pf_plane* planes, int nplanes, const double* kturns,
-                                     int nf, const pf_prop_geom* g, const void* tw2,
-                                     const void* uhat, int64_t uhat_fs, const double* ill_xyz,
-                                     const void* frame_w, void* vol, void* ws_part, int groups,
+                                     int nf, const pf_prop_geom* g, const void* uhat,
+                                     int64_t uhat_fs, const double* ill_xyz, const void* frame_w,
+                                     void* vol, void* ws_part, int groups, int warps,
                                      void* stream) {
-  PF_ARG_CHECK(g && planes && kturns && tw2 && uhat && ill_xyz && frame_w && vol && nplanes >= 1 &&
+  PF_ARG_CHECK(g && planes && kturns && uhat && ill_xyz && frame_w && vol && nplanes >= 1 &&
                    nf >= 1 && groups >= 1 && groups <= nf,
                "pf_prop_fbatch_onchip: bad args");
   PF_ARG_CHECK(pf_prop_onchip_ok(g),
                "pf_prop_fbatch_onchip: needs px = py = 140, one illumination and a plane that "
                "fits shared memory");
+  if (warps <= 0) warps = OC_NW;
+  PF_ARG_CHECK(warps == 12 || warps == 16,
+               "pf_prop_fbatch_onchip: warps per CTA must be 12 or 16 (0: default)");
   const int fpc = pf_cdiv(nf, groups);
   const int gy = pf_cdiv(nf, fpc);   // groups actually populated
   PF_ARG_CHECK(gy == 1 || ws_part, "pf_prop_fbatch_onchip: ws_part needed for groups > 1");
@@ -303,11 +349,18 @@ extern "C" int pf_prop_fbatch_onchip(const pf_plane* planes, int nplanes, const 
     int d = 0, smax = 232448;
     cudaGetDevice(&d);
     cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
-    cudaFuncSetAttribute(k_prop_onchip<OC_NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    cudaFuncSetAttribute(k_prop_onchip<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    cudaFuncSetAttribute(k_prop_onchip<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
   }
-  k_prop_onchip<OC_NW><<<dim3(nplanes, gy), OC_NW * 32, smem, st>>>(
-      planes, kturns, nf, fpc, *g, (const float2*)tw2, (const float2*)uhat, uhat_fs, ill_xyz,
-      (const float2*)frame_w, (float2*)vol, (float2*)ws_part, acc_pitch(g->ny));
+  const dim3 grid(nplanes, gy);
+#define OC_LAUNCH(KERN, NWV)                                                                  \
+  KERN<<<grid, NWV * 32, smem, st>>>(planes, kturns, nf, fpc, *g,                             \
+                                                    (const float2*)uhat, uhat_fs, ill_xyz,     \
+                                                    (const float2*)frame_w, (float2*)vol,      \
+                                                    (float2*)ws_part, acc_pitch(g->ny))
+  if (warps == 16) OC_LAUNCH(k_prop_onchip<16>, 16);
+  else OC_LAUNCH(k_prop_onchip<12>, 12);
+#undef OC_LAUNCH
   PF_LAUNCH_CHECK("k_prop_onchip");
   if (gy > 1) {
     const long long pe = (long long)g->ny * g->nx;

@@ -50,6 +50,7 @@ _FBATCH_BYTES = int(os.environ.get("PF_FBATCH_MB", "256")) << 20
 _FBATCH_GENERIC = os.environ.get("PF_FBATCH_GENERIC", "1") != "0"
 _ONCHIP = os.environ.get("PF_ONCHIP", "1") != "0"   # P = 140: whole units in shared memory
 _ONCHIP_GROUPS = int(os.environ.get("PF_ONCHIP_GROUPS", "0"))   # 0: from the geometry
+_ONCHIP_WARPS = int(os.environ.get("PF_ONCHIP_WARPS", "0"))     # 0: the library default
 _HORNER = os.environ.get("PF_HORNER", "1") != "0"   # kernel C phases by Horner's rule
 _HORNER_BLOCK = int(os.environ.get("PF_HORNER_BLOCK", "32"))   # frequencies per nested block
 
@@ -306,10 +307,6 @@ class Propagator:
         if self.onchip:
             groups = self.onchip_groups(nf)
             if getattr(self, "_oc_key", None) != (nf, groups):
-                k1 = np.arange(35)[:, None]
-                t = np.arange(4)[None, :]
-                tw = np.exp(-2j * np.pi * ((k1 * t) % 140) / 140.0).astype(np.complex64)
-                self._oc_tw = torch.from_numpy(tw.ravel().copy()).to(self.device)
                 ng = -(-nf // -(-nf // groups))
                 self._oc_part = (torch.empty((ng * self.nplanes * g.ny * g.nx,),
                                              dtype=torch.complex64, device=self.device)
@@ -317,9 +314,9 @@ class Propagator:
                 self._oc_key = (nf, groups)
             part = 0 if self._oc_part is None else dev.ptr(self._oc_part)
             _lib.call("pf_prop_fbatch_onchip", dev.ptr(self.planes_dev), self.nplanes,
-                      dev.ptr(self._fb_kt), nf, ctypes.byref(g), dev.ptr(self._oc_tw),
-                      dev.ptr(uhat), uhat_fs, ill_ptr, dev.ptr(frame_w), dev.ptr(vol), part,
-                      groups, dev.stream_ptr(stream))
+                      dev.ptr(self._fb_kt), nf, ctypes.byref(g), dev.ptr(uhat), uhat_fs, ill_ptr,
+                      dev.ptr(frame_w), dev.ptr(vol), part, groups, _ONCHIP_WARPS,
+                      dev.stream_ptr(stream))
             return
         if not self.transposed:
             _lib.call("pf_prop_fbatch_generic", dev.ptr(self.planes_dev), self.nplanes,
@@ -460,7 +457,7 @@ def cached_engine(kind: str, slices, grid, options: tuple, factory):
     # the module's path switches are part of the key: an engine captured under other
     # switches would replay their launch sequence
     flags = (_LANES, _FAST_BATCH_CAP, _FBATCH_BYTES, _FBATCH_GENERIC, _HORNER, _HORNER_BLOCK,
-             _BATCH_BYTES, _ONCHIP, _ONCHIP_GROUPS)
+             _BATCH_BYTES, _ONCHIP, _ONCHIP_GROUPS, _ONCHIP_WARPS)
     devi = torch.cuda.current_device() if torch.cuda.is_available() else -1
     key = (kind, devi, _slices_geometry(slices), _fingerprint(grid),
            _fingerprint(options), flags)
