@@ -120,7 +120,8 @@ def test_rescale_to_torus_round_trip_and_errors():
 
 
 @pytest.mark.parametrize("shape,modes,nb", [((12, 10), (5, 6), 2), ((8, 12, 10), (3, 5, 6), 2),
-                                            ((6, 9, 8), (6, 4, 3), 1)])
+                                            ((6, 9, 8), (6, 4, 3), 1), ((12, 10, 6), (5, 4, 3), 2),
+                                            ((40, 54, 54), (20, 27, 27), 2)])
 def test_fftn_pruned_line_sets(monkeypatch, shape, modes, nb):
     """The NUFFT's pruned fftn (host line-set logic) against numpy: type 1 keeps every
     kept output, type 2 (zero off the kept slots) is exact everywhere.  pf_fft_lines is
