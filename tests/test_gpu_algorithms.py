@@ -77,6 +77,7 @@ def test_generic_fbatch_matches_per_frequency(rng, monkeypatch, n_ill):
     grid = pf.CuboidGrid(pf.UniformGrid3D(64, 64, 5, p, p, 0.3, -1 + p / 2, -1 + p / 2, 0.5))
     eng = Nursd1Engine(sl, grid)
     assert not eng.prop.transposed and eng.px == 140
+    eng.prop.onchip = False   # the Stockham path (the on-chip kernel: test_gpu_onchip.py)
     coeff = pf.phasor.device_coefficients(sl)
     assert eng.prop.fbatch_ok(sl.n_freq, 1)
     batched = eng.run(coeff).clone()
