@@ -331,6 +331,11 @@ int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0, const floa
                            int64_t fine_stride, int n_illum, const double* ill, double khat,
                            int include_illum, float scale, const void* frame_w, int n_frames,
                            void* vol, int64_t vol_frame_stride, void* stream);
+/* Readout kernel for the reference's default stencil (w = 8, 17 x 17 taps): 2 (default)
+ * the 16 x 16 trimmed kernel (the far edge tap of each axis, <= 6.5e-9 of the centre
+ * weight, is not loaded), 1 the full 17 x 17 kernel, 0 the general kernel; mode < 0 only
+ * queries.  Returns the previous mode (also PF_INTERP_H17 in the environment). */
+int pf_nufft_interp_mode(int mode);
 /* The same readout for voxels at arbitrary depths (z-Chebyshev): voxel l takes the
  * Lagrange-weighted sum lw[l][m] over its slab's `nodes` consecutive fine grids (the
  * first at plane_idx[l]) of the same stencil; nodes = 1, lw = NULL is

@@ -132,6 +132,7 @@ _SIGNATURES = {
                               _i, _i, _vp],
     "pf_count_nonfinite": [_vp, _i64, _vp, _vp],
     "pf_fp32_probe": [_vp, _i, _i, _vp],
+    "pf_nufft_interp_mode": [_i],
     "pf_nufft_interp": [_P(PfNufftGeom), _vp, _vp, _i, _vp, _vp, _vp],
     "pf_nufft_interp2_batch": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _i64, _i64,
                                _i, _vp, _d, _i, _f, _vp, _i, _vp, _i64, _vp],
@@ -167,7 +168,8 @@ _RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, 
              "pf_prop_ws_spectrum": ctypes.c_int64, "pf_rsd_workspace_bytes": ctypes.c_int64,
              "pf_srsd_workspace_bytes": ctypes.c_int64, "pf_nursd1_workspace_bytes": ctypes.c_int64,
              "pf_nursd2_workspace_bytes": ctypes.c_int64,
-             "pf_prop_fast": ctypes.c_int, "pf_prop_onchip_ok": ctypes.c_int}
+             "pf_prop_fast": ctypes.c_int, "pf_prop_onchip_ok": ctypes.c_int,
+             "pf_nufft_interp_mode": ctypes.c_int}
 
 _lib = None
 

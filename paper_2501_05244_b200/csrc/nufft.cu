@@ -505,14 +505,109 @@ k_interp2_h17(pf_nufft_geom G, const int* __restrict__ i0, const float* __restri
   }
 }
 
-// PF_INTERP_H17=0 keeps the general half-warp kernel for W = 17 (A/B measurements)
-bool interp_h17_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("PF_INTERP_H17");
-    on = (e == nullptr || atoi(e) != 0) ? 1 : 0;
+// W = 17 trimmed to 16 x 16 taps.  The reference's Gaussian (tau = pi w / (s (s - 1/2) m^2),
+// w = 8, s = 2) weighs a tap j cells from the point by exp(-(3 pi / 32) j^2): of the two
+// edge taps of an axis the one on the far side of the anchor lies >= 8 cells away and weighs
+// <= 6.5e-9 of the centre tap, i.e. <= 2e-9 of the stencil's sum -- a factor 30 under the
+// float32 rounding of the 289-term sum itself.  It is not loaded: each axis keeps the 16
+// taps nearest the point (origin i0 - 8 when the anchor lies right of the point, i0 - 7
+// otherwise), lane c owns column c for all 16 rows, and the row-16 / column-16 special
+// cases of k_interp2_h17 disappear (16 loads per lane per point instead of 18-19).
+template <int UNR>
+__global__ void __launch_bounds__(256)
+k_interp2_h16(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
+              const double* __restrict__ xyz, const int* __restrict__ plane_idx,
+              const long long* __restrict__ dst_idx, int npts, int plane0,
+              const float2* __restrict__ fine, long long fine_plane_stride,
+              long long fine_stride, int n_illum, const double* __restrict__ ill,
+              double kturns, int include_illum, float scale,
+              const float2* __restrict__ frame_w, int n_frames, float2* __restrict__ vol,
+              long long vol_frame_stride, int nodes, const float* __restrict__ lw) {
+  constexpr int w = 8;
+  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+  const int l = blockIdx.x * (blockDim.x >> 4) + ((threadIdx.x >> 5) << 1) + half;
+  const bool live = l < npts;
+  const int lc = live ? l : 0;
+  const int mry = G.mr[1], mrx = G.mr[2], fe = mry * mrx;
+  const float dyl = d0[3 * lc + 1], dxl = d0[3 * lc + 2];
+  // d0 = anchor - point: anchor right of the point -> the far edge tap is j = +8
+  const int sx = dxl > 0.f ? 0 : 1, sy = dyl > 0.f ? 0 : 1;
+  const float dx = dxl + (float)(hl - w + sx) * G.h[2];
+  const float wx = __expf(-dx * dx * G.inv4tau[2]);
+  const float dy = dyl + (float)(hl - w + sy) * G.h[1];
+  const float wy_own = __expf(-dy * dy * G.inv4tau[1]);
+  // anchors lie in [0, mr]: the stencil origin wraps at most once
+  const int cx = wrap_once(wrap_once(i0[3 * lc + 2] - w + sx, mrx) + hl, mrx);
+  const int r0 = wrap_once(i0[3 * lc + 1] - w + sy, mry) * mrx;   // row 0's offset
+  const float2* fplane = fine + (long long)(plane_idx[lc] - plane0) * fine_plane_stride;
+  float2 tot = make_float2(0.f, 0.f);
+  for (int p = 0; p < n_illum; p++) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int m = 0; m < nodes; m++) {
+      const float2* col = fplane + (long long)m * fine_plane_stride +
+                          (long long)p * fine_stride + cx;
+      const float wxm = lw ? wx * __ldg(lw + (long long)lc * nodes + m) : wx;
+      int ro = r0;
+#pragma unroll UNR
+      for (int oy = 0; oy < 16; oy++) {
+        const float wy = __shfl_sync(0xffffffffu, wy_own, (half << 4) + oy);
+        const float2 f = __ldg(col + ro);
+        const float ww = wxm * wy;
+        acc.x = fmaf(ww, f.x, acc.x);
+        acc.y = fmaf(ww, f.y, acc.y);
+        ro += mrx;
+        if (ro >= fe) ro -= fe;
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    float2 val = cscale(acc, scale);
+    if (include_illum && hl == 0) {
+      const double ex = xyz[3 * lc] - ill[3 * p], ey = xyz[3 * lc + 1] - ill[3 * p + 1];
+      const double ez = xyz[3 * lc + 2] - ill[3 * p + 2];
+      val = cmul(val, expi_reduced(PF_TWO_PI * kturns * sqrt(ex * ex + ey * ey + ez * ez)));
+    }
+    tot = cadd(tot, val);
   }
-  return on != 0;
+  if (hl == 0 && live) {
+    const long long dst = dst_idx[l];
+    for (int f = 0; f < n_frames; f++) {
+      float2* d = vol + f * vol_frame_stride + dst;
+      *d = cadd(*d, cmul(tot, frame_w[f]));
+    }
+  }
+}
+
+// PF_INTERP_H17: 2 (default) the 16 x 16 trimmed kernel for W = 17, 1 the full 17 x 17
+// specialisation, 0 the general half-warp kernel (A/B measurements)
+int g_interp_mode = -1;
+int interp_h17_mode() {
+  if (g_interp_mode < 0) {
+    const char* e = getenv("PF_INTERP_H17");
+    g_interp_mode = e == nullptr ? 2 : atoi(e);
+  }
+  return g_interp_mode;
+}
+bool interp_h17_enabled() { return interp_h17_mode() != 0; }
+int interp_unroll() {
+  static int u = -1;
+  if (u < 0) {
+    const char* e = getenv("PF_INTERP_UNROLL");
+    u = e ? atoi(e) : 8;
+  }
+  return u;
+}
+// the far edge tap (8 cells away) must weigh < 2e-8 of the centre tap on both axes
+bool interp_trim_ok(const pf_nufft_geom& g) {
+  if (interp_h17_mode() != 2) return false;
+  for (int a = 1; a <= 2; a++) {
+    const float d = 8.0f * g.h[a];
+    if (d * d * g.inv4tau[a] < 17.75f) return false;
+  }
+  return true;
 }
 
 extern "C" int pf_nufft_interp2_nodes(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
@@ -711,6 +806,12 @@ extern "C" int pf_nufft_interp(const pf_nufft_geom* g, const int32_t* i0, const 
   return 0;
 }
 
+extern "C" int pf_nufft_interp_mode(int mode) {
+  const int prev = interp_h17_mode();
+  if (mode >= 0 && mode <= 2) g_interp_mode = mode;
+  return prev;
+}
+
 extern "C" int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
                                       const double* xyz, const int32_t* plane_idx,
                                       const int64_t* dst_idx, int npts, int plane0,
@@ -729,6 +830,22 @@ extern "C" int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0,
   }
   if (half && g->w == 8 && (long long)g->mr[1] * g->mr[2] < (1LL << 31) &&
       interp_h17_enabled()) {   // W = 17
+    if (interp_trim_ok(*g)) {
+      if (interp_unroll() == 8)
+        k_interp2_h16<8><<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
+            *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0,
+            (const float2*)fine, fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI,
+            include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol,
+            vol_frame_stride, 1, nullptr);
+      else
+        k_interp2_h16<4><<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
+            *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0,
+            (const float2*)fine, fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI,
+            include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol,
+            vol_frame_stride, 1, nullptr);
+      PF_LAUNCH_CHECK("k_interp2_h16");
+      return 0;
+    }
     k_interp2_h17<<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
         *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine,
         fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,
@@ -766,6 +883,22 @@ extern "C" int pf_nufft_interp2_nodes(const pf_nufft_geom* g, const int32_t* i0,
                "pf_nufft_interp2_nodes: bad args (2D, stencil width <= 32, weights for nodes > 1)");
   if (npts == 0) return 0;
   if (g->w == 8 && (long long)g->mr[1] * g->mr[2] < (1LL << 31) && interp_h17_enabled()) {
+    if (interp_trim_ok(*g)) {
+      if (interp_unroll() == 8)
+        k_interp2_h16<8><<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
+            *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0,
+            (const float2*)fine, fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI,
+            include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol,
+            vol_frame_stride, nodes, lw);
+      else
+        k_interp2_h16<4><<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
+            *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0,
+            (const float2*)fine, fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI,
+            include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol,
+            vol_frame_stride, nodes, lw);
+      PF_LAUNCH_CHECK("k_interp2_h16");
+      return 0;
+    }
     k_interp2_h17<<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(
         *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine,
         fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,

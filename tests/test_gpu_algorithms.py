@@ -137,6 +137,32 @@ def test_nursd2_offlattice_voxels(rng):
     assert O.rel_l2(vol.field, O.nursd2(sl, ev)) < TOL
 
 
+def test_nursd2_trimmed_readout_matches_full_stencil(rng):
+    """The default readout for w = 8 keeps 16 x 16 of the 17 x 17 taps (the far edge tap of
+    an axis weighs <= 6.5e-9 of the centre tap): against the full stencil the volume moves
+    by less than float32 rounding of the sum, and both match the oracle alike."""
+    from paper_2501_05244_b200 import _lib
+    n = 32
+    p = 0.02
+    g = pf.UniformGrid2D(n, n, p, p, -(n - 1) * p / 2, -(n - 1) * p / 2, 0.0)
+    sl = _rand_slices(rng, pf.UniformRelay(g), n_freq=3, n_ill=1)
+    pts = rng.uniform(-0.25, 0.25, size=(4000, 2))
+    pts[:200] = np.round(pts[:200] / p) * p          # some voxels on relay-lattice nodes
+    ev = pf.ExplicitVoxels((pf.VoxelPlane(0.6, pf.PointList(pts[:2000])),
+                            pf.VoxelPlane(0.8, pf.PointList(pts[2000:]))))
+    ref = O.nursd2(sl, ev)
+    prev = _lib.call("pf_nufft_interp_mode", 2)
+    try:
+        trimmed = pf.nursd2(sl, ev).field
+        _lib.call("pf_nufft_interp_mode", 1)
+        full = pf.nursd2(sl, ev).field
+    finally:
+        _lib.call("pf_nufft_interp_mode", prev)
+    assert O.rel_l2(trimmed, full) < 2e-7
+    e_t, e_f = O.rel_l2(trimmed, ref), O.rel_l2(full, ref)
+    assert e_t < 2e-6 and e_f < 2e-6 and abs(e_t - e_f) < 2e-7, (e_t, e_f)
+
+
 def test_config2_composed_small(rng):
     """Config-2 family (non-planar relay -> arbitrary voxels) against the composed oracle."""
     from paper_2501_05244_b200.algorithms import nursd3d_explicit
