@@ -25,6 +25,9 @@ constexpr int K1_KB = 33;    // non-redundant bins of a real 64-point DFT
 
 // 64-point real DFT of x[0..63]: the non-redundant bins k in [0, 32] selected by
 // `mask` (bit k; warp-uniform) are stored to dst[0], dst[1], ... in ascending k.
+// TWICE: the bins are stored doubled (the split step's two halvings are left to the
+// caller, who folds one exact 0.5 into the final scale: 8 instead of 12 instructions a bin).
+template <bool TWICE = false>
 __device__ __forceinline__ void real_dft64_sel(const float* x, unsigned long long mask,
                                                float2* dst, int stride = 1) {
   float2 z[32];
@@ -36,9 +39,10 @@ __device__ __forceinline__ void real_dft64_sel(const float* x, unsigned long lon
     if ((mask >> k) & 1ull) {
       const float2 a = z[k & 31];
       const float2 b = cconj(z[(32 - k) & 31]);
-      const float2 e = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y + b.y));
+      const float hf = TWICE ? 1.0f : 0.5f;
+      const float2 e = make_float2(hf * (a.x + b.x), hf * (a.y + b.y));
       // o = (a - b) / (2i)
-      const float2 o = make_float2(0.5f * (a.y - b.y), -0.5f * (a.x - b.x));
+      const float2 o = make_float2(hf * (a.y - b.y), -hf * (a.x - b.x));
       // W_64^k = exp(-2 pi i k / 64)
       const float c = Unit<64>::c(k & 63), sn = -Unit<64>::s(k & 63);
       *dst = make_float2(e.x + o.x * c - o.y * sn, e.y + o.x * sn + o.y * c);
@@ -49,7 +53,7 @@ __device__ __forceinline__ void real_dft64_sel(const float* x, unsigned long lon
 
 // all 33 bins (the TMA-fed variant)
 __device__ __forceinline__ void real_dft64(const float* x, float2* X) {
-  real_dft64_sel(x, (1ull << 33) - 1ull, X);
+  real_dft64_sel<false>(x, (1ull << 33) - 1ull, X);
 }
 
 // Only the inner bins k = b mod 64 the retained bins need are formed and
@@ -107,7 +111,7 @@ k_temporal_dft(const float* __restrict__ hist, long long n_traces, const int* __
       float x[64];
 #pragma unroll
       for (int q = 0; q < 64; q++) x[q] = __ldg(h + q * M);
-      real_dft64_sel(x, mask, xs + g * ts + r, MP);
+      real_dft64_sel<false>(x, mask, xs + g * ts + r, MP);
     }
     __syncthreads();
     for (int p0 = 0; p0 < 2 * G * F; p0 += K1_THREADS) {
@@ -163,11 +167,13 @@ k_temporal_dft_pair(const float* __restrict__ hist, long long n_traces,
   static_assert(M >= 32, "one or more whole warps per trace");
   constexpr int G = K1_THREADS / M;
   constexpr int T = M * K1_L;
-  constexpr int MP = M + 2 - (M & 1);
-  extern __shared__ float2 smem[];
+  // rows of M + 4 float2 (= 4 mod 16): the four bins x two halves of a quarter warp read
+  // eight different 16-byte bank groups in phase B's 16-byte loads
+  constexpr int MP = M + 4;
+  extern __shared__ __align__(16) float2 smem[];
   float2* tws = smem;
   int* ks = reinterpret_cast<int*>(tws + F * MP);
-  float2* xs = reinterpret_cast<float2*>(ks + ((F + 1) & ~1));
+  float2* xs = reinterpret_cast<float2*>(ks + ((F + 3) & ~3));
   unsigned long long mask = inner_mask;
   if (mask == 0) {
     for (int f = 0; f < F; f++) {
@@ -176,7 +182,7 @@ k_temporal_dft_pair(const float* __restrict__ hist, long long n_traces,
     }
   }
   const int nk = __popcll(mask);
-  const int ts = nk * MP + (((4 - nk * MP) % 16) + 16) % 16;
+  const int ts = nk * MP;   // even: every row of every trace stays 16-byte aligned
   if (ts > ts_cap) return;
   for (int f = threadIdx.x; f < F; f += K1_THREADS) {
     const int k = bins[f] & 63;
@@ -200,7 +206,7 @@ k_temporal_dft_pair(const float* __restrict__ hist, long long n_traces,
     float x[64];
 #pragma unroll
     for (int q = 0; q < 64; q++) x[q] = __ldg(h + q * M);
-    real_dft64_sel(x, mask, xg + r, MP);
+    real_dft64_sel<true>(x, mask, xg + r, MP);
     trace_sync(1 + g, M);
     for (int q0 = 0; q0 < 2 * F; q0 += M) {
       const int q = q0 + r;
@@ -209,16 +215,26 @@ k_temporal_dft_pair(const float* __restrict__ hist, long long n_traces,
       const int kv = ks[f];
       float2 acc = make_float2(0.f, 0.f);
       if (valid) {
-        const float2* src = xg + (kv & 255) * MP + hh;
-        const float2* tw = tws + f * MP + hh;
-#pragma unroll 16
-        for (int j = 0; j < M / 2; j++) cacc(acc, src[2 * j], tw[2 * j]);
+        // the two threads of a bin take the column pairs (4 j + 2 hh, + 1): one 16-byte
+        // load each of the parked bins and the twiddles per two terms
+        const float4* src = reinterpret_cast<const float4*>(xg + (kv & 255) * MP + 2 * hh);
+        const float4* tw = reinterpret_cast<const float4*>(tws + f * MP + 2 * hh);
+        float2 acc1 = make_float2(0.f, 0.f);
+#pragma unroll 8
+        for (int j = 0; j < M / 4; j++) {
+          const float4 sv = src[2 * j], tv = tw[2 * j];
+          cacc(acc, make_float2(sv.x, sv.y), make_float2(tv.x, tv.y));
+          cacc(acc1, make_float2(sv.z, sv.w), make_float2(tv.z, tv.w));
+        }
+        acc.x += acc1.x;
+        acc.y += acc1.y;
       }
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
       if (valid && hh == 0) {
         if (kv >> 8) acc.y = -acc.y;
-        const float2 val = cmul(acc, wphase[f]);
+        // 0.5: the split step's halving (exact), left out of the parked bins
+        const float2 val = cscale(cmul(acc, wphase[f]), 0.5f);
         if (n_peers == 0) {
           out[(long long)f * out_stride + trace] = val;
         } else {
@@ -410,10 +426,10 @@ int launch_k1(const float* hist, long long n_traces, const int* bins, const floa
   // (the kernel parks exactly inner_mask's bins when it is given, else at most min(33, FC)
   // per chunk, so ts <= ts_cap by construction)
   int nk = n_inner >= 1 ? n_inner : (K1_KB < FC ? K1_KB : FC);
-  constexpr int MP = M + 2 - (M & 1);
+  constexpr int MP = M + 4;          // the decoupled kernel's row pitch (>= the lock-step M + 2)
   const int ts_cap = nk * MP + 15;   // per-trace stride incl. the bank-alignment pad
   const size_t smem = ((size_t)G * ts_cap + (size_t)FC * MP) * sizeof(float2) +
-                      ((FC + 1) & ~1) * sizeof(int);
+                      ((FC + 3) & ~3) * sizeof(int);
   static PfDevOnce attr;  
   if (attr.first()) {
     cudaFuncSetAttribute(k_temporal_dft<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
