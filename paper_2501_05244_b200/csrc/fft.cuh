@@ -344,7 +344,8 @@ __host__ __device__ inline int xfft_L(int n) {
 // v: the lane's R inputs; row: the line's exchange row base in shared memory (>= L R
 // elements, the line's own, written and read by this line's lanes only); tw2: the plan's
 // k1-major twiddle table [R][L] (W_n^{k1 t}); t: lane within the line.
-template <int L, int DIR>
+// TWS: the table lives in shared memory (plain loads) instead of global memory (__ldg).
+template <int L, int DIR, bool TWS = false>
 __device__ __forceinline__ void xfft(float2 (&v)[XFFT_R], float2 (&w)[xfft_J(L)][L],
                                      float2* __restrict__ row, const float2* __restrict__ tw2,
                                      int t, bool active) {
@@ -353,7 +354,7 @@ __device__ __forceinline__ void xfft(float2 (&v)[XFFT_R], float2 (&w)[xfft_J(L)]
   if (t != 0) {
 #pragma unroll
     for (int k1 = 1; k1 < R; k1++) {
-      const float2 c = __ldg(tw2 + k1 * L + t);
+      const float2 c = TWS ? tw2[k1 * L + t] : __ldg(tw2 + k1 * L + t);
       v[k1] = DIR < 0 ? cmul(v[k1], c) : cmulc(v[k1], c);
     }
   }
@@ -379,7 +380,7 @@ __device__ __forceinline__ void xfft(float2 (&v)[XFFT_R], float2 (&w)[xfft_J(L)]
 // place, natural order in and out; each warp owns 32 / L lines at a time and uses their
 // own rows as the exchange buffer.  Block-wide: every thread calls it; synchronised on
 // return.
-template <int L, int DIR>
+template <int L, int DIR, bool TWS = false>
 __device__ __forceinline__ void xfft_tile(float2* __restrict__ a, int ld, int cnt,
                                        const float2* __restrict__ tw2) {
   constexpr int LPW = 32 / L, J = xfft_J(L);
@@ -393,7 +394,7 @@ __device__ __forceinline__ void xfft_tile(float2* __restrict__ a, int ld, int cn
 #pragma unroll
     for (int m = 0; m < XFFT_R; m++) v[m] = row[t + L * m];
     float2 w[J][L];
-    xfft<L, DIR>(v, w, row, tw2, t, active);
+    xfft<L, DIR, TWS>(v, w, row, tw2, t, active);
     if (active) {
 #pragma unroll
       for (int j = 0; j < J; j++) {

@@ -99,6 +99,107 @@ k_t2_cols(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fine_str
   }
 }
 
+// ---- split passes for mr = 2 m (the reference's fine grid whenever 2 m is a fast length) --
+// A fine line holds the m centred modes c[k], k in [-m/2, m - m/2), and zeros elsewhere, so
+// its 2 m-point inverse transform splits by output parity into two m-point transforms of
+// the modes alone:
+//     X[2 j]     = sum_k c[k]                    e^{2 pi i j k / m}
+//     X[2 j + 1] = sum_k c[k] e^{i pi k / m}     e^{2 pi i j k / m}
+// (the radix-2 decimation-in-frequency step whose other half of the inputs is zero).  Each
+// fine line becomes two half-lines of length m = 35 L' run by the register FFT with L'
+// lanes: no zero is loaded or transformed, and for 700 = 2 x 350 the lines fill 30 of a
+// warp's 32 lanes (3 lines x 10 lanes) where the 700-point transform fills 20.  The
+// half-length twiddle table W_m^{k1 t} is formed in shared memory from the 2 m plan's
+// unit roots.  Results differ from the unsplit passes by float32 rounding only.
+template <int HL>
+__device__ __forceinline__ void t2_half_table(float2* tw2, int m, const float2* __restrict__ roots2m) {
+  for (int e = threadIdx.x; e < XFFT_R * HL; e += T2_THREADS) {
+    const int k1 = e / HL, t = e - k1 * HL;
+    tw2[e] = __ldg(roots2m + 2 * ((k1 * t) % m));
+  }
+}
+
+template <int HL>
+__global__ void __launch_bounds__(T2_THREADS, 2)
+k_t2_rows_split(pf_nufft_geom G, const float2* __restrict__ S, long long s_stride,
+                const float* __restrict__ ky, const float* __restrict__ kx, int nv,
+                float2* __restrict__ fine, long long fine_stride, pf_fft_plan plan_x, int cnt) {
+  extern __shared__ float2 sm[];
+  const int mrx = G.mr[2], mx = G.m[2], my = G.m[1], mry = G.mr[1];
+  const int ld = pf_ld(mx);
+  float2* a = sm;                                   // [2 cnt][ld]: line c -> rows 2c (even), 2c + 1
+  float2* tw2 = sm + (size_t)2 * cnt * ld;          // [35][HL]
+  const float2* roots = reinterpret_cast<const float2*>(plan_x.tw);
+  t2_half_table<HL>(tw2, mx, roots);
+  const long long nlines = (long long)nv * my;
+  const long long l0 = (long long)blockIdx.x * cnt;
+  const int nl = (int)(nlines - l0 < cnt ? nlines - l0 : cnt);
+  const FastDiv dmx(mx);
+  for (int e = threadIdx.x; e < nl * mx; e += T2_THREADS) {
+    const int c = dmx.div(e), q = e - c * mx;
+    const long long l = l0 + c;
+    const int v = (int)(l / my), i = (int)(l - (long long)v * my);
+    const int cy = i - my / 2, cx = q - mx / 2;
+    const int jy = natural(cy, my), jx = natural(cx, mx);
+    const float den = 1.0f * ky[i] * kx[q];
+    const float2 s = S[(long long)v * s_stride + (long long)jy * mx + jx];
+    const float2 val = make_float2(s.x / den, s.y / den);
+    a[(2 * c) * ld + jx] = val;
+    a[(2 * c + 1) * ld + jx] = cmulc(val, __ldg(roots + (cx < 0 ? cx + mrx : cx)));
+  }
+  __syncthreads();
+  xfft_tile<HL, 1, true>(a, ld, 2 * nl, tw2);
+  for (int e = threadIdx.x; e < nl * mx; e += T2_THREADS) {
+    const int c = dmx.div(e), j = e - c * mx;
+    const long long l = l0 + c;
+    const int v = (int)(l / my), i = (int)(l - (long long)v * my);
+    const int cy = i - my / 2;
+    const int fy = cy < 0 ? cy + mry : cy;
+    const float2 ev = a[(2 * c) * ld + j], od = a[(2 * c + 1) * ld + j];
+    *reinterpret_cast<float4*>(fine + (long long)v * fine_stride + (long long)fy * mrx + 2 * j) =
+        make_float4(ev.x, ev.y, od.x, od.y);
+  }
+}
+
+template <int HL>
+__global__ void __launch_bounds__(T2_THREADS, 2)
+k_t2_cols_split(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fine_stride,
+                pf_fft_plan plan_y, int cnt) {
+  extern __shared__ float2 sm[];
+  __shared__ long long lbase[64];
+  const int mrx = G.mr[2], my = G.m[1], mry = G.mr[1];
+  const int ld = pf_ld(my);
+  float2* a = sm;                                   // [2 cnt][ld]
+  float2* tw2 = sm + (size_t)2 * cnt * ld;
+  const float2* roots = reinterpret_cast<const float2*>(plan_y.tw);
+  t2_half_table<HL>(tw2, my, roots);
+  const long long nlines = (long long)nv * mrx;
+  const long long l0 = (long long)blockIdx.x * cnt;
+  const int nl = (int)(nlines - l0 < cnt ? nlines - l0 : cnt);
+  for (int c = threadIdx.x; c < nl; c += T2_THREADS) {
+    const long long l = l0 + c;
+    const long long v = l / mrx;
+    lbase[c] = v * fine_stride + (l - v * mrx);
+  }
+  __syncthreads();
+  const FastDiv dnl(nl);
+  for (int e = threadIdx.x; e < nl * my; e += T2_THREADS) {
+    const int q = dnl.div(e), c = e - q * nl;
+    const int cy = q - my / 2;
+    const int fy = cy < 0 ? cy + mry : cy;      // the kept fine row holding mode cy
+    const int jy = natural(cy, my);
+    const float2 val = fine[lbase[c] + (long long)fy * mrx];
+    a[(2 * c) * ld + jy] = val;
+    a[(2 * c + 1) * ld + jy] = cmulc(val, __ldg(roots + fy));
+  }
+  __syncthreads();
+  xfft_tile<HL, 1, true>(a, ld, 2 * nl, tw2);
+  for (int e = threadIdx.x; e < nl * mry; e += T2_THREADS) {
+    const int fy = dnl.div(e), c = e - fy * nl;
+    fine[lbase[c] + (long long)fy * mrx] = a[(2 * c + (fy & 1)) * ld + (fy >> 1)];
+  }
+}
+
 // lines per CTA: register FFT: 32 / L lines per warp, `rounds` passes of the 8 warps;
 // Stockham: enough lines to keep the 256 threads busy.  Both within the smem budget.
 size_t t2_per_line(int n, int xl) { return (xl ? 1 : 2) * (size_t)pf_ld(n) * sizeof(float2); }
@@ -122,6 +223,37 @@ template <int XL>
 void t2_allow_all() {
   t2_allow(k_t2_rows<XL>);
   t2_allow(k_t2_cols<XL>);
+  if constexpr (XL > 0) {
+    t2_allow(k_t2_rows_split<XL>);
+    t2_allow(k_t2_cols_split<XL>);
+  }
+}
+
+// PF_T2_SPLIT=0 keeps the full-length passes (A/B measurements)
+int t2_split_L(int m) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PF_T2_SPLIT");
+    on = (e == nullptr || atoi(e) != 0) ? 1 : 0;
+  }
+  return on ? xfft_L(m) : 0;
+}
+// fine lines per CTA: one round of the 8 warps' 32 / L' half-lines each
+int t2_split_cnt(int m, int hl) {
+  (void)m;
+  int cnt = (T2_THREADS / 32) * (32 / hl) / 2;
+  return cnt < 1 ? 1 : (cnt > 32 ? 32 : cnt);
+}
+size_t t2_split_smem(int m, int hl, int cnt) {
+  return ((size_t)2 * cnt * pf_ld(m) + (size_t)XFFT_R * hl) * sizeof(float2);
+}
+template <int HL, typename... A>
+void t2_launch_rows_split(unsigned grid, size_t smem, cudaStream_t st, A... args) {
+  if constexpr (HL > 0) k_t2_rows_split<HL><<<grid, T2_THREADS, smem, st>>>(args...);
+}
+template <int HL, typename... A>
+void t2_launch_cols_split(unsigned grid, size_t smem, cudaStream_t st, A... args) {
+  if constexpr (HL > 0) k_t2_cols_split<HL><<<grid, T2_THREADS, smem, st>>>(args...);
 }
 
 }  // namespace
@@ -141,7 +273,18 @@ extern "C" int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, in
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int xlx = plan_xl(*plan_x), xly = plan_xl(*plan_y);
-  {
+  // split passes (two half-length register FFTs per fine line) when mr = 2 m = 70 L'
+  const int hlx = g->mr[2] == 2 * g->m[2] ? t2_split_L(g->m[2]) : 0;
+  const int hly = g->mr[1] == 2 * g->m[1] ? t2_split_L(g->m[1]) : 0;
+  if (hlx) {
+    const int cnt = t2_split_cnt(g->m[2], hlx);
+    const long long nl = (long long)nv * g->m[1];
+    const size_t smem = t2_split_smem(g->m[2], hlx, cnt);
+    PF_XL_DISPATCH(hlx, (t2_launch_rows_split<XL>((unsigned)((nl + cnt - 1) / cnt), smem, st, *g,
+                                                  (const float2*)S, s_stride, ky, kx, nv,
+                                                  (float2*)fine, fine_stride, *plan_x, cnt)));
+    PF_LAUNCH_CHECK("k_t2_rows_split");
+  } else {
     const int cnt = t2_cnt(g->mr[2], xlx, 1, 1);
     const long long nl = (long long)nv * g->m[1];
     const size_t smem = cnt * t2_per_line(g->mr[2], xlx);
@@ -150,7 +293,14 @@ extern "C" int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, in
                              fine_stride, *plan_x, cnt)));
     PF_LAUNCH_CHECK("k_t2_rows");
   }
-  {
+  if (hly) {
+    const int cnt = t2_split_cnt(g->m[1], hly);
+    const long long nl = (long long)nv * g->mr[2];
+    const size_t smem = t2_split_smem(g->m[1], hly, cnt);
+    PF_XL_DISPATCH(hly, (t2_launch_cols_split<XL>((unsigned)((nl + cnt - 1) / cnt), smem, st, *g,
+                                                  nv, (float2*)fine, fine_stride, *plan_y, cnt)));
+    PF_LAUNCH_CHECK("k_t2_cols_split");
+  } else {
     // columns: >= 16 adjacent columns per CTA for 128-byte row segments
     const int cnt = t2_cnt(g->mr[1], xly, 2, 16);
     const long long nl = (long long)nv * g->mr[2];

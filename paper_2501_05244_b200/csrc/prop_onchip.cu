@@ -337,8 +337,8 @@ extern "C" int pf_prop_fbatch_onchip(const pf_plane* planes, int nplanes, const 
                "pf_prop_fbatch_onchip: needs px = py = 140, one illumination and a plane that "
                "fits shared memory");
   if (warps <= 0) warps = OC_NW;
-  PF_ARG_CHECK(warps == 12 || warps == 16,
-               "pf_prop_fbatch_onchip: warps per CTA must be 12 or 16 (0: default)");
+  PF_ARG_CHECK(warps == 8 || warps == 9 || warps == 10 || warps == 12 || warps == 16,
+               "pf_prop_fbatch_onchip: warps per CTA must be 8, 9, 10, 12 or 16 (0: default)");
   const int fpc = pf_cdiv(nf, groups);
   const int gy = pf_cdiv(nf, fpc);   // groups actually populated
   PF_ARG_CHECK(gy == 1 || ws_part, "pf_prop_fbatch_onchip: ws_part needed for groups > 1");
@@ -349,6 +349,9 @@ extern "C" int pf_prop_fbatch_onchip(const pf_plane* planes, int nplanes, const 
     int d = 0, smax = 232448;
     cudaGetDevice(&d);
     cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+    cudaFuncSetAttribute(k_prop_onchip<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    cudaFuncSetAttribute(k_prop_onchip<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    cudaFuncSetAttribute(k_prop_onchip<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
     cudaFuncSetAttribute(k_prop_onchip<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
     cudaFuncSetAttribute(k_prop_onchip<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
   }
@@ -359,6 +362,9 @@ extern "C" int pf_prop_fbatch_onchip(const pf_plane* planes, int nplanes, const 
                                                     (const float2*)frame_w, (float2*)vol,      \
                                                     (float2*)ws_part, acc_pitch(g->ny))
   if (warps == 16) OC_LAUNCH(k_prop_onchip<16>, 16);
+  else if (warps == 8) OC_LAUNCH(k_prop_onchip<8>, 8);
+  else if (warps == 9) OC_LAUNCH(k_prop_onchip<9>, 9);
+  else if (warps == 10) OC_LAUNCH(k_prop_onchip<10>, 10);
   else OC_LAUNCH(k_prop_onchip<12>, 12);
 #undef OC_LAUNCH
   PF_LAUNCH_CHECK("k_prop_onchip");
