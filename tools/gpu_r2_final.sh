@@ -2,8 +2,8 @@
 # One GPU call refreshing the round-2 record: GPU suite (incl. full-size parity), bench lines
 # (ours + reference arm) for configs 4 (headline), 0, 1, 2, 3, 5, 6, the config-4 launch list,
 # ncu --set full of K1 and the propagation kernels, steady-state traffic.
-mkdir -p gpurun_out/final4
-O=gpurun_out/final4
+mkdir -p gpurun_out/final5
+O=gpurun_out/final5
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
 PF_PARITY_LOG=$O/parity.jsonl timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; tail -3 $O/pytest_gpu.log
 python bench.py > $O/bench_c4.json 2> $O/bench_c4.err; tail -c 300 $O/bench_c4.err
