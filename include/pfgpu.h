@@ -274,9 +274,11 @@ int pf_bluestein_warp(int xpass, const void* src, int64_t src_ps, int64_t src_ls
                       const void* khat, void* stream);
 
 /* ---------------------------------------------------------------- NUFFT
- * Gaussian gridding (spectral.py:230-381).  Axis order (z, y, x); 2D uses
- * mr[0] = m[0] = 1.  Per point (device): i0[L][3] int32 nearest fine node,
- * d0[L][3] float32 = i0*h - x (the window offset of stencil tap 0).  */
+ * Gridding NUFFT (spectral.py:230-381): the reference's Gaussian stencil (window 0) or the
+ * exponential-of-semicircle window on the same 2x-oversampled fine grid (window 1, the
+ * default of the Python layer; same eps contract, half the stencil width).  Axis order
+ * (z, y, x); 2D uses mr[0] = m[0] = 1.  Per point (device): i0[L][3] int32 nearest fine
+ * node, d0[L][3] float32 = i0*h - x (the offset of the centre tap); taps -w..w.  */
 typedef struct pf_nufft_geom {
   int dim;
   int w;
@@ -286,6 +288,9 @@ typedef struct pf_nufft_geom {
   float inv4tau[3];
   int tile[3];
   int ntiles[3];
+  int window;      /* 0: Gaussian (the reference's stencil), 1: exponential of semicircle */
+  float beta;      /* window 1: exp(beta (sqrt(1 - (d / (w h))^2) - 1)), beta = 2.30 * 2 w */
+  float inv_hw[3]; /* window 1: 1 / (w h[a]) */
 } pf_nufft_geom;
 
 /* type-1 spreading (spectral.py:353-355) as a tiled gather: fine[v][cell] =
@@ -443,6 +448,11 @@ int64_t pf_srsd_workspace_bytes(const pf_srsd_args* args);
 int pf_srsd(const pf_srsd_args* args, const void* slices, void* vol, void* ws, int64_t ws_bytes,
             void* stream);
 
+/* Spreading window of the plans the C entry points build (pf_nursd1, pf_nursd2): 1 (default)
+ * the exponential of semicircle, 0 the reference's Gaussian stencil (spectral.py:230-315);
+ * any other value only queries.  Returns the previous setting (initially from
+ * PF_NUFFT_WINDOW = "es" | "gaussian"). */
+int pf_nufft_window(int mode);
 /* nursd1 (reference reconstruct.py:335-385, nursd1(slices, grid, eps, times, threads,
  * include_illumination)) in one call: detections scattered on the plane z = relay_z
  * (relay_xy host [n_points][2], x then y) -> cuboid grid, via a type-1 NUFFT at accuracy

@@ -40,7 +40,8 @@ class PfNufftGeom(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int), ("w", ctypes.c_int), ("mr", ctypes.c_int * 3),
                 ("m", ctypes.c_int * 3), ("h", ctypes.c_float * 3),
                 ("inv4tau", ctypes.c_float * 3), ("tile", ctypes.c_int * 3),
-                ("ntiles", ctypes.c_int * 3)]
+                ("ntiles", ctypes.c_int * 3), ("window", ctypes.c_int), ("beta", ctypes.c_float),
+                ("inv_hw", ctypes.c_float * 3)]
 
 
 class PfRsdArgs(ctypes.Structure):
@@ -133,6 +134,7 @@ _SIGNATURES = {
     "pf_count_nonfinite": [_vp, _i64, _vp, _vp],
     "pf_fp32_probe": [_vp, _i, _i, _vp],
     "pf_nufft_interp_mode": [_i],
+    "pf_nufft_window": [_i],
     "pf_nufft_interp": [_P(PfNufftGeom), _vp, _vp, _i, _vp, _vp, _vp],
     "pf_nufft_interp2_batch": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _i64, _i64,
                                _i, _vp, _d, _i, _f, _vp, _i, _vp, _i64, _vp],
@@ -169,7 +171,7 @@ _RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, 
              "pf_srsd_workspace_bytes": ctypes.c_int64, "pf_nursd1_workspace_bytes": ctypes.c_int64,
              "pf_nursd2_workspace_bytes": ctypes.c_int64,
              "pf_prop_fast": ctypes.c_int, "pf_prop_onchip_ok": ctypes.c_int,
-             "pf_nufft_interp_mode": ctypes.c_int}
+             "pf_nufft_interp_mode": ctypes.c_int, "pf_nufft_window": ctypes.c_int}
 
 _lib = None
 

@@ -162,6 +162,13 @@ int plan(const pf_nursd1_args* a, Plan* P) {
 
 }  // namespace
 
+extern "C" int pf_nufft_window(int mode) {
+  int& w = pfalgo::nufft_window_ref();
+  const int prev = w;
+  if (mode == 0 || mode == 1) w = mode;
+  return prev;
+}
+
 extern "C" int64_t pf_nursd1_workspace_bytes(const pf_nursd1_args* a) {
   Plan P;
   if (plan(a, &P) != 0) return -1;

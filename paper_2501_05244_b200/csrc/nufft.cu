@@ -35,6 +35,17 @@ __device__ __forceinline__ int wrap_off(int d, int mr) {
   return d;
 }
 
+// Window weight of a tap dl (radians) from the point on axis a.  window 0: the reference's
+// Gaussian exp(-dl^2 / 4 tau) (spectral.py:303).  window 1: the exponential of semicircle
+// exp(beta (sqrt(1 - (dl / (w h))^2) - 1)) on |dl| < w h, zero outside: 2 w taps in support
+// where the Gaussian needs 2 w + 1 = 17 for the same eps = 1e-6 (w = 4 against 8).
+__device__ __forceinline__ float pf_win(const pf_nufft_geom& G, int a, float dl) {
+  if (G.window == 0) return __expf(-dl * dl * G.inv4tau[a]);
+  const float z = dl * G.inv_hw[a];
+  const float q = 1.0f - z * z;
+  return q > 0.f ? __expf(G.beta * (sqrtf(q) - 1.0f)) : 0.f;
+}
+
 // grid: (total tiles, ceil(nv / SP_V)); block: tile cells (<= 256 threads)
 template <int SP_V>
 __global__ void __launch_bounds__(NT)
@@ -76,7 +87,7 @@ k_spread(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ 
         const float base = d0[3 * pt + a];
         for (int o = 0; o < W; o++) {
           const float dl = base + (float)(o - G.w) * G.h[a];
-          wgt[p][a][o] = __expf(-dl * dl * G.inv4tau[a]);
+          wgt[p][a][o] = pf_win(G, a, dl);
         }
         const int t0 = a == 0 ? tile0z : (a == 1 ? tile0y : tile0x);
         pi0[p][a] = wrap_off(t0 - natural(i0[3 * pt + a], G.mr[a]), G.mr[a]);
@@ -211,10 +222,10 @@ k_interp2_warp(pf_nufft_geom G, const int* __restrict__ i0, const float* __restr
   const bool on = lane < W;
   const float dyl = d0[3 * l + 1], dxl = d0[3 * l + 2];
   const float dx = dxl + (float)(lane - G.w) * G.h[2];
-  const float wx = on ? __expf(-dx * dx * G.inv4tau[2]) : 0.f;
+  const float wx = on ? pf_win(G, 2, dx) : 0.f;
   // row weights: lane o forms row o's weight once; the row loop broadcasts it
   const float dyo = dyl + (float)(lane - G.w) * G.h[1];
-  const float wy_lane = on ? __expf(-dyo * dyo * G.inv4tau[1]) : 0.f;
+  const float wy_lane = on ? pf_win(G, 1, dyo) : 0.f;
   const int cx = wrap_once(natural((long long)i0[3 * l + 2] - G.w, mrx) + (on ? lane : 0), mrx);
   const int cy0 = natural((long long)i0[3 * l + 1] - G.w, mry);
   float2 tot = make_float2(0.f, 0.f);
@@ -271,10 +282,10 @@ k_interp2_batch(pf_nufft_geom G, const int* __restrict__ i0, const float* __rest
   const bool on = lane < W;
   const float dyl = d0[3 * l + 1], dxl = d0[3 * l + 2];
   const float dx = dxl + (float)(lane - G.w) * G.h[2];
-  const float wx = on ? __expf(-dx * dx * G.inv4tau[2]) : 0.f;
+  const float wx = on ? pf_win(G, 2, dx) : 0.f;
   // row weights: lane o forms row o's weight once; the row loop broadcasts it
   const float dyo = dyl + (float)(lane - G.w) * G.h[1];
-  const float wy_lane = on ? __expf(-dyo * dyo * G.inv4tau[1]) : 0.f;
+  const float wy_lane = on ? pf_win(G, 1, dyo) : 0.f;
   const int cx = wrap_once(natural((long long)i0[3 * l + 2] - G.w, mrx) + (on ? lane : 0), mrx);
   const int cy0 = natural((long long)i0[3 * l + 1] - G.w, mry);
   const float2* fplane = fine + (long long)(plane_idx[l] - plane0) * fine_plane_stride;
@@ -341,13 +352,13 @@ k_interp2_batch_h(pf_nufft_geom G, const int* __restrict__ i0, const float* __re
   const float dyl = d0[3 * lc + 1], dxl = d0[3 * lc + 2];
   const float dx1 = dxl + (float)(hl - G.w) * G.h[2];
   const float dx2 = dxl + (float)(hl + 16 - G.w) * G.h[2];
-  const float wx1 = on1 ? __expf(-dx1 * dx1 * G.inv4tau[2]) : 0.f;
-  const float wx2 = on2 ? __expf(-dx2 * dx2 * G.inv4tau[2]) : 0.f;
+  const float wx1 = on1 ? pf_win(G, 2, dx1) : 0.f;
+  const float wx2 = on2 ? pf_win(G, 2, dx2) : 0.f;
   // row weights: lane c forms rows c and c + 16; the row loop broadcasts them
   const float dy1 = dyl + (float)(hl - G.w) * G.h[1];
   const float dy2 = dyl + (float)(hl + 16 - G.w) * G.h[1];
-  const float wy1 = on1 ? __expf(-dy1 * dy1 * G.inv4tau[1]) : 0.f;
-  const float wy2 = on2 ? __expf(-dy2 * dy2 * G.inv4tau[1]) : 0.f;
+  const float wy1 = on1 ? pf_win(G, 1, dy1) : 0.f;
+  const float wy2 = on2 ? pf_win(G, 1, dy2) : 0.f;
   const int cxb = natural((long long)i0[3 * lc + 2] - G.w, mrx);
   const int cx1 = wrap_once(cxb + (on1 ? hl : 0), mrx);
   const int cx2 = wrap_once(cxb + (on2 ? hl + 16 : 0), mrx);
@@ -581,6 +592,90 @@ k_interp2_h16(pf_nufft_geom G, const int* __restrict__ i0, const float* __restri
   }
 }
 
+// Exponential-of-semicircle readout for w = 4 (the default accuracy eps = 1e-6): the window
+// vanishes at |d| >= 4 h, so of the taps -4..4 about the nearest node the one on the far side
+// of the anchor has weight exactly zero and each axis keeps 8 taps -- a quarter warp per
+// point (lane c owns column c, 64-byte row segments), four points per warp, 8 loads per lane
+// per point and node.  Same weights as the general kernels; float32 summation order only.
+template <int UNR>
+__global__ void __launch_bounds__(256)
+k_interp2_es8(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
+              const double* __restrict__ xyz, const int* __restrict__ plane_idx,
+              const long long* __restrict__ dst_idx, int npts, int plane0,
+              const float2* __restrict__ fine, long long fine_plane_stride,
+              long long fine_stride, int n_illum, const double* __restrict__ ill,
+              double kturns, int include_illum, float scale,
+              const float2* __restrict__ frame_w, int n_frames, float2* __restrict__ vol,
+              long long vol_frame_stride, int nodes, const float* __restrict__ lw) {
+  constexpr int w = 4;
+  const int lane = threadIdx.x & 31, ql = lane & 7, grp = lane >> 3;
+  const int l = blockIdx.x * (blockDim.x >> 3) + ((threadIdx.x >> 5) << 2) + grp;
+  const bool live = l < npts;
+  const int lc = live ? l : 0;
+  const int mry = G.mr[1], mrx = G.mr[2], fe = mry * mrx;
+  const float dyl = d0[3 * lc + 1], dxl = d0[3 * lc + 2];
+  // d0 = anchor - point: anchor right of the point -> tap +4 lies outside the support
+  const int sx = dxl > 0.f ? 0 : 1, sy = dyl > 0.f ? 0 : 1;
+  const float wx = pf_win(G, 2, dxl + (float)(ql - w + sx) * G.h[2]);
+  const float wy_own = pf_win(G, 1, dyl + (float)(ql - w + sy) * G.h[1]);
+  const int cx = wrap_once(wrap_once(i0[3 * lc + 2] - w + sx, mrx) + ql, mrx);
+  const int r0 = wrap_once(i0[3 * lc + 1] - w + sy, mry) * mrx;
+  const float2* fplane = fine + (long long)(plane_idx[lc] - plane0) * fine_plane_stride;
+  // the point's tail data (lane 0 of its quarter warp) is requested ahead of the gathers,
+  // so the position, target index and target value arrive while the stencil is summed
+  const bool tail = ql == 0 && live;
+  double px = 0.0, py = 0.0, pz = 0.0;
+  long long dst = 0;
+  float2 old = make_float2(0.f, 0.f);
+  if (tail) {
+    dst = dst_idx[l];
+    if (include_illum) {
+      px = xyz[3 * lc];
+      py = xyz[3 * lc + 1];
+      pz = xyz[3 * lc + 2];
+    }
+    old = vol[dst];
+  }
+  float2 tot = make_float2(0.f, 0.f);
+  for (int p = 0; p < n_illum; p++) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int m = 0; m < nodes; m++) {
+      const float2* col = fplane + (long long)m * fine_plane_stride +
+                          (long long)p * fine_stride + cx;
+      const float wxm = lw ? wx * __ldg(lw + (long long)lc * nodes + m) : wx;
+      int ro = r0;
+#pragma unroll UNR
+      for (int oy = 0; oy < 8; oy++) {
+        const float wy = __shfl_sync(0xffffffffu, wy_own, (grp << 3) + oy);
+        const float2 f = __ldg(col + ro);
+        const float ww = wxm * wy;
+        acc.x = fmaf(ww, f.x, acc.x);
+        acc.y = fmaf(ww, f.y, acc.y);
+        ro += mrx;
+        if (ro >= fe) ro -= fe;
+      }
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    float2 val = cscale(acc, scale);
+    if (include_illum && tail) {
+      const double ex = px - ill[3 * p], ey = py - ill[3 * p + 1], ez = pz - ill[3 * p + 2];
+      val = cmul(val, expi_reduced(PF_TWO_PI * kturns * sqrt(ex * ex + ey * ey + ez * ez)));
+    }
+    tot = cadd(tot, val);
+  }
+  if (tail) {
+    vol[dst] = cadd(old, cmul(tot, frame_w[0]));   // each target belongs to one point
+    for (int f = 1; f < n_frames; f++) {
+      float2* d = vol + f * vol_frame_stride + dst;
+      *d = cadd(*d, cmul(tot, frame_w[f]));
+    }
+  }
+}
+
 // PF_INTERP_H17: 2 (default) the 16 x 16 trimmed kernel for W = 17, 1 the full 17 x 17
 // specialisation, 0 the general half-warp kernel (A/B measurements)
 int g_interp_mode = -1;
@@ -592,13 +687,25 @@ int interp_h17_mode() {
   return g_interp_mode;
 }
 bool interp_h17_enabled() { return interp_h17_mode() != 0; }
-int interp_unroll() {
+// row-loop unroll of the quarter / half warp readouts (PF_INTERP_UNROLL overrides): 8 rows
+// in flight for the many-node gathers, 4 (fewer registers, more resident warps) for the
+// single-grid readout -- measured: config 2 20.2 -> 18.9 ms with 4, config 7 51.9 -> 49.5 with 8
+int interp_unroll(int nodes = 2) {
   static int u = -1;
   if (u < 0) {
     const char* e = getenv("PF_INTERP_UNROLL");
-    u = e ? atoi(e) : 8;
+    u = e ? atoi(e) : 0;
   }
-  return u;
+  return u ? u : (nodes > 1 ? 8 : 4);
+}
+// PF_INTERP_ES8=0 keeps the general kernels for the w = 4 exponential-of-semicircle stencil
+bool interp_es8_ok(const pf_nufft_geom& g) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PF_INTERP_ES8");
+    on = (e == nullptr || atoi(e) != 0) ? 1 : 0;
+  }
+  return on && g.window == 1 && g.w == 4 && (long long)g.mr[1] * g.mr[2] < (1LL << 31);
 }
 // the far edge tap (8 cells away) must weigh < 2e-8 of the centre tap on both axes
 bool interp_trim_ok(const pf_nufft_geom& g) {
@@ -641,12 +748,12 @@ __global__ void k_interp2_acc(pf_nufft_geom G, const int* __restrict__ i0,
     int y = cy;
     for (int oy = 0; oy < W; oy++) {
       const float dy = d0[3 * l + 1] + (float)(oy - G.w) * G.h[1];
-      const float wy = __expf(-dy * dy * G.inv4tau[1]);
+      const float wy = pf_win(G, 1, dy);
       float2 row = make_float2(0.f, 0.f);
       int x = cx0;
       for (int ox = 0; ox < W; ox++) {
         const float dx = d0[3 * l + 2] + (float)(ox - G.w) * G.h[2];
-        const float wx = __expf(-dx * dx * G.inv4tau[2]);
+        const float wx = pf_win(G, 2, dx);
         const float2 f = fp[(long long)y * mrx + x];
         row.x = fmaf(wx, f.x, row.x);
         row.y = fmaf(wx, f.y, row.y);
@@ -685,7 +792,7 @@ k_interp_any(pf_nufft_geom G, const int* __restrict__ i0, const float* __restric
   const int mrz = G.mr[0], mry = G.mr[1], mrx = G.mr[2];
   const bool on = lane < W;
   const float dx = d0[3 * l + 2] + (float)(lane - G.w) * G.h[2];
-  const float wx = on ? __expf(-dx * dx * G.inv4tau[2]) : 0.f;
+  const float wx = on ? pf_win(G, 2, dx) : 0.f;
   const int cx = wrap_once(natural((long long)i0[3 * l + 2] - G.w, mrx) + (on ? lane : 0), mrx);
   const int cy0 = Wy > 1 ? natural((long long)i0[3 * l + 1] - G.w, mry) : 0;
   int cz = Wz > 1 ? natural((long long)i0[3 * l] - G.w, mrz) : 0;
@@ -694,14 +801,14 @@ k_interp_any(pf_nufft_geom G, const int* __restrict__ i0, const float* __restric
     float wz = 1.f;
     if (Wz > 1) {
       const float dz = d0[3 * l] + (float)(oz - G.w) * G.h[0];
-      wz = __expf(-dz * dz * G.inv4tau[0]);
+      wz = pf_win(G, 0, dz);
     }
     int cy = cy0;
     for (int oy = 0; oy < Wy; oy++) {
       float wy = 1.f;
       if (Wy > 1) {
         const float dy = d0[3 * l + 1] + (float)(oy - G.w) * G.h[1];
-        wy = __expf(-dy * dy * G.inv4tau[1]);
+        wy = pf_win(G, 1, dy);
       }
       const float w = wx * wy * wz;
       const float2 f = __ldg(fine + ((long long)cz * mry + cy) * mrx + cx);
@@ -828,7 +935,23 @@ extern "C" int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0,
     const char* e = getenv("PF_INTERP_HALF");
     half = (e == nullptr || atoi(e) != 0) ? 1 : 0;
   }
-  if (half && g->w == 8 && (long long)g->mr[1] * g->mr[2] < (1LL << 31) &&
+  if (interp_es8_ok(*g)) {
+    if (interp_unroll(1) == 4)
+      k_interp2_es8<4><<<pf_cdiv(npts, 32), 256, 0, (cudaStream_t)stream>>>(
+          *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0,
+          (const float2*)fine, fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI,
+          include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol,
+          vol_frame_stride, 1, nullptr);
+    else
+      k_interp2_es8<8><<<pf_cdiv(npts, 32), 256, 0, (cudaStream_t)stream>>>(
+          *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0,
+          (const float2*)fine, fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI,
+          include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol,
+          vol_frame_stride, 1, nullptr);
+    PF_LAUNCH_CHECK("k_interp2_es8");
+    return 0;
+  }
+  if (half && g->window == 0 && g->w == 8 && (long long)g->mr[1] * g->mr[2] < (1LL << 31) &&
       interp_h17_enabled()) {   // W = 17
     if (interp_trim_ok(*g)) {
       if (interp_unroll() == 8)
@@ -882,7 +1005,24 @@ extern "C" int pf_nufft_interp2_nodes(const pf_nufft_geom* g, const int32_t* i0,
                    (nodes == 1 || lw != nullptr),
                "pf_nufft_interp2_nodes: bad args (2D, stencil width <= 32, weights for nodes > 1)");
   if (npts == 0) return 0;
-  if (g->w == 8 && (long long)g->mr[1] * g->mr[2] < (1LL << 31) && interp_h17_enabled()) {
+  if (interp_es8_ok(*g)) {
+    if (interp_unroll(nodes) == 4)
+      k_interp2_es8<4><<<pf_cdiv(npts, 32), 256, 0, (cudaStream_t)stream>>>(
+          *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0,
+          (const float2*)fine, fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI,
+          include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol,
+          vol_frame_stride, nodes, lw);
+    else
+      k_interp2_es8<8><<<pf_cdiv(npts, 32), 256, 0, (cudaStream_t)stream>>>(
+          *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0,
+          (const float2*)fine, fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI,
+          include_illum, scale, (const float2*)frame_w, n_frames, (float2*)vol,
+          vol_frame_stride, nodes, lw);
+    PF_LAUNCH_CHECK("k_interp2_es8");
+    return 0;
+  }
+  if (g->window == 0 && g->w == 8 && (long long)g->mr[1] * g->mr[2] < (1LL << 31) &&
+      interp_h17_enabled()) {
     if (interp_trim_ok(*g)) {
       if (interp_unroll() == 8)
         k_interp2_h16<8><<<pf_cdiv(npts, 16), 256, 0, (cudaStream_t)stream>>>(

@@ -1,13 +1,19 @@
 // Host planning of the 2D GPU NUFFT for the whole-algorithm C entry points
 // (algo_nursd1.cu, algo_nursd2.cu); the C++ counterpart of nufft.NufftPlan /
-// NufftPoints, following reference NufftPlan (spectral.py:230-315):
-//   w = max(2, ceil(log10(1/eps)) + 2), fine grid mr = next_fast_len(max(2m, 2w + 2)),
-//   tau = pi w / (s (s - 1/2) m^2) with s = mr/m, the DISCRETE deconvolution
-//   ker[k] = 1 + 2 sum_j exp(-(j h)^2 / 4 tau) cos(k j h) (h = 2 pi / mr),
-// and the per-point stencil anchors of spectral.py:281-303.
+// NufftPoints, following reference NufftPlan (spectral.py:230-315): fine grid
+// mr = next_fast_len(max(2m, 2w + 2)) (h = 2 pi / mr), the per-point stencil anchors of
+// spectral.py:281-303, and one of two windows (pf_nufft_window / PF_NUFFT_WINDOW):
+//   1 (default) exponential of semicircle exp(beta (sqrt(1 - (d / (w h))^2) - 1)),
+//     2w = ceil(log10(1/eps)) + 2 taps, beta = 2.30 * 2w, deconvolved by its continuous
+//     transform (64-node Gauss-Legendre);
+//   0 the reference's Gaussian: w = max(2, ceil(log10(1/eps)) + 2),
+//     tau = pi w / (s (s - 1/2) m^2) with s = mr/m, the DISCRETE deconvolution
+//     ker[k] = 1 + 2 sum_j exp(-(j h)^2 / 4 tau) cos(k j h).
 #pragma once
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <numeric>
@@ -34,6 +40,42 @@ inline std::vector<std::pair<int, int>> kept_ranges(int m, int mr) {
   return {{0, m - m / 2}};
 }
 
+// default window of the C++ planner: PF_NUFFT_WINDOW ("es" | "gaussian"), or pf_nufft_window
+inline int& nufft_window_ref() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PF_NUFFT_WINDOW");
+    v = (e && strcmp(e, "gaussian") == 0) ? 0 : 1;
+  }
+  return v;
+}
+
+// n-node Gauss-Legendre rule on [-1, 1] (Newton on P_n from the Chebyshev guess)
+inline void gauss_legendre(int n, std::vector<double>* x, std::vector<double>* wt) {
+  x->assign(n, 0.0);
+  wt->assign(n, 0.0);
+  for (int i = 0; i < (n + 1) / 2; i++) {
+    double z = cos(M_PI * (i + 0.75) / (n + 0.5)), dp = 1.0;
+    for (int it = 0; it < 100; it++) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= n; k++) {
+        const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (z * p1 - p0) / (z * z - 1.0);
+      const double dz = p1 / dp;
+      z -= dz;
+      if (fabs(dz) < 1e-15) break;
+    }
+    (*x)[i] = -z;
+    (*x)[n - 1 - i] = z;
+    (*wt)[i] = (*wt)[n - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+
+constexpr double ES_BETA_PER_TAP = 2.30;
+
 struct Nufft2Plan {
   pf_nufft_geom g;
   std::vector<float> ker[3];   // z (= {1}), y, x deconvolution factors
@@ -47,7 +89,9 @@ inline int nufft2_plan(int my, int mx, double eps, Nufft2Plan* N) {
     pf_set_error("accuracy target must lie in [1e-14, 0.1]");
     return -1;
   }
-  const int w = std::max(2, (int)ceil(log10(1.0 / eps)) + 2);
+  const int window = nufft_window_ref();
+  const int digits = (int)ceil(log10(1.0 / eps)) + 2;
+  const int w = window == 1 ? std::max(2, (digits + 1) / 2) : std::max(2, digits);
   if (w > 16) {
     pf_set_error("accuracy target too tight for the GPU stencil (w <= 16)");
     return -1;
@@ -56,6 +100,10 @@ inline int nufft2_plan(int my, int mx, double eps, Nufft2Plan* N) {
   g = pf_nufft_geom{};
   g.dim = 2;
   g.w = w;
+  g.window = window;
+  g.beta = (float)(ES_BETA_PER_TAP * 2 * w);
+  std::vector<double> gx, gw;
+  if (window == 1) gauss_legendre(64, &gx, &gw);
   const int modes[3] = {1, my, mx};
   for (int a = 0; a < 3; a++) {
     const int m = modes[a];
@@ -74,14 +122,23 @@ inline int nufft2_plan(int my, int mx, double eps, Nufft2Plan* N) {
       for (int i = 0; i < m; i++) {
         const double k = i - m / 2;
         double acc = 0.0;
-        for (int j = 1; j <= w; j++) acc += exp(-(j * h) * (j * h) / (4.0 * tau)) * cos(k * (j * h));
-        N->ker[a][i] = (float)(1.0 + 2.0 * acc);
+        if (window == 1) {
+          for (size_t q = 0; q < gx.size(); q++)
+            acc += exp(ES_BETA_PER_TAP * 2 * w * (sqrt(1.0 - gx[q] * gx[q]) - 1.0)) * gw[q] * w *
+                   cos(k * h * gx[q] * w);
+          N->ker[a][i] = (float)acc;
+        } else {
+          for (int j = 1; j <= w; j++)
+            acc += exp(-(j * h) * (j * h) / (4.0 * tau)) * cos(k * (j * h));
+          N->ker[a][i] = (float)(1.0 + 2.0 * acc);
+        }
       }
     }
     g.mr[a] = mr;
     g.m[a] = m;
     g.h[a] = (float)(2.0 * M_PI / mr);
     g.inv4tau[a] = (float)(1.0 / (4.0 * tau));
+    g.inv_hw[a] = (float)(1.0 / (w * (2.0 * M_PI / mr)));
     g.tile[a] = a == 0 ? 1 : NUFFT_TILE;
     g.ntiles[a] = (mr + g.tile[a] - 1) / g.tile[a];
   }

@@ -448,6 +448,11 @@ def _slices_geometry(slices):
             _fingerprint(slices.relay), _fingerprint(slices.illuminations))
 
 
+def _nufft_window() -> str:
+    from . import nufft
+    return nufft.DEFAULT_WINDOW
+
+
 def cached_engine(kind: str, slices, grid, options: tuple, factory):
     """Engine for (kind, slices geometry, grid, options) from a small LRU cache; ``factory``
     builds it on a miss.  Engines hold only geometry-derived plans and workspaces, so a
@@ -457,7 +462,7 @@ def cached_engine(kind: str, slices, grid, options: tuple, factory):
     # the module's path switches are part of the key: an engine captured under other
     # switches would replay their launch sequence
     flags = (_LANES, _FAST_BATCH_CAP, _FBATCH_BYTES, _FBATCH_GENERIC, _HORNER, _HORNER_BLOCK,
-             _BATCH_BYTES, _ONCHIP, _ONCHIP_GROUPS, _ONCHIP_WARPS)
+             _BATCH_BYTES, _ONCHIP, _ONCHIP_GROUPS, _ONCHIP_WARPS, _nufft_window())
     devi = torch.cuda.current_device() if torch.cuda.is_available() else -1
     key = (kind, devi, _slices_geometry(slices), _fingerprint(grid),
            _fingerprint(options), flags)

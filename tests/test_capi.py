@@ -279,7 +279,7 @@ def test_nursd1_workspace_and_validation(rng):
     dict(n_ill=2, F=3),               # two illuminations
     dict(lattice=True),               # on-lattice: P = 128 register path, pow2 type-1 finish, Horner C
     dict(lattice=True, F=40),         # Horner in 32-frequency blocks
-    dict(kw=dict(eps=1e-9)),          # tighter stencil (w = 11)
+    dict(kw=dict(eps=1e-9)),          # tighter stencil (w = 6; 11 for the Gaussian)
 ])
 def test_pf_nursd1_matches_oracle_and_engine(rng, case):
     kw = case.pop("kw", {})
@@ -287,6 +287,30 @@ def test_pf_nursd1_matches_oracle_and_engine(rng, case):
     got = capi_nursd1(sl, grid, **kw)[0]
     assert O.rel_l2(got, O.nursd1(sl, grid, **kw)) < TOL
     assert O.rel_l2(got, pf.nursd1(sl, grid, **kw).field) < 1e-5
+
+
+@pytest.fixture
+def gaussian_window(monkeypatch):
+    """The reference's Gaussian stencil in both planners (Python plans, C entry points)."""
+    from paper_2501_05244_b200 import nufft as nu
+    monkeypatch.setattr(nu, "DEFAULT_WINDOW", "gaussian")
+    prev = _lib.call("pf_nufft_window", 0)
+    yield
+    _lib.call("pf_nufft_window", prev)
+
+
+@pytest.mark.gpu
+def test_pf_nursd1_and_nursd2_gaussian_window(rng, gaussian_window):
+    """The C planner's Gaussian plan (pf_nufft_window(0)) equals the Python one: the C entry
+    points reproduce the engines and the oracle with the reference's own stencil."""
+    sl, grid = _scatter_scene(rng)
+    got = capi_nursd1(sl, grid)[0]
+    assert O.rel_l2(got, O.nursd1(sl, grid)) < 2e-6
+    assert O.rel_l2(got, pf.nursd1(sl, grid).field) < 1e-5
+    sl, ev = _voxel_scene(rng)
+    got = capi_nursd2(sl, ev)[0]
+    assert O.rel_l2(got, O.nursd2(sl, ev)) < 2e-6
+    assert O.rel_l2(got, pf.nursd2(sl, ev).field) < 1e-5
 
 
 @pytest.mark.gpu

@@ -18,8 +18,20 @@ CASES = ["chain_srsd_unit", "chain_srsd_08", "chain_nursd1", "chain_nursd2", "ch
          "rsd3d_curved_near"]
 
 
+@pytest.fixture(params=["es", "gaussian"])
+def window(request, monkeypatch):
+    """Run under both NUFFT windows: the default exponential of semicircle and the
+    reference's Gaussian stencil (Python plans and the C entry points' planner)."""
+    from paper_2501_05244_b200 import _lib
+    from paper_2501_05244_b200 import nufft as nu
+    monkeypatch.setattr(nu, "DEFAULT_WINDOW", request.param)
+    prev = _lib.call("pf_nufft_window", 1 if request.param == "es" else 0)
+    yield request.param
+    _lib.call("pf_nufft_window", prev)
+
+
 @pytest.mark.parametrize("name", CASES)
-def test_algorithm_golden(name):
+def test_algorithm_golden(name, window):
     d = load(f"rec_{name}")
     sl, grid = slices_from(d), grid_from(d)
     alg, kw = case_call(name)
@@ -52,7 +64,7 @@ def _rand_slices(rng, relay, n_freq=3, n_ill=1, lam=0.06):
     return pf.FrequencySlices(freqs, coeff, relay, ill)
 
 
-def test_nursd1_c1_like(rng):
+def test_nursd1_c1_like(rng, window):
     """Config-1 shape (i.i.d. relay points, P=140 from the reference pad rule), reduced size."""
     pts = rng.uniform(-1.0, 1.0, size=(4096, 2))
     sl = _rand_slices(rng, pf.NonUniformPlanarRelay(pf.PointList(pts), 0.0), n_freq=2)
@@ -125,7 +137,7 @@ def test_srsd_frustum_vs_oracle(rng, n, frames):
     assert O.rel_l2(vol.field, ref) < TOL
 
 
-def test_nursd2_offlattice_voxels(rng):
+def test_nursd2_offlattice_voxels(rng, window):
     n = 24
     p = 0.02
     g = pf.UniformGrid2D(n, n, p, p, -(n - 1) * p / 2, -(n - 1) * p / 2, 0.0)
@@ -137,11 +149,13 @@ def test_nursd2_offlattice_voxels(rng):
     assert O.rel_l2(vol.field, O.nursd2(sl, ev)) < TOL
 
 
-def test_nursd2_trimmed_readout_matches_full_stencil(rng):
-    """The default readout for w = 8 keeps 16 x 16 of the 17 x 17 taps (the far edge tap of
+def test_nursd2_trimmed_readout_matches_full_stencil(rng, monkeypatch):
+    """The Gaussian readout for w = 8 keeps 16 x 16 of the 17 x 17 taps (the far edge tap of
     an axis weighs <= 6.5e-9 of the centre tap): against the full stencil the volume moves
     by less than float32 rounding of the sum, and both match the oracle alike."""
     from paper_2501_05244_b200 import _lib
+    from paper_2501_05244_b200 import nufft as nu
+    monkeypatch.setattr(nu, "DEFAULT_WINDOW", "gaussian")
     n = 32
     p = 0.02
     g = pf.UniformGrid2D(n, n, p, p, -(n - 1) * p / 2, -(n - 1) * p / 2, 0.0)
@@ -163,7 +177,7 @@ def test_nursd2_trimmed_readout_matches_full_stencil(rng):
     assert e_t < 2e-6 and e_f < 2e-6 and abs(e_t - e_f) < 2e-7, (e_t, e_f)
 
 
-def test_config2_composed_small(rng):
+def test_config2_composed_small(rng, window):
     """Config-2 family (non-planar relay -> arbitrary voxels) against the composed oracle."""
     from paper_2501_05244_b200.algorithms import nursd3d_explicit
     xy = rng.uniform(-0.3, 0.3, size=(600, 2))

@@ -1,6 +1,6 @@
 #!/bin/bash
-# ncu --set full of one type-2 readout launch at config 2 (current default kernel).
+# ncu --set full of the type-2 readout kernel in one config-2 step
 O=gpurun_out/interp_ncu; mkdir -p $O
-PF_CFG=2 ncu --set full --clock-control none --import-source on -k regex:"k_interp2" -s 4 -c 1 \
-    -o $O/${1:-cur} python tools/prof_step.py > $O/${1:-cur}.log 2>&1
-ls -la $O
+PF_CFG=2 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_interp2 -s 3 -c 1 \
+   --profile-from-start off -o $O/interp python tools/prof_step.py > $O/ncu.log 2>&1
+tail -2 $O/ncu.log
