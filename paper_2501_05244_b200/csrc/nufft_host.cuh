@@ -4,7 +4,7 @@
 // mr = next_fast_len(max(2m, 2w + 2)) (h = 2 pi / mr), the per-point stencil anchors of
 // spectral.py:281-303, and one of two windows (pf_nufft_window / PF_NUFFT_WINDOW):
 //   1 (default) exponential of semicircle exp(beta (sqrt(1 - (d / (w h))^2) - 1)),
-//     2w = ceil(log10(1/eps)) + 2 taps, beta = 2.30 * 2w, deconvolved by its continuous
+//     2w = max(6, ceil(log10(1/eps)) + 2) taps, beta = 2.30 * 2w, deconvolved by its continuous
 //     transform (64-node Gauss-Legendre);
 //   0 the reference's Gaussian: w = max(2, ceil(log10(1/eps)) + 2),
 //     tau = pi w / (s (s - 1/2) m^2) with s = mr/m, the DISCRETE deconvolution
@@ -91,7 +91,7 @@ inline int nufft2_plan(int my, int mx, double eps, Nufft2Plan* N) {
   }
   const int window = nufft_window_ref();
   const int digits = (int)ceil(log10(1.0 / eps)) + 2;
-  const int w = window == 1 ? std::max(2, (digits + 1) / 2) : std::max(2, digits);
+  const int w = window == 1 ? std::max(3, (digits + 1) / 2) : std::max(2, digits);
   if (w > 16) {
     pf_set_error("accuracy target too tight for the GPU stencil (w <= 16)");
     return -1;

@@ -6,7 +6,7 @@ divided out of the kept modes, the same ``eps`` contract.  Two windows:
 
 * ``"es"`` (default; BASELINE north star (3)): the exponential of semicircle
   ``exp(beta (sqrt(1 - (d / (w h))^2) - 1))`` with ``beta = 2.30 * 2w`` and
-  ``2w = ceil(log10(1/eps)) + 2`` taps (8 at the default ``eps = 1e-6``), deconvolved by its
+  ``2w = max(6, ceil(log10(1/eps)) + 2)`` taps (8 at the default ``eps = 1e-6``), deconvolved by its
   continuous transform (Gauss-Legendre quadrature).  Measured error against direct sums:
   1e-7 at ``w = 4`` in float64, 3e-7 with float32 weights.
 * ``"gaussian"`` (``PF_NUFFT_WINDOW=gaussian``): the reference's own stencil, half-width
@@ -43,8 +43,10 @@ _ES_BETA_PER_TAP = 2.30
 
 
 def es_half_width(eps: float) -> int:
-    """Half-width w of the exponential-of-semicircle window: 2w = ceil(log10(1/eps)) + 2 taps."""
-    return max(2, -(-(math.ceil(math.log10(1.0 / eps)) + 2) // 2))
+    """Half-width w of the exponential-of-semicircle window: 2w = ceil(log10(1/eps)) + 2 taps,
+    at least 6 (1e-5 against direct sums), so that even the loosest request stays inside the
+    1e-4 parity gate against the reference, whose Gaussian over-delivers at loose eps."""
+    return max(3, -(-(math.ceil(math.log10(1.0 / eps)) + 2) // 2))
 
 
 def es_transform(w: int, xi: np.ndarray) -> np.ndarray:

@@ -129,7 +129,7 @@ def test_type1_register_finish_vs_oracle(rng, m, eps):
         assert O.rel_l2(got[i], ref_nat) < max(2e-6, 0.2 * eps)
 
 
-@pytest.mark.parametrize("window,eps,tol", [("es", 1e-6, 1e-6), ("es", 1e-4, 3e-5),
+@pytest.mark.parametrize("window,eps,tol", [("es", 1e-6, 1e-6), ("es", 1e-4, 3e-5), ("es", 1e-2, 3e-5),
                                             ("es", 1e-9, 1e-6), ("gaussian", 1e-6, 1e-6)])
 def test_nufft_windows_vs_direct_sums(rng, window, eps, tol):
     """Type 1 and type 2 in 2D against the direct sums (no NUFFT in the reference value):
