@@ -82,32 +82,42 @@ def main(d):
             "byte", "D T 4 + D F 8 bytes")
         if c == 5:
             row(out, c, "k_spread (type-1 spreading)", pick(agg, "k_spread"),
-                32 * 131072 * 17 * 17 * 8, "flop", "F x L x 17^2 taps x 8")
+                32 * 131072 * 8 * 8 * 8, "flop", "F x L x 8^2 taps x 8 (ES window)")
             m = 2048
             row(out, c, "k_t1_rows + k_t1_cols (type-1 finish)", pick(agg, "k_t1_"),
                 32 * (m + m // 2) * fft(m), "flop", f"F x ({m} rows + {m // 2} kept columns) x FFT({m})")
-    p = os.path.join(d, "step_c2.csv")
-    if os.path.exists(p):
+    for c, planes, nodes in ((2, 64, 1), (7, 228, 12)):
+        p = os.path.join(d, f"step_c{c}.csv")
+        if not os.path.exists(p):
+            continue
         agg, cnt = times(p)
-        row(out, 2, "k_interp2_batch_h (type-2 readout)", pick(agg, "k_interp2"),
-            16 * 1_000_000 * 17 * 17 * 8, "flop", "F x 1e6 voxels x 17^2 taps x 8")
-        row(out, 2, "k_xfft_lines<20> + k_fft_lines (fine-grid inverse FFTs, 700 points)",
-            pick(agg, "k_xfft_lines", "k_fft_lines<1>"), 16 * 64 * (350 + 700) * fft(700),
-            "flop", "F x 64 planes x (350 rows + 700 columns) x FFT(700)")
-        row(out, 2, "k_place (spectrum onto the fine grid)", pick(agg, "k_place"),
-            16 * 64 * (350 * 350 * 8 + 700 * 700 * 8), "byte",
-            "F x 64 x (350^2 read + 700^2 written) x 8 B")
-        row(out, 2, "k_spread<16> (3D type-1 spreading)", pick(agg, "k_spread"),
-            16 * 16384 * 17 ** 3 * 8, "flop", "F x L x 17^3 taps x 8")
+        what = "64 planes" if c == 2 else "228 node planes"
+        row(out, c, "k_interp2_es8 (type-2 readout, ES window 8 x 8 taps)", pick(agg, "k_interp2"),
+            16 * 1_000_000 * nodes * 8 * 8 * 8, "flop",
+            f"F x 1e6 voxels x {nodes} grid(s) x 8^2 taps x 8")
+        row(out, c, "k_t2_rows_split + k_t2_cols_split (type-2 start: place + fine-grid inverse FFT)",
+            pick(agg, "k_t2_"), 16 * planes * (350 + 700) * 2 * fft(350), "flop",
+            f"F x {what} x (350 rows + 700 columns) x 2 FFT(350)")
+        row(out, c, "k_prop_kernel_rows + k_prop_columns (generic, P = 350: kernel and product spectra)",
+            pick(agg, "k_prop_"), 16 * planes * (176 + 176 + 350) * fft(350), "flop",
+            f"F x {what} x (176 + 176 + 350) lines x FFT(350)")
+        s1 = 16 * (5.0 * 20 * 270 * 270 * math.log2(20 * 270 * 270)
+                   + (40 * 540 + 40 * 270) * fft(540) + 270 * 270 * fft(40)
+                   + 4 * 270 * fft(270))
+        row(out, c, "k_fft_lines (stage 1: 3D kernel FFT, pruned fine-grid FFT, slab 2D transforms)",
+            pick(agg, "k_fft_lines"), s1, "flop",
+            "F x (FFT3(20 x 270 x 270) + pruned FFT3(40 x 540 x 540 -> 20 x 270 x 270) + 2 FFT2(270^2))")
+        row(out, c, "k_spread<16> (3D type-1 spreading, ES 8^3 taps)", pick(agg, "k_spread"),
+            16 * 16384 * 8 ** 3 * 8, "flop", "F x L x 8^3 taps x 8")
     p = os.path.join(d, "step_c1.csv")
     if os.path.exists(p):
         agg, _ = times(p)
         P, U = 140, 16 * 64
-        row(out, 1, "k_prop_kernel_rows + k_prop_columns + k_prop_rows_out_fb (generic, P = 140)",
-            pick(agg, "k_prop_"), U * (71 + 71 + 140 + 64) * fft(P), "flop",
+        row(out, 1, "k_prop_onchip (P = 140: every stage of a unit in shared memory)",
+            pick(agg, "k_prop_onchip", "k_onchip_sum"), U * (71 + 71 + 140 + 64) * fft(P), "flop",
             f"{U} units x (71 + 71 + 140 + 64) lines x FFT(140)")
-        row(out, 1, "k_spread<16> (type-1 spreading)", pick(agg, "k_spread"),
-            16 * 4096 * 17 * 17 * 8, "flop", "F x L x 17^2 taps x 8")
+        row(out, 1, "k_spread<16> (type-1 spreading, ES 8^2 taps)", pick(agg, "k_spread"),
+            16 * 4096 * 8 * 8 * 8, "flop", "F x L x 8^2 taps x 8")
         row(out, 1, "k_fft_lines (280-point fine grid)", pick(agg, "k_fft_lines", "k_xfft_lines"),
             16 * (280 + 140) * fft(280), "flop", "F x (280 rows + 140 kept columns) x FFT(280)")
     print("\n".join(out))
