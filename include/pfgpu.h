@@ -322,6 +322,16 @@ int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, int64_t s_str
                             const float* ky, const float* kx, int nv, void* fine,
                             int64_t fine_stride, const pf_fft_plan* plan_x,
                             const pf_fft_plan* plan_y, void* stream);
+/* The same with an output window: only the fine cells of columns [col0, col0 + ncols) and
+ * rows [row0, row0 + nrows) (indices on the torus: they may wrap past mr) are needed by the
+ * caller -- the cells its readout stencils touch.  With the split passes (mr = 2 m = 70 L)
+ * the y pass transforms only the window's columns and stores only its rows; cells outside
+ * the window are left unwritten.  (Without them the whole grid is formed.) */
+int pf_nufft_type2_start_2d_win(const pf_nufft_geom* g, const void* S, int64_t s_stride,
+                                const float* ky, const float* kx, int nv, void* fine,
+                                int64_t fine_stride, const pf_fft_plan* plan_x,
+                                const pf_fft_plan* plan_y, int col0, int ncols, int row0,
+                                int nrows, void* stream);
 /* type-2 start (spectral.py:374): modes / deconvolution onto their fine slots, 0 elsewhere. */
 int pf_nufft_place(const pf_nufft_geom* g, const void* S, int64_t s_stride, const float* kz,
                    const float* ky, const float* kx, int nv, void* fine, int64_t fine_stride,

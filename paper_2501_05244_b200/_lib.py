@@ -148,6 +148,7 @@ _SIGNATURES = {
     "pf_nufft_spread": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i64, _i, _vp, _i64, _vp],
     "pf_nufft_deconv": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp],
     "pf_nufft_type2_start_2d": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _i, _vp, _i64, _P(PfFftPlan), _P(PfFftPlan), _vp],
+    "pf_nufft_type2_start_2d_win": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _i, _vp, _i64, _P(PfFftPlan), _P(PfFftPlan), _i, _i, _i, _i, _vp],
     "pf_nufft_place": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp],
     "pf_nufft_interp2_acc": [_P(PfNufftGeom), _vp, _vp, _vp, _i, _vp, _i64, _i, _vp, _d, _i, _f,
                              _vp, _i, _vp, _i64, _i64, _vp, _vp],

@@ -360,9 +360,11 @@ class _Type2Readout:
         # every plane's points, cell-sorted within the plane, concatenated in plane order:
         # one interpolation launch serves a whole plane batch
         i0s, d0s, xyzs, pls, dsts, self.pt_lo = [], [], [], [], [], [0]
+        psets = []
         for k, (start, cnt, nux, nuy, pts, z) in enumerate(geo):
             tor = np.column_stack([2.0 * np.pi * nux / px, 2.0 * np.pi * nuy / py])
             npts = self.plan.points(tor, cell_sorted=True)
+            psets.append(npts)
             xyz = np.column_stack([pts[:, 0], pts[:, 1], np.full(cnt, z)])[npts.order]
             i0s.append(npts.i0)
             d0s.append(npts.d0)
@@ -370,6 +372,8 @@ class _Type2Readout:
             pls.append(np.full(cnt, k, dtype=np.int32))
             dsts.append(start + npts.order.astype(np.int64))
             self.pt_lo.append(self.pt_lo[-1] + cnt)
+        # the fine cells any voxel's stencil touches: the type-2 start forms no others
+        self.window = nu.stencil_window(self.plan, psets) if _T2_WINDOW else None
         self.i0_all = torch.cat(i0s)
         self.d0_all = torch.cat(d0s)
         self.xyz_all = torch.from_numpy(np.ascontiguousarray(np.vstack(xyzs))).to(device)
@@ -399,7 +403,8 @@ class _Type2Readout:
                           dev.ptr(self.prop.ws_a), s)
                 _lib.call("pf_prop_columns", pp, n, gref, self.prop.plan_y.ref,
                           dev.ptr(self.prop.ws_a), dev.ptr(uhat), dev.ptr(self.spec), 1, s)
-                nu.place_and_inverse(self.plan, self.spec, n * I, py * px, self.fine, stream)
+                nu.place_and_inverse(self.plan, self.spec, n * I, py * px, self.fine, stream,
+                                     self.window)
                 lo, hi = self.pt_lo[b0], self.pt_lo[b0 + n]
                 fe = self.plan.fine_elems
                 _lib.call("pf_nufft_interp2_batch", self.plan.gref,
@@ -415,6 +420,7 @@ class _Type2Readout:
 # arbitrary voxel depths: z-Chebyshev type-2 readout
 # ---------------------------------------------------------------------------
 
+_T2_WINDOW = os.environ.get("PF_T2_WINDOW", "1") != "0"   # type-2 start limited to the stencils' cells
 _ZCHEB_NODES = int(os.environ.get("PF_ZCHEB_NODES", "12"))
 _ZCHEB_KAPPA = float(os.environ.get("PF_ZCHEB_KAPPA", "6.0"))   # k_max x slab thickness
 
@@ -489,6 +495,7 @@ class _ZChebReadout:
         # voxels slab by slab, cell-sorted within a slab; each carries its slab's first
         # node plane and its node weights
         i0s, d0s, xyzs, pls, dsts, lws, self.pt_lo = [], [], [], [], [], [], [0]
+        psets = []
         for s in range(S):
             idx = np.nonzero(slab == s)[0]
             if idx.size:
@@ -496,6 +503,7 @@ class _ZChebReadout:
                 tor = np.column_stack([2.0 * np.pi * (sp[:, 0] - cx) / dx / px,
                                        2.0 * np.pi * (sp[:, 1] - cy) / dy / py])
                 npts = self.plan.points(tor, cell_sorted=True)
+                psets.append(npts)
                 o = npts.order
                 i0s.append(npts.i0)
                 d0s.append(npts.d0)
@@ -504,6 +512,7 @@ class _ZChebReadout:
                 dsts.append(idx[o].astype(np.int64))
                 lws.append(lw[idx[o]])
             self.pt_lo.append(self.pt_lo[-1] + idx.size)
+        self.window = nu.stencil_window(self.plan, psets) if _T2_WINDOW else None
         cat = torch.cat
         self.i0_all = cat(i0s)
         self.d0_all = cat(d0s)
@@ -535,7 +544,8 @@ class _ZChebReadout:
                           dev.ptr(self.prop.ws_a), s)
                 _lib.call("pf_prop_columns", pp, n, gref, self.prop.plan_y.ref,
                           dev.ptr(self.prop.ws_a), dev.ptr(uhat), dev.ptr(self.spec), 1, s)
-                nu.place_and_inverse(self.plan, self.spec, n * I, py * px, self.fine, stream)
+                nu.place_and_inverse(self.plan, self.spec, n * I, py * px, self.fine, stream,
+                                     self.window)
                 lo, hi = self.pt_lo[s0], self.pt_lo[s1]
                 if hi == lo:
                     continue

@@ -40,6 +40,7 @@ struct Plan {
   std::vector<float> d0;
   std::vector<double> xyz;
   std::vector<int64_t> dst, pt_lo;
+  int win[4];        // col0, ncols, row0, nrows: the fine cells the voxels' stencils touch
   int64_t n_tw[4];   // px, py, mry, mrx tables (0 = shared with an earlier one)
   int64_t off_tw[4], off_planes, off_ill, off_fw, off_ker[3], off_i0, off_d0, off_xyz, off_pl,
       off_dst, off_uhat, off_wa, off_spec, off_fine, total;
@@ -112,6 +113,7 @@ int plan(const pf_nursd2_args* a, Plan* P) {
     start += cnt;
     P->pt_lo.push_back(start);
   }
+  nufft2_stencil_window(P->nu, P->i0, N, P->win);
   // product-only propagation geometry over the whole pad (reconstruct.py:441-449)
   pf_prop_geom& g = P->g;
   g = pf_prop_geom{};
@@ -249,8 +251,9 @@ extern "C" int pf_nursd2(const pf_nursd2_args* a, const void* slices, void* vol,
       // type-2 first half (spectral.py:373-375): place (spectrum / deconvolution) and the
       // inverse fine-grid FFT, fused (pf_nufft_type2_start_2d)
       if (rc == 0)
-        rc = pf_nufft_type2_start_2d(&P.nu.g, spec, (int64_t)py * px, ky, kx, nv, fine, fe,
-                                     &pl[3], &pl[2], stream);
+        rc = pf_nufft_type2_start_2d_win(&P.nu.g, spec, (int64_t)py * px, ky, kx, nv, fine, fe,
+                                         &pl[3], &pl[2], P.win[0], P.win[1], P.win[2], P.win[3],
+                                         stream);
       const int64_t lo = P.pt_lo[b0], hi = P.pt_lo[b0 + n];
       if (rc == 0 && hi > lo)
         rc = pf_nufft_interp2_batch(

@@ -189,6 +189,42 @@ inline int nufft2_points(const Nufft2Plan& N, const double* tx, const double* ty
   return 0;
 }
 
+// (col0, ncols, row0, nrows): per axis the shortest arc of the fine-grid torus holding every
+// stencil cell (anchor - w .. anchor + w) of the points i0 [L][3] (nufft.stencil_window):
+// all a type-2 readout of these points reads
+inline void nufft2_stencil_window(const Nufft2Plan& N, const std::vector<int32_t>& i0, int64_t L,
+                                  int win[4]) {
+  for (int s = 0; s < 2; s++) {
+    const int a = s == 0 ? 2 : 1;
+    const int mr = N.g.mr[a], w = N.g.w;
+    std::vector<char> touched((size_t)mr, 0);
+    for (int64_t l = 0; l < L; l++)
+      for (int j = -w; j <= w; j++) touched[(size_t)((((i0[3 * l + a] + j) % mr) + mr) % mr)] = 1;
+    int first = -1, best_gap = -1, best_after = 0, prev = -1;
+    for (int c = 0; c < mr; c++) {
+      if (!touched[c]) continue;
+      if (first < 0) first = c;
+      if (prev >= 0 && c - prev - 1 > best_gap) {
+        best_gap = c - prev - 1;
+        best_after = c;
+      }
+      prev = c;
+    }
+    if (first < 0) {   // no points
+      win[2 * s] = 0;
+      win[2 * s + 1] = mr;
+      continue;
+    }
+    const int wrap_gap = first + mr - prev - 1;   // the run across the seam
+    if (wrap_gap > best_gap) {
+      best_gap = wrap_gap;
+      best_after = first;
+    }
+    win[2 * s] = best_gap > 0 ? best_after : 0;
+    win[2 * s + 1] = mr - (best_gap > 0 ? best_gap : 0);
+  }
+}
+
 // tile buckets of the gather-spread kernel (NufftPoints.tiles): CSR over the fine-grid
 // tiles each point's (2w + 1)^2 stencil touches, points ascending within a tile
 inline void nufft2_tiles(const Nufft2Plan& N, const std::vector<int32_t>& i0, int64_t L,

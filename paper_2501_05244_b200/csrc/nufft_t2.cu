@@ -111,31 +111,32 @@ k_t2_cols(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fine_str
 // warp's 32 lanes (3 lines x 10 lanes) where the 700-point transform fills 20.  The
 // half-length twiddle table W_m^{k1 t} is formed in shared memory from the 2 m plan's
 // unit roots.  Results differ from the unsplit passes by float32 rounding only.
-template <int HL>
+template <int HL, int NT>
 __device__ __forceinline__ void t2_half_table(float2* tw2, int m, const float2* __restrict__ roots2m) {
-  for (int e = threadIdx.x; e < XFFT_R * HL; e += T2_THREADS) {
+  for (int e = threadIdx.x; e < XFFT_R * HL; e += NT) {
     const int k1 = e / HL, t = e - k1 * HL;
     tw2[e] = __ldg(roots2m + 2 * ((k1 * t) % m));
   }
 }
 
-template <int HL>
-__global__ void __launch_bounds__(T2_THREADS, 2)
+template <int HL, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
 k_t2_rows_split(pf_nufft_geom G, const float2* __restrict__ S, long long s_stride,
                 const float* __restrict__ ky, const float* __restrict__ kx, int nv,
-                float2* __restrict__ fine, long long fine_stride, pf_fft_plan plan_x, int cnt) {
+                float2* __restrict__ fine, long long fine_stride, pf_fft_plan plan_x, int cnt,
+                int col0, int ncols) {
   extern __shared__ float2 sm[];
   const int mrx = G.mr[2], mx = G.m[2], my = G.m[1], mry = G.mr[1];
   const int ld = pf_ld(mx);
   float2* a = sm;                                   // [2 cnt][ld]: line c -> rows 2c (even), 2c + 1
   float2* tw2 = sm + (size_t)2 * cnt * ld;          // [35][HL]
   const float2* roots = reinterpret_cast<const float2*>(plan_x.tw);
-  t2_half_table<HL>(tw2, mx, roots);
+  t2_half_table<HL, NT>(tw2, mx, roots);
   const long long nlines = (long long)nv * my;
   const long long l0 = (long long)blockIdx.x * cnt;
   const int nl = (int)(nlines - l0 < cnt ? nlines - l0 : cnt);
   const FastDiv dmx(mx);
-  for (int e = threadIdx.x; e < nl * mx; e += T2_THREADS) {
+  for (int e = threadIdx.x; e < nl * mx; e += NT) {
     const int c = dmx.div(e), q = e - c * mx;
     const long long l = l0 + c;
     const int v = (int)(l / my), i = (int)(l - (long long)v * my);
@@ -149,22 +150,35 @@ k_t2_rows_split(pf_nufft_geom G, const float2* __restrict__ S, long long s_strid
   }
   __syncthreads();
   xfft_tile<HL, 1, true>(a, ld, 2 * nl, tw2);
-  for (int e = threadIdx.x; e < nl * mx; e += T2_THREADS) {
+  for (int e = threadIdx.x; e < nl * mx; e += NT) {
     const int c = dmx.div(e), j = e - c * mx;
     const long long l = l0 + c;
     const int v = (int)(l / my), i = (int)(l - (long long)v * my);
     const int cy = i - my / 2;
     const int fy = cy < 0 ? cy + mry : cy;
+    // only the columns some readout stencil touches are stored (window [col0, col0 + ncols)
+    // on the torus): the column pass transforms no others
+    int d0 = 2 * j - col0, d1 = 2 * j + 1 - col0;
+    d0 += d0 < 0 ? mrx : 0;
+    d1 += d1 < 0 ? mrx : 0;
+    const bool in0 = d0 < ncols, in1 = d1 < ncols;
+    if (!in0 && !in1) continue;
     const float2 ev = a[(2 * c) * ld + j], od = a[(2 * c + 1) * ld + j];
-    *reinterpret_cast<float4*>(fine + (long long)v * fine_stride + (long long)fy * mrx + 2 * j) =
-        make_float4(ev.x, ev.y, od.x, od.y);
+    float2* dst = fine + (long long)v * fine_stride + (long long)fy * mrx + 2 * j;
+    if (in0 && in1) {
+      *reinterpret_cast<float4*>(dst) = make_float4(ev.x, ev.y, od.x, od.y);
+    } else if (in0) {
+      dst[0] = ev;
+    } else {
+      dst[1] = od;
+    }
   }
 }
 
-template <int HL>
-__global__ void __launch_bounds__(T2_THREADS, 2)
+template <int HL, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
 k_t2_cols_split(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fine_stride,
-                pf_fft_plan plan_y, int cnt) {
+                pf_fft_plan plan_y, int cnt, int col0, int ncols, int row0, int nrows) {
   extern __shared__ float2 sm[];
   __shared__ long long lbase[64];
   const int mrx = G.mr[2], my = G.m[1], mry = G.mr[1];
@@ -172,18 +186,22 @@ k_t2_cols_split(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fi
   float2* a = sm;                                   // [2 cnt][ld]
   float2* tw2 = sm + (size_t)2 * cnt * ld;
   const float2* roots = reinterpret_cast<const float2*>(plan_y.tw);
-  t2_half_table<HL>(tw2, my, roots);
-  const long long nlines = (long long)nv * mrx;
+  t2_half_table<HL, NT>(tw2, my, roots);
+  // only the columns of the window [col0, col0 + ncols) (torus) are transformed, and of each
+  // only the rows of [row0, row0 + nrows) are stored: the cells the readout stencils touch
+  const long long nlines = (long long)nv * ncols;
   const long long l0 = (long long)blockIdx.x * cnt;
   const int nl = (int)(nlines - l0 < cnt ? nlines - l0 : cnt);
-  for (int c = threadIdx.x; c < nl; c += T2_THREADS) {
+  for (int c = threadIdx.x; c < nl; c += NT) {
     const long long l = l0 + c;
-    const long long v = l / mrx;
-    lbase[c] = v * fine_stride + (l - v * mrx);
+    const long long v = l / ncols;
+    int col = col0 + (int)(l - v * ncols);
+    col -= col >= mrx ? mrx : 0;
+    lbase[c] = v * fine_stride + col;
   }
   __syncthreads();
   const FastDiv dnl(nl);
-  for (int e = threadIdx.x; e < nl * my; e += T2_THREADS) {
+  for (int e = threadIdx.x; e < nl * my; e += NT) {
     const int q = dnl.div(e), c = e - q * nl;
     const int cy = q - my / 2;
     const int fy = cy < 0 ? cy + mry : cy;      // the kept fine row holding mode cy
@@ -194,8 +212,10 @@ k_t2_cols_split(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fi
   }
   __syncthreads();
   xfft_tile<HL, 1, true>(a, ld, 2 * nl, tw2);
-  for (int e = threadIdx.x; e < nl * mry; e += T2_THREADS) {
-    const int fy = dnl.div(e), c = e - fy * nl;
+  for (int e = threadIdx.x; e < nl * nrows; e += NT) {
+    const int r = dnl.div(e), c = e - r * nl;
+    int fy = row0 + r;
+    fy -= fy >= mry ? mry : 0;
     fine[lbase[c] + (long long)fy * mrx] = a[(2 * c + (fy & 1)) * ld + (fy >> 1)];
   }
 }
@@ -224,8 +244,10 @@ void t2_allow_all() {
   t2_allow(k_t2_rows<XL>);
   t2_allow(k_t2_cols<XL>);
   if constexpr (XL > 0) {
-    t2_allow(k_t2_rows_split<XL>);
-    t2_allow(k_t2_cols_split<XL>);
+    t2_allow(k_t2_rows_split<XL, 128>);
+    t2_allow(k_t2_cols_split<XL, 128>);
+    t2_allow(k_t2_rows_split<XL, 256>);
+    t2_allow(k_t2_cols_split<XL, 256>);
   }
 }
 
@@ -238,35 +260,56 @@ int t2_split_L(int m) {
   }
   return on ? xfft_L(m) : 0;
 }
-// fine lines per CTA: one round of the 8 warps' 32 / L' half-lines each
-int t2_split_cnt(int m, int hl) {
-  (void)m;
-  int cnt = (T2_THREADS / 32) * (32 / hl) / 2;
+// threads per CTA of the split passes (PF_T2_THREADS_ROWS / PF_T2_THREADS_COLS: 128 or 256)
+int t2_split_threads(bool cols) {
+  static int tr = -1, tc = -1;
+  if (tr < 0) {
+    const char* e = getenv("PF_T2_THREADS_ROWS");
+    tr = (e && atoi(e) == 256) ? 256 : 128;
+    e = getenv("PF_T2_THREADS_COLS");
+    tc = (e && atoi(e) == 128) ? 128 : 256;
+  }
+  return cols ? tc : tr;
+}
+// fine lines per CTA: one round of the warps' 32 / L' half-lines each
+int t2_split_cnt(int nt, int hl) {
+  int cnt = (nt / 32) * (32 / hl) / 2;
   return cnt < 1 ? 1 : (cnt > 32 ? 32 : cnt);
 }
 size_t t2_split_smem(int m, int hl, int cnt) {
   return ((size_t)2 * cnt * pf_ld(m) + (size_t)XFFT_R * hl) * sizeof(float2);
 }
 template <int HL, typename... A>
-void t2_launch_rows_split(unsigned grid, size_t smem, cudaStream_t st, A... args) {
-  if constexpr (HL > 0) k_t2_rows_split<HL><<<grid, T2_THREADS, smem, st>>>(args...);
+void t2_launch_rows_split(int nt, unsigned grid, size_t smem, cudaStream_t st, A... args) {
+  if constexpr (HL > 0) {
+    if (nt == 128) k_t2_rows_split<HL, 128><<<grid, 128, smem, st>>>(args...);
+    else k_t2_rows_split<HL, 256><<<grid, 256, smem, st>>>(args...);
+  }
 }
 template <int HL, typename... A>
-void t2_launch_cols_split(unsigned grid, size_t smem, cudaStream_t st, A... args) {
-  if constexpr (HL > 0) k_t2_cols_split<HL><<<grid, T2_THREADS, smem, st>>>(args...);
+void t2_launch_cols_split(int nt, unsigned grid, size_t smem, cudaStream_t st, A... args) {
+  if constexpr (HL > 0) {
+    if (nt == 128) k_t2_cols_split<HL, 128><<<grid, 128, smem, st>>>(args...);
+    else k_t2_cols_split<HL, 256><<<grid, 256, smem, st>>>(args...);
+  }
 }
 
 }  // namespace
 
-extern "C" int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, int64_t s_stride,
-                                       const float* ky, const float* kx, int nv, void* fine,
-                                       int64_t fine_stride, const pf_fft_plan* plan_x,
-                                       const pf_fft_plan* plan_y, void* stream) {
+extern "C" int pf_nufft_type2_start_2d_win(const pf_nufft_geom* g, const void* S,
+                                           int64_t s_stride, const float* ky, const float* kx,
+                                           int nv, void* fine, int64_t fine_stride,
+                                           const pf_fft_plan* plan_x, const pf_fft_plan* plan_y,
+                                           int col0, int ncols, int row0, int nrows,
+                                           void* stream) {
   PF_ARG_CHECK(g && g->dim == 2 && g->mr[0] == 1 && nv >= 1 && plan_x && plan_y &&
                    plan_x->n == g->mr[2] && plan_y->n == g->mr[1] && g->m[2] <= g->mr[2] &&
                    g->m[1] <= g->mr[1],
                "pf_nufft_type2_start_2d: bad args (2D plan, plans of the fine-grid lengths)");
   PF_ARG_CHECK(S && fine && ky && kx, "pf_nufft_type2_start_2d: null buffer");
+  PF_ARG_CHECK(col0 >= 0 && col0 < g->mr[2] && ncols >= 1 && ncols <= g->mr[2] && row0 >= 0 &&
+                   row0 < g->mr[1] && nrows >= 1 && nrows <= g->mr[1],
+               "pf_nufft_type2_start_2d_win: window outside the fine grid");
   static PfDevOnce attr;
   if (attr.first()) {   // every instantiation: later calls may take other lengths
     for (int xl : {0, 4, 5, 8, 10, 15, 20, 30}) PF_XL_DISPATCH(xl, (t2_allow_all<XL>()));
@@ -277,12 +320,14 @@ extern "C" int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, in
   const int hlx = g->mr[2] == 2 * g->m[2] ? t2_split_L(g->m[2]) : 0;
   const int hly = g->mr[1] == 2 * g->m[1] ? t2_split_L(g->m[1]) : 0;
   if (hlx) {
-    const int cnt = t2_split_cnt(g->m[2], hlx);
+    const int nt = t2_split_threads(false);
+    const int cnt = t2_split_cnt(nt, hlx);
     const long long nl = (long long)nv * g->m[1];
     const size_t smem = t2_split_smem(g->m[2], hlx, cnt);
-    PF_XL_DISPATCH(hlx, (t2_launch_rows_split<XL>((unsigned)((nl + cnt - 1) / cnt), smem, st, *g,
+    PF_XL_DISPATCH(hlx, (t2_launch_rows_split<XL>(nt, (unsigned)((nl + cnt - 1) / cnt), smem, st, *g,
                                                   (const float2*)S, s_stride, ky, kx, nv,
-                                                  (float2*)fine, fine_stride, *plan_x, cnt)));
+                                                  (float2*)fine, fine_stride, *plan_x, cnt,
+                                                  hly ? col0 : 0, hly ? ncols : g->mr[2])));
     PF_LAUNCH_CHECK("k_t2_rows_split");
   } else {
     const int cnt = t2_cnt(g->mr[2], xlx, 1, 1);
@@ -294,11 +339,13 @@ extern "C" int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, in
     PF_LAUNCH_CHECK("k_t2_rows");
   }
   if (hly) {
-    const int cnt = t2_split_cnt(g->m[1], hly);
-    const long long nl = (long long)nv * g->mr[2];
+    const int nt = t2_split_threads(true);
+    const int cnt = t2_split_cnt(nt, hly);
+    const long long nl = (long long)nv * ncols;
     const size_t smem = t2_split_smem(g->m[1], hly, cnt);
-    PF_XL_DISPATCH(hly, (t2_launch_cols_split<XL>((unsigned)((nl + cnt - 1) / cnt), smem, st, *g,
-                                                  nv, (float2*)fine, fine_stride, *plan_y, cnt)));
+    PF_XL_DISPATCH(hly, (t2_launch_cols_split<XL>(nt, (unsigned)((nl + cnt - 1) / cnt), smem, st, *g,
+                                                  nv, (float2*)fine, fine_stride, *plan_y, cnt,
+                                                  col0, ncols, row0, nrows)));
     PF_LAUNCH_CHECK("k_t2_cols_split");
   } else {
     // columns: >= 16 adjacent columns per CTA for 128-byte row segments
@@ -310,4 +357,13 @@ extern "C" int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, in
     PF_LAUNCH_CHECK("k_t2_cols");
   }
   return 0;
+}
+
+extern "C" int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, int64_t s_stride,
+                                       const float* ky, const float* kx, int nv, void* fine,
+                                       int64_t fine_stride, const pf_fft_plan* plan_x,
+                                       const pf_fft_plan* plan_y, void* stream) {
+  PF_ARG_CHECK(g, "pf_nufft_type2_start_2d: null geometry");
+  return pf_nufft_type2_start_2d_win(g, S, s_stride, ky, kx, nv, fine, fine_stride, plan_x,
+                                     plan_y, 0, g->mr[2], 0, g->mr[1], stream);
 }

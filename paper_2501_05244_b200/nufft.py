@@ -260,16 +260,44 @@ def type1(plan: NufftPlan, pts: NufftPoints, vals: torch.Tensor, nv: int, val_st
     return out
 
 
+def stencil_window(plan: NufftPlan, point_sets) -> tuple[int, int, int, int]:
+    """(col0, ncols, row0, nrows): per axis the shortest arc of the fine-grid torus that holds
+    every stencil cell (anchor - w .. anchor + w) of every point in ``point_sets``
+    (NufftPoints of a 2D plan) -- all a type-2 readout of these points ever reads."""
+    out = []
+    for a in (2, 1):
+        mr, w = plan.mrs[a], plan.w
+        touched = np.zeros(mr, dtype=bool)
+        for ps in point_sets:
+            i0 = np.unique(ps._i0_host[:, a] % mr)
+            for j in range(-w, w + 1):
+                touched[(i0 + j) % mr] = True
+        if touched.all() or not touched.any():
+            out += [0, mr]
+            continue
+        # longest circular run of untouched cells; the window is its complement
+        idx = np.flatnonzero(touched)
+        gaps = np.diff(np.append(idx, idx[0] + mr)) - 1
+        g = int(np.argmax(gaps))
+        start = int(idx[(g + 1) % idx.size])
+        out += [start, mr - int(gaps[g])]
+    return tuple(out)
+
+
 def place_and_inverse(plan: NufftPlan, S: torch.Tensor, nv: int, s_stride: int,
-                      fine: torch.Tensor, stream=None) -> torch.Tensor:
-    """Type-2 first half (spectral.py:373-375): fine = ifftn(place(S / ker)) * prod(mr)."""
+                      fine: torch.Tensor, stream=None, window=None) -> torch.Tensor:
+    """Type-2 first half (spectral.py:373-375): fine = ifftn(place(S / ker)) * prod(mr).
+    ``window`` (``stencil_window``): the caller reads only these fine cells, the others may
+    be left unformed."""
     kz, ky, kx = plan.kers
     if plan.dim == 2 and _T2_FUSED:
-        # place + pruned inverse FFT in two fused passes (bit-identical)
-        _lib.call("pf_nufft_type2_start_2d", plan.gref, dev.ptr(S), s_stride, dev.ptr(ky),
+        # place + pruned inverse FFT in two fused passes
+        c0, nc, r0, nr = window if window is not None else (0, plan.mrs[2], 0, plan.mrs[1])
+        _lib.call("pf_nufft_type2_start_2d_win", plan.gref, dev.ptr(S), s_stride, dev.ptr(ky),
                   dev.ptr(kx), nv, dev.ptr(fine), plan.fine_elems,
                   dev.fft_plan(plan.mrs[2], plan.device).ref,
-                  dev.fft_plan(plan.mrs[1], plan.device).ref, dev.stream_ptr(stream))
+                  dev.fft_plan(plan.mrs[1], plan.device).ref, c0, nc, r0, nr,
+                  dev.stream_ptr(stream))
         return fine
     _lib.call("pf_nufft_place", plan.gref, dev.ptr(S), s_stride, dev.ptr(kz), dev.ptr(ky),
               dev.ptr(kx), nv, dev.ptr(fine), plan.fine_elems, 0, dev.stream_ptr(stream))

@@ -199,3 +199,53 @@ def test_type2_start_fused_equals_place_and_pruned_fft(rng, monkeypatch, modes, 
     ref = np.fft.ifft2(grid) * mry * mrx
     got = fine_a[0].cpu().numpy().reshape(mry, mrx)
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5
+
+
+@pytest.mark.parametrize("modes,win", [((350, 350), (632, 136, 282, 140)),   # columns wrap the seam
+                                       ((140, 140), (10, 50, 250, 60)),      # rows wrap the seam
+                                       ((70, 350), (100, 200, 0, 140))])     # x split only
+def test_type2_start_window(rng, modes, win):
+    """pf_nufft_type2_start_2d_win: the fine cells inside the window are bit-identical to the
+    full start and (where the column pass is split) cells in columns outside it stay
+    unwritten -- the readout stencils never touch them (nufft.stencil_window)."""
+    import torch
+    from paper_2501_05244_b200 import nufft as nu
+    plan = nu.NufftPlan(modes, 1e-6, torch.device("cuda"))
+    my, mx = modes
+    mry, mrx = plan.mrs[1], plan.mrs[2]
+    nv = 3
+    S = torch.from_numpy((rng.normal(size=(nv, my * mx)) + 1j * rng.normal(size=(nv, my * mx)))
+                         .astype(np.complex64)).cuda()
+    full = torch.empty((nv, plan.fine_elems), dtype=torch.complex64, device="cuda")
+    part = torch.full_like(full, complex(np.nan, np.nan))
+    nu.place_and_inverse(plan, S, nv, my * mx, full)
+    nu.place_and_inverse(plan, S, nv, my * mx, part, window=win)
+    torch.cuda.synchronize()
+    c0, nc, r0, nr = win
+    cols = (c0 + np.arange(nc)) % mrx
+    rows = (r0 + np.arange(nr)) % mry
+    f = full.cpu().numpy().reshape(nv, mry, mrx)
+    g = part.cpu().numpy().reshape(nv, mry, mrx)
+    inside = np.ix_(np.arange(nv), rows, cols)
+    assert np.array_equal(f[inside], g[inside])
+    if mry == 2 * my and my % 35 == 0 and my // 35 in (4, 5, 8, 10, 15, 20, 30):   # split column pass
+        out_cols = np.setdiff1d(np.arange(mrx), cols)
+        out_rows = np.setdiff1d(np.arange(mry), np.concatenate([np.arange(my - my // 2),
+                                                                np.arange(mry - my // 2, mry)]))
+        assert np.isnan(g[np.ix_(np.arange(nv), out_rows, out_cols)]).all()
+
+
+def test_stencil_window_covers_every_tap(rng):
+    """nufft.stencil_window holds every stencil cell of every point, across the seam too."""
+    import torch
+    from paper_2501_05244_b200 import nufft as nu
+    plan = nu.NufftPlan((350, 350), 1e-6, torch.device("cuda"))
+    pts = np.column_stack([rng.uniform(-0.4, 0.7, 500), rng.uniform(2.6, 3.6, 500)])
+    pts[:, 1] = (pts[:, 1] + np.pi) % (2 * np.pi) - np.pi          # y straddles +-pi
+    P = plan.points(pts)
+    c0, nc, r0, nr = nu.stencil_window(plan, [P])
+    assert nc < 300 and nr < 200
+    for a, (s0, n) in ((2, (c0, nc)), (1, (r0, nr))):
+        mr = plan.mrs[a]
+        cells = (P._i0_host[:, a][:, None] + np.arange(-plan.w, plan.w + 1)[None, :]) % mr
+        assert (((cells - s0) % mr) < n).all()
