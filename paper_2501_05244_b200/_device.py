@@ -175,7 +175,7 @@ def kept_ranges(m: int, mr: int) -> list[tuple[int, int]]:
 
 
 def fftn_pruned(buf: torch.Tensor, shape: tuple[int, ...], nbatch: int, direction: int,
-                kept: list, outputs: bool, stream=None) -> None:
+                kept: list, outputs: bool, stream=None, nonzero: list | None = None) -> None:
     """In-place 2D/3D FFT of ``nbatch`` contiguous arrays computing only the lines a
     NUFFT needs.  ``kept[a]``: (start, length) runs of the kept slots on axis a.
     outputs=True (type 1, forward): only kept outputs are read afterwards, so an axis
@@ -183,7 +183,10 @@ def fftn_pruned(buf: torch.Tensor, shape: tuple[int, ...], nbatch: int, directio
     outputs=False (type 2, inverse): the input is zero off the kept slots, so an axis
     is transformed only along lines whose not-yet-transformed coordinates are kept
     (the other lines are zero and stay zero).  Axes run last to first, as in
-    ``fftn_natural``; line sets map onto pf_fft_lines' (inner, istr, ostr) indexing."""
+    ``fftn_natural``; line sets map onto pf_fft_lines' (inner, istr, ostr) indexing.
+    ``nonzero[a]`` (outputs=True only): runs of the slots of axis a that can be nonzero on
+    input (the cells a type-1 spreading touched); lines through all-zero slots of a
+    not-yet-transformed axis are zero and stay zero, so they are skipped as well."""
     d = len(shape)
     assert d in (2, 3)
     strides = [int(np.prod(shape[a + 1:])) for a in range(d)]
@@ -200,7 +203,9 @@ def fftn_pruned(buf: torch.Tensor, shape: tuple[int, ...], nbatch: int, directio
         if n == 1:
             continue
         others = [a for a in range(d) if a != ax]
-        runs = [kept[a] if (a > ax) == outputs else [(0, shape[a])] for a in others]
+        full = [(nonzero[a] if (outputs and nonzero is not None) else [(0, shape[a])])
+                for a in range(d)]
+        runs = [kept[a] if (a > ax) == outputs else full[a] for a in others]
         if d == 2:
             (o,) = others
             for s0, ln in runs[0]:

@@ -40,6 +40,7 @@ struct Plan {
   // NUFFT (modes (py, px), 2D)
   Nufft2Plan nu;
   std::vector<int32_t> i0, tstart, tpts;
+  int win[4];   // col0, ncols, row0, nrows: fine cells the relay points' stencils touch
   std::vector<float> d0;
   // workspace
   int64_t n_tw[4];   // px, py, mry, mrx tables (0 = shared with an earlier one)
@@ -100,6 +101,7 @@ int plan(const pf_nursd1_args* a, Plan* P) {
       return -1;
   }
   nufft2_tiles(P->nu, P->i0, Lp, &P->tstart, &P->tpts);
+  nufft2_stencil_window(P->nu, P->i0, Lp, P->win);
   const int mry = P->nu.g.mr[1], mrx = P->nu.g.mr[2];
   // ---- propagation geometry (algorithms._UhatPropEngine: centred output windows)
   pf_prop_geom& g = P->g;
@@ -243,8 +245,13 @@ extern "C" int pf_nursd1(const pf_nursd1_args* a, const void* slices, void* vol,
     // pruned fine-grid FFT (_device.fftn_pruned, outputs=True): every row along x, then
     // along y only the columns holding kept modes
     const int mry = P.nu.g.mr[1], mrx = P.nu.g.mr[2];
-    rc = pf_fft_lines(fine, &pl[3], (int64_t)nv * mry, mry, mrx, P.nu.fine_elems, 1, -1, 1.0f,
-                      stream);
+    // (x pass: only the rows the spreading touched; the other rows are zero and stay zero)
+    const int r0 = P.win[2], nr = P.win[3];
+    const int runs[2][2] = {{r0, r0 + nr <= mry ? nr : mry - r0}, {0, r0 + nr <= mry ? 0 : r0 + nr - mry}};
+    for (int q = 0; q < 2 && rc == 0; q++)
+      if (runs[q][1] > 0)
+        rc = pf_fft_lines(fine + (int64_t)runs[q][0] * mrx, &pl[3], (int64_t)nv * runs[q][1],
+                          runs[q][1], mrx, P.nu.fine_elems, 1, -1, 1.0f, stream);
     for (auto r : kept_ranges(P.px, mrx)) {
       if (rc != 0 || r.second == 0) continue;
       rc = pf_fft_lines(fine + r.first, &pl[2], (int64_t)nv * r.second, r.second, 1,

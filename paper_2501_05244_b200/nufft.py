@@ -38,6 +38,7 @@ _COORD_TOL = 1e-9
 TILE_2D = (1, 16, 16)
 TILE_3D = (4, 8, 8)
 _T2_FUSED = os.environ.get("PF_T2_FUSED", "1") != "0"
+_T1_SKIP_ZERO = os.environ.get("PF_T1_SKIP_ZERO", "1") != "0"
 DEFAULT_WINDOW = os.environ.get("PF_NUFFT_WINDOW", "es")
 _ES_BETA_PER_TAP = 2.30
 
@@ -187,6 +188,31 @@ class NufftPoints:
         self.plan = plan
         self._tiles = None
 
+    def touched_runs(self):
+        """Per transformed axis: runs (start, length) of the fine slots some stencil of these
+        points touches -- the shortest covering arc of the torus, split at the seam.  Every
+        other slot of a spread fine grid is zero."""
+        if getattr(self, "_runs", None) is None:
+            p = self.plan
+            runs = []
+            for a in range(3 - p.dim, 3):
+                mr, w = p.mrs[a], p.w
+                touched = np.zeros(mr, dtype=bool)
+                i0 = np.unique(self._i0_host[:, a] % mr)
+                for j in range(-w, w + 1):
+                    touched[(i0 + j) % mr] = True
+                if touched.all():
+                    runs.append([(0, mr)])
+                    continue
+                idx = np.flatnonzero(touched)
+                gaps = np.diff(np.append(idx, idx[0] + mr)) - 1
+                g = int(np.argmax(gaps))
+                start, n = int(idx[(g + 1) % idx.size]), mr - int(gaps[g])
+                runs.append([(start, n)] if start + n <= mr else
+                            [(0, start + n - mr), (start, mr - start)])
+            self._runs = runs
+        return self._runs
+
     def tiles(self):
         """CSR (tile_start, tile_pts) of the tiles each point's stencil touches."""
         if self._tiles is not None:
@@ -254,7 +280,10 @@ def type1(plan: NufftPlan, pts: NufftPoints, vals: torch.Tensor, nv: int, val_st
         return out
     shape = plan.mrs[3 - plan.dim:]
     # only the kept modes are gathered: transform only the lines that reach them
-    dev.fftn_pruned(fine, shape, nv, -1, plan.kept, True, stream)
+    # ... and, before an axis is transformed, only along lines through cells the spreading
+    # touched (the rest of the grid is zero and stays zero)
+    dev.fftn_pruned(fine, shape, nv, -1, plan.kept, True, stream,
+                    pts.touched_runs() if _T1_SKIP_ZERO else None)
     _lib.call("pf_nufft_deconv", plan.gref, dev.ptr(fine), plan.fine_elems, dev.ptr(kz),
               dev.ptr(ky), dev.ptr(kx), nv, dev.ptr(out), out_stride, int(transpose), s)
     return out

@@ -166,6 +166,53 @@ def test_fftn_pruned_line_sets(monkeypatch, shape, modes, nb):
     np.testing.assert_allclose(flat.reshape((nb,) + shape), ref2, rtol=1e-4, atol=1e-4)
 
 
+@pytest.mark.parametrize("shape,modes,nz,nb", [
+    ((12, 10), (5, 6), [[(3, 5)], [(0, 2), (7, 3)]], 2),                      # 2D, x arc wraps
+    ((8, 12, 10), (3, 5, 6), [[(6, 2), (0, 1)], [(2, 7)], [(1, 6)]], 2),      # 3D, z arc wraps
+    ((40, 54, 54), (20, 27, 27), [[(3, 30)], [(10, 26)], [(40, 14), (0, 12)]], 2)])
+def test_fftn_pruned_skips_zero_lines(monkeypatch, shape, modes, nz, nb):
+    """Type-1 line sets with the spreading's touched arcs (``nonzero``): the input is zero
+    off the arcs, and every kept output still equals numpy's fftn."""
+    import torch
+    from paper_2501_05244_b200 import _device as dev
+    rng = np.random.default_rng(6)
+    x = np.zeros((nb,) + shape, dtype=np.complex64)
+    idx = np.ix_(*[np.concatenate([np.arange(s0, s0 + ln) for s0, ln in r]) for r in nz])
+    for b in range(nb):
+        blk = x[b][idx].shape
+        x[b][idx] = (rng.normal(size=blk) + 1j * rng.normal(size=blk)).astype(np.complex64)
+    kept = [dev.kept_ranges(m, n) for m, n in zip(modes, shape)]
+    t = torch.from_numpy(x.copy())
+    flat = t.view(-1).numpy()
+    base = t.data_ptr()
+    lines = [0]
+
+    def fake(name, p, planref, nl, inner, istr, ostr, estr, direction, scale, stream):
+        n = planref._obj.n
+        off = (p - base) // 8
+        lines[0] += nl
+        for ln in range(nl):
+            i = off + (ln // inner) * ostr + (ln % inner) * istr + np.arange(n) * estr
+            flat[i] = np.fft.fft(flat[i].astype(np.complex128))
+        return 0
+
+    monkeypatch.setattr(dev._lib, "call", fake)
+    st = type("S", (), {"cuda_stream": 0})()
+    dev.fftn_pruned(t, shape, nb, -1, kept, True, st, nz)
+    with_skip = lines[0]
+    sel = np.ix_(*[np.concatenate([np.arange(s0, s0 + ln) for s0, ln in k]) for k in kept])
+    ref = np.fft.fftn(x.astype(np.complex128), axes=tuple(range(1, len(shape) + 1)))
+    for b in range(nb):
+        np.testing.assert_allclose(flat.reshape((nb,) + shape)[b][sel], ref[b][sel], rtol=1e-4,
+                                   atol=1e-4)
+    lines[0] = 0
+    t = torch.from_numpy(x.copy())
+    flat = t.view(-1).numpy()
+    base = t.data_ptr()
+    dev.fftn_pruned(t, shape, nb, -1, kept, True, st)
+    assert with_skip < lines[0]
+
+
 def test_zcheb_slabs_interpolate_kernel_phases():
     """The depth slabs / Chebyshev nodes of the arbitrary-depth readout reproduce an
     exp(i k r)/r kernel sample at random depths to < 1e-6 (CPU: host planning only)."""
