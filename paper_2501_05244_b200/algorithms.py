@@ -844,23 +844,30 @@ class _Lattice3dEngine(_UhatPropEngine):
         s = dev.stream_ptr(stream)
         gf = max(1, min(F, getattr(self, "group_f", 1)))   # frequencies per lattice-spectrum call
         uhat3g = torch.empty((gf * I * n3,), dtype=torch.complex64, device=self.device)
-        g3 = torch.empty((n3,), dtype=torch.complex64, device=self.device)
+        g3g = torch.empty((gf * n3,), dtype=torch.complex64, device=self.device)
         out = torch.empty((F * I * py * px,), dtype=torch.complex64, device=self.device)
-        for fi in range(F):
-            if fi % gf == 0:
-                self._lattice_spectra(coeff, fi, min(F, fi + gf), uhat3g, n3, stream)
-            uhat3 = uhat3g[(fi % gf) * I * n3:(fi % gf + 1) * I * n3]
-            khat = float(self.freqs[fi]) / C
-            _lib.call("pf_kernel3d", dev.ptr(g3), pz, py, px, self.vg.dx, self.vg.dy, self.dz3,
-                      khat, s)
-            dev.fftn_natural(g3, (pz, py, px), 1, -1, 1.0, stream)
-            _lib.call("pf_cmul", dev.ptr(uhat3), dev.ptr(g3), I * n3, n3, 1.0, s)
+        for f0 in range(0, F, gf):
+            f1 = min(F, f0 + gf)
+            ng = f1 - f0
+            self._lattice_spectra(coeff, f0, f1, uhat3g, n3, stream)
+            # the group's kernels, then every later step once for the whole group (one launch
+            # per pass over ng frequencies instead of ng small ones)
+            for j, fi in enumerate(range(f0, f1)):
+                _lib.call("pf_kernel3d", dev.ptr(g3g) + 8 * j * n3, pz, py, px, self.vg.dx,
+                          self.vg.dy, self.dz3, float(self.freqs[fi]) / C, s)
+            dev.fftn_natural(g3g, (pz, py, px), ng, -1, 1.0, stream)
+            if I == 1:
+                _lib.call("pf_cmul", dev.ptr(uhat3g), dev.ptr(g3g), ng * n3, ng * n3, 1.0, s)
+            else:
+                for j in range(ng):
+                    _lib.call("pf_cmul", dev.ptr(uhat3g) + 8 * j * I * n3, dev.ptr(g3g) + 8 * j * n3,
+                              I * n3, n3, 1.0, s)
             # cifft_n, then the slab plane: the z pass is evaluated at the slab only, then
             # the plane's y/x inverse transforms (the 3D inverse is never formed)
-            out_f = out[fi * I * py * px:(fi + 1) * I * py * px]
-            _lib.call("pf_zslab", dev.ptr(uhat3), I, pz, py * px, dev.ptr(self._zslab_w),
-                      1.0 / n3, dev.ptr(out_f), s)
-            dev.fft2_natural(out_f, py, px, I, +1, 1.0, stream)
+            out_g = out[f0 * I * py * px:f1 * I * py * px]
+            _lib.call("pf_zslab", dev.ptr(uhat3g), ng * I, pz, py * px, dev.ptr(self._zslab_w),
+                      1.0 / n3, dev.ptr(out_g), s)
+            dev.fft2_natural(out_g, py, px, ng * I, +1, 1.0, stream)
         return out
 
     def _lattice_spectra(self, coeff, f0, f1, uhat3g, n3, stream):
