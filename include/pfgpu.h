@@ -82,6 +82,13 @@ int pf_temporal_dft_direct(const float* hist, int64_t n_traces, int n_bins,
 int pf_fft_lines(void* data, const pf_fft_plan* plan, int64_t nlines, int64_t inner,
                  int64_t inner_stride, int64_t outer_stride, int64_t elem_stride, int dir,
                  float scale, void* stream);
+/* The same over a three-level line set: line l has inner index l % inner (stride
+ * inner_stride), middle index (l / inner) % mid (stride mid_stride) and outer index
+ * l / (inner mid) (stride outer_stride) -- e.g. the lines of a sub-block of the two other
+ * axes of every array of a batch in one launch (the NUFFT's pruned 3D transforms). */
+int pf_fft_lines3(void* data, const pf_fft_plan* plan, int64_t nlines, int64_t inner,
+                  int64_t inner_stride, int64_t mid, int64_t mid_stride, int64_t outer_stride,
+                  int64_t elem_stride, int dir, float scale, void* stream);
 
 /* Embed relay planes into zero-padded natural-order grids (the reference's
  * _pad_embed + ifftshift, reconstruct.py:113-119 with spectral.py:107-109).

@@ -215,11 +215,12 @@ def fftn_pruned(buf: torch.Tensor, shape: tuple[int, ...], nbatch: int, directio
         oa, ia = others
         for so, lo in runs[0]:
             for si, li in runs[1]:
-                fold = oa == 0 and lo == shape[0]   # a full leading axis runs into the next batch
-                for b in ([0] if fold else range(nbatch)):
-                    nl = (nbatch if fold else 1) * lo * li
-                    run(b * total + so * strides[oa] + si * strides[ia], n, nl, li, strides[ia],
-                        strides[oa], strides[ax])
+                # the block's lines of every array of the batch in one launch: inner run on
+                # axis ia, middle run on axis oa, outer level = the batch
+                if lo > 0 and li > 0:
+                    _lib.call("pf_fft_lines3", base + 8 * (so * strides[oa] + si * strides[ia]),
+                              fft_plan(n, buf.device).ref, nbatch * lo * li, li, strides[ia], lo,
+                              strides[oa], total, strides[ax], direction, 1.0, stream_ptr(stream))
 
 
 def c64(t: torch.Tensor) -> torch.Tensor:

@@ -105,6 +105,7 @@ _SIGNATURES = {
     "pf_temporal_dft": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, ctypes.c_uint64, _vp],
     "pf_temporal_dft_direct": [_vp, _i64, _i, _vp, _vp, _vp, _i, _vp, _i64, _vp],
     "pf_fft_lines": [_vp, _P(PfFftPlan), _i64, _i64, _i64, _i64, _i64, _i, _f, _vp],
+    "pf_fft_lines3": [_vp, _P(PfFftPlan), _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i, _f, _vp],
     "pf_embed_centered": [_vp, _i64, _i, _i, _i64, _vp, _i, _i, _i, _vp],
     "pf_prop_fast": [_P(PfPropGeom)],
     "pf_rsd_workspace_bytes": [_P(PfRsdArgs)],

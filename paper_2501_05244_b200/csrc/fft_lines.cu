@@ -15,15 +15,22 @@ namespace {
 constexpr int FL_THREADS = 256;
 constexpr size_t FL_SMEM_BUDGET = 200 * 1024;
 
-__device__ __forceinline__ long long line_base(long long l, long long inner, long long istr,
-                                               long long ostr) {
-  return (l / inner) * ostr + (l % inner) * istr;
+// line l of a three-level set: inner index l % inner (stride istr), middle index
+// (l / inner) % mid (stride mstr), outer index l / (inner mid) (stride ostr).  The two-level
+// sets of pf_fft_lines pass mid = LLONG_MAX (no outer level).
+struct LineSet {
+  long long inner, istr, mid, mstr, ostr;
+};
+__device__ __forceinline__ long long line_base(long long l, const LineSet& s) {
+  const long long q = l / s.inner;
+  const long long o = q / s.mid;
+  return o * s.ostr + (q - o * s.mid) * s.mstr + (l - q * s.inner) * s.istr;
 }
 
 template <int DIR>
 __global__ void __launch_bounds__(FL_THREADS)
-k_fft_lines(float2* __restrict__ data, pf_fft_plan plan, long long nlines, long long inner,
-            long long istr, long long ostr, long long estr, int cnt, float scale) {
+k_fft_lines(float2* __restrict__ data, pf_fft_plan plan, long long nlines, LineSet ls,
+            long long estr, int cnt, float scale) {
   extern __shared__ float2 sm[];
   __shared__ long long lbase[64];
   const int n = plan.n;
@@ -35,7 +42,7 @@ k_fft_lines(float2* __restrict__ data, pf_fft_plan plan, long long nlines, long 
   const int tot = nl * n;
   const bool rows = (estr == 1);
   // per-line base offsets once (64-bit div/mod), element index split by a fast divide
-  for (int c = threadIdx.x; c < nl; c += FL_THREADS) lbase[c] = line_base(l0 + c, inner, istr, ostr);
+  for (int c = threadIdx.x; c < nl; c += FL_THREADS) lbase[c] = line_base(l0 + c, ls);
   __syncthreads();
   const FastDiv split(rows ? n : nl);
   for (int e = threadIdx.x; e < tot; e += FL_THREADS) {
@@ -61,7 +68,7 @@ k_fft_lines(float2* __restrict__ data, pf_fft_plan plan, long long nlines, long 
 template <int L, int DIR>
 __global__ void __launch_bounds__(FL_THREADS, 2)
 k_xfft_lines(float2* __restrict__ data, const float2* __restrict__ tw2, long long nlines,
-             long long inner, long long istr, long long ostr, long long estr, float scale) {
+             LineSet ls, long long estr, float scale) {
   constexpr int N = XFFT_R * L, LD = N + ((N % 16) == 0 ? 1 : 0), LPW = 32 / L;
   constexpr int CNT = 8 * LPW, J = xfft_J(L);
   extern __shared__ float2 sm[];
@@ -70,7 +77,7 @@ k_xfft_lines(float2* __restrict__ data, const float2* __restrict__ tw2, long lon
   const int nl = (int)(nlines - l0 < CNT ? nlines - l0 : CNT);
   const int tot = nl * N;
   const bool rows = (estr == 1);
-  for (int c = threadIdx.x; c < nl; c += FL_THREADS) lbase[c] = line_base(l0 + c, inner, istr, ostr);
+  for (int c = threadIdx.x; c < nl; c += FL_THREADS) lbase[c] = line_base(l0 + c, ls);
   __syncthreads();
   const FastDiv split(rows ? N : nl);
   for (int e = threadIdx.x; e < tot; e += FL_THREADS) {
@@ -109,8 +116,8 @@ k_xfft_lines(float2* __restrict__ data, const float2* __restrict__ tw2, long lon
 }
 
 template <int L, int DIR>
-int launch_xlines(float2* data, const pf_fft_plan& p, long long nlines, long long inner,
-                  long long istr, long long ostr, long long estr, float scale, cudaStream_t st) {
+int launch_xlines(float2* data, const pf_fft_plan& p, long long nlines, const LineSet& ls,
+                  long long estr, float scale, cudaStream_t st) {
   constexpr int N = XFFT_R * L, LD = N + ((N % 16) == 0 ? 1 : 0), CNT = 8 * (32 / L);
   const size_t smem = (size_t)CNT * LD * sizeof(float2);
   static PfDevOnce attr;
@@ -119,23 +126,23 @@ int launch_xlines(float2* data, const pf_fft_plan& p, long long nlines, long lon
                          (int)smem);
   const long long grid = (nlines + CNT - 1) / CNT;
   const float2* tw2 = reinterpret_cast<const float2*>(p.tw) + N;   // after the n unit roots
-  k_xfft_lines<L, DIR><<<(unsigned)grid, FL_THREADS, smem, st>>>(data, tw2, nlines, inner, istr,
-                                                                  ostr, estr, scale);
+  k_xfft_lines<L, DIR><<<(unsigned)grid, FL_THREADS, smem, st>>>(data, tw2, nlines, ls, estr,
+                                                                  scale);
   PF_LAUNCH_CHECK("k_xfft_lines");
   return 0;
 }
 
 template <int DIR>
-int launch_xfft(float2* data, const pf_fft_plan& p, long long nlines, long long inner,
-                long long istr, long long ostr, long long estr, float scale, cudaStream_t st) {
+int launch_xfft(float2* data, const pf_fft_plan& p, long long nlines, const LineSet& ls,
+                long long estr, float scale, cudaStream_t st) {
   switch (xfft_L(p.n)) {
-    case 4: return launch_xlines<4, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
-    case 5: return launch_xlines<5, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
-    case 8: return launch_xlines<8, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
-    case 10: return launch_xlines<10, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
-    case 15: return launch_xlines<15, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
-    case 20: return launch_xlines<20, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
-    case 30: return launch_xlines<30, DIR>(data, p, nlines, inner, istr, ostr, estr, scale, st);
+    case 4: return launch_xlines<4, DIR>(data, p, nlines, ls, estr, scale, st);
+    case 5: return launch_xlines<5, DIR>(data, p, nlines, ls, estr, scale, st);
+    case 8: return launch_xlines<8, DIR>(data, p, nlines, ls, estr, scale, st);
+    case 10: return launch_xlines<10, DIR>(data, p, nlines, ls, estr, scale, st);
+    case 15: return launch_xlines<15, DIR>(data, p, nlines, ls, estr, scale, st);
+    case 20: return launch_xlines<20, DIR>(data, p, nlines, ls, estr, scale, st);
+    case 30: return launch_xlines<30, DIR>(data, p, nlines, ls, estr, scale, st);
     default: return 1;
   }
 }
@@ -160,8 +167,8 @@ __global__ void k_embed_centered(const float2* __restrict__ src, long long nb, i
 }
 
 template <int DIR>
-int launch_lines(float2* data, const pf_fft_plan& p, long long nlines, long long inner,
-                 long long istr, long long ostr, long long estr, float scale, cudaStream_t st) {
+int launch_lines(float2* data, const pf_fft_plan& p, long long nlines, const LineSet& ls,
+                 long long estr, float scale, cudaStream_t st) {
   static PfDevOnce attr;  
   if (attr.first()) {
     cudaFuncSetAttribute(k_fft_lines<DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -194,35 +201,44 @@ int launch_lines(float2* data, const pf_fft_plan& p, long long nlines, long long
   if (cnt > 64) cnt = 64;
   if (cnt > nlines) cnt = (int)nlines;
   const int grid = (int)((nlines + cnt - 1) / cnt);
-  k_fft_lines<DIR><<<grid, FL_THREADS, cnt * per_line, st>>>(data, p, nlines, inner, istr, ostr,
-                                                             estr, cnt, scale);
+  k_fft_lines<DIR><<<grid, FL_THREADS, cnt * per_line, st>>>(data, p, nlines, ls, estr, cnt,
+                                                             scale);
   PF_LAUNCH_CHECK("k_fft_lines");
   return 0;
 }
 
 }  // namespace
 
-extern "C" int pf_fft_lines(void* data, const pf_fft_plan* plan, int64_t nlines, int64_t inner,
-                            int64_t inner_stride, int64_t outer_stride, int64_t elem_stride,
-                            int dir, float scale, void* stream) {
+static int fft_lines_run(void* data, const pf_fft_plan* plan, int64_t nlines, const LineSet& ls,
+                         int64_t elem_stride, int dir, float scale, void* stream) {
   PF_ARG_CHECK(plan != nullptr && plan->n >= 1 && plan->nst <= PF_MAX_STAGES,
                "pf_fft_lines: bad plan");
-  PF_ARG_CHECK(inner >= 1 && nlines >= 0, "pf_fft_lines: bad line layout");
+  PF_ARG_CHECK(ls.inner >= 1 && ls.mid >= 1 && nlines >= 0, "pf_fft_lines: bad line layout");
   if (nlines == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   // 35 L lengths: the register mixed-radix kernel (the plan carries its twiddle table)
   // (the plan builder decides: it tags a plan only where the register FFT is wanted)
   if (plan_xl(*plan)) {
-    return dir < 0 ? launch_xfft<-1>((float2*)data, *plan, nlines, inner, inner_stride,
-                                     outer_stride, elem_stride, scale, st)
-                   : launch_xfft<1>((float2*)data, *plan, nlines, inner, inner_stride,
-                                    outer_stride, elem_stride, scale, st);
+    return dir < 0 ? launch_xfft<-1>((float2*)data, *plan, nlines, ls, elem_stride, scale, st)
+                   : launch_xfft<1>((float2*)data, *plan, nlines, ls, elem_stride, scale, st);
   }
-  if (dir < 0)
-    return launch_lines<-1>((float2*)data, *plan, nlines, inner, inner_stride, outer_stride,
-                            elem_stride, scale, st);
-  return launch_lines<1>((float2*)data, *plan, nlines, inner, inner_stride, outer_stride,
-                         elem_stride, scale, st);
+  if (dir < 0) return launch_lines<-1>((float2*)data, *plan, nlines, ls, elem_stride, scale, st);
+  return launch_lines<1>((float2*)data, *plan, nlines, ls, elem_stride, scale, st);
+}
+
+extern "C" int pf_fft_lines(void* data, const pf_fft_plan* plan, int64_t nlines, int64_t inner,
+                            int64_t inner_stride, int64_t outer_stride, int64_t elem_stride,
+                            int dir, float scale, void* stream) {
+  const LineSet ls{inner, inner_stride, LLONG_MAX, outer_stride, 0};
+  return fft_lines_run(data, plan, nlines, ls, elem_stride, dir, scale, stream);
+}
+
+extern "C" int pf_fft_lines3(void* data, const pf_fft_plan* plan, int64_t nlines, int64_t inner,
+                             int64_t inner_stride, int64_t mid, int64_t mid_stride,
+                             int64_t outer_stride, int64_t elem_stride, int dir, float scale,
+                             void* stream) {
+  const LineSet ls{inner, inner_stride, mid, mid_stride, outer_stride};
+  return fft_lines_run(data, plan, nlines, ls, elem_stride, dir, scale, stream);
 }
 
 extern "C" int pf_embed_centered(const void* src, int64_t nb, int ny, int nx,

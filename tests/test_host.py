@@ -135,12 +135,18 @@ def test_fftn_pruned_line_sets(monkeypatch, shape, modes, nb):
     flat = t.view(-1).numpy()
     base = t.data_ptr()
 
-    def fake(name, p, planref, nl, inner, istr, ostr, estr, direction, scale, stream):
-        assert name == "pf_fft_lines"
+    def fake(name, p, planref, nl, inner, istr, *rest):
+        if name == "pf_fft_lines":
+            mid, mstr, (ostr, estr, direction, scale, stream) = 1 << 62, rest[0], (0,) + rest[1:]
+        else:
+            assert name == "pf_fft_lines3"
+            mid, mstr, ostr, estr, direction, scale, stream = rest
         n = planref._obj.n
         off = (p - base) // 8
         for ln in range(nl):
-            idx = off + (ln // inner) * ostr + (ln % inner) * istr + np.arange(n) * estr
+            q = ln // inner
+            idx = (off + (q // mid) * ostr + (q % mid) * mstr + (ln % inner) * istr
+                   + np.arange(n) * estr)
             v = flat[idx].astype(np.complex128)
             flat[idx] = np.fft.fft(v) if direction < 0 else np.fft.ifft(v) * n
         return 0
@@ -187,12 +193,18 @@ def test_fftn_pruned_skips_zero_lines(monkeypatch, shape, modes, nz, nb):
     base = t.data_ptr()
     lines = [0]
 
-    def fake(name, p, planref, nl, inner, istr, ostr, estr, direction, scale, stream):
+    def fake(name, p, planref, nl, inner, istr, *rest):
+        if name == "pf_fft_lines":
+            mid, mstr, ostr, estr = 1 << 62, rest[0], 0, rest[1]
+        else:
+            mid, mstr, ostr, estr = rest[:4]
         n = planref._obj.n
         off = (p - base) // 8
         lines[0] += nl
         for ln in range(nl):
-            i = off + (ln // inner) * ostr + (ln % inner) * istr + np.arange(n) * estr
+            q = ln // inner
+            i = (off + (q // mid) * ostr + (q % mid) * mstr + (ln % inner) * istr
+                 + np.arange(n) * estr)
             flat[i] = np.fft.fft(flat[i].astype(np.complex128))
         return 0
 
