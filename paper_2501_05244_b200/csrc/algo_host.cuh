@@ -81,7 +81,10 @@ inline std::vector<float2> twiddles(long n) {
   const char* ev = getenv("PF_XFFT");
   long xl = xfft_L((int)n);
   if (ev && strcmp(ev, "0") == 0) xl = 0;
-  if (!(ev && strcmp(ev, "all") == 0) && xl < 20) xl = 0;
+  long lmin = 20;   // _device.xfft_plan_L: "all", an integer minimum, or "large" (20)
+  if (ev && strcmp(ev, "all") == 0) lmin = 1;
+  else if (ev && ev[0] >= '1' && ev[0] <= '9') lmin = atol(ev);
+  if (xl < lmin) xl = 0;
   if (xl) {   // mixed-radix register FFT: k1-major [35][L]
     for (long k1 = 0; k1 < 35; k1++)
       for (long t = 0; t < xl; t++) {
