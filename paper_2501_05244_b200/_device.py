@@ -66,7 +66,7 @@ def xfft_L(n: int) -> int:
 
 def xfft_plan_L(n: int) -> int:
     """Lanes of the register FFT a plan of length n is tagged for (0: Stockham stages).
-    PF_XFFT = "large" (default): only L >= 20 (n = 700, 1050), where it measured faster
+    PF_XFFT = "large" (default): only L >= 10 (n = 350, 525, 700, 1050), where it measured faster
     (config 2's 700-point fine-grid lines); "all": every 35 L length (slower at 140 and 280:
     the generic propagation kernels drop to one CTA per SM); an integer: L at least that;
     "0": never."""
@@ -74,7 +74,7 @@ def xfft_plan_L(n: int) -> int:
     L = xfft_L(n)
     if mode == "0":
         return 0
-    lmin = 1 if mode == "all" else (int(mode) if mode.isdigit() else 20)
+    lmin = 1 if mode == "all" else (int(mode) if mode.isdigit() else 10)
     return L if L >= lmin else 0
 
 

@@ -77,11 +77,11 @@ inline std::vector<float2> twiddles(long n) {
     const double a = -2.0 * M_PI * (double)m / (double)n;
     w.push_back(make_float2((float)cos(a), (float)sin(a)));
   }
-  // register FFT tables as the Python plans (_device.xfft_plan_L): L >= 20 by default
+  // register FFT tables as the Python plans (_device.xfft_plan_L): L >= 10 by default
   const char* ev = getenv("PF_XFFT");
   long xl = xfft_L((int)n);
   if (ev && strcmp(ev, "0") == 0) xl = 0;
-  long lmin = 20;   // _device.xfft_plan_L: "all", an integer minimum, or "large" (20)
+  long lmin = 10;   // _device.xfft_plan_L: "all", an integer minimum, or "large" (10)
   if (ev && strcmp(ev, "all") == 0) lmin = 1;
   else if (ev && ev[0] >= '1' && ev[0] <= '9') lmin = atol(ev);
   if (xl < lmin) xl = 0;
