@@ -698,6 +698,23 @@ def _ref_unit(unit):
     return max(a - per_k, 0.0), per_k
 
 
+def _ref_task(task):
+    """Worker of the reference arm: one task of a step's bounded sub-workload, either
+    ("s3", f, k0, k1): the reference algorithm's term of frequency f on planes [k0, k1), or
+    ("s1", n): to_frequency on n traces.  Returns the seconds it took."""
+    from oracle import pf_oracle as O
+    t = time.perf_counter()
+    if task[0] == "s3":
+        _, f, k0, k1 = task
+        fn = {"rsd": O.rsd, "srsd": O.srsd, "nursd1": O.nursd1}[_REF_STATE["alg"]]
+        fn(_REF_STATE["slices"], _REF_STATE["grid"], freq_range=(f, f + 1), plane_range=(k0, k1))
+    else:
+        k = _REF_STATE["kernel"]
+        O.to_frequency(_REF_STATE["hist"][:task[1]], k.bin_indices, k.frequencies, k.weights,
+                       _REF_STATE["t0"])
+    return time.perf_counter() - t
+
+
 def run_reference(args):
     world, rank, _ = _dist_env()
     if rank != 0:
@@ -720,39 +737,53 @@ def run_reference(args):
     ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     if cfg.algorithm == "nursd3d-explicit":
         return _run_reference_explicit(args, cfg, kernel, sl, ncores, world)
-    n_tr = 2048
-    h = rng.poisson(2.0, size=(n_tr, cfg.n_bins)).astype(np.float64)
-    units = [(i % F, (3 * i) % max(1, nz - 3)) for i in range(ncores)]
-    _REF_STATE["slices"], _REF_STATE["grid"], _REF_STATE["alg"] = sl, cfg.grid, cfg.algorithm
+    # A step = the reference algorithm's complete work for a bounded part of the capture: n_s
+    # of the nz depth planes with every frequency term (tasks of one frequency x a block of
+    # planes, shared by all host cores) and to_frequency on the same fraction n_s / nz of the
+    # traces.  value = the voxels of those planes / the step's measured wall time: measured,
+    # not extrapolated.  n_s is sized from one calibration task so a step takes a few seconds.
+    _REF_STATE.update(slices=sl, grid=cfg.grid, alg=cfg.algorithm, kernel=kernel, t0=cfg.t0)
+    t = time.perf_counter()
+    _ref_task(("s3", 0, 0, 1))
+    t_one = time.perf_counter() - t          # one frequency x one plane (incl. its relay spectrum)
+    target_s = float(os.environ.get("PF_REF_STEP_SECONDS", "5"))
+    n_s = int(max(1, min(nz, target_s * ncores / max(F * 0.6 * t_one, 1e-9))))
+    pb = max(1, min(8, n_s))                 # planes per task: the per-frequency cost over >= pb planes
+    n_s = max(pb, n_s // pb * pb)
+    n_s = min(n_s, nz // pb * pb) if nz >= pb else nz
+    blocks = [(k0, min(n_s, k0 + pb)) for k0 in range(0, n_s, pb)]
+    n_tr = max(ncores, int(round(D * n_s / nz)))
+    per = -(-n_tr // ncores)
+    _REF_STATE["hist"] = rng.poisson(2.0, size=(per, cfg.n_bins)).astype(np.float64)
+    tasks = [("s3", f, k0, k1) for (k0, k1) in blocks for f in range(F)]
+    tasks += [("s1", min(per, n_tr - i * per)) for i in range(ncores) if n_tr - i * per > 0]
+    plane_vox = cfg.n_voxels // nz
     ctx = mp.get_context("fork")
     times = []
     with ctx.Pool(ncores) as pool:
         for it in range(args.warmup + args.steps):
             t = time.perf_counter()
-            res = pool.map(_ref_unit, units)
-            t_par = time.perf_counter() - t
-            per_f = statistics.mean(r[0] for r in res)
-            per_k = statistics.mean(r[1] for r in res)
-            # ncores processes share the F x Nz units; each step's sample is 4 planes per process
-            serial = F * (per_f + nz * per_k)
-            t = time.perf_counter()
-            O.to_frequency(h, kernel.bin_indices, kernel.frequencies, kernel.weights, cfg.t0)
-            t_s1 = (time.perf_counter() - t) * D / n_tr / ncores
+            list(pool.imap_unordered(_ref_task, tasks, chunksize=1))
+            dt = time.perf_counter() - t
             if it >= args.warmup:
-                times.append(serial / ncores + t_s1)
+                times.append(dt)
     est = statistics.mean(times)
-    value = cfg.n_voxels / est
+    value = n_s * plane_vox / est
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "c128 (float64)", "data": "synthetic (seeded random-phase slices, Poisson hist)",
         "config": {"workload": f"config{args.config}-{cfg.algorithm}", "voxels": cfg.n_voxels,
-                   "pad": "reference pad rule"},
+                   "pad": "reference pad rule",
+                   "step": f"{n_s} of {nz} planes x all {F} frequencies + to_frequency on "
+                           f"{n_tr} of {D} traces ({n_s * plane_vox} voxels per step)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
-                         "sample": f"per step: {len(units)} processes x (1 freq x 1+3 planes) of "
-                                   f"oracle.{cfg.algorithm} + to_frequency on {n_tr} traces, extrapolated to "
-                                   f"{F}x{nz} units and {D} traces"},
+                         "sample": f"per step, measured (not extrapolated): oracle.{cfg.algorithm} "
+                                   f"for {n_s} of {nz} planes, every frequency term ({len(blocks) * F} "
+                                   f"tasks of 1 frequency x {pb} planes over {ncores} processes; the "
+                                   f"cross-process sum of the terms is not formed) + to_frequency on "
+                                   f"{n_tr} of {D} traces; value = those planes' voxels / step time"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
