@@ -135,36 +135,51 @@ k_t2_rows_split(pf_nufft_geom G, const float2* __restrict__ S, long long s_strid
   const long long nlines = (long long)nv * my;
   const long long l0 = (long long)blockIdx.x * cnt;
   const int nl = (int)(nlines - l0 < cnt ? nlines - l0 : cnt);
+  // per line: source row of S, target row of the fine grid, 1 / ker_y (the 64-bit divisions
+  // once per line, not per element); per column: 1 / ker_x
+  __shared__ long long src_row[32], dst_row[32];
+  __shared__ float rky[32];
+  float* rkx = reinterpret_cast<float*>(tw2 + XFFT_R * HL);   // [mx]
+  for (int c = threadIdx.x; c < nl; c += NT) {
+    const long long l = l0 + c;
+    const int v = (int)(l / my), i = (int)(l - (long long)v * my);
+    const int cy = i - my / 2;
+    src_row[c] = (long long)v * s_stride + (long long)natural(cy, my) * mx;
+    dst_row[c] = (long long)v * fine_stride + (long long)(cy < 0 ? cy + mry : cy) * mrx;
+    rky[c] = 1.0f / ky[i];
+  }
+  for (int q = threadIdx.x; q < mx; q += NT) rkx[q] = 1.0f / kx[q];
+  __syncthreads();
   const FastDiv dmx(mx);
   for (int e = threadIdx.x; e < nl * mx; e += NT) {
     const int c = dmx.div(e), q = e - c * mx;
-    const long long l = l0 + c;
-    const int v = (int)(l / my), i = (int)(l - (long long)v * my);
-    const int cy = i - my / 2, cx = q - mx / 2;
-    const int jy = natural(cy, my), jx = natural(cx, mx);
-    const float den = 1.0f * ky[i] * kx[q];
-    const float2 s = S[(long long)v * s_stride + (long long)jy * mx + jx];
-    const float2 val = make_float2(s.x / den, s.y / den);
+    const int cx = q - mx / 2;
+    const int jx = cx < 0 ? cx + mx : cx;
+    const float inv = rky[c] * rkx[q];
+    const float2 sv = S[src_row[c] + jx];
+    const float2 val = make_float2(sv.x * inv, sv.y * inv);
     a[(2 * c) * ld + jx] = val;
     a[(2 * c + 1) * ld + jx] = cmulc(val, __ldg(roots + (cx < 0 ? cx + mrx : cx)));
   }
   __syncthreads();
   xfft_tile<HL, 1, true>(a, ld, 2 * nl, tw2);
-  for (int e = threadIdx.x; e < nl * mx; e += NT) {
-    const int c = dmx.div(e), j = e - c * mx;
-    const long long l = l0 + c;
-    const int v = (int)(l / my), i = (int)(l - (long long)v * my);
-    const int cy = i - my / 2;
-    const int fy = cy < 0 ? cy + mry : cy;
-    // only the columns some readout stencil touches are stored (window [col0, col0 + ncols)
-    // on the torus): the column pass transforms no others
+  // only the columns some readout stencil touches are stored (window [col0, col0 + ncols) on
+  // the torus; the column pass transforms no others): output pairs (2 j, 2 j + 1) from
+  // j = col0 / 2 on, around the seam
+  const int j0 = col0 >> 1;
+  const int npairs = min(mx, ((col0 + ncols - 1) >> 1) - j0 + 1);
+  const FastDiv dnp(npairs);
+  for (int e = threadIdx.x; e < nl * npairs; e += NT) {
+    const int c = dnp.div(e);
+    int j = j0 + (e - c * npairs);
+    j -= j >= mx ? mx : 0;
     int d0 = 2 * j - col0, d1 = 2 * j + 1 - col0;
     d0 += d0 < 0 ? mrx : 0;
     d1 += d1 < 0 ? mrx : 0;
     const bool in0 = d0 < ncols, in1 = d1 < ncols;
     if (!in0 && !in1) continue;
     const float2 ev = a[(2 * c) * ld + j], od = a[(2 * c + 1) * ld + j];
-    float2* dst = fine + (long long)v * fine_stride + (long long)fy * mrx + 2 * j;
+    float2* dst = fine + dst_row[c] + 2 * j;
     if (in0 && in1) {
       *reinterpret_cast<float4*>(dst) = make_float4(ev.x, ev.y, od.x, od.y);
     } else if (in0) {
@@ -276,8 +291,8 @@ int t2_split_cnt(int nt, int hl) {
   int cnt = (nt / 32) * (32 / hl) / 2;
   return cnt < 1 ? 1 : (cnt > 32 ? 32 : cnt);
 }
-size_t t2_split_smem(int m, int hl, int cnt) {
-  return ((size_t)2 * cnt * pf_ld(m) + (size_t)XFFT_R * hl) * sizeof(float2);
+size_t t2_split_smem(int m, int hl, int cnt) {   // lines + half-length twiddles + 1 / ker (m floats)
+  return ((size_t)2 * cnt * pf_ld(m) + (size_t)XFFT_R * hl + (size_t)(m + 1) / 2) * sizeof(float2);
 }
 template <int HL, typename... A>
 void t2_launch_rows_split(int nt, unsigned grid, size_t smem, cudaStream_t st, A... args) {
