@@ -20,6 +20,8 @@
 //   uhat  [.. per plane offset ..][n_illum][py][px]
 //   ws_b  [nplanes][n_illum][ny][px]    column pass output (rows already cropped)
 //   vol   [n_frames][.. plane k at k*ny*nx ..]
+#include <stdlib.h>
+
 #include "fft.cuh"
 
 namespace {
@@ -402,7 +404,16 @@ extern "C" int pf_prop_columns(const pf_plane* planes, int nplanes, const pf_pro
   static PfDevOnce attr;
   if (attr.first()) allow_all_generic();
   const int cols_a = g->px / 2 + 1;
-  const int xl = plan_xl(*plan_y);
+  int xl = plan_xl(*plan_y);
+  // product-only columns (one forward transform and two products per column) measured
+  // faster on the Stockham stages than on the 10-lane register FFT (P = 350: 58.9 vs 73.4 us
+  // per launch at config 7); PF_PROP_COLS_XL=1 keeps the register FFT there
+  static int cols_xl = -1;
+  if (cols_xl < 0) {
+    const char* e = getenv("PF_PROP_COLS_XL");
+    cols_xl = (e && atoi(e) != 0) ? 1 : 0;
+  }
+  if (product_only && xl > 0 && xl <= 10 && !cols_xl) xl = 0;
   int cpc = lines_for(g->py, 3, 8, xl);
   if (cpc < 1) { pf_set_error("pf_prop_columns: py too large"); return -1; }
   dim3 grid(pf_cdiv(cols_a, cpc), nplanes);
