@@ -339,6 +339,15 @@ int pf_nufft_type2_start_2d_win(const pf_nufft_geom* g, const void* S, int64_t s
                                 int64_t fine_stride, const pf_fft_plan* plan_x,
                                 const pf_fft_plan* plan_y, int col0, int ncols, int row0,
                                 int nrows, void* stream);
+/* The same with the column pass writing to `out` with every il consecutive grids interleaved
+ * cell by cell: out[(v / il) * (fine_stride * il) + cell * il + v % il] (il = 1, out = fine:
+ * pf_nufft_type2_start_2d_win).  Needs the split column pass (pf_nufft_type2_il_ok). */
+int pf_nufft_type2_start_2d_il(const pf_nufft_geom* g, const void* S, int64_t s_stride,
+                               const float* ky, const float* kx, int nv, void* fine,
+                               int64_t fine_stride, const pf_fft_plan* plan_x,
+                               const pf_fft_plan* plan_y, int col0, int ncols, int row0,
+                               int nrows, void* out, int il, void* stream);
+int pf_nufft_type2_il_ok(const pf_nufft_geom* g);
 /* type-2 start (spectral.py:374): modes / deconvolution onto their fine slots, 0 elsewhere. */
 int pf_nufft_place(const pf_nufft_geom* g, const void* S, int64_t s_stride, const float* kz,
                    const float* ky, const float* kx, int nv, void* fine, int64_t fine_stride,
@@ -353,6 +362,16 @@ int pf_nufft_interp2_batch(const pf_nufft_geom* g, const int32_t* i0, const floa
                            int64_t fine_stride, int n_illum, const double* ill, double khat,
                            int include_illum, float scale, const void* frame_w, int n_frames,
                            void* vol, int64_t vol_frame_stride, void* stream);
+/* pf_nufft_interp2_nodes on node-interleaved fine grids (pf_nufft_type2_start_2d_il with
+ * il = nodes): a tap's node values are contiguous, read with 16-byte loads.  ES window at
+ * w = 4, 12 nodes, one illumination. */
+int pf_nufft_interp2_nodes_il(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                              const double* xyz, const int32_t* plane_idx,
+                              const int64_t* dst_idx, int npts, int plane0, const void* fine_il,
+                              int64_t slab_stride, const double* ill, double khat,
+                              int include_illum, float scale, const void* frame_w, int n_frames,
+                              void* vol, int64_t vol_frame_stride, int nodes, const float* lw,
+                              void* stream);
 /* Readout kernel for the reference's default stencil (w = 8, 17 x 17 taps): 2 (default)
  * the 16 x 16 trimmed kernel (the far edge tap of each axis, <= 6.5e-9 of the centre
  * weight, is not loaded), 1 the full 17 x 17 kernel, 0 the general kernel; mode < 0 only

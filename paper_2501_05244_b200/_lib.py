@@ -150,6 +150,9 @@ _SIGNATURES = {
     "pf_nufft_deconv": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp],
     "pf_nufft_type2_start_2d": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _i, _vp, _i64, _P(PfFftPlan), _P(PfFftPlan), _vp],
     "pf_nufft_type2_start_2d_win": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _i, _vp, _i64, _P(PfFftPlan), _P(PfFftPlan), _i, _i, _i, _i, _vp],
+    "pf_nufft_type2_start_2d_il": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _i, _vp, _i64, _P(PfFftPlan), _P(PfFftPlan), _i, _i, _i, _i, _vp, _i, _vp],
+    "pf_nufft_type2_il_ok": [_P(PfNufftGeom)],
+    "pf_nufft_interp2_nodes_il": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _i64, _vp, _d, _i, _f, _vp, _i, _vp, _i64, _i, _vp, _vp],
     "pf_nufft_place": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp],
     "pf_nufft_interp2_acc": [_P(PfNufftGeom), _vp, _vp, _vp, _i, _vp, _i64, _i, _vp, _d, _i, _f,
                              _vp, _i, _vp, _i64, _i64, _vp, _vp],
@@ -173,7 +176,7 @@ _RESTYPES = {"pf_launch_count": ctypes.c_int64, "pf_prop_ws_a": ctypes.c_int64, 
              "pf_srsd_workspace_bytes": ctypes.c_int64, "pf_nursd1_workspace_bytes": ctypes.c_int64,
              "pf_nursd2_workspace_bytes": ctypes.c_int64,
              "pf_prop_fast": ctypes.c_int, "pf_prop_onchip_ok": ctypes.c_int,
-             "pf_nufft_interp_mode": ctypes.c_int, "pf_nufft_window": ctypes.c_int}
+             "pf_nufft_interp_mode": ctypes.c_int, "pf_nufft_window": ctypes.c_int, "pf_nufft_type2_il_ok": ctypes.c_int}
 
 _lib = None
 

@@ -421,6 +421,7 @@ class _Type2Readout:
 # ---------------------------------------------------------------------------
 
 _T2_WINDOW = os.environ.get("PF_T2_WINDOW", "1") != "0"   # type-2 start limited to the stencils' cells
+_ZCHEB_IL = os.environ.get("PF_ZCHEB_IL", "1") != "0"      # node-interleaved fine grids in the readout
 _ZCHEB_NODES = int(os.environ.get("PF_ZCHEB_NODES", "12"))
 _ZCHEB_KAPPA = float(os.environ.get("PF_ZCHEB_KAPPA", "6.0"))   # k_max x slab thickness
 
@@ -525,6 +526,13 @@ class _ZChebReadout:
                                 device=device)
         self.ill = _ill_tensor(slices, device)
         self.frame_w = _frame_weights(self.freqs, times, device)
+        # node-interleaved fine grids (a tap's node values contiguous: wide loads in the
+        # readout): ES window at w = 4, 12 nodes, one illumination, split column pass
+        self.interleaved = bool(
+            _ZCHEB_IL and self.plan.window == "es" and self.plan.w == 4 and M == 12 and I == 1
+            and self.plan.fine_elems * M < (1 << 31)
+            and _lib.call("pf_nufft_type2_il_ok", self.plan.gref))
+        self.fine_il = torch.empty_like(self.fine) if self.interleaved else None
 
     def run(self, uhat_of, vol, stream=None):
         s = dev.stream_ptr(stream)
@@ -544,9 +552,26 @@ class _ZChebReadout:
                           dev.ptr(self.prop.ws_a), s)
                 _lib.call("pf_prop_columns", pp, n, gref, self.prop.plan_y.ref,
                           dev.ptr(self.prop.ws_a), dev.ptr(uhat), dev.ptr(self.spec), 1, s)
+                lo, hi = self.pt_lo[s0], self.pt_lo[s1]
+                if self.interleaved:
+                    p = self.plan
+                    c0, nc, r0, nr = self.window or (0, p.mrs[2], 0, p.mrs[1])
+                    _lib.call("pf_nufft_type2_start_2d_il", p.gref, dev.ptr(self.spec), py * px,
+                              dev.ptr(p.kers[1]), dev.ptr(p.kers[2]), n, dev.ptr(self.fine), fe,
+                              dev.fft_plan(p.mrs[2], p.device).ref,
+                              dev.fft_plan(p.mrs[1], p.device).ref, c0, nc, r0, nr,
+                              dev.ptr(self.fine_il), M, s)
+                    if hi > lo:
+                        _lib.call("pf_nufft_interp2_nodes_il", p.gref,
+                                  dev.ptr(self.i0_all) + 12 * lo, dev.ptr(self.d0_all) + 12 * lo,
+                                  dev.ptr(self.xyz_all) + 24 * lo, dev.ptr(self.plane_all) + 4 * lo,
+                                  dev.ptr(self.dst_all) + 8 * lo, hi - lo, b0,
+                                  dev.ptr(self.fine_il), fe * M, dev.ptr(self.ill), khat,
+                                  int(self.include), 1.0 / (px * py), fw, self.n_frames,
+                                  dev.ptr(vol), self.count, M, dev.ptr(self.lw_all) + 4 * M * lo, s)
+                    continue
                 nu.place_and_inverse(self.plan, self.spec, n * I, py * px, self.fine, stream,
                                      self.window)
-                lo, hi = self.pt_lo[s0], self.pt_lo[s1]
                 if hi == lo:
                     continue
                 _lib.call("pf_nufft_interp2_nodes", self.plan.gref,

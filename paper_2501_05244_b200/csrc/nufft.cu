@@ -676,6 +676,133 @@ k_interp2_es8(pf_nufft_geom G, const int* __restrict__ i0, const float* __restri
   }
 }
 
+// The node-gathering readout (arbitrary voxel depths) on node-interleaved fine grids: the M
+// node grids of a depth slab are stored cell by cell (fine_il[slab][cell][node], written by
+// pf_nufft_type2_start_2d_il), so a tap's M node values are 8 M contiguous bytes and a lane
+// reads them with 16-byte loads -- every sector fetched is fully used, where the per-grid
+// layout fetches a 64-byte row segment (2-3 partly used sectors) per node and row.  Quarter
+// warp per voxel as k_interp2_es8 (w = 4, one illumination); the Lagrange-weighted node sum
+// of a tap is formed first, then weighted by the stencil.
+template <int M>
+__global__ void __launch_bounds__(256, 4)
+k_interp2_es8_il(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
+                 const double* __restrict__ xyz, const int* __restrict__ plane_idx,
+                 const long long* __restrict__ dst_idx, int npts, int plane0,
+                 const float2* __restrict__ fine_il, long long slab_stride,
+                 const double* __restrict__ ill, double kturns, int include_illum, float scale,
+                 const float2* __restrict__ frame_w, int n_frames, float2* __restrict__ vol,
+                 long long vol_frame_stride, const float* __restrict__ lw) {
+  static_assert(M % 2 == 0, "node pairs are read as float4");
+  constexpr int w = 4;
+  const int lane = threadIdx.x & 31, ql = lane & 7, grp = lane >> 3;
+  const int l = blockIdx.x * (blockDim.x >> 3) + ((threadIdx.x >> 5) << 2) + grp;
+  const bool live = l < npts;
+  const int lc = live ? l : 0;
+  const int mry = G.mr[1], mrx = G.mr[2], fe = mry * mrx;
+  const float dyl = d0[3 * lc + 1], dxl = d0[3 * lc + 2];
+  const int sx = dxl > 0.f ? 0 : 1, sy = dyl > 0.f ? 0 : 1;
+  const float wx = pf_win(G, 2, dxl + (float)(ql - w + sx) * G.h[2]) * scale;
+  const float wy_own = pf_win(G, 1, dyl + (float)(ql - w + sy) * G.h[1]);
+  const int cx = wrap_once(wrap_once(i0[3 * lc + 2] - w + sx, mrx) + ql, mrx);
+  const int r0 = wrap_once(i0[3 * lc + 1] - w + sy, mry) * mrx;
+  const float2* base = fine_il + (long long)((plane_idx[lc] - plane0) / M) * slab_stride;
+  const bool tail = ql == 0 && live;
+  double px = 0.0, py = 0.0, pz = 0.0;
+  long long dst = 0;
+  float2 old = make_float2(0.f, 0.f);
+  if (tail) {
+    dst = dst_idx[l];
+    if (include_illum) {
+      px = xyz[3 * lc];
+      py = xyz[3 * lc + 1];
+      pz = xyz[3 * lc + 2];
+    }
+    old = vol[dst];
+  }
+  // A row of the stencil is 8 columns x M nodes = 8 M contiguous float2.  The quarter warp
+  // reads it as NP 128-byte pieces (lane ql takes the 16 bytes at 128 q + 16 ql: one cache
+  // line per piece and voxel instead of eight), so lane ql's piece q holds node pair
+  // (8 q + ql) % (M / 2) of column (8 q + ql) / (M / 2); its weights are fetched once.
+  constexpr int NP = M / 2;                  // 16-byte pieces per lane and row (8 M / 2 / 8)
+  float wq[NP];
+  float2 lq[NP];
+#pragma unroll
+  for (int q = 0; q < NP; q++) {
+    const int t = 8 * q + ql;
+    const int colq = t / NP, pair = t - colq * NP;
+    wq[q] = __shfl_sync(0xffffffffu, wx, (grp << 3) + colq);
+    lq[q] = __ldg(reinterpret_cast<const float2*>(lw + (long long)lc * M) + pair);
+  }
+  // the row's first byte: column 0 of the stencil (the columns wrap with the torus: a row
+  // whose 8 columns straddle the seam falls back to per-column addresses)
+  const int cx0 = wrap_once(i0[3 * lc + 2] - w + sx, mrx);
+  const bool straddle = cx0 + 8 > mrx;
+  float2 acc = make_float2(0.f, 0.f);
+  int ro = r0;
+  if (!straddle) {
+#pragma unroll 2
+    for (int oy = 0; oy < 8; oy++) {
+      const float wy = __shfl_sync(0xffffffffu, wy_own, (grp << 3) + oy);
+      const float4* p4 = reinterpret_cast<const float4*>(base + (long long)(ro + cx0) * M) + ql;
+      float4 v[NP];
+#pragma unroll
+      for (int q = 0; q < NP; q++) v[q] = __ldg(p4 + 8 * q);
+      float sxr = 0.f, syr = 0.f;
+#pragma unroll
+      for (int q = 0; q < NP; q++) {
+        const float a0 = wq[q] * lq[q].x, a1 = wq[q] * lq[q].y;
+        sxr = fmaf(a0, v[q].x, sxr);
+        syr = fmaf(a0, v[q].y, syr);
+        sxr = fmaf(a1, v[q].z, sxr);
+        syr = fmaf(a1, v[q].w, syr);
+      }
+      acc.x = fmaf(wy, sxr, acc.x);
+      acc.y = fmaf(wy, syr, acc.y);
+      ro += mrx;
+      if (ro >= fe) ro -= fe;
+    }
+  } else {
+    for (int oy = 0; oy < 8; oy++) {
+      const float wy = __shfl_sync(0xffffffffu, wy_own, (grp << 3) + oy);
+      float sxr = 0.f, syr = 0.f;
+#pragma unroll
+      for (int q = 0; q < NP; q++) {
+        const int t = 8 * q + ql;
+        const int colq = t / NP, pair = t - colq * NP;
+        const int cxq = wrap_once(cx0 + colq, mrx);
+        const float4 v =
+            __ldg(reinterpret_cast<const float4*>(base + (long long)(ro + cxq) * M) + pair);
+        const float a0 = wq[q] * lq[q].x, a1 = wq[q] * lq[q].y;
+        sxr = fmaf(a0, v.x, sxr);
+        syr = fmaf(a0, v.y, syr);
+        sxr = fmaf(a1, v.z, sxr);
+        syr = fmaf(a1, v.w, syr);
+      }
+      acc.x = fmaf(wy, sxr, acc.x);
+      acc.y = fmaf(wy, syr, acc.y);
+      ro += mrx;
+      if (ro >= fe) ro -= fe;
+    }
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  }
+  if (tail) {
+    float2 val = acc;
+    if (include_illum) {
+      const double ex = px - ill[0], ey = py - ill[1], ez = pz - ill[2];
+      val = cmul(val, expi_reduced(PF_TWO_PI * kturns * sqrt(ex * ex + ey * ey + ez * ez)));
+    }
+    vol[dst] = cadd(old, cmul(val, frame_w[0]));
+    for (int f = 1; f < n_frames; f++) {
+      float2* d = vol + f * vol_frame_stride + dst;
+      *d = cadd(*d, cmul(val, frame_w[f]));
+    }
+  }
+}
+
 // PF_INTERP_H17: 2 (default) the 16 x 16 trimmed kernel for W = 17, 1 the full 17 x 17
 // specialisation, 0 the general half-warp kernel (A/B measurements)
 int g_interp_mode = -1;
@@ -1051,5 +1178,28 @@ extern "C" int pf_nufft_interp2_nodes(const pf_nufft_geom* g, const int32_t* i0,
       fine_plane_stride, fine_stride, n_illum, ill, khat / PF_TWO_PI, include_illum, scale,
       (const float2*)frame_w, n_frames, (float2*)vol, vol_frame_stride, nodes, lw);
   PF_LAUNCH_CHECK("k_interp2_nodes");
+  return 0;
+}
+
+// Node-gathering readout on node-interleaved fine grids (pf_nufft_type2_start_2d_il with
+// il = nodes): fine_il[slab][cell][node], slab s of the batch at fine_il + s * slab_stride.
+// ES window at w = 4, 12 nodes, one illumination; other cases: pf_nufft_interp2_nodes.
+extern "C" int pf_nufft_interp2_nodes_il(const pf_nufft_geom* g, const int32_t* i0,
+                                         const float* d0, const double* xyz,
+                                         const int32_t* plane_idx, const int64_t* dst_idx,
+                                         int npts, int plane0, const void* fine_il,
+                                         int64_t slab_stride, const double* ill, double khat,
+                                         int include_illum, float scale, const void* frame_w,
+                                         int n_frames, void* vol, int64_t vol_frame_stride,
+                                         int nodes, const float* lw, void* stream) {
+  PF_ARG_CHECK(g && g->dim == 2 && g->window == 1 && g->w == 4 && nodes == 12 && lw && npts >= 0 &&
+                   (long long)g->mr[1] * g->mr[2] * nodes < (1LL << 31),
+               "pf_nufft_interp2_nodes_il: needs the ES window at w = 4 and 12 nodes");
+  if (npts == 0) return 0;
+  k_interp2_es8_il<12><<<pf_cdiv(npts, 32), 256, 0, (cudaStream_t)stream>>>(
+      *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine_il,
+      slab_stride, ill, khat / PF_TWO_PI, include_illum, scale, (const float2*)frame_w, n_frames,
+      (float2*)vol, vol_frame_stride, lw);
+  PF_LAUNCH_CHECK("k_interp2_es8_il");
   return 0;
 }

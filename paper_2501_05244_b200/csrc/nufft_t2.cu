@@ -193,9 +193,13 @@ k_t2_rows_split(pf_nufft_geom G, const float2* __restrict__ S, long long s_strid
 template <int HL, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT)
 k_t2_cols_split(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fine_stride,
-                pf_fft_plan plan_y, int cnt, int col0, int ncols, int row0, int nrows) {
+                pf_fft_plan plan_y, int cnt, int col0, int ncols, int row0, int nrows,
+                float2* __restrict__ out, int il) {
+  // out / il: the transformed columns go to `out` with every il consecutive grids
+  // interleaved cell by cell, out[(v / il) (fine_stride il) + cell il + v % il] (il = 1,
+  // out = fine: in place) -- the layout the node-gathering readout reads with wide loads
   extern __shared__ float2 sm[];
-  __shared__ long long lbase[64];
+  __shared__ long long lbase[64], obase[64];
   const int mrx = G.mr[2], my = G.m[1], mry = G.mr[1];
   const int ld = pf_ld(my);
   float2* a = sm;                                   // [2 cnt][ld]
@@ -213,6 +217,8 @@ k_t2_cols_split(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fi
     int col = col0 + (int)(l - v * ncols);
     col -= col >= mrx ? mrx : 0;
     lbase[c] = v * fine_stride + col;
+    const long long vg = v / il;
+    obase[c] = vg * (fine_stride * il) + (long long)col * il + (v - vg * il);
   }
   __syncthreads();
   const FastDiv dnl(nl);
@@ -231,7 +237,7 @@ k_t2_cols_split(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fi
     const int r = dnl.div(e), c = e - r * nl;
     int fy = row0 + r;
     fy -= fy >= mry ? mry : 0;
-    fine[lbase[c] + (long long)fy * mrx] = a[(2 * c + (fy & 1)) * ld + (fy >> 1)];
+    out[obase[c] + (long long)fy * mrx * il] = a[(2 * c + (fy & 1)) * ld + (fy >> 1)];
   }
 }
 
@@ -311,12 +317,12 @@ void t2_launch_cols_split(int nt, unsigned grid, size_t smem, cudaStream_t st, A
 
 }  // namespace
 
-extern "C" int pf_nufft_type2_start_2d_win(const pf_nufft_geom* g, const void* S,
-                                           int64_t s_stride, const float* ky, const float* kx,
-                                           int nv, void* fine, int64_t fine_stride,
-                                           const pf_fft_plan* plan_x, const pf_fft_plan* plan_y,
-                                           int col0, int ncols, int row0, int nrows,
-                                           void* stream) {
+extern "C" int pf_nufft_type2_start_2d_il(const pf_nufft_geom* g, const void* S,
+                                          int64_t s_stride, const float* ky, const float* kx,
+                                          int nv, void* fine, int64_t fine_stride,
+                                          const pf_fft_plan* plan_x, const pf_fft_plan* plan_y,
+                                          int col0, int ncols, int row0, int nrows, void* out,
+                                          int il, void* stream) {
   PF_ARG_CHECK(g && g->dim == 2 && g->mr[0] == 1 && nv >= 1 && plan_x && plan_y &&
                    plan_x->n == g->mr[2] && plan_y->n == g->mr[1] && g->m[2] <= g->mr[2] &&
                    g->m[1] <= g->mr[1],
@@ -325,6 +331,8 @@ extern "C" int pf_nufft_type2_start_2d_win(const pf_nufft_geom* g, const void* S
   PF_ARG_CHECK(col0 >= 0 && col0 < g->mr[2] && ncols >= 1 && ncols <= g->mr[2] && row0 >= 0 &&
                    row0 < g->mr[1] && nrows >= 1 && nrows <= g->mr[1],
                "pf_nufft_type2_start_2d_win: window outside the fine grid");
+  PF_ARG_CHECK(out && il >= 1 && (il == 1 || nv % il == 0),
+               "pf_nufft_type2_start_2d_il: nv must be a multiple of the interleave");
   static PfDevOnce attr;
   if (attr.first()) {   // every instantiation: later calls may take other lengths
     for (int xl : {0, 4, 5, 8, 10, 15, 20, 30}) PF_XL_DISPATCH(xl, (t2_allow_all<XL>()));
@@ -360,9 +368,12 @@ extern "C" int pf_nufft_type2_start_2d_win(const pf_nufft_geom* g, const void* S
     const size_t smem = t2_split_smem(g->m[1], hly, cnt);
     PF_XL_DISPATCH(hly, (t2_launch_cols_split<XL>(nt, (unsigned)((nl + cnt - 1) / cnt), smem, st, *g,
                                                   nv, (float2*)fine, fine_stride, *plan_y, cnt,
-                                                  col0, ncols, row0, nrows)));
+                                                  col0, ncols, row0, nrows, (float2*)out, il)));
     PF_LAUNCH_CHECK("k_t2_cols_split");
   } else {
+    PF_ARG_CHECK(il == 1 && out == fine,
+                 "pf_nufft_type2_start_2d_il: interleaved output needs the split column pass "
+                 "(mr = 2 m = 70 L)");
     // columns: >= 16 adjacent columns per CTA for 128-byte row segments
     const int cnt = t2_cnt(g->mr[1], xly, 2, 16);
     const long long nl = (long long)nv * g->mr[2];
@@ -372,6 +383,21 @@ extern "C" int pf_nufft_type2_start_2d_win(const pf_nufft_geom* g, const void* S
     PF_LAUNCH_CHECK("k_t2_cols");
   }
   return 0;
+}
+
+extern "C" int pf_nufft_type2_start_2d_win(const pf_nufft_geom* g, const void* S,
+                                           int64_t s_stride, const float* ky, const float* kx,
+                                           int nv, void* fine, int64_t fine_stride,
+                                           const pf_fft_plan* plan_x, const pf_fft_plan* plan_y,
+                                           int col0, int ncols, int row0, int nrows,
+                                           void* stream) {
+  return pf_nufft_type2_start_2d_il(g, S, s_stride, ky, kx, nv, fine, fine_stride, plan_x, plan_y,
+                                    col0, ncols, row0, nrows, fine, 1, stream);
+}
+
+// 1 when the column pass of this plan is split (interleaved output available)
+extern "C" int pf_nufft_type2_il_ok(const pf_nufft_geom* g) {
+  return g && g->dim == 2 && g->mr[1] == 2 * g->m[1] && t2_split_L(g->m[1]) > 0 ? 1 : 0;
 }
 
 extern "C" int pf_nufft_type2_start_2d(const pf_nufft_geom* g, const void* S, int64_t s_stride,
