@@ -347,6 +347,14 @@ int pf_nufft_type2_start_2d_il(const pf_nufft_geom* g, const void* S, int64_t s_
                                int64_t fine_stride, const pf_fft_plan* plan_x,
                                const pf_fft_plan* plan_y, int col0, int ncols, int row0,
                                int nrows, void* out, int il, void* stream);
+/* ... and with every grid v of the call stored as slot `member` of its own group v
+ * (out[v * (fine_stride * il) + cell * il + member]): one frequency of every plane per call,
+ * the frequencies of a plane interleaved (member < 0: pf_nufft_type2_start_2d_il). */
+int pf_nufft_type2_start_2d_ilm(const pf_nufft_geom* g, const void* S, int64_t s_stride,
+                                const float* ky, const float* kx, int nv, void* fine,
+                                int64_t fine_stride, const pf_fft_plan* plan_x,
+                                const pf_fft_plan* plan_y, int col0, int ncols, int row0,
+                                int nrows, void* out, int il, int member, void* stream);
 int pf_nufft_type2_il_ok(const pf_nufft_geom* g);
 /* type-2 start (spectral.py:374): modes / deconvolution onto their fine slots, 0 elsewhere. */
 int pf_nufft_place(const pf_nufft_geom* g, const void* S, int64_t s_stride, const float* kz,
@@ -372,6 +380,17 @@ int pf_nufft_interp2_nodes_il(const pf_nufft_geom* g, const int32_t* i0, const f
                               int include_illum, float scale, const void* frame_w, int n_frames,
                               void* vol, int64_t vol_frame_stride, int nodes, const float* lw,
                               void* stream);
+/* The plane readout (pf_nufft_interp2_batch) over all n_freq frequencies in one launch, on
+ * frequency-interleaved fine grids fine_f[group][plane][cell][16] (pf_nufft_type2_start_2d_ilm
+ * with il = 16, member = f % 16; unused slots zero): vol[dst] += sum_f frame_w[f]
+ * exp(i k_f |x - s|) scale * stencil(fine_f).  kturns_f [n_freq] = k_f / (2 pi) on the device.
+ * ES window at w = 4, one illumination, one frame. */
+int pf_nufft_interp2_freqs(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                           const double* xyz, const int32_t* plane_idx, const int64_t* dst_idx,
+                           int npts, int plane0, const void* fine_f, int64_t plane_stride,
+                           int64_t group_stride, int n_freq, const double* kturns_f,
+                           const double* ill, int include_illum, float scale,
+                           const void* frame_w, void* vol, void* stream);
 /* Readout kernel for the reference's default stencil (w = 8, 17 x 17 taps): 2 (default)
  * the 16 x 16 trimmed kernel (the far edge tap of each axis, <= 6.5e-9 of the centre
  * weight, is not loaded), 1 the full 17 x 17 kernel, 0 the general kernel; mode < 0 only

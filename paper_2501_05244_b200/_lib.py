@@ -152,6 +152,8 @@ _SIGNATURES = {
     "pf_nufft_type2_start_2d_win": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _i, _vp, _i64, _P(PfFftPlan), _P(PfFftPlan), _i, _i, _i, _i, _vp],
     "pf_nufft_type2_start_2d_il": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _i, _vp, _i64, _P(PfFftPlan), _P(PfFftPlan), _i, _i, _i, _i, _vp, _i, _vp],
     "pf_nufft_type2_il_ok": [_P(PfNufftGeom)],
+    "pf_nufft_type2_start_2d_ilm": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _i, _vp, _i64, _P(PfFftPlan), _P(PfFftPlan), _i, _i, _i, _i, _vp, _i, _i, _vp],
+    "pf_nufft_interp2_freqs": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _i64, _i64, _i, _vp, _vp, _i, _f, _vp, _vp, _vp],
     "pf_nufft_interp2_nodes_il": [_P(PfNufftGeom), _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _i64, _vp, _d, _i, _f, _vp, _i, _vp, _i64, _i, _vp, _vp],
     "pf_nufft_place": [_P(PfNufftGeom), _vp, _i64, _vp, _vp, _vp, _i, _vp, _i64, _i, _vp],
     "pf_nufft_interp2_acc": [_P(PfNufftGeom), _vp, _vp, _vp, _i, _vp, _i64, _i, _vp, _d, _i, _f,

@@ -354,6 +354,17 @@ class _Type2Readout:
         # planes per launch: product spectra and fine grids of a whole batch resident
         per_plane = 8 * I * (self.plan.fine_elems + py * px)
         self.nb = max(1, min(len(planes), _READOUT_BYTES // per_plane))
+        # readout over all frequencies in one launch per plane batch, on frequency-interleaved
+        # fine grids (16 frequencies per group): ES window at w = 4, one illumination, static
+        nf = self.freqs.size
+        self.n_groups = -(-nf // 16)
+        self.fused_f = bool(
+            _READOUT_FUSED and self.plan.window == "es" and self.plan.w == 4 and I == 1
+            and times is None and self.plan.fine_elems * 16 < (1 << 31)
+            and _lib.call("pf_nufft_type2_il_ok", self.plan.gref))
+        if self.fused_f:
+            per_f = 8 * 16 * self.n_groups * self.plan.fine_elems
+            self.nb = max(1, min(len(planes), self.nb, _READOUT_FUSED_BYTES // per_f))
         self.prop = Propagator(device, px, py, px, py, 0, 0, I, include_illumination, planes,
                                py * px, batch=self.nb)
         self.prop.geom.flags = 1      # register path off: generic product-only columns
@@ -385,8 +396,50 @@ class _Type2Readout:
                                 device=device)
         self.ill = _ill_tensor(slices, device)
         self.frame_w = _frame_weights(self.freqs, times, device)
+        if self.fused_f:
+            # zero once: the slots of frequencies beyond F and the cells outside the stencil
+            # window are never written, the rest is rewritten every run
+            self.fine_f = torch.zeros((self.n_groups * self.nb * self.plan.fine_elems * 16,),
+                                      dtype=torch.complex64, device=device)
+            self.kturns = torch.from_numpy(self.freqs / (C * 2.0 * np.pi)).to(device)
+
+    def _run_fused(self, uhat_of, vol, stream):
+        """Per plane batch: every frequency's product spectra and type-2 start into the
+        frequency-interleaved fine grids, then one readout launch over all frequencies."""
+        s = dev.stream_ptr(stream)
+        py, px, p = self.py, self.px, self.plan
+        gref = ctypes.byref(self.prop.geom)
+        base = dev.ptr(self.prop.planes_dev)
+        fe = p.fine_elems
+        c0, nc, r0, nr = self.window or (0, p.mrs[2], 0, p.mrs[1])
+        gstride = self.nb * fe * 16
+        for b0 in range(0, self.n_planes, self.nb):
+            n = min(self.nb, self.n_planes - b0)
+            pp = base + b0 * self.prop.plane_size
+            for fi in range(self.freqs.size):
+                khat = float(self.freqs[fi]) / C
+                _lib.call("pf_prop_kernel_rows", pp, n, khat, gref, self.prop.plan_x.ref,
+                          dev.ptr(self.prop.ws_a), s)
+                _lib.call("pf_prop_columns", pp, n, gref, self.prop.plan_y.ref,
+                          dev.ptr(self.prop.ws_a), dev.ptr(uhat_of(fi)), dev.ptr(self.spec), 1, s)
+                _lib.call("pf_nufft_type2_start_2d_ilm", p.gref, dev.ptr(self.spec), py * px,
+                          dev.ptr(p.kers[1]), dev.ptr(p.kers[2]), n, dev.ptr(self.fine), fe,
+                          dev.fft_plan(p.mrs[2], p.device).ref, dev.fft_plan(p.mrs[1], p.device).ref,
+                          c0, nc, r0, nr, dev.ptr(self.fine_f) + 8 * (fi // 16) * gstride, 16,
+                          fi % 16, s)
+            lo, hi = self.pt_lo[b0], self.pt_lo[b0 + n]
+            if hi > lo:
+                _lib.call("pf_nufft_interp2_freqs", p.gref, dev.ptr(self.i0_all) + 12 * lo,
+                          dev.ptr(self.d0_all) + 12 * lo, dev.ptr(self.xyz_all) + 24 * lo,
+                          dev.ptr(self.plane_all) + 4 * lo, dev.ptr(self.dst_all) + 8 * lo,
+                          hi - lo, b0, dev.ptr(self.fine_f), fe * 16, gstride, self.freqs.size,
+                          dev.ptr(self.kturns), dev.ptr(self.ill), int(self.include),
+                          1.0 / (px * py), dev.ptr(self.frame_w), dev.ptr(vol), s)
+        return vol
 
     def run(self, uhat_of, vol, stream=None):
+        if self.fused_f:
+            return self._run_fused(uhat_of, vol, stream)
         s = dev.stream_ptr(stream)
         I, py, px = self.n_illum, self.py, self.px
         gref = ctypes.byref(self.prop.geom)
@@ -420,6 +473,8 @@ class _Type2Readout:
 # arbitrary voxel depths: z-Chebyshev type-2 readout
 # ---------------------------------------------------------------------------
 
+_READOUT_FUSED = os.environ.get("PF_READOUT_FUSED", "1") != "0"   # all frequencies per readout launch
+_READOUT_FUSED_BYTES = int(os.environ.get("PF_READOUT_FUSED_MB", "2048")) << 20
 _T2_WINDOW = os.environ.get("PF_T2_WINDOW", "1") != "0"   # type-2 start limited to the stencils' cells
 _ZCHEB_IL = os.environ.get("PF_ZCHEB_IL", "1") != "0"      # node-interleaved fine grids in the readout
 _ZCHEB_NODES = int(os.environ.get("PF_ZCHEB_NODES", "12"))

@@ -803,6 +803,106 @@ k_interp2_es8_il(pf_nufft_geom G, const int* __restrict__ i0, const float* __res
   }
 }
 
+// The plane readout over all frequencies at once, on frequency-interleaved fine grids
+// (fine_f[group][plane][cell][16], written by pf_nufft_type2_start_2d_ilm with il = 16 and
+// member = f % 16): a stencil row is 8 columns x 16 frequencies = 1024 contiguous bytes, read
+// by the quarter warp as eight 128-byte pieces in which lane ql holds frequencies 2 ql and
+// 2 ql + 1 of one column.  Each lane sums the stencil for its two frequencies, applies their
+// illumination phases and frame weights (all eight lanes work on phases, where the
+// per-frequency kernels use one), and the frequency sum is a shuffle reduction; the voxel's
+// indices, weights and target update are formed once instead of once per frequency.
+// ES window at w = 4, one illumination, one frame.
+__global__ void __launch_bounds__(256, 4)
+k_interp2_es8_f16(pf_nufft_geom G, const int* __restrict__ i0, const float* __restrict__ d0,
+                  const double* __restrict__ xyz, const int* __restrict__ plane_idx,
+                  const long long* __restrict__ dst_idx, int npts, int plane0,
+                  const float2* __restrict__ fine_f, long long plane_stride,
+                  long long group_stride, int F, const double* __restrict__ kturns_f,
+                  const double* __restrict__ ill, int include_illum, float scale,
+                  const float2* __restrict__ frame_w, float2* __restrict__ vol) {
+  constexpr int w = 4;
+  const int lane = threadIdx.x & 31, ql = lane & 7, grp = lane >> 3;
+  const int l = blockIdx.x * (blockDim.x >> 3) + ((threadIdx.x >> 5) << 2) + grp;
+  const bool live = l < npts;
+  const int lc = live ? l : 0;
+  const int mry = G.mr[1], mrx = G.mr[2], fe = mry * mrx;
+  const float dyl = d0[3 * lc + 1], dxl = d0[3 * lc + 2];
+  const int sx = dxl > 0.f ? 0 : 1, sy = dyl > 0.f ? 0 : 1;
+  const float wx_own = pf_win(G, 2, dxl + (float)(ql - w + sx) * G.h[2]) * scale;
+  const float wy_own = pf_win(G, 1, dyl + (float)(ql - w + sy) * G.h[1]);
+  float wxs[8];
+#pragma unroll
+  for (int q = 0; q < 8; q++) wxs[q] = __shfl_sync(0xffffffffu, wx_own, (grp << 3) + q);
+  const int cx0 = wrap_once(i0[3 * lc + 2] - w + sx, mrx);
+  const bool straddle = cx0 + 8 > mrx;
+  const int r0 = wrap_once(i0[3 * lc + 1] - w + sy, mry) * mrx;
+  const float2* base = fine_f + (long long)(plane_idx[lc] - plane0) * plane_stride;
+  const bool tail = ql == 0 && live;
+  long long dst = 0;
+  float2 old = make_float2(0.f, 0.f);
+  if (tail) {
+    dst = dst_idx[l];
+    old = vol[dst];
+  }
+  double dist = 0.0;
+  if (include_illum) {
+    const double ex = xyz[3 * lc] - ill[0], ey = xyz[3 * lc + 1] - ill[1];
+    const double ez = xyz[3 * lc + 2] - ill[2];
+    dist = sqrt(ex * ex + ey * ey + ez * ez);
+  }
+  float2 tot = make_float2(0.f, 0.f);
+  for (int f0 = 0; f0 < F; f0 += 16, base += group_stride) {
+    float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+    int ro = r0;
+#pragma unroll 2
+    for (int oy = 0; oy < 8; oy++) {
+      const float wy = __shfl_sync(0xffffffffu, wy_own, (grp << 3) + oy);
+      float4 v[8];
+      if (!straddle) {
+        const float4* p4 = reinterpret_cast<const float4*>(base + (long long)(ro + cx0) * 16) + ql;
+#pragma unroll
+        for (int q = 0; q < 8; q++) v[q] = __ldg(p4 + 8 * q);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+          v[q] = __ldg(reinterpret_cast<const float4*>(
+                           base + (long long)(ro + wrap_once(cx0 + q, mrx)) * 16) + ql);
+      }
+      float sx0 = 0.f, sy0 = 0.f, sx1 = 0.f, sy1 = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        sx0 = fmaf(wxs[q], v[q].x, sx0);
+        sy0 = fmaf(wxs[q], v[q].y, sy0);
+        sx1 = fmaf(wxs[q], v[q].z, sx1);
+        sy1 = fmaf(wxs[q], v[q].w, sy1);
+      }
+      a0.x = fmaf(wy, sx0, a0.x);
+      a0.y = fmaf(wy, sy0, a0.y);
+      a1.x = fmaf(wy, sx1, a1.x);
+      a1.y = fmaf(wy, sy1, a1.y);
+      ro += mrx;
+      if (ro >= fe) ro -= fe;
+    }
+    const int fa = f0 + 2 * ql;
+    if (fa < F) {
+      float2 val = a0;
+      if (include_illum) val = cmul(val, expi_reduced(PF_TWO_PI * kturns_f[fa] * dist));
+      tot = cadd(tot, cmul(val, frame_w[fa]));
+    }
+    if (fa + 1 < F) {
+      float2 val = a1;
+      if (include_illum) val = cmul(val, expi_reduced(PF_TWO_PI * kturns_f[fa + 1] * dist));
+      tot = cadd(tot, cmul(val, frame_w[fa + 1]));
+    }
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    tot.x += __shfl_xor_sync(0xffffffffu, tot.x, o);
+    tot.y += __shfl_xor_sync(0xffffffffu, tot.y, o);
+  }
+  if (tail) vol[dst] = cadd(old, tot);
+}
+
 // PF_INTERP_H17: 2 (default) the 16 x 16 trimmed kernel for W = 17, 1 the full 17 x 17
 // specialisation, 0 the general half-warp kernel (A/B measurements)
 int g_interp_mode = -1;
@@ -1201,5 +1301,29 @@ extern "C" int pf_nufft_interp2_nodes_il(const pf_nufft_geom* g, const int32_t* 
       slab_stride, ill, khat / PF_TWO_PI, include_illum, scale, (const float2*)frame_w, n_frames,
       (float2*)vol, vol_frame_stride, lw);
   PF_LAUNCH_CHECK("k_interp2_es8_il");
+  return 0;
+}
+
+// Plane readout over all frequencies in one launch on frequency-interleaved fine grids:
+// fine_f[group][plane][cell][16] (group g = frequencies 16 g .. 16 g + 15; plane p of the
+// batch at + p * plane_stride, group g at + g * group_stride; slots of frequencies >= F must
+// be zero).  kturns_f [F] = k_f / (2 pi) (device), frame_w [F].  ES window at w = 4, one
+// illumination, one frame.
+extern "C" int pf_nufft_interp2_freqs(const pf_nufft_geom* g, const int32_t* i0, const float* d0,
+                                      const double* xyz, const int32_t* plane_idx,
+                                      const int64_t* dst_idx, int npts, int plane0,
+                                      const void* fine_f, int64_t plane_stride,
+                                      int64_t group_stride, int n_freq, const double* kturns_f,
+                                      const double* ill, int include_illum, float scale,
+                                      const void* frame_w, void* vol, void* stream) {
+  PF_ARG_CHECK(g && g->dim == 2 && g->window == 1 && g->w == 4 && n_freq >= 1 && npts >= 0 &&
+                   kturns_f && frame_w && (long long)g->mr[1] * g->mr[2] * 16 < (1LL << 31),
+               "pf_nufft_interp2_freqs: needs the ES window at w = 4");
+  if (npts == 0) return 0;
+  k_interp2_es8_f16<<<pf_cdiv(npts, 32), 256, 0, (cudaStream_t)stream>>>(
+      *g, i0, d0, xyz, plane_idx, (const long long*)dst_idx, npts, plane0, (const float2*)fine_f,
+      plane_stride, group_stride, n_freq, kturns_f, ill, include_illum, scale,
+      (const float2*)frame_w, (float2*)vol);
+  PF_LAUNCH_CHECK("k_interp2_es8_f16");
   return 0;
 }

@@ -194,10 +194,12 @@ template <int HL, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT)
 k_t2_cols_split(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fine_stride,
                 pf_fft_plan plan_y, int cnt, int col0, int ncols, int row0, int nrows,
-                float2* __restrict__ out, int il) {
+                float2* __restrict__ out, int il, int member) {
   // out / il: the transformed columns go to `out` with every il consecutive grids
   // interleaved cell by cell, out[(v / il) (fine_stride il) + cell il + v % il] (il = 1,
-  // out = fine: in place) -- the layout the node-gathering readout reads with wide loads
+  // out = fine: in place) -- the layout the node-gathering readout reads with wide loads;
+  // member >= 0: every grid v of this call is slot `member` of its own group v (the call
+  // holds one frequency of every plane: out[v (fine_stride il) + cell il + member])
   extern __shared__ float2 sm[];
   __shared__ long long lbase[64], obase[64];
   const int mrx = G.mr[2], my = G.m[1], mry = G.mr[1];
@@ -217,8 +219,8 @@ k_t2_cols_split(pf_nufft_geom G, int nv, float2* __restrict__ fine, long long fi
     int col = col0 + (int)(l - v * ncols);
     col -= col >= mrx ? mrx : 0;
     lbase[c] = v * fine_stride + col;
-    const long long vg = v / il;
-    obase[c] = vg * (fine_stride * il) + (long long)col * il + (v - vg * il);
+    const long long vg = member >= 0 ? v : v / il;
+    obase[c] = vg * (fine_stride * il) + (long long)col * il + (member >= 0 ? member : v - vg * il);
   }
   __syncthreads();
   const FastDiv dnl(nl);
@@ -317,12 +319,12 @@ void t2_launch_cols_split(int nt, unsigned grid, size_t smem, cudaStream_t st, A
 
 }  // namespace
 
-extern "C" int pf_nufft_type2_start_2d_il(const pf_nufft_geom* g, const void* S,
-                                          int64_t s_stride, const float* ky, const float* kx,
-                                          int nv, void* fine, int64_t fine_stride,
-                                          const pf_fft_plan* plan_x, const pf_fft_plan* plan_y,
-                                          int col0, int ncols, int row0, int nrows, void* out,
-                                          int il, void* stream) {
+extern "C" int pf_nufft_type2_start_2d_ilm(const pf_nufft_geom* g, const void* S,
+                                           int64_t s_stride, const float* ky, const float* kx,
+                                           int nv, void* fine, int64_t fine_stride,
+                                           const pf_fft_plan* plan_x, const pf_fft_plan* plan_y,
+                                           int col0, int ncols, int row0, int nrows, void* out,
+                                           int il, int member, void* stream) {
   PF_ARG_CHECK(g && g->dim == 2 && g->mr[0] == 1 && nv >= 1 && plan_x && plan_y &&
                    plan_x->n == g->mr[2] && plan_y->n == g->mr[1] && g->m[2] <= g->mr[2] &&
                    g->m[1] <= g->mr[1],
@@ -331,7 +333,7 @@ extern "C" int pf_nufft_type2_start_2d_il(const pf_nufft_geom* g, const void* S,
   PF_ARG_CHECK(col0 >= 0 && col0 < g->mr[2] && ncols >= 1 && ncols <= g->mr[2] && row0 >= 0 &&
                    row0 < g->mr[1] && nrows >= 1 && nrows <= g->mr[1],
                "pf_nufft_type2_start_2d_win: window outside the fine grid");
-  PF_ARG_CHECK(out && il >= 1 && (il == 1 || nv % il == 0),
+  PF_ARG_CHECK(out && il >= 1 && member < il && (il == 1 || member >= 0 || nv % il == 0),
                "pf_nufft_type2_start_2d_il: nv must be a multiple of the interleave");
   static PfDevOnce attr;
   if (attr.first()) {   // every instantiation: later calls may take other lengths
@@ -368,7 +370,8 @@ extern "C" int pf_nufft_type2_start_2d_il(const pf_nufft_geom* g, const void* S,
     const size_t smem = t2_split_smem(g->m[1], hly, cnt);
     PF_XL_DISPATCH(hly, (t2_launch_cols_split<XL>(nt, (unsigned)((nl + cnt - 1) / cnt), smem, st, *g,
                                                   nv, (float2*)fine, fine_stride, *plan_y, cnt,
-                                                  col0, ncols, row0, nrows, (float2*)out, il)));
+                                                  col0, ncols, row0, nrows, (float2*)out, il,
+                                                  member)));
     PF_LAUNCH_CHECK("k_t2_cols_split");
   } else {
     PF_ARG_CHECK(il == 1 && out == fine,
@@ -383,6 +386,16 @@ extern "C" int pf_nufft_type2_start_2d_il(const pf_nufft_geom* g, const void* S,
     PF_LAUNCH_CHECK("k_t2_cols");
   }
   return 0;
+}
+
+extern "C" int pf_nufft_type2_start_2d_il(const pf_nufft_geom* g, const void* S,
+                                          int64_t s_stride, const float* ky, const float* kx,
+                                          int nv, void* fine, int64_t fine_stride,
+                                          const pf_fft_plan* plan_x, const pf_fft_plan* plan_y,
+                                          int col0, int ncols, int row0, int nrows, void* out,
+                                          int il, void* stream) {
+  return pf_nufft_type2_start_2d_ilm(g, S, s_stride, ky, kx, nv, fine, fine_stride, plan_x, plan_y,
+                                     col0, ncols, row0, nrows, out, il, -1, stream);
 }
 
 extern "C" int pf_nufft_type2_start_2d_win(const pf_nufft_geom* g, const void* S,
