@@ -177,6 +177,31 @@ def test_nursd2_trimmed_readout_matches_full_stencil(rng, monkeypatch):
     assert e_t < 2e-6 and e_f < 2e-6 and abs(e_t - e_f) < 2e-7, (e_t, e_f)
 
 
+@pytest.mark.parametrize("n_freq", [3, 16, 20])
+def test_nursd2_fused_frequency_readout_matches_per_frequency(rng, monkeypatch, n_freq):
+    """The readout over all frequencies in one launch (frequency-interleaved fine grids, 16
+    per group: 3 = padded slots, 20 = two groups) against the per-frequency launches and the
+    oracle; voxels up to the edge of the reference pad."""
+    import importlib
+    A = importlib.import_module("paper_2501_05244_b200.algorithms")
+    n = 32
+    p = 0.02
+    g = pf.UniformGrid2D(n, n, p, p, -(n - 1) * p / 2, -(n - 1) * p / 2, 0.0)
+    sl = _rand_slices(rng, pf.UniformRelay(g), n_freq=n_freq, n_ill=1)
+    pts = rng.uniform(-0.6, 0.6, size=(3000, 2))
+    ev = pf.ExplicitVoxels((pf.VoxelPlane(0.6, pf.PointList(pts[:1500])),
+                            pf.VoxelPlane(0.9, pf.PointList(pts[1500:]))))
+    from paper_2501_05244_b200.reconstruct import clear_engine_cache
+    clear_engine_cache()
+    fused = pf.nursd2(sl, ev).field
+    monkeypatch.setattr(A, "_READOUT_FUSED", False)
+    clear_engine_cache()
+    per_f = pf.nursd2(sl, ev).field
+    clear_engine_cache()
+    assert O.rel_l2(fused, per_f) < 1e-6
+    assert O.rel_l2(fused, O.nursd2(sl, ev)) < 2e-6
+
+
 def test_config2_composed_small(rng, window):
     """Config-2 family (non-planar relay -> arbitrary voxels) against the composed oracle."""
     from paper_2501_05244_b200.algorithms import nursd3d_explicit
