@@ -240,3 +240,63 @@ def test_zcheb_slabs_interpolate_kernel_phases():
             return np.exp(1j * k * r) / r
         approx = (lw * f(node_z)[slab]).sum(axis=1)
         assert np.abs(approx - f(z)).max() / np.abs(f(z)).max() < 1e-6
+
+
+def test_es_window_plan_meets_eps_against_direct_sums():
+    """Host side of the exponential-of-semicircle NUFFT window (nufft.es_half_width /
+    es_transform: half-width, beta, continuous deconvolution) in a float64 numpy type-1
+    transform against the direct sum: within the requested eps (CPU: planning only)."""
+    from paper_2501_05244_b200 import nufft as nu
+    rng = np.random.default_rng(11)
+    m = 48
+    mr = 2 * m
+    h = 2 * np.pi / mr
+    x = rng.uniform(-np.pi, np.pi, 400)
+    x[:40] = -np.pi + h * rng.integers(0, mr, 40)            # some points on fine-grid nodes
+    c = rng.normal(size=400) + 1j * rng.normal(size=400)
+    k = np.arange(m) - m // 2
+    exact = (c[None, :] * np.exp(-1j * np.outer(k, x))).sum(axis=1)
+    for eps, tol in ((1e-2, 3e-5), (1e-4, 3e-5), (1e-6, 3e-7), (1e-9, 1e-9)):
+        w = nu.es_half_width(eps)
+        assert w == max(3, -(-(int(np.ceil(np.log10(1 / eps))) + 2) // 2))
+        beta = 2.30 * 2 * w
+        ker = nu.es_transform(w, k * h)
+        assert (ker > 0).all()
+        xi = x - 2 * np.pi * np.floor(x / (2 * np.pi))
+        i0 = np.floor(xi / h + 0.5).astype(int)
+        offs = np.arange(-w, w + 1)
+        z = ((i0[:, None] + offs[None, :]) * h - xi[:, None]) / (w * h)
+        q = 1 - z * z
+        wt = np.where(q > 0, np.exp(beta * (np.sqrt(np.maximum(q, 0)) - 1)), 0.0)
+        fine = np.zeros(mr, complex)
+        np.add.at(fine, (i0[:, None] + offs[None, :]) % mr, c[:, None] * wt)
+        got = np.fft.fft(fine)[k % mr] / ker
+        err = np.linalg.norm(got - exact) / np.linalg.norm(exact)
+        assert err < tol and err < eps, (eps, w, err)
+
+
+def test_stencil_window_and_touched_runs_host():
+    """nufft.stencil_window (type-2: the fine cells any stencil touches) and
+    NufftPoints.touched_runs (type-1: the arcs a spread grid is nonzero on), host logic on a
+    stand-in plan: every stencil cell inside, shortest arcs, seam handled."""
+    import types
+    from paper_2501_05244_b200 import nufft as nu
+    plan = types.SimpleNamespace(mrs=(1, 700, 540), w=4, dim=2)
+    rng = np.random.default_rng(12)
+    i0 = np.zeros((2000, 3), dtype=np.int64)
+    i0[:, 1] = rng.integers(286, 414, 2000)                  # rows: one arc inside
+    i0[:, 2] = rng.integers(-64, 64, 2000) % 540             # columns: an arc across the seam
+    ps = types.SimpleNamespace(_i0_host=i0, plan=plan, _runs=None)
+    c0, nc, r0, nr = nu.stencil_window(plan, [ps])
+    assert (r0, nr) == (int(i0[:, 1].min()) - 4, int(i0[:, 1].max() - i0[:, 1].min()) + 9)
+    assert c0 + nc > 540 and nc <= 128 + 9                   # wraps, and stays the short arc
+    for a, (s0, n) in ((2, (c0, nc)), (1, (r0, nr))):
+        mr = plan.mrs[a]
+        cells = (i0[:, a][:, None] + np.arange(-4, 5)[None, :]) % mr
+        assert (((cells - s0) % mr) < n).all()
+    runs = nu.NufftPoints.touched_runs(ps)
+    assert runs[0] == [(r0, nr)]
+    assert runs[1] == [(0, c0 + nc - 540), (c0, 540 - c0)]
+    # everything touched -> the whole axis
+    i0[:, 1] = rng.integers(0, 700, 2000)
+    assert nu.stencil_window(plan, [ps])[2:] == (0, 700)
