@@ -402,7 +402,7 @@ def _e2e_leg(rec, hist_shard, cfg, world, device):
     import torch.distributed as dist
     hist_host = torch.empty(hist_shard.shape, dtype=torch.float32, pin_memory=True)
     hist_host.copy_(hist_shard)
-    n_e2e = 8   # captures in the timed window
+    n_e2e = 16   # captures in the timed window (the pipeline fill is part of it)
     for _ in range(2):
         rec.result(rec.submit(hist_host))
     torch.cuda.synchronize()
