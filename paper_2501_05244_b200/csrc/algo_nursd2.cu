@@ -30,6 +30,7 @@ namespace {
 using namespace pfalgo;
 
 constexpr int64_t READOUT_BYTES = 256LL << 20;   // algorithms._READOUT_BYTES
+constexpr int64_t READOUT_FUSED_BYTES = 2048LL << 20;   // algorithms._READOUT_FUSED_BYTES
 
 struct Plan {
   int px, py, nb;
@@ -41,6 +42,9 @@ struct Plan {
   std::vector<double> xyz;
   std::vector<int64_t> dst, pt_lo;
   int win[4];        // col0, ncols, row0, nrows: the fine cells the voxels' stencils touch
+  bool fused;        // readout over all frequencies per launch (frequency-interleaved grids)
+  int n_groups;      // groups of 16 frequencies
+  int64_t off_fine_f, off_kturns;
   int64_t n_tw[4];   // px, py, mry, mrx tables (0 = shared with an earlier one)
   int64_t off_tw[4], off_planes, off_ill, off_fw, off_ker[3], off_i0, off_d0, off_xyz, off_pl,
       off_dst, off_uhat, off_wa, off_spec, off_fine, total;
@@ -128,6 +132,17 @@ int plan(const pf_nursd2_args* a, Plan* P) {
   const int64_t per_plane = 8 * (int64_t)I * (P->nu.fine_elems + px * py);
   int64_t nb = READOUT_BYTES / per_plane;
   if (nb > a->n_planes) nb = a->n_planes;
+  // algorithms._Type2Readout.fused_f: ES window at w = 4, one illumination, static scene,
+  // split column pass -> one readout launch per plane batch over all frequencies
+  P->n_groups = (F + 15) / 16;
+  P->fused = P->nu.g.window == 1 && P->nu.g.w == 4 && I == 1 && a->n_frames <= 0 &&
+             P->nu.fine_elems * 16 < (1LL << 31) && pf_nufft_type2_il_ok(&P->nu.g) &&
+             !(getenv("PF_READOUT_FUSED") && atoi(getenv("PF_READOUT_FUSED")) == 0);
+  if (P->fused) {
+    const int64_t per_f = 8LL * 16 * P->n_groups * P->nu.fine_elems;
+    const int64_t cap = READOUT_FUSED_BYTES / per_f;
+    if (nb > cap) nb = cap;
+  }
   P->nb = nb < 1 ? 1 : (int)nb;
   // workspace layout
   const long lens[4] = {px, py, P->nu.g.mr[1], P->nu.g.mr[2]};
@@ -157,6 +172,9 @@ int plan(const pf_nursd2_args* a, Plan* P) {
   P->off_wa = o; o = align256(o + 8 * pf_prop_ws_a(&g, P->nb));
   P->off_spec = o; o = align256(o + 8 * (int64_t)P->nb * I * px * py);
   P->off_fine = o; o = align256(o + 8 * (int64_t)P->nb * I * P->nu.fine_elems);
+  P->off_fine_f = o;
+  if (P->fused) o = align256(o + 8LL * 16 * P->n_groups * P->nb * P->nu.fine_elems);
+  P->off_kturns = o; o = align256(o + 8 * (int64_t)F);
   P->total = o;
   return 0;
 }
@@ -240,6 +258,44 @@ extern "C" int pf_nursd2(const pf_nursd2_args* a, const void* slices, void* vol,
   float2* spec = (float2*)(w + P.off_spec);
   float2* fine = (float2*)(w + P.off_fine);
   const int64_t per_f = (int64_t)I * px * py;
+  if (P.fused) {
+    // per plane batch: every frequency's product spectra and type-2 start into the
+    // frequency-interleaved fine grids, then one readout launch over all frequencies
+    float2* fine_f = (float2*)(w + P.off_fine_f);
+    const int64_t gstride = (int64_t)P.nb * fe * 16;
+    std::vector<double> kt(F);
+    for (int f = 0; f < F; f++) kt[f] = a->frequencies[f] / C_LIGHT / (2.0 * M_PI);
+    UPLOAD(P.off_kturns, kt.data(), 8 * (size_t)F);
+    if (F % 16)   // the unused frequency slots of the last group are read: zero them
+      PF_CUDA_CHECK(cudaMemsetAsync(fine_f + (int64_t)(P.n_groups - 1) * gstride, 0,
+                                    8 * (size_t)gstride, st),
+                    "pf_nursd2: zero fine grids");
+    for (int b0 = 0; b0 < a->n_planes && rc == 0; b0 += P.nb) {
+      const int n = a->n_planes - b0 < P.nb ? a->n_planes - b0 : P.nb;
+      const pf_plane* pp = planes_d + b0;
+      for (int f = 0; f < F && rc == 0; f++) {
+        const double khat = a->frequencies[f] / C_LIGHT;
+        rc = pf_prop_kernel_rows(pp, n, khat, &P.g, &pl[0], wa, stream);
+        if (rc == 0)
+          rc = pf_prop_columns(pp, n, &P.g, &pl[1], wa, uhat + f * per_f, spec, 1, stream);
+        if (rc == 0)
+          rc = pf_nufft_type2_start_2d_ilm(&P.nu.g, spec, (int64_t)py * px, ky, kx, n, fine, fe,
+                                           &pl[3], &pl[2], P.win[0], P.win[1], P.win[2],
+                                           P.win[3], fine_f + (int64_t)(f / 16) * gstride, 16,
+                                           f % 16, stream);
+      }
+      const int64_t lo = P.pt_lo[b0], hi = P.pt_lo[b0 + n];
+      if (rc == 0 && hi > lo)
+        rc = pf_nufft_interp2_freqs(
+            &P.nu.g, (const int32_t*)(w + P.off_i0) + 3 * lo, (const float*)(w + P.off_d0) + 3 * lo,
+            (const double*)(w + P.off_xyz) + 3 * lo, (const int32_t*)(w + P.off_pl) + lo,
+            (const int64_t*)(w + P.off_dst) + lo, (int)(hi - lo), b0, fine_f, fe * 16, gstride, F,
+            (const double*)(w + P.off_kturns), (const double*)(w + P.off_ill),
+            a->include_illum ? 1 : 0, (float)(1.0 / ((double)px * py)),
+            (const float2*)(w + P.off_fw), vol, stream);
+    }
+    return rc;
+  }
   for (int f = 0; f < F && rc == 0; f++) {
     const double khat = a->frequencies[f] / C_LIGHT;
     for (int b0 = 0; b0 < a->n_planes && rc == 0; b0 += P.nb) {
