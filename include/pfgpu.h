@@ -428,6 +428,15 @@ int pf_kernel3d(void* out, int pz, int py, int px, double dx, double dy, double 
                 void* stream);
 /* a[i] = a[i] * b[i % b_period] * scale */
 int pf_cmul(void* a, const void* b, int64_t n, int64_t b_period, float scale, void* stream);
+/* Even 3D kernels (the lattice stages' G3 is even in every lag, so is its transform): the
+ * mirrored half of an axis filled by copy before that axis' pass -- axis 1: rows y > py/2
+ * for z <= lim, x <= xmax; axis 0: planes z > pz/2 for y <= lim, x <= xmax -- and the
+ * product a[f][i][z][y][x] *= g[f][z][min(y, py - y)][min(x, px - x)] * scale with g formed
+ * on that octant only (_kernel_3d and the product of reconstruct.py:624-638, 758). */
+int pf_mirror_fill(void* buf, int nb, int pz, int py, int px, int axis, int lim, int xmax,
+                   void* stream);
+int pf_cmul_even(void* a, const void* g, int nf, int ni, int pz, int py, int px, float scale,
+                 void* stream);
 /* dst[b][:] = src[b*src_stride + plane_off + :plane_elems] (slab extraction, :760) */
 /* One output plane of an inverse DFT along the leading axis: dst[b][j] = scale *
  * sum_z src[b][z][j] * w[z] (w = exp(+2 pi i z slab / nz), complex64, host-built in

@@ -160,6 +160,8 @@ _SIGNATURES = {
                              _vp, _i, _vp, _i64, _i64, _vp, _vp],
     "pf_kernel3d": [_vp, _i, _i, _i, _d, _d, _d, _d, _vp],
     "pf_cmul": [_vp, _vp, _i64, _i64, _f, _vp],
+    "pf_mirror_fill": [_vp, _i, _i, _i, _i, _i, _i, _i, _vp],
+    "pf_cmul_even": [_vp, _vp, _i, _i, _i, _i, _i, _f, _vp],
     "pf_copy_planes": [_vp, _i, _i64, _i64, _i64, _vp, _vp],
     "pf_zslab": [_vp, _i, _i, _i64, _vp, _f, _vp, _vp],
     "pf_roll": [_vp, _vp, _i64, _i, _i, _i, _i, _i, _i, _vp],

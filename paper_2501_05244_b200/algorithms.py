@@ -888,6 +888,7 @@ def _lattice_3d(slices, grid, z_pitch):
 
 
 _GROUP_FINE_BYTES = 4 << 30   # type-1 fine grids of one nursd3d frequency group
+_G3_EVEN = os.environ.get("PF_G3_EVEN", "1") != "0"   # 3D kernel transform on the even octant
 
 
 class _Lattice3dEngine(_UhatPropEngine):
@@ -935,13 +936,30 @@ class _Lattice3dEngine(_UhatPropEngine):
             for j, fi in enumerate(range(f0, f1)):
                 _lib.call("pf_kernel3d", dev.ptr(g3g) + 8 * j * n3, pz, py, px, self.vg.dx,
                           self.vg.dy, self.dz3, float(self.freqs[fi]) / C, s)
-            dev.fftn_natural(g3g, (pz, py, px), ng, -1, 1.0, stream)
-            if I == 1:
-                _lib.call("pf_cmul", dev.ptr(uhat3g), dev.ptr(g3g), ng * n3, ng * n3, 1.0, s)
+            if _G3_EVEN and min(pz, py, px) >= 2:
+                # G3 is even in every lag, so is its transform: each pass runs only over the
+                # non-negative half of the other two axes (a quarter of the lines), the
+                # mirrored half of the pass' own axis is filled by copy, and the product
+                # reads the spectrum folded onto its octant
+                hz, hy, hx = pz // 2, py // 2, px // 2
+                g3p = dev.ptr(g3g)
+                _lib.call("pf_fft_lines3", g3p, dev.fft_plan(px, self.device).ref,
+                          ng * (hz + 1) * (hy + 1), hy + 1, px, hz + 1, py * px, n3, 1, -1, 1.0, s)
+                _lib.call("pf_mirror_fill", g3p, ng, pz, py, px, 1, hz, hx, s)
+                _lib.call("pf_fft_lines3", g3p, dev.fft_plan(py, self.device).ref,
+                          ng * (hz + 1) * (hx + 1), hx + 1, 1, hz + 1, py * px, n3, px, -1, 1.0, s)
+                _lib.call("pf_mirror_fill", g3p, ng, pz, py, px, 0, hy, hx, s)
+                _lib.call("pf_fft_lines3", g3p, dev.fft_plan(pz, self.device).ref,
+                          ng * (hy + 1) * (hx + 1), hx + 1, 1, hy + 1, px, n3, py * px, -1, 1.0, s)
+                _lib.call("pf_cmul_even", dev.ptr(uhat3g), g3p, ng, I, pz, py, px, 1.0, s)
             else:
-                for j in range(ng):
-                    _lib.call("pf_cmul", dev.ptr(uhat3g) + 8 * j * I * n3, dev.ptr(g3g) + 8 * j * n3,
-                              I * n3, n3, 1.0, s)
+                dev.fftn_natural(g3g, (pz, py, px), ng, -1, 1.0, stream)
+                if I == 1:
+                    _lib.call("pf_cmul", dev.ptr(uhat3g), dev.ptr(g3g), ng * n3, ng * n3, 1.0, s)
+                else:
+                    for j in range(ng):
+                        _lib.call("pf_cmul", dev.ptr(uhat3g) + 8 * j * I * n3,
+                                  dev.ptr(g3g) + 8 * j * n3, I * n3, n3, 1.0, s)
             # cifft_n, then the slab plane: the z pass is evaluated at the slab only, then
             # the plane's y/x inverse transforms (the 3D inverse is never formed)
             out_g = out[f0 * I * py * px:f1 * I * py * px]

@@ -67,6 +67,79 @@ extern "C" int pf_cmul(void* a, const void* b, int64_t n, int64_t b_period, floa
   return 0;
 }
 
+// ---- even 3D kernels (G3 of the lattice stages is even in every lag) ---------------------
+// The transform of an array that is even along an axis is even along it, so the 3D transform
+// of G3 needs only the lines of the non-negative half of the other two axes; the mirrored
+// halves an axis' own pass reads are filled by copy.
+namespace {
+// axis 1: buf[b][z][y][x] = buf[b][z][py - y][x] for y in (py/2, py), z <= zmax, x <= xmax
+// axis 0: buf[b][z][y][x] = buf[b][pz - z][y][x] for z in (pz/2, pz), y <= ymax, x <= xmax
+__global__ void k_mirror_fill(float2* __restrict__ buf, int nb, int pz, int py, int px, int axis,
+                              int lim_a, int xmax) {
+  const int n_ax = axis == 1 ? py : pz;
+  const int h = n_ax / 2;
+  const int n_m = n_ax - h - 1;                     // mirrored slots h + 1 .. n_ax - 1
+  const long long per = (long long)(lim_a + 1) * n_m * (xmax + 1);
+  const long long total = (long long)nb * per;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / per;
+    long long r = e - b * per;
+    const int x = (int)(r % (xmax + 1));
+    r /= (xmax + 1);
+    const int m = (int)(r % n_m) + h + 1;
+    const int o = (int)(r / n_m);                   // the other (non-mirrored) axis index
+    float2* a = buf + b * (long long)pz * py * px;
+    if (axis == 1)
+      a[((long long)o * py + m) * px + x] = a[((long long)o * py + (py - m)) * px + x];
+    else
+      a[((long long)m * py + o) * px + x] = a[((long long)(pz - m) * py + o) * px + x];
+  }
+}
+
+// a[f][i][z][y][x] *= g[f][z][min(y, py - y)][min(x, px - x)] * scale (g valid on that octant)
+__global__ void k_cmul_even(float2* __restrict__ a, const float2* __restrict__ g, int nf, int ni,
+                            int pz, int py, int px, float scale) {
+  const long long n3 = (long long)pz * py * px;
+  const long long total = (long long)nf * ni * n3;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long fi = e / n3;
+    const long long r = e - fi * n3;
+    const int x = (int)(r % px);
+    const long long q = r / px;
+    const int y = (int)(q % py), z = (int)(q / py);
+    const int ym = 2 * y > py ? py - y : y, xm = 2 * x > px ? px - x : x;
+    const float2 gv = g[(fi / ni) * n3 + ((long long)z * py + ym) * px + xm];
+    a[e] = cscale(cmul(a[e], gv), scale);
+  }
+}
+}  // namespace
+
+extern "C" int pf_mirror_fill(void* buf, int nb, int pz, int py, int px, int axis, int lim,
+                              int xmax, void* stream) {
+  PF_ARG_CHECK(buf && nb >= 1 && pz >= 1 && py >= 1 && px >= 1 && (axis == 0 || axis == 1) &&
+                   lim >= 0 && lim < (axis == 1 ? pz : py) && xmax >= 0 && xmax < px,
+               "pf_mirror_fill: bad args");
+  const int n_ax = axis == 1 ? py : pz;
+  const long long total = (long long)nb * (lim + 1) * (n_ax - n_ax / 2 - 1) * (xmax + 1);
+  if (total <= 0) return 0;
+  k_mirror_fill<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>((float2*)buf, nb, pz, py, px,
+                                                                   axis, lim, xmax);
+  PF_LAUNCH_CHECK("k_mirror_fill");
+  return 0;
+}
+
+extern "C" int pf_cmul_even(void* a, const void* g, int nf, int ni, int pz, int py, int px,
+                            float scale, void* stream) {
+  PF_ARG_CHECK(a && g && nf >= 1 && ni >= 1 && pz >= 1 && py >= 1 && px >= 1,
+               "pf_cmul_even: bad args");
+  k_cmul_even<<<grid_for((long long)nf * ni * pz * py * px), 256, 0, (cudaStream_t)stream>>>(
+      (float2*)a, (const float2*)g, nf, ni, pz, py, px, scale);
+  PF_LAUNCH_CHECK("k_cmul_even");
+  return 0;
+}
+
 extern "C" int pf_copy_planes(const void* src, int nb, int64_t src_stride, int64_t plane_off,
                               int64_t plane_elems, void* dst, void* stream) {
   PF_ARG_CHECK(nb >= 0 && plane_elems >= 0, "pf_copy_planes: bad sizes");
