@@ -1,7 +1,7 @@
 #!/bin/bash
 # Record after the exponential-of-semicircle window: GPU suite (full-size parity), bench lines
 # of the NUFFT configurations 1, 2, 5, 7 (ours) and step launch lists of 1, 2, 7.
-O=gpurun_out/final10; mkdir -p $O
+O=gpurun_out/final11; mkdir -p $O
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
 PF_PARITY_LOG=$O/parity.jsonl timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; tail -3 $O/pytest_gpu.log
 for c in 1 2 5; do
